@@ -1,0 +1,191 @@
+/*
+ * lancet_moe.h -- C-ABI of the B200-native expert-parallel MoE layer step
+ * (Lancet, arXiv 2404.19429: "Accelerating Mixture-of-Experts Training via Whole Graph
+ *  Computation-Communication Overlapping").
+ *
+ * Citations are PAPER.md line numbers (P:Lnnn) of /root/reference/PAPER.md and DESIGN.md
+ * readings (Rn) where the paper is silent.
+ *
+ * The operation:
+ *   Each of G ranks holds T tokens x[T][d] (data parallel) and E_l = E/G experts
+ *   (expert parallel; expert e lives on rank e / E_l, "G = E / E_l").
+ *   forward:  logit = x Wg (fp32, R1); top-k by logit (R2); combine weight
+ *             w = softmax(logit)[idx] (R3); capacity C = max(1, min(T, ceil(cf*k*T/E))) per
+ *             (rank, expert) (R4); token-major admission (R7) -- chunked routing
+ *             equals unchunked routing, which is Lancet's capacity passing;
+ *             dispatch all-to-all (irregular: P:L517-L526); expert FFN
+ *             o = act(x W1^T) W2^T (R5); combine all-to-all; gather
+ *             y_t = sum_{admitted j} w_tj o_tj (dropped -> 0, R6).
+ *   The batch is split into n_chunks contiguous chunks (R9); the all-to-all of
+ *   chunk c overlaps expert compute of other chunks, and in the backward the
+ *   weight-gradient GEMMs are issued right after an all-to-all launch so they overlap it
+ *   (P:L168-L169).
+ *
+ * Conventions
+ *   - All tensor pointers are DEVICE pointers on the context's CUDA device unless marked
+ *     (host).  Row-major, densely packed, 16-byte aligned.
+ *   - "dtype" tensors are bf16 (LANCET_BF16) or fp32 (LANCET_FP32); the gate Wg, combine
+ *     weights and all weight gradients are always fp32.
+ *   - Every function returns a lancet_status; no C++ exception crosses the ABI.  Argument
+ *     errors return LANCET_ERR_ARG before anything is enqueued.  CUDA / NCCL failures
+ *     return LANCET_ERR_CUDA / LANCET_ERR_NCCL and poison the context (every later call
+ *     returns LANCET_ERR_STATE).  lancet_last_error() gives the message.
+ *   - Work is enqueued on the caller's `stream` (ordered after prior work on it); results
+ *     are valid for later work on `stream`.  Internally the library forks to its own
+ *     compute / comm streams and joins back with events.
+ */
+#ifndef LANCET_MOE_H_
+#define LANCET_MOE_H_
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LANCET_ABI_VERSION 1
+
+typedef struct lancet_ctx lancet_ctx;                 /* opaque, library-owned */
+typedef struct lancet_local_group lancet_local_group; /* opaque, library-owned */
+typedef void* lancet_stream_t;                        /* a cudaStream_t (0 = legacy default) */
+
+typedef enum {
+    LANCET_OK = 0,
+    LANCET_ERR_ARG = 1,          /* invalid argument; nothing was enqueued               */
+    LANCET_ERR_CUDA = 2,         /* CUDA runtime / driver error; context poisoned        */
+    LANCET_ERR_NCCL = 3,         /* NCCL error; context poisoned                         */
+    LANCET_ERR_NOMEM = 4,        /* device or pinned allocation failed                   */
+    LANCET_ERR_STATE = 5,        /* call out of order, or context poisoned               */
+    LANCET_ERR_UNSUPPORTED = 6   /* valid request this build / device does not support   */
+} lancet_status;
+
+typedef enum { LANCET_BF16 = 0, LANCET_FP32 = 1 } lancet_dtype;
+
+/* Expert activation (R5).  IDENTITY_EXPERT: o = x (no GEMMs; W1/W2 ignored and may be
+ * NULL) -- the dispatch/combine test mode of the north star. */
+typedef enum {
+    LANCET_ACT_GELU_TANH = 0,
+    LANCET_ACT_RELU = 1,
+    LANCET_ACT_IDENTITY_EXPERT = 2
+} lancet_act;
+
+/* Behaviour flags (lancet_layer_config.flags, or lancet_set_flags). */
+enum {
+    LANCET_FLAG_RENORMALIZE = 1u << 0,  /* w = p[idx] / sum_j p[idx_j] (R3); default off     */
+    LANCET_FLAG_TIMELINE    = 1u << 1,  /* record per-op events (lancet_last_timeline)       */
+    LANCET_FLAG_SERIAL      = 1u << 2,  /* unoverlapped baseline: one stream, chunks merged,
+                                           no dW reordering (the "unoverlapped a2a" of §8(d)) */
+    LANCET_FLAG_SIMT_GEMM   = 1u << 3,  /* bf16: use the SIMT GEMM instead of tcgen05 (debug) */
+    LANCET_FLAG_NO_DW_OVERLAP = 1u << 4 /* backward: dW GEMMs after all a2a (ablation)       */
+};
+
+typedef struct {
+    int32_t d_model;      /* d                                                         */
+    int32_t d_ffn;        /* f                                                         */
+    int32_t n_experts;    /* E (total over all ranks); E % world == 0                  */
+    int32_t max_tokens;   /* upper bound on T per call (sizes the workspace)           */
+    int32_t max_k;        /* upper bound on k                                          */
+    int32_t max_chunks;   /* upper bound on n_chunks (<= 64)                           */
+    int32_t dtype;        /* lancet_dtype                                              */
+    int32_t act;          /* lancet_act                                                */
+    uint32_t flags;       /* LANCET_FLAG_*                                             */
+    int32_t gemm_sms;     /* SMs the persistent GEMMs may use (0 = all)                */
+} lancet_layer_config;
+
+/* Per-op record of the last forward/backward (LANCET_FLAG_TIMELINE).  Times are
+ * microseconds from the start event recorded on the caller's stream. */
+typedef struct {
+    char name[24];        /* e.g. "gate", "a2a_dispatch[2]", "expert_fc1[2]"          */
+    int32_t lane;         /* 0 = compute stream, 1 = comm stream                       */
+    int32_t chunk;        /* chunk index or -1                                         */
+    float start_us;
+    float end_us;
+} lancet_op_record;
+
+int32_t lancet_abi_version(void);
+
+/* Message for the last error of `ctx`, or of the calling thread if ctx == NULL. */
+const char* lancet_last_error(const lancet_ctx* ctx);
+
+/* Rank 0 creates the NCCL unique id (128 bytes, host); the caller broadcasts it. */
+lancet_status lancet_nccl_unique_id(void* id_out /* host, 128 B */);
+
+/* Create a context for `rank` of `world`.  world == 1: no communication (id ignored).
+ * world > 1: NCCL communicator from `nccl_id` (host, 128 B); collective over all ranks,
+ * each on its own device.  The config must be identical on every rank (checked). */
+lancet_status lancet_create(lancet_ctx** out, int32_t world, int32_t rank, int32_t cuda_device,
+                            const void* nccl_id, const lancet_layer_config* cfg);
+
+/* Simulated ranks in ONE process on ONE device (tests of the multi-rank data path without
+ * several GPUs): the group is the transport; data all-to-alls become device-to-device
+ * copies between the ranks' buffers, ordered with events exactly where NCCL would
+ * synchronise.  Each rank's calls must be made from its own host thread (they block at the
+ * exchange points like a collective). */
+lancet_status lancet_local_group_create(lancet_local_group** out, int32_t world);
+lancet_status lancet_local_group_destroy(lancet_local_group* group);
+lancet_status lancet_create_local(lancet_ctx** out, lancet_local_group* group, int32_t rank,
+                                  int32_t cuda_device, const lancet_layer_config* cfg);
+
+/* Destroy; aborts the communicator if the context is poisoned.  Safe on NULL. */
+lancet_status lancet_destroy(lancet_ctx* ctx);
+
+lancet_status lancet_set_flags(lancet_ctx* ctx, uint32_t flags);
+
+/* Forward of the MoE layer (collective when world > 1).
+ *   x   [T][d]      dtype   caller-owned; must stay valid and unmodified until backward
+ *   wg  [d][E]      fp32    replicated gate
+ *   w1  [E_l][f][d] dtype   this rank's experts e = rank*E_l + i; valid until backward
+ *   w2  [E_l][d][f] dtype
+ *   T in [1, max_tokens]; k in [1, min(E, max_k)]; capacity_factor > 0;
+ *   n_chunks in [1, min(T, max_chunks)]
+ *   y          [T][d] dtype  out
+ *   expert_idx [T][k] int32  out or NULL   (rank order; idx[:,0] is the best expert)
+ *   slot       [T][k] int32  out or NULL   (position in the expert's buffer; -1 = dropped)
+ *   combine_w  [T][k] fp32   out or NULL
+ * world > 1: blocks the host once (the counts exchange of P:L525 must reach the host to
+ * size the NCCL sends).  world == 1: never blocks.
+ * One outstanding forward per context: a second forward before backward is allowed (the
+ * first is discarded); backward without forward returns LANCET_ERR_STATE. */
+lancet_status lancet_moe_forward(lancet_ctx* ctx, const void* x, const float* wg,
+                                 const void* w1, const void* w2, int32_t T, int32_t k,
+                                 float capacity_factor, int32_t n_chunks, void* y,
+                                 int32_t* expert_idx, int32_t* slot, float* combine_w,
+                                 lancet_stream_t stream);
+
+/* Backward of the last forward (collective when world > 1).  Gradient of <dy, y>:
+ *   dy  [T][d]      dtype  in
+ *   dx  [T][d]      dtype  out (overwritten)
+ *   dwg [d][E]      fp32   out (overwritten) -- LOCAL: the caller all-reduces it
+ *   dw1 [E_l][f][d] fp32   out (overwritten; NULL allowed for identity experts)
+ *   dw2 [E_l][d][f] fp32   out (overwritten; NULL allowed for identity experts)
+ * Never blocks the host. */
+lancet_status lancet_moe_backward(lancet_ctx* ctx, const void* dy, void* dx, float* dwg,
+                                  float* dw1, float* dw2, lancet_stream_t stream);
+
+/* Routing sizes of the last forward (host arrays; synchronises with the forward):
+ *   send_counts [E][n_chunks]         rows this rank admitted per expert per chunk
+ *   recv_counts [G][E_l][n_chunks]    rows this rank's experts receive per source rank
+ *   capacity    C of the last forward  (out or NULL) */
+lancet_status lancet_get_counts(lancet_ctx* ctx, int32_t* send_counts, int32_t* recv_counts,
+                                int32_t* capacity);
+
+/* Timeline of the last forward+backward (LANCET_FLAG_TIMELINE); synchronises. */
+lancet_status lancet_last_timeline(lancet_ctx* ctx, lancet_op_record* out, int32_t cap,
+                                   int32_t* n_out);
+
+/* Copy an internal buffer of the last forward to host (tests and diagnostics; synchronises).
+ * which: 0 = gate logits [T][E] fp32 (R1 chain). */
+lancet_status lancet_debug_copy(lancet_ctx* ctx, int32_t which, void* host_dst, size_t bytes);
+
+/* Bytes of device workspace the context owns. */
+lancet_status lancet_workspace_bytes(const lancet_ctx* ctx, size_t* bytes);
+
+/* Number of this library's kernel launches enqueued by the last forward / backward. */
+lancet_status lancet_launch_counts(const lancet_ctx* ctx, int32_t* fwd, int32_t* bwd);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LANCET_MOE_H_ */

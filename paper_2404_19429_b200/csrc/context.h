@@ -1,0 +1,87 @@
+// context.h -- internal definition of lancet_ctx (the library-owned state behind the C-ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/lancet_moe.h"
+#include "kernels.h"
+
+namespace lancet {
+
+struct Transport;   // comm.cpp: NCCL or in-process local group
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+};
+
+struct OpEvent {
+    std::string name;
+    int lane, chunk;
+    cudaEvent_t beg, end;
+};
+
+}  // namespace lancet
+
+struct lancet_ctx {
+    // configuration
+    int world = 1, rank = 0, device = 0, E_l = 0, num_sms = 0;
+    lancet_layer_config cfg{};
+    bool bf16 = true;
+    size_t elt = 2;
+
+    // comm
+    lancet::Transport* comm = nullptr;
+
+    // streams / events
+    cudaStream_t s_comp = nullptr, s_comm = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_counts = nullptr, ev_tl_base = nullptr;
+    std::vector<cudaEvent_t> ev_pool;                 // generic sync events
+    std::vector<lancet::OpEvent> ops;                 // timeline of the last fwd+bwd
+    std::vector<cudaEvent_t> tl_events;               // event pool for the timeline
+    size_t tl_used = 0;
+
+    // source-side workspace (rows_src = max_tokens*max_k + E*128)
+    int rows_src = 0;
+    float* logits = nullptr;  int* idx = nullptr;  float* w = nullptr;  int* slot = nullptr;
+    int* hist = nullptr;  int* S = nullptr;  int* send_rows = nullptr;  int* send_off = nullptr;
+    void* xs = nullptr;        // [rows_src][d]  dispatch / send buffer
+    void* comb = nullptr;      // [rows_src][d]  combined expert outputs (world > 1)
+    void* dcomb = nullptr;     // [rows_src][d]  grad of expert outputs (source side)
+    void* dxcomb = nullptr;    // [rows_src][d]  grad of expert inputs returned (world > 1)
+    float* g = nullptr;  float* dlogit = nullptr;  float* dwg_partial = nullptr;
+    int* counts_dev = nullptr;   // [E][n] send counts, then [G][E_l][n] recv counts
+    int* grp_dev = nullptr;      // expert-side group table: rows[n_groups] | off[n_groups]
+
+    // expert-side workspace (rows_exp rows; == rows_src when world == 1)
+    int rows_exp = 0;
+    void* xe = nullptr;        // [rows_exp][d]  received tokens (world > 1; == xs at world 1)
+    void* H = nullptr;         // [rows_exp][f]  act(a)
+    void* Gp = nullptr;        // [rows_exp][f]  act'(a)
+    void* out = nullptr;       // [rows_exp][d]  expert outputs
+    void* dout = nullptr;      // [rows_exp][d]  received grads of expert outputs (world > 1)
+    void* dA = nullptr;        // [rows_exp][f]
+    void* dXe = nullptr;       // [rows_exp][d]
+
+    // pinned host mirrors (world > 1)
+    int* h_counts = nullptr;   // send [E][n] | recv [G][E_l][n]
+    int* h_grp = nullptr;
+
+    std::vector<lancet::DevBuf> allocs;
+
+    // state of the last forward (pointers only; the caller keeps the tensors alive)
+    bool have_fwd = false;
+    const void* x = nullptr; const float* wg = nullptr; const void* w1 = nullptr; const void* w2 = nullptr;
+    int T = 0, k = 0, n = 0, C = 0;
+    float cf = 0.f;
+    int n_groups = 0;          // expert-side GEMM groups of the last forward
+    std::vector<int> host_send, host_recv, host_grp_rows, host_grp_off;  // world > 1
+    int launches_fwd = 0, launches_bwd = 0;
+
+    // errors
+    bool poisoned = false;
+    std::string err;
+};

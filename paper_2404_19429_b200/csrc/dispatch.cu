@@ -1,0 +1,410 @@
+// dispatch.cu -- data movement of the MoE layer and the gate backward.
+//
+// K3 permute:   "The tokens are re-arranged according to their target experts":
+//               row x[t] -> xs[off_e + slot] for every admitted (t, j); one warp per token,
+//               16-byte vector loads issued before the k stores.  Expert e's rows of chunk c
+//               are the contiguous range [off_e + S[e][c], off_e + S[e][c+1]) -- the chunk's
+//               send message needs no repacking.
+// K4 combine:   "Reverting tokens to their original order yields the MoE layer's output"
+//               (gather): y_t = sum_{admitted j} w_tj o_tj as an fp32 fma chain
+//               over j in order, dropped choices contribute 0 (R6).
+// K5 combine backward:  g_tj = <dy_t, o_tj>, dcomb[off_e + slot] = w_tj dy_t.
+// K6 dispatch backward + gate:  dx_t = sum_{admitted j} dX_e[off_e + slot]
+//               + sum_e dlogit_te Wg[:, e], with dlogit from the softmax Jacobian (R3).
+// K7 dWg = x^T dlogit (two-pass deterministic reduction over tokens).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace lancet {
+
+constexpr int kWarpsPerBlock = 8;
+
+template <typename Elt>
+__global__ void __launch_bounds__(256)
+permute_kernel(const Elt* __restrict__ x, const int* __restrict__ idx, const int* __restrict__ slot,
+               int T, int k, int d, const int* __restrict__ send_off,
+               const int* __restrict__ send_rows, Elt* __restrict__ xs, int tok_blocks)
+{
+    constexpr int V = Vec16<Elt>::N;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nvec = d / V;
+    if ((int)blockIdx.x < tok_blocks) {
+        const int t = blockIdx.x * kWarpsPerBlock + w;
+        if (t >= T) return;
+        int myrow = -1;
+        if (lane < k) {
+            const int s = slot[(size_t)t * k + lane];
+            myrow = s >= 0 ? send_off[idx[(size_t)t * k + lane]] + s : -1;
+        }
+        int rows[kMaxK];
+#pragma unroll
+        for (int j = 0; j < kMaxK; ++j) rows[j] = __shfl_sync(0xffffffffu, myrow, j);
+        const uint4* src = reinterpret_cast<const uint4*>(x + (size_t)t * d);
+        constexpr int U = 4;
+        for (int v0 = lane; v0 < nvec; v0 += 32 * U) {
+            uint4 val[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (v0 + 32 * u < nvec) val[u] = ld_nc_v4(src + v0 + 32 * u);
+#pragma unroll
+            for (int j = 0; j < kMaxK; ++j) {
+                if (j < k && rows[j] >= 0) {
+                    uint4* dst = reinterpret_cast<uint4*>(xs + (size_t)rows[j] * d);
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+                        if (v0 + 32 * u < nvec) st_v4(dst + v0 + 32 * u, val[u]);
+                }
+            }
+        }
+    } else {
+        // zero the pad rows [off_e + rows_e, off_e + round_up(rows_e, 128)) of expert e
+        const int e = blockIdx.x - tok_blocks;
+        const int r0 = send_off[e] + send_rows[e];
+        const int r1 = send_off[e] + round_up(send_rows[e], kRowAlign);
+        for (int r = r0 + w; r < r1; r += kWarpsPerBlock) {
+            uint4* dst = reinterpret_cast<uint4*>(xs + (size_t)r * d);
+            for (int v = lane; v < nvec; v += 32) st_v4(dst + v, make_uint4(0, 0, 0, 0));
+        }
+    }
+}
+
+template <typename Elt>
+__global__ void __launch_bounds__(256)
+combine_kernel(const Elt* __restrict__ comb, const int* __restrict__ idx,
+               const int* __restrict__ slot, const float* __restrict__ wts,
+               const int* __restrict__ send_off, int t0, int t1, int k, int d,
+               Elt* __restrict__ y)
+{
+    constexpr int V = Vec16<Elt>::N;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int t = t0 + blockIdx.x * kWarpsPerBlock + w;
+    if (t >= t1) return;
+    int myrow = -1;
+    float myw = 0.f;
+    if (lane < k) {
+        const int s = slot[(size_t)t * k + lane];
+        myrow = s >= 0 ? send_off[idx[(size_t)t * k + lane]] + s : -1;
+        myw = wts[(size_t)t * k + lane];
+    }
+    int rows[kMaxK];
+    float wj[kMaxK];
+#pragma unroll
+    for (int j = 0; j < kMaxK; ++j) {
+        rows[j] = __shfl_sync(0xffffffffu, myrow, j);
+        wj[j] = __shfl_sync(0xffffffffu, myw, j);
+    }
+    const int nvec = d / V;
+    uint4* dst = reinterpret_cast<uint4*>(y + (size_t)t * d);
+    for (int v = lane; v < nvec; v += 32) {
+        float acc[V];
+#pragma unroll
+        for (int q = 0; q < V; ++q) acc[q] = 0.f;
+        uint4 raw[kMaxK];
+#pragma unroll
+        for (int j = 0; j < kMaxK; ++j)
+            if (j < k && rows[j] >= 0)
+                raw[j] = ld_nc_v4(reinterpret_cast<const uint4*>(comb + (size_t)rows[j] * d) + v);
+#pragma unroll
+        for (int j = 0; j < kMaxK; ++j) {
+            if (j < k && rows[j] >= 0) {
+                float f[V];
+                unpack16<Elt>(raw[j], f);
+#pragma unroll
+                for (int q = 0; q < V; ++q) acc[q] = __fmaf_rn(wj[j], f[q], acc[q]);
+            }
+        }
+        st_v4(dst + v, pack16<Elt>(acc));
+    }
+}
+
+template <typename Elt>
+__global__ void __launch_bounds__(256)
+combine_bwd_kernel(const Elt* __restrict__ dy, const Elt* __restrict__ comb,
+                   const int* __restrict__ idx, const int* __restrict__ slot,
+                   const float* __restrict__ wts, const int* __restrict__ send_off,
+                   const int* __restrict__ send_rows, int t0, int t1, int k, int d,
+                   float* __restrict__ g, Elt* __restrict__ dcomb, int tok_blocks)
+{
+    constexpr int V = Vec16<Elt>::N;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nvec = d / V;
+    if ((int)blockIdx.x >= tok_blocks) {
+        const int e = blockIdx.x - tok_blocks;
+        const int r0 = send_off[e] + send_rows[e];
+        const int r1 = send_off[e] + round_up(send_rows[e], kRowAlign);
+        for (int r = r0 + w; r < r1; r += kWarpsPerBlock) {
+            uint4* dst = reinterpret_cast<uint4*>(dcomb + (size_t)r * d);
+            for (int v = lane; v < nvec; v += 32) st_v4(dst + v, make_uint4(0, 0, 0, 0));
+        }
+        return;
+    }
+    const int t = t0 + blockIdx.x * kWarpsPerBlock + w;
+    if (t >= t1) return;
+    int myrow = -1;
+    float myw = 0.f;
+    if (lane < k) {
+        const int s = slot[(size_t)t * k + lane];
+        myrow = s >= 0 ? send_off[idx[(size_t)t * k + lane]] + s : -1;
+        myw = wts[(size_t)t * k + lane];
+    }
+    int rows[kMaxK];
+    float wj[kMaxK], part[kMaxK];
+#pragma unroll
+    for (int j = 0; j < kMaxK; ++j) {
+        rows[j] = __shfl_sync(0xffffffffu, myrow, j);
+        wj[j] = __shfl_sync(0xffffffffu, myw, j);
+        part[j] = 0.f;
+    }
+    const uint4* dyr = reinterpret_cast<const uint4*>(dy + (size_t)t * d);
+    for (int v = lane; v < nvec; v += 32) {
+        float fdy[V];
+        unpack16<Elt>(ld_nc_v4(dyr + v), fdy);
+#pragma unroll
+        for (int j = 0; j < kMaxK; ++j) {
+            if (j < k && rows[j] >= 0) {
+                float fo[V], sc[V];
+                unpack16<Elt>(ld_nc_v4(reinterpret_cast<const uint4*>(comb + (size_t)rows[j] * d) + v), fo);
+#pragma unroll
+                for (int q = 0; q < V; ++q) {
+                    part[j] = fmaf(fdy[q], fo[q], part[j]);
+                    sc[q] = wj[j] * fdy[q];
+                }
+                st_v4(reinterpret_cast<uint4*>(dcomb + (size_t)rows[j] * d) + v, pack16<Elt>(sc));
+            }
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < kMaxK; ++j) {
+        if (j < k) {
+            const float s = warp_sum(part[j]);
+            if (lane == 0) g[(size_t)t * k + j] = rows[j] >= 0 ? s : 0.f;
+        }
+    }
+}
+
+// dlogit in smem per warp; E <= kMaxExperts
+template <typename Elt>
+__global__ void __launch_bounds__(256)
+unpermute_gate_bwd_kernel(const Elt* __restrict__ dxe, const int* __restrict__ idx,
+                          const int* __restrict__ slot, const float* __restrict__ wts,
+                          const float* __restrict__ g, const float* __restrict__ logits,
+                          const float* __restrict__ wg, const int* __restrict__ send_off,
+                          int renorm, int t0, int t1, int k, int d, int E,
+                          Elt* __restrict__ dx, float* __restrict__ dlogit)
+{
+    extern __shared__ float sdl_all[];
+    constexpr int V = Vec16<Elt>::N;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int t = t0 + blockIdx.x * kWarpsPerBlock + w;
+    if (t >= t1) return;
+    float* sdl = sdl_all + w * E;
+    int myrow = -1, myidx = -1;
+    float myw = 0.f, myg = 0.f;
+    if (lane < k) {
+        const int s = slot[(size_t)t * k + lane];
+        myidx = idx[(size_t)t * k + lane];
+        myrow = s >= 0 ? send_off[myidx] + s : -1;
+        myw = wts[(size_t)t * k + lane];
+        myg = g[(size_t)t * k + lane];
+    }
+    int rows[kMaxK], ids[kMaxK];
+    float wj[kMaxK], gj[kMaxK];
+    float sg = 0.f;                                   // sum_j g_j w_j
+#pragma unroll
+    for (int j = 0; j < kMaxK; ++j) {
+        rows[j] = __shfl_sync(0xffffffffu, myrow, j);
+        ids[j] = __shfl_sync(0xffffffffu, myidx, j);
+        wj[j] = __shfl_sync(0xffffffffu, myw, j);
+        gj[j] = __shfl_sync(0xffffffffu, myg, j);
+        if (j < k) sg = fmaf(gj[j], wj[j], sg);
+    }
+    // softmax Jacobian (R3): dlogit_e = p_e (g~_e - sg), or renormalised at the selected e
+    const float* lr = logits + (size_t)t * E;
+    float m = -INFINITY;
+    for (int e = lane; e < E; e += 32) m = fmaxf(m, lr[e]);
+    m = warp_max(m);
+    float s = 0.f;
+    for (int e = lane; e < E; e += 32) s += expf(lr[e] - m);
+    s = warp_sum(s);
+    for (int e = lane; e < E; e += 32) {
+        float gt = 0.f, wsel = 0.f;
+        bool sel = false;
+#pragma unroll
+        for (int j = 0; j < kMaxK; ++j)
+            if (j < k && ids[j] == e) { gt = gj[j]; wsel = wj[j]; sel = true; }
+        float dl;
+        if (renorm) dl = sel ? wsel * (gt - sg) : 0.f;
+        else dl = (expf(lr[e] - m) / s) * (gt - sg);
+        sdl[e] = dl;
+        dlogit[(size_t)t * E + e] = dl;
+    }
+    __syncwarp();
+    const int nvec = d / V;
+    for (int v = lane; v < nvec; v += 32) {
+        float acc[V];
+#pragma unroll
+        for (int q = 0; q < V; ++q) acc[q] = 0.f;
+#pragma unroll
+        for (int j = 0; j < kMaxK; ++j) {
+            if (j < k && rows[j] >= 0) {
+                float f[V];
+                unpack16<Elt>(ld_nc_v4(reinterpret_cast<const uint4*>(dxe + (size_t)rows[j] * d) + v), f);
+#pragma unroll
+                for (int q = 0; q < V; ++q) acc[q] += f[q];
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < V; ++q) {
+            const float* wr = wg + (size_t)(v * V + q) * E;
+            float a = 0.f;
+            for (int e = 0; e < E; ++e) a = fmaf(sdl[e], wr[e], a);
+            acc[q] += a;
+        }
+        st_v4(reinterpret_cast<uint4*>(dx + (size_t)t * d) + v, pack16<Elt>(acc));
+    }
+}
+
+constexpr int kDwgTok = 256;     // tokens per partial block
+constexpr int kDwgDim = 128;     // dims per partial block (one per thread)
+constexpr int kDwgE = 32;        // experts per pass
+
+template <typename Elt>
+__global__ void __launch_bounds__(kDwgDim)
+dwg_partial_kernel(const Elt* __restrict__ x, const float* __restrict__ dlogit, int T, int d,
+                   int E, float* __restrict__ partial)
+{
+    __shared__ float sdl[kDwgTok][kDwgE + 1];
+    const int i = blockIdx.y * kDwgDim + threadIdx.x;
+    const int tb = blockIdx.x;
+    const int e0 = blockIdx.z * kDwgE;
+    const int ne = min(kDwgE, E - e0);
+    const int tbeg = tb * kDwgTok, tend = min(T, tbeg + kDwgTok);
+    for (int q = threadIdx.x; q < kDwgTok * kDwgE; q += kDwgDim) {
+        const int r = q / kDwgE, c = q % kDwgE, t = tbeg + r;
+        sdl[r][c] = (t < tend && c < ne) ? dlogit[(size_t)t * E + e0 + c] : 0.f;
+    }
+    __syncthreads();
+    if (i >= d) return;
+    float acc[kDwgE];
+#pragma unroll
+    for (int c = 0; c < kDwgE; ++c) acc[c] = 0.f;
+    for (int t = tbeg; t < tend; ++t) {
+        const float xv = to_f(x[(size_t)t * d + i]);
+#pragma unroll
+        for (int c = 0; c < kDwgE; ++c) acc[c] = fmaf(xv, sdl[t - tbeg][c], acc[c]);
+    }
+    float* out = partial + ((size_t)tb * d + i) * E + e0;
+    for (int c = 0; c < ne; ++c) out[c] = acc[c];
+}
+
+__global__ void dwg_reduce_kernel(const float* __restrict__ partial, int nb, int d, int E,
+                                  float* __restrict__ dwg)
+{
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= d * E) return;
+    float s = 0.f;
+    for (int b = 0; b < nb; ++b) s += partial[(size_t)b * d * E + q];
+    dwg[q] = s;
+}
+
+__global__ void zero_pads_kernel(char* __restrict__ buf, int row_bytes,
+                                 const int* __restrict__ grp_off, const int* __restrict__ grp_rows)
+{
+    const int g = blockIdx.x;
+    const int r0 = grp_off[g] + grp_rows[g];
+    const int r1 = grp_off[g] + round_up(grp_rows[g], kRowAlign);
+    const int nv = row_bytes / 16;
+    for (int q = threadIdx.x; q < (r1 - r0) * nv; q += blockDim.x) {
+        const int r = r0 + q / nv, v = q % nv;
+        st_v4(buf + (size_t)r * row_bytes + (size_t)v * 16, make_uint4(0, 0, 0, 0));
+    }
+}
+
+// ---- launchers ---------------------------------------------------------------------------
+
+int launch_permute(const DispatchArgs& a, const void* x, void* xs, bool is_bf16, cudaStream_t s)
+{
+    const int tok_blocks = ceil_div(a.T, kWarpsPerBlock);
+    const int grid = tok_blocks + a.E;
+    if (is_bf16)
+        permute_kernel<bf16><<<grid, 256, 0, s>>>((const bf16*)x, a.idx, a.slot, a.T, a.k, a.d,
+                                                 a.send_off, a.send_rows, (bf16*)xs, tok_blocks);
+    else
+        permute_kernel<float><<<grid, 256, 0, s>>>((const float*)x, a.idx, a.slot, a.T, a.k, a.d,
+                                                  a.send_off, a.send_rows, (float*)xs, tok_blocks);
+    return 1;
+}
+
+int launch_combine(const DispatchArgs& a, const void* comb, void* y, int t0, int t1, bool is_bf16,
+                   cudaStream_t s)
+{
+    if (t1 <= t0) return 0;
+    const int grid = ceil_div(t1 - t0, kWarpsPerBlock);
+    if (is_bf16)
+        combine_kernel<bf16><<<grid, 256, 0, s>>>((const bf16*)comb, a.idx, a.slot, a.w, a.send_off,
+                                                 t0, t1, a.k, a.d, (bf16*)y);
+    else
+        combine_kernel<float><<<grid, 256, 0, s>>>((const float*)comb, a.idx, a.slot, a.w,
+                                                  a.send_off, t0, t1, a.k, a.d, (float*)y);
+    return 1;
+}
+
+int launch_combine_bwd(const DispatchArgs& a, const void* dy, const void* comb, float* g,
+                       void* dcomb, int t0, int t1, bool zero_pads, bool is_bf16, cudaStream_t s)
+{
+    const int tok_blocks = ceil_div(t1 - t0, kWarpsPerBlock);
+    const int grid = tok_blocks + (zero_pads ? a.E : 0);
+    if (grid == 0) return 0;
+    if (is_bf16)
+        combine_bwd_kernel<bf16><<<grid, 256, 0, s>>>((const bf16*)dy, (const bf16*)comb, a.idx,
+                                                     a.slot, a.w, a.send_off, a.send_rows, t0, t1,
+                                                     a.k, a.d, g, (bf16*)dcomb, tok_blocks);
+    else
+        combine_bwd_kernel<float><<<grid, 256, 0, s>>>((const float*)dy, (const float*)comb, a.idx,
+                                                      a.slot, a.w, a.send_off, a.send_rows, t0, t1,
+                                                      a.k, a.d, g, (float*)dcomb, tok_blocks);
+    return 1;
+}
+
+int launch_unpermute_gate_bwd(const DispatchArgs& a, const void* dxe, const float* g,
+                              const float* logits, const float* wg, int renorm, void* dx,
+                              float* dlogit, int t0, int t1, bool is_bf16, cudaStream_t s)
+{
+    if (t1 <= t0) return 0;
+    const int grid = ceil_div(t1 - t0, kWarpsPerBlock);
+    const size_t smem = sizeof(float) * kWarpsPerBlock * a.E;
+    if (is_bf16)
+        unpermute_gate_bwd_kernel<bf16><<<grid, 256, smem, s>>>(
+            (const bf16*)dxe, a.idx, a.slot, a.w, g, logits, wg, a.send_off, renorm, t0, t1, a.k,
+            a.d, a.E, (bf16*)dx, dlogit);
+    else
+        unpermute_gate_bwd_kernel<float><<<grid, 256, smem, s>>>(
+            (const float*)dxe, a.idx, a.slot, a.w, g, logits, wg, a.send_off, renorm, t0, t1, a.k,
+            a.d, a.E, (float*)dx, dlogit);
+    return 1;
+}
+
+size_t dwg_partial_floats(int T, int d, int E) { return (size_t)ceil_div(T, kDwgTok) * d * E; }
+
+int launch_dwg(const void* x, const float* dlogit, int T, int d, int E, float* partial,
+               float* dwg, bool is_bf16, cudaStream_t s)
+{
+    const int nb = ceil_div(T, kDwgTok);
+    dim3 grid(nb, ceil_div(d, kDwgDim), ceil_div(E, kDwgE));
+    if (is_bf16)
+        dwg_partial_kernel<bf16><<<grid, kDwgDim, 0, s>>>((const bf16*)x, dlogit, T, d, E, partial);
+    else
+        dwg_partial_kernel<float><<<grid, kDwgDim, 0, s>>>((const float*)x, dlogit, T, d, E, partial);
+    dwg_reduce_kernel<<<ceil_div(d * E, 256), 256, 0, s>>>(partial, nb, d, E, dwg);
+    return 2;
+}
+
+int launch_zero_pads(void* buf, int row_elems, const int* grp_off, const int* grp_rows,
+                     int n_groups, int elt_bytes, cudaStream_t s)
+{
+    if (n_groups <= 0) return 0;
+    zero_pads_kernel<<<n_groups, 256, 0, s>>>((char*)buf, row_elems * elt_bytes, grp_off, grp_rows);
+    return 1;
+}
+
+}  // namespace lancet

@@ -1,0 +1,78 @@
+// kernels.h -- host launchers of the lancet_moe kernels (internal, C++).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace lancet {
+
+// ---- K1 / K2: routing (routing.cu) -------------------------------------------------------
+struct RouteArgs {
+    const void* x;        // [T][d] elt
+    const float* wg;      // [d][E]
+    int T, d, E, k, C, n_chunks, renorm;
+    float* logits;        // [T][E]   out
+    int* idx;             // [T][k]   out
+    float* w;             // [T][k]   out
+    int* slot;            // [T][k]   out
+    int* hist;            // [n_tiles][E] scratch (zeroed here)
+    int* S;               // [E][n+1] out: S[e][c] = min(C, P_e(t_c)) (capacity state)
+    int* send_rows;       // [E]      out: admitted rows per expert
+    int* send_off;        // [E]      out: 128-aligned packed row offset of expert e
+};
+// Enqueues memset(hist) + K1 + K2.  Returns the number of kernels launched.
+int launch_routing(const RouteArgs& a, bool is_bf16, cudaStream_t s);
+
+// ---- K3..K6: dispatch / combine (dispatch.cu) --------------------------------------------
+struct DispatchArgs {
+    int T, k, d, E;
+    const int* idx; const int* slot; const float* w;
+    const int* send_off; const int* send_rows;
+};
+int launch_permute(const DispatchArgs& a, const void* x, void* xs, bool is_bf16, cudaStream_t s);
+int launch_combine(const DispatchArgs& a, const void* comb, void* y, int t0, int t1, bool is_bf16,
+                   cudaStream_t s);
+int launch_combine_bwd(const DispatchArgs& a, const void* dy, const void* comb, float* g,
+                       void* dcomb, int t0, int t1, bool zero_pads, bool is_bf16, cudaStream_t s);
+int launch_unpermute_gate_bwd(const DispatchArgs& a, const void* dxe, const float* g,
+                              const float* logits, const float* wg, int renorm, void* dx,
+                              float* dlogit, int t0, int t1, bool is_bf16, cudaStream_t s);
+// dWg = x^T dlogit (K7); partial: [ceil(T/256)][d][E] fp32 scratch
+int launch_dwg(const void* x, const float* dlogit, int T, int d, int E, float* partial,
+               float* dwg, bool is_bf16, cudaStream_t s);
+size_t dwg_partial_floats(int T, int d, int E);
+// zero rows [off_g + rows_g, off_g + round_up(rows_g, 128)) of a packed buffer
+int launch_zero_pads(void* buf, int row_elems, const int* grp_off, const int* grp_rows,
+                     int n_groups, int elt_bytes, cudaStream_t s);
+
+// ---- grouped GEMMs (gemm_simt.cu, gemm_tc.cu) --------------------------------------------
+enum GemmMode { GEMM_M_GROUPED = 0, GEMM_K_GROUPED = 1 };
+enum GemmEpi { EPI_STORE = 0, EPI_ACT = 1, EPI_DACT = 2, EPI_F32 = 3 };
+
+struct GemmArgs {
+    // A(m,k): A_MN ? A[(row0+k)*lda + m] : A[(row0+m)*lda + k]
+    const void* A; long lda;
+    // B(n,k): B_MN ? B[(krow0+k)*ldb + n] : B[n*ldb + k], B += (g / gpw) * b_group_stride
+    const void* B; long ldb; long b_group_stride;
+    // C(m,n): M-grouped C[(row0+m)*ldc + n];  K-grouped C[g*c_group_stride + m*ldc + n]
+    void* C; long ldc; long c_group_stride;
+    void* C2;             // EPI_ACT: act'(a) stored beside act(a) (same layout as C)
+    const void* aux;      // EPI_DACT: act'(a) multiplied into the accumulator
+    int M, N, K;          // M-grouped: N, K fixed, rows per group from the table;
+                          // K-grouped: M, N fixed, K per group from the table
+    int max_rows;         // M-grouped: upper bound of round_up(rows_g, 128) (grid sizing)
+    int mode, n_groups, gpw;
+    const int* grp_rows;  // [n_groups] valid rows (M-grouped) / tokens (K-grouped)
+    const int* grp_off;   // [n_groups] first row (128-aligned) in A / C (M) or A / B (K)
+    int epi, act, accumulate;
+    bool a_mn, b_mn;
+};
+int launch_gemm_simt(const GemmArgs& a, bool is_bf16, cudaStream_t s);
+
+// tcgen05 / TMEM / TMA grouped GEMM, bf16 in, fp32 accumulate (gemm_tc.cu).
+// Returns <0 if the shape is unsupported (caller reports LANCET_ERR_UNSUPPORTED).
+int launch_gemm_tc(const GemmArgs& a, int num_sms, cudaStream_t s);
+bool gemm_tc_supported(const GemmArgs& a);
+
+}  // namespace lancet

@@ -1,0 +1,987 @@
+// lancet.cu -- the C-ABI (include/lancet_moe.h): context, workspace, and the stream/event
+// chunk scheduler of the MoE layer step (S1 forward, S2 backward).
+//
+// Scheduling (Lancet, PAPER.md):
+//   * forward (S1): the MoE input/output is partitioned on the batch dimension and
+//     the all-to-all and experts irregularly inside (fig:proposed_partition); chunk
+//     c's all-to-all overlaps other chunks' expert compute; the comm lane runs
+//     the chunks in stage order D0..D(n-1), C0..C(n-1).
+//   * backward (S2): the dW GEMMs of chunk c are enqueued right after chunk c's dX GEMMs, i.e.
+//     right after the launch of the all-to-all they overlap.
+//   * the irregular all-to-all is a size exchange followed by the data exchange of only the
+//     real rows; the size exchange happens once per forward for all chunks
+//     (R11) -- the only host synchronisation of the step (world > 1).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "comm.h"
+#include "common.cuh"
+#include "context.h"
+#include "kernels.h"
+
+#define LANCET_API extern "C" __attribute__((visibility("default")))
+
+using namespace lancet;
+
+struct lancet_local_group {
+    LocalGroupImpl* impl;
+    int world;
+};
+
+namespace {
+
+thread_local std::string g_thread_err;
+
+lancet_status fail(lancet_ctx* c, lancet_status st, const std::string& msg)
+{
+    if (c) {
+        c->err = msg;
+        if (st == LANCET_ERR_CUDA || st == LANCET_ERR_NCCL) c->poisoned = true;
+    }
+    g_thread_err = msg;
+    return st;
+}
+
+#define CK(call)                                                                        \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess)                                                          \
+            return fail(c, LANCET_ERR_CUDA,                                             \
+                        std::string(#call) + ": " + cudaGetErrorString(e_));            \
+    } while (0)
+
+#define CHECK_LAUNCH()                                                                  \
+    do {                                                                                \
+        cudaError_t e_ = cudaGetLastError();                                            \
+        if (e_ != cudaSuccess)                                                          \
+            return fail(c, LANCET_ERR_CUDA, std::string("kernel launch: ") +            \
+                                                cudaGetErrorString(e_));                \
+    } while (0)
+
+int capacity_of(int T, int k, int E, float cf)
+{
+    // R4: C = max(1, min(T, ceil(cf*k*T/E))) in double
+    const double v = std::ceil((double)cf * (double)k * (double)T / (double)E);
+    long c = (long)v;
+    if (c > T) c = T;
+    if (c < 1) c = 1;
+    return (int)c;
+}
+
+unsigned long long cfg_hash(const lancet_layer_config& c)
+{
+    unsigned long long h = 1469598103934665603ull;
+    const int32_t v[] = {c.d_model, c.d_ffn, c.n_experts, c.max_k, c.max_chunks, c.dtype, c.act,
+                         (int32_t)(c.flags & LANCET_FLAG_RENORMALIZE)};
+    for (int32_t x : v) { h ^= (unsigned)x; h *= 1099511628211ull; }
+    return h;
+}
+
+template <typename T>
+lancet_status dalloc(lancet_ctx* c, T** p, size_t bytes)
+{
+    bytes = std::max<size_t>(bytes, 256);
+    void* q = nullptr;
+    if (cudaMalloc(&q, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(c, LANCET_ERR_NOMEM, "cudaMalloc of " + std::to_string(bytes) + " bytes failed");
+    }
+    c->allocs.push_back({q, bytes});
+    *p = reinterpret_cast<T*>(q);
+    return LANCET_OK;
+}
+
+void free_all(lancet_ctx* c)
+{
+    for (auto& b : c->allocs) cudaFree(b.p);
+    c->allocs.clear();
+    if (c->h_counts) cudaFreeHost(c->h_counts);
+    if (c->h_grp) cudaFreeHost(c->h_grp);
+    c->h_counts = c->h_grp = nullptr;
+}
+
+// ---- timeline -----------------------------------------------------------------------------
+struct OpScope {
+    lancet_ctx* c;
+    size_t i;
+    cudaStream_t s;
+    OpScope(lancet_ctx* ctx, const char* name, int lane, int chunk, cudaStream_t st) : c(ctx), s(st) {
+        i = (size_t)-1;
+        if (!(c->cfg.flags & LANCET_FLAG_TIMELINE)) return;
+        if (c->tl_used + 2 > c->tl_events.size()) {
+            for (int q = 0; q < 64; ++q) {
+                cudaEvent_t e;
+                cudaEventCreate(&e);
+                c->tl_events.push_back(e);
+            }
+        }
+        OpEvent op;
+        op.name = name;
+        op.lane = lane;
+        op.chunk = chunk;
+        op.beg = c->tl_events[c->tl_used++];
+        op.end = c->tl_events[c->tl_used++];
+        cudaEventRecord(op.beg, s);
+        c->ops.push_back(op);
+        i = c->ops.size() - 1;
+    }
+    ~OpScope() {
+        if (i != (size_t)-1) cudaEventRecord(c->ops[i].end, s);
+    }
+};
+
+// ---- grouped GEMM dispatch ---------------------------------------------------------------
+lancet_status run_gemm(lancet_ctx* c, GemmArgs& a, cudaStream_t s, int* launches)
+{
+    const bool use_tc = c->bf16 && !(c->cfg.flags & LANCET_FLAG_SIMT_GEMM) && gemm_tc_supported(a);
+    if (use_tc) {
+        const int sms = c->cfg.gemm_sms > 0 ? std::min(c->cfg.gemm_sms, c->num_sms) : c->num_sms;
+        *launches += launch_gemm_tc(a, sms, s);
+    } else {
+        *launches += launch_gemm_simt(a, c->bf16, s);
+    }
+    CHECK_LAUNCH();
+    return LANCET_OK;
+}
+
+// M-grouped expert GEMMs of the forward over groups [g0, g0+ng) of the expert-side table.
+lancet_status expert_forward(lancet_ctx* c, const int* grp_rows, const int* grp_off, int ng,
+                             int max_rows, cudaStream_t s, int chunk, int* launches)
+{
+    const int d = c->cfg.d_model, f = c->cfg.d_ffn;
+    GemmArgs a{};
+    a.mode = GEMM_M_GROUPED; a.n_groups = ng; a.gpw = 1;
+    a.grp_rows = grp_rows; a.grp_off = grp_off; a.max_rows = max_rows; a.act = c->cfg.act;
+    {   // fc1: H = act(X W1^T), G' = act'(X W1^T)
+        OpScope op(c, "expert_fc1", 0, chunk, s);
+        a.A = c->world > 1 ? c->xe : c->xs; a.lda = d;
+        a.B = c->w1; a.ldb = d; a.b_group_stride = (long)f * d; a.b_mn = false; a.a_mn = false;
+        a.C = c->H; a.C2 = c->Gp; a.ldc = f; a.N = f; a.K = d; a.epi = EPI_ACT;
+        lancet_status st = run_gemm(c, a, s, launches);
+        if (st) return st;
+    }
+    {   // fc2: O = H W2^T
+        OpScope op(c, "expert_fc2", 0, chunk, s);
+        a.A = c->H; a.lda = f;
+        a.B = c->w2; a.ldb = f; a.b_group_stride = (long)d * f;
+        a.C = c->out; a.C2 = nullptr; a.ldc = d; a.N = d; a.K = f; a.epi = EPI_STORE;
+        return run_gemm(c, a, s, launches);
+    }
+}
+
+// dX GEMMs (critical path) of the backward.
+lancet_status expert_backward_dx(lancet_ctx* c, const void* dout, const int* grp_rows,
+                                 const int* grp_off, int ng, int max_rows, cudaStream_t s,
+                                 int chunk, int* launches)
+{
+    const int d = c->cfg.d_model, f = c->cfg.d_ffn;
+    GemmArgs a{};
+    a.mode = GEMM_M_GROUPED; a.n_groups = ng; a.gpw = 1;
+    a.grp_rows = grp_rows; a.grp_off = grp_off; a.max_rows = max_rows; a.act = c->cfg.act;
+    {   // dA = (dO W2) * act'(A):  B(n=f, k=d) = W2[e][k][n]  (MN-major)
+        OpScope op(c, "expert_dfc2", 0, chunk, s);
+        a.A = dout; a.lda = d; a.a_mn = false;
+        a.B = c->w2; a.ldb = f; a.b_group_stride = (long)d * f; a.b_mn = true;
+        a.C = c->dA; a.ldc = f; a.aux = c->Gp; a.N = f; a.K = d; a.epi = EPI_DACT;
+        lancet_status st = run_gemm(c, a, s, launches);
+        if (st) return st;
+    }
+    {   // dX = dA W1:  B(n=d, k=f) = W1[e][k][n]  (MN-major)
+        OpScope op(c, "expert_dfc1", 0, chunk, s);
+        a.A = c->dA; a.lda = f;
+        a.B = c->w1; a.ldb = d; a.b_group_stride = (long)f * d; a.b_mn = true;
+        a.C = c->dXe; a.ldc = d; a.aux = nullptr; a.N = d; a.K = f; a.epi = EPI_STORE;
+        return run_gemm(c, a, s, launches);
+    }
+}
+
+// dW GEMMs (K-grouped over each group's token rows): dW2 (+)= dO^T H, dW1 (+)= dA^T X.
+lancet_status expert_backward_dw(lancet_ctx* c, const void* dout, const int* grp_rows,
+                                 const int* grp_off, int ng, float* dw1, float* dw2,
+                                 int accumulate, cudaStream_t s, int chunk, int* launches)
+{
+    const int d = c->cfg.d_model, f = c->cfg.d_ffn;
+    GemmArgs a{};
+    a.mode = GEMM_K_GROUPED; a.n_groups = ng; a.gpw = 1;
+    a.grp_rows = grp_rows; a.grp_off = grp_off; a.accumulate = accumulate;
+    a.a_mn = true; a.b_mn = true; a.epi = EPI_F32; a.b_group_stride = 0;
+    {
+        OpScope op(c, "expert_dw2", 0, chunk, s);
+        a.A = dout; a.lda = d; a.B = c->H; a.ldb = f;
+        a.C = dw2; a.ldc = f; a.c_group_stride = (long)d * f; a.M = d; a.N = f;
+        lancet_status st = run_gemm(c, a, s, launches);
+        if (st) return st;
+    }
+    {
+        OpScope op(c, "expert_dw1", 0, chunk, s);
+        a.A = c->dA; a.lda = f; a.B = c->world > 1 ? c->xe : c->xs; a.ldb = d;
+        a.C = dw1; a.ldc = d; a.c_group_stride = (long)f * d; a.M = f; a.N = d;
+        return run_gemm(c, a, s, launches);
+    }
+}
+
+lancet_status validate_cfg(const lancet_layer_config* cfg, int world)
+{
+    if (!cfg) return fail(nullptr, LANCET_ERR_ARG, "cfg is NULL");
+    if (cfg->d_model <= 0 || cfg->d_model % 8) return fail(nullptr, LANCET_ERR_ARG, "d_model must be a positive multiple of 8");
+    if (cfg->d_ffn <= 0 || cfg->d_ffn % 8) return fail(nullptr, LANCET_ERR_ARG, "d_ffn must be a positive multiple of 8");
+    if (cfg->n_experts < 1 || cfg->n_experts > kMaxExperts) return fail(nullptr, LANCET_ERR_ARG, "n_experts must be in [1, 256]");
+    if (world < 1 || cfg->n_experts % world) return fail(nullptr, LANCET_ERR_ARG, "n_experts % world != 0");
+    if (cfg->max_tokens < 1) return fail(nullptr, LANCET_ERR_ARG, "max_tokens < 1");
+    if (cfg->max_k < 1 || cfg->max_k > kMaxK || cfg->max_k > cfg->n_experts) return fail(nullptr, LANCET_ERR_ARG, "max_k must be in [1, min(8, E)]");
+    if (cfg->max_chunks < 1 || cfg->max_chunks > kMaxChunks) return fail(nullptr, LANCET_ERR_ARG, "max_chunks must be in [1, 64]");
+    if (cfg->dtype != LANCET_BF16 && cfg->dtype != LANCET_FP32) return fail(nullptr, LANCET_ERR_ARG, "bad dtype");
+    if (cfg->act < 0 || cfg->act > 2) return fail(nullptr, LANCET_ERR_ARG, "bad act");
+    return LANCET_OK;
+}
+
+lancet_status create_common(lancet_ctx* c, int world, int rank, int device, const lancet_layer_config* cfg)
+{
+    c->world = world;
+    c->rank = rank;
+    c->device = device;
+    c->cfg = *cfg;
+    c->E_l = cfg->n_experts / world;
+    c->bf16 = cfg->dtype == LANCET_BF16;
+    c->elt = c->bf16 ? 2 : 4;
+    CK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+        return fail(c, LANCET_ERR_UNSUPPORTED, std::string("lancet_moe needs an sm_100 (B200) device, found ") + prop.name);
+    c->num_sms = prop.multiProcessorCount;
+    CK(cudaStreamCreateWithFlags(&c->s_comp, cudaStreamNonBlocking));
+    int lo, hi;
+    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CK(cudaStreamCreateWithPriority(&c->s_comm, cudaStreamNonBlocking, hi));
+    CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->ev_counts, cudaEventDisableTiming));
+    CK(cudaEventCreate(&c->ev_tl_base));
+    for (int i = 0; i < 8 * kMaxChunks + 16; ++i) {
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c->ev_pool.push_back(e);
+    }
+
+    const int E = cfg->n_experts, T = cfg->max_tokens, K = cfg->max_k, d = cfg->d_model, f = cfg->d_ffn;
+    const int n_tiles = ceil_div(T, kScanTile);
+    c->rows_src = T * K + E * kRowAlign;
+    lancet_status st;
+#define AL(ptr, bytes) if ((st = dalloc(c, &(ptr), (bytes)))) return st
+    AL(c->logits, sizeof(float) * (size_t)T * E);
+    AL(c->idx, sizeof(int) * (size_t)T * K);
+    AL(c->w, sizeof(float) * (size_t)T * K);
+    AL(c->slot, sizeof(int) * (size_t)T * K);
+    AL(c->hist, sizeof(int) * (size_t)n_tiles * E);
+    AL(c->S, sizeof(int) * (size_t)E * (kMaxChunks + 1));
+    AL(c->send_rows, sizeof(int) * E);
+    AL(c->send_off, sizeof(int) * E);
+    AL(c->g, sizeof(float) * (size_t)T * K);
+    AL(c->dlogit, sizeof(float) * (size_t)T * E);
+    AL(c->dwg_partial, sizeof(float) * dwg_partial_floats(T, d, E));
+    AL(c->counts_dev, sizeof(int) * 2 * (size_t)E * kMaxChunks);
+    AL(c->grp_dev, sizeof(int) * 2 * (size_t)c->E_l * kMaxChunks);
+    const size_t rs = (size_t)c->rows_src * d * c->elt;
+    AL(c->xs, rs);
+    AL(c->dcomb, rs);
+    if (world == 1) {
+        c->rows_exp = c->rows_src;
+        c->xe = c->xs;
+        c->comb = nullptr;                      // world 1: comb == out
+        c->dout = c->dcomb;
+        c->dxcomb = nullptr;                    // world 1: dxcomb == dXe
+        const size_t rf = (size_t)c->rows_exp * f * c->elt, rd = (size_t)c->rows_exp * d * c->elt;
+        if (cfg->act != LANCET_ACT_IDENTITY_EXPERT) {
+            AL(c->H, rf); AL(c->Gp, rf); AL(c->dA, rf);
+            AL(c->out, rd); AL(c->dXe, rd);
+        }
+    } else {
+        AL(c->comb, rs);
+        AL(c->dxcomb, rs);
+        CK(cudaMallocHost(&c->h_counts, sizeof(int) * 2 * (size_t)E * kMaxChunks));
+        CK(cudaMallocHost(&c->h_grp, sizeof(int) * 2 * (size_t)c->E_l * kMaxChunks));
+        c->rows_exp = 0;                        // grown on demand by the forward
+    }
+#undef AL
+    CK(cudaMemset(c->xs, 0, rs));
+    CK(cudaMemset(c->dcomb, 0, rs));
+    CK(cudaDeviceSynchronize());
+    return LANCET_OK;
+}
+
+// Expert-side buffers for world > 1, grown to `rows` rows.
+lancet_status ensure_expert_rows(lancet_ctx* c, int rows)
+{
+    if (rows <= c->rows_exp) return LANCET_OK;
+    const int d = c->cfg.d_model, f = c->cfg.d_ffn;
+    const int newrows = round_up(std::max(rows, c->rows_exp + c->rows_exp / 4), kRowAlign);
+    CK(cudaDeviceSynchronize());
+    void* olds[] = {c->xe, c->H, c->Gp, c->out, c->dout, c->dA, c->dXe};
+    for (void* p : olds) {
+        if (!p) continue;
+        for (size_t i = 0; i < c->allocs.size(); ++i)
+            if (c->allocs[i].p == p) { cudaFree(p); c->allocs.erase(c->allocs.begin() + i); break; }
+    }
+    c->xe = c->H = c->Gp = c->out = c->dout = c->dA = c->dXe = nullptr;
+    const size_t rf = (size_t)newrows * f * c->elt, rd = (size_t)newrows * d * c->elt;
+    lancet_status st;
+    if ((st = dalloc(c, &c->xe, rd))) return st;
+    if ((st = dalloc(c, &c->dout, rd))) return st;
+    if (c->cfg.act != LANCET_ACT_IDENTITY_EXPERT) {
+        if ((st = dalloc(c, &c->H, rf))) return st;
+        if ((st = dalloc(c, &c->Gp, rf))) return st;
+        if ((st = dalloc(c, &c->dA, rf))) return st;
+        if ((st = dalloc(c, &c->out, rd))) return st;
+        if ((st = dalloc(c, &c->dXe, rd))) return st;
+    }
+    c->rows_exp = newrows;
+    return LANCET_OK;
+}
+
+lancet_status check_ready(lancet_ctx* c)
+{
+    if (!c) return fail(nullptr, LANCET_ERR_ARG, "ctx is NULL");
+    if (c->poisoned) return fail(c, LANCET_ERR_STATE, "context poisoned by an earlier error: " + c->err);
+    cudaError_t e = cudaSetDevice(c->device);
+    if (e != cudaSuccess) return fail(c, LANCET_ERR_CUDA, cudaGetErrorString(e));
+    return LANCET_OK;
+}
+
+// ---- world > 1 exchange plans -----------------------------------------------------------
+// Host view of the routing sizes after the counts exchange.
+struct Plan {
+    int E, E_l, G, n;
+    std::vector<int> send;      // [E][n]
+    std::vector<int> recv;      // [G][E_l][n]
+    std::vector<int> S;         // [E][n+1] prefix of send over chunks
+    std::vector<int> send_off;  // [E]
+    std::vector<int> grp_rows;  // [n][E_l]  (table order: chunk-major)
+    std::vector<int> grp_off;   // [n][E_l]  row offsets, buffer order (e_l, c)
+    std::vector<int> src_off;   // [G][E_l][n] row offset of src's rows inside group (e_l, c)
+    int rows_total = 0;
+
+    void build(const int* h_send, const int* h_recv) {
+        send.assign(h_send, h_send + E * n);
+        recv.assign(h_recv, h_recv + G * E_l * n);
+        S.assign(E * (n + 1), 0);
+        send_off.assign(E, 0);
+        int off = 0;
+        for (int e = 0; e < E; ++e) {
+            for (int c = 0; c < n; ++c) S[e * (n + 1) + c + 1] = S[e * (n + 1) + c] + send[e * n + c];
+            send_off[e] = off;
+            off += round_up(S[e * (n + 1) + n], kRowAlign);
+        }
+        grp_rows.assign(n * E_l, 0);
+        grp_off.assign(n * E_l, 0);
+        src_off.assign(G * E_l * n, 0);
+        int row = 0;
+        for (int el = 0; el < E_l; ++el)
+            for (int c = 0; c < n; ++c) {
+                int r = 0;
+                for (int src = 0; src < G; ++src) {
+                    src_off[(src * E_l + el) * n + c] = r;
+                    r += recv[(src * E_l + el) * n + c];
+                }
+                grp_rows[c * E_l + el] = r;
+                grp_off[c * E_l + el] = row;
+                row += round_up(r, kRowAlign);
+            }
+        rows_total = row;
+    }
+};
+
+__global__ void send_counts_kernel(const int* __restrict__ S, int E, int n, int* __restrict__ out)
+{
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= E * n) return;
+    const int e = q / n, c = q % n;
+    out[q] = S[e * (n + 1) + c + 1] - S[e * (n + 1) + c];
+}
+
+}  // namespace
+
+// =========================================================================================
+// C-ABI
+// =========================================================================================
+
+LANCET_API int32_t lancet_abi_version(void) { return LANCET_ABI_VERSION; }
+
+LANCET_API const char* lancet_last_error(const lancet_ctx* ctx)
+{
+    return ctx ? ctx->err.c_str() : g_thread_err.c_str();
+}
+
+LANCET_API lancet_status lancet_nccl_unique_id(void* id_out)
+{
+    if (!id_out) return fail(nullptr, LANCET_ERR_ARG, "id_out is NULL");
+    std::string err;
+    if (nccl_unique_id(id_out, err)) return fail(nullptr, LANCET_ERR_NCCL, err);
+    return LANCET_OK;
+}
+
+LANCET_API lancet_status lancet_create(lancet_ctx** out, int32_t world, int32_t rank,
+                                       int32_t cuda_device, const void* nccl_id,
+                                       const lancet_layer_config* cfg)
+{
+    if (!out) return fail(nullptr, LANCET_ERR_ARG, "out is NULL");
+    *out = nullptr;
+    if (world < 1 || rank < 0 || rank >= world) return fail(nullptr, LANCET_ERR_ARG, "bad world/rank");
+    if (world > 1 && !nccl_id) return fail(nullptr, LANCET_ERR_ARG, "world > 1 needs an NCCL id");
+    lancet_status st = validate_cfg(cfg, world);
+    if (st) return st;
+    auto* c = new lancet_ctx();
+    st = create_common(c, world, rank, cuda_device, cfg);
+    if (!st && world > 1) {
+        std::string err;
+        c->comm = make_nccl_transport(world, rank, nccl_id, err);
+        if (!c->comm) st = fail(c, LANCET_ERR_NCCL, err);
+        else if (c->comm->check_same(cfg_hash(*cfg), c->s_comm, err)) st = fail(c, LANCET_ERR_ARG, err);
+    }
+    if (st) {
+        g_thread_err = c->err;
+        lancet_destroy(c);
+        return st;
+    }
+    *out = c;
+    return LANCET_OK;
+}
+
+LANCET_API lancet_status lancet_local_group_create(lancet_local_group** out, int32_t world)
+{
+    if (!out || world < 1) return fail(nullptr, LANCET_ERR_ARG, "bad arguments");
+    *out = new lancet_local_group{local_group_create(world), world};
+    return LANCET_OK;
+}
+
+LANCET_API lancet_status lancet_local_group_destroy(lancet_local_group* g)
+{
+    if (g) {
+        local_group_destroy(g->impl);
+        delete g;
+    }
+    return LANCET_OK;
+}
+
+LANCET_API lancet_status lancet_create_local(lancet_ctx** out, lancet_local_group* group,
+                                             int32_t rank, int32_t cuda_device,
+                                             const lancet_layer_config* cfg)
+{
+    if (!out || !group) return fail(nullptr, LANCET_ERR_ARG, "bad arguments");
+    *out = nullptr;
+    const int world = group->world;
+    if (rank < 0 || rank >= world) return fail(nullptr, LANCET_ERR_ARG, "bad rank");
+    lancet_status st = validate_cfg(cfg, world);
+    if (st) return st;
+    auto* c = new lancet_ctx();
+    st = create_common(c, world, rank, cuda_device, cfg);
+    if (!st && world > 1) {
+        std::string err;
+        c->comm = make_local_transport(group->impl, rank, err);
+        if (!c->comm) st = fail(c, LANCET_ERR_ARG, err);
+        else if (c->comm->check_same(cfg_hash(*cfg), c->s_comm, err)) st = fail(c, LANCET_ERR_ARG, err);
+    }
+    if (st) {
+        g_thread_err = c->err;
+        lancet_destroy(c);
+        return st;
+    }
+    *out = c;
+    return LANCET_OK;
+}
+
+LANCET_API lancet_status lancet_destroy(lancet_ctx* c)
+{
+    if (!c) return LANCET_OK;
+    cudaSetDevice(c->device);
+    if (c->comm) {
+        if (c->poisoned) c->comm->abort();
+        else cudaDeviceSynchronize();
+        delete c->comm;
+    }
+    free_all(c);
+    for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->tl_events) cudaEventDestroy(e);
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
+    if (c->ev_counts) cudaEventDestroy(c->ev_counts);
+    if (c->ev_tl_base) cudaEventDestroy(c->ev_tl_base);
+    if (c->s_comp) cudaStreamDestroy(c->s_comp);
+    if (c->s_comm) cudaStreamDestroy(c->s_comm);
+    delete c;
+    return LANCET_OK;
+}
+
+LANCET_API lancet_status lancet_set_flags(lancet_ctx* c, uint32_t flags)
+{
+    if (!c) return fail(nullptr, LANCET_ERR_ARG, "ctx is NULL");
+    if ((flags & LANCET_FLAG_RENORMALIZE) != (c->cfg.flags & LANCET_FLAG_RENORMALIZE) && c->world > 1)
+        return fail(c, LANCET_ERR_ARG, "RENORMALIZE must be set at creation (checked across ranks)");
+    c->cfg.flags = flags;
+    return LANCET_OK;
+}
+
+LANCET_API lancet_status lancet_moe_forward(lancet_ctx* c, const void* x, const float* wg,
+                                            const void* w1, const void* w2, int32_t T, int32_t k,
+                                            float cf, int32_t n, void* y, int32_t* expert_idx,
+                                            int32_t* slot_out, float* combine_w,
+                                            lancet_stream_t stream_)
+{
+    lancet_status st = check_ready(c);
+    if (st) return st;
+    const bool ident = c->cfg.act == LANCET_ACT_IDENTITY_EXPERT;
+    const int E = c->cfg.n_experts, d = c->cfg.d_model;
+    if (!x || !wg || !y || (!ident && (!w1 || !w2))) return fail(c, LANCET_ERR_ARG, "null required pointer");
+    if (T < 1 || T > c->cfg.max_tokens) return fail(c, LANCET_ERR_ARG, "T must be in [1, max_tokens]");
+    if (k < 1 || k > c->cfg.max_k || k > E) return fail(c, LANCET_ERR_ARG, "k must be in [1, min(E, max_k)]");
+    if (!(cf > 0.f) || !std::isfinite(cf)) return fail(c, LANCET_ERR_ARG, "capacity_factor must be > 0");
+    if (n < 1 || n > std::min<int>(T, c->cfg.max_chunks)) return fail(c, LANCET_ERR_ARG, "n_chunks must be in [1, min(T, max_chunks)]");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream_);
+    c->have_fwd = false;
+    c->x = x; c->wg = wg; c->w1 = w1; c->w2 = w2;
+    c->T = T; c->k = k; c->n = n; c->cf = cf;
+    c->C = capacity_of(T, k, E, cf);
+    c->launches_fwd = 0;
+    c->ops.clear();
+    c->tl_used = 0;
+    int& L = c->launches_fwd;
+    const bool tl = c->cfg.flags & LANCET_FLAG_TIMELINE;
+    if (tl) CK(cudaEventRecord(c->ev_tl_base, s));
+
+    RouteArgs ra{};
+    ra.x = x; ra.wg = wg; ra.T = T; ra.d = d; ra.E = E; ra.k = k; ra.C = c->C; ra.n_chunks = n;
+    ra.renorm = (c->cfg.flags & LANCET_FLAG_RENORMALIZE) ? 1 : 0;
+    ra.logits = c->logits; ra.idx = c->idx; ra.w = c->w; ra.slot = c->slot; ra.hist = c->hist;
+    ra.S = c->S; ra.send_rows = c->send_rows; ra.send_off = c->send_off;
+    DispatchArgs da{T, k, d, E, c->idx, c->slot, c->w, c->send_off, c->send_rows};
+
+    if (c->world == 1) {
+        // ---- single GPU: no exchange, no host synchronisation --------------------------
+        { OpScope op(c, "gate", 0, -1, s); L += launch_routing(ra, c->bf16, s); }
+        CHECK_LAUNCH();
+        { OpScope op(c, "permute", 0, -1, s); L += launch_permute(da, x, c->xs, c->bf16, s); }
+        CHECK_LAUNCH();
+        const void* comb = c->xs;
+        if (!ident) {
+            const int max_rows = round_up(c->C, kRowAlign);
+            st = expert_forward(c, c->send_rows, c->send_off, E, max_rows, s, -1, &L);
+            if (st) return st;
+            comb = c->out;
+        }
+        { OpScope op(c, "combine", 0, -1, s); L += launch_combine(da, comb, y, 0, T, c->bf16, s); }
+        CHECK_LAUNCH();
+    } else {
+        // ---- expert parallel over world ranks ---------------------------------------------
+        const int G = c->world, E_l = c->E_l;
+        const bool serial = c->cfg.flags & LANCET_FLAG_SERIAL;
+        cudaStream_t sc = c->s_comp, sm = serial ? c->s_comp : c->s_comm;
+        CK(cudaEventRecord(c->ev_fork, s));
+        CK(cudaStreamWaitEvent(sc, c->ev_fork, 0));
+        CK(cudaStreamWaitEvent(c->s_comm, c->ev_fork, 0));
+        size_t ev_i = 0;
+        auto next_ev = [&]() { return c->ev_pool[ev_i++]; };
+
+        { OpScope op(c, "gate", 0, -1, sc); L += launch_routing(ra, c->bf16, sc); }
+        int* d_send = c->counts_dev;                       // [E][n]
+        int* d_recv = c->counts_dev + E * n;               // [G][E_l][n]
+        send_counts_kernel<<<ceil_div(E * n, 256), 256, 0, sc>>>(c->S, E, n, d_send);
+        ++L;
+        CHECK_LAUNCH();
+        cudaEvent_t ev_route = next_ev();
+        CK(cudaEventRecord(ev_route, sc));
+        {   // C1: size exchange, once for all chunks (R11)
+            CK(cudaStreamWaitEvent(sm, ev_route, 0));
+            OpScope op(c, "a2a_counts", 1, -1, sm);
+            std::vector<P2P> sends, recvs;
+            const size_t b = sizeof(int) * E_l * n;
+            for (int p = 0; p < G; ++p) {
+                sends.push_back({p, d_send + p * E_l * n, b});
+                recvs.push_back({p, d_recv + p * E_l * n, b});
+            }
+            std::string err;
+            if (c->comm->exchange(sends, recvs, sm, err)) return fail(c, LANCET_ERR_NCCL, err);
+            CK(cudaMemcpyAsync(c->h_counts, c->counts_dev, sizeof(int) * (E * n + G * E_l * n),
+                               cudaMemcpyDeviceToHost, sm));
+            CK(cudaEventRecord(c->ev_counts, sm));
+        }
+        // K3 permute overlaps the size exchange
+        { OpScope op(c, "permute", 0, -1, sc); L += launch_permute(da, x, c->xs, c->bf16, sc); }
+        CHECK_LAUNCH();
+        cudaEvent_t ev_perm = next_ev();
+        CK(cudaEventRecord(ev_perm, sc));
+        CK(cudaEventSynchronize(c->ev_counts));            // the one host synchronisation
+        Plan pl{E, E_l, G, n};
+        pl.build(c->h_counts, c->h_counts + E * n);
+        st = ensure_expert_rows(c, std::max(pl.rows_total, kRowAlign));
+        if (st) return st;
+        c->host_send = pl.send;
+        c->host_recv = pl.recv;
+        c->host_grp_rows = pl.grp_rows;
+        c->host_grp_off = pl.grp_off;
+        c->n_groups = n * E_l;
+        int* d_grp_rows = c->grp_dev;
+        int* d_grp_off = c->grp_dev + n * E_l;
+        memcpy(c->h_grp, pl.grp_rows.data(), sizeof(int) * n * E_l);
+        memcpy(c->h_grp + n * E_l, pl.grp_off.data(), sizeof(int) * n * E_l);
+        CK(cudaMemcpyAsync(c->grp_dev, c->h_grp, sizeof(int) * 2 * n * E_l, cudaMemcpyHostToDevice, sc));
+        L += launch_zero_pads(c->xe, d, d_grp_off, d_grp_rows, n * E_l, (int)c->elt, sc);
+        CHECK_LAUNCH();
+        const size_t rowb = (size_t)d * c->elt;
+        char* xs = (char*)c->xs;
+        char* xe = (char*)c->xe;
+        char* comb = (char*)c->comb;
+        const int nc = serial ? 1 : n;                     // serial baseline: chunks merged
+        auto chunk_range = [&](int cc, int& c0, int& c1) {
+            if (serial) { c0 = 0; c1 = n; } else { c0 = cc; c1 = cc + 1; }
+        };
+        // S1: dispatch all-to-alls D0..D(n-1) on the comm lane (stage order)
+        std::vector<cudaEvent_t> ev_disp(nc), ev_exp(nc), ev_comb(nc);
+        CK(cudaStreamWaitEvent(sm, ev_perm, 0));
+        cudaEvent_t ev_pads = next_ev();
+        CK(cudaEventRecord(ev_pads, sc));
+        CK(cudaStreamWaitEvent(sm, ev_pads, 0));
+        for (int cc = 0; cc < nc; ++cc) {
+            int c0, c1;
+            chunk_range(cc, c0, c1);
+            OpScope op(c, "a2a_dispatch", 1, serial ? -1 : cc, sm);
+            std::vector<P2P> sends, recvs;
+            for (int p = 0; p < G; ++p)
+                for (int i = 0; i < E_l; ++i) {
+                    const int e = p * E_l + i;
+                    for (int ch = c0; ch < c1; ++ch)
+                        sends.push_back({p, xs + (size_t)(pl.send_off[e] + pl.S[e * (n + 1) + ch]) * rowb,
+                                         (size_t)pl.send[e * n + ch] * rowb});
+                }
+            for (int p = 0; p < G; ++p)
+                for (int el = 0; el < E_l; ++el)
+                    for (int ch = c0; ch < c1; ++ch)
+                        recvs.push_back({p, xe + (size_t)(pl.grp_off[ch * E_l + el] + pl.src_off[(p * E_l + el) * n + ch]) * rowb,
+                                         (size_t)pl.recv[(p * E_l + el) * n + ch] * rowb});
+            std::string err;
+            if (c->comm->exchange(sends, recvs, sm, err)) return fail(c, LANCET_ERR_NCCL, err);
+            ev_disp[cc] = next_ev();
+            CK(cudaEventRecord(ev_disp[cc], sm));
+        }
+        // experts per chunk on the compute lane
+        for (int cc = 0; cc < nc; ++cc) {
+            int c0, c1;
+            chunk_range(cc, c0, c1);
+            CK(cudaStreamWaitEvent(sc, ev_disp[cc], 0));
+            if (!ident) {
+                int mr = 0;
+                for (int ch = c0; ch < c1; ++ch)
+                    for (int el = 0; el < E_l; ++el) mr = std::max(mr, round_up(pl.grp_rows[ch * E_l + el], kRowAlign));
+                st = expert_forward(c, d_grp_rows + c0 * E_l, d_grp_off + c0 * E_l, (c1 - c0) * E_l,
+                                    std::max(mr, kRowAlign), sc, serial ? -1 : cc, &L);
+                if (st) return st;
+            }
+            ev_exp[cc] = next_ev();
+            CK(cudaEventRecord(ev_exp[cc], sc));
+        }
+        // combine all-to-alls C0..C(n-1)
+        const char* eout = ident ? xe : (const char*)c->out;
+        for (int cc = 0; cc < nc; ++cc) {
+            int c0, c1;
+            chunk_range(cc, c0, c1);
+            CK(cudaStreamWaitEvent(sm, ev_exp[cc], 0));
+            OpScope op(c, "a2a_combine", 1, serial ? -1 : cc, sm);
+            std::vector<P2P> sends, recvs;
+            for (int p = 0; p < G; ++p)
+                for (int el = 0; el < E_l; ++el)
+                    for (int ch = c0; ch < c1; ++ch)
+                        sends.push_back({p, (void*)(eout + (size_t)(pl.grp_off[ch * E_l + el] + pl.src_off[(p * E_l + el) * n + ch]) * rowb),
+                                         (size_t)pl.recv[(p * E_l + el) * n + ch] * rowb});
+            for (int p = 0; p < G; ++p)
+                for (int i = 0; i < E_l; ++i) {
+                    const int e = p * E_l + i;
+                    for (int ch = c0; ch < c1; ++ch)
+                        recvs.push_back({p, comb + (size_t)(pl.send_off[e] + pl.S[e * (n + 1) + ch]) * rowb,
+                                         (size_t)pl.send[e * n + ch] * rowb});
+                }
+            std::string err;
+            if (c->comm->exchange(sends, recvs, sm, err)) return fail(c, LANCET_ERR_NCCL, err);
+            ev_comb[cc] = next_ev();
+            CK(cudaEventRecord(ev_comb[cc], sm));
+        }
+        // gather per chunk (chunk c's tokens are final as soon as combine c lands)
+        for (int cc = 0; cc < nc; ++cc) {
+            CK(cudaStreamWaitEvent(sc, ev_comb[cc], 0));
+            const int t0 = serial ? 0 : chunk_start(T, n, cc), t1 = serial ? T : chunk_start(T, n, cc + 1);
+            OpScope op(c, "combine", 0, serial ? -1 : cc, sc);
+            L += launch_combine(da, comb, y, t0, t1, c->bf16, sc);
+        }
+        CHECK_LAUNCH();
+        CK(cudaEventRecord(c->ev_join, sc));
+        CK(cudaStreamWaitEvent(s, c->ev_join, 0));
+        if (sm != sc) {
+            cudaEvent_t e2 = next_ev();
+            CK(cudaEventRecord(e2, sm));
+            CK(cudaStreamWaitEvent(s, e2, 0));
+        }
+    }
+    const size_t tk = (size_t)T * k;
+    if (expert_idx) CK(cudaMemcpyAsync(expert_idx, c->idx, tk * sizeof(int), cudaMemcpyDeviceToDevice, s));
+    if (slot_out) CK(cudaMemcpyAsync(slot_out, c->slot, tk * sizeof(int), cudaMemcpyDeviceToDevice, s));
+    if (combine_w) CK(cudaMemcpyAsync(combine_w, c->w, tk * sizeof(float), cudaMemcpyDeviceToDevice, s));
+    c->have_fwd = true;
+    return LANCET_OK;
+}
+
+LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void* dx, float* dwg,
+                                             float* dw1, float* dw2, lancet_stream_t stream_)
+{
+    lancet_status st = check_ready(c);
+    if (st) return st;
+    if (!c->have_fwd) return fail(c, LANCET_ERR_STATE, "backward without a preceding forward");
+    const bool ident = c->cfg.act == LANCET_ACT_IDENTITY_EXPERT;
+    if (!dy || !dx || !dwg || (!ident && (!dw1 || !dw2))) return fail(c, LANCET_ERR_ARG, "null required pointer");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream_);
+    const int E = c->cfg.n_experts, d = c->cfg.d_model, T = c->T, k = c->k, n = c->n;
+    const int renorm = (c->cfg.flags & LANCET_FLAG_RENORMALIZE) ? 1 : 0;
+    c->launches_bwd = 0;
+    int& L = c->launches_bwd;
+    DispatchArgs da{T, k, d, E, c->idx, c->slot, c->w, c->send_off, c->send_rows};
+
+    if (c->world == 1) {
+        const void* comb = ident ? c->xs : c->out;
+        { OpScope op(c, "combine_bwd", 0, -1, s);
+          L += launch_combine_bwd(da, dy, comb, c->g, c->dcomb, 0, T, true, c->bf16, s); }
+        CHECK_LAUNCH();
+        const void* dxe = c->dcomb;
+        if (!ident) {
+            const int max_rows = round_up(c->C, kRowAlign);
+            st = expert_backward_dx(c, c->dcomb, c->send_rows, c->send_off, E, max_rows, s, -1, &L);
+            if (st) return st;
+            st = expert_backward_dw(c, c->dcomb, c->send_rows, c->send_off, E, dw1, dw2, 0, s, -1, &L);
+            if (st) return st;
+            dxe = c->dXe;
+        }
+        { OpScope op(c, "unpermute_gate_bwd", 0, -1, s);
+          L += launch_unpermute_gate_bwd(da, dxe, c->g, c->logits, c->wg, renorm, dx, c->dlogit, 0, T, c->bf16, s); }
+        CHECK_LAUNCH();
+        { OpScope op(c, "gate_dwg", 0, -1, s);
+          L += launch_dwg(c->x, c->dlogit, T, d, E, c->dwg_partial, dwg, c->bf16, s); }
+        CHECK_LAUNCH();
+        return LANCET_OK;
+    }
+
+    // ---- expert parallel (S2) ---------------------------------------------------------------
+    const int G = c->world, E_l = c->E_l;
+    const bool serial = c->cfg.flags & LANCET_FLAG_SERIAL;
+    const bool late_dw = serial || (c->cfg.flags & LANCET_FLAG_NO_DW_OVERLAP);
+    cudaStream_t sc = c->s_comp, sm = serial ? c->s_comp : c->s_comm;
+    CK(cudaEventRecord(c->ev_fork, s));
+    CK(cudaStreamWaitEvent(sc, c->ev_fork, 0));
+    CK(cudaStreamWaitEvent(c->s_comm, c->ev_fork, 0));
+    size_t ev_i = 0;
+    auto next_ev = [&]() { return c->ev_pool[ev_i++]; };
+    Plan pl{E, E_l, G, n};
+    pl.build(c->host_send.data(), c->host_recv.data());
+    int* d_grp_rows = c->grp_dev;
+    int* d_grp_off = c->grp_dev + n * E_l;
+    const size_t rowb = (size_t)d * c->elt;
+    const int nc = serial ? 1 : n;
+    auto chunk_range = [&](int cc, int& c0, int& c1) {
+        if (serial) { c0 = 0; c1 = n; } else { c0 = cc; c1 = cc + 1; }
+    };
+    auto tok_range = [&](int cc, int& t0, int& t1) {
+        t0 = serial ? 0 : chunk_start(T, n, cc);
+        t1 = serial ? T : chunk_start(T, n, cc + 1);
+    };
+    // pads of the received dO rows must be zero (K-grouped dW reads whole 128-row blocks)
+    L += launch_zero_pads(c->dout, d, d_grp_off, d_grp_rows, n * E_l, (int)c->elt, sc);
+    const void* comb = c->comb;     // o_tj returned by the combine all-to-all (source side)
+    std::vector<cudaEvent_t> ev_k5(nc), ev_b1(nc), ev_dx(nc), ev_b2(nc);
+    for (int cc = 0; cc < nc; ++cc) {
+        int t0, t1;
+        tok_range(cc, t0, t1);
+        OpScope op(c, "combine_bwd", 0, serial ? -1 : cc, sc);
+        L += launch_combine_bwd(da, dy, comb, c->g, c->dcomb, t0, t1, cc == 0, c->bf16, sc);
+        ev_k5[cc] = next_ev();
+        CK(cudaEventRecord(ev_k5[cc], sc));
+    }
+    CHECK_LAUNCH();
+    char* dcomb = (char*)c->dcomb;
+    char* dout = (char*)c->dout;
+    // backward a2a #1: dO rows to the experts (same plan as the dispatch)
+    for (int cc = 0; cc < nc; ++cc) {
+        int c0, c1;
+        chunk_range(cc, c0, c1);
+        CK(cudaStreamWaitEvent(sm, ev_k5[cc], 0));
+        OpScope op(c, "a2a_bwd_dispatch", 1, serial ? -1 : cc, sm);
+        std::vector<P2P> sends, recvs;
+        for (int p = 0; p < G; ++p)
+            for (int i = 0; i < E_l; ++i) {
+                const int e = p * E_l + i;
+                for (int ch = c0; ch < c1; ++ch)
+                    sends.push_back({p, dcomb + (size_t)(pl.send_off[e] + pl.S[e * (n + 1) + ch]) * rowb,
+                                     (size_t)pl.send[e * n + ch] * rowb});
+            }
+        for (int p = 0; p < G; ++p)
+            for (int el = 0; el < E_l; ++el)
+                for (int ch = c0; ch < c1; ++ch)
+                    recvs.push_back({p, dout + (size_t)(pl.grp_off[ch * E_l + el] + pl.src_off[(p * E_l + el) * n + ch]) * rowb,
+                                     (size_t)pl.recv[(p * E_l + el) * n + ch] * rowb});
+        std::string err;
+        if (c->comm->exchange(sends, recvs, sm, err)) return fail(c, LANCET_ERR_NCCL, err);
+        ev_b1[cc] = next_ev();
+        CK(cudaEventRecord(ev_b1[cc], sm));
+    }
+    // dX GEMMs per chunk, each followed immediately by the chunk's dW GEMMs
+    for (int cc = 0; cc < nc; ++cc) {
+        int c0, c1;
+        chunk_range(cc, c0, c1);
+        CK(cudaStreamWaitEvent(sc, ev_b1[cc], 0));
+        if (!ident) {
+            int mr = 0;
+            for (int ch = c0; ch < c1; ++ch)
+                for (int el = 0; el < E_l; ++el) mr = std::max(mr, round_up(pl.grp_rows[ch * E_l + el], kRowAlign));
+            st = expert_backward_dx(c, c->dout, d_grp_rows + c0 * E_l, d_grp_off + c0 * E_l,
+                                    (c1 - c0) * E_l, std::max(mr, kRowAlign), sc, serial ? -1 : cc, &L);
+            if (st) return st;
+        }
+        ev_dx[cc] = next_ev();
+        CK(cudaEventRecord(ev_dx[cc], sc));
+        if (!ident && !late_dw) {
+            for (int ch = c0; ch < c1; ++ch) {
+                st = expert_backward_dw(c, c->dout, d_grp_rows + ch * E_l, d_grp_off + ch * E_l, E_l,
+                                        dw1, dw2, ch > 0, sc, ch, &L);
+                if (st) return st;
+            }
+        }
+    }
+    // backward a2a #2: dX rows back to the token owners (same plan as the combine)
+    const char* dxe = ident ? (const char*)c->dout : (const char*)c->dXe;
+    char* dxcomb = (char*)c->dxcomb;
+    for (int cc = 0; cc < nc; ++cc) {
+        int c0, c1;
+        chunk_range(cc, c0, c1);
+        CK(cudaStreamWaitEvent(sm, ev_dx[cc], 0));
+        OpScope op(c, "a2a_bwd_combine", 1, serial ? -1 : cc, sm);
+        std::vector<P2P> sends, recvs;
+        for (int p = 0; p < G; ++p)
+            for (int el = 0; el < E_l; ++el)
+                for (int ch = c0; ch < c1; ++ch)
+                    sends.push_back({p, (void*)(dxe + (size_t)(pl.grp_off[ch * E_l + el] + pl.src_off[(p * E_l + el) * n + ch]) * rowb),
+                                     (size_t)pl.recv[(p * E_l + el) * n + ch] * rowb});
+        for (int p = 0; p < G; ++p)
+            for (int i = 0; i < E_l; ++i) {
+                const int e = p * E_l + i;
+                for (int ch = c0; ch < c1; ++ch)
+                    recvs.push_back({p, dxcomb + (size_t)(pl.send_off[e] + pl.S[e * (n + 1) + ch]) * rowb,
+                                     (size_t)pl.send[e * n + ch] * rowb});
+            }
+        std::string err;
+        if (c->comm->exchange(sends, recvs, sm, err)) return fail(c, LANCET_ERR_NCCL, err);
+        ev_b2[cc] = next_ev();
+        CK(cudaEventRecord(ev_b2[cc], sm));
+    }
+    if (!ident && late_dw) {    // ablation / serial baseline: all dW after the last a2a
+        for (int ch = 0; ch < n; ++ch) {
+            st = expert_backward_dw(c, c->dout, d_grp_rows + ch * E_l, d_grp_off + ch * E_l, E_l,
+                                    dw1, dw2, ch > 0, sc, ch, &L);
+            if (st) return st;
+        }
+    }
+    for (int cc = 0; cc < nc; ++cc) {
+        int t0, t1;
+        tok_range(cc, t0, t1);
+        CK(cudaStreamWaitEvent(sc, ev_b2[cc], 0));
+        OpScope op(c, "unpermute_gate_bwd", 0, serial ? -1 : cc, sc);
+        L += launch_unpermute_gate_bwd(da, dxcomb, c->g, c->logits, c->wg, renorm, dx, c->dlogit, t0, t1, c->bf16, sc);
+    }
+    CHECK_LAUNCH();
+    { OpScope op(c, "gate_dwg", 0, -1, sc);
+      L += launch_dwg(c->x, c->dlogit, T, d, E, c->dwg_partial, dwg, c->bf16, sc); }
+    CHECK_LAUNCH();
+    CK(cudaEventRecord(c->ev_join, sc));
+    CK(cudaStreamWaitEvent(s, c->ev_join, 0));
+    if (sm != sc) {
+        cudaEvent_t e2 = next_ev();
+        CK(cudaEventRecord(e2, sm));
+        CK(cudaStreamWaitEvent(s, e2, 0));
+    }
+    return LANCET_OK;
+}
+
+LANCET_API lancet_status lancet_get_counts(lancet_ctx* c, int32_t* send_counts,
+                                           int32_t* recv_counts, int32_t* capacity)
+{
+    lancet_status st = check_ready(c);
+    if (st) return st;
+    if (!c->have_fwd) return fail(c, LANCET_ERR_STATE, "no forward yet");
+    const int E = c->cfg.n_experts, n = c->n, G = c->world, E_l = c->E_l;
+    CK(cudaDeviceSynchronize());
+    std::vector<int> S(E * (n + 1));
+    CK(cudaMemcpy(S.data(), c->S, sizeof(int) * S.size(), cudaMemcpyDeviceToHost));
+    std::vector<int> send(E * n);
+    for (int e = 0; e < E; ++e)
+        for (int ch = 0; ch < n; ++ch) send[e * n + ch] = S[e * (n + 1) + ch + 1] - S[e * (n + 1) + ch];
+    if (send_counts) memcpy(send_counts, send.data(), sizeof(int) * E * n);
+    if (recv_counts) {
+        if (G == 1) memcpy(recv_counts, send.data(), sizeof(int) * E * n);
+        else memcpy(recv_counts, c->host_recv.data(), sizeof(int) * G * E_l * n);
+    }
+    if (capacity) *capacity = c->C;
+    return LANCET_OK;
+}
+
+LANCET_API lancet_status lancet_last_timeline(lancet_ctx* c, lancet_op_record* out, int32_t cap,
+                                              int32_t* n_out)
+{
+    lancet_status st = check_ready(c);
+    if (st) return st;
+    CK(cudaDeviceSynchronize());
+    int m = 0;
+    for (const OpEvent& op : c->ops) {
+        if (m >= cap) break;
+        lancet_op_record& r = out[m++];
+        memset(&r, 0, sizeof(r));
+        strncpy(r.name, op.name.c_str(), sizeof(r.name) - 1);
+        r.lane = op.lane;
+        r.chunk = op.chunk;
+        CK(cudaEventElapsedTime(&r.start_us, c->ev_tl_base, op.beg));
+        CK(cudaEventElapsedTime(&r.end_us, c->ev_tl_base, op.end));
+        r.start_us *= 1000.f;
+        r.end_us *= 1000.f;
+    }
+    if (n_out) *n_out = m;
+    return LANCET_OK;
+}
+
+LANCET_API lancet_status lancet_debug_copy(lancet_ctx* c, int32_t which, void* host_dst, size_t bytes)
+{
+    lancet_status st = check_ready(c);
+    if (st) return st;
+    if (!c->have_fwd) return fail(c, LANCET_ERR_STATE, "no forward yet");
+    if (which != 0) return fail(c, LANCET_ERR_ARG, "unknown buffer");
+    const size_t need = sizeof(float) * (size_t)c->T * c->cfg.n_experts;
+    if (!host_dst || bytes < need) return fail(c, LANCET_ERR_ARG, "destination too small");
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(host_dst, c->logits, need, cudaMemcpyDeviceToHost));
+    return LANCET_OK;
+}
+
+LANCET_API lancet_status lancet_workspace_bytes(const lancet_ctx* c, size_t* bytes)
+{
+    if (!c || !bytes) return fail(nullptr, LANCET_ERR_ARG, "null argument");
+    size_t b = 0;
+    for (const DevBuf& x : c->allocs) b += x.bytes;
+    *bytes = b;
+    return LANCET_OK;
+}
+
+LANCET_API lancet_status lancet_launch_counts(const lancet_ctx* c, int32_t* fwd, int32_t* bwd)
+{
+    if (!c) return fail(nullptr, LANCET_ERR_ARG, "ctx is NULL");
+    if (fwd) *fwd = c->launches_fwd;
+    if (bwd) *bwd = c->launches_bwd;
+    return LANCET_OK;
+}

@@ -1,0 +1,287 @@
+"""Thin Python binding of liblancet_moe.so (include/lancet_moe.h).
+
+Argument marshalling only: every step of the MoE layer runs in the library's CUDA kernels.
+torch provides device memory, streams and (for world > 1) the process group used to
+broadcast the NCCL unique id.  There is no fallback: if the shared library is missing or the
+device is not a B200 the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from dataclasses import dataclass
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liblancet_moe.so")
+
+STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_CUDA", 3: "ERR_NCCL", 4: "ERR_NOMEM", 5: "ERR_STATE",
+          6: "ERR_UNSUPPORTED"}
+DTYPES = {"bf16": 0, "fp32": 1}
+ACTS = {"gelu_tanh": 0, "relu": 1, "identity_expert": 2}
+FLAG_RENORMALIZE, FLAG_TIMELINE, FLAG_SERIAL, FLAG_SIMT_GEMM, FLAG_NO_DW_OVERLAP = 1, 2, 4, 8, 16
+
+EXPORTS = ["lancet_abi_version", "lancet_last_error", "lancet_nccl_unique_id", "lancet_create",
+           "lancet_local_group_create", "lancet_local_group_destroy", "lancet_create_local",
+           "lancet_destroy", "lancet_set_flags", "lancet_moe_forward", "lancet_moe_backward",
+           "lancet_get_counts", "lancet_last_timeline", "lancet_debug_copy",
+           "lancet_workspace_bytes", "lancet_launch_counts"]
+
+
+class LancetError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class _Config(ctypes.Structure):
+    _fields_ = [("d_model", ctypes.c_int32), ("d_ffn", ctypes.c_int32),
+                ("n_experts", ctypes.c_int32), ("max_tokens", ctypes.c_int32),
+                ("max_k", ctypes.c_int32), ("max_chunks", ctypes.c_int32),
+                ("dtype", ctypes.c_int32), ("act", ctypes.c_int32), ("flags", ctypes.c_uint32),
+                ("gemm_sms", ctypes.c_int32)]
+
+
+class _OpRecord(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char * 24), ("lane", ctypes.c_int32), ("chunk", ctypes.c_int32),
+                ("start_us", ctypes.c_float), ("end_us", ctypes.c_float)]
+
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load liblancet_moe.so (build it with `python -m paper_2404_19429_b200.build`)."""
+    global _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise RuntimeError(f"{path} is missing: run `python -m paper_2404_19429_b200.build` "
+                               "(there is no CPU fallback)")
+        lib = ctypes.CDLL(path)
+        P, I32, U32, F32 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint32, ctypes.c_float
+        sig = {
+            "lancet_abi_version": ([], I32),
+            "lancet_last_error": ([P], ctypes.c_char_p),
+            "lancet_nccl_unique_id": ([P], I32),
+            "lancet_create": ([ctypes.POINTER(P), I32, I32, I32, P, ctypes.POINTER(_Config)], I32),
+            "lancet_local_group_create": ([ctypes.POINTER(P), I32], I32),
+            "lancet_local_group_destroy": ([P], I32),
+            "lancet_create_local": ([ctypes.POINTER(P), P, I32, I32, ctypes.POINTER(_Config)], I32),
+            "lancet_destroy": ([P], I32),
+            "lancet_set_flags": ([P, U32], I32),
+            "lancet_moe_forward": ([P, P, P, P, P, I32, I32, F32, I32, P, P, P, P, P], I32),
+            "lancet_moe_backward": ([P, P, P, P, P, P, P], I32),
+            "lancet_get_counts": ([P, P, P, P], I32),
+            "lancet_last_timeline": ([P, ctypes.POINTER(_OpRecord), I32, ctypes.POINTER(I32)], I32),
+            "lancet_debug_copy": ([P, I32, P, ctypes.c_size_t], I32),
+            "lancet_workspace_bytes": ([P, ctypes.POINTER(ctypes.c_size_t)], I32),
+            "lancet_launch_counts": ([P, ctypes.POINTER(I32), ctypes.POINTER(I32)], I32),
+        }
+        for name, (args, res) in sig.items():
+            f = getattr(lib, name)
+            f.argtypes, f.restype = args, res
+        _lib = lib
+        return lib
+
+
+def _check(st: int, ctx_ptr=None):
+    if st != 0:
+        msg = load_library().lancet_last_error(ctx_ptr)
+        raise LancetError(st, msg.decode() if msg else "")
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream) -> ctypes.c_void_p:
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+@dataclass
+class LayerConfig:
+    d_model: int
+    d_ffn: int
+    n_experts: int
+    max_tokens: int
+    max_k: int = 2
+    max_chunks: int = 8
+    dtype: str = "bf16"
+    act: str = "gelu_tanh"
+    flags: int = 0
+    gemm_sms: int = 0
+
+    def _c(self) -> _Config:
+        return _Config(self.d_model, self.d_ffn, self.n_experts, self.max_tokens, self.max_k,
+                       self.max_chunks, DTYPES[self.dtype], ACTS[self.act], self.flags,
+                       self.gemm_sms)
+
+    @property
+    def torch_dtype(self):
+        return torch.bfloat16 if self.dtype == "bf16" else torch.float32
+
+
+class LocalGroup:
+    """G simulated ranks in one process on one device (lancet_local_group)."""
+
+    def __init__(self, world: int):
+        lib = load_library()
+        self.world = world
+        self._p = ctypes.c_void_p()
+        _check(lib.lancet_local_group_create(ctypes.byref(self._p), world))
+
+    def close(self):
+        if self._p:
+            load_library().lancet_local_group_destroy(self._p)
+            self._p = ctypes.c_void_p()
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(load_library().lancet_nccl_unique_id(buf))
+    return buf.raw
+
+
+class Context:
+    """One rank's lancet_ctx.
+
+    world == 1: no communication.  world > 1 with `pg` (a torch.distributed group): NCCL,
+    rank 0 creates the unique id and it is broadcast over `pg`.  `local_group`: a
+    LocalGroup of simulated ranks on one device (each rank must call from its own thread).
+    """
+
+    def __init__(self, cfg: LayerConfig, world: int = 1, rank: int = 0, device: int | None = None,
+                 pg=None, local_group: LocalGroup | None = None):
+        lib = load_library()
+        self.cfg = cfg
+        self.world, self.rank = world, rank
+        self.device = torch.cuda.current_device() if device is None else device
+        self._p = ctypes.c_void_p()
+        c = cfg._c()
+        if local_group is not None:
+            _check(lib.lancet_create_local(ctypes.byref(self._p), local_group._p, rank, self.device,
+                                           ctypes.byref(c)))
+        else:
+            nid = None
+            if world > 1:
+                import torch.distributed as dist
+                obj = [nccl_unique_id() if rank == 0 else None]
+                dist.broadcast_object_list(obj, src=0, group=pg)
+                nid = ctypes.create_string_buffer(obj[0], 128)
+            _check(lib.lancet_create(ctypes.byref(self._p), world, rank, self.device, nid,
+                                     ctypes.byref(c)))
+        self.E_l = cfg.n_experts // world
+        self._last = None
+
+    # -- lifecycle --------------------------------------------------------------------------
+    def close(self):
+        if self._p:
+            load_library().lancet_destroy(self._p)
+            self._p = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_flags(self, flags: int):
+        _check(load_library().lancet_set_flags(self._p, flags), self._p)
+        self.cfg.flags = flags
+
+    # -- the layer ----------------------------------------------------------------------------
+    def forward(self, x, wg, w1, w2, k: int, capacity_factor: float, n_chunks: int,
+                y=None, stream=None, routing: bool = True):
+        T = x.shape[0]
+        dev = x.device
+        y = torch.empty_like(x) if y is None else y
+        idx = slot = w = None
+        if routing:
+            idx = torch.empty((T, k), dtype=torch.int32, device=dev)
+            slot = torch.empty((T, k), dtype=torch.int32, device=dev)
+            w = torch.empty((T, k), dtype=torch.float32, device=dev)
+        st = load_library().lancet_moe_forward(
+            self._p, _ptr(x), _ptr(wg), _ptr(w1), _ptr(w2), T, k, float(capacity_factor),
+            n_chunks, _ptr(y), _ptr(idx), _ptr(slot), _ptr(w), _stream(stream))
+        _check(st, self._p)
+        self._last = (x, wg, w1, w2)       # the library keeps pointers until backward
+        return y, idx, slot, w
+
+    def backward(self, dy, dx=None, dwg=None, dw1=None, dw2=None, stream=None):
+        x, wg, w1, w2 = self._last
+        dx = torch.empty_like(dy) if dx is None else dx
+        dwg = torch.empty(wg.shape, dtype=torch.float32, device=dy.device) if dwg is None else dwg
+        if self.cfg.act != "identity_expert":
+            dw1 = torch.empty(w1.shape, dtype=torch.float32, device=dy.device) if dw1 is None else dw1
+            dw2 = torch.empty(w2.shape, dtype=torch.float32, device=dy.device) if dw2 is None else dw2
+        st = load_library().lancet_moe_backward(self._p, _ptr(dy), _ptr(dx), _ptr(dwg), _ptr(dw1),
+                                                _ptr(dw2), _stream(stream))
+        _check(st, self._p)
+        return dx, dwg, dw1, dw2
+
+    # -- introspection ------------------------------------------------------------------------
+    def counts(self, n_chunks: int):
+        import numpy as np
+        E, G = self.cfg.n_experts, self.world
+        send = np.zeros((E, n_chunks), dtype=np.int32)
+        recv = np.zeros((G, self.E_l, n_chunks), dtype=np.int32)
+        C = ctypes.c_int32()
+        _check(load_library().lancet_get_counts(self._p, send.ctypes.data_as(ctypes.c_void_p),
+                                                recv.ctypes.data_as(ctypes.c_void_p),
+                                                ctypes.byref(C)), self._p)
+        return send, recv, C.value
+
+    def logits(self, T: int):
+        import numpy as np
+        out = np.empty((T, self.cfg.n_experts), dtype=np.float32)
+        _check(load_library().lancet_debug_copy(self._p, 0, out.ctypes.data_as(ctypes.c_void_p),
+                                                out.nbytes), self._p)
+        return out
+
+    def timeline(self, cap: int = 1024):
+        recs = (_OpRecord * cap)()
+        n = ctypes.c_int32()
+        _check(load_library().lancet_last_timeline(self._p, recs, cap, ctypes.byref(n)), self._p)
+        return [dict(name=r.name.decode(), lane=r.lane, chunk=r.chunk, start_us=r.start_us,
+                     end_us=r.end_us) for r in recs[:n.value]]
+
+    def workspace_bytes(self) -> int:
+        b = ctypes.c_size_t()
+        _check(load_library().lancet_workspace_bytes(self._p, ctypes.byref(b)), self._p)
+        return b.value
+
+    def launch_counts(self):
+        f, b = ctypes.c_int32(), ctypes.c_int32()
+        _check(load_library().lancet_launch_counts(self._p, ctypes.byref(f), ctypes.byref(b)), self._p)
+        return f.value, b.value
+
+
+def exposed_comm_us(timeline) -> dict:
+    """SPEC-style decomposition of one timeline: comm time not covered by any
+    compute op ('exposed'), total comm busy time, compute busy time."""
+    def union(iv):
+        iv = sorted(iv)
+        out = []
+        for a, b in iv:
+            if out and a <= out[-1][1]:
+                out[-1][1] = max(out[-1][1], b)
+            else:
+                out.append([a, b])
+        return out
+    comm = union([(r["start_us"], r["end_us"]) for r in timeline if r["lane"] == 1])
+    comp = union([(r["start_us"], r["end_us"]) for r in timeline if r["lane"] == 0])
+    tot_comm = sum(b - a for a, b in comm)
+    overlap = 0.0
+    for a, b in comm:
+        for c, d in comp:
+            lo, hi = max(a, c), min(b, d)
+            if hi > lo:
+                overlap += hi - lo
+    return dict(exposed_us=tot_comm - overlap, comm_us=tot_comm,
+                compute_us=sum(b - a for a, b in comp))

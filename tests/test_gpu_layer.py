@@ -1,0 +1,126 @@
+"""GPU parity of the MoE layer step (single rank) against the oracle, through the C-ABI.
+
+Sizes span several tiles of every kernel (gate blocks of 128 tokens, 1024-token scan tiles,
+128-row GEMM tiles) with ragged tails; BASELINE.json configs[1] (the bench workload) is
+checked at full size on sampled outputs."""
+import numpy as np
+import pytest
+
+from gpu_harness import (TOL, assert_routing_exact, inputs, normwise, run_gpu, run_oracle)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2404_19429_b200 import build
+    build.build()
+
+
+@pytest.mark.parametrize("T,d,E,k,beta,cf,n", [
+    (64, 16, 4, 2, 0.5, 1.25, 2),          # BASELINE configs[0] per-rank shape, 64 tokens
+    (2500, 256, 8, 2, 0.5, 1.25, 3),       # 3 scan tiles, ragged
+    (3001, 96, 64, 4, 1.0, 1.0, 8),        # many experts, k=4, drops
+    (777, 64, 3, 1, 0.0, 0.5, 5),          # odd E, top-1, capacity binding hard
+    (1, 32, 8, 2, 0.5, 1.25, 1),           # single token
+    (513, 32, 1, 1, 0.0, 1.0, 2),          # one expert
+])
+def test_routing_bit_exact(T, d, E, k, beta, cf, n):
+    ins = inputs(T, d, 8, E, k, beta=beta, seed=T)
+    g = run_gpu(ins, E, k, cf, n, act="identity_expert", backward=False)
+    o = run_oracle(ins, k, cf, n, act="identity_expert", backward=False)
+    assert_routing_exact(g, o)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+@pytest.mark.parametrize("act", ["gelu_tanh", "relu"])
+def test_forward_backward_parity(dtype, act):
+    T, d, f, E, k, cf, n = 1000, 128, 256, 8, 2, 1.0, 3
+    ins = inputs(T, d, f, E, k, beta=0.5, dtype=dtype, seed=11)
+    g = run_gpu(ins, E, k, cf, n, dtype=dtype, act=act)
+    o = run_oracle(ins, k, cf, n, act=act)
+    assert_routing_exact(g, o)
+    assert np.any(o["rt"].slot < 0), "case must exercise drops"
+    for key in ("y", "dx", "dwg", "dw1", "dw2"):
+        err = normwise(g[key], o[key])
+        assert err <= TOL[dtype], (key, err)
+
+
+def test_identity_experts_reproduce_gate_weighted_inputs():
+    T, d, E, k = 1500, 64, 8, 2
+    ins = inputs(T, d, 8, E, k, beta=1.0, seed=5)
+    g = run_gpu(ins, E, k, 0.75, 4, act="identity_expert")
+    o = run_oracle(ins, k, 0.75, 4, act="identity_expert")
+    assert_routing_exact(g, o)
+    scale = np.where(g["slot"] >= 0, g["w"], 0.0).sum(1, dtype=np.float64)
+    want = scale[:, None] * ins["x"].astype(np.float64)
+    # one fp32 fma chain + one bf16 rounding: within 1 bf16 ulp (2^-8 relative)
+    assert np.all(np.abs(g["y"] - want) <= 2.0 ** -8 * np.abs(want) + 1e-30)
+    for key in ("y", "dx", "dwg"):
+        assert normwise(g[key], o[key]) <= TOL["bf16"], key
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+def test_chunk_count_does_not_change_results(dtype):
+    # capacity passing: chunked routing == unchunked routing, so every output is identical
+    T, d, f, E, k = 1200, 128, 256, 8, 2
+    ins = inputs(T, d, f, E, k, beta=0.5, dtype=dtype, seed=3)
+    ref = run_gpu(ins, E, k, 1.0, 1, dtype=dtype)
+    for n in (2, 4, 8):
+        g = run_gpu(ins, E, k, 1.0, n, dtype=dtype)
+        for key in ("y", "dx", "idx", "slot", "dw1", "dw2", "dwg"):
+            assert np.array_equal(g[key], ref[key]), (n, key)
+        assert np.array_equal(g["send"].sum(1), ref["send"][:, 0])
+
+
+def test_renormalized_weights():
+    from paper_2404_19429_b200 import FLAG_RENORMALIZE
+    T, d, f, E, k = 700, 64, 128, 8, 2
+    ins = inputs(T, d, f, E, k, beta=0.5, seed=9)
+    g = run_gpu(ins, E, k, 1.0, 2, flags=FLAG_RENORMALIZE)
+    o = run_oracle(ins, k, 1.0, 2, renorm=True)
+    assert np.allclose(g["w"].sum(1), 1.0, atol=1e-6)
+    for key in ("y", "dx", "dwg", "dw1", "dw2"):
+        assert normwise(g[key], o[key]) <= TOL["bf16"], key
+
+
+def test_api_errors_on_device():
+    import torch
+    from paper_2404_19429_b200 import lancet
+    cfg = lancet.LayerConfig(d_model=64, d_ffn=128, n_experts=4, max_tokens=32, max_k=2)
+    ctx = lancet.Context(cfg)
+    dy = torch.zeros(32, 64, dtype=torch.bfloat16, device="cuda")
+    ctx._last = (dy, dy, dy, dy)
+    with pytest.raises(lancet.LancetError) as e:
+        ctx.backward(dy)
+    assert e.value.status == 5                                   # ERR_STATE
+    ins = inputs(32, 64, 128, 4, 2)
+    x = torch.from_numpy(ins["x"]).cuda().bfloat16()
+    wg = torch.from_numpy(ins["wg"]).cuda()
+    w1 = torch.from_numpy(ins["w1"]).cuda().bfloat16()
+    w2 = torch.from_numpy(ins["w2"]).cuda().bfloat16()
+    for kw in (dict(k=3, cf=1.0, n=1), dict(k=2, cf=0.0, n=1), dict(k=2, cf=1.0, n=9)):
+        with pytest.raises(lancet.LancetError) as e:
+            ctx.forward(x, wg, w1, w2, kw["k"], kw["cf"], kw["n"])
+        assert e.value.status == 1                               # ERR_ARG
+    ctx.close()
+
+
+def test_full_size_gpt_moe_layer_sampled():
+    # BASELINE.json configs[1] per GPU: T=16384, d=1024, f=4096, E=8, top-2, bf16; n=4 chunks
+    T, d, f, E, k, cf, n = 16384, 1024, 4096, 8, 2, 1.25, 4
+    ins = inputs(T, d, f, E, k, beta=0.25, seed=2024)
+    g = run_gpu(ins, E, k, cf, n)
+    rng = np.random.default_rng(0)
+    sub = np.sort(np.concatenate([rng.choice(T, 48, replace=False), [0, T - 1]]))
+    o = run_oracle(ins, k, cf, n, token_subset=[sub])
+    assert_routing_exact(g, o)
+    assert normwise(g["y"][sub], o["y"][sub]) <= TOL["bf16"]
+    assert normwise(g["dx"][sub], o["dx"][sub]) <= TOL["bf16"]
+    # properties at full size: dropped-everywhere tokens have y = 0; weight grads finite
+    dropped = np.all(g["slot"] < 0, axis=1)
+    assert np.all(g["y"][dropped] == 0)
+    assert np.isfinite(g["dw1"]).all() and np.isfinite(g["dw2"]).all()
