@@ -1,6 +1,439 @@
-// gemm_tc.cu -- placeholder until the tcgen05 grouped GEMM lands.
+// gemm_tc.cu -- the expert GEMMs on the 5th-generation tensor cores (tcgen05 + TMEM + TMA).
+//
+// "Each expert processes the C received tokens": per expert an FFN,
+// whose token count per (expert, chunk) is irregular and known only on the device after the
+// gate (fig:proposed_partition).  One persistent, warp-specialised kernel serves all
+// six expert GEMMs of a fwd+bwd step:
+//   M-grouped (rows = tokens of a group, 128-row aligned):      fc1 (act epilogue: H and
+//     act'(A)), fc2, dfc2 (epilogue multiplies act'(A)), dfc1
+//   K-grouped (reduction over a group's token rows, fp32 out):  dW2 = dO^T H, dW1 = dA^T X
+// Operands are TMA-loaded with 128-byte swizzle into a 4-stage shared-memory ring; a single
+// elected thread issues tcgen05.mma (kind::f16, bf16 in, fp32 accumulate) into one of two
+// TMEM accumulators (BN fp32 columns each), so the epilogue warpgroup drains tile i while the
+// tensor core computes tile i+1.  Operands may be K-major or MN-major (the weights of the dX
+// GEMMs and both operands of the dW GEMMs are read transposed in place -- no transposition
+// pass over HBM).
+//
+// Roles (256 threads):  warp 0 TMA producer | warp 1 MMA issuer | warp 2 TMEM allocator |
+//                       warp 3 idle | warps 4-7 epilogue (TMEM lanes 32*(w%4) ...).
+#include <cuda.h>
+
+#include <mutex>
+
+#include "common.cuh"
 #include "kernels.h"
+
 namespace lancet {
-bool gemm_tc_supported(const GemmArgs&) { return false; }
-int launch_gemm_tc(const GemmArgs&, int, cudaStream_t) { return -1; }
+namespace tc {
+
+constexpr int BM = 128, BK = 64, STAGES = 4, UMMA_K = 16;
+constexpr int kThreads = 256;
+constexpr int kMaxGroups = 512;
+constexpr uint32_t A_STAGE = BM * BK * 2;                 // 16 KiB
+
+struct Params {
+    int mode, n_groups, gpw, epi, act, accumulate;
+    int M, N, K;
+    const int* grp_rows;
+    const int* grp_off;
+    void* C;
+    long ldc, c_group_stride;
+    void* C2;
+    const void* aux;
+};
+
+// ---------------------------------------------------------------- PTX wrappers ----------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+        : "memory");
+}
+// 32 lanes x 32 columns of 32-bit: thread t of the warp gets row (lane base + t), 32 columns
+__device__ __forceinline__ void tmem_ld32(uint32_t addr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(addr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Shared-memory matrix descriptor (sm_100 UMMA): start>>4 [0,14), LBO>>4 [16,30),
+// SBO>>4 [32,46), version 1 at [46,48), base offset 0, layout SWIZZLE_128B (=2) at [61,64).
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (2ull << 61);
+}
+// K-major SW128 tile: rows of 128 B (64 bf16 of K), 8-row atoms 1024 B apart (SBO); the k-th
+// 16-wide K step starts 32 B further.  MN-major SW128 tile: built from TMA boxes of
+// [64 K rows][64 MN] (8 KiB, LBO apart); 8-row K groups 1024 B apart (SBO); a 16-deep K step
+// spans two groups = 2048 B.
+template <bool MN>
+__device__ __forceinline__ uint64_t operand_desc(uint32_t base, int k) {
+    return MN ? make_desc(base + k * 2048, 8192, 1024) : make_desc(base + k * 32, 16, 1024);
+}
+
+template <int BN, bool A_MN, bool B_MN>
+__device__ __forceinline__ constexpr uint32_t instr_desc() {
+    // c_format F32 [4,6) | a_format BF16 [7,10) | b_format BF16 [10,13) | a_major [15] |
+    // b_major [16] | N>>3 [17,23) | M>>4 [24,29)
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((A_MN ? 1u : 0u) << 15) | ((B_MN ? 1u : 0u) << 16) |
+           ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
+__device__ __forceinline__ void decode_tile(int tile, const int* tstart, int ng, int ntn, int& g, int& mt, int& nt) {
+    int lo = 0, hi = ng - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (tstart[mid] <= tile) lo = mid;
+        else hi = mid - 1;
+    }
+    g = lo;
+    const int local = tile - tstart[g];
+    mt = local / ntn;
+    nt = local % ntn;
+}
+
+template <int BN>
+constexpr size_t smem_bytes() {
+    return 1024 + STAGES * (A_STAGE + (size_t)BN * BK * 2) + 256 + sizeof(int) * (kMaxGroups + 1);
+}
+
+template <int BN, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(kThreads, 1)
+tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Params p)
+{
+    constexpr uint32_t B_STAGE = BN * BK * 2;
+    constexpr uint32_t TMEM_COLS = 2 * BN;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + STAGES * A_STAGE;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    int* tstart = reinterpret_cast<int*>(smem + STAGES * (A_STAGE + B_STAGE) + 256);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ntn = p.N / BN;
+
+    if (threadIdx.x == 0) {
+        int acc = 0;
+        for (int g = 0; g < p.n_groups; ++g) {
+            tstart[g] = acc;
+            const int mt = p.mode == GEMM_M_GROUPED ? ceil_div(p.grp_rows[g], BM) : p.M / BM;
+            acc += mt * ntn;
+        }
+        tstart[p.n_groups] = acc;
+    }
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tmA);
+        tma_prefetch(&tmB);
+    }
+    if (warp == 1 && lane == 0) {
+        for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+        for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const int total = tstart[p.n_groups];
+
+    if (warp == 0) {
+        // ===================== TMA producer =====================
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+                int g, mt, nt;
+                decode_tile(tile, tstart, p.n_groups, ntn, g, mt, nt);
+                const int n0 = nt * BN;
+                int num_kb, arow, brow;
+                if (p.mode == GEMM_M_GROUPED) {
+                    num_kb = p.K / BK;
+                    arow = p.grp_off[g] + mt * BM;
+                    brow = (g / p.gpw) * (B_MN ? p.K : p.N);
+                } else {
+                    num_kb = round_up(p.grp_rows[g], kRowAlign) / BK;
+                    arow = p.grp_off[g];
+                    brow = p.grp_off[g];
+                }
+                const int m0 = mt * BM;
+                for (int kb = 0; kb < num_kb; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_expect_tx(&full[stage], A_STAGE + B_STAGE);
+                    uint8_t* a_dst = sA + stage * A_STAGE;
+                    uint8_t* b_dst = sB + stage * B_STAGE;
+                    if (A_MN) {
+#pragma unroll
+                        for (int i = 0; i < BM / 64; ++i)
+                            tma_load_2d(&tmA, &full[stage], a_dst + i * 8192, m0 + 64 * i, arow + kb * BK);
+                    } else {
+                        tma_load_2d(&tmA, &full[stage], a_dst, kb * BK, arow);
+                    }
+                    if (B_MN) {
+#pragma unroll
+                        for (int i = 0; i < BN / 64; ++i)
+                            tma_load_2d(&tmB, &full[stage], b_dst + i * 8192, n0 + 64 * i, brow + kb * BK);
+                    } else {
+                        tma_load_2d(&tmB, &full[stage], b_dst, kb * BK, brow + n0);
+                    }
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer (one thread) =====================
+        if (lane == 0) {
+            constexpr uint32_t idesc = instr_desc<BN, A_MN, B_MN>();
+            int stage = 0;
+            uint32_t phase = 0;
+            int it = 0;
+            for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
+                int g, mt, nt;
+                decode_tile(tile, tstart, p.n_groups, ntn, g, mt, nt);
+                const int num_kb = p.mode == GEMM_M_GROUPED ? p.K / BK : round_up(p.grp_rows[g], kRowAlign) / BK;
+                const int acc = it & 1;
+                const uint32_t acc_phase = (it >> 1) & 1;
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t tmem_d = tmem_base + acc * BN;
+                for (int kb = 0; kb < num_kb; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t a_base = smem_u32(sA + stage * A_STAGE);
+                    const uint32_t b_base = smem_u32(sB + stage * B_STAGE);
+#pragma unroll
+                    for (int k = 0; k < BK / UMMA_K; ++k)
+                        tc_mma(tmem_d, operand_desc<A_MN>(a_base, k), operand_desc<B_MN>(b_base, k), idesc,
+                               (kb | k) != 0 ? 1u : 0u);
+                    tc_commit(&empty[stage]);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+                tc_commit(&tfull[acc]);
+            }
+        }
+    } else if (warp >= 4) {
+        // ===================== epilogue warpgroup =====================
+        const int q = warp & 3;
+        int it = 0;
+        for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
+            int g, mt, nt;
+            decode_tile(tile, tstart, p.n_groups, ntn, g, mt, nt);
+            const int acc = it & 1;
+            const uint32_t acc_phase = (it >> 1) & 1;
+            const bool has_k = p.mode == GEMM_M_GROUPED ? (p.K > 0) : (p.grp_rows[g] > 0);
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const int lrow = q * 32 + lane;
+            const int n0 = nt * BN;
+            long orow;
+            if (p.mode == GEMM_M_GROUPED) orow = (long)p.grp_off[g] + mt * BM + lrow;
+            else orow = (long)mt * BM + lrow;
+#pragma unroll 1
+            for (int cc = 0; cc < BN / 32; ++cc) {
+                uint32_t v[32];
+                tmem_ld32(tmem_base + acc * BN + cc * 32 + ((uint32_t)(q * 32) << 16), v);
+                float f[32];
+#pragma unroll
+                for (int i = 0; i < 32; ++i) f[i] = has_k ? __uint_as_float(v[i]) : 0.f;
+                const long col = n0 + cc * 32;
+                if (p.epi == EPI_F32) {
+                    float* C = reinterpret_cast<float*>(p.C) + (long)g * p.c_group_stride + orow * p.ldc + col;
+                    if (p.accumulate) {
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            float o[4];
+                            unpack16<float>(ld_v4(C + 4 * i), o);
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) f[4 * i + j] += o[j];
+                        }
+                    }
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) st_v4(C + 4 * i, pack16<float>(f + 4 * i));
+                } else {
+                    bf16* C = reinterpret_cast<bf16*>(p.C) + orow * p.ldc + col;
+                    if (p.epi == EPI_ACT) {
+                        float h[32], gr[32];
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) act_fwd_grad(p.act, f[i], h[i], gr[i]);
+                        bf16* C2 = reinterpret_cast<bf16*>(p.C2) + orow * p.ldc + col;
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            st_v4(C + 8 * i, pack16<bf16>(h + 8 * i));
+                            st_v4(C2 + 8 * i, pack16<bf16>(gr + 8 * i));
+                        }
+                    } else {
+                        if (p.epi == EPI_DACT) {
+                            const bf16* X = reinterpret_cast<const bf16*>(p.aux) + orow * p.ldc + col;
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) {
+                                float a8[8];
+                                unpack16<bf16>(ld_v4(X + 8 * i), a8);
+#pragma unroll
+                                for (int j = 0; j < 8; ++j) f[8 * i + j] *= a8[j];
+                            }
+                        }
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) st_v4(C + 8 * i, pack16<bf16>(f + 8 * i));
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+    }
+}
+
+// ---------------------------------------------------------------- host side -------------
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                             const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                             CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeFn get_encode()
+{
+    static EncodeFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(p);
+    });
+    return fn;
+}
+
+// 2D bf16 map: inner dimension `inner` (contiguous), `outer` rows of `stride_elems`.
+static bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t stride_elems,
+                     uint32_t box_inner, uint32_t box_outer)
+{
+    EncodeFn enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {stride_elems * 2};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+template <int BN, bool A_MN, bool B_MN>
+static int launch_cfg(const GemmArgs& a, int num_sms, cudaStream_t s)
+{
+    CUtensorMap ta, tb;
+    bool ok;
+    if (A_MN) ok = make_map(&ta, a.A, a.M, a.a_rows, a.lda, 64, 64);
+    else ok = make_map(&ta, a.A, a.K, a.a_rows, a.lda, 64, BM);
+    if (B_MN) ok = ok && make_map(&tb, a.B, a.N, a.b_rows, a.ldb, 64, 64);
+    else ok = ok && make_map(&tb, a.B, a.K, a.b_rows, a.ldb, 64, BN);
+    if (!ok) return -1;
+    Params p{a.mode, a.n_groups, a.gpw, a.epi, a.act, a.accumulate, a.M, a.N, a.K, a.grp_rows, a.grp_off,
+             a.C, a.ldc, a.c_group_stride, a.C2, a.aux};
+    constexpr size_t smem = smem_bytes<BN>();
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(tc_gemm_kernel<BN, A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    // persistent grid: at most one CTA per SM, never more CTAs than the upper bound of tiles
+    long max_tiles;
+    if (a.mode == GEMM_M_GROUPED) max_tiles = (long)ceil_div(a.max_rows, BM) * a.n_groups * (a.N / BN);
+    else max_tiles = (long)(a.M / BM) * (a.N / BN) * a.n_groups;
+    const int grid = (int)std::max<long>(1, std::min<long>(num_sms, max_tiles));
+    tc_gemm_kernel<BN, A_MN, B_MN><<<grid, kThreads, smem, s>>>(ta, tb, p);
+    return 1;
+}
+
+}  // namespace tc
+
+bool gemm_tc_supported(const GemmArgs& a)
+{
+    if (a.n_groups > tc::kMaxGroups || a.n_groups <= 0) return false;
+    if (a.N % 128) return false;
+    if (a.mode == GEMM_M_GROUPED) {
+        if (a.a_mn) return false;
+        if (a.K % tc::BK) return false;
+    } else {
+        if (!a.a_mn || !a.b_mn) return false;
+        if (a.M % tc::BM) return false;
+    }
+    if (a.epi == EPI_F32 && a.mode != GEMM_K_GROUPED) return false;
+    return a.a_rows > 0 && a.b_rows > 0;
+}
+
+int launch_gemm_tc(const GemmArgs& a, int num_sms, cudaStream_t s)
+{
+    if (!gemm_tc_supported(a)) return -1;
+    const bool bn256 = a.N % 256 == 0;
+    if (!a.a_mn && !a.b_mn) return bn256 ? tc::launch_cfg<256, false, false>(a, num_sms, s)
+                                         : tc::launch_cfg<128, false, false>(a, num_sms, s);
+    if (!a.a_mn && a.b_mn) return bn256 ? tc::launch_cfg<256, false, true>(a, num_sms, s)
+                                        : tc::launch_cfg<128, false, true>(a, num_sms, s);
+    return bn256 ? tc::launch_cfg<256, true, true>(a, num_sms, s) : tc::launch_cfg<128, true, true>(a, num_sms, s);
+}
+
 }  // namespace lancet

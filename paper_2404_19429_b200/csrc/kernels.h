@@ -67,6 +67,7 @@ struct GemmArgs {
     const int* grp_off;   // [n_groups] first row (128-aligned) in A / C (M) or A / B (K)
     int epi, act, accumulate;
     bool a_mn, b_mn;
+    long a_rows, b_rows;  // outer extents of A and B viewed as 2D row-major tensors (TMA maps)
 };
 int launch_gemm_simt(const GemmArgs& a, bool is_bf16, cudaStream_t s);
 

@@ -161,8 +161,9 @@ lancet_status expert_forward(lancet_ctx* c, const int* grp_rows, const int* grp_
     a.grp_rows = grp_rows; a.grp_off = grp_off; a.max_rows = max_rows; a.act = c->cfg.act;
     {   // fc1: H = act(X W1^T), G' = act'(X W1^T)
         OpScope op(c, "expert_fc1", 0, chunk, s);
-        a.A = c->world > 1 ? c->xe : c->xs; a.lda = d;
+        a.A = c->world > 1 ? c->xe : c->xs; a.lda = d; a.a_rows = c->rows_exp;
         a.B = c->w1; a.ldb = d; a.b_group_stride = (long)f * d; a.b_mn = false; a.a_mn = false;
+        a.b_rows = (long)c->E_l * f;
         a.C = c->H; a.C2 = c->Gp; a.ldc = f; a.N = f; a.K = d; a.epi = EPI_ACT;
         lancet_status st = run_gemm(c, a, s, launches);
         if (st) return st;
@@ -170,7 +171,7 @@ lancet_status expert_forward(lancet_ctx* c, const int* grp_rows, const int* grp_
     {   // fc2: O = H W2^T
         OpScope op(c, "expert_fc2", 0, chunk, s);
         a.A = c->H; a.lda = f;
-        a.B = c->w2; a.ldb = f; a.b_group_stride = (long)d * f;
+        a.B = c->w2; a.ldb = f; a.b_group_stride = (long)d * f; a.b_rows = (long)c->E_l * d;
         a.C = c->out; a.C2 = nullptr; a.ldc = d; a.N = d; a.K = f; a.epi = EPI_STORE;
         return run_gemm(c, a, s, launches);
     }
@@ -187,8 +188,9 @@ lancet_status expert_backward_dx(lancet_ctx* c, const void* dout, const int* grp
     a.grp_rows = grp_rows; a.grp_off = grp_off; a.max_rows = max_rows; a.act = c->cfg.act;
     {   // dA = (dO W2) * act'(A):  B(n=f, k=d) = W2[e][k][n]  (MN-major)
         OpScope op(c, "expert_dfc2", 0, chunk, s);
-        a.A = dout; a.lda = d; a.a_mn = false;
+        a.A = dout; a.lda = d; a.a_mn = false; a.a_rows = c->rows_exp;
         a.B = c->w2; a.ldb = f; a.b_group_stride = (long)d * f; a.b_mn = true;
+        a.b_rows = (long)c->E_l * d;
         a.C = c->dA; a.ldc = f; a.aux = c->Gp; a.N = f; a.K = d; a.epi = EPI_DACT;
         lancet_status st = run_gemm(c, a, s, launches);
         if (st) return st;
@@ -197,6 +199,7 @@ lancet_status expert_backward_dx(lancet_ctx* c, const void* dout, const int* grp
         OpScope op(c, "expert_dfc1", 0, chunk, s);
         a.A = c->dA; a.lda = f;
         a.B = c->w1; a.ldb = d; a.b_group_stride = (long)f * d; a.b_mn = true;
+        a.b_rows = (long)c->E_l * f;
         a.C = c->dXe; a.ldc = d; a.aux = nullptr; a.N = d; a.K = f; a.epi = EPI_STORE;
         return run_gemm(c, a, s, launches);
     }
@@ -212,6 +215,7 @@ lancet_status expert_backward_dw(lancet_ctx* c, const void* dout, const int* grp
     a.mode = GEMM_K_GROUPED; a.n_groups = ng; a.gpw = 1;
     a.grp_rows = grp_rows; a.grp_off = grp_off; a.accumulate = accumulate;
     a.a_mn = true; a.b_mn = true; a.epi = EPI_F32; a.b_group_stride = 0;
+    a.a_rows = c->rows_exp; a.b_rows = c->rows_exp;
     {
         OpScope op(c, "expert_dw2", 0, chunk, s);
         a.A = dout; a.lda = d; a.B = c->H; a.ldb = f;

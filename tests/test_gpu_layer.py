@@ -124,3 +124,24 @@ def test_full_size_gpt_moe_layer_sampled():
     dropped = np.all(g["slot"] < 0, axis=1)
     assert np.all(g["y"][dropped] == 0)
     assert np.isfinite(g["dw1"]).all() and np.isfinite(g["dw2"]).all()
+
+
+@pytest.mark.parametrize("T,d,f,E,k,n", [
+    (1000, 128, 256, 8, 2, 3),        # BN=128 (fc2/dfc1 N=d=128) and BN=256 (fc1 N=f=256)
+    (2300, 256, 512, 4, 2, 2),        # K = 256 / 512: several k-blocks per tile, ring wraps
+    (300, 128, 384, 2, 1, 1),         # N = 384: BN=128 x 3 n-tiles; tiny groups
+])
+def test_tcgen05_gemm_matches_simt_gemm(T, d, f, E, k, n):
+    # the tcgen05/TMA path and the SIMT path compute the same fp32-accumulated GEMMs;
+    # they may differ only by accumulation order -> far below the bf16 tolerance
+    from paper_2404_19429_b200 import FLAG_SIMT_GEMM
+    ins = inputs(T, d, f, E, k, beta=0.5, seed=T + d)
+    tc = run_gpu(ins, E, k, 1.0, n)
+    simt = run_gpu(ins, E, k, 1.0, n, flags=FLAG_SIMT_GEMM)
+    for key in ("idx", "slot"):
+        assert np.array_equal(tc[key], simt[key])
+    for key in ("y", "dx", "dwg", "dw1", "dw2"):
+        assert normwise(tc[key], simt[key]) <= 3e-3, (key, normwise(tc[key], simt[key]))
+    o = run_oracle(ins, k, 1.0, n)
+    for key in ("y", "dx", "dwg", "dw1", "dw2"):
+        assert normwise(tc[key], o[key]) <= TOL["bf16"], key
