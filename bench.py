@@ -1,0 +1,422 @@
+#!/usr/bin/env python
+"""bench.py -- MoE layer fwd+bwd tokens/s on B200 (BASELINE.json metric), plus exposed
+all-to-all ms/iter, roofline of the dominant kernel, end-to-end (host buffers) throughput and
+the CPU oracle baseline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl lancet|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...          (N > 1, one rank per GPU)
+
+Workload (BASELINE.json configs[1], per GPU): GPT-MoE layer d_model=1024, ffn=4096, E=8
+experts in total (E/N per GPU), top-2, capacity factor 1.25, 16384 tokens per GPU, bf16,
+n_chunks=4, synthetic inputs (synthetic/, routing skew beta=0.25).  One step = forward +
+backward of the layer through the C-ABI (lancet_moe_forward / lancet_moe_backward).
+
+--impl reference times the CPU oracle (oracle/, the reference arm of this tier) on bounded
+samples of the same workload, on rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MoE layer fwd+bwd tokens/s at 1/2/4/8 B200; exposed all-to-all ms/iter"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["lancet", "reference"], default="lancet")
+    ap.add_argument("--tokens", type=int, default=16384, help="tokens per GPU")
+    ap.add_argument("--d", type=int, default=1024)
+    ap.add_argument("--f", type=int, default=4096)
+    ap.add_argument("--experts", type=int, default=8)
+    ap.add_argument("--k", type=int, default=2)
+    ap.add_argument("--cf", type=float, default=1.25)
+    ap.add_argument("--chunks", type=int, default=4)
+    ap.add_argument("--beta", type=float, default=0.25)
+    ap.add_argument("--seed", type=int, default=2024)
+    ap.add_argument("--flags", type=int, default=0, help="extra LANCET_FLAG_* bits")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    a = ap.parse_args()
+    a.warmup = max(a.warmup, 3)
+    return a
+
+
+def workload(a, world):
+    return {
+        "workload": f"GPT-MoE layer fwd+bwd: d_model={a.d} ffn={a.f} experts={a.experts} "
+                    f"({a.experts // world}/GPU) top-{a.k} cf={a.cf} {a.tokens} tokens/GPU "
+                    f"n_chunks={a.chunks} bf16",
+        "tokens_per_gpu": a.tokens, "d_model": a.d, "d_ffn": a.f, "experts": a.experts,
+        "top_k": a.k, "capacity_factor": a.cf, "n_chunks": a.chunks, "routing_skew_beta": a.beta,
+        "global_batch_tokens": a.tokens * world,
+        "l2": "inputs larger than L2: per-step working set >= 1.4 GiB vs 126 MB L2 (no flush)",
+    }
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        j = json.load(open(p))
+        return dict(hbm=j["hbm_gbs"], bf16=j["bf16_tflops"], bf16_sus=j.get("bf16_tflops_sustained", j["bf16_tflops"]),
+                    src="measured (MEASURED_PEAKS.json)")
+    return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="fallback (B200_PROFILING.md)")
+
+
+# ------------------------------------------------------------------------ clocks -----------
+class ClockSampler:
+    NAMES = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+             0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+             0x2: "applications_clocks_setting"}
+
+    def __init__(self, device: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # noqa: BLE001
+            self._nv = None
+            self.err = str(e)
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                mhz = self._nv.nvmlDeviceGetClockInfo(self._h, self._nv.NVML_CLOCK_SM)
+                r = self._nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                util = self._nv.nvmlDeviceGetUtilizationRates(self._h).gpu
+                self.samples.append((mhz, r, util))
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.02)
+
+    def start(self):
+        if self._nv:
+            self._t.start()
+        return self
+
+    def stop(self):
+        self._stop.set()
+        if self._nv:
+            self._t.join(timeout=1)
+        busy = [s for s in self.samples if s[2] > 0] or self.samples
+        reasons = set()
+        for _, r, _ in busy:
+            for bit, name in self.NAMES.items():
+                if r & bit:
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median([s[0] for s in busy]) if busy else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(reasons), "samples": len(busy)}
+
+
+# ------------------------------------------------------------------------ oracle -----------
+def oracle_step(a, T, seed):
+    """One fwd+bwd of the oracle on T tokens of the workload (one rank, all E experts local)."""
+    import synthetic as S
+    from oracle import moe
+    sh = S.LayerShape(T=T, d=a.d, f=a.f, E=a.experts, G=1, k=a.k, cf=a.cf, n_chunks=1)
+    ins = S.gen_rank_inputs(seed, 0, sh, beta=a.beta)
+    t0 = time.perf_counter()
+    fwd = moe.forward([ins["x"]], ins["wg"], [ins["w1"]], [ins["w2"]], a.k, a.cf, a.chunks)
+    moe.backward(fwd, [ins["x"]], ins["wg"], [ins["w1"]], [ins["w2"]], [ins["dy"]])
+    return time.perf_counter() - t0
+
+
+def oracle_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        n = max((i.get("num_threads", 1) for i in threadpool_info()), default=1)
+        return int(n)
+    except Exception:  # noqa: BLE001
+        return os.cpu_count()
+
+
+def calibrate_sample(a, budget_s):
+    """Largest power-of-two token sample whose oracle fwd+bwd fits in ~budget_s seconds."""
+    T = 256
+    dt = oracle_step(a, T, a.seed)
+    per_tok = dt / T
+    Ts = 256
+    while Ts * 2 <= a.tokens and per_tok * Ts * 2 <= budget_s:
+        Ts *= 2
+    return Ts, per_tok
+
+
+def cpu_baseline(a, budget_s=15.0):
+    Ts, _ = calibrate_sample(a, budget_s)
+    dt = oracle_step(a, Ts, a.seed + 1)
+    return {"value": Ts / dt, "unit": "tokens/s", "cores": oracle_threads(), "kind": "oracle",
+            "sample": f"oracle fwd+bwd of {Ts} of the {a.tokens} tokens/GPU of the workload "
+                      f"(one rank, all {a.experts} experts local), {dt:.1f} s, fp64 numpy "
+                      f"matmuls + fp32 C gate, host cpu_count={os.cpu_count()}"}
+
+
+def run_reference(a, world, rank):
+    if rank != 0:
+        return
+    Ts, per_tok = calibrate_sample(a, 150.0 / max(1, a.steps + a.warmup))
+    for i in range(a.warmup):
+        oracle_step(a, Ts, a.seed + 10 + i)
+    times = [oracle_step(a, Ts, a.seed + 100 + i) for i in range(a.steps)]
+    ms = 1000.0 * statistics.mean(times)
+    val = Ts / (ms / 1000.0)
+    sample = (f"each step: oracle fwd+bwd of {Ts} tokens of the workload (one rank, all "
+              f"{a.experts} experts local); fp64 numpy matmuls + fp32 C gate")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "tokens/s", "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload(a, world),
+        "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": oracle_threads(), "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# ------------------------------------------------------------------------ GPU --------------
+GEMM_OPS = ("expert_fc1", "expert_fc2", "expert_dfc2", "expert_dfc1", "expert_dw2", "expert_dw1")
+
+
+def op_stats(tl, steps):
+    tot = {}
+    for r in tl:
+        tot.setdefault(r["name"], [0.0, 0])
+        tot[r["name"]][0] += r["end_us"] - r["start_us"]
+        tot[r["name"]][1] += 1
+    return {k: {"us_per_step": v[0] / steps, "launch_groups_per_step": v[1] / steps} for k, v in tot.items()}
+
+
+def exposure_per_step(tl, steps):
+    from paper_2404_19429_b200.lancet import exposed_comm_us
+    d = exposed_comm_us(tl)
+    return d["exposed_us"] / steps / 1000.0, d["comm_us"] / steps / 1000.0
+
+
+def run_lancet(a, world, rank, local_rank):
+    import torch
+    import torch.distributed as dist
+    import synthetic as S
+    from paper_2404_19429_b200 import build, lancet
+    if rank == 0:
+        build.build()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    E_l = a.experts // world
+    sh = S.LayerShape(T=a.tokens, d=a.d, f=a.f, E=a.experts, G=world, k=a.k, cf=a.cf, n_chunks=a.chunks)
+    ins = S.gen_rank_inputs(a.seed, rank, sh, beta=a.beta)
+    bf = torch.bfloat16
+    x = torch.from_numpy(ins["x"]).to(dev, bf)
+    wg = torch.from_numpy(ins["wg"]).to(dev)
+    w1 = torch.from_numpy(ins["w1"]).to(dev, bf)
+    w2 = torch.from_numpy(ins["w2"]).to(dev, bf)
+    dy = torch.from_numpy(ins["dy"]).to(dev, bf)
+    flags = lancet.FLAG_TIMELINE | a.flags
+    cfg = lancet.LayerConfig(d_model=a.d, d_ffn=a.f, n_experts=a.experts, max_tokens=a.tokens,
+                             max_k=a.k, max_chunks=max(8, a.chunks), dtype="bf16", flags=flags)
+    ctx = lancet.Context(cfg, world=world, rank=rank, device=local_rank,
+                         pg=dist.group.WORLD if world > 1 else None)
+    stream = torch.cuda.current_stream()
+    y = torch.empty_like(x)
+    dx = torch.empty_like(x)
+    dwg = torch.empty_like(wg)
+    dw1 = torch.empty(w1.shape, dtype=torch.float32, device=dev)
+    dw2 = torch.empty(w2.shape, dtype=torch.float32, device=dev)
+
+    def step(xx=x, dyy=dy):
+        ctx.forward(xx, wg, w1, w2, a.k, a.cf, a.chunks, y=y, routing=False)
+        ctx.backward(dyy, dx=dx, dwg=dwg, dw1=dw1, dw2=dw2)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    clocks = ClockSampler(local_rank).start()
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    # ---- timed region (device time, CUDA events on the caller stream) -------------------
+    ctx.timeline_begin(stream)
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(a.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1) / a.steps)
+    clk = clocks.stop()
+    tl = ctx.timeline(cap=200000)
+    ops = op_stats(tl, a.steps)
+    f_l, b_l = ctx.launch_counts()
+    send, recv, C = ctx.counts(a.chunks)
+    rows_expert = int(recv.sum())                     # rows this rank's experts processed
+    exposed_ms, comm_ms = exposure_per_step(tl, a.steps) if world > 1 else (0.0, 0.0)
+    exposed_ms = max_over_ranks(exposed_ms)
+
+    # ---- unoverlapped baseline (world > 1): serial schedule, one stream, chunks merged -------
+    unoverlapped_ms = 0.0
+    if world > 1:
+        ctx.set_flags(flags | lancet.FLAG_SERIAL)
+        for _ in range(2):
+            step()
+        torch.cuda.synchronize()
+        ctx.timeline_begin(stream)
+        barrier()
+        ns = max(3, min(10, a.steps))
+        for _ in range(ns):
+            step()
+        torch.cuda.synchronize()
+        tls = ctx.timeline(cap=200000)
+        unoverlapped_ms = max_over_ranks(
+            sum(r["end_us"] - r["start_us"] for r in tls if r["lane"] == 1) / ns / 1000.0)
+        ctx.set_flags(flags)
+
+    # ---- end to end through the public API with host buffers ---------------------------------
+    e2e = None
+    if not a.no_e2e:
+        xh = torch.from_numpy(ins["x"]).to(bf).pin_memory()
+        dyh = torch.from_numpy(ins["dy"]).to(bf).pin_memory()
+        yh = torch.empty(xh.shape, dtype=bf).pin_memory()
+        dxh = torch.empty(xh.shape, dtype=bf).pin_memory()
+        xd, dyd = torch.empty_like(x), torch.empty_like(dy)
+        ne = max(3, min(a.steps, 20))
+        for _ in range(2):
+            xd.copy_(xh, non_blocking=True); dyd.copy_(dyh, non_blocking=True)
+            step(xd, dyd)
+            yh.copy_(y, non_blocking=True); dxh.copy_(dx, non_blocking=True)
+        torch.cuda.synchronize()
+        barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(ne):
+            xd.copy_(xh, non_blocking=True); dyd.copy_(dyh, non_blocking=True)
+            step(xd, dyd)
+            yh.copy_(y, non_blocking=True); dxh.copy_(dx, non_blocking=True)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ems = max_over_ranks(f0.elapsed_time(f1) / ne)
+        nb = x.numel() * x.element_size()
+        e2e = {"value": world * a.tokens / (ems / 1000.0), "unit": "tokens/s",
+               "h2d_bytes_per_step": 2 * nb, "d2h_bytes_per_step": 2 * nb, "ms_per_step": ems,
+               "path": "pinned host x, dy -> device; lancet_moe_forward + lancet_moe_backward; "
+                       "y, dx -> pinned host, all on one stream inside the timed region"}
+
+    # ---- roofline of the dominant kernel (the tcgen05 grouped GEMM, 6 launches per step) ----
+    pk = peaks()
+    gemm_us = sum(ops[o]["us_per_step"] for o in GEMM_OPS if o in ops)
+    gemm_flops = 12.0 * rows_expert * a.d * a.f       # algorithmic: admitted rows only
+    achieved = gemm_flops / (gemm_us * 1e-6) / 1e12 if gemm_us > 0 else 0.0
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_gemm_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_step")
+        except Exception:  # noqa: BLE001
+            traffic = None
+    kernels = {}
+    for o in GEMM_OPS:
+        if o in ops and ops[o]["us_per_step"] > 0:
+            kernels[o] = {"us": ops[o]["us_per_step"],
+                          "tflops": 2.0 * rows_expert * a.d * a.f / (ops[o]["us_per_step"] * 1e-6) / 1e12}
+    # memory-bound kernels: algorithmic bytes per step
+    tk = a.tokens * a.k
+    adm = int(send.sum())
+    rowb = a.d * 2
+    mem_bytes = {
+        "gate": a.tokens * rowb + a.tokens * (a.experts * 4 + a.k * 8),
+        "permute": a.tokens * rowb + adm * rowb,
+        "combine": adm * rowb + a.tokens * rowb,
+        "combine_bwd": a.tokens * rowb + 2 * adm * rowb,
+        "unpermute_gate_bwd": adm * rowb + a.tokens * rowb,
+        "gate_dwg": a.tokens * rowb + a.tokens * a.experts * 4,
+    }
+    for o, b in mem_bytes.items():
+        if o in ops and ops[o]["us_per_step"] > 0:
+            kernels[o] = {"us": ops[o]["us_per_step"],
+                          "gbs": b / (ops[o]["us_per_step"] * 1e-6) / 1e9,
+                          "hbm_frac": b / (ops[o]["us_per_step"] * 1e-6) / 1e9 / pk["hbm"]}
+    del tk
+
+    out = {
+        "metric": METRIC, "value": world * a.tokens / (ms / 1000.0), "unit": "tokens/s",
+        "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (seeded; synthetic/ recipe, DESIGN.md)",
+        "config": workload(a, world),
+        "exposed_a2a_ms": exposed_ms, "a2a_ms_on_comm_lane": comm_ms,
+        "unoverlapped_a2a_ms": unoverlapped_ms,
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": pk["bf16_sus"], "unit": "TFLOP/s",
+                     "frac": achieved / pk["bf16_sus"], "traffic": traffic,
+                     "kernel": "tc_gemm_kernel (tcgen05 grouped GEMM), 6 launches/step; "
+                               "achieved = 12*rows*d*f algorithmic FLOP / summed CUDA-event time",
+                     "peak_source": pk["src"] + " bf16_tflops_sustained"},
+        "kernels": kernels,
+        "gpu_launches": (f_l + b_l) * a.steps,
+        "clocks": clk,
+        "routing": {"capacity": C, "admitted_pairs": adm, "dropped_pairs": a.tokens * a.k - adm,
+                    "expert_rows_this_rank": rows_expert},
+    }
+    if e2e:
+        out["e2e"] = e2e
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(a)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    ctx.close()
+
+
+def main():
+    a = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != a.gpus and rank == 0:
+        print(f"warning: --gpus {a.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+    if a.experts % world:
+        raise SystemExit("experts must be divisible by the number of GPUs")
+    if a.impl == "reference":
+        run_reference(a, world, rank)
+        return
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_lancet(a, world, rank, local_rank)
+    finally:
+        if world > 1:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

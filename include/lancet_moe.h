@@ -170,7 +170,13 @@ lancet_status lancet_moe_backward(lancet_ctx* ctx, const void* dy, void* dx, flo
 lancet_status lancet_get_counts(lancet_ctx* ctx, int32_t* send_counts, int32_t* recv_counts,
                                 int32_t* capacity);
 
-/* Timeline of the last forward+backward (LANCET_FLAG_TIMELINE); synchronises. */
+/* Start accumulating the timeline (LANCET_FLAG_TIMELINE) of every following forward and
+ * backward until the next call; times are relative to an event recorded on `stream` now.
+ * Without it, each forward starts a fresh timeline. */
+lancet_status lancet_timeline_begin(lancet_ctx* ctx, lancet_stream_t stream);
+
+/* Timeline of the last forward+backward, or of everything since lancet_timeline_begin
+ * (LANCET_FLAG_TIMELINE); synchronises the device. */
 lancet_status lancet_last_timeline(lancet_ctx* ctx, lancet_op_record* out, int32_t cap,
                                    int32_t* n_out);
 

@@ -43,6 +43,7 @@ struct lancet_ctx {
     std::vector<lancet::OpEvent> ops;                 // timeline of the last fwd+bwd
     std::vector<cudaEvent_t> tl_events;               // event pool for the timeline
     size_t tl_used = 0;
+    bool tl_accumulate = false;
 
     // source-side workspace (rows_src = max_tokens*max_k + E*128)
     int rows_src = 0;

@@ -553,11 +553,12 @@ LANCET_API lancet_status lancet_moe_forward(lancet_ctx* c, const void* x, const 
     c->T = T; c->k = k; c->n = n; c->cf = cf;
     c->C = capacity_of(T, k, E, cf);
     c->launches_fwd = 0;
-    c->ops.clear();
-    c->tl_used = 0;
     int& L = c->launches_fwd;
-    const bool tl = c->cfg.flags & LANCET_FLAG_TIMELINE;
-    if (tl) CK(cudaEventRecord(c->ev_tl_base, s));
+    if (!c->tl_accumulate) {
+        c->ops.clear();
+        c->tl_used = 0;
+        if (c->cfg.flags & LANCET_FLAG_TIMELINE) CK(cudaEventRecord(c->ev_tl_base, s));
+    }
 
     RouteArgs ra{};
     ra.x = x; ra.wg = wg; ra.T = T; ra.d = d; ra.E = E; ra.k = k; ra.C = c->C; ra.n_chunks = n;
@@ -934,6 +935,18 @@ LANCET_API lancet_status lancet_get_counts(lancet_ctx* c, int32_t* send_counts,
         else memcpy(recv_counts, c->host_recv.data(), sizeof(int) * G * E_l * n);
     }
     if (capacity) *capacity = c->C;
+    return LANCET_OK;
+}
+
+LANCET_API lancet_status lancet_timeline_begin(lancet_ctx* c, lancet_stream_t stream)
+{
+    lancet_status st = check_ready(c);
+    if (st) return st;
+    CK(cudaDeviceSynchronize());
+    c->ops.clear();
+    c->tl_used = 0;
+    c->tl_accumulate = true;
+    CK(cudaEventRecord(c->ev_tl_base, reinterpret_cast<cudaStream_t>(stream)));
     return LANCET_OK;
 }
 

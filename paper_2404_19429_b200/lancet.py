@@ -26,7 +26,7 @@ FLAG_RENORMALIZE, FLAG_TIMELINE, FLAG_SERIAL, FLAG_SIMT_GEMM, FLAG_NO_DW_OVERLAP
 EXPORTS = ["lancet_abi_version", "lancet_last_error", "lancet_nccl_unique_id", "lancet_create",
            "lancet_local_group_create", "lancet_local_group_destroy", "lancet_create_local",
            "lancet_destroy", "lancet_set_flags", "lancet_moe_forward", "lancet_moe_backward",
-           "lancet_get_counts", "lancet_last_timeline", "lancet_debug_copy",
+           "lancet_get_counts", "lancet_timeline_begin", "lancet_last_timeline", "lancet_debug_copy",
            "lancet_workspace_bytes", "lancet_launch_counts"]
 
 
@@ -77,6 +77,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "lancet_moe_forward": ([P, P, P, P, P, I32, I32, F32, I32, P, P, P, P, P], I32),
             "lancet_moe_backward": ([P, P, P, P, P, P, P], I32),
             "lancet_get_counts": ([P, P, P, P], I32),
+            "lancet_timeline_begin": ([P, P], I32),
             "lancet_last_timeline": ([P, ctypes.POINTER(_OpRecord), I32, ctypes.POINTER(I32)], I32),
             "lancet_debug_copy": ([P, I32, P, ctypes.c_size_t], I32),
             "lancet_workspace_bytes": ([P, ctypes.POINTER(ctypes.c_size_t)], I32),
@@ -243,6 +244,9 @@ class Context:
         _check(load_library().lancet_debug_copy(self._p, 0, out.ctypes.data_as(ctypes.c_void_p),
                                                 out.nbytes), self._p)
         return out
+
+    def timeline_begin(self, stream=None):
+        _check(load_library().lancet_timeline_begin(self._p, _stream(stream)), self._p)
 
     def timeline(self, cap: int = 1024):
         recs = (_OpRecord * cap)()

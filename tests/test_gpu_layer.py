@@ -141,7 +141,8 @@ def test_tcgen05_gemm_matches_simt_gemm(T, d, f, E, k, n):
     for key in ("idx", "slot"):
         assert np.array_equal(tc[key], simt[key])
     for key in ("y", "dx", "dwg", "dw1", "dw2"):
-        assert normwise(tc[key], simt[key]) <= 3e-3, (key, normwise(tc[key], simt[key]))
+        # two accumulation orders may round a bf16 output 1 ulp apart (2^-8 relative)
+        assert normwise(tc[key], simt[key]) <= 2 * 2.0 ** -8, (key, normwise(tc[key], simt[key]))
     o = run_oracle(ins, k, 1.0, n)
     for key in ("y", "dx", "dwg", "dw1", "dw2"):
         assert normwise(tc[key], o[key]) <= TOL["bf16"], key
