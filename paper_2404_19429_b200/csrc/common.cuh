@@ -127,4 +127,25 @@ __device__ __forceinline__ void act_fwd_grad(int act, float a, float& h, float& 
     }
 }
 
+// bf16-output variant (tcgen05 epilogues): tanh via the SFU (tanh.approx.f32, ~2^-11 rel.
+// error, far below the bf16 rounding of the stored result).
+__device__ __forceinline__ float tanh_fast(float x) {
+    float y;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ void act_fwd_grad_fast(int act, float a, float& h, float& g) {
+    if (act == ACT_RELU) {
+        h = a > 0.f ? a : 0.f;
+        g = a > 0.f ? 1.f : 0.f;
+    } else {
+        const float c = 0.7978845608028654f;
+        const float a2 = a * a;
+        const float th = tanh_fast(c * fmaf(0.044715f * a, a2, a));
+        const float hp = 0.5f * (1.f + th);
+        h = a * hp;
+        g = fmaf(0.5f * a * (1.f - th * th) * c, fmaf(3.f * 0.044715f, a2, 1.f), hp);
+    }
+}
+
 }  // namespace lancet

@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(256)
 unpermute_gate_bwd_kernel(const Elt* __restrict__ dxe, const int* __restrict__ idx,
                           const int* __restrict__ slot, const float* __restrict__ wts,
                           const float* __restrict__ g, const float* __restrict__ logits,
-                          const float* __restrict__ wg, const int* __restrict__ send_off,
+                          const float* __restrict__ wgT, const int* __restrict__ send_off,
                           int renorm, int t0, int t1, int k, int d, int E,
                           Elt* __restrict__ dx, float* __restrict__ dlogit)
 {
@@ -253,48 +253,74 @@ unpermute_gate_bwd_kernel(const Elt* __restrict__ dxe, const int* __restrict__ i
                 for (int q = 0; q < V; ++q) acc[q] += f[q];
             }
         }
+        // gate term: sum_e dlogit_e Wg[i][e], Wg read transposed ([E][d]) so lanes are coalesced
+        for (int e = 0; e < E; ++e) {
+            const float sv = sdl[e];
+            const float4* wt = reinterpret_cast<const float4*>(wgT + (size_t)e * d + (size_t)v * V);
 #pragma unroll
-        for (int q = 0; q < V; ++q) {
-            const float* wr = wg + (size_t)(v * V + q) * E;
-            float a = 0.f;
-            for (int e = 0; e < E; ++e) a = fmaf(sdl[e], wr[e], a);
-            acc[q] += a;
+            for (int h = 0; h < V / 4; ++h) {
+                const float4 w4 = __ldg(wt + h);
+                acc[4 * h + 0] = fmaf(sv, w4.x, acc[4 * h + 0]);
+                acc[4 * h + 1] = fmaf(sv, w4.y, acc[4 * h + 1]);
+                acc[4 * h + 2] = fmaf(sv, w4.z, acc[4 * h + 2]);
+                acc[4 * h + 3] = fmaf(sv, w4.w, acc[4 * h + 3]);
+            }
         }
         st_v4(reinterpret_cast<uint4*>(dx + (size_t)t * d) + v, pack16<Elt>(acc));
     }
 }
 
-constexpr int kDwgTok = 256;     // tokens per partial block
-constexpr int kDwgDim = 128;     // dims per partial block (one per thread)
-constexpr int kDwgE = 32;        // experts per pass
+constexpr int kDwgTok = 128;     // tokens per partial block
+constexpr int kDwgThreads = 128; // each thread owns 4 consecutive dims -> 512 dims per block
+constexpr int kDwgE = 8;         // experts per pass (32 accumulators per thread)
 
 template <typename Elt>
-__global__ void __launch_bounds__(kDwgDim)
+__global__ void __launch_bounds__(kDwgThreads)
 dwg_partial_kernel(const Elt* __restrict__ x, const float* __restrict__ dlogit, int T, int d,
                    int E, float* __restrict__ partial)
 {
-    __shared__ float sdl[kDwgTok][kDwgE + 1];
-    const int i = blockIdx.y * kDwgDim + threadIdx.x;
+    __shared__ __align__(16) float sdl[kDwgTok][kDwgE];
+    const int i0 = (blockIdx.y * kDwgThreads + threadIdx.x) * 4;
     const int tb = blockIdx.x;
     const int e0 = blockIdx.z * kDwgE;
     const int ne = min(kDwgE, E - e0);
     const int tbeg = tb * kDwgTok, tend = min(T, tbeg + kDwgTok);
-    for (int q = threadIdx.x; q < kDwgTok * kDwgE; q += kDwgDim) {
+    for (int q = threadIdx.x; q < kDwgTok * kDwgE; q += kDwgThreads) {
         const int r = q / kDwgE, c = q % kDwgE, t = tbeg + r;
         sdl[r][c] = (t < tend && c < ne) ? dlogit[(size_t)t * E + e0 + c] : 0.f;
     }
     __syncthreads();
-    if (i >= d) return;
-    float acc[kDwgE];
+    if (i0 >= d) return;
+    float acc[4][kDwgE];
 #pragma unroll
-    for (int c = 0; c < kDwgE; ++c) acc[c] = 0.f;
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < kDwgE; ++c) acc[a][c] = 0.f;
+#pragma unroll 4
     for (int t = tbeg; t < tend; ++t) {
-        const float xv = to_f(x[(size_t)t * d + i]);
+        float xv[4];
+        if constexpr (sizeof(Elt) == 2) {
+            const uint2 raw = __ldg(reinterpret_cast<const uint2*>(x + (size_t)t * d + i0));
+            xv[0] = __uint_as_float(raw.x << 16); xv[1] = __uint_as_float(raw.x & 0xffff0000u);
+            xv[2] = __uint_as_float(raw.y << 16); xv[3] = __uint_as_float(raw.y & 0xffff0000u);
+        } else {
+            const float4 f4 = __ldg(reinterpret_cast<const float4*>(x + (size_t)t * d + i0));
+            xv[0] = f4.x; xv[1] = f4.y; xv[2] = f4.z; xv[3] = f4.w;
+        }
+        const float4 l0 = *reinterpret_cast<const float4*>(&sdl[t - tbeg][0]);
+        const float4 l1 = *reinterpret_cast<const float4*>(&sdl[t - tbeg][4]);
+        const float lv[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
 #pragma unroll
-        for (int c = 0; c < kDwgE; ++c) acc[c] = fmaf(xv, sdl[t - tbeg][c], acc[c]);
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int c = 0; c < kDwgE; ++c) acc[a][c] = fmaf(xv[a], lv[c], acc[a][c]);
     }
-    float* out = partial + ((size_t)tb * d + i) * E + e0;
-    for (int c = 0; c < ne; ++c) out[c] = acc[c];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        if (i0 + a >= d) break;
+        float* out = partial + ((size_t)tb * d + i0 + a) * E + e0;
+        for (int c = 0; c < ne; ++c) out[c] = acc[a][c];
+    }
 }
 
 __global__ void dwg_reduce_kernel(const float* __restrict__ partial, int nb, int d, int E,
@@ -305,6 +331,15 @@ __global__ void dwg_reduce_kernel(const float* __restrict__ partial, int nb, int
     float s = 0.f;
     for (int b = 0; b < nb; ++b) s += partial[(size_t)b * d * E + q];
     dwg[q] = s;
+}
+
+__global__ void transpose_f32_kernel(const float* __restrict__ in, int rows, int cols,
+                                     float* __restrict__ out)
+{
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= rows * cols) return;
+    const int r = q / cols, c = q % cols;
+    out[(size_t)c * rows + r] = in[q];
 }
 
 __global__ void zero_pads_kernel(char* __restrict__ buf, int row_bytes,
@@ -366,8 +401,14 @@ int launch_combine_bwd(const DispatchArgs& a, const void* dy, const void* comb, 
     return 1;
 }
 
+int launch_wg_transpose(const float* wg, int d, int E, float* wgT, cudaStream_t s)
+{
+    transpose_f32_kernel<<<ceil_div(d * E, 256), 256, 0, s>>>(wg, d, E, wgT);
+    return 1;
+}
+
 int launch_unpermute_gate_bwd(const DispatchArgs& a, const void* dxe, const float* g,
-                              const float* logits, const float* wg, int renorm, void* dx,
+                              const float* logits, const float* wgT, int renorm, void* dx,
                               float* dlogit, int t0, int t1, bool is_bf16, cudaStream_t s)
 {
     if (t1 <= t0) return 0;
@@ -375,11 +416,11 @@ int launch_unpermute_gate_bwd(const DispatchArgs& a, const void* dxe, const floa
     const size_t smem = sizeof(float) * kWarpsPerBlock * a.E;
     if (is_bf16)
         unpermute_gate_bwd_kernel<bf16><<<grid, 256, smem, s>>>(
-            (const bf16*)dxe, a.idx, a.slot, a.w, g, logits, wg, a.send_off, renorm, t0, t1, a.k,
+            (const bf16*)dxe, a.idx, a.slot, a.w, g, logits, wgT, a.send_off, renorm, t0, t1, a.k,
             a.d, a.E, (bf16*)dx, dlogit);
     else
         unpermute_gate_bwd_kernel<float><<<grid, 256, smem, s>>>(
-            (const float*)dxe, a.idx, a.slot, a.w, g, logits, wg, a.send_off, renorm, t0, t1, a.k,
+            (const float*)dxe, a.idx, a.slot, a.w, g, logits, wgT, a.send_off, renorm, t0, t1, a.k,
             a.d, a.E, (float*)dx, dlogit);
     return 1;
 }
@@ -390,11 +431,11 @@ int launch_dwg(const void* x, const float* dlogit, int T, int d, int E, float* p
                float* dwg, bool is_bf16, cudaStream_t s)
 {
     const int nb = ceil_div(T, kDwgTok);
-    dim3 grid(nb, ceil_div(d, kDwgDim), ceil_div(E, kDwgE));
+    dim3 grid(nb, ceil_div(d, kDwgThreads * 4), ceil_div(E, kDwgE));
     if (is_bf16)
-        dwg_partial_kernel<bf16><<<grid, kDwgDim, 0, s>>>((const bf16*)x, dlogit, T, d, E, partial);
+        dwg_partial_kernel<bf16><<<grid, kDwgThreads, 0, s>>>((const bf16*)x, dlogit, T, d, E, partial);
     else
-        dwg_partial_kernel<float><<<grid, kDwgDim, 0, s>>>((const float*)x, dlogit, T, d, E, partial);
+        dwg_partial_kernel<float><<<grid, kDwgThreads, 0, s>>>((const float*)x, dlogit, T, d, E, partial);
     dwg_reduce_kernel<<<ceil_div(d * E, 256), 256, 0, s>>>(partial, nb, d, E, dwg);
     return 2;
 }

@@ -14,8 +14,8 @@
 // GEMMs and both operands of the dW GEMMs are read transposed in place -- no transposition
 // pass over HBM).
 //
-// Roles (256 threads):  warp 0 TMA producer | warp 1 MMA issuer | warp 2 TMEM allocator |
-//                       warp 3 idle | warps 4-7 epilogue (TMEM lanes 32*(w%4) ...).
+// Roles (384 threads):  warp 0 TMA producer | warp 1 MMA issuer | warp 2 TMEM allocator |
+//                       warp 3 idle | warps 4-11 epilogue (TMEM lanes 32*(w%4) ...).
 #include <cuda.h>
 
 #include <mutex>
@@ -27,7 +27,7 @@ namespace lancet {
 namespace tc {
 
 constexpr int BM = 128, BK = 64, STAGES = 4, UMMA_K = 16;
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;            // 4 control warps + 8 epilogue warps
 constexpr int kMaxGroups = 512;
 constexpr uint32_t A_STAGE = BM * BK * 2;                 // 16 KiB
 
@@ -179,7 +179,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     }
     if (warp == 1 && lane == 0) {
         for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-        for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
+        for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 8); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 2) {
@@ -268,8 +268,10 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             }
         }
     } else if (warp >= 4) {
-        // ===================== epilogue warpgroup =====================
+        // ===================== epilogue: 8 warps =====================
+        // warp w may only touch TMEM lanes 32*(w%4)..; warps w and w+4 split the columns
         const int q = warp & 3;
+        const int half = (warp - 4) >> 2;
         int it = 0;
         for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
             int g, mt, nt;
@@ -285,7 +287,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             if (p.mode == GEMM_M_GROUPED) orow = (long)p.grp_off[g] + mt * BM + lrow;
             else orow = (long)mt * BM + lrow;
 #pragma unroll 1
-            for (int cc = 0; cc < BN / 32; ++cc) {
+            for (int cc = half * (BN / 64); cc < (half + 1) * (BN / 64); ++cc) {
                 uint32_t v[32];
                 tmem_ld32(tmem_base + acc * BN + cc * 32 + ((uint32_t)(q * 32) << 16), v);
                 float f[32];
@@ -310,7 +312,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                     if (p.epi == EPI_ACT) {
                         float h[32], gr[32];
 #pragma unroll
-                        for (int i = 0; i < 32; ++i) act_fwd_grad(p.act, f[i], h[i], gr[i]);
+                        for (int i = 0; i < 32; ++i) act_fwd_grad_fast(p.act, f[i], h[i], gr[i]);
                         bf16* C2 = reinterpret_cast<bf16*>(p.C2) + orow * p.ldc + col;
 #pragma unroll
                         for (int i = 0; i < 4; ++i) {

@@ -35,10 +35,11 @@ int launch_combine(const DispatchArgs& a, const void* comb, void* y, int t0, int
                    cudaStream_t s);
 int launch_combine_bwd(const DispatchArgs& a, const void* dy, const void* comb, float* g,
                        void* dcomb, int t0, int t1, bool zero_pads, bool is_bf16, cudaStream_t s);
+int launch_wg_transpose(const float* wg, int d, int E, float* wgT, cudaStream_t s);
 int launch_unpermute_gate_bwd(const DispatchArgs& a, const void* dxe, const float* g,
-                              const float* logits, const float* wg, int renorm, void* dx,
+                              const float* logits, const float* wgT, int renorm, void* dx,
                               float* dlogit, int t0, int t1, bool is_bf16, cudaStream_t s);
-// dWg = x^T dlogit (K7); partial: [ceil(T/256)][d][E] fp32 scratch
+// dWg = x^T dlogit (K7); partial: [ceil(T/128)][d][E] fp32 scratch
 int launch_dwg(const void* x, const float* dlogit, int T, int d, int E, float* partial,
                float* dwg, bool is_bf16, cudaStream_t s);
 size_t dwg_partial_floats(int T, int d, int E);

@@ -291,6 +291,7 @@ lancet_status create_common(lancet_ctx* c, int world, int rank, int device, cons
     AL(c->g, sizeof(float) * (size_t)T * K);
     AL(c->dlogit, sizeof(float) * (size_t)T * E);
     AL(c->dwg_partial, sizeof(float) * dwg_partial_floats(T, d, E));
+    AL(c->wgT, sizeof(float) * (size_t)d * E);
     AL(c->counts_dev, sizeof(int) * 2 * (size_t)E * kMaxChunks);
     AL(c->grp_dev, sizeof(int) * 2 * (size_t)c->E_l * kMaxChunks);
     const size_t rs = (size_t)c->rows_src * d * c->elt;
@@ -769,7 +770,8 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
             dxe = c->dXe;
         }
         { OpScope op(c, "unpermute_gate_bwd", 0, -1, s);
-          L += launch_unpermute_gate_bwd(da, dxe, c->g, c->logits, c->wg, renorm, dx, c->dlogit, 0, T, c->bf16, s); }
+          L += launch_wg_transpose(c->wg, d, E, c->wgT, s);
+          L += launch_unpermute_gate_bwd(da, dxe, c->g, c->logits, c->wgT, renorm, dx, c->dlogit, 0, T, c->bf16, s); }
         CHECK_LAUNCH();
         { OpScope op(c, "gate_dwg", 0, -1, s);
           L += launch_dwg(c->x, c->dlogit, T, d, E, c->dwg_partial, dwg, c->bf16, s); }
@@ -802,6 +804,7 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
     };
     // pads of the received dO rows must be zero (K-grouped dW reads whole 128-row blocks)
     L += launch_zero_pads(c->dout, d, d_grp_off, d_grp_rows, n * E_l, (int)c->elt, sc);
+    L += launch_wg_transpose(c->wg, d, E, c->wgT, sc);
     const void* comb = c->comb;     // o_tj returned by the combine all-to-all (source side)
     std::vector<cudaEvent_t> ev_k5(nc), ev_b1(nc), ev_dx(nc), ev_b2(nc);
     for (int cc = 0; cc < nc; ++cc) {
@@ -900,7 +903,7 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
         tok_range(cc, t0, t1);
         CK(cudaStreamWaitEvent(sc, ev_b2[cc], 0));
         OpScope op(c, "unpermute_gate_bwd", 0, serial ? -1 : cc, sc);
-        L += launch_unpermute_gate_bwd(da, dxcomb, c->g, c->logits, c->wg, renorm, dx, c->dlogit, t0, t1, c->bf16, sc);
+        L += launch_unpermute_gate_bwd(da, dxcomb, c->g, c->logits, c->wgT, renorm, dx, c->dlogit, t0, t1, c->bf16, sc);
     }
     CHECK_LAUNCH();
     { OpScope op(c, "gate_dwg", 0, -1, sc);

@@ -18,64 +18,124 @@
 
 namespace lancet {
 
-constexpr int kGateThreads = 256;
-constexpr int kGateTPT = 4;    // (token, expert) chains per thread: 4 tokens x 1 expert
-constexpr int kGateTI = 64;    // d-tile staged in shared memory
-constexpr int kGateMaxGroups = 64;   // <= 256 tokens per block
+constexpr int kGateDT = 256;     // d-tile staged in shared memory (double-buffered cp.async)
+constexpr int kGateMaxTB = 64;   // tokens per block
+constexpr int kGateThreadCap = 128;
+
+struct GateGeom {
+    int ce;        // experts per thread (4 if E % 4 == 0, else 1)
+    int tpt;       // threads per token = E / ce
+    int TB;        // tokens per block
+    int threads;   // TB * tpt
+    size_t smem;
+};
+
+__host__ __device__ inline GateGeom gate_geom(int E, int elt_bytes)
+{
+    GateGeom g;
+    g.ce = (E % 4 == 0) ? 4 : 1;
+    g.tpt = E / g.ce;
+    g.TB = kGateThreadCap / g.tpt;
+    if (g.TB > kGateMaxTB) g.TB = kGateMaxTB;
+    if (g.TB < 1) g.TB = 1;
+    g.threads = g.TB * g.tpt;
+    const size_t row = (size_t)kGateDT * elt_bytes + 16;           // +16 B: no bank conflicts
+    const size_t xs = 2 * (size_t)g.TB * row;
+    const size_t lg = sizeof(float) * (size_t)g.TB * E;
+    g.smem = xs > lg ? xs : lg;
+    return g;
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+                 "l"(gmem)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 template <typename Elt>
-__global__ void __launch_bounds__(kGateThreads)
+__device__ __forceinline__ void gate_load_tile(const Elt* __restrict__ x, int T, int d, int t0, int TB,
+                                               int i0, uint8_t* buf, int row_bytes)
+{
+    const int ilim = min(kGateDT, d - i0);
+    const int cpr = ilim * (int)sizeof(Elt) / 16;                 // 16-byte chunks per row
+    for (int q = threadIdx.x; q < TB * cpr; q += blockDim.x) {
+        const int r = q / cpr, c = q % cpr, t = t0 + r;
+        if (t < T)
+            cp_async16(buf + (size_t)r * row_bytes + c * 16,
+                       reinterpret_cast<const uint8_t*>(x + (size_t)t * d + i0) + c * 16);
+    }
+}
+
+// K1.  Thread (token r, experts e0..e0+CE-1) runs CE independent R1 chains; x tiles of 256 dims
+// stream through shared memory (cp.async double buffer), Wg rows come through L1 (__ldg).
+template <typename Elt, int CE>
+__global__ void __launch_bounds__(kGateThreadCap)
 gate_topk_kernel(const Elt* __restrict__ x, const float* __restrict__ wg, int T, int d, int E,
                  int k, int renorm, float* __restrict__ logits, int* __restrict__ idx_out,
                  float* __restrict__ w_out, int* __restrict__ hist, int n_tiles)
 {
-    extern __shared__ float smem[];
+    extern __shared__ __align__(16) uint8_t gsm[];
     __shared__ int sh_hist[2 * kMaxExperts];
-    const int ngroups = min(kGateThreads / E, kGateMaxGroups);
-    const int TB = ngroups * kGateTPT;              // tokens of this block (<= 256)
-    constexpr int LD = kGateTI + 1;
-    float* xs = smem;                                // [TB][LD]
-    float* ws = xs + TB * LD;                        // [TI][E]
+    const GateGeom geo = gate_geom(E, sizeof(Elt));
+    const int TB = geo.TB;
+    const int row_bytes = kGateDT * sizeof(Elt) + 16;
+    uint8_t* buf0 = gsm;
+    uint8_t* buf1 = gsm + (size_t)TB * row_bytes;
     const int tid = threadIdx.x;
-    const int e = tid % E, grp = tid / E;
-    const bool active = grp < ngroups;
+    const int r = tid / geo.tpt;                      // token within block
+    const int e0 = (tid % geo.tpt) * CE;
     const int t0 = blockIdx.x * TB;
+    const bool active = tid < geo.threads;
 
-    for (int q = tid; q < 2 * E; q += kGateThreads) sh_hist[q] = 0;
+    for (int q = tid; q < 2 * E; q += blockDim.x) sh_hist[q] = 0;
 
-    float acc[kGateTPT];
+    float acc[CE];
 #pragma unroll
-    for (int c = 0; c < kGateTPT; ++c) acc[c] = 0.f;
+    for (int c = 0; c < CE; ++c) acc[c] = 0.f;
 
-    for (int i0 = 0; i0 < d; i0 += kGateTI) {
-        const int ilim = min(kGateTI, d - i0);
-        for (int q = tid; q < TB * kGateTI; q += kGateThreads) {
-            const int r = q / kGateTI, c = q % kGateTI, t = t0 + r;
-            xs[r * LD + c] = (t < T && c < ilim) ? to_f(x[(size_t)t * d + i0 + c]) : 0.f;
-        }
-        for (int q = tid; q < kGateTI * E; q += kGateThreads) {
-            const int i = q / E;
-            ws[q] = (i < ilim) ? wg[(size_t)(i0 + i) * E + (q % E)] : 0.f;
-        }
+    const int ntiles = ceil_div(d, kGateDT);
+    gate_load_tile(x, T, d, t0, TB, 0, buf0, row_bytes);
+    cp_async_commit();
+    for (int it = 0; it < ntiles; ++it) {
+        uint8_t* cur = (it & 1) ? buf1 : buf0;
+        uint8_t* nxt = (it & 1) ? buf0 : buf1;
+        if (it + 1 < ntiles) gate_load_tile(x, T, d, t0, TB, (it + 1) * kGateDT, nxt, row_bytes);
+        cp_async_commit();
+        cp_async_wait<1>();
         __syncthreads();
-        if (active) {
-            const float* xr = xs + grp * kGateTPT * LD;
-            for (int i = 0; i < ilim; ++i) {            // R1: increasing i, fused steps
-                const float wv = ws[i * E + e];
-#pragma unroll
-                for (int c = 0; c < kGateTPT; ++c) acc[c] = __fmaf_rn(xr[c * LD + i], wv, acc[c]);
+        const int i0 = it * kGateDT;
+        const int ilim = min(kGateDT, d - i0);
+        if (active && t0 + r < T) {
+            const Elt* xr = reinterpret_cast<const Elt*>(cur + (size_t)r * row_bytes);
+            const float* wrow = wg + (size_t)i0 * E + e0;
+#pragma unroll 4
+            for (int i = 0; i < ilim; ++i) {           // R1: increasing i, one fused step each
+                const float xv = to_f(xr[i]);
+                if constexpr (CE == 4) {
+                    const float4 w4 = __ldg(reinterpret_cast<const float4*>(wrow + (size_t)i * E));
+                    acc[0] = __fmaf_rn(xv, w4.x, acc[0]);
+                    acc[1] = __fmaf_rn(xv, w4.y, acc[1]);
+                    acc[2] = __fmaf_rn(xv, w4.z, acc[2]);
+                    acc[3] = __fmaf_rn(xv, w4.w, acc[3]);
+                } else {
+                    acc[0] = __fmaf_rn(xv, __ldg(wrow + (size_t)i * E), acc[0]);
+                }
             }
         }
         __syncthreads();
     }
+    cp_async_wait<0>();
 
-    float* lg = smem;                                // [TB][E] (xs is free now)
+    float* lg = reinterpret_cast<float*>(gsm);        // [TB][E]; x buffers are free now
     if (active) {
 #pragma unroll
-        for (int c = 0; c < kGateTPT; ++c) {
-            const int r = grp * kGateTPT + c, t = t0 + r;
-            lg[r * E + e] = acc[c];
-            if (t < T) logits[(size_t)t * E + e] = acc[c];
+        for (int c = 0; c < CE; ++c) {
+            lg[r * E + e0 + c] = acc[c];
+            if (t0 + r < T) logits[(size_t)(t0 + r) * E + e0 + c] = acc[c];
         }
     }
     __syncthreads();
@@ -120,7 +180,7 @@ gate_topk_kernel(const Elt* __restrict__ x, const float* __restrict__ wg, int T,
         }
     }
     __syncthreads();
-    for (int q = tid; q < 2 * E; q += kGateThreads) {
+    for (int q = tid; q < 2 * E; q += blockDim.x) {
         const int tile = tile0 + q / E;
         if (sh_hist[q] && tile < n_tiles) atomicAdd(&hist[tile * E + (q % E)], sh_hist[q]);
     }
@@ -218,42 +278,36 @@ slot_scan_kernel(const int* __restrict__ idx, int T, int k, int E, int C, int n,
     }
 }
 
-size_t routing_smem_bytes(int E);
-
 int launch_routing(const RouteArgs& a, bool is_bf16, cudaStream_t s)
 {
     const int n_tiles = ceil_div(a.T, kScanTile);
     cudaMemsetAsync(a.hist, 0, sizeof(int) * n_tiles * a.E, s);
-    const size_t smem = routing_smem_bytes(a.E);
-    const int TB = std::min(kGateThreads / a.E, kGateMaxGroups) * kGateTPT;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(gate_topk_kernel<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(gate_topk_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(gate_topk_kernel<bf16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(gate_topk_kernel<bf16, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(gate_topk_kernel<float, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(gate_topk_kernel<float, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaFuncSetAttribute(slot_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr_set = true;
     }
-    const int blocks = ceil_div(a.T, TB);
-    if (is_bf16)
-        gate_topk_kernel<bf16><<<blocks, kGateThreads, smem, s>>>(
-            (const bf16*)a.x, a.wg, a.T, a.d, a.E, a.k, a.renorm, a.logits, a.idx, a.w, a.hist,
-            n_tiles);
-    else
-        gate_topk_kernel<float><<<blocks, kGateThreads, smem, s>>>(
-            (const float*)a.x, a.wg, a.T, a.d, a.E, a.k, a.renorm, a.logits, a.idx, a.w, a.hist,
-            n_tiles);
+    const GateGeom g = gate_geom(a.E, is_bf16 ? 2 : 4);
+    const int blocks = ceil_div(a.T, g.TB);
+    const int thr = round_up(g.threads, 32);
+#define GATE_ARGS a.T, a.d, a.E, a.k, a.renorm, a.logits, a.idx, a.w, a.hist, n_tiles
+    if (is_bf16) {
+        if (g.ce == 4) gate_topk_kernel<bf16, 4><<<blocks, thr, g.smem, s>>>((const bf16*)a.x, a.wg, GATE_ARGS);
+        else gate_topk_kernel<bf16, 1><<<blocks, thr, g.smem, s>>>((const bf16*)a.x, a.wg, GATE_ARGS);
+    } else {
+        if (g.ce == 4) gate_topk_kernel<float, 4><<<blocks, thr, g.smem, s>>>((const float*)a.x, a.wg, GATE_ARGS);
+        else gate_topk_kernel<float, 1><<<blocks, thr, g.smem, s>>>((const float*)a.x, a.wg, GATE_ARGS);
+    }
+#undef GATE_ARGS
     const size_t smem2 = sizeof(int) * (a.E + 32 * a.E + 32 * a.E + a.E);
     slot_scan_kernel<<<n_tiles, kScanTile, smem2, s>>>(a.idx, a.T, a.k, a.E, a.C, a.n_chunks,
                                                        a.hist, n_tiles, a.slot, a.S, a.send_rows,
                                                        a.send_off);
     return 2;
-}
-
-// Host-side shared-memory needs (checked against the device limit at context creation).
-size_t routing_smem_bytes(int E)
-{
-    const int TB = std::min(kGateThreads / E, kGateMaxGroups) * kGateTPT;
-    return sizeof(float) * (TB * (kGateTI + 1) + kGateTI * E);
 }
 
 }  // namespace lancet
