@@ -97,7 +97,7 @@ typedef struct {
  * microseconds from the start event recorded on the caller's stream. */
 typedef struct {
     char name[24];        /* e.g. "gate", "a2a_dispatch[2]", "expert_fc1[2]"          */
-    int32_t lane;         /* 0 = compute stream, 1 = comm stream                       */
+    int32_t lane;         /* 0 = compute stream, 1 = comm stream, 2 = side compute    */
     int32_t chunk;        /* chunk index or -1                                         */
     float start_us;
     float end_us;

@@ -2,9 +2,9 @@
 //
 // K3 permute:   "The tokens are re-arranged according to their target experts":
 //               row x[t] -> xs[off_e + slot] for every admitted (t, j); one warp per token,
-//               16-byte vector loads issued before the k stores.  Expert e's rows of chunk c
-//               are the contiguous range [off_e + S[e][c], off_e + S[e][c+1]) -- the chunk's
-//               send message needs no repacking.
+//               all 16-byte loads of the row issued before the k stores.  Expert e's rows of
+//               chunk c are the contiguous range [off_e + S[e][c], off_e + S[e][c+1]) -- the
+//               chunk's send message needs no repacking.
 // K4 combine:   "Reverting tokens to their original order yields the MoE layer's output"
 //               (gather): y_t = sum_{admitted j} w_tj o_tj as an fp32 fma chain
 //               over j in order, dropped choices contribute 0 (R6).
@@ -12,6 +12,10 @@
 // K6 dispatch backward + gate:  dx_t = sum_{admitted j} dX_e[off_e + slot]
 //               + sum_e dlogit_te Wg[:, e], with dlogit from the softmax Jacobian (R3).
 // K7 dWg = x^T dlogit (two-pass deterministic reduction over tokens).
+//
+// All token kernels are templated on KK >= k (compile-time top-k width) so a lane keeps the
+// k source/destination rows of its vectors in registers and issues every load of an
+// iteration before the first use (memory-level parallelism is what bounds them).
 #include "common.cuh"
 #include "kernels.h"
 
@@ -19,7 +23,31 @@ namespace lancet {
 
 constexpr int kWarpsPerBlock = 8;
 
-template <typename Elt>
+// rows[j] = packed row of choice j (-1 dropped or j >= k); wj[j] = combine weight; ids[j] = expert
+template <int KK>
+__device__ __forceinline__ void load_choices(const int* __restrict__ idx, const int* __restrict__ slot,
+                                             const float* __restrict__ wts, const int* __restrict__ send_off,
+                                             int t, int k, int lane, int (&rows)[KK], float (&wj)[KK],
+                                             int (&ids)[KK])
+{
+    int myrow = -1, myidx = -1;
+    float myw = 0.f;
+    if (lane < k) {
+        const int s = slot[(size_t)t * k + lane];
+        myidx = idx[(size_t)t * k + lane];
+        myrow = s >= 0 ? send_off[myidx] + s : -1;
+        if (wts) myw = wts[(size_t)t * k + lane];
+    }
+#pragma unroll
+    for (int j = 0; j < KK; ++j) {
+        rows[j] = __shfl_sync(0xffffffffu, myrow, j);
+        wj[j] = __shfl_sync(0xffffffffu, myw, j);
+        ids[j] = __shfl_sync(0xffffffffu, myidx, j);
+        if (j >= k) rows[j] = -1;
+    }
+}
+
+template <typename Elt, int KK>
 __global__ void __launch_bounds__(256)
 permute_kernel(const Elt* __restrict__ x, const int* __restrict__ idx, const int* __restrict__ slot,
                int T, int k, int d, const int* __restrict__ send_off,
@@ -31,14 +59,9 @@ permute_kernel(const Elt* __restrict__ x, const int* __restrict__ idx, const int
     if ((int)blockIdx.x < tok_blocks) {
         const int t = blockIdx.x * kWarpsPerBlock + w;
         if (t >= T) return;
-        int myrow = -1;
-        if (lane < k) {
-            const int s = slot[(size_t)t * k + lane];
-            myrow = s >= 0 ? send_off[idx[(size_t)t * k + lane]] + s : -1;
-        }
-        int rows[kMaxK];
-#pragma unroll
-        for (int j = 0; j < kMaxK; ++j) rows[j] = __shfl_sync(0xffffffffu, myrow, j);
+        int rows[KK], ids[KK];
+        float wj[KK];
+        load_choices<KK>(idx, slot, nullptr, send_off, t, k, lane, rows, wj, ids);
         const uint4* src = reinterpret_cast<const uint4*>(x + (size_t)t * d);
         constexpr int U = 4;
         for (int v0 = lane; v0 < nvec; v0 += 32 * U) {
@@ -47,8 +70,8 @@ permute_kernel(const Elt* __restrict__ x, const int* __restrict__ idx, const int
             for (int u = 0; u < U; ++u)
                 if (v0 + 32 * u < nvec) val[u] = ld_nc_v4(src + v0 + 32 * u);
 #pragma unroll
-            for (int j = 0; j < kMaxK; ++j) {
-                if (j < k && rows[j] >= 0) {
+            for (int j = 0; j < KK; ++j) {
+                if (rows[j] >= 0) {
                     uint4* dst = reinterpret_cast<uint4*>(xs + (size_t)rows[j] * d);
 #pragma unroll
                     for (int u = 0; u < U; ++u)
@@ -68,7 +91,7 @@ permute_kernel(const Elt* __restrict__ x, const int* __restrict__ idx, const int
     }
 }
 
-template <typename Elt>
+template <typename Elt, int KK>
 __global__ void __launch_bounds__(256)
 combine_kernel(const Elt* __restrict__ comb, const int* __restrict__ idx,
                const int* __restrict__ slot, const float* __restrict__ wts,
@@ -76,48 +99,44 @@ combine_kernel(const Elt* __restrict__ comb, const int* __restrict__ idx,
                Elt* __restrict__ y)
 {
     constexpr int V = Vec16<Elt>::N;
+    constexpr int U = 2;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int t = t0 + blockIdx.x * kWarpsPerBlock + w;
     if (t >= t1) return;
-    int myrow = -1;
-    float myw = 0.f;
-    if (lane < k) {
-        const int s = slot[(size_t)t * k + lane];
-        myrow = s >= 0 ? send_off[idx[(size_t)t * k + lane]] + s : -1;
-        myw = wts[(size_t)t * k + lane];
-    }
-    int rows[kMaxK];
-    float wj[kMaxK];
-#pragma unroll
-    for (int j = 0; j < kMaxK; ++j) {
-        rows[j] = __shfl_sync(0xffffffffu, myrow, j);
-        wj[j] = __shfl_sync(0xffffffffu, myw, j);
-    }
+    int rows[KK], ids[KK];
+    float wj[KK];
+    load_choices<KK>(idx, slot, wts, send_off, t, k, lane, rows, wj, ids);
     const int nvec = d / V;
     uint4* dst = reinterpret_cast<uint4*>(y + (size_t)t * d);
-    for (int v = lane; v < nvec; v += 32) {
-        float acc[V];
+    for (int v0 = lane; v0 < nvec; v0 += 32 * U) {
+        uint4 raw[U][KK];
 #pragma unroll
-        for (int q = 0; q < V; ++q) acc[q] = 0.f;
-        uint4 raw[kMaxK];
+        for (int u = 0; u < U; ++u)
 #pragma unroll
-        for (int j = 0; j < kMaxK; ++j)
-            if (j < k && rows[j] >= 0)
-                raw[j] = ld_nc_v4(reinterpret_cast<const uint4*>(comb + (size_t)rows[j] * d) + v);
+            for (int j = 0; j < KK; ++j)
+                if (rows[j] >= 0 && v0 + 32 * u < nvec)
+                    raw[u][j] = ld_nc_v4(reinterpret_cast<const uint4*>(comb + (size_t)rows[j] * d) + v0 + 32 * u);
 #pragma unroll
-        for (int j = 0; j < kMaxK; ++j) {
-            if (j < k && rows[j] >= 0) {
-                float f[V];
-                unpack16<Elt>(raw[j], f);
+        for (int u = 0; u < U; ++u) {
+            if (v0 + 32 * u >= nvec) break;
+            float acc[V];
 #pragma unroll
-                for (int q = 0; q < V; ++q) acc[q] = __fmaf_rn(wj[j], f[q], acc[q]);
+            for (int q = 0; q < V; ++q) acc[q] = 0.f;
+#pragma unroll
+            for (int j = 0; j < KK; ++j) {
+                if (rows[j] >= 0) {
+                    float f[V];
+                    unpack16<Elt>(raw[u][j], f);
+#pragma unroll
+                    for (int q = 0; q < V; ++q) acc[q] = __fmaf_rn(wj[j], f[q], acc[q]);
+                }
             }
+            st_v4(dst + v0 + 32 * u, pack16<Elt>(acc));
         }
-        st_v4(dst + v, pack16<Elt>(acc));
     }
 }
 
-template <typename Elt>
+template <typename Elt, int KK>
 __global__ void __launch_bounds__(256)
 combine_bwd_kernel(const Elt* __restrict__ dy, const Elt* __restrict__ comb,
                    const int* __restrict__ idx, const int* __restrict__ slot,
@@ -126,6 +145,7 @@ combine_bwd_kernel(const Elt* __restrict__ dy, const Elt* __restrict__ comb,
                    float* __restrict__ g, Elt* __restrict__ dcomb, int tok_blocks)
 {
     constexpr int V = Vec16<Elt>::N;
+    constexpr int U = 2;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nvec = d / V;
     if ((int)blockIdx.x >= tok_blocks) {
@@ -140,41 +160,46 @@ combine_bwd_kernel(const Elt* __restrict__ dy, const Elt* __restrict__ comb,
     }
     const int t = t0 + blockIdx.x * kWarpsPerBlock + w;
     if (t >= t1) return;
-    int myrow = -1;
-    float myw = 0.f;
-    if (lane < k) {
-        const int s = slot[(size_t)t * k + lane];
-        myrow = s >= 0 ? send_off[idx[(size_t)t * k + lane]] + s : -1;
-        myw = wts[(size_t)t * k + lane];
-    }
-    int rows[kMaxK];
-    float wj[kMaxK], part[kMaxK];
+    int rows[KK], ids[KK];
+    float wj[KK], part[KK];
+    load_choices<KK>(idx, slot, wts, send_off, t, k, lane, rows, wj, ids);
 #pragma unroll
-    for (int j = 0; j < kMaxK; ++j) {
-        rows[j] = __shfl_sync(0xffffffffu, myrow, j);
-        wj[j] = __shfl_sync(0xffffffffu, myw, j);
-        part[j] = 0.f;
-    }
+    for (int j = 0; j < KK; ++j) part[j] = 0.f;
     const uint4* dyr = reinterpret_cast<const uint4*>(dy + (size_t)t * d);
-    for (int v = lane; v < nvec; v += 32) {
-        float fdy[V];
-        unpack16<Elt>(ld_nc_v4(dyr + v), fdy);
+    for (int v0 = lane; v0 < nvec; v0 += 32 * U) {
+        uint4 rdy[U], ro[U][KK];
 #pragma unroll
-        for (int j = 0; j < kMaxK; ++j) {
-            if (j < k && rows[j] >= 0) {
-                float fo[V], sc[V];
-                unpack16<Elt>(ld_nc_v4(reinterpret_cast<const uint4*>(comb + (size_t)rows[j] * d) + v), fo);
+        for (int u = 0; u < U; ++u) {
+            if (v0 + 32 * u < nvec) {
+                rdy[u] = ld_nc_v4(dyr + v0 + 32 * u);
 #pragma unroll
-                for (int q = 0; q < V; ++q) {
-                    part[j] = fmaf(fdy[q], fo[q], part[j]);
-                    sc[q] = wj[j] * fdy[q];
+                for (int j = 0; j < KK; ++j)
+                    if (rows[j] >= 0)
+                        ro[u][j] = ld_nc_v4(reinterpret_cast<const uint4*>(comb + (size_t)rows[j] * d) + v0 + 32 * u);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (v0 + 32 * u >= nvec) break;
+            float fdy[V];
+            unpack16<Elt>(rdy[u], fdy);
+#pragma unroll
+            for (int j = 0; j < KK; ++j) {
+                if (rows[j] >= 0) {
+                    float fo[V], sc[V];
+                    unpack16<Elt>(ro[u][j], fo);
+#pragma unroll
+                    for (int q = 0; q < V; ++q) {
+                        part[j] = fmaf(fdy[q], fo[q], part[j]);
+                        sc[q] = wj[j] * fdy[q];
+                    }
+                    st_v4(reinterpret_cast<uint4*>(dcomb + (size_t)rows[j] * d) + v0 + 32 * u, pack16<Elt>(sc));
                 }
-                st_v4(reinterpret_cast<uint4*>(dcomb + (size_t)rows[j] * d) + v, pack16<Elt>(sc));
             }
         }
     }
 #pragma unroll
-    for (int j = 0; j < kMaxK; ++j) {
+    for (int j = 0; j < KK; ++j) {
         if (j < k) {
             const float s = warp_sum(part[j]);
             if (lane == 0) g[(size_t)t * k + j] = rows[j] >= 0 ? s : 0.f;
@@ -182,8 +207,10 @@ combine_bwd_kernel(const Elt* __restrict__ dy, const Elt* __restrict__ comb,
     }
 }
 
-// dlogit in smem per warp; E <= kMaxExperts
-template <typename Elt>
+// K6: kTPW tokens per warp so each transposed-Wg vector is reused kTPW times.
+constexpr int kTPW = 4;
+
+template <typename Elt, int KK>
 __global__ void __launch_bounds__(256)
 unpermute_gate_bwd_kernel(const Elt* __restrict__ dxe, const int* __restrict__ idx,
                           const int* __restrict__ slot, const float* __restrict__ wts,
@@ -192,87 +219,105 @@ unpermute_gate_bwd_kernel(const Elt* __restrict__ dxe, const int* __restrict__ i
                           int renorm, int t0, int t1, int k, int d, int E,
                           Elt* __restrict__ dx, float* __restrict__ dlogit)
 {
-    extern __shared__ float sdl_all[];
+    extern __shared__ float sdl_all[];                 // [warps][kTPW][E]
     constexpr int V = Vec16<Elt>::N;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int t = t0 + blockIdx.x * kWarpsPerBlock + w;
-    if (t >= t1) return;
-    float* sdl = sdl_all + w * E;
-    int myrow = -1, myidx = -1;
-    float myw = 0.f, myg = 0.f;
-    if (lane < k) {
-        const int s = slot[(size_t)t * k + lane];
-        myidx = idx[(size_t)t * k + lane];
-        myrow = s >= 0 ? send_off[myidx] + s : -1;
-        myw = wts[(size_t)t * k + lane];
-        myg = g[(size_t)t * k + lane];
-    }
-    int rows[kMaxK], ids[kMaxK];
-    float wj[kMaxK], gj[kMaxK];
-    float sg = 0.f;                                   // sum_j g_j w_j
+    const int tb = t0 + (blockIdx.x * kWarpsPerBlock + w) * kTPW;
+    if (tb >= t1) return;
+    float* sdl = sdl_all + (size_t)w * kTPW * E;
+    int rows[kTPW][KK];
+    bool valid[kTPW];
 #pragma unroll
-    for (int j = 0; j < kMaxK; ++j) {
-        rows[j] = __shfl_sync(0xffffffffu, myrow, j);
-        ids[j] = __shfl_sync(0xffffffffu, myidx, j);
-        wj[j] = __shfl_sync(0xffffffffu, myw, j);
-        gj[j] = __shfl_sync(0xffffffffu, myg, j);
-        if (j < k) sg = fmaf(gj[j], wj[j], sg);
-    }
-    // softmax Jacobian (R3): dlogit_e = p_e (g~_e - sg), or renormalised at the selected e
-    const float* lr = logits + (size_t)t * E;
-    float m = -INFINITY;
-    for (int e = lane; e < E; e += 32) m = fmaxf(m, lr[e]);
-    m = warp_max(m);
-    float s = 0.f;
-    for (int e = lane; e < E; e += 32) s += expf(lr[e] - m);
-    s = warp_sum(s);
-    for (int e = lane; e < E; e += 32) {
-        float gt = 0.f, wsel = 0.f;
-        bool sel = false;
+    for (int q = 0; q < kTPW; ++q) {
+        const int t = tb + q;
+        valid[q] = t < t1;
+        int ids[KK];
+        float wj[KK];
+        if (valid[q]) {
+            load_choices<KK>(idx, slot, wts, send_off, t, k, lane, rows[q], wj, ids);
+            const float myg = lane < k ? g[(size_t)t * k + lane] : 0.f;
+            float gj[KK];
+            float sg = 0.f;                               // sum_j g_j w_j
 #pragma unroll
-        for (int j = 0; j < kMaxK; ++j)
-            if (j < k && ids[j] == e) { gt = gj[j]; wsel = wj[j]; sel = true; }
-        float dl;
-        if (renorm) dl = sel ? wsel * (gt - sg) : 0.f;
-        else dl = (expf(lr[e] - m) / s) * (gt - sg);
-        sdl[e] = dl;
-        dlogit[(size_t)t * E + e] = dl;
+            for (int j = 0; j < KK; ++j) {
+                gj[j] = __shfl_sync(0xffffffffu, myg, j);
+                if (j < k) sg = fmaf(gj[j], wj[j], sg);
+            }
+            // softmax Jacobian (R3): dlogit_e = p_e (g~_e - sg), or renormalised at the selected e
+            const float* lr = logits + (size_t)t * E;
+            float m = -INFINITY;
+            for (int e = lane; e < E; e += 32) m = fmaxf(m, lr[e]);
+            m = warp_max(m);
+            float s = 0.f;
+            for (int e = lane; e < E; e += 32) s += expf(lr[e] - m);
+            s = warp_sum(s);
+            for (int e = lane; e < E; e += 32) {
+                float gt = 0.f, wsel = 0.f;
+                bool sel = false;
+#pragma unroll
+                for (int j = 0; j < KK; ++j)
+                    if (j < k && ids[j] == e) { gt = gj[j]; wsel = wj[j]; sel = true; }
+                const float dl = renorm ? (sel ? wsel * (gt - sg) : 0.f) : (expf(lr[e] - m) / s) * (gt - sg);
+                sdl[q * E + e] = dl;
+                dlogit[(size_t)t * E + e] = dl;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < KK; ++j) rows[q][j] = -1;
+            for (int e = lane; e < E; e += 32) sdl[q * E + e] = 0.f;
+        }
     }
     __syncwarp();
     const int nvec = d / V;
     for (int v = lane; v < nvec; v += 32) {
-        float acc[V];
+        float acc[kTPW][V];
+        uint4 raw[kTPW][KK];
 #pragma unroll
-        for (int q = 0; q < V; ++q) acc[q] = 0.f;
+        for (int q = 0; q < kTPW; ++q)
 #pragma unroll
-        for (int j = 0; j < kMaxK; ++j) {
-            if (j < k && rows[j] >= 0) {
-                float f[V];
-                unpack16<Elt>(ld_nc_v4(reinterpret_cast<const uint4*>(dxe + (size_t)rows[j] * d) + v), f);
+            for (int j = 0; j < KK; ++j)
+                if (rows[q][j] >= 0)
+                    raw[q][j] = ld_nc_v4(reinterpret_cast<const uint4*>(dxe + (size_t)rows[q][j] * d) + v);
 #pragma unroll
-                for (int q = 0; q < V; ++q) acc[q] += f[q];
+        for (int q = 0; q < kTPW; ++q) {
+#pragma unroll
+            for (int i = 0; i < V; ++i) acc[q][i] = 0.f;
+#pragma unroll
+            for (int j = 0; j < KK; ++j) {
+                if (rows[q][j] >= 0) {
+                    float f[V];
+                    unpack16<Elt>(raw[q][j], f);
+#pragma unroll
+                    for (int i = 0; i < V; ++i) acc[q][i] += f[i];
+                }
             }
         }
-        // gate term: sum_e dlogit_e Wg[i][e], Wg read transposed ([E][d]) so lanes are coalesced
+        // gate term: sum_e dlogit_e Wg[i][e]; Wg read transposed ([E][d]) so lanes coalesce
         for (int e = 0; e < E; ++e) {
-            const float sv = sdl[e];
             const float4* wt = reinterpret_cast<const float4*>(wgT + (size_t)e * d + (size_t)v * V);
+            float wv[V];
 #pragma unroll
             for (int h = 0; h < V / 4; ++h) {
                 const float4 w4 = __ldg(wt + h);
-                acc[4 * h + 0] = fmaf(sv, w4.x, acc[4 * h + 0]);
-                acc[4 * h + 1] = fmaf(sv, w4.y, acc[4 * h + 1]);
-                acc[4 * h + 2] = fmaf(sv, w4.z, acc[4 * h + 2]);
-                acc[4 * h + 3] = fmaf(sv, w4.w, acc[4 * h + 3]);
+                wv[4 * h] = w4.x; wv[4 * h + 1] = w4.y; wv[4 * h + 2] = w4.z; wv[4 * h + 3] = w4.w;
+            }
+#pragma unroll
+            for (int q = 0; q < kTPW; ++q) {
+                const float sv = sdl[q * E + e];
+#pragma unroll
+                for (int i = 0; i < V; ++i) acc[q][i] = fmaf(sv, wv[i], acc[q][i]);
             }
         }
-        st_v4(reinterpret_cast<uint4*>(dx + (size_t)t * d) + v, pack16<Elt>(acc));
+#pragma unroll
+        for (int q = 0; q < kTPW; ++q)
+            if (valid[q]) st_v4(reinterpret_cast<uint4*>(dx + (size_t)(tb + q) * d) + v, pack16<Elt>(acc[q]));
     }
 }
 
-constexpr int kDwgTok = 128;     // tokens per partial block
-constexpr int kDwgThreads = 128; // each thread owns 4 consecutive dims -> 512 dims per block
+constexpr int kDwgTok = 64;      // tokens per partial block
+constexpr int kDwgThreads = 256; // each thread owns 4 consecutive dims -> 1024 dims per block
 constexpr int kDwgE = 8;         // experts per pass (32 accumulators per thread)
+constexpr int kDwgU = 8;         // tokens whose loads are in flight together
 
 template <typename Elt>
 __global__ void __launch_bounds__(kDwgThreads)
@@ -296,24 +341,35 @@ dwg_partial_kernel(const Elt* __restrict__ x, const float* __restrict__ dlogit, 
     for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int c = 0; c < kDwgE; ++c) acc[a][c] = 0.f;
-#pragma unroll 4
-    for (int t = tbeg; t < tend; ++t) {
-        float xv[4];
-        if constexpr (sizeof(Elt) == 2) {
-            const uint2 raw = __ldg(reinterpret_cast<const uint2*>(x + (size_t)t * d + i0));
-            xv[0] = __uint_as_float(raw.x << 16); xv[1] = __uint_as_float(raw.x & 0xffff0000u);
-            xv[2] = __uint_as_float(raw.y << 16); xv[3] = __uint_as_float(raw.y & 0xffff0000u);
-        } else {
-            const float4 f4 = __ldg(reinterpret_cast<const float4*>(x + (size_t)t * d + i0));
-            xv[0] = f4.x; xv[1] = f4.y; xv[2] = f4.z; xv[3] = f4.w;
+    for (int tt = tbeg; tt < tend; tt += kDwgU) {
+        float xv[kDwgU][4];
+#pragma unroll
+        for (int u = 0; u < kDwgU; ++u) {
+            const int t = tt + u;
+            if (t < tend) {
+                if constexpr (sizeof(Elt) == 2) {
+                    const uint2 raw = __ldg(reinterpret_cast<const uint2*>(x + (size_t)t * d + i0));
+                    xv[u][0] = __uint_as_float(raw.x << 16); xv[u][1] = __uint_as_float(raw.x & 0xffff0000u);
+                    xv[u][2] = __uint_as_float(raw.y << 16); xv[u][3] = __uint_as_float(raw.y & 0xffff0000u);
+                } else {
+                    const float4 f4 = __ldg(reinterpret_cast<const float4*>(x + (size_t)t * d + i0));
+                    xv[u][0] = f4.x; xv[u][1] = f4.y; xv[u][2] = f4.z; xv[u][3] = f4.w;
+                }
+            } else {
+                xv[u][0] = xv[u][1] = xv[u][2] = xv[u][3] = 0.f;
+            }
         }
-        const float4 l0 = *reinterpret_cast<const float4*>(&sdl[t - tbeg][0]);
-        const float4 l1 = *reinterpret_cast<const float4*>(&sdl[t - tbeg][4]);
-        const float lv[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
+        for (int u = 0; u < kDwgU; ++u) {
+            if (tt + u >= tend) break;
+            const float4 l0 = *reinterpret_cast<const float4*>(&sdl[tt + u - tbeg][0]);
+            const float4 l1 = *reinterpret_cast<const float4*>(&sdl[tt + u - tbeg][4]);
+            const float lv[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
 #pragma unroll
-            for (int c = 0; c < kDwgE; ++c) acc[a][c] = fmaf(xv[a], lv[c], acc[a][c]);
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int c = 0; c < kDwgE; ++c) acc[a][c] = fmaf(xv[u][a], lv[c], acc[a][c]);
+        }
     }
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
@@ -328,9 +384,16 @@ __global__ void dwg_reduce_kernel(const float* __restrict__ partial, int nb, int
 {
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= d * E) return;
-    float s = 0.f;
-    for (int b = 0; b < nb; ++b) s += partial[(size_t)b * d * E + q];
-    dwg[q] = s;
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+    int b = 0;
+    for (; b + 4 <= nb; b += 4) {
+        s0 += partial[(size_t)b * d * E + q];
+        s1 += partial[(size_t)(b + 1) * d * E + q];
+        s2 += partial[(size_t)(b + 2) * d * E + q];
+        s3 += partial[(size_t)(b + 3) * d * E + q];
+    }
+    for (; b < nb; ++b) s0 += partial[(size_t)b * d * E + q];
+    dwg[q] = (s0 + s1) + (s2 + s3);
 }
 
 __global__ void transpose_f32_kernel(const float* __restrict__ in, int rows, int cols,
@@ -356,17 +419,27 @@ __global__ void zero_pads_kernel(char* __restrict__ buf, int row_bytes,
 }
 
 // ---- launchers ---------------------------------------------------------------------------
+// dispatch on KK = the smallest of {1, 2, 4, 8} >= k
+#define LANCET_DISPATCH_K(k, ...)                                             \
+    do {                                                                      \
+        if ((k) <= 1) { constexpr int KK = 1; __VA_ARGS__; }                  \
+        else if ((k) <= 2) { constexpr int KK = 2; __VA_ARGS__; }             \
+        else if ((k) <= 4) { constexpr int KK = 4; __VA_ARGS__; }             \
+        else { constexpr int KK = 8; __VA_ARGS__; }                           \
+    } while (0)
 
 int launch_permute(const DispatchArgs& a, const void* x, void* xs, bool is_bf16, cudaStream_t s)
 {
     const int tok_blocks = ceil_div(a.T, kWarpsPerBlock);
     const int grid = tok_blocks + a.E;
-    if (is_bf16)
-        permute_kernel<bf16><<<grid, 256, 0, s>>>((const bf16*)x, a.idx, a.slot, a.T, a.k, a.d,
-                                                 a.send_off, a.send_rows, (bf16*)xs, tok_blocks);
-    else
-        permute_kernel<float><<<grid, 256, 0, s>>>((const float*)x, a.idx, a.slot, a.T, a.k, a.d,
-                                                  a.send_off, a.send_rows, (float*)xs, tok_blocks);
+    LANCET_DISPATCH_K(a.k, {
+        if (is_bf16)
+            permute_kernel<bf16, KK><<<grid, 256, 0, s>>>((const bf16*)x, a.idx, a.slot, a.T, a.k, a.d,
+                                                         a.send_off, a.send_rows, (bf16*)xs, tok_blocks);
+        else
+            permute_kernel<float, KK><<<grid, 256, 0, s>>>((const float*)x, a.idx, a.slot, a.T, a.k, a.d,
+                                                          a.send_off, a.send_rows, (float*)xs, tok_blocks);
+    });
     return 1;
 }
 
@@ -375,12 +448,14 @@ int launch_combine(const DispatchArgs& a, const void* comb, void* y, int t0, int
 {
     if (t1 <= t0) return 0;
     const int grid = ceil_div(t1 - t0, kWarpsPerBlock);
-    if (is_bf16)
-        combine_kernel<bf16><<<grid, 256, 0, s>>>((const bf16*)comb, a.idx, a.slot, a.w, a.send_off,
-                                                 t0, t1, a.k, a.d, (bf16*)y);
-    else
-        combine_kernel<float><<<grid, 256, 0, s>>>((const float*)comb, a.idx, a.slot, a.w,
-                                                  a.send_off, t0, t1, a.k, a.d, (float*)y);
+    LANCET_DISPATCH_K(a.k, {
+        if (is_bf16)
+            combine_kernel<bf16, KK><<<grid, 256, 0, s>>>((const bf16*)comb, a.idx, a.slot, a.w, a.send_off,
+                                                         t0, t1, a.k, a.d, (bf16*)y);
+        else
+            combine_kernel<float, KK><<<grid, 256, 0, s>>>((const float*)comb, a.idx, a.slot, a.w,
+                                                          a.send_off, t0, t1, a.k, a.d, (float*)y);
+    });
     return 1;
 }
 
@@ -390,14 +465,16 @@ int launch_combine_bwd(const DispatchArgs& a, const void* dy, const void* comb, 
     const int tok_blocks = ceil_div(t1 - t0, kWarpsPerBlock);
     const int grid = tok_blocks + (zero_pads ? a.E : 0);
     if (grid == 0) return 0;
-    if (is_bf16)
-        combine_bwd_kernel<bf16><<<grid, 256, 0, s>>>((const bf16*)dy, (const bf16*)comb, a.idx,
-                                                     a.slot, a.w, a.send_off, a.send_rows, t0, t1,
-                                                     a.k, a.d, g, (bf16*)dcomb, tok_blocks);
-    else
-        combine_bwd_kernel<float><<<grid, 256, 0, s>>>((const float*)dy, (const float*)comb, a.idx,
-                                                      a.slot, a.w, a.send_off, a.send_rows, t0, t1,
-                                                      a.k, a.d, g, (float*)dcomb, tok_blocks);
+    LANCET_DISPATCH_K(a.k, {
+        if (is_bf16)
+            combine_bwd_kernel<bf16, KK><<<grid, 256, 0, s>>>((const bf16*)dy, (const bf16*)comb, a.idx,
+                                                             a.slot, a.w, a.send_off, a.send_rows, t0, t1,
+                                                             a.k, a.d, g, (bf16*)dcomb, tok_blocks);
+        else
+            combine_bwd_kernel<float, KK><<<grid, 256, 0, s>>>((const float*)dy, (const float*)comb, a.idx,
+                                                              a.slot, a.w, a.send_off, a.send_rows, t0, t1,
+                                                              a.k, a.d, g, (float*)dcomb, tok_blocks);
+    });
     return 1;
 }
 
@@ -412,16 +489,18 @@ int launch_unpermute_gate_bwd(const DispatchArgs& a, const void* dxe, const floa
                               float* dlogit, int t0, int t1, bool is_bf16, cudaStream_t s)
 {
     if (t1 <= t0) return 0;
-    const int grid = ceil_div(t1 - t0, kWarpsPerBlock);
-    const size_t smem = sizeof(float) * kWarpsPerBlock * a.E;
-    if (is_bf16)
-        unpermute_gate_bwd_kernel<bf16><<<grid, 256, smem, s>>>(
-            (const bf16*)dxe, a.idx, a.slot, a.w, g, logits, wgT, a.send_off, renorm, t0, t1, a.k,
-            a.d, a.E, (bf16*)dx, dlogit);
-    else
-        unpermute_gate_bwd_kernel<float><<<grid, 256, smem, s>>>(
-            (const float*)dxe, a.idx, a.slot, a.w, g, logits, wgT, a.send_off, renorm, t0, t1, a.k,
-            a.d, a.E, (float*)dx, dlogit);
+    const int grid = ceil_div(t1 - t0, kWarpsPerBlock * kTPW);
+    const size_t smem = sizeof(float) * kWarpsPerBlock * kTPW * a.E;
+    LANCET_DISPATCH_K(a.k, {
+        if (is_bf16)
+            unpermute_gate_bwd_kernel<bf16, KK><<<grid, 256, smem, s>>>(
+                (const bf16*)dxe, a.idx, a.slot, a.w, g, logits, wgT, a.send_off, renorm, t0, t1, a.k,
+                a.d, a.E, (bf16*)dx, dlogit);
+        else
+            unpermute_gate_bwd_kernel<float, KK><<<grid, 256, smem, s>>>(
+                (const float*)dxe, a.idx, a.slot, a.w, g, logits, wgT, a.send_off, renorm, t0, t1, a.k,
+                a.d, a.E, (float*)dx, dlogit);
+    });
     return 1;
 }
 

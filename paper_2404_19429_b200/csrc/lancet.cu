@@ -761,21 +761,30 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
           L += launch_combine_bwd(da, dy, comb, c->g, c->dcomb, 0, T, true, c->bf16, s); }
         CHECK_LAUNCH();
         const void* dxe = c->dcomb;
+        const int max_rows = round_up(c->C, kRowAlign);
         if (!ident) {
-            const int max_rows = round_up(c->C, kRowAlign);
             st = expert_backward_dx(c, c->dcomb, c->send_rows, c->send_off, E, max_rows, s, -1, &L);
-            if (st) return st;
-            st = expert_backward_dw(c, c->dcomb, c->send_rows, c->send_off, E, dw1, dw2, 0, s, -1, &L);
             if (st) return st;
             dxe = c->dXe;
         }
-        { OpScope op(c, "unpermute_gate_bwd", 0, -1, s);
-          L += launch_wg_transpose(c->wg, d, E, c->wgT, s);
-          L += launch_unpermute_gate_bwd(da, dxe, c->g, c->logits, c->wgT, renorm, dx, c->dlogit, 0, T, c->bf16, s); }
+        // K6 + K7 need only dX: run them on a second stream beside the dW GEMMs (the weight
+        // gradients have no consumer inside the layer)
+        cudaStream_t sa = c->s_comm;
+        CK(cudaEventRecord(c->ev_fork, s));
+        CK(cudaStreamWaitEvent(sa, c->ev_fork, 0));
+        { OpScope op(c, "unpermute_gate_bwd", 2, -1, sa);
+          L += launch_wg_transpose(c->wg, d, E, c->wgT, sa);
+          L += launch_unpermute_gate_bwd(da, dxe, c->g, c->logits, c->wgT, renorm, dx, c->dlogit, 0, T, c->bf16, sa); }
         CHECK_LAUNCH();
-        { OpScope op(c, "gate_dwg", 0, -1, s);
-          L += launch_dwg(c->x, c->dlogit, T, d, E, c->dwg_partial, dwg, c->bf16, s); }
+        { OpScope op(c, "gate_dwg", 2, -1, sa);
+          L += launch_dwg(c->x, c->dlogit, T, d, E, c->dwg_partial, dwg, c->bf16, sa); }
         CHECK_LAUNCH();
+        CK(cudaEventRecord(c->ev_join, sa));
+        if (!ident) {
+            st = expert_backward_dw(c, c->dcomb, c->send_rows, c->send_off, E, dw1, dw2, 0, s, -1, &L);
+            if (st) return st;
+        }
+        CK(cudaStreamWaitEvent(s, c->ev_join, 0));
         return LANCET_OK;
     }
 

@@ -27,7 +27,9 @@ struct GateGeom {
     int tpt;       // threads per token = E / ce
     int TB;        // tokens per block
     int threads;   // TB * tpt
-    size_t smem;
+    int dt;        // dims per staged tile
+    int row_bytes; // bytes per staged x row
+    size_t buf_bytes, smem;
 };
 
 __host__ __device__ inline GateGeom gate_geom(int E, int elt_bytes)
@@ -39,8 +41,14 @@ __host__ __device__ inline GateGeom gate_geom(int E, int elt_bytes)
     if (g.TB > kGateMaxTB) g.TB = kGateMaxTB;
     if (g.TB < 1) g.TB = 1;
     g.threads = g.TB * g.tpt;
-    const size_t row = (size_t)kGateDT * elt_bytes + 16;           // +16 B: no bank conflicts
-    const size_t xs = 2 * (size_t)g.TB * row;
+    // d-tile: 256 dims, fewer when the Wg tile (DT x E fp32) would exceed 16 KiB
+    int dt = 4096 / E;
+    dt = dt > kGateDT ? kGateDT : dt;
+    dt = dt < 8 ? 8 : (dt & ~7);
+    g.dt = dt;
+    g.row_bytes = dt * elt_bytes + 16;                              // +16 B: fewer bank conflicts
+    g.buf_bytes = (size_t)g.TB * g.row_bytes + (size_t)dt * E * 4;
+    const size_t xs = 2 * g.buf_bytes;
     const size_t lg = sizeof(float) * (size_t)g.TB * E;
     g.smem = xs > lg ? xs : lg;
     return g;
@@ -57,21 +65,27 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 template <typename Elt>
-__device__ __forceinline__ void gate_load_tile(const Elt* __restrict__ x, int T, int d, int t0, int TB,
-                                               int i0, uint8_t* buf, int row_bytes)
+__device__ __forceinline__ void gate_load_tile(const Elt* __restrict__ x, const float* __restrict__ wg,
+                                               int T, int d, int E, int t0, const GateGeom& geo,
+                                               int i0, uint8_t* buf)
 {
-    const int ilim = min(kGateDT, d - i0);
-    const int cpr = ilim * (int)sizeof(Elt) / 16;                 // 16-byte chunks per row
-    for (int q = threadIdx.x; q < TB * cpr; q += blockDim.x) {
+    const int ilim = min(geo.dt, d - i0);
+    const int cpr = ilim * (int)sizeof(Elt) / 16;                 // 16-byte chunks per x row
+    for (int q = threadIdx.x; q < geo.TB * cpr; q += blockDim.x) {
         const int r = q / cpr, c = q % cpr, t = t0 + r;
         if (t < T)
-            cp_async16(buf + (size_t)r * row_bytes + c * 16,
+            cp_async16(buf + (size_t)r * geo.row_bytes + c * 16,
                        reinterpret_cast<const uint8_t*>(x + (size_t)t * d + i0) + c * 16);
     }
+    // Wg rows [i0, i0 + ilim) x E (contiguous in global memory)
+    uint8_t* wb = buf + (size_t)geo.TB * geo.row_bytes;
+    const int wchunks = ilim * E * 4 / 16;
+    const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(wg + (size_t)i0 * E);
+    for (int q = threadIdx.x; q < wchunks; q += blockDim.x) cp_async16(wb + q * 16, wsrc + q * 16);
 }
 
-// K1.  Thread (token r, experts e0..e0+CE-1) runs CE independent R1 chains; x tiles of 256 dims
-// stream through shared memory (cp.async double buffer), Wg rows come through L1 (__ldg).
+// K1.  Thread (token r, experts e0..e0+CE-1) runs CE independent R1 chains; tiles of x and of
+// Wg stream through shared memory (cp.async, double-buffered).
 template <typename Elt, int CE>
 __global__ void __launch_bounds__(kGateThreadCap)
 gate_topk_kernel(const Elt* __restrict__ x, const float* __restrict__ wg, int T, int d, int E,
@@ -82,9 +96,8 @@ gate_topk_kernel(const Elt* __restrict__ x, const float* __restrict__ wg, int T,
     __shared__ int sh_hist[2 * kMaxExperts];
     const GateGeom geo = gate_geom(E, sizeof(Elt));
     const int TB = geo.TB;
-    const int row_bytes = kGateDT * sizeof(Elt) + 16;
     uint8_t* buf0 = gsm;
-    uint8_t* buf1 = gsm + (size_t)TB * row_bytes;
+    uint8_t* buf1 = gsm + geo.buf_bytes;
     const int tid = threadIdx.x;
     const int r = tid / geo.tpt;                      // token within block
     const int e0 = (tid % geo.tpt) * CE;
@@ -97,32 +110,31 @@ gate_topk_kernel(const Elt* __restrict__ x, const float* __restrict__ wg, int T,
 #pragma unroll
     for (int c = 0; c < CE; ++c) acc[c] = 0.f;
 
-    const int ntiles = ceil_div(d, kGateDT);
-    gate_load_tile(x, T, d, t0, TB, 0, buf0, row_bytes);
+    const int ntiles = ceil_div(d, geo.dt);
+    gate_load_tile(x, wg, T, d, E, t0, geo, 0, buf0);
     cp_async_commit();
     for (int it = 0; it < ntiles; ++it) {
         uint8_t* cur = (it & 1) ? buf1 : buf0;
         uint8_t* nxt = (it & 1) ? buf0 : buf1;
-        if (it + 1 < ntiles) gate_load_tile(x, T, d, t0, TB, (it + 1) * kGateDT, nxt, row_bytes);
+        if (it + 1 < ntiles) gate_load_tile(x, wg, T, d, E, t0, geo, (it + 1) * geo.dt, nxt);
         cp_async_commit();
         cp_async_wait<1>();
         __syncthreads();
-        const int i0 = it * kGateDT;
-        const int ilim = min(kGateDT, d - i0);
+        const int ilim = min(geo.dt, d - it * geo.dt);
         if (active && t0 + r < T) {
-            const Elt* xr = reinterpret_cast<const Elt*>(cur + (size_t)r * row_bytes);
-            const float* wrow = wg + (size_t)i0 * E + e0;
-#pragma unroll 4
+            const Elt* xr = reinterpret_cast<const Elt*>(cur + (size_t)r * geo.row_bytes);
+            const float* ws = reinterpret_cast<const float*>(cur + (size_t)TB * geo.row_bytes) + e0;
+#pragma unroll 8
             for (int i = 0; i < ilim; ++i) {           // R1: increasing i, one fused step each
                 const float xv = to_f(xr[i]);
                 if constexpr (CE == 4) {
-                    const float4 w4 = __ldg(reinterpret_cast<const float4*>(wrow + (size_t)i * E));
+                    const float4 w4 = *reinterpret_cast<const float4*>(ws + i * E);
                     acc[0] = __fmaf_rn(xv, w4.x, acc[0]);
                     acc[1] = __fmaf_rn(xv, w4.y, acc[1]);
                     acc[2] = __fmaf_rn(xv, w4.z, acc[2]);
                     acc[3] = __fmaf_rn(xv, w4.w, acc[3]);
                 } else {
-                    acc[0] = __fmaf_rn(xv, __ldg(wrow + (size_t)i * E), acc[0]);
+                    acc[0] = __fmaf_rn(xv, ws[i * E], acc[0]);
                 }
             }
         }

@@ -279,7 +279,7 @@ def exposed_comm_us(timeline) -> dict:
                 out.append([a, b])
         return out
     comm = union([(r["start_us"], r["end_us"]) for r in timeline if r["lane"] == 1])
-    comp = union([(r["start_us"], r["end_us"]) for r in timeline if r["lane"] == 0])
+    comp = union([(r["start_us"], r["end_us"]) for r in timeline if r["lane"] != 1])
     tot_comm = sum(b - a for a, b in comm)
     overlap = 0.0
     for a, b in comm:
