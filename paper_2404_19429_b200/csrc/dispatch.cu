@@ -314,6 +314,148 @@ unpermute_gate_bwd_kernel(const Elt* __restrict__ dxe, const int* __restrict__ i
     }
 }
 
+// ---- K6 + K7 fused (E <= 8) --------------------------------------------------------------
+// Block = 64 tokens x 1024 dims.  Prologue: one warp per token computes dlogit (softmax
+// Jacobian, R3) into shared memory.  Main loop: thread owns 4 consecutive dims, keeps
+// Wg[i0..i0+3][0..E) and its dWg partial in registers, and streams the block's tokens:
+//   dx_t[i]  = sum_j dX[row_tj][i] + sum_e dlogit_te Wg[i][e]
+//   dWg[i][e] += x_t[i] dlogit_te        (partial per block; reduced by dwg_reduce_kernel)
+constexpr int kFTok = 64;
+constexpr int kFThreads = 256;
+constexpr int kFU = 4;           // tokens whose loads are in flight together
+
+template <typename Elt> struct Quad;                 // 4 consecutive elements
+template <> struct Quad<bf16> {
+    using T = uint2;
+    static __device__ __forceinline__ void unpack(T v, float* f) {
+        f[0] = __uint_as_float(v.x << 16); f[1] = __uint_as_float(v.x & 0xffff0000u);
+        f[2] = __uint_as_float(v.y << 16); f[3] = __uint_as_float(v.y & 0xffff0000u);
+    }
+    static __device__ __forceinline__ T pack(const float* f) {
+        __nv_bfloat162 a = __floats2bfloat162_rn(f[0], f[1]), b = __floats2bfloat162_rn(f[2], f[3]);
+        return make_uint2(*reinterpret_cast<uint32_t*>(&a), *reinterpret_cast<uint32_t*>(&b));
+    }
+};
+template <> struct Quad<float> {
+    using T = uint4;
+    static __device__ __forceinline__ void unpack(T v, float* f) {
+        f[0] = __uint_as_float(v.x); f[1] = __uint_as_float(v.y);
+        f[2] = __uint_as_float(v.z); f[3] = __uint_as_float(v.w);
+    }
+    static __device__ __forceinline__ T pack(const float* f) {
+        return make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]), __float_as_uint(f[2]), __float_as_uint(f[3]));
+    }
+};
+
+template <typename Elt, int KK>
+__global__ void __launch_bounds__(kFThreads)
+gate_bwd_fused_kernel(const Elt* __restrict__ dxe, const Elt* __restrict__ x,
+                      const int* __restrict__ idx, const int* __restrict__ slot,
+                      const float* __restrict__ wts, const float* __restrict__ g,
+                      const float* __restrict__ logits, const float* __restrict__ wg,
+                      const int* __restrict__ send_off, int renorm, int t0, int t1, int k, int d,
+                      int E, Elt* __restrict__ dx, float* __restrict__ partial, int pbase)
+{
+    using Q = Quad<Elt>;
+    __shared__ float sdl[kFTok][8];
+    __shared__ int srow[kFTok][KK];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tb = t0 + blockIdx.x * kFTok;
+    const int tn = min(kFTok, t1 - tb);
+    for (int q = w; q < kFTok; q += kFThreads / 32) {
+        const int t = tb + q;
+        if (q >= tn) {
+            if (lane < 8) sdl[q][lane] = 0.f;
+            if (lane < KK) srow[q][lane] = -1;
+            continue;
+        }
+        int rows[KK], ids[KK];
+        float wj[KK];
+        load_choices<KK>(idx, slot, wts, send_off, t, k, lane, rows, wj, ids);
+        const float myg = lane < k ? g[(size_t)t * k + lane] : 0.f;
+        float gj[KK];
+        float sg = 0.f;
+#pragma unroll
+        for (int j = 0; j < KK; ++j) {
+            gj[j] = __shfl_sync(0xffffffffu, myg, j);
+            if (j < k) sg = fmaf(gj[j], wj[j], sg);
+        }
+        const float* lr = logits + (size_t)t * E;
+        const float l = lane < E ? lr[lane] : -INFINITY;
+        const float m = warp_max(l);
+        const float ex = lane < E ? expf(l - m) : 0.f;
+        const float s = warp_sum(ex);
+        float gt = 0.f, wsel = 0.f;
+        bool sel = false;
+#pragma unroll
+        for (int j = 0; j < KK; ++j)
+            if (j < k && ids[j] == lane) { gt = gj[j]; wsel = wj[j]; sel = true; }
+        const float dl = renorm ? (sel ? wsel * (gt - sg) : 0.f) : (ex / s) * (gt - sg);
+        if (lane < 8) sdl[q][lane] = lane < E ? dl : 0.f;
+        if (lane < KK) srow[q][lane] = rows[lane];
+    }
+    __syncthreads();
+    const int i0 = (blockIdx.y * kFThreads + threadIdx.x) * 4;
+    if (i0 >= d) return;
+    float wgr[4][8], acc[4][8];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            wgr[a][e] = e < E ? wg[(size_t)(i0 + a) * E + e] : 0.f;
+            acc[a][e] = 0.f;
+        }
+    for (int q0 = 0; q0 < tn; q0 += kFU) {
+        typename Q::T rx[kFU], rd[kFU][KK];
+#pragma unroll
+        for (int u = 0; u < kFU; ++u) {
+            const int q = q0 + u;
+            if (q < tn) {
+                rx[u] = __ldg(reinterpret_cast<const typename Q::T*>(x + (size_t)(tb + q) * d + i0));
+#pragma unroll
+                for (int j = 0; j < KK; ++j) {
+                    const int row = srow[q][j];
+                    if (row >= 0) rd[u][j] = __ldg(reinterpret_cast<const typename Q::T*>(dxe + (size_t)row * d + i0));
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kFU; ++u) {
+            const int q = q0 + u;
+            if (q >= tn) break;
+            float dl[8];
+            const float4 l0 = *reinterpret_cast<const float4*>(&sdl[q][0]);
+            const float4 l1 = *reinterpret_cast<const float4*>(&sdl[q][4]);
+            dl[0] = l0.x; dl[1] = l0.y; dl[2] = l0.z; dl[3] = l0.w;
+            dl[4] = l1.x; dl[5] = l1.y; dl[6] = l1.z; dl[7] = l1.w;
+            float o[4] = {0.f, 0.f, 0.f, 0.f}, xf[4];
+#pragma unroll
+            for (int j = 0; j < KK; ++j) {
+                if (srow[q][j] >= 0) {
+                    float f[4];
+                    Q::unpack(rd[u][j], f);
+#pragma unroll
+                    for (int a = 0; a < 4; ++a) o[a] += f[a];
+                }
+            }
+            Q::unpack(rx[u], xf);
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    o[a] = fmaf(dl[e], wgr[a][e], o[a]);
+                    acc[a][e] = fmaf(xf[a], dl[e], acc[a][e]);
+                }
+            *reinterpret_cast<typename Q::T*>(dx + (size_t)(tb + q) * d + i0) = Q::pack(o);
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        float* out = partial + ((size_t)(pbase + blockIdx.x) * d + i0 + a) * E;
+        for (int e = 0; e < E; ++e) out[e] = acc[a][e];
+    }
+}
+
 constexpr int kDwgTok = 64;      // tokens per partial block
 constexpr int kDwgThreads = 256; // each thread owns 4 consecutive dims -> 1024 dims per block
 constexpr int kDwgE = 8;         // experts per pass (32 accumulators per thread)
@@ -504,7 +646,37 @@ int launch_unpermute_gate_bwd(const DispatchArgs& a, const void* dxe, const floa
     return 1;
 }
 
-size_t dwg_partial_floats(int T, int d, int E) { return (size_t)ceil_div(T, kDwgTok) * d * E; }
+size_t dwg_partial_floats(int T, int d, int E)
+{
+    return (size_t)(ceil_div(T, kDwgTok > kFTok ? kFTok : kDwgTok) + kMaxChunks) * d * E;
+}
+
+int launch_gate_bwd_fused(const DispatchArgs& a, const void* dxe, const void* x, const float* g,
+                          const float* logits, const float* wg, int renorm, void* dx, float* partial,
+                          int pbase, int t0, int t1, bool is_bf16, cudaStream_t s)
+{
+    if (t1 <= t0) return 0;
+    dim3 grid(ceil_div(t1 - t0, kFTok), ceil_div(a.d, kFThreads * 4));
+    LANCET_DISPATCH_K(a.k, {
+        if (is_bf16)
+            gate_bwd_fused_kernel<bf16, KK><<<grid, kFThreads, 0, s>>>(
+                (const bf16*)dxe, (const bf16*)x, a.idx, a.slot, a.w, g, logits, wg, a.send_off, renorm,
+                t0, t1, a.k, a.d, a.E, (bf16*)dx, partial, pbase);
+        else
+            gate_bwd_fused_kernel<float, KK><<<grid, kFThreads, 0, s>>>(
+                (const float*)dxe, (const float*)x, a.idx, a.slot, a.w, g, logits, wg, a.send_off, renorm,
+                t0, t1, a.k, a.d, a.E, (float*)dx, partial, pbase);
+    });
+    return 1;
+}
+
+int fused_partial_blocks(int t0, int t1) { return ceil_div(t1 - t0, kFTok); }
+
+int launch_dwg_reduce(const float* partial, int nb, int d, int E, float* dwg, cudaStream_t s)
+{
+    dwg_reduce_kernel<<<ceil_div(d * E, 256), 256, 0, s>>>(partial, nb, d, E, dwg);
+    return 1;
+}
 
 int launch_dwg(const void* x, const float* dlogit, int T, int d, int E, float* partial,
                float* dwg, bool is_bf16, cudaStream_t s)

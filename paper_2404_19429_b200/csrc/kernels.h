@@ -43,6 +43,13 @@ int launch_unpermute_gate_bwd(const DispatchArgs& a, const void* dxe, const floa
 int launch_dwg(const void* x, const float* dlogit, int T, int d, int E, float* partial,
                float* dwg, bool is_bf16, cudaStream_t s);
 size_t dwg_partial_floats(int T, int d, int E);
+// K6 + K7 fused (E <= 8): dx for tokens [t0, t1) and dWg partials in blocks
+// [pbase, pbase + fused_partial_blocks(t0, t1)) of `partial` ([blocks][d][E]).
+int launch_gate_bwd_fused(const DispatchArgs& a, const void* dxe, const void* x, const float* g,
+                          const float* logits, const float* wg, int renorm, void* dx, float* partial,
+                          int pbase, int t0, int t1, bool is_bf16, cudaStream_t s);
+int fused_partial_blocks(int t0, int t1);
+int launch_dwg_reduce(const float* partial, int nb, int d, int E, float* dwg, cudaStream_t s);
 // zero rows [off_g + rows_g, off_g + round_up(rows_g, 128)) of a packed buffer
 int launch_zero_pads(void* buf, int row_elems, const int* grp_off, const int* grp_rows,
                      int n_groups, int elt_bytes, cudaStream_t s);

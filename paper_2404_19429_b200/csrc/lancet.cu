@@ -403,6 +403,47 @@ struct Plan {
     }
 };
 
+// K6 + K7 for the tokens of chunk cc of nc (nc == 1: all tokens): dx (expert path + gate
+// term) and, after the last chunk, dWg.  E <= 8 uses the fused kernel (dWg partials per
+// 64-token block, `*pbase` counts them across chunks); larger E the two-kernel path.
+lancet_status gate_backward(lancet_ctx* c, const DispatchArgs& da, const void* dxe, void* dx,
+                            float* dwg, int renorm, cudaStream_t s, int cc, int nc, int* L,
+                            int* pbase = nullptr)
+{
+    const int T = c->T, d = c->cfg.d_model, E = c->cfg.n_experts;
+    const int t0 = chunk_start(T, nc, cc), t1 = chunk_start(T, nc, cc + 1);
+    int pb_local = 0;
+    int* pb = pbase ? pbase : &pb_local;
+    if (cc == 0) *pb = 0;
+    if (E <= 8) {
+        {
+            OpScope op(c, "gate_bwd_fused", 0, nc > 1 ? cc : -1, s);
+            *L += launch_gate_bwd_fused(da, dxe, c->x, c->g, c->logits, c->wg, renorm, dx,
+                                        c->dwg_partial, *pb, t0, t1, c->bf16, s);
+            *pb += fused_partial_blocks(t0, t1);
+        }
+        CHECK_LAUNCH();
+        if (cc == nc - 1) {
+            OpScope op(c, "gate_dwg_reduce", 0, -1, s);
+            *L += launch_dwg_reduce(c->dwg_partial, *pb, d, E, dwg, s);
+        }
+    } else {
+        {
+            OpScope op(c, "unpermute_gate_bwd", 0, nc > 1 ? cc : -1, s);
+            if (cc == 0) *L += launch_wg_transpose(c->wg, d, E, c->wgT, s);
+            *L += launch_unpermute_gate_bwd(da, dxe, c->g, c->logits, c->wgT, renorm, dx, c->dlogit,
+                                            t0, t1, c->bf16, s);
+        }
+        CHECK_LAUNCH();
+        if (cc == nc - 1) {
+            OpScope op(c, "gate_dwg", 0, -1, s);
+            *L += launch_dwg(c->x, c->dlogit, T, d, E, c->dwg_partial, dwg, c->bf16, s);
+        }
+    }
+    CHECK_LAUNCH();
+    return LANCET_OK;
+}
+
 __global__ void send_counts_kernel(const int* __restrict__ S, int E, int n, int* __restrict__ out)
 {
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
@@ -767,25 +808,12 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
             if (st) return st;
             dxe = c->dXe;
         }
-        // K6 + K7 need only dX: run them on a second stream beside the dW GEMMs (the weight
-        // gradients have no consumer inside the layer)
-        cudaStream_t sa = c->s_comm;
-        CK(cudaEventRecord(c->ev_fork, s));
-        CK(cudaStreamWaitEvent(sa, c->ev_fork, 0));
-        { OpScope op(c, "unpermute_gate_bwd", 2, -1, sa);
-          L += launch_wg_transpose(c->wg, d, E, c->wgT, sa);
-          L += launch_unpermute_gate_bwd(da, dxe, c->g, c->logits, c->wgT, renorm, dx, c->dlogit, 0, T, c->bf16, sa); }
-        CHECK_LAUNCH();
-        { OpScope op(c, "gate_dwg", 2, -1, sa);
-          L += launch_dwg(c->x, c->dlogit, T, d, E, c->dwg_partial, dwg, c->bf16, sa); }
-        CHECK_LAUNCH();
-        CK(cudaEventRecord(c->ev_join, sa));
         if (!ident) {
             st = expert_backward_dw(c, c->dcomb, c->send_rows, c->send_off, E, dw1, dw2, 0, s, -1, &L);
             if (st) return st;
         }
-        CK(cudaStreamWaitEvent(s, c->ev_join, 0));
-        return LANCET_OK;
+        st = gate_backward(c, da, dxe, dx, dwg, renorm, s, 0, 1, &L);
+        return st;
     }
 
     // ---- expert parallel (S2) ---------------------------------------------------------------
@@ -813,7 +841,6 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
     };
     // pads of the received dO rows must be zero (K-grouped dW reads whole 128-row blocks)
     L += launch_zero_pads(c->dout, d, d_grp_off, d_grp_rows, n * E_l, (int)c->elt, sc);
-    L += launch_wg_transpose(c->wg, d, E, c->wgT, sc);
     const void* comb = c->comb;     // o_tj returned by the combine all-to-all (source side)
     std::vector<cudaEvent_t> ev_k5(nc), ev_b1(nc), ev_dx(nc), ev_b2(nc);
     for (int cc = 0; cc < nc; ++cc) {
@@ -907,17 +934,12 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
             if (st) return st;
         }
     }
+    int pbase = 0;
     for (int cc = 0; cc < nc; ++cc) {
-        int t0, t1;
-        tok_range(cc, t0, t1);
         CK(cudaStreamWaitEvent(sc, ev_b2[cc], 0));
-        OpScope op(c, "unpermute_gate_bwd", 0, serial ? -1 : cc, sc);
-        L += launch_unpermute_gate_bwd(da, dxcomb, c->g, c->logits, c->wgT, renorm, dx, c->dlogit, t0, t1, c->bf16, sc);
+        st = gate_backward(c, da, dxcomb, dx, dwg, renorm, sc, cc, nc, &L, &pbase);
+        if (st) return st;
     }
-    CHECK_LAUNCH();
-    { OpScope op(c, "gate_dwg", 0, -1, sc);
-      L += launch_dwg(c->x, c->dlogit, T, d, E, c->dwg_partial, dwg, c->bf16, sc); }
-    CHECK_LAUNCH();
     CK(cudaEventRecord(c->ev_join, sc));
     CK(cudaStreamWaitEvent(s, c->ev_join, 0));
     if (sm != sc) {

@@ -35,7 +35,7 @@ struct GateGeom {
 __host__ __device__ inline GateGeom gate_geom(int E, int elt_bytes)
 {
     GateGeom g;
-    g.ce = (E % 4 == 0) ? 4 : 1;
+    g.ce = (E % 8 == 0) ? 8 : ((E % 4 == 0) ? 4 : 1);
     g.tpt = E / g.ce;
     g.TB = kGateThreadCap / g.tpt;
     if (g.TB > kGateMaxTB) g.TB = kGateMaxTB;
@@ -124,17 +124,46 @@ gate_topk_kernel(const Elt* __restrict__ x, const float* __restrict__ wg, int T,
         if (active && t0 + r < T) {
             const Elt* xr = reinterpret_cast<const Elt*>(cur + (size_t)r * geo.row_bytes);
             const float* ws = reinterpret_cast<const float*>(cur + (size_t)TB * geo.row_bytes) + e0;
+            if constexpr (CE >= 4 && sizeof(Elt) == 2) {
+                // two x values per 32-bit shared load; CE/4 float4 Wg loads per i
+                const uint32_t* xp = reinterpret_cast<const uint32_t*>(xr);
+#pragma unroll 4
+                for (int i = 0; i < ilim; i += 2) {    // R1: increasing i, one fused step each
+                    const uint32_t pr = xp[i >> 1];
+                    const float xa = __uint_as_float(pr << 16), xb = __uint_as_float(pr & 0xffff0000u);
+#pragma unroll
+                    for (int h = 0; h < CE / 4; ++h) {
+                        const float4 w4 = *reinterpret_cast<const float4*>(ws + i * E + 4 * h);
+                        acc[4 * h + 0] = __fmaf_rn(xa, w4.x, acc[4 * h + 0]);
+                        acc[4 * h + 1] = __fmaf_rn(xa, w4.y, acc[4 * h + 1]);
+                        acc[4 * h + 2] = __fmaf_rn(xa, w4.z, acc[4 * h + 2]);
+                        acc[4 * h + 3] = __fmaf_rn(xa, w4.w, acc[4 * h + 3]);
+                    }
+#pragma unroll
+                    for (int h = 0; h < CE / 4; ++h) {
+                        const float4 w4 = *reinterpret_cast<const float4*>(ws + (i + 1) * E + 4 * h);
+                        acc[4 * h + 0] = __fmaf_rn(xb, w4.x, acc[4 * h + 0]);
+                        acc[4 * h + 1] = __fmaf_rn(xb, w4.y, acc[4 * h + 1]);
+                        acc[4 * h + 2] = __fmaf_rn(xb, w4.z, acc[4 * h + 2]);
+                        acc[4 * h + 3] = __fmaf_rn(xb, w4.w, acc[4 * h + 3]);
+                    }
+                }
+            } else {
 #pragma unroll 8
-            for (int i = 0; i < ilim; ++i) {           // R1: increasing i, one fused step each
-                const float xv = to_f(xr[i]);
-                if constexpr (CE == 4) {
-                    const float4 w4 = *reinterpret_cast<const float4*>(ws + i * E);
-                    acc[0] = __fmaf_rn(xv, w4.x, acc[0]);
-                    acc[1] = __fmaf_rn(xv, w4.y, acc[1]);
-                    acc[2] = __fmaf_rn(xv, w4.z, acc[2]);
-                    acc[3] = __fmaf_rn(xv, w4.w, acc[3]);
-                } else {
-                    acc[0] = __fmaf_rn(xv, ws[i * E], acc[0]);
+                for (int i = 0; i < ilim; ++i) {       // R1: increasing i, one fused step each
+                    const float xv = to_f(xr[i]);
+                    if constexpr (CE >= 4) {
+#pragma unroll
+                        for (int h = 0; h < CE / 4; ++h) {
+                            const float4 w4 = *reinterpret_cast<const float4*>(ws + i * E + 4 * h);
+                            acc[4 * h + 0] = __fmaf_rn(xv, w4.x, acc[4 * h + 0]);
+                            acc[4 * h + 1] = __fmaf_rn(xv, w4.y, acc[4 * h + 1]);
+                            acc[4 * h + 2] = __fmaf_rn(xv, w4.z, acc[4 * h + 2]);
+                            acc[4 * h + 3] = __fmaf_rn(xv, w4.w, acc[4 * h + 3]);
+                        }
+                    } else {
+                        acc[0] = __fmaf_rn(xv, ws[i * E], acc[0]);
+                    }
                 }
             }
         }
@@ -297,6 +326,8 @@ int launch_routing(const RouteArgs& a, bool is_bf16, cudaStream_t s)
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(gate_topk_kernel<bf16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(gate_topk_kernel<bf16, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(gate_topk_kernel<float, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaFuncSetAttribute(gate_topk_kernel<bf16, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaFuncSetAttribute(gate_topk_kernel<float, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaFuncSetAttribute(gate_topk_kernel<float, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -308,10 +339,12 @@ int launch_routing(const RouteArgs& a, bool is_bf16, cudaStream_t s)
     const int thr = round_up(g.threads, 32);
 #define GATE_ARGS a.T, a.d, a.E, a.k, a.renorm, a.logits, a.idx, a.w, a.hist, n_tiles
     if (is_bf16) {
-        if (g.ce == 4) gate_topk_kernel<bf16, 4><<<blocks, thr, g.smem, s>>>((const bf16*)a.x, a.wg, GATE_ARGS);
+        if (g.ce == 8) gate_topk_kernel<bf16, 8><<<blocks, thr, g.smem, s>>>((const bf16*)a.x, a.wg, GATE_ARGS);
+        else if (g.ce == 4) gate_topk_kernel<bf16, 4><<<blocks, thr, g.smem, s>>>((const bf16*)a.x, a.wg, GATE_ARGS);
         else gate_topk_kernel<bf16, 1><<<blocks, thr, g.smem, s>>>((const bf16*)a.x, a.wg, GATE_ARGS);
     } else {
-        if (g.ce == 4) gate_topk_kernel<float, 4><<<blocks, thr, g.smem, s>>>((const float*)a.x, a.wg, GATE_ARGS);
+        if (g.ce == 8) gate_topk_kernel<float, 8><<<blocks, thr, g.smem, s>>>((const float*)a.x, a.wg, GATE_ARGS);
+        else if (g.ce == 4) gate_topk_kernel<float, 4><<<blocks, thr, g.smem, s>>>((const float*)a.x, a.wg, GATE_ARGS);
         else gate_topk_kernel<float, 1><<<blocks, thr, g.smem, s>>>((const float*)a.x, a.wg, GATE_ARGS);
     }
 #undef GATE_ARGS

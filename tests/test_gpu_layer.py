@@ -146,3 +146,15 @@ def test_tcgen05_gemm_matches_simt_gemm(T, d, f, E, k, n):
     o = run_oracle(ins, k, 1.0, n)
     for key in ("y", "dx", "dwg", "dw1", "dw2"):
         assert normwise(tc[key], o[key]) <= TOL["bf16"], key
+
+
+@pytest.mark.parametrize("E,k", [(16, 2), (4, 1), (8, 4)])
+def test_gate_backward_paths(E, k):
+    # E <= 8: fused K6+K7 kernel; E > 8: two-kernel path (transposed Wg + dWg reduction)
+    T, d, f = 900, 128, 256
+    ins = inputs(T, d, f, E, k, beta=0.5, seed=E * 10 + k)
+    g = run_gpu(ins, E, k, 1.0, 3)
+    o = run_oracle(ins, k, 1.0, 3)
+    assert_routing_exact(g, o)
+    for key in ("y", "dx", "dwg", "dw1", "dw2"):
+        assert normwise(g[key], o[key]) <= TOL["bf16"], key
