@@ -364,6 +364,9 @@ def run_lancet(a, world, rank, local_rank):
             kernels[o] = {"us": ops[o]["us_per_step"],
                           "gbs": b / (ops[o]["us_per_step"] * 1e-6) / 1e9,
                           "hbm_frac": b / (ops[o]["us_per_step"] * 1e-6) / 1e9 / pk["hbm"]}
+    for o, v in ops.items():
+        if o not in kernels:
+            kernels[o] = {"us": v["us_per_step"]}
     del tk
 
     out = {

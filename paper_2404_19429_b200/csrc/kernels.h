@@ -36,20 +36,15 @@ int launch_combine(const DispatchArgs& a, const void* comb, void* y, int t0, int
 int launch_combine_bwd(const DispatchArgs& a, const void* dy, const void* comb, float* g,
                        void* dcomb, int t0, int t1, bool zero_pads, bool is_bf16, cudaStream_t s);
 int launch_wg_transpose(const float* wg, int d, int E, float* wgT, cudaStream_t s);
+bool gate_bwd_needs_wgT(int d, int E);   // true: K6 reads Wg^T from global (too big for smem)
 int launch_unpermute_gate_bwd(const DispatchArgs& a, const void* dxe, const float* g,
-                              const float* logits, const float* wgT, int renorm, void* dx,
-                              float* dlogit, int t0, int t1, bool is_bf16, cudaStream_t s);
-// dWg = x^T dlogit (K7); partial: [ceil(T/128)][d][E] fp32 scratch
+                              const float* logits, const float* wg, const float* wgT, int renorm,
+                              void* dx, float* dlogit, int t0, int t1, int num_sms, bool is_bf16,
+                              cudaStream_t s);
+// dWg = x^T dlogit (K7); partial: [ceil(T/64)][d][E] fp32 scratch
 int launch_dwg(const void* x, const float* dlogit, int T, int d, int E, float* partial,
                float* dwg, bool is_bf16, cudaStream_t s);
 size_t dwg_partial_floats(int T, int d, int E);
-// K6 + K7 fused (E <= 8): dx for tokens [t0, t1) and dWg partials in blocks
-// [pbase, pbase + fused_partial_blocks(t0, t1)) of `partial` ([blocks][d][E]).
-int launch_gate_bwd_fused(const DispatchArgs& a, const void* dxe, const void* x, const float* g,
-                          const float* logits, const float* wg, int renorm, void* dx, float* partial,
-                          int pbase, int t0, int t1, bool is_bf16, cudaStream_t s);
-int fused_partial_blocks(int t0, int t1);
-int launch_dwg_reduce(const float* partial, int nb, int d, int E, float* dwg, cudaStream_t s);
 // zero rows [off_g + rows_g, off_g + round_up(rows_g, 128)) of a packed buffer
 int launch_zero_pads(void* buf, int row_elems, const int* grp_off, const int* grp_rows,
                      int n_groups, int elt_bytes, cudaStream_t s);

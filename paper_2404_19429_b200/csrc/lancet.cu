@@ -404,41 +404,24 @@ struct Plan {
 };
 
 // K6 + K7 for the tokens of chunk cc of nc (nc == 1: all tokens): dx (expert path + gate
-// term) and, after the last chunk, dWg.  E <= 8 uses the fused kernel (dWg partials per
-// 64-token block, `*pbase` counts them across chunks); larger E the two-kernel path.
+// term) and, after the last chunk, dWg.
 lancet_status gate_backward(lancet_ctx* c, const DispatchArgs& da, const void* dxe, void* dx,
                             float* dwg, int renorm, cudaStream_t s, int cc, int nc, int* L,
                             int* pbase = nullptr)
 {
+    (void)pbase;
     const int T = c->T, d = c->cfg.d_model, E = c->cfg.n_experts;
     const int t0 = chunk_start(T, nc, cc), t1 = chunk_start(T, nc, cc + 1);
-    int pb_local = 0;
-    int* pb = pbase ? pbase : &pb_local;
-    if (cc == 0) *pb = 0;
-    if (E <= 8) {
-        {
-            OpScope op(c, "gate_bwd_fused", 0, nc > 1 ? cc : -1, s);
-            *L += launch_gate_bwd_fused(da, dxe, c->x, c->g, c->logits, c->wg, renorm, dx,
-                                        c->dwg_partial, *pb, t0, t1, c->bf16, s);
-            *pb += fused_partial_blocks(t0, t1);
-        }
-        CHECK_LAUNCH();
-        if (cc == nc - 1) {
-            OpScope op(c, "gate_dwg_reduce", 0, -1, s);
-            *L += launch_dwg_reduce(c->dwg_partial, *pb, d, E, dwg, s);
-        }
-    } else {
-        {
-            OpScope op(c, "unpermute_gate_bwd", 0, nc > 1 ? cc : -1, s);
-            if (cc == 0) *L += launch_wg_transpose(c->wg, d, E, c->wgT, s);
-            *L += launch_unpermute_gate_bwd(da, dxe, c->g, c->logits, c->wgT, renorm, dx, c->dlogit,
-                                            t0, t1, c->bf16, s);
-        }
-        CHECK_LAUNCH();
-        if (cc == nc - 1) {
-            OpScope op(c, "gate_dwg", 0, -1, s);
-            *L += launch_dwg(c->x, c->dlogit, T, d, E, c->dwg_partial, dwg, c->bf16, s);
-        }
+    {
+        OpScope op(c, "unpermute_gate_bwd", 0, nc > 1 ? cc : -1, s);
+        if (cc == 0 && gate_bwd_needs_wgT(d, E)) *L += launch_wg_transpose(c->wg, d, E, c->wgT, s);
+        *L += launch_unpermute_gate_bwd(da, dxe, c->g, c->logits, c->wg, c->wgT, renorm, dx, c->dlogit,
+                                        t0, t1, c->num_sms, c->bf16, s);
+    }
+    CHECK_LAUNCH();
+    if (cc == nc - 1) {
+        OpScope op(c, "gate_dwg", 0, -1, s);
+        *L += launch_dwg(c->x, c->dlogit, T, d, E, c->dwg_partial, dwg, c->bf16, s);
     }
     CHECK_LAUNCH();
     return LANCET_OK;

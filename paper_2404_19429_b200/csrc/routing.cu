@@ -23,7 +23,7 @@ constexpr int kGateMaxTB = 64;   // tokens per block
 constexpr int kGateThreadCap = 128;
 
 struct GateGeom {
-    int ce;        // experts per thread (4 if E % 4 == 0, else 1)
+    int ce;        // experts (R1 chains) per thread: 2 if E is even, else 1
     int tpt;       // threads per token = E / ce
     int TB;        // tokens per block
     int threads;   // TB * tpt
@@ -35,7 +35,7 @@ struct GateGeom {
 __host__ __device__ inline GateGeom gate_geom(int E, int elt_bytes)
 {
     GateGeom g;
-    g.ce = (E % 8 == 0) ? 8 : ((E % 4 == 0) ? 4 : 1);
+    g.ce = (E % 2 == 0) ? 2 : 1;   // 2 chains per thread: 4x the warps of 8, latency-bound kernel
     g.tpt = E / g.ce;
     g.TB = kGateThreadCap / g.tpt;
     if (g.TB > kGateMaxTB) g.TB = kGateMaxTB;
@@ -84,6 +84,28 @@ __device__ __forceinline__ void gate_load_tile(const Elt* __restrict__ x, const 
     for (int q = threadIdx.x; q < wchunks; q += blockDim.x) cp_async16(wb + q * 16, wsrc + q * 16);
 }
 
+// acc[c] = fma(xv, w[c], acc[c]) for the CE experts of this thread (one R1 step each)
+template <int CE>
+__device__ __forceinline__ void gate_fma_row(const float* w, float xv, float (&acc)[CE])
+{
+    if constexpr (CE % 4 == 0) {
+#pragma unroll
+        for (int h = 0; h < CE / 4; ++h) {
+            const float4 w4 = *reinterpret_cast<const float4*>(w + 4 * h);
+            acc[4 * h + 0] = __fmaf_rn(xv, w4.x, acc[4 * h + 0]);
+            acc[4 * h + 1] = __fmaf_rn(xv, w4.y, acc[4 * h + 1]);
+            acc[4 * h + 2] = __fmaf_rn(xv, w4.z, acc[4 * h + 2]);
+            acc[4 * h + 3] = __fmaf_rn(xv, w4.w, acc[4 * h + 3]);
+        }
+    } else if constexpr (CE == 2) {
+        const float2 w2 = *reinterpret_cast<const float2*>(w);
+        acc[0] = __fmaf_rn(xv, w2.x, acc[0]);
+        acc[1] = __fmaf_rn(xv, w2.y, acc[1]);
+    } else {
+        acc[0] = __fmaf_rn(xv, w[0], acc[0]);
+    }
+}
+
 // K1.  Thread (token r, experts e0..e0+CE-1) runs CE independent R1 chains; tiles of x and of
 // Wg stream through shared memory (cp.async, double-buffered).
 template <typename Elt, int CE>
@@ -124,47 +146,19 @@ gate_topk_kernel(const Elt* __restrict__ x, const float* __restrict__ wg, int T,
         if (active && t0 + r < T) {
             const Elt* xr = reinterpret_cast<const Elt*>(cur + (size_t)r * geo.row_bytes);
             const float* ws = reinterpret_cast<const float*>(cur + (size_t)TB * geo.row_bytes) + e0;
-            if constexpr (CE >= 4 && sizeof(Elt) == 2) {
-                // two x values per 32-bit shared load; CE/4 float4 Wg loads per i
+            if constexpr (sizeof(Elt) == 2) {
+                // two x values per 32-bit shared load
                 const uint32_t* xp = reinterpret_cast<const uint32_t*>(xr);
 #pragma unroll 4
                 for (int i = 0; i < ilim; i += 2) {    // R1: increasing i, one fused step each
                     const uint32_t pr = xp[i >> 1];
-                    const float xa = __uint_as_float(pr << 16), xb = __uint_as_float(pr & 0xffff0000u);
-#pragma unroll
-                    for (int h = 0; h < CE / 4; ++h) {
-                        const float4 w4 = *reinterpret_cast<const float4*>(ws + i * E + 4 * h);
-                        acc[4 * h + 0] = __fmaf_rn(xa, w4.x, acc[4 * h + 0]);
-                        acc[4 * h + 1] = __fmaf_rn(xa, w4.y, acc[4 * h + 1]);
-                        acc[4 * h + 2] = __fmaf_rn(xa, w4.z, acc[4 * h + 2]);
-                        acc[4 * h + 3] = __fmaf_rn(xa, w4.w, acc[4 * h + 3]);
-                    }
-#pragma unroll
-                    for (int h = 0; h < CE / 4; ++h) {
-                        const float4 w4 = *reinterpret_cast<const float4*>(ws + (i + 1) * E + 4 * h);
-                        acc[4 * h + 0] = __fmaf_rn(xb, w4.x, acc[4 * h + 0]);
-                        acc[4 * h + 1] = __fmaf_rn(xb, w4.y, acc[4 * h + 1]);
-                        acc[4 * h + 2] = __fmaf_rn(xb, w4.z, acc[4 * h + 2]);
-                        acc[4 * h + 3] = __fmaf_rn(xb, w4.w, acc[4 * h + 3]);
-                    }
+                    gate_fma_row<CE>(ws + i * E, __uint_as_float(pr << 16), acc);
+                    gate_fma_row<CE>(ws + (i + 1) * E, __uint_as_float(pr & 0xffff0000u), acc);
                 }
             } else {
 #pragma unroll 8
-                for (int i = 0; i < ilim; ++i) {       // R1: increasing i, one fused step each
-                    const float xv = to_f(xr[i]);
-                    if constexpr (CE >= 4) {
-#pragma unroll
-                        for (int h = 0; h < CE / 4; ++h) {
-                            const float4 w4 = *reinterpret_cast<const float4*>(ws + i * E + 4 * h);
-                            acc[4 * h + 0] = __fmaf_rn(xv, w4.x, acc[4 * h + 0]);
-                            acc[4 * h + 1] = __fmaf_rn(xv, w4.y, acc[4 * h + 1]);
-                            acc[4 * h + 2] = __fmaf_rn(xv, w4.z, acc[4 * h + 2]);
-                            acc[4 * h + 3] = __fmaf_rn(xv, w4.w, acc[4 * h + 3]);
-                        }
-                    } else {
-                        acc[0] = __fmaf_rn(xv, ws[i * E], acc[0]);
-                    }
-                }
+                for (int i = 0; i < ilim; ++i)         // R1: increasing i, one fused step each
+                    gate_fma_row<CE>(ws + i * E, to_f(xr[i]), acc);
             }
         }
         __syncthreads();
@@ -326,8 +320,8 @@ int launch_routing(const RouteArgs& a, bool is_bf16, cudaStream_t s)
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(gate_topk_kernel<bf16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(gate_topk_kernel<bf16, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(gate_topk_kernel<float, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(gate_topk_kernel<bf16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(gate_topk_kernel<float, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaFuncSetAttribute(gate_topk_kernel<bf16, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaFuncSetAttribute(gate_topk_kernel<float, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaFuncSetAttribute(gate_topk_kernel<float, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -339,11 +333,11 @@ int launch_routing(const RouteArgs& a, bool is_bf16, cudaStream_t s)
     const int thr = round_up(g.threads, 32);
 #define GATE_ARGS a.T, a.d, a.E, a.k, a.renorm, a.logits, a.idx, a.w, a.hist, n_tiles
     if (is_bf16) {
-        if (g.ce == 8) gate_topk_kernel<bf16, 8><<<blocks, thr, g.smem, s>>>((const bf16*)a.x, a.wg, GATE_ARGS);
+        if (g.ce == 2) gate_topk_kernel<bf16, 2><<<blocks, thr, g.smem, s>>>((const bf16*)a.x, a.wg, GATE_ARGS);
         else if (g.ce == 4) gate_topk_kernel<bf16, 4><<<blocks, thr, g.smem, s>>>((const bf16*)a.x, a.wg, GATE_ARGS);
         else gate_topk_kernel<bf16, 1><<<blocks, thr, g.smem, s>>>((const bf16*)a.x, a.wg, GATE_ARGS);
     } else {
-        if (g.ce == 8) gate_topk_kernel<float, 8><<<blocks, thr, g.smem, s>>>((const float*)a.x, a.wg, GATE_ARGS);
+        if (g.ce == 2) gate_topk_kernel<float, 2><<<blocks, thr, g.smem, s>>>((const float*)a.x, a.wg, GATE_ARGS);
         else if (g.ce == 4) gate_topk_kernel<float, 4><<<blocks, thr, g.smem, s>>>((const float*)a.x, a.wg, GATE_ARGS);
         else gate_topk_kernel<float, 1><<<blocks, thr, g.smem, s>>>((const float*)a.x, a.wg, GATE_ARGS);
     }

@@ -9,4 +9,6 @@ print(f"value {d['value']/1e6:.3f} M tok/s  ms/step {d['ms_per_step']:.3f}  "
 if 'e2e' in d:
     print(f"e2e {d['e2e']['value']/1e6:.3f} M tok/s")
 for k, v in d.get('kernels', {}).items():
-    print(f"  {k:20s} {v['us']:8.1f} us  " + (f"{v['tflops']:7.0f} TF/s" if 'tflops' in v else f"{v['gbs']:7.0f} GB/s ({v['hbm_frac']:.2f})"))
+    extra = f"{v['tflops']:7.0f} TF/s" if 'tflops' in v else (f"{v['gbs']:7.0f} GB/s ({v['hbm_frac']:.2f})" if 'gbs' in v else "")
+    print(f"  {k:20s} {v['us']:8.1f} us  " + extra)
+print(f"  sum of ops {sum(v['us'] for v in d.get('kernels', {}).values()):.1f} us")
