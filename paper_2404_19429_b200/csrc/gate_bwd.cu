@@ -88,11 +88,9 @@ unpermute_gate_bwd_kernel(const Elt* __restrict__ dxe, const int* __restrict__ i
     float* sdl = ksm + (size_t)w * kTPW * E;          // [kTPW][E] per warp
     const float* W = wgT;
     if constexpr (SMEM_WG) {
-        float* swt = ksm + (size_t)kWarps * kTPW * E;
-        for (int q = threadIdx.x; q < d * E; q += blockDim.x) {
-            const int i = q / E, e = q % E;
-            swt[(size_t)e * d + i] = wg[q];
-        }
+        float* swt = ksm + (size_t)kWarps * kTPW * E;   // 16-byte aligned (kTPW*E*kWarps*4 % 16 == 0)
+        for (int q = threadIdx.x; q < d * E / 4; q += blockDim.x)
+            reinterpret_cast<float4*>(swt)[q] = __ldg(reinterpret_cast<const float4*>(wgT) + q);
         __syncthreads();
         W = swt;
     }

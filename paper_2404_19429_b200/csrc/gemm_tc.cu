@@ -7,17 +7,21 @@
 //   M-grouped (rows = tokens of a group, 128-row aligned):      fc1 (act epilogue: H and
 //     act'(A)), fc2, dfc2 (epilogue multiplies act'(A)), dfc1
 //   K-grouped (reduction over a group's token rows, fp32 out):  dW2 = dO^T H, dW1 = dA^T X
-// Operands are TMA-loaded with 128-byte swizzle into a 4-stage shared-memory ring; a single
-// elected thread issues tcgen05.mma (kind::f16, bf16 in, fp32 accumulate) into one of two
-// TMEM accumulators (BN fp32 columns each), so the epilogue warpgroup drains tile i while the
-// tensor core computes tile i+1.  Operands may be K-major or MN-major (the weights of the dX
-// GEMMs and both operands of the dW GEMMs are read transposed in place -- no transposition
-// pass over HBM).
+// Operands are TMA-loaded with 128-byte swizzle into a shared-memory ring; a single elected
+// thread issues tcgen05.mma (kind::f16, bf16 in, fp32 accumulate) into one of two TMEM
+// accumulators (BN fp32 columns each), so the epilogue drains tile i while the tensor core
+// computes tile i+1.  Operands may be K-major or MN-major (the dX GEMMs read W1/W2 and the dW
+// GEMMs read both activations transposed in place -- no transposition pass over HBM).
+// bf16 epilogues stage each warp's 32x32 sub-tile in 64B-swizzled shared memory and write it
+// with TMA bulk-tensor stores; the act'(A) operand of dfc2 arrives by TMA the same way.
 //
 // Roles (384 threads):  warp 0 TMA producer | warp 1 MMA issuer | warp 2 TMEM allocator |
-//                       warp 3 idle | warps 4-11 epilogue (TMEM lanes 32*(w%4) ...).
+//                       warp 3 idle | warps 4-11 epilogue (TMEM lanes 32*(w%4), column half
+//                       (w-4)/4).
 #include <cuda.h>
 
+#include <algorithm>
+#include <cstring>
 #include <mutex>
 
 #include "common.cuh"
@@ -26,10 +30,22 @@
 namespace lancet {
 namespace tc {
 
-constexpr int BM = 128, BK = 64, STAGES = 4, UMMA_K = 16;
+constexpr int BM = 128, BK = 64, UMMA_K = 16;
 constexpr int kThreads = 384;            // 4 control warps + 8 epilogue warps
+constexpr int kEpiWarps = 8;
 constexpr int kMaxGroups = 512;
 constexpr uint32_t A_STAGE = BM * BK * 2;                 // 16 KiB
+constexpr uint32_t kWarpStage = 6144;                     // per epilogue warp: out0 | out1 | aux
+
+template <int BN, bool A_MN>
+struct Cfg {
+    static constexpr bool kStaged = !A_MN;                // M-grouped: bf16 out via TMA store
+    static constexpr int STAGES = (kStaged && BN == 256) ? 3 : 4;
+    static constexpr uint32_t B_STAGE = BN * BK * 2;
+    static constexpr size_t kRing = (size_t)STAGES * (A_STAGE + B_STAGE);
+    static constexpr size_t kEpi = kStaged ? (size_t)kEpiWarps * kWarpStage : 0;
+    static constexpr size_t kSmem = 1024 + kRing + kEpi + 256 + sizeof(int) * (kMaxGroups + 1);
+};
 
 struct Params {
     int mode, n_groups, gpw, epi, act, accumulate;
@@ -38,8 +54,6 @@ struct Params {
     const int* grp_off;
     void* C;
     long ldc, c_group_stride;
-    void* C2;
-    const void* aux;
 };
 
 // ---------------------------------------------------------------- PTX wrappers ----------
@@ -72,6 +86,15 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* ba
         "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
         : "memory");
 }
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
 }
@@ -139,27 +162,31 @@ __device__ __forceinline__ void decode_tile(int tile, const int* tstart, int ng,
     nt = local % ntn;
 }
 
-template <int BN>
-constexpr size_t smem_bytes() {
-    return 1024 + STAGES * (A_STAGE + (size_t)BN * BK * 2) + 256 + sizeof(int) * (kMaxGroups + 1);
-}
+// byte offset of 16-byte chunk j of row r in a [32 rows][64 B] box stored with SWIZZLE_64B
+__device__ __forceinline__ uint32_t sw64(int r, int j) { return r * 64 + ((j ^ ((r >> 1) & 3)) << 4); }
 
 template <int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kThreads, 1)
-tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Params p)
+tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+               const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2,
+               const __grid_constant__ CUtensorMap tmX, Params p)
 {
-    constexpr uint32_t B_STAGE = BN * BK * 2;
+    using CF = Cfg<BN, A_MN>;
+    constexpr int STAGES = CF::STAGES;
+    constexpr uint32_t B_STAGE = CF::B_STAGE;
     constexpr uint32_t TMEM_COLS = 2 * BN;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
     uint8_t* sB = smem + STAGES * A_STAGE;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE);
+    uint8_t* sEpi = smem + CF::kRing;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + CF::kEpi);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-    int* tstart = reinterpret_cast<int*>(smem + STAGES * (A_STAGE + B_STAGE) + 256);
+    uint64_t* abar = tempty + 2;                       // [kEpiWarps] aux-load barriers
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(abar + kEpiWarps);
+    int* tstart = reinterpret_cast<int*>(sEpi + CF::kEpi + 256);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ntn = p.N / BN;
@@ -176,10 +203,16 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tmA);
         tma_prefetch(&tmB);
+        if (CF::kStaged) {
+            tma_prefetch(&tmC);
+            if (p.epi == EPI_ACT) tma_prefetch(&tmC2);
+            if (p.epi == EPI_DACT) tma_prefetch(&tmX);
+        }
     }
     if (warp == 1 && lane == 0) {
         for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-        for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 8); }
+        for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], kEpiWarps); }
+        for (int i = 0; i < kEpiWarps; ++i) mbar_init(&abar[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 2) {
@@ -271,7 +304,14 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         // ===================== epilogue: 8 warps =====================
         // warp w may only touch TMEM lanes 32*(w%4)..; warps w and w+4 split the columns
         const int q = warp & 3;
-        const int half = (warp - 4) >> 2;
+        const int ew = warp - 4;
+        const int half = ew >> 2;
+        const int cc0 = half * (BN / 64), cc1 = cc0 + BN / 64;
+        uint8_t* sO0 = sEpi + ew * kWarpStage;
+        uint8_t* sO1 = sO0 + 2048;
+        uint8_t* sX = sO0 + 4096;
+        uint64_t* xbar = &abar[ew];
+        uint32_t xphase = 0;
         int it = 0;
         for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
             int g, mt, nt;
@@ -279,23 +319,75 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
             const bool has_k = p.mode == GEMM_M_GROUPED ? (p.K > 0) : (p.grp_rows[g] > 0);
-            mbar_wait(&tfull[acc], acc_phase);
-            tc_fence_after();
-            const int lrow = q * 32 + lane;
             const int n0 = nt * BN;
-            long orow;
-            if (p.mode == GEMM_M_GROUPED) orow = (long)p.grp_off[g] + mt * BM + lrow;
-            else orow = (long)mt * BM + lrow;
+            if constexpr (CF::kStaged) {
+                const int row0 = p.grp_off[g] + mt * BM + q * 32;      // this warp's 32 rows
+                if (p.epi == EPI_DACT && lane == 0) {                    // prefetch act'(A), chunk cc0
+                    mbar_expect_tx(xbar, 2048);
+                    tma_load_2d(&tmX, xbar, sX, n0 + cc0 * 32, row0);
+                }
+                mbar_wait(&tfull[acc], acc_phase);
+                tc_fence_after();
 #pragma unroll 1
-            for (int cc = half * (BN / 64); cc < (half + 1) * (BN / 64); ++cc) {
-                uint32_t v[32];
-                tmem_ld32(tmem_base + acc * BN + cc * 32 + ((uint32_t)(q * 32) << 16), v);
-                float f[32];
+                for (int cc = cc0; cc < cc1; ++cc) {
+                    uint32_t v[32];
+                    tmem_ld32(tmem_base + acc * BN + cc * 32 + ((uint32_t)(q * 32) << 16), v);
+                    float f[32];
 #pragma unroll
-                for (int i = 0; i < 32; ++i) f[i] = has_k ? __uint_as_float(v[i]) : 0.f;
-                const long col = n0 + cc * 32;
-                if (p.epi == EPI_F32) {
-                    float* C = reinterpret_cast<float*>(p.C) + (long)g * p.c_group_stride + orow * p.ldc + col;
+                    for (int i = 0; i < 32; ++i) f[i] = has_k ? __uint_as_float(v[i]) : 0.f;
+                    if (p.epi == EPI_DACT) {
+                        mbar_wait(xbar, xphase);
+                        xphase ^= 1;
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            float a8[8];
+                            unpack16<bf16>(*reinterpret_cast<const uint4*>(sX + sw64(lane, j)), a8);
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) f[8 * j + i] *= a8[i];
+                        }
+                        __syncwarp();
+                        if (cc + 1 < cc1 && lane == 0) {
+                            mbar_expect_tx(xbar, 2048);
+                            tma_load_2d(&tmX, xbar, sX, n0 + (cc + 1) * 32, row0);
+                        }
+                    }
+                    // the previous chunk's TMA stores must have read the staging buffers
+                    if (lane == 0) bulk_wait_read0();
+                    __syncwarp();
+                    if (p.epi == EPI_ACT) {
+                        float h[32], gr[32];
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) act_fwd_grad_fast(p.act, f[i], h[i], gr[i]);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            *reinterpret_cast<uint4*>(sO0 + sw64(lane, j)) = pack16<bf16>(h + 8 * j);
+                            *reinterpret_cast<uint4*>(sO1 + sw64(lane, j)) = pack16<bf16>(gr + 8 * j);
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j)
+                            *reinterpret_cast<uint4*>(sO0 + sw64(lane, j)) = pack16<bf16>(f + 8 * j);
+                    }
+                    fence_proxy_async();
+                    __syncwarp();
+                    if (lane == 0) {
+                        tma_store_2d(&tmC, sO0, n0 + cc * 32, row0);
+                        if (p.epi == EPI_ACT) tma_store_2d(&tmC2, sO1, n0 + cc * 32, row0);
+                        bulk_commit();
+                    }
+                }
+            } else {
+                mbar_wait(&tfull[acc], acc_phase);
+                tc_fence_after();
+                const long orow = (long)mt * BM + q * 32 + lane;
+#pragma unroll 1
+                for (int cc = cc0; cc < cc1; ++cc) {
+                    uint32_t v[32];
+                    tmem_ld32(tmem_base + acc * BN + cc * 32 + ((uint32_t)(q * 32) << 16), v);
+                    float f[32];
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) f[i] = has_k ? __uint_as_float(v[i]) : 0.f;
+                    float* C = reinterpret_cast<float*>(p.C) + (long)g * p.c_group_stride + orow * p.ldc + n0 + cc * 32;
                     if (p.accumulate) {
 #pragma unroll
                         for (int i = 0; i < 8; ++i) {
@@ -307,38 +399,13 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                     }
 #pragma unroll
                     for (int i = 0; i < 8; ++i) st_v4(C + 4 * i, pack16<float>(f + 4 * i));
-                } else {
-                    bf16* C = reinterpret_cast<bf16*>(p.C) + orow * p.ldc + col;
-                    if (p.epi == EPI_ACT) {
-                        float h[32], gr[32];
-#pragma unroll
-                        for (int i = 0; i < 32; ++i) act_fwd_grad_fast(p.act, f[i], h[i], gr[i]);
-                        bf16* C2 = reinterpret_cast<bf16*>(p.C2) + orow * p.ldc + col;
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) {
-                            st_v4(C + 8 * i, pack16<bf16>(h + 8 * i));
-                            st_v4(C2 + 8 * i, pack16<bf16>(gr + 8 * i));
-                        }
-                    } else {
-                        if (p.epi == EPI_DACT) {
-                            const bf16* X = reinterpret_cast<const bf16*>(p.aux) + orow * p.ldc + col;
-#pragma unroll
-                            for (int i = 0; i < 4; ++i) {
-                                float a8[8];
-                                unpack16<bf16>(ld_v4(X + 8 * i), a8);
-#pragma unroll
-                                for (int j = 0; j < 8; ++j) f[8 * i + j] *= a8[j];
-                            }
-                        }
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) st_v4(C + 8 * i, pack16<bf16>(f + 8 * i));
-                    }
                 }
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
         }
+        if (CF::kStaged && lane == 0) bulk_wait0();
     }
     tc_fence_before();
     __syncthreads();
@@ -369,7 +436,7 @@ static EncodeFn get_encode()
 
 // 2D bf16 map: inner dimension `inner` (contiguous), `outer` rows of `stride_elems`.
 static bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t stride_elems,
-                     uint32_t box_inner, uint32_t box_outer)
+                     uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B)
 {
     EncodeFn enc = get_encode();
     if (!enc) return false;
@@ -378,7 +445,7 @@ static bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t o
     cuuint32_t box[2] = {box_inner, box_outer};
     cuuint32_t es[2] = {1, 1};
     CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
@@ -386,16 +453,25 @@ static bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t o
 template <int BN, bool A_MN, bool B_MN>
 static int launch_cfg(const GemmArgs& a, int num_sms, cudaStream_t s)
 {
-    CUtensorMap ta, tb;
+    using CF = Cfg<BN, A_MN>;
+    CUtensorMap ta, tb, tcm, tc2, tx;
+    memset(&tcm, 0, sizeof(tcm));
+    memset(&tc2, 0, sizeof(tc2));
+    memset(&tx, 0, sizeof(tx));
     bool ok;
     if (A_MN) ok = make_map(&ta, a.A, a.M, a.a_rows, a.lda, 64, 64);
     else ok = make_map(&ta, a.A, a.K, a.a_rows, a.lda, 64, BM);
     if (B_MN) ok = ok && make_map(&tb, a.B, a.N, a.b_rows, a.ldb, 64, 64);
     else ok = ok && make_map(&tb, a.B, a.K, a.b_rows, a.ldb, 64, BN);
+    if (CF::kStaged) {
+        ok = ok && make_map(&tcm, a.C, a.N, a.c_rows, a.ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+        if (a.epi == EPI_ACT) ok = ok && make_map(&tc2, a.C2, a.N, a.c_rows, a.ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+        if (a.epi == EPI_DACT) ok = ok && make_map(&tx, a.aux, a.N, a.c_rows, a.ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+    }
     if (!ok) return -1;
     Params p{a.mode, a.n_groups, a.gpw, a.epi, a.act, a.accumulate, a.M, a.N, a.K, a.grp_rows, a.grp_off,
-             a.C, a.ldc, a.c_group_stride, a.C2, a.aux};
-    constexpr size_t smem = smem_bytes<BN>();
+             a.C, a.ldc, a.c_group_stride};
+    constexpr size_t smem = CF::kSmem;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(tc_gemm_kernel<BN, A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -406,7 +482,7 @@ static int launch_cfg(const GemmArgs& a, int num_sms, cudaStream_t s)
     if (a.mode == GEMM_M_GROUPED) max_tiles = (long)ceil_div(a.max_rows, BM) * a.n_groups * (a.N / BN);
     else max_tiles = (long)(a.M / BM) * (a.N / BN) * a.n_groups;
     const int grid = (int)std::max<long>(1, std::min<long>(num_sms, max_tiles));
-    tc_gemm_kernel<BN, A_MN, B_MN><<<grid, kThreads, smem, s>>>(ta, tb, p);
+    tc_gemm_kernel<BN, A_MN, B_MN><<<grid, kThreads, smem, s>>>(ta, tb, tcm, tc2, tx, p);
     return 1;
 }
 
@@ -419,11 +495,13 @@ bool gemm_tc_supported(const GemmArgs& a)
     if (a.mode == GEMM_M_GROUPED) {
         if (a.a_mn) return false;
         if (a.K % tc::BK) return false;
+        if (a.epi == EPI_F32) return false;
+        if (a.c_rows <= 0 || a.ldc % 8) return false;
     } else {
         if (!a.a_mn || !a.b_mn) return false;
         if (a.M % tc::BM) return false;
+        if (a.epi != EPI_F32) return false;
     }
-    if (a.epi == EPI_F32 && a.mode != GEMM_K_GROUPED) return false;
     return a.a_rows > 0 && a.b_rows > 0;
 }
 

@@ -71,6 +71,7 @@ struct GemmArgs {
     int epi, act, accumulate;
     bool a_mn, b_mn;
     long a_rows, b_rows;  // outer extents of A and B viewed as 2D row-major tensors (TMA maps)
+    long c_rows;          // outer extent of C / C2 / aux (M-grouped; TMA store maps)
 };
 int launch_gemm_simt(const GemmArgs& a, bool is_bf16, cudaStream_t s);
 

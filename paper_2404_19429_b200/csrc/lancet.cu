@@ -159,6 +159,7 @@ lancet_status expert_forward(lancet_ctx* c, const int* grp_rows, const int* grp_
     GemmArgs a{};
     a.mode = GEMM_M_GROUPED; a.n_groups = ng; a.gpw = 1;
     a.grp_rows = grp_rows; a.grp_off = grp_off; a.max_rows = max_rows; a.act = c->cfg.act;
+    a.c_rows = c->rows_exp;
     {   // fc1: H = act(X W1^T), G' = act'(X W1^T)
         OpScope op(c, "expert_fc1", 0, chunk, s);
         a.A = c->world > 1 ? c->xe : c->xs; a.lda = d; a.a_rows = c->rows_exp;
@@ -186,6 +187,7 @@ lancet_status expert_backward_dx(lancet_ctx* c, const void* dout, const int* grp
     GemmArgs a{};
     a.mode = GEMM_M_GROUPED; a.n_groups = ng; a.gpw = 1;
     a.grp_rows = grp_rows; a.grp_off = grp_off; a.max_rows = max_rows; a.act = c->cfg.act;
+    a.c_rows = c->rows_exp;
     {   // dA = (dO W2) * act'(A):  B(n=f, k=d) = W2[e][k][n]  (MN-major)
         OpScope op(c, "expert_dfc2", 0, chunk, s);
         a.A = dout; a.lda = d; a.a_mn = false; a.a_rows = c->rows_exp;
@@ -414,7 +416,7 @@ lancet_status gate_backward(lancet_ctx* c, const DispatchArgs& da, const void* d
     const int t0 = chunk_start(T, nc, cc), t1 = chunk_start(T, nc, cc + 1);
     {
         OpScope op(c, "unpermute_gate_bwd", 0, nc > 1 ? cc : -1, s);
-        if (cc == 0 && gate_bwd_needs_wgT(d, E)) *L += launch_wg_transpose(c->wg, d, E, c->wgT, s);
+        if (cc == 0) *L += launch_wg_transpose(c->wg, d, E, c->wgT, s);
         *L += launch_unpermute_gate_bwd(da, dxe, c->g, c->logits, c->wg, c->wgT, renorm, dx, c->dlogit,
                                         t0, t1, c->num_sms, c->bf16, s);
     }
