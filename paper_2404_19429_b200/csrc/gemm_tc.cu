@@ -33,14 +33,14 @@ namespace tc {
 constexpr int BM = 128, BK = 64, UMMA_K = 16;
 constexpr int kThreads = 384;            // 4 control warps + 8 epilogue warps
 constexpr int kEpiWarps = 8;
-constexpr int kMaxGroups = 512;
+constexpr int kMaxGroups = 256;
 constexpr uint32_t A_STAGE = BM * BK * 2;                 // 16 KiB
-constexpr uint32_t kWarpStage = 6144;                     // per epilogue warp: out0 | out1 | aux
+constexpr uint32_t kWarpStage = 4096;                     // per epilogue warp: out0 | (out1 or aux)
 
 template <int BN, bool A_MN>
 struct Cfg {
     static constexpr bool kStaged = !A_MN;                // M-grouped: bf16 out via TMA store
-    static constexpr int STAGES = (kStaged && BN == 256) ? 3 : 4;
+    static constexpr int STAGES = 4;
     static constexpr uint32_t B_STAGE = BN * BK * 2;
     static constexpr size_t kRing = (size_t)STAGES * (A_STAGE + B_STAGE);
     static constexpr size_t kEpi = kStaged ? (size_t)kEpiWarps * kWarpStage : 0;
@@ -309,7 +309,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         const int cc0 = half * (BN / 64), cc1 = cc0 + BN / 64;
         uint8_t* sO0 = sEpi + ew * kWarpStage;
         uint8_t* sO1 = sO0 + 2048;
-        uint8_t* sX = sO0 + 4096;
+        uint8_t* sX = sO0 + 2048;                      // dfc2 has no second output
         uint64_t* xbar = &abar[ew];
         uint32_t xphase = 0;
         int it = 0;

@@ -1,0 +1,160 @@
+"""GPU parity of the expert-parallel (world > 1) path on ONE device: G simulated ranks of a
+lancet_local_group, one host thread and one CUDA stream per rank.  The exchange uses the same
+plans, kernels and scheduler as the NCCL path; only the transport differs (device-to-device
+copies ordered by events where the grouped NCCL send/recv would synchronise)."""
+import threading
+
+import numpy as np
+import pytest
+import torch
+
+import synthetic as S
+from gpu_harness import TOL, normwise
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2404_19429_b200 import build
+    build.build()
+
+
+def run_group(G, ins, E, k, cf, n, flags=0, act="gelu_tanh", dtype="bf16", repeat=1):
+    from paper_2404_19429_b200 import lancet
+    d = ins[0]["x"].shape[1]
+    f = ins[0]["w1"].shape[1]
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    group = lancet.LocalGroup(G)
+    cfg = lancet.LayerConfig(d_model=d, d_ffn=f, n_experts=E,
+                             max_tokens=max(i["x"].shape[0] for i in ins), max_k=k, max_chunks=8,
+                             dtype=dtype, act=act, flags=flags)
+    dev = torch.device("cuda", 0)
+    tens = []
+    for i in ins:
+        tens.append(dict(x=torch.from_numpy(i["x"]).to(dev, tdt), wg=torch.from_numpy(i["wg"]).to(dev),
+                         w1=torch.from_numpy(i["w1"]).to(dev, tdt), w2=torch.from_numpy(i["w2"]).to(dev, tdt),
+                         dy=torch.from_numpy(i["dy"]).to(dev, tdt)))
+    torch.cuda.synchronize()
+    out = [None] * G
+    errs = []
+
+    def worker(r):
+        try:
+            torch.cuda.set_device(dev)
+            st = torch.cuda.Stream(device=dev)
+            ctx = lancet.Context(cfg, world=G, rank=r, device=0, local_group=group)
+            t = tens[r]
+            with torch.cuda.stream(st):
+                for _ in range(repeat):
+                    y, idx, slot, w = ctx.forward(t["x"], t["wg"], t["w1"], t["w2"], k, cf, n, stream=st)
+                    dx, dwg, dw1, dw2 = ctx.backward(t["dy"], stream=st)
+            st.synchronize()
+            send, recv, C = ctx.counts(n)
+            res = dict(y=y.float().cpu().numpy(), idx=idx.cpu().numpy(), slot=slot.cpu().numpy(),
+                       dx=dx.float().cpu().numpy(), dwg=dwg.cpu().numpy(), send=send, recv=recv, C=C)
+            if dw1 is not None:
+                res.update(dw1=dw1.cpu().numpy(), dw2=dw2.cpu().numpy())
+            out[r] = res
+            ctx.close()
+        except Exception as e:  # noqa: BLE001
+            errs.append((r, e))
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(G)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    group.close()
+    assert not errs, errs
+    assert all(o is not None for o in out), "a rank did not finish"
+    return out
+
+
+def oracle_group(ins, k, cf, n, act="gelu_tanh"):
+    from oracle import moe
+    xs = [i["x"] for i in ins]
+    wg = ins[0]["wg"]
+    w1 = [i["w1"] for i in ins]
+    w2 = [i["w2"] for i in ins]
+    fwd = moe.forward(xs, wg, w1, w2, k, cf, n, act=act)
+    b = moe.backward(fwd, xs, wg, w1, w2, [i["dy"] for i in ins], act=act)
+    return fwd, b
+
+
+def make_inputs(G, Ts, d, f, E, k, seed=0, beta=0.5, dtype="bf16"):
+    ins = []
+    for r in range(G):
+        sh = S.LayerShape(T=Ts[r], d=d, f=f, E=E, G=G, k=k, cf=1.0, n_chunks=1)
+        ins.append(S.gen_rank_inputs(seed, r, sh, beta=beta, dtype=dtype))
+    return ins
+
+
+@pytest.mark.parametrize("G,Ts,E,k,n", [
+    (2, [600, 600], 8, 2, 1),
+    (2, [700, 513], 8, 2, 3),            # different T per rank, ragged chunks
+    (4, [512, 640, 384, 700], 8, 2, 4),
+    (4, [300, 300, 300, 300], 4, 1, 2),  # E_l = 1, top-1
+])
+def test_expert_parallel_matches_oracle(G, Ts, E, k, n):
+    d, f, cf = 128, 256, 1.0
+    ins = make_inputs(G, Ts, d, f, E, k, seed=G * 100 + n)
+    g = run_group(G, ins, E, k, cf, n)
+    fwd, b = oracle_group(ins, k, cf, n)
+    from oracle import moe
+    sends = [rt.counts for rt in fwd.routing]
+    for r in range(G):
+        rt = fwd.routing[r]
+        assert np.array_equal(g[r]["idx"], rt.idx) and np.array_equal(g[r]["slot"], rt.slot)
+        assert g[r]["C"] == rt.C
+        assert np.array_equal(g[r]["send"], rt.counts)
+        assert np.array_equal(g[r]["recv"], moe.recv_counts(sends, G, r)), "recv counts (size a2a)"
+        for key in ("y", "dx", "dwg", "dw1", "dw2"):
+            ref = {"y": fwd.y[r], "dx": b["dx"][r], "dwg": b["dwg"][r], "dw1": b["dw1"][r], "dw2": b["dw2"][r]}[key]
+            assert normwise(g[r][key], ref) <= TOL["bf16"], (r, key, normwise(g[r][key], ref))
+
+
+def test_identity_experts_across_ranks():
+    G, E, k = 2, 4, 2
+    ins = make_inputs(G, [400, 450], 64, 128, E, k, seed=3, beta=1.0)
+    g = run_group(G, ins, E, k, 0.75, 2, act="identity_expert")
+    fwd, b = oracle_group(ins, k, 0.75, 2, act="identity_expert")
+    for r in range(G):
+        rt = fwd.routing[r]
+        assert np.any(rt.slot < 0), "case must exercise drops"
+        sc = np.where(rt.slot >= 0, rt.w, 0.0).sum(1)
+        want = sc[:, None] * ins[r]["x"].astype(np.float64)
+        # dispatch a2a -> identity expert -> combine a2a -> gather: (sum admitted w) x, 1 bf16 ulp
+        assert np.all(np.abs(g[r]["y"] - want) <= 2.0 ** -8 * np.abs(want) + 1e-30)
+        assert normwise(g[r]["dx"], b["dx"][r]) <= TOL["bf16"]
+
+
+def test_serial_schedule_is_bitwise_identical_to_pipelined():
+    from paper_2404_19429_b200 import FLAG_SERIAL, FLAG_NO_DW_OVERLAP
+    G, E, k, n = 2, 8, 2, 4
+    ins = make_inputs(G, [900, 800], 128, 256, E, k, seed=9)
+    a = run_group(G, ins, E, k, 1.0, n)
+    b = run_group(G, ins, E, k, 1.0, n, flags=FLAG_SERIAL)
+    c = run_group(G, ins, E, k, 1.0, n, flags=FLAG_NO_DW_OVERLAP)
+    for r in range(G):
+        for key in ("y", "dx", "dwg"):
+            assert np.array_equal(a[r][key], b[r][key]), ("serial", r, key)
+            assert np.array_equal(a[r][key], c[r][key]), ("no-dw-overlap", r, key)
+        for key in ("dw1", "dw2"):
+            assert np.array_equal(a[r][key], c[r][key]), ("no-dw-overlap", r, key)
+            assert normwise(a[r][key], b[r][key]) <= 1e-5, ("serial", r, key)
+
+
+def test_chunking_invariance_across_ranks_and_repeats():
+    G, E, k = 2, 8, 2
+    ins = make_inputs(G, [1000, 1000], 128, 256, E, k, seed=5)
+    ref = run_group(G, ins, E, k, 1.0, 1)
+    for n in (2, 8):
+        g = run_group(G, ins, E, k, 1.0, n, repeat=2)      # repeat: buffers reused across steps
+        for r in range(G):
+            for key in ("y", "dx", "idx", "slot"):
+                assert np.array_equal(g[r][key], ref[r][key]), (n, r, key)
+            for key in ("dw1", "dw2", "dwg"):
+                assert normwise(g[r][key], ref[r][key]) <= 1e-5, (n, r, key)
