@@ -34,7 +34,7 @@ __global__ void __launch_bounds__(256) simt_gemm_kernel(GemmArgs p)
     }
     if (m0 >= Mg) return;
     const Elt* A = reinterpret_cast<const Elt*>(p.A);
-    const Elt* B = reinterpret_cast<const Elt*>(p.B) + (long)(g / p.gpw) * p.b_group_stride;
+    const Elt* B = reinterpret_cast<const Elt*>(p.B) + (long)((g / p.gpw) % p.n_weights) * p.b_group_stride;
     const long krow0 = p.mode == GEMM_K_GROUPED ? row0 : 0;
     const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
 

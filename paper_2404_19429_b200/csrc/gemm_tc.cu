@@ -48,7 +48,7 @@ struct Cfg {
 };
 
 struct Params {
-    int mode, n_groups, gpw, epi, act, accumulate;
+    int mode, n_groups, gpw, n_weights, epi, act, accumulate;
     int M, N, K;
     const int* grp_rows;
     const int* grp_off;
@@ -239,7 +239,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 if (p.mode == GEMM_M_GROUPED) {
                     num_kb = p.K / BK;
                     arow = p.grp_off[g] + mt * BM;
-                    brow = (g / p.gpw) * (B_MN ? p.K : p.N);
+                    brow = ((g / p.gpw) % p.n_weights) * (B_MN ? p.K : p.N);
                 } else {
                     num_kb = round_up(p.grp_rows[g], kRowAlign) / BK;
                     arow = p.grp_off[g];
@@ -469,7 +469,7 @@ static int launch_cfg(const GemmArgs& a, int num_sms, cudaStream_t s)
         if (a.epi == EPI_DACT) ok = ok && make_map(&tx, a.aux, a.N, a.c_rows, a.ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
     }
     if (!ok) return -1;
-    Params p{a.mode, a.n_groups, a.gpw, a.epi, a.act, a.accumulate, a.M, a.N, a.K, a.grp_rows, a.grp_off,
+    Params p{a.mode, a.n_groups, a.gpw, a.n_weights > 0 ? a.n_weights : (1 << 30), a.epi, a.act, a.accumulate, a.M, a.N, a.K, a.grp_rows, a.grp_off,
              a.C, a.ldc, a.c_group_stride};
     constexpr size_t smem = CF::kSmem;
     static bool attr = false;

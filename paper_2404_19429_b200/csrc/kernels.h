@@ -66,6 +66,7 @@ struct GemmArgs {
                           // K-grouped: M, N fixed, K per group from the table
     int max_rows;         // M-grouped: upper bound of round_up(rows_g, 128) (grid sizing)
     int mode, n_groups, gpw;
+    int n_weights;        // B group index = (g / gpw) % n_weights (groups of several chunks)
     const int* grp_rows;  // [n_groups] valid rows (M-grouped) / tokens (K-grouped)
     const int* grp_off;   // [n_groups] first row (128-aligned) in A / C (M) or A / B (K)
     int epi, act, accumulate;

@@ -157,7 +157,7 @@ lancet_status expert_forward(lancet_ctx* c, const int* grp_rows, const int* grp_
 {
     const int d = c->cfg.d_model, f = c->cfg.d_ffn;
     GemmArgs a{};
-    a.mode = GEMM_M_GROUPED; a.n_groups = ng; a.gpw = 1;
+    a.mode = GEMM_M_GROUPED; a.n_groups = ng; a.gpw = 1; a.n_weights = c->E_l;
     a.grp_rows = grp_rows; a.grp_off = grp_off; a.max_rows = max_rows; a.act = c->cfg.act;
     a.c_rows = c->rows_exp;
     {   // fc1: H = act(X W1^T), G' = act'(X W1^T)
@@ -185,7 +185,7 @@ lancet_status expert_backward_dx(lancet_ctx* c, const void* dout, const int* grp
 {
     const int d = c->cfg.d_model, f = c->cfg.d_ffn;
     GemmArgs a{};
-    a.mode = GEMM_M_GROUPED; a.n_groups = ng; a.gpw = 1;
+    a.mode = GEMM_M_GROUPED; a.n_groups = ng; a.gpw = 1; a.n_weights = c->E_l;
     a.grp_rows = grp_rows; a.grp_off = grp_off; a.max_rows = max_rows; a.act = c->cfg.act;
     a.c_rows = c->rows_exp;
     {   // dA = (dO W2) * act'(A):  B(n=f, k=d) = W2[e][k][n]  (MN-major)
@@ -214,7 +214,7 @@ lancet_status expert_backward_dw(lancet_ctx* c, const void* dout, const int* grp
 {
     const int d = c->cfg.d_model, f = c->cfg.d_ffn;
     GemmArgs a{};
-    a.mode = GEMM_K_GROUPED; a.n_groups = ng; a.gpw = 1;
+    a.mode = GEMM_K_GROUPED; a.n_groups = ng; a.gpw = 1; a.n_weights = c->E_l;
     a.grp_rows = grp_rows; a.grp_off = grp_off; a.accumulate = accumulate;
     a.a_mn = true; a.b_mn = true; a.epi = EPI_F32; a.b_group_stride = 0;
     a.a_rows = c->rows_exp; a.b_rows = c->rows_exp;
