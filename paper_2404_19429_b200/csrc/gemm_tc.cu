@@ -10,8 +10,11 @@
 // Operands are TMA-loaded with 128-byte swizzle into a shared-memory ring; a single elected
 // thread issues tcgen05.mma (kind::f16, bf16 in, fp32 accumulate) into one of two TMEM
 // accumulators (BN fp32 columns each), so the epilogue drains tile i while the tensor core
-// computes tile i+1.  Operands may be K-major or MN-major (the dX GEMMs read W1/W2 and the dW
-// GEMMs read both activations transposed in place -- no transposition pass over HBM).
+// computes tile i+1.  With CG = 2 a cluster of two CTAs (one TPC) computes a 256 x BN tile
+// with tcgen05.mma.cta_group::2: each CTA loads its own 128 rows of A and half of B, the
+// leader CTA issues the MMAs and commits to both CTAs' barriers (halves the operand traffic
+// per SM).  Operands may be K-major or MN-major (the dX GEMMs read W1/W2 and the dW GEMMs
+// read both activations transposed in place -- no transposition pass over HBM).
 // bf16 epilogues stage each warp's 32x32 sub-tile in 64B-swizzled shared memory and write it
 // with TMA bulk-tensor stores; the act'(A) operand of dfc2 arrives by TMA the same way.
 //
@@ -36,15 +39,18 @@ constexpr int kEpiWarps = 8;
 constexpr int kMaxGroups = 256;
 constexpr uint32_t A_STAGE = BM * BK * 2;                 // 16 KiB
 constexpr uint32_t kWarpStage = 4096;                     // per epilogue warp: out0 | (out1 or aux)
+constexpr size_t kSmemLimit = 232448;                     // 227 KiB opt-in per block
 
-template <int BN, bool A_MN>
+template <int BN, bool A_MN, int CG>
 struct Cfg {
     static constexpr bool kStaged = !A_MN;                // M-grouped: bf16 out via TMA store
-    static constexpr int STAGES = 4;
-    static constexpr uint32_t B_STAGE = BN * BK * 2;
-    static constexpr size_t kRing = (size_t)STAGES * (A_STAGE + B_STAGE);
+    static constexpr uint32_t B_STAGE = BN * BK * 2 / CG; // this CTA's share of B
     static constexpr size_t kEpi = kStaged ? (size_t)kEpiWarps * kWarpStage : 0;
-    static constexpr size_t kSmem = 1024 + kRing + kEpi + 256 + sizeof(int) * (kMaxGroups + 1);
+    static constexpr size_t kFixed = 1024 + kEpi + 256 + sizeof(int) * (kMaxGroups + 1);
+    static constexpr int STAGES_FIT = (int)((kSmemLimit - kFixed) / (A_STAGE + B_STAGE));
+    static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
+    static constexpr size_t kRing = (size_t)STAGES * (A_STAGE + B_STAGE);
+    static constexpr size_t kSmem = kFixed + kRing;
 };
 
 struct Params {
@@ -60,6 +66,14 @@ struct Params {
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+__device__ __forceinline__ uint32_t cta_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
 }
@@ -69,6 +83,12 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+// arrive on the barrier at the same offset in CTA `rank` of the cluster
+__device__ __forceinline__ void mbar_arrive_cluster(uint64_t* b, uint32_t rank) {
+    uint32_t remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(b)), "r"(rank));
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
     asm volatile(
@@ -86,6 +106,15 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* ba
         "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
         : "memory");
 }
+// 2-SM load: data lands in this CTA's shared memory, the transaction bytes are counted on the
+// barrier at the same offset in the leader CTA (peer bit cleared).
+__device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1)
+        : "memory");
+}
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
     asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
                  "r"(smem_u32(src)), "r"(c0), "r"(c1)
@@ -100,17 +129,36 @@ __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
 }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+template <int CG>
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-                 : "memory");
+    if constexpr (CG == 1) {
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                     : "memory");
+    } else {   // arrive on the barrier at this offset in both CTAs of the pair
+        asm volatile(
+            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                smem_u32(bar)),
+            "h"((uint16_t)0x3)
+            : "memory");
+    }
 }
+template <int CG>
 __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
-        : "memory");
+    if constexpr (CG == 1) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+            : "memory");
+    } else {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+            : "memory");
+    }
 }
 // 32 lanes x 32 columns of 32-bit: thread t of the warp gets row (lane base + t), 32 columns
 __device__ __forceinline__ void tmem_ld32(uint32_t addr, uint32_t (&v)[32]) {
@@ -141,12 +189,12 @@ __device__ __forceinline__ uint64_t operand_desc(uint32_t base, int k) {
     return MN ? make_desc(base + k * 2048, 8192, 1024) : make_desc(base + k * 32, 16, 1024);
 }
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, int CG>
 __device__ __forceinline__ constexpr uint32_t instr_desc() {
     // c_format F32 [4,6) | a_format BF16 [7,10) | b_format BF16 [10,13) | a_major [15] |
-    // b_major [16] | N>>3 [17,23) | M>>4 [24,29)
+    // b_major [16] | N>>3 [17,23) | M>>4 [24,29)   (M = 128 per CTA, 256 per CTA pair)
     return (1u << 4) | (1u << 7) | (1u << 10) | ((A_MN ? 1u : 0u) << 15) | ((B_MN ? 1u : 0u) << 16) |
-           ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+           ((uint32_t)(BN >> 3) << 17) | ((uint32_t)((BM * CG) >> 4) << 24);
 }
 
 __device__ __forceinline__ void decode_tile(int tile, const int* tstart, int ng, int ntn, int& g, int& mt, int& nt) {
@@ -165,16 +213,17 @@ __device__ __forceinline__ void decode_tile(int tile, const int* tstart, int ng,
 // byte offset of 16-byte chunk j of row r in a [32 rows][64 B] box stored with SWIZZLE_64B
 __device__ __forceinline__ uint32_t sw64(int r, int j) { return r * 64 + ((j ^ ((r >> 1) & 3)) << 4); }
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2,
                const __grid_constant__ CUtensorMap tmX, Params p)
 {
-    using CF = Cfg<BN, A_MN>;
+    using CF = Cfg<BN, A_MN, CG>;
     constexpr int STAGES = CF::STAGES;
     constexpr uint32_t B_STAGE = CF::B_STAGE;
     constexpr uint32_t TMEM_COLS = 2 * BN;
+    constexpr int BNC = BN / CG;                          // B rows (N) loaded by this CTA
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
@@ -190,12 +239,16 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ntn = p.N / BN;
+    const uint32_t rank = CG == 2 ? cta_rank() : 0;   // CTA within the pair
+    const bool leader = rank == 0;
+    const int cluster = blockIdx.x / CG, n_clusters = gridDim.x / CG;
+    constexpr int MT = BM * CG;                        // rows of A per (pair) tile
 
     if (threadIdx.x == 0) {
         int acc = 0;
         for (int g = 0; g < p.n_groups; ++g) {
             tstart[g] = acc;
-            const int mt = p.mode == GEMM_M_GROUPED ? ceil_div(p.grp_rows[g], BM) : p.M / BM;
+            const int mt = p.mode == GEMM_M_GROUPED ? ceil_div(p.grp_rows[g], MT) : p.M / MT;
             acc += mt * ntn;
         }
         tstart[p.n_groups] = acc;
@@ -211,72 +264,83 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     }
     if (warp == 1 && lane == 0) {
         for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-        for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], kEpiWarps); }
+        for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], kEpiWarps * CG); }
         for (int i = 0; i < kEpiWarps; ++i) mbar_init(&abar[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 2) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(TMEM_COLS));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if constexpr (CG == 1) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                         "r"(TMEM_COLS));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                         "r"(TMEM_COLS));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        }
     }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (CG == 2) cluster_sync();
+    else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     const int total = tstart[p.n_groups];
 
     if (warp == 0) {
-        // ===================== TMA producer =====================
+        // ===================== TMA producer (each CTA loads its own rows) =====================
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+            for (int tile = cluster; tile < total; tile += n_clusters) {
                 int g, mt, nt;
                 decode_tile(tile, tstart, p.n_groups, ntn, g, mt, nt);
-                const int n0 = nt * BN;
+                const int nb = nt * BN + (int)rank * BNC;      // this CTA's B rows / columns
                 int num_kb, arow, brow;
                 if (p.mode == GEMM_M_GROUPED) {
                     num_kb = p.K / BK;
-                    arow = p.grp_off[g] + mt * BM;
+                    arow = p.grp_off[g] + mt * MT + (int)rank * BM;
                     brow = ((g / p.gpw) % p.n_weights) * (B_MN ? p.K : p.N);
                 } else {
                     num_kb = round_up(p.grp_rows[g], kRowAlign) / BK;
                     arow = p.grp_off[g];
                     brow = p.grp_off[g];
                 }
-                const int m0 = mt * BM;
+                const int m0 = mt * MT + (int)rank * BM;
                 for (int kb = 0; kb < num_kb; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    mbar_expect_tx(&full[stage], A_STAGE + B_STAGE);
+                    if (leader) mbar_expect_tx(&full[stage], CG * (A_STAGE + B_STAGE));
                     uint8_t* a_dst = sA + stage * A_STAGE;
                     uint8_t* b_dst = sB + stage * B_STAGE;
+#define LOAD(map, dst, c0, c1)                                                               \
+    do {                                                                                     \
+        if constexpr (CG == 1) tma_load_2d(map, &full[stage], dst, c0, c1);                  \
+        else tma_load_2d_pair(map, &full[stage], dst, c0, c1);                               \
+    } while (0)
                     if (A_MN) {
 #pragma unroll
-                        for (int i = 0; i < BM / 64; ++i)
-                            tma_load_2d(&tmA, &full[stage], a_dst + i * 8192, m0 + 64 * i, arow + kb * BK);
+                        for (int i = 0; i < BM / 64; ++i) LOAD(&tmA, a_dst + i * 8192, m0 + 64 * i, arow + kb * BK);
                     } else {
-                        tma_load_2d(&tmA, &full[stage], a_dst, kb * BK, arow);
+                        LOAD(&tmA, a_dst, kb * BK, arow);
                     }
                     if (B_MN) {
 #pragma unroll
-                        for (int i = 0; i < BN / 64; ++i)
-                            tma_load_2d(&tmB, &full[stage], b_dst + i * 8192, n0 + 64 * i, brow + kb * BK);
+                        for (int i = 0; i < BNC / 64; ++i) LOAD(&tmB, b_dst + i * 8192, nb + 64 * i, brow + kb * BK);
                     } else {
-                        tma_load_2d(&tmB, &full[stage], b_dst, kb * BK, brow + n0);
+                        LOAD(&tmB, b_dst, kb * BK, brow + nb);
                     }
+#undef LOAD
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }
         }
     } else if (warp == 1) {
-        // ===================== MMA issuer (one thread) =====================
-        if (lane == 0) {
-            constexpr uint32_t idesc = instr_desc<BN, A_MN, B_MN>();
+        // ===================== MMA issuer (one thread of the leader CTA) =====================
+        if (lane == 0 && leader) {
+            constexpr uint32_t idesc = instr_desc<BN, A_MN, B_MN, CG>();
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
-            for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
+            for (int tile = cluster; tile < total; tile += n_clusters, ++it) {
                 int g, mt, nt;
                 decode_tile(tile, tstart, p.n_groups, ntn, g, mt, nt);
                 const int num_kb = p.mode == GEMM_M_GROUPED ? p.K / BK : round_up(p.grp_rows[g], kRowAlign) / BK;
@@ -292,16 +356,16 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                     const uint32_t b_base = smem_u32(sB + stage * B_STAGE);
 #pragma unroll
                     for (int k = 0; k < BK / UMMA_K; ++k)
-                        tc_mma(tmem_d, operand_desc<A_MN>(a_base, k), operand_desc<B_MN>(b_base, k), idesc,
-                               (kb | k) != 0 ? 1u : 0u);
-                    tc_commit(&empty[stage]);
+                        tc_mma<CG>(tmem_d, operand_desc<A_MN>(a_base, k), operand_desc<B_MN>(b_base, k), idesc,
+                                   (kb | k) != 0 ? 1u : 0u);
+                    tc_commit<CG>(&empty[stage]);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
-                tc_commit(&tfull[acc]);
+                tc_commit<CG>(&tfull[acc]);
             }
         }
     } else if (warp >= 4) {
-        // ===================== epilogue: 8 warps =====================
+        // ===================== epilogue: 8 warps per CTA =====================
         // warp w may only touch TMEM lanes 32*(w%4)..; warps w and w+4 split the columns
         const int q = warp & 3;
         const int ew = warp - 4;
@@ -313,7 +377,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         uint64_t* xbar = &abar[ew];
         uint32_t xphase = 0;
         int it = 0;
-        for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
+        for (int tile = cluster; tile < total; tile += n_clusters, ++it) {
             int g, mt, nt;
             decode_tile(tile, tstart, p.n_groups, ntn, g, mt, nt);
             const int acc = it & 1;
@@ -321,65 +385,70 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             const bool has_k = p.mode == GEMM_M_GROUPED ? (p.K > 0) : (p.grp_rows[g] > 0);
             const int n0 = nt * BN;
             if constexpr (CF::kStaged) {
-                const int row0 = p.grp_off[g] + mt * BM + q * 32;      // this warp's 32 rows
-                if (p.epi == EPI_DACT && lane == 0) {                    // prefetch act'(A), chunk cc0
+                const int mrow = mt * MT + (int)rank * BM;                // first row of this CTA
+                const int row0 = p.grp_off[g] + mrow + q * 32;            // this warp's 32 rows
+                // a pair tile may extend past the group's 128-aligned rows: skip that half
+                const bool live = mrow < round_up(p.grp_rows[g], kRowAlign);
+                if (live && p.epi == EPI_DACT && lane == 0) {             // prefetch act'(A)
                     mbar_expect_tx(xbar, 2048);
                     tma_load_2d(&tmX, xbar, sX, n0 + cc0 * 32, row0);
                 }
                 mbar_wait(&tfull[acc], acc_phase);
                 tc_fence_after();
+                if (live) {
 #pragma unroll 1
-                for (int cc = cc0; cc < cc1; ++cc) {
-                    uint32_t v[32];
-                    tmem_ld32(tmem_base + acc * BN + cc * 32 + ((uint32_t)(q * 32) << 16), v);
-                    float f[32];
+                    for (int cc = cc0; cc < cc1; ++cc) {
+                        uint32_t v[32];
+                        tmem_ld32(tmem_base + acc * BN + cc * 32 + ((uint32_t)(q * 32) << 16), v);
+                        float f[32];
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) f[i] = has_k ? __uint_as_float(v[i]) : 0.f;
-                    if (p.epi == EPI_DACT) {
-                        mbar_wait(xbar, xphase);
-                        xphase ^= 1;
+                        for (int i = 0; i < 32; ++i) f[i] = has_k ? __uint_as_float(v[i]) : 0.f;
+                        if (p.epi == EPI_DACT) {
+                            mbar_wait(xbar, xphase);
+                            xphase ^= 1;
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            float a8[8];
-                            unpack16<bf16>(*reinterpret_cast<const uint4*>(sX + sw64(lane, j)), a8);
+                            for (int j = 0; j < 4; ++j) {
+                                float a8[8];
+                                unpack16<bf16>(*reinterpret_cast<const uint4*>(sX + sw64(lane, j)), a8);
 #pragma unroll
-                            for (int i = 0; i < 8; ++i) f[8 * j + i] *= a8[i];
+                                for (int i = 0; i < 8; ++i) f[8 * j + i] *= a8[i];
+                            }
+                            __syncwarp();
+                            if (cc + 1 < cc1 && lane == 0) {
+                                mbar_expect_tx(xbar, 2048);
+                                tma_load_2d(&tmX, xbar, sX, n0 + (cc + 1) * 32, row0);
+                            }
                         }
+                        // the previous chunk's TMA stores must have read the staging buffers
+                        if (lane == 0) bulk_wait_read0();
                         __syncwarp();
-                        if (cc + 1 < cc1 && lane == 0) {
-                            mbar_expect_tx(xbar, 2048);
-                            tma_load_2d(&tmX, xbar, sX, n0 + (cc + 1) * 32, row0);
+                        if (p.epi == EPI_ACT) {
+                            float h[32], gr[32];
+#pragma unroll
+                            for (int i = 0; i < 32; ++i) act_fwd_grad_fast(p.act, f[i], h[i], gr[i]);
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                *reinterpret_cast<uint4*>(sO0 + sw64(lane, j)) = pack16<bf16>(h + 8 * j);
+                                *reinterpret_cast<uint4*>(sO1 + sw64(lane, j)) = pack16<bf16>(gr + 8 * j);
+                            }
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 4; ++j)
+                                *reinterpret_cast<uint4*>(sO0 + sw64(lane, j)) = pack16<bf16>(f + 8 * j);
                         }
-                    }
-                    // the previous chunk's TMA stores must have read the staging buffers
-                    if (lane == 0) bulk_wait_read0();
-                    __syncwarp();
-                    if (p.epi == EPI_ACT) {
-                        float h[32], gr[32];
-#pragma unroll
-                        for (int i = 0; i < 32; ++i) act_fwd_grad_fast(p.act, f[i], h[i], gr[i]);
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            *reinterpret_cast<uint4*>(sO0 + sw64(lane, j)) = pack16<bf16>(h + 8 * j);
-                            *reinterpret_cast<uint4*>(sO1 + sw64(lane, j)) = pack16<bf16>(gr + 8 * j);
+                        fence_proxy_async();
+                        __syncwarp();
+                        if (lane == 0) {
+                            tma_store_2d(&tmC, sO0, n0 + cc * 32, row0);
+                            if (p.epi == EPI_ACT) tma_store_2d(&tmC2, sO1, n0 + cc * 32, row0);
+                            bulk_commit();
                         }
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < 4; ++j)
-                            *reinterpret_cast<uint4*>(sO0 + sw64(lane, j)) = pack16<bf16>(f + 8 * j);
-                    }
-                    fence_proxy_async();
-                    __syncwarp();
-                    if (lane == 0) {
-                        tma_store_2d(&tmC, sO0, n0 + cc * 32, row0);
-                        if (p.epi == EPI_ACT) tma_store_2d(&tmC2, sO1, n0 + cc * 32, row0);
-                        bulk_commit();
                     }
                 }
             } else {
                 mbar_wait(&tfull[acc], acc_phase);
                 tc_fence_after();
-                const long orow = (long)mt * BM + q * 32 + lane;
+                const long orow = (long)mt * MT + (int)rank * BM + q * 32 + lane;
 #pragma unroll 1
                 for (int cc = cc0; cc < cc1; ++cc) {
                     uint32_t v[32];
@@ -403,15 +472,22 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (lane == 0) {
+                if constexpr (CG == 1) mbar_arrive(&tempty[acc]);
+                else mbar_arrive_cluster(&tempty[acc], 0);        // the leader's MMA waits on it
+            }
         }
         if (CF::kStaged && lane == 0) bulk_wait0();
     }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (CG == 2) cluster_sync();
+    else __syncthreads();
     if (warp == 2) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+        if constexpr (CG == 1)
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+        else
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
     }
 }
 
@@ -450,10 +526,12 @@ static bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t o
     return r == CUDA_SUCCESS;
 }
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, int CG>
 static int launch_cfg(const GemmArgs& a, int num_sms, cudaStream_t s)
 {
-    using CF = Cfg<BN, A_MN>;
+    using CF = Cfg<BN, A_MN, CG>;
+    static_assert(CF::STAGES >= 3, "shared-memory ring too shallow");
+    static_assert(CF::kSmem <= kSmemLimit, "shared memory over the per-block limit");
     CUtensorMap ta, tb, tcm, tc2, tx;
     memset(&tcm, 0, sizeof(tcm));
     memset(&tc2, 0, sizeof(tc2));
@@ -462,28 +540,52 @@ static int launch_cfg(const GemmArgs& a, int num_sms, cudaStream_t s)
     if (A_MN) ok = make_map(&ta, a.A, a.M, a.a_rows, a.lda, 64, 64);
     else ok = make_map(&ta, a.A, a.K, a.a_rows, a.lda, 64, BM);
     if (B_MN) ok = ok && make_map(&tb, a.B, a.N, a.b_rows, a.ldb, 64, 64);
-    else ok = ok && make_map(&tb, a.B, a.K, a.b_rows, a.ldb, 64, BN);
+    else ok = ok && make_map(&tb, a.B, a.K, a.b_rows, a.ldb, 64, BN / CG);
     if (CF::kStaged) {
         ok = ok && make_map(&tcm, a.C, a.N, a.c_rows, a.ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
         if (a.epi == EPI_ACT) ok = ok && make_map(&tc2, a.C2, a.N, a.c_rows, a.ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
         if (a.epi == EPI_DACT) ok = ok && make_map(&tx, a.aux, a.N, a.c_rows, a.ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
     }
     if (!ok) return -1;
-    Params p{a.mode, a.n_groups, a.gpw, a.n_weights > 0 ? a.n_weights : (1 << 30), a.epi, a.act, a.accumulate, a.M, a.N, a.K, a.grp_rows, a.grp_off,
-             a.C, a.ldc, a.c_group_stride};
+    Params p{a.mode, a.n_groups, a.gpw, a.n_weights > 0 ? a.n_weights : (1 << 30), a.epi, a.act, a.accumulate,
+             a.M, a.N, a.K, a.grp_rows, a.grp_off, a.C, a.ldc, a.c_group_stride};
     constexpr size_t smem = CF::kSmem;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(tc_gemm_kernel<BN, A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(tc_gemm_kernel<BN, A_MN, B_MN, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
         attr = true;
     }
-    // persistent grid: at most one CTA per SM, never more CTAs than the upper bound of tiles
+    // persistent grid: at most one CTA per SM (pairs on one TPC when CG == 2), never more
+    // (pair) tiles than the upper bound of tiles
     long max_tiles;
-    if (a.mode == GEMM_M_GROUPED) max_tiles = (long)ceil_div(a.max_rows, BM) * a.n_groups * (a.N / BN);
-    else max_tiles = (long)(a.M / BM) * (a.N / BN) * a.n_groups;
-    const int grid = (int)std::max<long>(1, std::min<long>(num_sms, max_tiles));
-    tc_gemm_kernel<BN, A_MN, B_MN><<<grid, kThreads, smem, s>>>(ta, tb, tcm, tc2, tx, p);
+    if (a.mode == GEMM_M_GROUPED) max_tiles = (long)ceil_div(a.max_rows, BM * CG) * a.n_groups * (a.N / BN);
+    else max_tiles = (long)(a.M / (BM * CG)) * (a.N / BN) * a.n_groups;
+    const int clusters = (int)std::max<long>(1, std::min<long>(num_sms / CG, max_tiles));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(clusters * CG);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attrs[1];
+    attrs[0].id = cudaLaunchAttributeClusterDimension;
+    attrs[0].val.clusterDim.x = CG;
+    attrs[0].val.clusterDim.y = 1;
+    attrs[0].val.clusterDim.z = 1;
+    cfg.attrs = attrs;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, A_MN, B_MN, CG>, ta, tb, tcm, tc2, tx, p) != cudaSuccess)
+        return -1;
     return 1;
+}
+
+template <int BN, bool A_MN, bool B_MN>
+static int launch_cg(const GemmArgs& a, int num_sms, cudaStream_t s)
+{
+    // CTA pairs need 256-row (pair) tiles: always possible for M-grouped GEMMs (a pair tile's
+    // upper half past a group is computed but not stored), for K-grouped when M % 256 == 0
+    const bool pair = a.mode == GEMM_M_GROUPED || a.M % (2 * BM) == 0;
+    return pair ? launch_cfg<BN, A_MN, B_MN, 2>(a, num_sms, s) : launch_cfg<BN, A_MN, B_MN, 1>(a, num_sms, s);
 }
 
 }  // namespace tc
@@ -509,11 +611,11 @@ int launch_gemm_tc(const GemmArgs& a, int num_sms, cudaStream_t s)
 {
     if (!gemm_tc_supported(a)) return -1;
     const bool bn256 = a.N % 256 == 0;
-    if (!a.a_mn && !a.b_mn) return bn256 ? tc::launch_cfg<256, false, false>(a, num_sms, s)
-                                         : tc::launch_cfg<128, false, false>(a, num_sms, s);
-    if (!a.a_mn && a.b_mn) return bn256 ? tc::launch_cfg<256, false, true>(a, num_sms, s)
-                                        : tc::launch_cfg<128, false, true>(a, num_sms, s);
-    return bn256 ? tc::launch_cfg<256, true, true>(a, num_sms, s) : tc::launch_cfg<128, true, true>(a, num_sms, s);
+    if (!a.a_mn && !a.b_mn) return bn256 ? tc::launch_cg<256, false, false>(a, num_sms, s)
+                                         : tc::launch_cg<128, false, false>(a, num_sms, s);
+    if (!a.a_mn && a.b_mn) return bn256 ? tc::launch_cg<256, false, true>(a, num_sms, s)
+                                        : tc::launch_cg<128, false, true>(a, num_sms, s);
+    return bn256 ? tc::launch_cg<256, true, true>(a, num_sms, s) : tc::launch_cg<128, true, true>(a, num_sms, s);
 }
 
 }  // namespace lancet
