@@ -15,7 +15,8 @@ from dataclasses import dataclass
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblancet_moe.so")
+# LANCET_LIB: alternative build of the same library (A/B experiments); default the in-tree build
+LIB_PATH = os.environ.get("LANCET_LIB") or os.path.join(_HERE, "liblancet_moe.so")
 
 STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_CUDA", 3: "ERR_NCCL", 4: "ERR_NOMEM", 5: "ERR_STATE",
           6: "ERR_UNSUPPORTED"}
