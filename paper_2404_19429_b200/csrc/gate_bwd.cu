@@ -167,152 +167,6 @@ unpermute_gate_bwd_kernel(const Elt* __restrict__ dxe, const int* __restrict__ i
     }
 }
 
-// ---- dim-sliced variants for E <= 8 ---------------------------------------------------------
-// K6': block = 32 tokens x (128 threads x V dims).  Prologue: one warp per token computes
-// dlogit (smem + global) and the k source rows.  Main loop: each thread keeps its V x 8 slice
-// of Wg in registers and streams the block's tokens with kU tokens' row loads in flight.
-constexpr int kSliceThreads = 128;
-constexpr int kK6Tok = 32;
-constexpr int kK6U = 4;
-
-template <typename Elt, int KK>
-__global__ void __launch_bounds__(kSliceThreads)
-k6_dimslice_kernel(const Elt* __restrict__ dxe, const int* __restrict__ idx, const int* __restrict__ slot,
-                   const float* __restrict__ wts, const float* __restrict__ g, const float* __restrict__ logits,
-                   const float* __restrict__ wg, const int* __restrict__ send_off, int renorm, int t0, int t1,
-                   int k, int d, int E, Elt* __restrict__ dx, float* __restrict__ dlogit)
-{
-    constexpr int V = Vec16<Elt>::N;
-    __shared__ __align__(16) float sdl[kK6Tok][8];
-    __shared__ int srow[kK6Tok][KK];
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int tb = t0 + blockIdx.x * kK6Tok;
-    const int tn = min(kK6Tok, t1 - tb);
-    for (int q = w; q < kK6Tok; q += kSliceThreads / 32) {
-        if (q >= tn) {
-            if (lane < 8) sdl[q][lane] = 0.f;
-            if (lane < KK) srow[q][lane] = -1;
-            continue;
-        }
-        const int t = tb + q;
-        int rows[KK], ids[KK];
-        float wj[KK], gj[KK];
-        choices<KK>(idx, slot, wts, g, send_off, t, k, lane, rows, wj, ids, gj);
-        float sg = 0.f;
-#pragma unroll
-        for (int j = 0; j < KK; ++j)
-            if (j < k) sg = fmaf(gj[j], wj[j], sg);
-        const float l = lane < E ? logits[(size_t)t * E + lane] : -INFINITY;
-        const float m = warp_max(l);
-        const float ex = lane < E ? expf(l - m) : 0.f;
-        const float s = warp_sum(ex);
-        float gt = 0.f, wsel = 0.f;
-        bool sel = false;
-#pragma unroll
-        for (int j = 0; j < KK; ++j)
-            if (j < k && ids[j] == lane) { gt = gj[j]; wsel = wj[j]; sel = true; }
-        const float dl = renorm ? (sel ? wsel * (gt - sg) : 0.f) : (ex / s) * (gt - sg);
-        if (lane < 8) sdl[q][lane] = lane < E ? dl : 0.f;
-        if (lane < E && blockIdx.y == 0) dlogit[(size_t)t * E + lane] = dl;
-        if (lane < KK) srow[q][lane] = rows[lane];
-    }
-    __syncthreads();
-    const int i0 = (blockIdx.y * kSliceThreads + threadIdx.x) * V;
-    if (i0 >= d) return;
-    float wr[V][8];
-#pragma unroll
-    for (int a = 0; a < V; ++a)
-#pragma unroll
-        for (int e = 0; e < 8; ++e) wr[a][e] = e < E ? __ldg(wg + (size_t)(i0 + a) * E + e) : 0.f;
-    for (int q0 = 0; q0 < tn; q0 += kK6U) {
-        uint4 rd[kK6U][KK];
-#pragma unroll
-        for (int u = 0; u < kK6U; ++u)
-#pragma unroll
-            for (int j = 0; j < KK; ++j) {
-                const int row = q0 + u < tn ? srow[q0 + u][j] : -1;
-                if (row >= 0) rd[u][j] = ld_nc_v4(dxe + (size_t)row * d + i0);
-            }
-#pragma unroll
-        for (int u = 0; u < kK6U; ++u) {
-            const int q = q0 + u;
-            if (q >= tn) break;
-            float o[V];
-#pragma unroll
-            for (int a = 0; a < V; ++a) o[a] = 0.f;
-#pragma unroll
-            for (int j = 0; j < KK; ++j) {
-                if (srow[q][j] >= 0) {
-                    float f[V];
-                    unpack16<Elt>(rd[u][j], f);
-#pragma unroll
-                    for (int a = 0; a < V; ++a) o[a] += f[a];
-                }
-            }
-            const float4 l0 = *reinterpret_cast<const float4*>(&sdl[q][0]);
-            const float4 l1 = *reinterpret_cast<const float4*>(&sdl[q][4]);
-            const float dl[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
-#pragma unroll
-            for (int a = 0; a < V; ++a)
-#pragma unroll
-                for (int e = 0; e < 8; ++e) o[a] = fmaf(dl[e], wr[a][e], o[a]);
-            st_v4(dx + (size_t)(tb + q) * d + i0, pack16<Elt>(o));
-        }
-    }
-}
-
-// K7': block = 32 tokens x (128 threads x V dims); dWg partial per block in registers.
-constexpr int kK7Tok = 32;
-constexpr int kK7U = 8;
-
-template <typename Elt>
-__global__ void __launch_bounds__(kSliceThreads)
-k7_dimslice_kernel(const Elt* __restrict__ x, const float* __restrict__ dlogit, int T, int d, int E,
-                   float* __restrict__ partial)
-{
-    constexpr int V = Vec16<Elt>::N;
-    __shared__ __align__(16) float sdl[kK7Tok][8];
-    const int tb = blockIdx.x * kK7Tok;
-    const int tn = min(kK7Tok, T - tb);
-    for (int q = threadIdx.x; q < kK7Tok * 8; q += kSliceThreads) {
-        const int r = q / 8, e = q % 8;
-        sdl[r][e] = (r < tn && e < E) ? dlogit[(size_t)(tb + r) * E + e] : 0.f;
-    }
-    __syncthreads();
-    const int i0 = (blockIdx.y * kSliceThreads + threadIdx.x) * V;
-    if (i0 >= d) return;
-    float acc[V][8];
-#pragma unroll
-    for (int a = 0; a < V; ++a)
-#pragma unroll
-        for (int e = 0; e < 8; ++e) acc[a][e] = 0.f;
-    for (int q0 = 0; q0 < tn; q0 += kK7U) {
-        uint4 rx[kK7U];
-#pragma unroll
-        for (int u = 0; u < kK7U; ++u)
-            if (q0 + u < tn) rx[u] = ld_nc_v4(x + (size_t)(tb + q0 + u) * d + i0);
-#pragma unroll
-        for (int u = 0; u < kK7U; ++u) {
-            if (q0 + u >= tn) break;
-            float xf[V];
-            unpack16<Elt>(rx[u], xf);
-            const float4 l0 = *reinterpret_cast<const float4*>(&sdl[q0 + u][0]);
-            const float4 l1 = *reinterpret_cast<const float4*>(&sdl[q0 + u][4]);
-            const float dl[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
-#pragma unroll
-            for (int a = 0; a < V; ++a)
-#pragma unroll
-                for (int e = 0; e < 8; ++e) acc[a][e] = fmaf(xf[a], dl[e], acc[a][e]);
-        }
-    }
-    float* out = partial + ((size_t)blockIdx.x * d + i0) * E;
-#pragma unroll
-    for (int a = 0; a < V; ++a)
-#pragma unroll
-        for (int e = 0; e < 8; ++e)
-            if (e < E) out[a * E + e] = acc[a][e];
-}
-
 constexpr int kDwgTok = 64;      // tokens per partial block
 constexpr int kDwgThreads = 256; // each thread owns 4 consecutive dims -> 1024 dims per block
 constexpr int kDwgE = 8;         // experts per pass (32 accumulators per thread)
@@ -466,21 +320,6 @@ int launch_unpermute_gate_bwd(const DispatchArgs& a, const void* dxe, const floa
                               cudaStream_t s)
 {
     if (t1 <= t0) return 0;
-    if (a.E <= 8) {                      // dim-sliced: Wg slice in registers
-        const int V = is_bf16 ? 8 : 4;
-        dim3 grid(ceil_div(t1 - t0, kK6Tok), ceil_div(a.d, kSliceThreads * V));
-        LANCET_DISPATCH_K(a.k, {
-            if (is_bf16)
-                k6_dimslice_kernel<bf16, KK><<<grid, kSliceThreads, 0, s>>>(
-                    (const bf16*)dxe, a.idx, a.slot, a.w, g, logits, wg, a.send_off, renorm, t0, t1, a.k, a.d, a.E,
-                    (bf16*)dx, dlogit);
-            else
-                k6_dimslice_kernel<float, KK><<<grid, kSliceThreads, 0, s>>>(
-                    (const float*)dxe, a.idx, a.slot, a.w, g, logits, wg, a.send_off, renorm, t0, t1, a.k, a.d, a.E,
-                    (float*)dx, dlogit);
-        });
-        return 1;
-    }
     const bool sm = !gate_bwd_needs_wgT(a.d, a.E);
     LANCET_DISPATCH_K(a.k, {
         if (is_bf16) {
@@ -494,22 +333,11 @@ int launch_unpermute_gate_bwd(const DispatchArgs& a, const void* dxe, const floa
     return 1;
 }
 
-size_t dwg_partial_floats(int T, int d, int E) { return (size_t)ceil_div(T, std::min(kDwgTok, kK7Tok)) * d * E; }
+size_t dwg_partial_floats(int T, int d, int E) { return (size_t)ceil_div(T, kDwgTok) * d * E; }
 
 int launch_dwg(const void* x, const float* dlogit, int T, int d, int E, float* partial,
                float* dwg, bool is_bf16, cudaStream_t s)
 {
-    if (E <= 8) {
-        const int V = is_bf16 ? 8 : 4;
-        const int nb = ceil_div(T, kK7Tok);
-        dim3 grid(nb, ceil_div(d, kSliceThreads * V));
-        if (is_bf16)
-            k7_dimslice_kernel<bf16><<<grid, kSliceThreads, 0, s>>>((const bf16*)x, dlogit, T, d, E, partial);
-        else
-            k7_dimslice_kernel<float><<<grid, kSliceThreads, 0, s>>>((const float*)x, dlogit, T, d, E, partial);
-        dwg_reduce_kernel<<<ceil_div(d * E, 32), 256, 0, s>>>(partial, nb, d * E, dwg);
-        return 2;
-    }
     const int nb = ceil_div(T, kDwgTok);
     dim3 grid(nb, ceil_div(d, kDwgThreads * 4), ceil_div(E, kDwgE));
     if (is_bf16)
