@@ -55,6 +55,7 @@ struct lancet_ctx {
     void* dxcomb = nullptr;    // [rows_src][d]  grad of expert inputs returned (world > 1)
     float* g = nullptr;  float* dlogit = nullptr;  float* dwg_partial = nullptr;
     float* wgT = nullptr;      // [E][d] transposed gate (backward, coalesced dx gate term)
+    int* prow = nullptr;       // [T][k] packed source row of each choice (-1 dropped), from K5
     int* counts_dev = nullptr;   // [E][n] send counts, then [G][E_l][n] recv counts
     int* grp_dev = nullptr;      // expert-side group table: rows[n_groups] | off[n_groups]
 

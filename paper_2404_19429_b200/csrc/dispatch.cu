@@ -8,7 +8,8 @@
 // K4 combine:   "Reverting tokens to their original order yields the MoE layer's output"
 //               (gather): y_t = sum_{admitted j} w_tj o_tj as an fp32 fma chain
 //               over j in order, dropped choices contribute 0 (R6).
-// K5 combine backward:  g_tj = <dy_t, o_tj>, dcomb[off_e + slot] = w_tj dy_t.
+// K5 combine backward:  g_tj = <dy_t, o_tj>, dcomb[off_e + slot] = w_tj dy_t; also dlogit
+//               (softmax Jacobian, R3) and the packed source rows for K6/K7.
 // (K6 dispatch backward + gate term and K7 dWg live in gate_bwd.cu.)
 //
 // All token kernels are templated on KK >= k (compile-time top-k width) so a lane keeps the
@@ -140,7 +141,9 @@ combine_bwd_kernel(const Elt* __restrict__ dy, const Elt* __restrict__ comb,
                    const int* __restrict__ idx, const int* __restrict__ slot,
                    const float* __restrict__ wts, const int* __restrict__ send_off,
                    const int* __restrict__ send_rows, int t0, int t1, int k, int d,
-                   float* __restrict__ g, Elt* __restrict__ dcomb, int tok_blocks)
+                   float* __restrict__ g, Elt* __restrict__ dcomb, int tok_blocks,
+                   const float* __restrict__ logits, int E, int renorm, float* __restrict__ dlogit,
+                   int* __restrict__ prow)
 {
     constexpr int V = Vec16<Elt>::N;
     constexpr int U = 2;
@@ -196,12 +199,37 @@ combine_bwd_kernel(const Elt* __restrict__ dy, const Elt* __restrict__ comb,
             }
         }
     }
+    float gj[KK];
+    float sg = 0.f;                                    // sum_j g_j w_j
+    int myrow = -1;
 #pragma unroll
     for (int j = 0; j < KK; ++j) {
+        gj[j] = 0.f;
         if (j < k) {
             const float s = warp_sum(part[j]);
-            if (lane == 0) g[(size_t)t * k + j] = rows[j] >= 0 ? s : 0.f;
+            gj[j] = rows[j] >= 0 ? s : 0.f;
+            if (lane == 0) g[(size_t)t * k + j] = gj[j];
+            sg = fmaf(gj[j], wj[j], sg);
+            if (lane == j) myrow = rows[j];
         }
+    }
+    // inputs of the gate backward (K6/K7): packed source rows and dlogit from the softmax
+    // Jacobian (R3): p_e (g~_e - sg), or renormalised at the selected experts
+    if (lane < k) prow[(size_t)t * k + lane] = myrow;
+    const float* lr = logits + (size_t)t * E;
+    float m = -INFINITY;
+    for (int e = lane; e < E; e += 32) m = fmaxf(m, lr[e]);
+    m = warp_max(m);
+    float se = 0.f;
+    for (int e = lane; e < E; e += 32) se += expf(lr[e] - m);
+    se = warp_sum(se);
+    for (int e = lane; e < E; e += 32) {
+        float gt = 0.f, wsel = 0.f;
+        bool sel = false;
+#pragma unroll
+        for (int j = 0; j < KK; ++j)
+            if (j < k && ids[j] == e) { gt = gj[j]; wsel = wj[j]; sel = true; }
+        dlogit[(size_t)t * E + e] = renorm ? (sel ? wsel * (gt - sg) : 0.f) : (expf(lr[e] - m) / se) * (gt - sg);
     }
 }
 
@@ -260,7 +288,8 @@ int launch_combine(const DispatchArgs& a, const void* comb, void* y, int t0, int
 }
 
 int launch_combine_bwd(const DispatchArgs& a, const void* dy, const void* comb, float* g,
-                       void* dcomb, int t0, int t1, bool zero_pads, bool is_bf16, cudaStream_t s)
+                       void* dcomb, int t0, int t1, bool zero_pads, const float* logits, int renorm,
+                       float* dlogit, int* prow, bool is_bf16, cudaStream_t s)
 {
     const int tok_blocks = ceil_div(t1 - t0, kWarpsPerBlock);
     const int grid = tok_blocks + (zero_pads ? a.E : 0);
@@ -269,11 +298,13 @@ int launch_combine_bwd(const DispatchArgs& a, const void* dy, const void* comb, 
         if (is_bf16)
             combine_bwd_kernel<bf16, KK><<<grid, 256, 0, s>>>((const bf16*)dy, (const bf16*)comb, a.idx,
                                                              a.slot, a.w, a.send_off, a.send_rows, t0, t1,
-                                                             a.k, a.d, g, (bf16*)dcomb, tok_blocks);
+                                                             a.k, a.d, g, (bf16*)dcomb, tok_blocks, logits, a.E,
+                                                             renorm, dlogit, prow);
         else
             combine_bwd_kernel<float, KK><<<grid, 256, 0, s>>>((const float*)dy, (const float*)comb, a.idx,
                                                               a.slot, a.w, a.send_off, a.send_rows, t0, t1,
-                                                              a.k, a.d, g, (float*)dcomb, tok_blocks);
+                                                              a.k, a.d, g, (float*)dcomb, tok_blocks, logits, a.E,
+                                                              renorm, dlogit, prow);
     });
     return 1;
 }

@@ -1,10 +1,10 @@
 // gate_bwd.cu -- K6 (dispatch backward + gate term of dx) and K7 (dWg) of the MoE layer.
 //
 //   dx_t     = sum_{admitted j} dX[row_tj] + sum_e dlogit_te Wg[:, e]
-//   dlogit_t = p_t (g~_t - sum_j g_tj w_tj)                 (softmax Jacobian, R3)
-//            = w_tj (g_tj - sum_j' g_tj' w_tj') at idx_tj   (renormalised weights)
 //   dWg      = x^T dlogit     (local; the data-parallel all-reduce of the replicated gate,
 //                              P:L110, is the caller's)
+// dlogit (softmax Jacobian, R3) and the packed source rows row_tj are produced by
+// K5 (combine_bwd_kernel, dispatch.cu), which already holds g_tj for the token.
 // Top-k and capacity decisions are piecewise constant and carry no gradient.
 #include "common.cuh"
 #include "kernels.h"
@@ -15,155 +15,86 @@ namespace lancet {
 
 namespace {
 
-template <int KK>
-__device__ __forceinline__ void choices(const int* __restrict__ idx, const int* __restrict__ slot,
-                                        const float* __restrict__ wts, const float* __restrict__ g,
-                                        const int* __restrict__ send_off, int t, int k, int lane,
-                                        int (&rows)[KK], float (&wj)[KK], int (&ids)[KK], float (&gj)[KK])
-{
-    int myrow = -1, myidx = -1;
-    float myw = 0.f, myg = 0.f;
-    if (lane < k) {
-        const int s = slot[(size_t)t * k + lane];
-        myidx = idx[(size_t)t * k + lane];
-        myrow = s >= 0 ? send_off[myidx] + s : -1;
-        myw = wts[(size_t)t * k + lane];
-        myg = g[(size_t)t * k + lane];
-    }
-#pragma unroll
-    for (int j = 0; j < KK; ++j) {
-        rows[j] = j < k ? __shfl_sync(0xffffffffu, myrow, j) : -1;
-        wj[j] = __shfl_sync(0xffffffffu, myw, j);
-        ids[j] = __shfl_sync(0xffffffffu, myidx, j);
-        gj[j] = __shfl_sync(0xffffffffu, myg, j);
-    }
-}
-
-// dlogit of token t into sdl[0..E) (and global dlogit), computed by one warp.
-template <int KK>
-__device__ __forceinline__ void token_dlogit(const float* __restrict__ logits, int t, int E, int k, int renorm,
-                                             const int (&ids)[KK], const float (&wj)[KK], const float (&gj)[KK],
-                                             int lane, float* sdl, float* __restrict__ dlogit)
-{
-    float sg = 0.f;                                    // sum_j g_j w_j
-#pragma unroll
-    for (int j = 0; j < KK; ++j)
-        if (j < k) sg = fmaf(gj[j], wj[j], sg);
-    const float* lr = logits + (size_t)t * E;
-    float m = -INFINITY;
-    for (int e = lane; e < E; e += 32) m = fmaxf(m, lr[e]);
-    m = warp_max(m);
-    float s = 0.f;
-    for (int e = lane; e < E; e += 32) s += expf(lr[e] - m);
-    s = warp_sum(s);
-    for (int e = lane; e < E; e += 32) {
-        float gt = 0.f, wsel = 0.f;
-        bool sel = false;
-#pragma unroll
-        for (int j = 0; j < KK; ++j)
-            if (j < k && ids[j] == e) { gt = gj[j]; wsel = wj[j]; sel = true; }
-        const float dl = renorm ? (sel ? wsel * (gt - sg) : 0.f) : (expf(lr[e] - m) / s) * (gt - sg);
-        sdl[e] = dl;
-        dlogit[(size_t)t * E + e] = dl;
-    }
-}
-
 constexpr int kWarps = 8;
-constexpr int kTPW = 2;          // tokens per warp iteration (share every Wg^T vector load)
+constexpr size_t kSmemWgMax = 64 * 1024;
 
-// K6.  Persistent blocks; Wg^T ([E][d] fp32) is staged once per block in shared memory when
-// it fits (kSmemWg), else read through L1 from the transposed copy in global memory.
+// K6: one warp per token, all of the token's row loads in flight (like the combine), the gate
+// term from Wg^T ([E][d] fp32) staged once per persistent block in shared memory (or read
+// through L1 when it does not fit).  dlogit_te is held by lane e and broadcast with shuffles.
 template <typename Elt, int KK, bool SMEM_WG>
 __global__ void __launch_bounds__(kWarps * 32)
-unpermute_gate_bwd_kernel(const Elt* __restrict__ dxe, const int* __restrict__ idx,
-                          const int* __restrict__ slot, const float* __restrict__ wts,
-                          const float* __restrict__ g, const float* __restrict__ logits,
-                          const float* __restrict__ wg, const float* __restrict__ wgT,
-                          const int* __restrict__ send_off, int renorm, int t0, int t1, int k, int d,
-                          int E, Elt* __restrict__ dx, float* __restrict__ dlogit)
+k6_gather_kernel(const Elt* __restrict__ dxe, const int* __restrict__ prow,
+                 const float* __restrict__ dlogit, const float* __restrict__ wgT, int t0, int t1,
+                 int k, int d, int E, Elt* __restrict__ dx)
 {
-    extern __shared__ __align__(16) float ksm[];
+    extern __shared__ __align__(16) float swt[];
     constexpr int V = Vec16<Elt>::N;
+    constexpr int U = 4;                               // 16-byte vectors per lane per pass
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float* sdl = ksm + (size_t)w * kTPW * E;          // [kTPW][E] per warp
     const float* W = wgT;
     if constexpr (SMEM_WG) {
-        float* swt = ksm + (size_t)kWarps * kTPW * E;   // 16-byte aligned (kTPW*E*kWarps*4 % 16 == 0)
         for (int q = threadIdx.x; q < d * E / 4; q += blockDim.x)
             reinterpret_cast<float4*>(swt)[q] = __ldg(reinterpret_cast<const float4*>(wgT) + q);
         __syncthreads();
         W = swt;
     }
     const int nvec = d / V;
-    const int step = gridDim.x * kWarps * kTPW;
-    for (int tb = t0 + (blockIdx.x * kWarps + w) * kTPW; tb < t1; tb += step) {
-        int rows[kTPW][KK];
+    for (int t = t0 + blockIdx.x * kWarps + w; t < t1; t += gridDim.x * kWarps) {
+        const int myrow = lane < k ? prow[(size_t)t * k + lane] : -1;
+        int rows[KK];
 #pragma unroll
-        for (int q = 0; q < kTPW; ++q) {
-            const int t = tb + q;
-            if (t < t1) {
-                int ids[KK];
-                float wj[KK], gj[KK];
-                choices<KK>(idx, slot, wts, g, send_off, t, k, lane, rows[q], wj, ids, gj);
-                token_dlogit<KK>(logits, t, E, k, renorm, ids, wj, gj, lane, sdl + q * E, dlogit);
-            } else {
-#pragma unroll
-                for (int j = 0; j < KK; ++j) rows[q][j] = -1;
-                for (int e = lane; e < E; e += 32) sdl[q * E + e] = 0.f;
-            }
-        }
-        __syncwarp();
-        constexpr int U = 2;
+        for (int j = 0; j < KK; ++j) rows[j] = __shfl_sync(0xffffffffu, myrow, j);
+        const float* dlr = dlogit + (size_t)t * E;
         for (int v0 = lane; v0 < nvec; v0 += 32 * U) {
-            uint4 raw[kTPW][U][KK];
+            uint4 raw[U][KK];
 #pragma unroll
-            for (int q = 0; q < kTPW; ++q)
+            for (int u = 0; u < U; ++u)
 #pragma unroll
-                for (int u = 0; u < U; ++u)
-#pragma unroll
-                    for (int j = 0; j < KK; ++j)
-                        if (rows[q][j] >= 0 && v0 + 32 * u < nvec)
-                            raw[q][u][j] = ld_nc_v4(reinterpret_cast<const uint4*>(dxe + (size_t)rows[q][j] * d) + v0 + 32 * u);
+                for (int j = 0; j < KK; ++j)
+                    if (rows[j] >= 0 && v0 + 32 * u < nvec)
+                        raw[u][j] = ld_nc_v4(reinterpret_cast<const uint4*>(dxe + (size_t)rows[j] * d) + v0 + 32 * u);
+            float acc[U][V];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                const int v = v0 + 32 * u;
-                if (v >= nvec) break;
-                float acc[kTPW][V];
 #pragma unroll
-                for (int q = 0; q < kTPW; ++q) {
+                for (int i = 0; i < V; ++i) acc[u][i] = 0.f;
 #pragma unroll
-                    for (int i = 0; i < V; ++i) acc[q][i] = 0.f;
+                for (int j = 0; j < KK; ++j) {
+                    if (rows[j] >= 0 && v0 + 32 * u < nvec) {
+                        float f[V];
+                        unpack16<Elt>(raw[u][j], f);
 #pragma unroll
-                    for (int j = 0; j < KK; ++j) {
-                        if (rows[q][j] >= 0) {
-                            float f[V];
-                            unpack16<Elt>(raw[q][u][j], f);
+                        for (int i = 0; i < V; ++i) acc[u][i] += f[i];
+                    }
+                }
+            }
+            for (int e0 = 0; e0 < E; e0 += 32) {
+                const float dl_lane = e0 + lane < E ? __ldg(dlr + e0 + lane) : 0.f;
+                const int ne = min(32, E - e0);
+                for (int e = 0; e < ne; ++e) {
+                    const float sv = __shfl_sync(0xffffffffu, dl_lane, e);
+                    const float* wrow = W + (size_t)(e0 + e) * d;
 #pragma unroll
-                            for (int i = 0; i < V; ++i) acc[q][i] += f[i];
+                    for (int u = 0; u < U; ++u) {
+                        const int v = v0 + 32 * u;
+                        if (v >= nvec) break;
+                        const float4* wt = reinterpret_cast<const float4*>(wrow + (size_t)v * V);
+#pragma unroll
+                        for (int h = 0; h < V / 4; ++h) {
+                            const float4 w4 = SMEM_WG ? wt[h] : __ldg(wt + h);
+                            acc[u][4 * h + 0] = fmaf(sv, w4.x, acc[u][4 * h + 0]);
+                            acc[u][4 * h + 1] = fmaf(sv, w4.y, acc[u][4 * h + 1]);
+                            acc[u][4 * h + 2] = fmaf(sv, w4.z, acc[u][4 * h + 2]);
+                            acc[u][4 * h + 3] = fmaf(sv, w4.w, acc[u][4 * h + 3]);
                         }
                     }
                 }
-                for (int e = 0; e < E; ++e) {
-                    const float4* wt = reinterpret_cast<const float4*>(W + (size_t)e * d + (size_t)v * V);
-                    float wv[V];
-#pragma unroll
-                    for (int h = 0; h < V / 4; ++h) {
-                        const float4 w4 = SMEM_WG ? wt[h] : __ldg(wt + h);
-                        wv[4 * h] = w4.x; wv[4 * h + 1] = w4.y; wv[4 * h + 2] = w4.z; wv[4 * h + 3] = w4.w;
-                    }
-#pragma unroll
-                    for (int q = 0; q < kTPW; ++q) {
-                        const float sv = sdl[q * E + e];
-#pragma unroll
-                        for (int i = 0; i < V; ++i) acc[q][i] = fmaf(sv, wv[i], acc[q][i]);
-                    }
-                }
-#pragma unroll
-                for (int q = 0; q < kTPW; ++q)
-                    if (tb + q < t1) st_v4(reinterpret_cast<uint4*>(dx + (size_t)(tb + q) * d) + v, pack16<Elt>(acc[q]));
             }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (v0 + 32 * u < nvec)
+                    st_v4(reinterpret_cast<uint4*>(dx + (size_t)t * d) + v0 + 32 * u, pack16<Elt>(acc[u]));
         }
-        __syncwarp();
     }
 }
 
@@ -235,7 +166,9 @@ dwg_partial_kernel(const Elt* __restrict__ x, const float* __restrict__ dlogit, 
     for (int a = 0; a < 4; ++a) {
         if (i0 + a >= d) break;
         float* out = partial + ((size_t)tb * d + i0 + a) * E + e0;
-        for (int c = 0; c < ne; ++c) out[c] = acc[a][c];
+#pragma unroll
+        for (int c = 0; c < kDwgE; ++c)
+            if (c < ne) out[c] = acc[a][c];
     }
 }
 
@@ -275,8 +208,6 @@ __global__ void transpose_f32_kernel(const float* __restrict__ in, int rows, int
     out[(size_t)c * rows + r] = in[q];
 }
 
-constexpr size_t kSmemWgMax = 96 * 1024;
-
 }  // namespace
 
 #define LANCET_DISPATCH_K(k, ...)                                             \
@@ -293,41 +224,38 @@ int launch_wg_transpose(const float* wg, int d, int E, float* wgT, cudaStream_t 
     return 1;
 }
 
-bool gate_bwd_needs_wgT(int d, int E) { return (size_t)d * E * 4 > kSmemWgMax; }
+bool gate_bwd_needs_wgT(int, int) { return true; }
 
 template <typename Elt, int KK, bool SM>
-static void launch_k6(const DispatchArgs& a, const void* dxe, const float* g, const float* logits,
-                      const float* wg, const float* wgT, int renorm, void* dx, float* dlogit, int t0,
-                      int t1, int num_sms, cudaStream_t s)
+static void launch_k6(const DispatchArgs& a, const void* dxe, const int* prow, const float* dlogit,
+                      const float* wgT, void* dx, int t0, int t1, int num_sms, cudaStream_t s)
 {
-    const size_t smem = sizeof(float) * (kWarps * kTPW * a.E + (SM ? (size_t)a.d * a.E : 0));
+    const size_t smem = SM ? sizeof(float) * (size_t)a.d * a.E : 0;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(unpermute_gate_bwd_kernel<Elt, KK, SM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(kSmemWgMax + 16 * 1024));
+        cudaFuncSetAttribute(k6_gather_kernel<Elt, KK, SM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kSmemWgMax);
         attr = true;
     }
-    const int need = ceil_div(t1 - t0, kWarps * kTPW);
-    const int grid = std::max(1, std::min(need, 2 * num_sms));
-    unpermute_gate_bwd_kernel<Elt, KK, SM><<<grid, kWarps * 32, smem, s>>>(
-        (const Elt*)dxe, a.idx, a.slot, a.w, g, logits, wg, wgT, a.send_off, renorm, t0, t1, a.k, a.d, a.E,
-        (Elt*)dx, dlogit);
+    const int need = ceil_div(t1 - t0, kWarps);
+    const int grid = std::max(1, std::min(need, 4 * num_sms));
+    k6_gather_kernel<Elt, KK, SM><<<grid, kWarps * 32, smem, s>>>((const Elt*)dxe, prow, dlogit, wgT, t0, t1,
+                                                                  a.k, a.d, a.E, (Elt*)dx);
 }
 
-int launch_unpermute_gate_bwd(const DispatchArgs& a, const void* dxe, const float* g,
-                              const float* logits, const float* wg, const float* wgT, int renorm,
-                              void* dx, float* dlogit, int t0, int t1, int num_sms, bool is_bf16,
-                              cudaStream_t s)
+int launch_unpermute_gate_bwd(const DispatchArgs& a, const void* dxe, const int* prow,
+                              const float* dlogit, const float* wgT, void* dx, int t0, int t1,
+                              int num_sms, bool is_bf16, cudaStream_t s)
 {
     if (t1 <= t0) return 0;
-    const bool sm = !gate_bwd_needs_wgT(a.d, a.E);
+    const bool sm = (size_t)a.d * a.E * 4 <= kSmemWgMax;
     LANCET_DISPATCH_K(a.k, {
         if (is_bf16) {
-            if (sm) launch_k6<bf16, KK, true>(a, dxe, g, logits, wg, wgT, renorm, dx, dlogit, t0, t1, num_sms, s);
-            else launch_k6<bf16, KK, false>(a, dxe, g, logits, wg, wgT, renorm, dx, dlogit, t0, t1, num_sms, s);
+            if (sm) launch_k6<bf16, KK, true>(a, dxe, prow, dlogit, wgT, dx, t0, t1, num_sms, s);
+            else launch_k6<bf16, KK, false>(a, dxe, prow, dlogit, wgT, dx, t0, t1, num_sms, s);
         } else {
-            if (sm) launch_k6<float, KK, true>(a, dxe, g, logits, wg, wgT, renorm, dx, dlogit, t0, t1, num_sms, s);
-            else launch_k6<float, KK, false>(a, dxe, g, logits, wg, wgT, renorm, dx, dlogit, t0, t1, num_sms, s);
+            if (sm) launch_k6<float, KK, true>(a, dxe, prow, dlogit, wgT, dx, t0, t1, num_sms, s);
+            else launch_k6<float, KK, false>(a, dxe, prow, dlogit, wgT, dx, t0, t1, num_sms, s);
         }
     });
     return 1;

@@ -33,14 +33,16 @@ struct DispatchArgs {
 int launch_permute(const DispatchArgs& a, const void* x, void* xs, bool is_bf16, cudaStream_t s);
 int launch_combine(const DispatchArgs& a, const void* comb, void* y, int t0, int t1, bool is_bf16,
                    cudaStream_t s);
+// K5: also writes dlogit [T][E] (softmax Jacobian) and prow [T][k] (packed row or -1)
 int launch_combine_bwd(const DispatchArgs& a, const void* dy, const void* comb, float* g,
-                       void* dcomb, int t0, int t1, bool zero_pads, bool is_bf16, cudaStream_t s);
+                       void* dcomb, int t0, int t1, bool zero_pads, const float* logits, int renorm,
+                       float* dlogit, int* prow, bool is_bf16, cudaStream_t s);
 int launch_wg_transpose(const float* wg, int d, int E, float* wgT, cudaStream_t s);
 bool gate_bwd_needs_wgT(int d, int E);   // true: K6 reads Wg^T from global (too big for smem)
-int launch_unpermute_gate_bwd(const DispatchArgs& a, const void* dxe, const float* g,
-                              const float* logits, const float* wg, const float* wgT, int renorm,
-                              void* dx, float* dlogit, int t0, int t1, int num_sms, bool is_bf16,
-                              cudaStream_t s);
+// K6: dx_t = sum_j dX[prow_tj] + sum_e dlogit_te Wg[:, e]   (wgT = Wg transposed, [E][d])
+int launch_unpermute_gate_bwd(const DispatchArgs& a, const void* dxe, const int* prow,
+                              const float* dlogit, const float* wgT, void* dx, int t0, int t1,
+                              int num_sms, bool is_bf16, cudaStream_t s);
 // dWg = x^T dlogit (K7); partial: [ceil(T/64)][d][E] fp32 scratch
 int launch_dwg(const void* x, const float* dlogit, int T, int d, int E, float* partial,
                float* dwg, bool is_bf16, cudaStream_t s);

@@ -291,6 +291,7 @@ lancet_status create_common(lancet_ctx* c, int world, int rank, int device, cons
     AL(c->send_rows, sizeof(int) * E);
     AL(c->send_off, sizeof(int) * E);
     AL(c->g, sizeof(float) * (size_t)T * K);
+    AL(c->prow, sizeof(int) * (size_t)T * K);
     AL(c->dlogit, sizeof(float) * (size_t)T * E);
     AL(c->dwg_partial, sizeof(float) * dwg_partial_floats(T, d, E));
     AL(c->wgT, sizeof(float) * (size_t)d * E);
@@ -417,8 +418,8 @@ lancet_status gate_backward(lancet_ctx* c, const DispatchArgs& da, const void* d
     {
         OpScope op(c, "unpermute_gate_bwd", 0, nc > 1 ? cc : -1, s);
         if (cc == 0) *L += launch_wg_transpose(c->wg, d, E, c->wgT, s);
-        *L += launch_unpermute_gate_bwd(da, dxe, c->g, c->logits, c->wg, c->wgT, renorm, dx, c->dlogit,
-                                        t0, t1, c->num_sms, c->bf16, s);
+        *L += launch_unpermute_gate_bwd(da, dxe, c->prow, c->dlogit, c->wgT, dx, t0, t1, c->num_sms,
+                                        c->bf16, s);
     }
     CHECK_LAUNCH();
     if (cc == nc - 1) {
@@ -784,7 +785,8 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
     if (c->world == 1) {
         const void* comb = ident ? c->xs : c->out;
         { OpScope op(c, "combine_bwd", 0, -1, s);
-          L += launch_combine_bwd(da, dy, comb, c->g, c->dcomb, 0, T, true, c->bf16, s); }
+          L += launch_combine_bwd(da, dy, comb, c->g, c->dcomb, 0, T, true, c->logits, renorm, c->dlogit,
+                                  c->prow, c->bf16, s); }
         CHECK_LAUNCH();
         const void* dxe = c->dcomb;
         const int max_rows = round_up(c->C, kRowAlign);
@@ -832,7 +834,8 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
         int t0, t1;
         tok_range(cc, t0, t1);
         OpScope op(c, "combine_bwd", 0, serial ? -1 : cc, sc);
-        L += launch_combine_bwd(da, dy, comb, c->g, c->dcomb, t0, t1, cc == 0, c->bf16, sc);
+        L += launch_combine_bwd(da, dy, comb, c->g, c->dcomb, t0, t1, cc == 0, c->logits, renorm, c->dlogit,
+                                c->prow, c->bf16, sc);
         ev_k5[cc] = next_ev();
         CK(cudaEventRecord(ev_k5[cc], sc));
     }
