@@ -18,9 +18,15 @@ namespace {
 constexpr int kWarps = 8;
 constexpr size_t kSmemWgMax = 64 * 1024;
 
-// K6: one warp per token, all of the token's row loads in flight (like the combine), the gate
-// term from Wg^T ([E][d] fp32) staged once per persistent block in shared memory (or read
-// through L1 when it does not fit).  dlogit_te is held by lane e and broadcast with shuffles.
+// K6: each warp handles two tokens per pass, lanes over 16-byte vectors of dims; all row loads
+// of the pass are issued before use (like the combine).  The gate term reads Wg^T ([E][d] fp32)
+// from shared memory, staged once per persistent block in an interleaved layout
+// [e][h][v][4] (h = which half of the lane's 8 dims) so a warp's 16-byte reads are contiguous
+// (bank-conflict free), and each Wg^T vector serves both tokens.  dlogit_te is held by lane e
+// and broadcast with shuffles.  Falls back to L1 reads of the plain [E][d] layout when the
+// gate does not fit in shared memory.
+constexpr int kK6T = 2;
+
 template <typename Elt, int KK, bool SMEM_WG>
 __global__ void __launch_bounds__(kWarps * 32)
 k6_gather_kernel(const Elt* __restrict__ dxe, const int* __restrict__ prow,
@@ -28,72 +34,91 @@ k6_gather_kernel(const Elt* __restrict__ dxe, const int* __restrict__ prow,
                  int k, int d, int E, Elt* __restrict__ dx)
 {
     extern __shared__ __align__(16) float swt[];
-    constexpr int V = Vec16<Elt>::N;
-    constexpr int U = 4;                               // 16-byte vectors per lane per pass
+    constexpr int V = Vec16<Elt>::N;                   // dims per 16-byte vector (8 bf16 / 4 fp32)
+    constexpr int H = V / 4;                           // float4 pieces of Wg per vector
+    constexpr int U = 2;                               // vectors per lane per pass
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const float* W = wgT;
-    if constexpr (SMEM_WG) {
-        for (int q = threadIdx.x; q < d * E / 4; q += blockDim.x)
-            reinterpret_cast<float4*>(swt)[q] = __ldg(reinterpret_cast<const float4*>(wgT) + q);
-        __syncthreads();
-        W = swt;
-    }
     const int nvec = d / V;
-    for (int t = t0 + blockIdx.x * kWarps + w; t < t1; t += gridDim.x * kWarps) {
-        const int myrow = lane < k ? prow[(size_t)t * k + lane] : -1;
-        int rows[KK];
+    if constexpr (SMEM_WG) {
+        // swt[((e * H + h) * nvec + v) * 4 + c] = Wg^T[e][v * V + 4 h + c]
+        for (int q = threadIdx.x; q < E * nvec * H; q += blockDim.x) {
+            const int e = q / (nvec * H), r = q % (nvec * H), v = r / H, h = r % H;
+            reinterpret_cast<float4*>(swt)[(e * H + h) * nvec + v] =
+                __ldg(reinterpret_cast<const float4*>(wgT + (size_t)e * d + (size_t)v * V) + h);
+        }
+        __syncthreads();
+    }
+    const int step = gridDim.x * kWarps * kK6T;
+    for (int tb = t0 + (blockIdx.x * kWarps + w) * kK6T; tb < t1; tb += step) {
+        int rows[kK6T][KK];
+        float dl_lane[kK6T];
 #pragma unroll
-        for (int j = 0; j < KK; ++j) rows[j] = __shfl_sync(0xffffffffu, myrow, j);
-        const float* dlr = dlogit + (size_t)t * E;
+        for (int q = 0; q < kK6T; ++q) {
+            const int t = tb + q;
+            const bool ok = t < t1;
+            const int myrow = (ok && lane < k) ? prow[(size_t)t * k + lane] : -1;
+#pragma unroll
+            for (int j = 0; j < KK; ++j) rows[q][j] = __shfl_sync(0xffffffffu, myrow, j);
+            dl_lane[q] = (ok && lane < E) ? __ldg(dlogit + (size_t)t * E + lane) : 0.f;
+        }
         for (int v0 = lane; v0 < nvec; v0 += 32 * U) {
-            uint4 raw[U][KK];
+            uint4 raw[kK6T][U][KK];
 #pragma unroll
-            for (int u = 0; u < U; ++u)
+            for (int q = 0; q < kK6T; ++q)
 #pragma unroll
-                for (int j = 0; j < KK; ++j)
-                    if (rows[j] >= 0 && v0 + 32 * u < nvec)
-                        raw[u][j] = ld_nc_v4(reinterpret_cast<const uint4*>(dxe + (size_t)rows[j] * d) + v0 + 32 * u);
-            float acc[U][V];
+                for (int u = 0; u < U; ++u)
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
+                    for (int j = 0; j < KK; ++j)
+                        if (rows[q][j] >= 0 && v0 + 32 * u < nvec)
+                            raw[q][u][j] = ld_nc_v4(reinterpret_cast<const uint4*>(dxe + (size_t)rows[q][j] * d) + v0 + 32 * u);
+            float acc[kK6T][U][V];
 #pragma unroll
-                for (int i = 0; i < V; ++i) acc[u][i] = 0.f;
+            for (int q = 0; q < kK6T; ++q)
 #pragma unroll
-                for (int j = 0; j < KK; ++j) {
-                    if (rows[j] >= 0 && v0 + 32 * u < nvec) {
-                        float f[V];
-                        unpack16<Elt>(raw[u][j], f);
+                for (int u = 0; u < U; ++u) {
 #pragma unroll
-                        for (int i = 0; i < V; ++i) acc[u][i] += f[i];
+                    for (int i = 0; i < V; ++i) acc[q][u][i] = 0.f;
+#pragma unroll
+                    for (int j = 0; j < KK; ++j) {
+                        if (rows[q][j] >= 0 && v0 + 32 * u < nvec) {
+                            float f[V];
+                            unpack16<Elt>(raw[q][u][j], f);
+#pragma unroll
+                            for (int i = 0; i < V; ++i) acc[q][u][i] += f[i];
+                        }
                     }
                 }
-            }
-            for (int e0 = 0; e0 < E; e0 += 32) {
-                const float dl_lane = e0 + lane < E ? __ldg(dlr + e0 + lane) : 0.f;
-                const int ne = min(32, E - e0);
-                for (int e = 0; e < ne; ++e) {
-                    const float sv = __shfl_sync(0xffffffffu, dl_lane, e);
-                    const float* wrow = W + (size_t)(e0 + e) * d;
+            for (int e = 0; e < E; ++e) {
+                float sv[kK6T];                        // dlogit_te: lane e holds it when E <= 32
 #pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        const int v = v0 + 32 * u;
-                        if (v >= nvec) break;
-                        const float4* wt = reinterpret_cast<const float4*>(wrow + (size_t)v * V);
+                for (int q = 0; q < kK6T; ++q)
+                    sv[q] = E <= 32 ? __shfl_sync(0xffffffffu, dl_lane[q], e)
+                                    : (tb + q < t1 ? __ldg(dlogit + (size_t)(tb + q) * E + e) : 0.f);
 #pragma unroll
-                        for (int h = 0; h < V / 4; ++h) {
-                            const float4 w4 = SMEM_WG ? wt[h] : __ldg(wt + h);
-                            acc[u][4 * h + 0] = fmaf(sv, w4.x, acc[u][4 * h + 0]);
-                            acc[u][4 * h + 1] = fmaf(sv, w4.y, acc[u][4 * h + 1]);
-                            acc[u][4 * h + 2] = fmaf(sv, w4.z, acc[u][4 * h + 2]);
-                            acc[u][4 * h + 3] = fmaf(sv, w4.w, acc[u][4 * h + 3]);
+                for (int u = 0; u < U; ++u) {
+                    const int v = v0 + 32 * u;
+                    if (v >= nvec) break;
+#pragma unroll
+                    for (int h = 0; h < H; ++h) {
+                        const float4 w4 = SMEM_WG
+                            ? reinterpret_cast<const float4*>(swt)[(e * H + h) * nvec + v]
+                            : __ldg(reinterpret_cast<const float4*>(wgT + (size_t)e * d + (size_t)v * V) + h);
+#pragma unroll
+                        for (int q = 0; q < kK6T; ++q) {
+                            acc[q][u][4 * h + 0] = fmaf(sv[q], w4.x, acc[q][u][4 * h + 0]);
+                            acc[q][u][4 * h + 1] = fmaf(sv[q], w4.y, acc[q][u][4 * h + 1]);
+                            acc[q][u][4 * h + 2] = fmaf(sv[q], w4.z, acc[q][u][4 * h + 2]);
+                            acc[q][u][4 * h + 3] = fmaf(sv[q], w4.w, acc[q][u][4 * h + 3]);
                         }
                     }
                 }
             }
 #pragma unroll
-            for (int u = 0; u < U; ++u)
-                if (v0 + 32 * u < nvec)
-                    st_v4(reinterpret_cast<uint4*>(dx + (size_t)t * d) + v0 + 32 * u, pack16<Elt>(acc[u]));
+            for (int q = 0; q < kK6T; ++q)
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (tb + q < t1 && v0 + 32 * u < nvec)
+                        st_v4(reinterpret_cast<uint4*>(dx + (size_t)(tb + q) * d) + v0 + 32 * u, pack16<Elt>(acc[q][u]));
         }
     }
 }
@@ -237,7 +262,7 @@ static void launch_k6(const DispatchArgs& a, const void* dxe, const int* prow, c
                              (int)kSmemWgMax);
         attr = true;
     }
-    const int need = ceil_div(t1 - t0, kWarps);
+    const int need = ceil_div(t1 - t0, kWarps * kK6T);
     const int grid = std::max(1, std::min(need, 4 * num_sms));
     k6_gather_kernel<Elt, KK, SM><<<grid, kWarps * 32, smem, s>>>((const Elt*)dxe, prow, dlogit, wgT, t0, t1,
                                                                   a.k, a.d, a.E, (Elt*)dx);
