@@ -85,11 +85,14 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
-// arrive on the barrier at the same offset in CTA `rank` of the cluster
+// arrive on the barrier at the same offset in CTA `rank` of the cluster.  Default (.release.cta)
+// semantics: the only hand-off is the TMEM accumulator, whose reads are already ordered by
+// tcgen05.wait::ld + tcgen05.fence::before_thread_sync; a .release.cluster arrive would add a
+// MEMBAR/ERRBAR that waits for every outstanding store of the warp on each tile.
 __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* b, uint32_t rank) {
     uint32_t remote;
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(b)), "r"(rank));
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
     asm volatile(
@@ -488,7 +491,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
-                if constexpr (CG == 1) mbar_arrive(&tempty[acc]);
+                if (CG == 1 || leader) mbar_arrive(&tempty[acc]);
                 else mbar_arrive_cluster(&tempty[acc], 0);        // the leader's MMA waits on it
             }
         }
