@@ -36,10 +36,10 @@ namespace tc {
 constexpr int BM = 128, BK = 64, UMMA_K = 16;
 constexpr int kThreads = 384;            // 4 control warps + 8 epilogue warps
 constexpr int kEpiWarps = 8;
-constexpr int kMaxGroups = 256;
+constexpr int kMaxGroups = 128;                 // group tables cached in shared memory
 constexpr uint32_t A_STAGE = BM * BK * 2;                 // 16 KiB
-constexpr uint32_t kWarpStage = 8192;                     // per epilogue warp: 4 x 2 KiB slots (double-buffered)
-constexpr uint32_t kBarBytes = 512;                       // mbarriers + TMEM address
+constexpr uint32_t kWarpStage = 4096;                     // per epilogue warp: out0 | (out1 or act'(A))
+constexpr uint32_t kBarBytes = 256;                       // mbarriers + TMEM address
 constexpr size_t kSmemLimit = 232448;                     // 227 KiB opt-in per block
 
 template <int BN, bool A_MN, int CG>
@@ -47,7 +47,7 @@ struct Cfg {
     static constexpr bool kStaged = !A_MN;                // M-grouped: bf16 out via TMA store
     static constexpr uint32_t B_STAGE = BN * BK * 2 / CG; // this CTA's share of B
     static constexpr size_t kEpi = kStaged ? (size_t)kEpiWarps * kWarpStage : 0;
-    static constexpr size_t kFixed = 1024 + kEpi + kBarBytes + sizeof(int) * (kMaxGroups + 1);
+    static constexpr size_t kFixed = 1024 + kEpi + kBarBytes + sizeof(int) * (3 * kMaxGroups + 1);
     static constexpr int STAGES_FIT = (int)((kSmemLimit - kFixed) / (A_STAGE + B_STAGE));
     static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
     static constexpr size_t kRing = (size_t)STAGES * (A_STAGE + B_STAGE);
@@ -125,7 +125,7 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
                  : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
@@ -237,9 +237,11 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + 2;
-    uint64_t* abar = tempty + 2;                       // [kEpiWarps][2] aux-load barriers
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(abar + 2 * kEpiWarps);
-    int* tstart = reinterpret_cast<int*>(sEpi + CF::kEpi + kBarBytes);
+    uint64_t* abar = tempty + 2;                       // [kEpiWarps] aux-load barriers
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(abar + kEpiWarps);
+    int* tstart = reinterpret_cast<int*>(sEpi + CF::kEpi + kBarBytes);   // [n_groups + 1]
+    int* srows = tstart + kMaxGroups + 1;              // group tables cached from global memory
+    int* soff = srows + kMaxGroups;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ntn = p.N / BN;
@@ -252,7 +254,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         int acc = 0;
         for (int g = 0; g < p.n_groups; ++g) {
             tstart[g] = acc;
-            const int mt = p.mode == GEMM_M_GROUPED ? ceil_div(p.grp_rows[g], MT) : p.M / MT;
+            srows[g] = p.grp_rows[g];
+            soff[g] = p.grp_off[g];
+            const int mt = p.mode == GEMM_M_GROUPED ? ceil_div(srows[g], MT) : p.M / MT;
             acc += mt * ntn;
         }
         tstart[p.n_groups] = acc;
@@ -269,7 +273,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     if (warp == 1 && lane == 0) {
         for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
         for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], kEpiWarps * CG); }
-        for (int i = 0; i < 2 * kEpiWarps; ++i) mbar_init(&abar[i], 1);
+        for (int i = 0; i < kEpiWarps; ++i) mbar_init(&abar[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 2) {
@@ -302,12 +306,12 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 int num_kb, arow, brow;
                 if (p.mode == GEMM_M_GROUPED) {
                     num_kb = p.K / BK;
-                    arow = p.grp_off[g] + mt * MT + (int)rank * BM;
+                    arow = soff[g] + mt * MT + (int)rank * BM;
                     brow = ((g / p.gpw) % p.n_weights) * (B_MN ? p.K : p.N);
                 } else {
-                    num_kb = round_up(p.grp_rows[g], kRowAlign) / BK;
-                    arow = p.grp_off[g];
-                    brow = p.grp_off[g];
+                    num_kb = round_up(srows[g], kRowAlign) / BK;
+                    arow = soff[g];
+                    brow = soff[g];
                 }
                 const int m0 = mt * MT + (int)rank * BM;
                 for (int kb = 0; kb < num_kb; ++kb) {
@@ -347,7 +351,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             for (int tile = cluster; tile < total; tile += n_clusters, ++it) {
                 int g, mt, nt;
                 decode_tile(tile, tstart, p.n_groups, ntn, g, mt, nt);
-                const int num_kb = p.mode == GEMM_M_GROUPED ? p.K / BK : round_up(p.grp_rows[g], kRowAlign) / BK;
+                const int num_kb = p.mode == GEMM_M_GROUPED ? p.K / BK : round_up(srows[g], kRowAlign) / BK;
                 const int acc = it & 1;
                 const uint32_t acc_phase = (it >> 1) & 1;
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -375,50 +379,43 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         const int ew = warp - 4;
         const int half = ew >> 2;
         const int cc0 = half * (BN / 64), cc1 = cc0 + BN / 64;
-        // staging slots (2 KiB = one 32x32 bf16 box, SWIZZLE_64B): double-buffered outputs;
-        // ACT: out0[b] = slot 2b, out1[b] = slot 2b+1; STORE: out0[b] = slot b;
-        // DACT: out0[b] = slot b, act'(A)[b] = slot 2+b (prefetched two chunks ahead)
-        uint8_t* slots = sEpi + ew * kWarpStage;
-        uint64_t* xbar = &abar[2 * ew];
-        uint32_t xphase[2] = {0, 0};
+        // staging (2 KiB = one 32x32 bf16 box, SWIZZLE_64B): out0 | out1 (ACT) or act'(A) (DACT)
+        uint8_t* sO0 = sEpi + ew * kWarpStage;
+        uint8_t* sO1 = sO0 + 2048;
+        uint8_t* sX = sO0 + 2048;
+        uint64_t* xbar = &abar[ew];
+        uint32_t xphase = 0;
         int it = 0;
         for (int tile = cluster; tile < total; tile += n_clusters, ++it) {
             int g, mt, nt;
             decode_tile(tile, tstart, p.n_groups, ntn, g, mt, nt);
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
-            const bool has_k = p.mode == GEMM_M_GROUPED ? (p.K > 0) : (p.grp_rows[g] > 0);
+            const bool has_k = p.mode == GEMM_M_GROUPED ? (p.K > 0) : (srows[g] > 0);
             const int n0 = nt * BN;
             if constexpr (CF::kStaged) {
                 const int mrow = mt * MT + (int)rank * BM;                // first row of this CTA
-                const int row0 = p.grp_off[g] + mrow + q * 32;            // this warp's 32 rows
+                const int row0 = soff[g] + mrow + q * 32;                 // this warp's 32 rows
                 // a pair tile may extend past the group's 128-aligned rows: skip that half
-                const bool live = mrow < round_up(p.grp_rows[g], kRowAlign);
+                const bool live = mrow < round_up(srows[g], kRowAlign);
                 const bool dact = p.epi == EPI_DACT;
                 if (live && dact && lane == 0) {                          // prefetch act'(A)
-#pragma unroll
-                    for (int b = 0; b < 2; ++b) {
-                        if (cc0 + b < cc1) {
-                            mbar_expect_tx(&xbar[b], 2048);
-                            tma_load_2d(&tmX, &xbar[b], slots + (2 + b) * 2048, n0 + (cc0 + b) * 32, row0);
-                        }
-                    }
+                    mbar_expect_tx(xbar, 2048);
+                    tma_load_2d(&tmX, xbar, sX, n0 + cc0 * 32, row0);
                 }
                 mbar_wait(&tfull[acc], acc_phase);
                 tc_fence_after();
                 if (live) {
 #pragma unroll 1
                     for (int cc = cc0; cc < cc1; ++cc) {
-                        const int b = (cc - cc0) & 1;
                         uint32_t v[32];
                         tmem_ld32(tmem_base + acc * BN + cc * 32 + ((uint32_t)(q * 32) << 16), v);
                         float f[32];
 #pragma unroll
                         for (int i = 0; i < 32; ++i) f[i] = has_k ? __uint_as_float(v[i]) : 0.f;
                         if (dact) {
-                            uint8_t* sX = slots + (2 + b) * 2048;
-                            mbar_wait(&xbar[b], xphase[b]);
-                            xphase[b] ^= 1;
+                            mbar_wait(xbar, xphase);
+                            xphase ^= 1;
 #pragma unroll
                             for (int j = 0; j < 4; ++j) {
                                 float a8[8];
@@ -427,38 +424,33 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                                 for (int i = 0; i < 8; ++i) f[8 * j + i] *= a8[i];
                             }
                             __syncwarp();
-                            if (cc + 2 < cc1 && lane == 0) {
-                                mbar_expect_tx(&xbar[b], 2048);
-                                tma_load_2d(&tmX, &xbar[b], sX, n0 + (cc + 2) * 32, row0);
-                            }
                         }
-                        // the stores of chunk cc-2 must have read this buffer (<= 1 group pending)
-                        if (lane == 0) bulk_wait_read1();
+                        // the previous chunk's TMA stores must have read the staging buffers
+                        if (lane == 0) bulk_wait_read0();
                         __syncwarp();
-                        uint8_t* o0;
-                        uint8_t* o1 = nullptr;
+                        if (dact && cc + 1 < cc1 && lane == 0) {          // act'(A) of the next chunk
+                            mbar_expect_tx(xbar, 2048);
+                            tma_load_2d(&tmX, xbar, sX, n0 + (cc + 1) * 32, row0);
+                        }
                         if (p.epi == EPI_ACT) {
-                            o0 = slots + (2 * b) * 2048;
-                            o1 = o0 + 2048;
                             float h[32], gr[32];
 #pragma unroll
                             for (int i = 0; i < 32; ++i) act_fwd_grad_fast(p.act, f[i], h[i], gr[i]);
 #pragma unroll
                             for (int j = 0; j < 4; ++j) {
-                                *reinterpret_cast<uint4*>(o0 + sw64(lane, j)) = pack16<bf16>(h + 8 * j);
-                                *reinterpret_cast<uint4*>(o1 + sw64(lane, j)) = pack16<bf16>(gr + 8 * j);
+                                *reinterpret_cast<uint4*>(sO0 + sw64(lane, j)) = pack16<bf16>(h + 8 * j);
+                                *reinterpret_cast<uint4*>(sO1 + sw64(lane, j)) = pack16<bf16>(gr + 8 * j);
                             }
                         } else {
-                            o0 = slots + b * 2048;
 #pragma unroll
                             for (int j = 0; j < 4; ++j)
-                                *reinterpret_cast<uint4*>(o0 + sw64(lane, j)) = pack16<bf16>(f + 8 * j);
+                                *reinterpret_cast<uint4*>(sO0 + sw64(lane, j)) = pack16<bf16>(f + 8 * j);
                         }
                         fence_proxy_async();
                         __syncwarp();
                         if (lane == 0) {
-                            tma_store_2d(&tmC, o0, n0 + cc * 32, row0);
-                            if (o1) tma_store_2d(&tmC2, o1, n0 + cc * 32, row0);
+                            tma_store_2d(&tmC, sO0, n0 + cc * 32, row0);
+                            if (p.epi == EPI_ACT) tma_store_2d(&tmC2, sO1, n0 + cc * 32, row0);
                             bulk_commit();
                         }
                     }
