@@ -184,6 +184,25 @@ lancet_status lancet_last_timeline(lancet_ctx* ctx, lancet_op_record* out, int32
  * which: 0 = gate logits [T][E] fp32 (R1 chain). */
 lancet_status lancet_debug_copy(lancet_ctx* ctx, int32_t which, void* host_dst, size_t bytes);
 
+/* Host-side plan of the expert-parallel exchange (no device; the scheduler posts every NCCL
+ * send/recv from exactly this layout).  Inputs (host):
+ *   send_counts [E][n]        rows this rank admitted per expert (E = G*E_l) per chunk
+ *   recv_counts [G][E_l][n]   rows this rank's experts receive per source rank, local expert,
+ *                             chunk (the result of the size all-to-all)
+ * Outputs (host, caller-allocated):
+ *   send_off [E], S [E][n+1]  chunk c of expert e is packed send rows
+ *                             [send_off[e] + S[e][c], send_off[e] + S[e][c+1])
+ *   grp_rows [n][E_l], grp_off [n][E_l]   rows and first (128-aligned) row of each
+ *                             (chunk, local expert) GEMM group in the receive buffer; the
+ *                             buffer holds the groups expert-major (e_l, c)
+ *   src_off [G][E_l][n]       row offset of each source's rows inside its group (R12)
+ *   total_rows                receive-buffer rows
+ * Errors: LANCET_ERR_ARG for null pointers, non-positive sizes or negative counts. */
+lancet_status lancet_plan_exchange(int32_t G, int32_t E_l, int32_t n, const int32_t* send_counts,
+                                   const int32_t* recv_counts, int32_t* send_off, int32_t* S,
+                                   int32_t* grp_rows, int32_t* grp_off, int32_t* src_off,
+                                   int32_t* total_rows);
+
 /* Bytes of device workspace the context owns. */
 lancet_status lancet_workspace_bytes(const lancet_ctx* ctx, size_t* bytes);
 

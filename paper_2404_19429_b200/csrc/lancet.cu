@@ -365,6 +365,41 @@ lancet_status check_ready(lancet_ctx* c)
 
 // ---- world > 1 exchange plans -----------------------------------------------------------
 // Host view of the routing sizes after the counts exchange.
+// Send side of the exchange (host): S[e][c] = prefix over chunks of the rows this rank
+// admitted to expert e, send_off[e] = 128-aligned packed row offset of expert e (the same
+// layout the device computes in K2) -- chunk c of expert e is rows
+// [send_off[e] + S[e][c], send_off[e] + S[e][c+1]).
+void plan_send(int E, int n, const int* send, int* S, int* send_off)
+{
+    int off = 0;
+    for (int e = 0; e < E; ++e) {
+        S[e * (n + 1)] = 0;
+        for (int c = 0; c < n; ++c) S[e * (n + 1) + c + 1] = S[e * (n + 1) + c] + send[e * n + c];
+        send_off[e] = off;
+        off += round_up(S[e * (n + 1) + n], kRowAlign);
+    }
+}
+
+// Receive side (host): one GEMM group per (chunk, local expert), table order chunk-major
+// [n][E_l]; buffer order expert-major (e_l, c) so an expert's rows over all chunks form one
+// K range for its dW GEMM; inside a group rows are ordered by source rank (R12).
+int plan_recv(int G, int E_l, int n, const int* recv, int* grp_rows, int* grp_off, int* src_off)
+{
+    int row = 0;
+    for (int el = 0; el < E_l; ++el)
+        for (int c = 0; c < n; ++c) {
+            int r = 0;
+            for (int src = 0; src < G; ++src) {
+                src_off[(src * E_l + el) * n + c] = r;
+                r += recv[(src * E_l + el) * n + c];
+            }
+            grp_rows[c * E_l + el] = r;
+            grp_off[c * E_l + el] = row;
+            row += round_up(r, kRowAlign);
+        }
+    return row;
+}
+
 struct Plan {
     int E, E_l, G, n;
     std::vector<int> send;      // [E][n]
@@ -381,28 +416,11 @@ struct Plan {
         recv.assign(h_recv, h_recv + G * E_l * n);
         S.assign(E * (n + 1), 0);
         send_off.assign(E, 0);
-        int off = 0;
-        for (int e = 0; e < E; ++e) {
-            for (int c = 0; c < n; ++c) S[e * (n + 1) + c + 1] = S[e * (n + 1) + c] + send[e * n + c];
-            send_off[e] = off;
-            off += round_up(S[e * (n + 1) + n], kRowAlign);
-        }
+        plan_send(E, n, send.data(), S.data(), send_off.data());
         grp_rows.assign(n * E_l, 0);
         grp_off.assign(n * E_l, 0);
         src_off.assign(G * E_l * n, 0);
-        int row = 0;
-        for (int el = 0; el < E_l; ++el)
-            for (int c = 0; c < n; ++c) {
-                int r = 0;
-                for (int src = 0; src < G; ++src) {
-                    src_off[(src * E_l + el) * n + c] = r;
-                    r += recv[(src * E_l + el) * n + c];
-                }
-                grp_rows[c * E_l + el] = r;
-                grp_off[c * E_l + el] = row;
-                row += round_up(r, kRowAlign);
-            }
-        rows_total = row;
+        rows_total = plan_recv(G, E_l, n, recv.data(), grp_rows.data(), grp_off.data(), src_off.data());
     }
 };
 
@@ -1005,6 +1023,21 @@ LANCET_API lancet_status lancet_debug_copy(lancet_ctx* c, int32_t which, void* h
     if (!host_dst || bytes < need) return fail(c, LANCET_ERR_ARG, "destination too small");
     CK(cudaDeviceSynchronize());
     CK(cudaMemcpy(host_dst, c->logits, need, cudaMemcpyDeviceToHost));
+    return LANCET_OK;
+}
+
+LANCET_API lancet_status lancet_plan_exchange(int32_t G, int32_t E_l, int32_t n,
+                                              const int32_t* send_counts, const int32_t* recv_counts,
+                                              int32_t* send_off, int32_t* S, int32_t* grp_rows,
+                                              int32_t* grp_off, int32_t* src_off, int32_t* total_rows)
+{
+    if (G < 1 || E_l < 1 || n < 1 || n > kMaxChunks || !send_counts || !recv_counts || !send_off || !S ||
+        !grp_rows || !grp_off || !src_off || !total_rows)
+        return fail(nullptr, LANCET_ERR_ARG, "bad arguments");
+    for (int i = 0; i < G * E_l * n; ++i)
+        if (send_counts[i] < 0 || recv_counts[i] < 0) return fail(nullptr, LANCET_ERR_ARG, "negative count");
+    plan_send(G * E_l, n, send_counts, S, send_off);
+    *total_rows = plan_recv(G, E_l, n, recv_counts, grp_rows, grp_off, src_off);
     return LANCET_OK;
 }
 

@@ -28,7 +28,7 @@ EXPORTS = ["lancet_abi_version", "lancet_last_error", "lancet_nccl_unique_id", "
            "lancet_local_group_create", "lancet_local_group_destroy", "lancet_create_local",
            "lancet_destroy", "lancet_set_flags", "lancet_moe_forward", "lancet_moe_backward",
            "lancet_get_counts", "lancet_timeline_begin", "lancet_last_timeline", "lancet_debug_copy",
-           "lancet_workspace_bytes", "lancet_launch_counts"]
+           "lancet_workspace_bytes", "lancet_launch_counts", "lancet_plan_exchange"]
 
 
 class LancetError(RuntimeError):
@@ -83,6 +83,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "lancet_debug_copy": ([P, I32, P, ctypes.c_size_t], I32),
             "lancet_workspace_bytes": ([P, ctypes.POINTER(ctypes.c_size_t)], I32),
             "lancet_launch_counts": ([P, ctypes.POINTER(I32), ctypes.POINTER(I32)], I32),
+            "lancet_plan_exchange": ([I32, I32, I32, P, P, P, P, P, P, P, ctypes.POINTER(I32)], I32),
         }
         for name, (args, res) in sig.items():
             f = getattr(lib, name)
@@ -144,6 +145,32 @@ class LocalGroup:
             self._p = ctypes.c_void_p()
 
 
+def plan_exchange(G: int, E_l: int, n: int, send_counts, recv_counts) -> dict:
+    """Host-side exchange plan (lancet_plan_exchange) as numpy arrays."""
+    import numpy as np
+    E = G * E_l
+    send = np.ascontiguousarray(send_counts, dtype=np.int32).reshape(E, n)
+    recv = np.ascontiguousarray(recv_counts, dtype=np.int32).reshape(G, E_l, n)
+    out = dict(send_off=np.zeros(E, np.int32), S=np.zeros((E, n + 1), np.int32),
+               grp_rows=np.zeros((n, E_l), np.int32), grp_off=np.zeros((n, E_l), np.int32),
+               src_off=np.zeros((G, E_l, n), np.int32))
+    tot = ctypes.c_int32()
+    p = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    _check(load_library().lancet_plan_exchange(G, E_l, n, p(send), p(recv), p(out["send_off"]), p(out["S"]),
+                                               p(out["grp_rows"]), p(out["grp_off"]), p(out["src_off"]),
+                                               ctypes.byref(tot)))
+    out["total_rows"] = tot.value
+    return out
+
+
+def share_nccl_id(pg=None, rank: int = 0) -> bytes:
+    """Rank 0 creates the NCCL unique id; it is broadcast over the torch process group."""
+    import torch.distributed as dist
+    obj = [nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=pg)
+    return obj[0]
+
+
 def nccl_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     _check(load_library().lancet_nccl_unique_id(buf))
@@ -172,10 +199,7 @@ class Context:
         else:
             nid = None
             if world > 1:
-                import torch.distributed as dist
-                obj = [nccl_unique_id() if rank == 0 else None]
-                dist.broadcast_object_list(obj, src=0, group=pg)
-                nid = ctypes.create_string_buffer(obj[0], 128)
+                nid = ctypes.create_string_buffer(share_nccl_id(pg, rank), 128)
             _check(lib.lancet_create(ctypes.byref(self._p), world, rank, self.device, nid,
                                      ctypes.byref(c)))
         self.E_l = cfg.n_experts // world
