@@ -424,26 +424,24 @@ struct Plan {
     }
 };
 
-// K6 + K7 for the tokens of chunk cc of nc (nc == 1: all tokens): dx (expert path + gate
-// term) and, after the last chunk, dWg.
-lancet_status gate_backward(lancet_ctx* c, const DispatchArgs& da, const void* dxe, void* dx,
-                            float* dwg, int renorm, cudaStream_t s, int cc, int nc, int* L,
-                            int* pbase = nullptr)
+// K6 for the tokens of chunk cc of nc (nc == 1: all tokens): dx = expert path + gate term.
+lancet_status gate_backward_dx(lancet_ctx* c, const DispatchArgs& da, const void* dxe, void* dx,
+                               cudaStream_t s, int cc, int nc, int* L)
 {
-    (void)pbase;
     const int T = c->T, d = c->cfg.d_model, E = c->cfg.n_experts;
     const int t0 = chunk_start(T, nc, cc), t1 = chunk_start(T, nc, cc + 1);
-    {
-        OpScope op(c, "unpermute_gate_bwd", 0, nc > 1 ? cc : -1, s);
-        if (cc == 0) *L += launch_wg_transpose(c->wg, d, E, c->wgT, s);
-        *L += launch_unpermute_gate_bwd(da, dxe, c->prow, c->dlogit, c->wgT, dx, t0, t1, c->num_sms,
-                                        c->bf16, s);
-    }
+    OpScope op(c, "unpermute_gate_bwd", s == c->s_comp ? 0 : 2, nc > 1 ? cc : -1, s);
+    if (cc == 0) *L += launch_wg_transpose(c->wg, d, E, c->wgT, s);
+    *L += launch_unpermute_gate_bwd(da, dxe, c->prow, c->dlogit, c->wgT, dx, t0, t1, c->num_sms, c->bf16, s);
     CHECK_LAUNCH();
-    if (cc == nc - 1) {
-        OpScope op(c, "gate_dwg", 0, -1, s);
-        *L += launch_dwg(c->x, c->dlogit, T, d, E, c->dwg_partial, dwg, c->bf16, s);
-    }
+    return LANCET_OK;
+}
+
+// K7: dWg = x^T dlogit over all tokens (after every K5 has written its dlogit rows).
+lancet_status gate_backward_dwg(lancet_ctx* c, float* dwg, cudaStream_t s, int* L)
+{
+    OpScope op(c, "gate_dwg", s == c->s_comp ? 0 : 2, -1, s);
+    *L += launch_dwg(c->x, c->dlogit, c->T, c->cfg.d_model, c->cfg.n_experts, c->dwg_partial, dwg, c->bf16, s);
     CHECK_LAUNCH();
     return LANCET_OK;
 }
@@ -808,17 +806,31 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
         CHECK_LAUNCH();
         const void* dxe = c->dcomb;
         const int max_rows = round_up(c->C, kRowAlign);
+        // K7 (dWg) needs only dlogit from K5, and K6 only dX: both run on a side stream beside
+        // the persistent GEMMs (one small block fits next to each GEMM CTA), so they hide under
+        // the dX / dW GEMMs instead of adding to the critical path
+        cudaStream_t sa = c->s_comm;
+        cudaEvent_t ev_k5 = c->ev_pool[0], ev_dx = c->ev_pool[1], ev_side = c->ev_pool[2];
+        CK(cudaEventRecord(ev_k5, s));
+        CK(cudaStreamWaitEvent(sa, ev_k5, 0));
+        st = gate_backward_dwg(c, dwg, sa, &L);
+        if (st) return st;
         if (!ident) {
             st = expert_backward_dx(c, c->dcomb, c->send_rows, c->send_off, E, max_rows, s, -1, &L);
             if (st) return st;
             dxe = c->dXe;
         }
+        CK(cudaEventRecord(ev_dx, s));
+        CK(cudaStreamWaitEvent(sa, ev_dx, 0));
+        st = gate_backward_dx(c, da, dxe, dx, sa, 0, 1, &L);
+        if (st) return st;
+        CK(cudaEventRecord(ev_side, sa));
         if (!ident) {
             st = expert_backward_dw(c, c->dcomb, c->send_rows, c->send_off, E, dw1, dw2, 0, s, -1, &L);
             if (st) return st;
         }
-        st = gate_backward(c, da, dxe, dx, dwg, renorm, s, 0, 1, &L);
-        return st;
+        CK(cudaStreamWaitEvent(s, ev_side, 0));
+        return LANCET_OK;
     }
 
     // ---- expert parallel (S2) ---------------------------------------------------------------
@@ -940,12 +952,13 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
             if (st) return st;
         }
     }
-    int pbase = 0;
     for (int cc = 0; cc < nc; ++cc) {
         CK(cudaStreamWaitEvent(sc, ev_b2[cc], 0));
-        st = gate_backward(c, da, dxcomb, dx, dwg, renorm, sc, cc, nc, &L, &pbase);
+        st = gate_backward_dx(c, da, dxcomb, dx, sc, cc, nc, &L);
         if (st) return st;
     }
+    st = gate_backward_dwg(c, dwg, sc, &L);
+    if (st) return st;
     CK(cudaEventRecord(c->ev_join, sc));
     CK(cudaStreamWaitEvent(s, c->ev_join, 0));
     if (sm != sc) {
