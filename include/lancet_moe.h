@@ -77,7 +77,9 @@ enum {
     LANCET_FLAG_SERIAL      = 1u << 2,  /* unoverlapped baseline: one stream, chunks merged,
                                            no dW reordering (the "unoverlapped a2a" of §8(d)) */
     LANCET_FLAG_SIMT_GEMM   = 1u << 3,  /* bf16: use the SIMT GEMM instead of tcgen05 (debug) */
-    LANCET_FLAG_NO_DW_OVERLAP = 1u << 4 /* backward: dW GEMMs after all a2a (ablation)       */
+    LANCET_FLAG_NO_DW_OVERLAP = 1u << 4,/* backward: dW GEMMs after all a2a (ablation)       */
+    LANCET_FLAG_NO_SIDE_STREAM = 1u << 5/* world 1 backward: K6/K7 on the caller stream, in
+                                           line with the GEMMs (A/B of the side stream)      */
 };
 
 typedef struct {

@@ -435,7 +435,12 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                         if (p.epi == EPI_ACT) {
                             float h[32], gr[32];
 #pragma unroll
-                            for (int i = 0; i < 32; ++i) act_fwd_grad_fast(p.act, f[i], h[i], gr[i]);
+                            for (int i = 0; i < 32; i += 2) {
+                                float2 h2, g2;
+                                act_fwd_grad_fast2(p.act, make_float2(f[i], f[i + 1]), h2, g2);
+                                h[i] = h2.x; h[i + 1] = h2.y;
+                                gr[i] = g2.x; gr[i + 1] = g2.y;
+                            }
 #pragma unroll
                             for (int j = 0; j < 4; ++j) {
                                 *reinterpret_cast<uint4*>(sO0 + sw64(lane, j)) = pack16<bf16>(h + 8 * j);

@@ -809,7 +809,7 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
         // K7 (dWg) needs only dlogit from K5, and K6 only dX: both run on a side stream beside
         // the persistent GEMMs (one small block fits next to each GEMM CTA), so they hide under
         // the dX / dW GEMMs instead of adding to the critical path
-        cudaStream_t sa = c->s_comm;
+        cudaStream_t sa = (c->cfg.flags & LANCET_FLAG_NO_SIDE_STREAM) ? s : c->s_comm;
         cudaEvent_t ev_k5 = c->ev_pool[0], ev_dx = c->ev_pool[1], ev_side = c->ev_pool[2];
         CK(cudaEventRecord(ev_k5, s));
         CK(cudaStreamWaitEvent(sa, ev_k5, 0));

@@ -18,36 +18,42 @@
 
 namespace lancet {
 
-constexpr int kGateDT = 256;     // d-tile staged in shared memory (double-buffered cp.async)
-constexpr int kGateMaxTB = 64;   // tokens per block
-constexpr int kGateThreadCap = 128;
+constexpr int kGateDT = 128;     // d-tile staged in shared memory (double-buffered cp.async)
+constexpr int kGateThreads = 128;
 
+// Thread (token r, experts e0..e0+CE-1) runs CE independent R1 chains, two at a time with the
+// packed fp32 FMA (fma.rn.f32x2: two IEEE fused multiply-adds, each rounded once -- bitwise the
+// same as two fmaf).  CE = 8, 4, 2 or 1 (largest dividing E).
 struct GateGeom {
-    int ce;        // experts (R1 chains) per thread: 2 if E is even, else 1
+    int ce;        // experts (R1 chains) per thread
     int tpt;       // threads per token = E / ce
     int TB;        // tokens per block
     int threads;   // TB * tpt
-    int dt;        // dims per staged tile
-    int row_bytes; // bytes per staged x row
-    size_t buf_bytes, smem;
+    int row_bytes; // bytes per staged x row (kGateDT elements + 16 B against bank conflicts)
+    size_t x_bytes, buf_bytes, smem;
 };
+
+__host__ __device__ inline int gate_ce(int E)
+{
+    // 8 chains per thread when there are enough tokens per block to keep the SMs busy
+    return (E % 8 == 0 && E >= 16) ? 8 : (E % 4 == 0) ? 4 : (E % 2 == 0) ? 2 : 1;
+}
+
+// floats per expert group of the staged Wg tile (+4: groups start in different banks)
+__host__ __device__ constexpr int gate_wg_stride(int ce) { return kGateDT * ce + 4; }
 
 __host__ __device__ inline GateGeom gate_geom(int E, int elt_bytes)
 {
     GateGeom g;
-    g.ce = (E % 2 == 0) ? 2 : 1;   // 2 chains per thread: 4x the warps of 8, latency-bound kernel
+    g.ce = gate_ce(E);
     g.tpt = E / g.ce;
-    g.TB = kGateThreadCap / g.tpt;
-    if (g.TB > kGateMaxTB) g.TB = kGateMaxTB;
+    g.TB = kGateThreads / g.tpt;
+    if (g.TB > 64) g.TB = 64;
     if (g.TB < 1) g.TB = 1;
     g.threads = g.TB * g.tpt;
-    // d-tile: 256 dims, fewer when the Wg tile (DT x E fp32) would exceed 16 KiB
-    int dt = 4096 / E;
-    dt = dt > kGateDT ? kGateDT : dt;
-    dt = dt < 8 ? 8 : (dt & ~7);
-    g.dt = dt;
-    g.row_bytes = dt * elt_bytes + 16;                              // +16 B: fewer bank conflicts
-    g.buf_bytes = (size_t)g.TB * g.row_bytes + (size_t)dt * E * 4;
+    g.row_bytes = kGateDT * elt_bytes + 16;
+    g.x_bytes = (size_t)g.TB * g.row_bytes;
+    g.buf_bytes = g.x_bytes + (size_t)g.tpt * gate_wg_stride(g.ce) * 4;   // x tile | Wg tile [E/CE][DT][CE]
     const size_t xs = 2 * g.buf_bytes;
     const size_t lg = sizeof(float) * (size_t)g.TB * E;
     g.smem = xs > lg ? xs : lg;
@@ -64,12 +70,27 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <typename Elt>
+// acc = fma(x, w, acc) on both halves (one IEEE rounding each)
+__device__ __forceinline__ void ffma2(float2& acc, float x, float2 w)
+{
+    asm("{\n\t.reg .b64 xx, ww, aa;\n\t"
+        "mov.b64 xx, {%2, %2};\n\t"
+        "mov.b64 ww, {%3, %4};\n\t"
+        "mov.b64 aa, {%0, %1};\n\t"
+        "fma.rn.f32x2 aa, xx, ww, aa;\n\t"
+        "mov.b64 {%0, %1}, aa;\n\t}"
+        : "+f"(acc.x), "+f"(acc.y)
+        : "f"(x), "f"(w.x), "f"(w.y));
+}
+
+// Stage x rows [t0, t0+TB) x dims [i0, i0+ilim) and Wg rows [i0, i0+ilim), the latter
+// regrouped as [E/CE][DT][CE] so a thread's CE weights of one dim are contiguous.
+template <typename Elt, int CE>
 __device__ __forceinline__ void gate_load_tile(const Elt* __restrict__ x, const float* __restrict__ wg,
                                                int T, int d, int E, int t0, const GateGeom& geo,
                                                int i0, uint8_t* buf)
 {
-    const int ilim = min(geo.dt, d - i0);
+    const int ilim = min(kGateDT, d - i0);
     const int cpr = ilim * (int)sizeof(Elt) / 16;                 // 16-byte chunks per x row
     for (int q = threadIdx.x; q < geo.TB * cpr; q += blockDim.x) {
         const int r = q / cpr, c = q % cpr, t = t0 + r;
@@ -77,88 +98,85 @@ __device__ __forceinline__ void gate_load_tile(const Elt* __restrict__ x, const 
             cp_async16(buf + (size_t)r * geo.row_bytes + c * 16,
                        reinterpret_cast<const uint8_t*>(x + (size_t)t * d + i0) + c * 16);
     }
-    // Wg rows [i0, i0 + ilim) x E (contiguous in global memory)
-    uint8_t* wb = buf + (size_t)geo.TB * geo.row_bytes;
-    const int wchunks = ilim * E * 4 / 16;
-    const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(wg + (size_t)i0 * E);
-    for (int q = threadIdx.x; q < wchunks; q += blockDim.x) cp_async16(wb + q * 16, wsrc + q * 16);
-}
-
-// acc[c] = fma(xv, w[c], acc[c]) for the CE experts of this thread (one R1 step each)
-template <int CE>
-__device__ __forceinline__ void gate_fma_row(const float* w, float xv, float (&acc)[CE])
-{
-    if constexpr (CE % 4 == 0) {
-#pragma unroll
-        for (int h = 0; h < CE / 4; ++h) {
-            const float4 w4 = *reinterpret_cast<const float4*>(w + 4 * h);
-            acc[4 * h + 0] = __fmaf_rn(xv, w4.x, acc[4 * h + 0]);
-            acc[4 * h + 1] = __fmaf_rn(xv, w4.y, acc[4 * h + 1]);
-            acc[4 * h + 2] = __fmaf_rn(xv, w4.z, acc[4 * h + 2]);
-            acc[4 * h + 3] = __fmaf_rn(xv, w4.w, acc[4 * h + 3]);
+    float* wb = reinterpret_cast<float*>(buf + geo.x_bytes);
+    const float* wsrc = wg + (size_t)i0 * E;
+    if constexpr (CE >= 4) {
+        const int q4 = E / 4;                                     // 16-byte chunks per Wg row
+        for (int q = threadIdx.x; q < ilim * q4; q += blockDim.x) {
+            const int i = q / q4, e = (q % q4) * 4;
+            cp_async16(wb + (size_t)(e / CE) * gate_wg_stride(CE) + i * CE + (e % CE), wsrc + (size_t)i * E + e);
         }
-    } else if constexpr (CE == 2) {
-        const float2 w2 = *reinterpret_cast<const float2*>(w);
-        acc[0] = __fmaf_rn(xv, w2.x, acc[0]);
-        acc[1] = __fmaf_rn(xv, w2.y, acc[1]);
     } else {
-        acc[0] = __fmaf_rn(xv, w[0], acc[0]);
+        for (int q = threadIdx.x; q < ilim * E; q += blockDim.x) {
+            const int i = q / E, e = q % E;
+            wb[(size_t)(e / CE) * gate_wg_stride(CE) + i * CE + (e % CE)] = __ldg(wsrc + q);
+        }
     }
 }
 
-// K1.  Thread (token r, experts e0..e0+CE-1) runs CE independent R1 chains; tiles of x and of
-// Wg stream through shared memory (cp.async, double-buffered).
+// K1.  Tiles of x and of Wg stream through shared memory (cp.async, double-buffered).
 template <typename Elt, int CE>
-__global__ void __launch_bounds__(kGateThreadCap)
+__global__ void __launch_bounds__(kGateThreads)
 gate_topk_kernel(const Elt* __restrict__ x, const float* __restrict__ wg, int T, int d, int E,
                  int k, int renorm, float* __restrict__ logits, int* __restrict__ idx_out,
                  float* __restrict__ w_out, int* __restrict__ hist, int n_tiles)
 {
     extern __shared__ __align__(16) uint8_t gsm[];
     __shared__ int sh_hist[2 * kMaxExperts];
+    constexpr int V = Vec16<Elt>::N;                  // x values per 16-byte shared load
+    constexpr int P = CE >= 2 ? CE / 2 : 1;           // packed chain pairs
     const GateGeom geo = gate_geom(E, sizeof(Elt));
     const int TB = geo.TB;
     uint8_t* buf0 = gsm;
     uint8_t* buf1 = gsm + geo.buf_bytes;
     const int tid = threadIdx.x;
     const int r = tid / geo.tpt;                      // token within block
-    const int e0 = (tid % geo.tpt) * CE;
+    const int grp = tid % geo.tpt;                    // expert group: e0 = grp * CE
+    const int e0 = grp * CE;
     const int t0 = blockIdx.x * TB;
     const bool active = tid < geo.threads;
 
     for (int q = tid; q < 2 * E; q += blockDim.x) sh_hist[q] = 0;
 
-    float acc[CE];
+    float2 acc2[P];
+    float acc1 = 0.f;
 #pragma unroll
-    for (int c = 0; c < CE; ++c) acc[c] = 0.f;
+    for (int c = 0; c < P; ++c) acc2[c] = make_float2(0.f, 0.f);
 
-    const int ntiles = ceil_div(d, geo.dt);
-    gate_load_tile(x, wg, T, d, E, t0, geo, 0, buf0);
+    const int ntiles = ceil_div(d, kGateDT);
+    gate_load_tile<Elt, CE>(x, wg, T, d, E, t0, geo, 0, buf0);
     cp_async_commit();
     for (int it = 0; it < ntiles; ++it) {
         uint8_t* cur = (it & 1) ? buf1 : buf0;
         uint8_t* nxt = (it & 1) ? buf0 : buf1;
-        if (it + 1 < ntiles) gate_load_tile(x, wg, T, d, E, t0, geo, (it + 1) * geo.dt, nxt);
+        if (it + 1 < ntiles) gate_load_tile<Elt, CE>(x, wg, T, d, E, t0, geo, (it + 1) * kGateDT, nxt);
         cp_async_commit();
         cp_async_wait<1>();
         __syncthreads();
-        const int ilim = min(geo.dt, d - it * geo.dt);
+        const int ilim = min(kGateDT, d - it * kGateDT);        // multiple of 8 (d % 8 == 0)
         if (active && t0 + r < T) {
-            const Elt* xr = reinterpret_cast<const Elt*>(cur + (size_t)r * geo.row_bytes);
-            const float* ws = reinterpret_cast<const float*>(cur + (size_t)TB * geo.row_bytes) + e0;
-            if constexpr (sizeof(Elt) == 2) {
-                // two x values per 32-bit shared load
-                const uint32_t* xp = reinterpret_cast<const uint32_t*>(xr);
-#pragma unroll 4
-                for (int i = 0; i < ilim; i += 2) {    // R1: increasing i, one fused step each
-                    const uint32_t pr = xp[i >> 1];
-                    gate_fma_row<CE>(ws + i * E, __uint_as_float(pr << 16), acc);
-                    gate_fma_row<CE>(ws + (i + 1) * E, __uint_as_float(pr & 0xffff0000u), acc);
+            const uint4* xr = reinterpret_cast<const uint4*>(cur + (size_t)r * geo.row_bytes);
+            const float* wp = reinterpret_cast<const float*>(cur + geo.x_bytes) + (size_t)grp * gate_wg_stride(CE);
+#pragma unroll 2
+            for (int iv = 0; iv < ilim / V; ++iv) {
+                float xf[V];
+                unpack16<Elt>(xr[iv], xf);
+#pragma unroll
+                for (int u = 0; u < V; ++u) {               // R1: increasing i, one fused step each
+                    const float* w = wp + (iv * V + u) * CE;
+                    if constexpr (CE >= 4) {
+#pragma unroll
+                        for (int h = 0; h < CE / 4; ++h) {
+                            const float4 w4 = *reinterpret_cast<const float4*>(w + 4 * h);
+                            ffma2(acc2[2 * h], xf[u], make_float2(w4.x, w4.y));
+                            ffma2(acc2[2 * h + 1], xf[u], make_float2(w4.z, w4.w));
+                        }
+                    } else if constexpr (CE == 2) {
+                        ffma2(acc2[0], xf[u], *reinterpret_cast<const float2*>(w));
+                    } else {
+                        acc1 = __fmaf_rn(xf[u], w[0], acc1);
+                    }
                 }
-            } else {
-#pragma unroll 8
-                for (int i = 0; i < ilim; ++i)         // R1: increasing i, one fused step each
-                    gate_fma_row<CE>(ws + i * E, to_f(xr[i]), acc);
             }
         }
         __syncthreads();
@@ -167,10 +185,24 @@ gate_topk_kernel(const Elt* __restrict__ x, const float* __restrict__ wg, int T,
 
     float* lg = reinterpret_cast<float*>(gsm);        // [TB][E]; x buffers are free now
     if (active) {
+        float acc[CE];
+        if constexpr (CE >= 2) {
 #pragma unroll
-        for (int c = 0; c < CE; ++c) {
-            lg[r * E + e0 + c] = acc[c];
-            if (t0 + r < T) logits[(size_t)(t0 + r) * E + e0 + c] = acc[c];
+            for (int c = 0; c < P; ++c) { acc[2 * c] = acc2[c].x; acc[2 * c + 1] = acc2[c].y; }
+        } else {
+            acc[0] = acc1;
+        }
+#pragma unroll
+        for (int c = 0; c < CE; ++c) lg[r * E + e0 + c] = acc[c];
+        if (t0 + r < T) {
+            float* dst = logits + (size_t)(t0 + r) * E + e0;
+            if constexpr (CE % 4 == 0) {
+#pragma unroll
+                for (int c = 0; c < CE; c += 4) *reinterpret_cast<float4*>(dst + c) = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
+            } else {
+#pragma unroll
+                for (int c = 0; c < CE; ++c) dst[c] = acc[c];
+            }
         }
     }
     __syncthreads();
@@ -319,12 +351,10 @@ int launch_routing(const RouteArgs& a, bool is_bf16, cudaStream_t s)
     cudaMemsetAsync(a.hist, 0, sizeof(int) * n_tiles * a.E, s);
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(gate_topk_kernel<bf16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(gate_topk_kernel<bf16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(gate_topk_kernel<float, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(gate_topk_kernel<bf16, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(gate_topk_kernel<float, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(gate_topk_kernel<float, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+#define SET(Elt, CE) cudaFuncSetAttribute(gate_topk_kernel<Elt, CE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)
+        SET(bf16, 8); SET(bf16, 4); SET(bf16, 2); SET(bf16, 1);
+        SET(float, 8); SET(float, 4); SET(float, 2); SET(float, 1);
+#undef SET
         cudaFuncSetAttribute(slot_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr_set = true;
     }
@@ -332,15 +362,15 @@ int launch_routing(const RouteArgs& a, bool is_bf16, cudaStream_t s)
     const int blocks = ceil_div(a.T, g.TB);
     const int thr = round_up(g.threads, 32);
 #define GATE_ARGS a.T, a.d, a.E, a.k, a.renorm, a.logits, a.idx, a.w, a.hist, n_tiles
-    if (is_bf16) {
-        if (g.ce == 2) gate_topk_kernel<bf16, 2><<<blocks, thr, g.smem, s>>>((const bf16*)a.x, a.wg, GATE_ARGS);
-        else if (g.ce == 4) gate_topk_kernel<bf16, 4><<<blocks, thr, g.smem, s>>>((const bf16*)a.x, a.wg, GATE_ARGS);
-        else gate_topk_kernel<bf16, 1><<<blocks, thr, g.smem, s>>>((const bf16*)a.x, a.wg, GATE_ARGS);
-    } else {
-        if (g.ce == 2) gate_topk_kernel<float, 2><<<blocks, thr, g.smem, s>>>((const float*)a.x, a.wg, GATE_ARGS);
-        else if (g.ce == 4) gate_topk_kernel<float, 4><<<blocks, thr, g.smem, s>>>((const float*)a.x, a.wg, GATE_ARGS);
-        else gate_topk_kernel<float, 1><<<blocks, thr, g.smem, s>>>((const float*)a.x, a.wg, GATE_ARGS);
+#define GATE_LAUNCH(Elt)                                                                                    \
+    switch (g.ce) {                                                                                         \
+    case 8: gate_topk_kernel<Elt, 8><<<blocks, thr, g.smem, s>>>((const Elt*)a.x, a.wg, GATE_ARGS); break;  \
+    case 4: gate_topk_kernel<Elt, 4><<<blocks, thr, g.smem, s>>>((const Elt*)a.x, a.wg, GATE_ARGS); break;  \
+    case 2: gate_topk_kernel<Elt, 2><<<blocks, thr, g.smem, s>>>((const Elt*)a.x, a.wg, GATE_ARGS); break;  \
+    default: gate_topk_kernel<Elt, 1><<<blocks, thr, g.smem, s>>>((const Elt*)a.x, a.wg, GATE_ARGS); break; \
     }
+    if (is_bf16) { GATE_LAUNCH(bf16) } else { GATE_LAUNCH(float) }
+#undef GATE_LAUNCH
 #undef GATE_ARGS
     const size_t smem2 = sizeof(int) * (a.E + 32 * a.E + 32 * a.E + a.E);
     slot_scan_kernel<<<n_tiles, kScanTile, smem2, s>>>(a.idx, a.T, a.k, a.E, a.C, a.n_chunks,
