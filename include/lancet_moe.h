@@ -78,8 +78,12 @@ enum {
                                            no dW reordering (the "unoverlapped a2a" of §8(d)) */
     LANCET_FLAG_SIMT_GEMM   = 1u << 3,  /* bf16: use the SIMT GEMM instead of tcgen05 (debug) */
     LANCET_FLAG_NO_DW_OVERLAP = 1u << 4,/* backward: dW GEMMs after all a2a (ablation)       */
-    LANCET_FLAG_NO_SIDE_STREAM = 1u << 5/* world 1 backward: K6/K7 on the caller stream, in
+    LANCET_FLAG_NO_SIDE_STREAM = 1u << 5,/* world 1 backward: K6/K7 on the caller stream, in
                                            line with the GEMMs (A/B of the side stream)      */
+    LANCET_FLAG_GEMM_MULTICAST = 1u << 6/* tcgen05 GEMMs: clusters of two CTA pairs sharing each
+                                           A tile by TMA multicast.  Off by default: clusters
+                                           of 4 fit on 132 of the 148 SMs, which costs more
+                                           than the L2 traffic it saves (profiles/)          */
 };
 
 typedef struct {

@@ -233,6 +233,273 @@ __global__ void transpose_f32_kernel(const float* __restrict__ in, int rows, int
     out[(size_t)c * rows + r] = in[q];
 }
 
+
+// ---------------------------------------------------------------------------------------
+// Streaming variants for E <= 8, d % 256 == 0, d <= 2048 (the GPT-MoE shapes).  A block covers a
+// contiguous token range; thread i owns dims [8i, 8i+8) of every token.  Row data reaches
+// shared memory through a per-thread cp.async ring (each thread copies exactly the 16-byte
+// pieces it later reads, so the ring needs no block barrier) -- the bytes in flight are
+// bounded by shared memory rather than registers, which is what these HBM-latency-bound
+// kernels need.  The packed rows / dlogit of the block's tokens are staged once up front.
+constexpr int kStreamStages = 4;
+
+template <typename Elt> struct Dims8 {                  // 8 elements = NV 16-byte vectors
+    static constexpr int NV = 8 * (int)sizeof(Elt) / 16;
+};
+
+template <typename Elt>
+__device__ __forceinline__ void unpack8(const uint4* v, float (&f)[8]) {
+    if constexpr (sizeof(Elt) == 2) {
+        unpack16<bf16>(v[0], f);
+    } else {
+        unpack16<float>(v[0], f);
+        unpack16<float>(v[1], f + 4);
+    }
+}
+
+__device__ __forceinline__ void cp_async16_s(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+                 "l"(gmem)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit_s() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_s() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <typename Elt, int KK>
+struct K6Geom {
+    static constexpr int NV = Dims8<Elt>::NV;
+    static constexpr int U = (8 / (KK * NV)) > 0 ? 8 / (KK * NV) : 1;   // tokens per ring slot
+    static constexpr int SLOT = U * KK * NV;                              // 16-byte pieces per thread
+};
+
+// K6: dx_t = sum_j dX[prow_tj] + sum_e dlogit_te Wg[:, e]; Wg^T slice of the thread in registers
+template <typename Elt, int KK, int EE>
+__global__ void __launch_bounds__(256)
+k6_stream_kernel(const Elt* __restrict__ dxe, const int* __restrict__ prow,
+                 const float* __restrict__ dlogit, const float* __restrict__ wgT, int t0, int t1,
+                 int k, int d, int E, int tpb, Elt* __restrict__ dx)
+{
+    using G = K6Geom<Elt, KK>;
+    constexpr int NV = G::NV, U = G::U, S = kStreamStages;
+    extern __shared__ __align__(16) uint4 ring[];          // [S][SLOT][NT]
+    const int NT = blockDim.x, tid = threadIdx.x;
+    int* srow = reinterpret_cast<int*>(ring + (size_t)S * G::SLOT * NT);   // [tpb][KK]
+    float* sdl = reinterpret_cast<float*>(srow + tpb * KK);                 // [tpb][EE]
+    const int tb0 = t0 + blockIdx.x * tpb;
+    const int tb1 = min(t1, tb0 + tpb);
+    if (tb0 >= tb1) return;
+    const int nt = tb1 - tb0;
+    for (int q = tid; q < nt * KK; q += NT) {
+        const int r = q / KK, j = q % KK;
+        srow[q] = j < k ? prow[(size_t)(tb0 + r) * k + j] : -1;
+    }
+    for (int q = tid; q < nt * EE; q += NT) {
+        const int r = q / EE, e = q % EE;
+        sdl[q] = e < E ? dlogit[(size_t)(tb0 + r) * E + e] : 0.f;
+    }
+    const int i0 = tid * 8;
+    float2 wg2[EE][4];
+#pragma unroll
+    for (int e = 0; e < EE; ++e) {
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+        if (e < E) {
+            a = __ldg(reinterpret_cast<const float4*>(wgT + (size_t)e * d + i0));
+            b = __ldg(reinterpret_cast<const float4*>(wgT + (size_t)e * d + i0) + 1);
+        }
+        wg2[e][0] = make_float2(a.x, a.y); wg2[e][1] = make_float2(a.z, a.w);
+        wg2[e][2] = make_float2(b.x, b.y); wg2[e][3] = make_float2(b.z, b.w);
+    }
+    __syncthreads();
+    const int ng = ceil_div(nt, U);
+    auto issue = [&](int g) {
+        uint4* slot = ring + (size_t)(g % S) * G::SLOT * NT;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int r = g * U + u;
+#pragma unroll
+            for (int j = 0; j < KK; ++j) {
+                const int row = r < nt ? srow[r * KK + j] : -1;
+                if (row >= 0) {
+                    const uint4* src = reinterpret_cast<const uint4*>(dxe + (size_t)row * d + i0);
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) cp_async16_s(slot + ((u * KK + j) * NV + v) * NT + tid, src + v);
+                }
+            }
+        }
+    };
+#pragma unroll
+    for (int g = 0; g < S - 1; ++g) {
+        if (g < ng) issue(g);
+        cp_async_commit_s();
+    }
+    for (int g = 0; g < ng; ++g) {
+        if (g + S - 1 < ng) issue(g + S - 1);
+        cp_async_commit_s();
+        cp_async_wait_s<S - 1>();
+        const uint4* slot = ring + (size_t)(g % S) * G::SLOT * NT;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int r = g * U + u;
+            if (r >= nt) break;
+            float acc[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+#pragma unroll
+            for (int j = 0; j < KK; ++j) {
+                if (srow[r * KK + j] >= 0) {
+                    uint4 raw[NV];
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) raw[v] = slot[((u * KK + j) * NV + v) * NT + tid];
+                    float f[8];
+                    unpack8<Elt>(raw, f);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) acc[i] += f[i];
+                }
+            }
+            float2 a2[4] = {make_float2(acc[0], acc[1]), make_float2(acc[2], acc[3]),
+                            make_float2(acc[4], acc[5]), make_float2(acc[6], acc[7])};
+#pragma unroll
+            for (int e = 0; e < EE; ++e) {
+                const float dl = sdl[r * EE + e];
+                const float2 dl2 = make_float2(dl, dl);
+#pragma unroll
+                for (int p = 0; p < 4; ++p) a2[p] = __ffma2_rn(dl2, wg2[e][p], a2[p]);
+            }
+            const float o[8] = {a2[0].x, a2[0].y, a2[1].x, a2[1].y, a2[2].x, a2[2].y, a2[3].x, a2[3].y};
+            Elt* dst = dx + (size_t)(tb0 + r) * d + i0;
+            if constexpr (sizeof(Elt) == 2) {
+                st_v4(dst, pack16<bf16>(o));
+            } else {
+                st_v4(dst, pack16<float>(o));
+                st_v4(dst + 4, pack16<float>(o + 4));
+            }
+        }
+    }
+    cp_async_wait_s<0>();
+}
+
+// K7 partials: block b sums x_t (x) dlogit_t over its contiguous token range -> partial[b][E][d]
+template <typename Elt, int EE>
+__global__ void __launch_bounds__(256)
+dwg_stream_kernel(const Elt* __restrict__ x, const float* __restrict__ dlogit, int T, int d, int E,
+                  int tpb, float* __restrict__ partial)
+{
+    constexpr int NV = Dims8<Elt>::NV, U = 8 / NV, S = kStreamStages;
+    extern __shared__ __align__(16) uint4 ring[];          // [S][U*NV][NT]
+    const int NT = blockDim.x, tid = threadIdx.x;
+    float* sdl = reinterpret_cast<float*>(ring + (size_t)S * U * NV * NT);   // [tpb][EE]
+    const int tb0 = blockIdx.x * tpb;
+    const int nt = max(0, min(T, tb0 + tpb) - tb0);
+    for (int q = tid; q < nt * EE; q += NT) {
+        const int r = q / EE, e = q % EE;
+        sdl[q] = e < E ? dlogit[(size_t)(tb0 + r) * E + e] : 0.f;
+    }
+    const int i0 = tid * 8;
+    float2 acc[8][EE / 2];
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int p = 0; p < EE / 2; ++p) acc[a][p] = make_float2(0.f, 0.f);
+    __syncthreads();
+    const int ng = ceil_div(nt, U);
+    auto issue = [&](int g) {
+        uint4* slot = ring + (size_t)(g % S) * U * NV * NT;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int r = g * U + u;
+            if (r < nt) {
+                const uint4* src = reinterpret_cast<const uint4*>(x + (size_t)(tb0 + r) * d + i0);
+#pragma unroll
+                for (int v = 0; v < NV; ++v) cp_async16_s(slot + (u * NV + v) * NT + tid, src + v);
+            }
+        }
+    };
+#pragma unroll
+    for (int g = 0; g < S - 1; ++g) {
+        if (g < ng) issue(g);
+        cp_async_commit_s();
+    }
+    for (int g = 0; g < ng; ++g) {
+        if (g + S - 1 < ng) issue(g + S - 1);
+        cp_async_commit_s();
+        cp_async_wait_s<S - 1>();
+        const uint4* slot = ring + (size_t)(g % S) * U * NV * NT;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int r = g * U + u;
+            if (r >= nt) break;
+            uint4 raw[NV];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) raw[v] = slot[(u * NV + v) * NT + tid];
+            float xf[8];
+            unpack8<Elt>(raw, xf);
+            float2 dl[EE / 2];
+#pragma unroll
+            for (int p = 0; p < EE / 2; ++p) dl[p] = *reinterpret_cast<const float2*>(sdl + r * EE + 2 * p);
+#pragma unroll
+            for (int a = 0; a < 8; ++a)
+#pragma unroll
+                for (int p = 0; p < EE / 2; ++p) acc[a][p] = __ffma2_rn(make_float2(xf[a], xf[a]), dl[p], acc[a][p]);
+        }
+    }
+    cp_async_wait_s<0>();
+    // partial[b][e][i]: for each expert the block's threads store consecutive 32-byte runs
+    float* out = partial + (size_t)blockIdx.x * E * d + i0;
+#pragma unroll
+    for (int p = 0; p < EE / 2; ++p) {
+        if (2 * p < E) {
+            float v[8];
+#pragma unroll
+            for (int a = 0; a < 8; ++a) v[a] = acc[a][p].x;
+            st_v4(out + (size_t)(2 * p) * d, pack16<float>(v));
+            st_v4(out + (size_t)(2 * p) * d + 4, pack16<float>(v + 4));
+        }
+        if (2 * p + 1 < E) {
+            float v[8];
+#pragma unroll
+            for (int a = 0; a < 8; ++a) v[a] = acc[a][p].y;
+            st_v4(out + (size_t)(2 * p + 1) * d, pack16<float>(v));
+            st_v4(out + (size_t)(2 * p + 1) * d + 4, pack16<float>(v + 4));
+        }
+    }
+}
+
+// Deterministic reduction of nb partials: block = 32 outputs (8 threads x float4) x 32 part
+// streams; stream s sums partials s, s+32, ... in order, the 32 stream sums are added in order.
+__global__ void __launch_bounds__(256)
+dwg_reduce4_kernel(const float* __restrict__ partial, int nb, int n_out, int d_model, int E,
+                   float* __restrict__ dwg)
+{
+    __shared__ float4 red[32][8];
+    const int q4 = threadIdx.x & 7, st = threadIdx.x >> 3;
+    const int o = blockIdx.x * 32 + q4 * 4;                 // n_out % 4 == 0
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (o < n_out) {
+#pragma unroll 8
+        for (int b = st; b < nb; b += 32) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(partial + (size_t)b * n_out + o));
+            s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+        }
+    }
+    red[st][q4] = s;
+    __syncthreads();
+    if (st == 0 && o < n_out) {
+        float4 r = red[0][q4];
+        for (int i = 1; i < 32; ++i) {
+            const float4 v = red[i][q4];
+            r.x += v.x; r.y += v.y; r.z += v.z; r.w += v.w;
+        }
+        // o indexes the [E][d] partial layout; dWg is [d][E]
+        const int e = o / d_model, i = o % d_model;
+        dwg[(size_t)i * E + e] = r.x;
+        dwg[(size_t)(i + 1) * E + e] = r.y;
+        dwg[(size_t)(i + 2) * E + e] = r.z;
+        dwg[(size_t)(i + 3) * E + e] = r.w;
+    }
+}
+
 }  // namespace
 
 #define LANCET_DISPATCH_K(k, ...)                                             \
@@ -268,11 +535,50 @@ static void launch_k6(const DispatchArgs& a, const void* dxe, const int* prow, c
                                                                   a.k, a.d, a.E, (Elt*)dx);
 }
 
+static bool stream_ok(int d, int E) { return E <= 8 && d % 256 == 0 && d <= 2048; }
+static int ee_of(int E) { return E <= 2 ? 2 : E <= 4 ? 4 : 8; }
+
+template <typename Elt, int KK, int EE>
+static void launch_k6_stream(const DispatchArgs& a, const void* dxe, const int* prow, const float* dlogit,
+                             const float* wgT, void* dx, int t0, int t1, int num_sms, cudaStream_t s)
+{
+    using G = K6Geom<Elt, KK>;
+    const int NT = a.d / 8;
+    // ~3 blocks per SM of 128 threads; a block's ring is kStreamStages slots of U tokens
+    const int per_sm = std::max(1, 384 / NT);
+    const int nb = std::max(1, std::min(ceil_div(t1 - t0, G::U), per_sm * num_sms));
+    const int tpb = ceil_div(t1 - t0, nb);
+    const size_t smem = (size_t)kStreamStages * G::SLOT * NT * 16 + (size_t)tpb * (KK + EE) * 4;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k6_stream_kernel<Elt, KK, EE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+    }
+    k6_stream_kernel<Elt, KK, EE><<<ceil_div(t1 - t0, tpb), NT, smem, s>>>(
+        (const Elt*)dxe, prow, dlogit, wgT, t0, t1, a.k, a.d, a.E, tpb, (Elt*)dx);
+}
+
 int launch_unpermute_gate_bwd(const DispatchArgs& a, const void* dxe, const int* prow,
                               const float* dlogit, const float* wgT, void* dx, int t0, int t1,
                               int num_sms, bool is_bf16, cudaStream_t s)
 {
     if (t1 <= t0) return 0;
+    if (stream_ok(a.d, a.E) && a.k <= 4) {
+        const int ee = ee_of(a.E);
+#define K6S(Elt, KK)                                                                                              \
+    do {                                                                                                          \
+        if (ee == 2) launch_k6_stream<Elt, KK, 2>(a, dxe, prow, dlogit, wgT, dx, t0, t1, num_sms, s);            \
+        else if (ee == 4) launch_k6_stream<Elt, KK, 4>(a, dxe, prow, dlogit, wgT, dx, t0, t1, num_sms, s);       \
+        else launch_k6_stream<Elt, KK, 8>(a, dxe, prow, dlogit, wgT, dx, t0, t1, num_sms, s);                    \
+    } while (0)
+        if (is_bf16) {
+            if (a.k == 1) K6S(bf16, 1); else if (a.k == 2) K6S(bf16, 2); else K6S(bf16, 4);
+        } else {
+            if (a.k == 1) K6S(float, 1); else if (a.k == 2) K6S(float, 2); else K6S(float, 4);
+        }
+#undef K6S
+        return 1;
+    }
     const bool sm = (size_t)a.d * a.E * 4 <= kSmemWgMax;
     LANCET_DISPATCH_K(a.k, {
         if (is_bf16) {
@@ -286,11 +592,50 @@ int launch_unpermute_gate_bwd(const DispatchArgs& a, const void* dxe, const int*
     return 1;
 }
 
-size_t dwg_partial_floats(int T, int d, int E) { return (size_t)ceil_div(T, kDwgTok) * d * E; }
+constexpr int kDwgStreamMaxBlocks = 512;
+
+size_t dwg_partial_floats(int T, int d, int E)
+{
+    size_t n = (size_t)ceil_div(T, kDwgTok) * d * E;
+    if (stream_ok(d, E)) n = std::max(n, (size_t)kDwgStreamMaxBlocks * d * E);
+    return n;
+}
+
+template <typename Elt, int EE>
+static void launch_dwg_stream(const Elt* x, const float* dlogit, int T, int d, int E, float* partial,
+                              float* dwg, int num_sms, cudaStream_t s)
+{
+    constexpr int NV = Dims8<Elt>::NV, U = 8 / NV;
+    const int NT = d / 8;
+    const int per_sm = std::max(1, 384 / NT);
+    const int nb = std::max(1, std::min({ceil_div(T, 2 * U), per_sm * num_sms, kDwgStreamMaxBlocks}));
+    const int tpb = ceil_div(T, nb);
+    const int grid = ceil_div(T, tpb);
+    const size_t smem = (size_t)kStreamStages * U * NV * NT * 16 + (size_t)tpb * EE * 4;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(dwg_stream_kernel<Elt, EE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+    }
+    dwg_stream_kernel<Elt, EE><<<grid, NT, smem, s>>>(x, dlogit, T, d, E, tpb, partial);
+    dwg_reduce4_kernel<<<ceil_div(d * E, 32), 256, 0, s>>>(partial, grid, d * E, d, E, dwg);
+}
 
 int launch_dwg(const void* x, const float* dlogit, int T, int d, int E, float* partial,
-               float* dwg, bool is_bf16, cudaStream_t s)
+               float* dwg, bool is_bf16, int num_sms, cudaStream_t s)
 {
+    if (stream_ok(d, E) && (d * E) % 4 == 0) {
+        const int ee = ee_of(E);
+#define DWS(Elt)                                                                                                  \
+    do {                                                                                                          \
+        if (ee == 2) launch_dwg_stream<Elt, 2>((const Elt*)x, dlogit, T, d, E, partial, dwg, num_sms, s);        \
+        else if (ee == 4) launch_dwg_stream<Elt, 4>((const Elt*)x, dlogit, T, d, E, partial, dwg, num_sms, s);   \
+        else launch_dwg_stream<Elt, 8>((const Elt*)x, dlogit, T, d, E, partial, dwg, num_sms, s);                \
+    } while (0)
+        if (is_bf16) DWS(bf16); else DWS(float);
+#undef DWS
+        return 2;
+    }
     const int nb = ceil_div(T, kDwgTok);
     dim3 grid(nb, ceil_div(d, kDwgThreads * 4), ceil_div(E, kDwgE));
     if (is_bf16)

@@ -119,6 +119,16 @@ __device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* map, uint64_
         "l"(map), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1)
         : "memory");
 }
+// 2-SM load multicast to the CTAs in `mask` (same smem offset in each); every destination's
+// bytes are counted on the barrier of that destination's pair leader.
+__device__ __forceinline__ void tma_load_2d_pair_mc(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1,
+                                                    uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1), "h"(mask)
+        : "memory");
+}
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
     asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
                  "r"(smem_u32(src)), "r"(c0), "r"(c1)
@@ -134,7 +144,7 @@ __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 template <int CG>
-__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+__device__ __forceinline__ void tc_commit(uint64_t* bar, uint16_t mask = 0x3) {
     if constexpr (CG == 1) {
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                      : "memory");
@@ -142,7 +152,7 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
         asm volatile(
             "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
                 smem_u32(bar)),
-            "h"((uint16_t)0x3)
+            "h"(mask)
             : "memory");
     }
 }
@@ -217,7 +227,7 @@ __device__ __forceinline__ void decode_tile(int tile, const int* tstart, int ng,
 // byte offset of 16-byte chunk j of row r in a [32 rows][64 B] box stored with SWIZZLE_64B
 __device__ __forceinline__ uint32_t sw64(int r, int j) { return r * 64 + ((j ^ ((r >> 1) & 3)) << 4); }
 
-template <int BN, bool A_MN, bool B_MN, int CG>
+template <int BN, bool A_MN, bool B_MN, int CG, int MC>
 __global__ void __launch_bounds__(kThreads, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2,
@@ -244,10 +254,16 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     int* soff = srows + kMaxGroups;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int ntn = p.N / BN;
-    const uint32_t rank = CG == 2 ? cta_rank() : 0;   // CTA within the pair
+    // MC pairs of a cluster share one A tile (TMA multicast) and compute MC adjacent N tiles:
+    // "super tiles" of MC * BN columns; pair pp takes n tile ntp * MC + pp
+    const int ntn = p.N / (BN * MC);
+    const uint32_t crank = CG * MC > 1 ? cta_rank() : 0;
+    const uint32_t rank = CG == 2 ? (crank & 1) : 0;    // CTA within the pair
+    const int pp = (int)(crank / CG);                   // pair within the cluster
+    const uint32_t lead_rank = crank - rank;            // cluster rank of the pair leader
+    const uint16_t pair_mask = (uint16_t)(0x3u << (2 * pp));
     const bool leader = rank == 0;
-    const int cluster = blockIdx.x / CG, n_clusters = gridDim.x / CG;
+    const int cluster = blockIdx.x / (CG * MC), n_clusters = gridDim.x / (CG * MC);
     constexpr int MT = BM * CG;                        // rows of A per (pair) tile
 
     if (threadIdx.x == 0) {
@@ -271,7 +287,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         }
     }
     if (warp == 1 && lane == 0) {
-        for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+        for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], MC); }
         for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], kEpiWarps * CG); }
         for (int i = 0; i < kEpiWarps; ++i) mbar_init(&abar[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -288,7 +304,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         }
     }
     tc_fence_before();
-    if constexpr (CG == 2) cluster_sync();
+    if constexpr (CG * MC > 1) cluster_sync();
     else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
@@ -302,7 +318,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             for (int tile = cluster; tile < total; tile += n_clusters) {
                 int g, mt, nt;
                 decode_tile(tile, tstart, p.n_groups, ntn, g, mt, nt);
-                const int nb = nt * BN + (int)rank * BNC;      // this CTA's B rows / columns
+                const int nb = (nt * MC + pp) * BN + (int)rank * BNC;   // this CTA's B rows / columns
                 int num_kb, arow, brow;
                 if (p.mode == GEMM_M_GROUPED) {
                     num_kb = p.K / BK;
@@ -324,7 +340,13 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         if constexpr (CG == 1) tma_load_2d(map, &full[stage], dst, c0, c1);                  \
         else tma_load_2d_pair(map, &full[stage], dst, c0, c1);                               \
     } while (0)
-                    if (A_MN) {
+                    if constexpr (MC == 2) {
+                        // this CTA loads 64 of its 128 A rows and multicasts them to the CTA
+                        // with the same rank in the other pair (which loads the other 64)
+                        const uint16_t mc_mask = (uint16_t)((1u << rank) | (1u << (CG + rank)));
+                        if (A_MN) tma_load_2d_pair_mc(&tmA, &full[stage], a_dst + pp * 8192, m0 + 64 * pp, arow + kb * BK, mc_mask);
+                        else tma_load_2d_pair_mc(&tmA, &full[stage], a_dst + pp * 8192, kb * BK, arow + 64 * pp, mc_mask);
+                    } else if (A_MN) {
 #pragma unroll
                         for (int i = 0; i < BM / 64; ++i) LOAD(&tmA, a_dst + i * 8192, m0 + 64 * i, arow + kb * BK);
                     } else {
@@ -366,10 +388,11 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                     for (int k = 0; k < BK / UMMA_K; ++k)
                         tc_mma<CG>(tmem_d, operand_desc<A_MN>(a_base, k), operand_desc<B_MN>(b_base, k), idesc,
                                    (kb | k) != 0 ? 1u : 0u);
-                    tc_commit<CG>(&empty[stage]);
+                    // the stage is free once BOTH pairs have read it (its A half came from each)
+                    tc_commit<CG>(&empty[stage], MC == 2 ? (uint16_t)0xF : pair_mask);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
-                tc_commit<CG>(&tfull[acc]);
+                tc_commit<CG>(&tfull[acc], pair_mask);
             }
         }
     } else if (warp >= 4) {
@@ -392,7 +415,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
             const bool has_k = p.mode == GEMM_M_GROUPED ? (p.K > 0) : (srows[g] > 0);
-            const int n0 = nt * BN;
+            const int n0 = (nt * MC + pp) * BN;
             if constexpr (CF::kStaged) {
                 const int mrow = mt * MT + (int)rank * BM;                // first row of this CTA
                 const int row0 = soff[g] + mrow + q * 32;                 // this warp's 32 rows
@@ -489,13 +512,13 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             __syncwarp();
             if (lane == 0) {
                 if (CG == 1 || leader) mbar_arrive(&tempty[acc]);
-                else mbar_arrive_cluster(&tempty[acc], 0);        // the leader's MMA waits on it
+                else mbar_arrive_cluster(&tempty[acc], lead_rank); // the leader's MMA waits on it
             }
         }
         if (CF::kStaged && lane == 0) bulk_wait0();
     }
     tc_fence_before();
-    if constexpr (CG == 2) cluster_sync();
+    if constexpr (CG * MC > 1) cluster_sync();
     else __syncthreads();
     if (warp == 2) {
         tc_fence_after();
@@ -541,7 +564,7 @@ static bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t o
     return r == CUDA_SUCCESS;
 }
 
-template <int BN, bool A_MN, bool B_MN, int CG>
+template <int BN, bool A_MN, bool B_MN, int CG, int MC>
 static int launch_cfg(const GemmArgs& a, int num_sms, cudaStream_t s)
 {
     using CF = Cfg<BN, A_MN, CG>;
@@ -553,7 +576,7 @@ static int launch_cfg(const GemmArgs& a, int num_sms, cudaStream_t s)
     memset(&tx, 0, sizeof(tx));
     bool ok;
     if (A_MN) ok = make_map(&ta, a.A, a.M, a.a_rows, a.lda, 64, 64);
-    else ok = make_map(&ta, a.A, a.K, a.a_rows, a.lda, 64, BM);
+    else ok = make_map(&ta, a.A, a.K, a.a_rows, a.lda, 64, BM / MC);
     if (B_MN) ok = ok && make_map(&tb, a.B, a.N, a.b_rows, a.ldb, 64, 64);
     else ok = ok && make_map(&tb, a.B, a.K, a.b_rows, a.ldb, 64, BN / CG);
     if (CF::kStaged) {
@@ -567,29 +590,48 @@ static int launch_cfg(const GemmArgs& a, int num_sms, cudaStream_t s)
     constexpr size_t smem = CF::kSmem;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(tc_gemm_kernel<BN, A_MN, B_MN, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(tc_gemm_kernel<BN, A_MN, B_MN, CG, MC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
         attr = true;
     }
     // persistent grid: at most one CTA per SM (pairs on one TPC when CG == 2), never more
     // (pair) tiles than the upper bound of tiles
     long max_tiles;
-    if (a.mode == GEMM_M_GROUPED) max_tiles = (long)ceil_div(a.max_rows, BM * CG) * a.n_groups * (a.N / BN);
-    else max_tiles = (long)(a.M / (BM * CG)) * (a.N / BN) * a.n_groups;
-    const int clusters = (int)std::max<long>(1, std::min<long>(num_sms / CG, max_tiles));
+    if (a.mode == GEMM_M_GROUPED) max_tiles = (long)ceil_div(a.max_rows, BM * CG) * a.n_groups * (a.N / (BN * MC));
+    else max_tiles = (long)(a.M / (BM * CG)) * (a.N / (BN * MC)) * a.n_groups;
+    // clusters of 4 cannot tile every GPC: cap the persistent grid at what is co-resident
+    static int max_active = -1;
+    if (max_active < 0) {
+        cudaLaunchConfig_t q{};
+        q.gridDim = dim3(num_sms);
+        q.blockDim = dim3(kThreads);
+        q.dynamicSmemBytes = smem;
+        cudaLaunchAttribute qa[1];
+        qa[0].id = cudaLaunchAttributeClusterDimension;
+        qa[0].val.clusterDim.x = CG * MC;
+        qa[0].val.clusterDim.y = 1;
+        qa[0].val.clusterDim.z = 1;
+        q.attrs = qa;
+        q.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, tc_gemm_kernel<BN, A_MN, B_MN, CG, MC>, &q) != cudaSuccess || n <= 0)
+            n = num_sms / (CG * MC);
+        max_active = n;
+    }
+    const int clusters = (int)std::max<long>(1, std::min<long>(std::min(num_sms / (CG * MC), max_active), max_tiles));
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(clusters * CG);
+    cfg.gridDim = dim3(clusters * CG * MC);
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attrs[1];
     attrs[0].id = cudaLaunchAttributeClusterDimension;
-    attrs[0].val.clusterDim.x = CG;
+    attrs[0].val.clusterDim.x = CG * MC;
     attrs[0].val.clusterDim.y = 1;
     attrs[0].val.clusterDim.z = 1;
     cfg.attrs = attrs;
     cfg.numAttrs = 1;
-    if (cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, A_MN, B_MN, CG>, ta, tb, tcm, tc2, tx, p) != cudaSuccess)
+    if (cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, A_MN, B_MN, CG, MC>, ta, tb, tcm, tc2, tx, p) != cudaSuccess)
         return -1;
     return 1;
 }
@@ -600,7 +642,10 @@ static int launch_cg(const GemmArgs& a, int num_sms, cudaStream_t s)
     // CTA pairs need 256-row (pair) tiles: always possible for M-grouped GEMMs (a pair tile's
     // upper half past a group is computed but not stored), for K-grouped when M % 256 == 0
     const bool pair = a.mode == GEMM_M_GROUPED || a.M % (2 * BM) == 0;
-    return pair ? launch_cfg<BN, A_MN, B_MN, 2>(a, num_sms, s) : launch_cfg<BN, A_MN, B_MN, 1>(a, num_sms, s);
+    if (!pair) return launch_cfg<BN, A_MN, B_MN, 1, 1>(a, num_sms, s);
+    // two pairs share each A tile (multicast) when the N tiles pair up
+    if (a.multicast && (a.N / BN) % 2 == 0) return launch_cfg<BN, A_MN, B_MN, 2, 2>(a, num_sms, s);
+    return launch_cfg<BN, A_MN, B_MN, 2, 1>(a, num_sms, s);
 }
 
 }  // namespace tc

@@ -45,7 +45,7 @@ int launch_unpermute_gate_bwd(const DispatchArgs& a, const void* dxe, const int*
                               int num_sms, bool is_bf16, cudaStream_t s);
 // dWg = x^T dlogit (K7); partial: [ceil(T/64)][d][E] fp32 scratch
 int launch_dwg(const void* x, const float* dlogit, int T, int d, int E, float* partial,
-               float* dwg, bool is_bf16, cudaStream_t s);
+               float* dwg, bool is_bf16, int num_sms, cudaStream_t s);
 size_t dwg_partial_floats(int T, int d, int E);
 // zero rows [off_g + rows_g, off_g + round_up(rows_g, 128)) of a packed buffer
 int launch_zero_pads(void* buf, int row_elems, const int* grp_off, const int* grp_rows,
@@ -75,6 +75,7 @@ struct GemmArgs {
     bool a_mn, b_mn;
     long a_rows, b_rows;  // outer extents of A and B viewed as 2D row-major tensors (TMA maps)
     long c_rows;          // outer extent of C / C2 / aux (M-grouped; TMA store maps)
+    bool multicast;       // tcgen05: two CTA pairs share each A tile by TMA multicast
 };
 int launch_gemm_simt(const GemmArgs& a, bool is_bf16, cudaStream_t s);
 

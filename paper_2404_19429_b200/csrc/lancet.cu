@@ -142,6 +142,7 @@ lancet_status run_gemm(lancet_ctx* c, GemmArgs& a, cudaStream_t s, int* launches
 {
     const bool use_tc = c->bf16 && !(c->cfg.flags & LANCET_FLAG_SIMT_GEMM) && gemm_tc_supported(a);
     if (use_tc) {
+        a.multicast = (c->cfg.flags & LANCET_FLAG_GEMM_MULTICAST) != 0;
         const int sms = c->cfg.gemm_sms > 0 ? std::min(c->cfg.gemm_sms, c->num_sms) : c->num_sms;
         *launches += launch_gemm_tc(a, sms, s);
     } else {
@@ -441,7 +442,7 @@ lancet_status gate_backward_dx(lancet_ctx* c, const DispatchArgs& da, const void
 lancet_status gate_backward_dwg(lancet_ctx* c, float* dwg, cudaStream_t s, int* L)
 {
     OpScope op(c, "gate_dwg", s == c->s_comp ? 0 : 2, -1, s);
-    *L += launch_dwg(c->x, c->dlogit, c->T, c->cfg.d_model, c->cfg.n_experts, c->dwg_partial, dwg, c->bf16, s);
+    *L += launch_dwg(c->x, c->dlogit, c->T, c->cfg.d_model, c->cfg.n_experts, c->dwg_partial, dwg, c->bf16, c->num_sms, s);
     CHECK_LAUNCH();
     return LANCET_OK;
 }

@@ -18,24 +18,28 @@
 
 namespace lancet {
 
-constexpr int kGateDT = 128;     // d-tile staged in shared memory (double-buffered cp.async)
+constexpr int kGateDT = 128;     // d-tile staged in shared memory (cp.async ring)
+constexpr int kGateStages = 4;   // ring depth: ~3 tiles of x in flight per block (HBM latency)
 constexpr int kGateThreads = 128;
+constexpr int kGateMaxTB = 64;   // tokens per block (T=16k -> 256 blocks, all resident)
 
-// Thread (token r, experts e0..e0+CE-1) runs CE independent R1 chains, two at a time with the
-// packed fp32 FMA (fma.rn.f32x2: two IEEE fused multiply-adds, each rounded once -- bitwise the
-// same as two fmaf).  CE = 8, 4, 2 or 1 (largest dividing E).
+// Thread (tokens r..r+TT-1, experts e0..e0+CE-1) runs TT*CE independent R1 chains, two at a
+// time with the packed fp32 FMA (fma.rn.f32x2: two IEEE fused multiply-adds, each rounded once
+// -- bitwise the same as two fmaf).  CE = 8, 4, 2 or 1 (largest dividing E); TT = 2 tokens per
+// thread when CE >= 4, so each staged Wg value feeds two tokens (the kernel is bound by
+// shared-memory reads and FMA-chain latency, not by HBM).
 struct GateGeom {
     int ce;        // experts (R1 chains) per thread
-    int tpt;       // threads per token = E / ce
+    int tt;        // tokens per thread
+    int tpt;       // threads per token group = E / ce
     int TB;        // tokens per block
-    int threads;   // TB * tpt
+    int threads;   // TB / tt * tpt
     int row_bytes; // bytes per staged x row (kGateDT elements + 16 B against bank conflicts)
     size_t x_bytes, buf_bytes, smem;
 };
 
 __host__ __device__ inline int gate_ce(int E)
 {
-    // 8 chains per thread when there are enough tokens per block to keep the SMs busy
     return (E % 8 == 0 && E >= 16) ? 8 : (E % 4 == 0) ? 4 : (E % 2 == 0) ? 2 : 1;
 }
 
@@ -46,15 +50,16 @@ __host__ __device__ inline GateGeom gate_geom(int E, int elt_bytes)
 {
     GateGeom g;
     g.ce = gate_ce(E);
+    g.tt = g.ce >= 4 ? 2 : 1;
     g.tpt = E / g.ce;
-    g.TB = kGateThreads / g.tpt;
-    if (g.TB > 64) g.TB = 64;
-    if (g.TB < 1) g.TB = 1;
-    g.threads = g.TB * g.tpt;
+    g.TB = kGateThreads * g.tt / g.tpt;
+    if (g.TB > kGateMaxTB) g.TB = kGateMaxTB;
+    if (g.TB < g.tt) g.TB = g.tt;
+    g.threads = g.TB / g.tt * g.tpt;
     g.row_bytes = kGateDT * elt_bytes + 16;
     g.x_bytes = (size_t)g.TB * g.row_bytes;
     g.buf_bytes = g.x_bytes + (size_t)g.tpt * gate_wg_stride(g.ce) * 4;   // x tile | Wg tile [E/CE][DT][CE]
-    const size_t xs = 2 * g.buf_bytes;
+    const size_t xs = kGateStages * g.buf_bytes;
     const size_t lg = sizeof(float) * (size_t)g.TB * E;
     g.smem = xs > lg ? xs : lg;
     return g;
@@ -91,12 +96,22 @@ __device__ __forceinline__ void gate_load_tile(const Elt* __restrict__ x, const 
                                                int i0, uint8_t* buf)
 {
     const int ilim = min(kGateDT, d - i0);
-    const int cpr = ilim * (int)sizeof(Elt) / 16;                 // 16-byte chunks per x row
-    for (int q = threadIdx.x; q < geo.TB * cpr; q += blockDim.x) {
-        const int r = q / cpr, c = q % cpr, t = t0 + r;
-        if (t < T)
-            cp_async16(buf + (size_t)r * geo.row_bytes + c * 16,
-                       reinterpret_cast<const uint8_t*>(x + (size_t)t * d + i0) + c * 16);
+    constexpr int kFull = kGateDT * (int)sizeof(Elt) / 16;       // 16-byte chunks per full row
+    if (ilim == kGateDT) {
+        for (int q = threadIdx.x; q < geo.TB * kFull; q += blockDim.x) {
+            const int r = q / kFull, c = q % kFull, t = t0 + r;     // kFull: power of two
+            if (t < T)
+                cp_async16(buf + (size_t)r * geo.row_bytes + c * 16,
+                           reinterpret_cast<const uint8_t*>(x + (size_t)t * d + i0) + c * 16);
+        }
+    } else {
+        const int cpr = ilim * (int)sizeof(Elt) / 16;
+        for (int q = threadIdx.x; q < geo.TB * cpr; q += blockDim.x) {
+            const int r = q / cpr, c = q % cpr, t = t0 + r;
+            if (t < T)
+                cp_async16(buf + (size_t)r * geo.row_bytes + c * 16,
+                           reinterpret_cast<const uint8_t*>(x + (size_t)t * d + i0) + c * 16);
+        }
     }
     float* wb = reinterpret_cast<float*>(buf + geo.x_bytes);
     const float* wsrc = wg + (size_t)i0 * E;
@@ -114,8 +129,8 @@ __device__ __forceinline__ void gate_load_tile(const Elt* __restrict__ x, const 
     }
 }
 
-// K1.  Tiles of x and of Wg stream through shared memory (cp.async, double-buffered).
-template <typename Elt, int CE>
+// K1.  Tiles of x and of Wg stream through shared memory (cp.async ring).
+template <typename Elt, int CE, int TT>
 __global__ void __launch_bounds__(kGateThreads)
 gate_topk_kernel(const Elt* __restrict__ x, const float* __restrict__ wg, int T, int d, int E,
                  int k, int renorm, float* __restrict__ logits, int* __restrict__ idx_out,
@@ -127,54 +142,67 @@ gate_topk_kernel(const Elt* __restrict__ x, const float* __restrict__ wg, int T,
     constexpr int P = CE >= 2 ? CE / 2 : 1;           // packed chain pairs
     const GateGeom geo = gate_geom(E, sizeof(Elt));
     const int TB = geo.TB;
-    uint8_t* buf0 = gsm;
-    uint8_t* buf1 = gsm + geo.buf_bytes;
     const int tid = threadIdx.x;
-    const int r = tid / geo.tpt;                      // token within block
+    const int q = tid / geo.tpt;                      // token group: rows q*TT .. q*TT+TT-1
     const int grp = tid % geo.tpt;                    // expert group: e0 = grp * CE
     const int e0 = grp * CE;
     const int t0 = blockIdx.x * TB;
     const bool active = tid < geo.threads;
 
-    for (int q = tid; q < 2 * E; q += blockDim.x) sh_hist[q] = 0;
+    for (int i = tid; i < 2 * E; i += blockDim.x) sh_hist[i] = 0;
 
-    float2 acc2[P];
-    float acc1 = 0.f;
+    float2 acc2[TT][P];
+    float acc1[TT];
 #pragma unroll
-    for (int c = 0; c < P; ++c) acc2[c] = make_float2(0.f, 0.f);
+    for (int u = 0; u < TT; ++u) {
+        acc1[u] = 0.f;
+#pragma unroll
+        for (int c = 0; c < P; ++c) acc2[u][c] = make_float2(0.f, 0.f);
+    }
 
     const int ntiles = ceil_div(d, kGateDT);
-    gate_load_tile<Elt, CE>(x, wg, T, d, E, t0, geo, 0, buf0);
-    cp_async_commit();
-    for (int it = 0; it < ntiles; ++it) {
-        uint8_t* cur = (it & 1) ? buf1 : buf0;
-        uint8_t* nxt = (it & 1) ? buf0 : buf1;
-        if (it + 1 < ntiles) gate_load_tile<Elt, CE>(x, wg, T, d, E, t0, geo, (it + 1) * kGateDT, nxt);
+#pragma unroll
+    for (int st = 0; st < kGateStages - 1; ++st) {             // prologue: tiles 0..S-2
+        if (st < ntiles) gate_load_tile<Elt, CE>(x, wg, T, d, E, t0, geo, st * kGateDT, gsm + st * geo.buf_bytes);
         cp_async_commit();
-        cp_async_wait<1>();
+    }
+    for (int it = 0; it < ntiles; ++it) {
+        uint8_t* cur = gsm + (it % kGateStages) * geo.buf_bytes;
+        const int nx = it + kGateStages - 1;                    // refill the slot freed last round
+        if (nx < ntiles) gate_load_tile<Elt, CE>(x, wg, T, d, E, t0, geo, nx * kGateDT, gsm + (nx % kGateStages) * geo.buf_bytes);
+        cp_async_commit();
+        cp_async_wait<kGateStages - 1>();
         __syncthreads();
         const int ilim = min(kGateDT, d - it * kGateDT);        // multiple of 8 (d % 8 == 0)
-        if (active && t0 + r < T) {
-            const uint4* xr = reinterpret_cast<const uint4*>(cur + (size_t)r * geo.row_bytes);
+        if (active) {
+            const uint8_t* xrow = cur + (size_t)(q * TT) * geo.row_bytes;
             const float* wp = reinterpret_cast<const float*>(cur + geo.x_bytes) + (size_t)grp * gate_wg_stride(CE);
 #pragma unroll 2
             for (int iv = 0; iv < ilim / V; ++iv) {
-                float xf[V];
-                unpack16<Elt>(xr[iv], xf);
+                float xf[TT][V];
 #pragma unroll
-                for (int u = 0; u < V; ++u) {               // R1: increasing i, one fused step each
-                    const float* w = wp + (iv * V + u) * CE;
+                for (int u = 0; u < TT; ++u)
+                    unpack16<Elt>(reinterpret_cast<const uint4*>(xrow + (size_t)u * geo.row_bytes)[iv], xf[u]);
+                const float* w = wp + iv * V * CE;
+#pragma unroll
+                for (int s = 0; s < V; ++s) {                   // R1: increasing i, one fused step each
                     if constexpr (CE >= 4) {
 #pragma unroll
                         for (int h = 0; h < CE / 4; ++h) {
-                            const float4 w4 = *reinterpret_cast<const float4*>(w + 4 * h);
-                            ffma2(acc2[2 * h], xf[u], make_float2(w4.x, w4.y));
-                            ffma2(acc2[2 * h + 1], xf[u], make_float2(w4.z, w4.w));
+                            const float4 w4 = *reinterpret_cast<const float4*>(w + s * CE + 4 * h);
+#pragma unroll
+                            for (int u = 0; u < TT; ++u) {
+                                ffma2(acc2[u][2 * h], xf[u][s], make_float2(w4.x, w4.y));
+                                ffma2(acc2[u][2 * h + 1], xf[u][s], make_float2(w4.z, w4.w));
+                            }
                         }
                     } else if constexpr (CE == 2) {
-                        ffma2(acc2[0], xf[u], *reinterpret_cast<const float2*>(w));
+                        const float2 w2 = *reinterpret_cast<const float2*>(w + s * 2);
+#pragma unroll
+                        for (int u = 0; u < TT; ++u) ffma2(acc2[u][0], xf[u][s], w2);
                     } else {
-                        acc1 = __fmaf_rn(xf[u], w[0], acc1);
+#pragma unroll
+                        for (int u = 0; u < TT; ++u) acc1[u] = __fmaf_rn(xf[u][s], w[s], acc1[u]);
                     }
                 }
             }
@@ -185,32 +213,37 @@ gate_topk_kernel(const Elt* __restrict__ x, const float* __restrict__ wg, int T,
 
     float* lg = reinterpret_cast<float*>(gsm);        // [TB][E]; x buffers are free now
     if (active) {
-        float acc[CE];
-        if constexpr (CE >= 2) {
 #pragma unroll
-            for (int c = 0; c < P; ++c) { acc[2 * c] = acc2[c].x; acc[2 * c + 1] = acc2[c].y; }
-        } else {
-            acc[0] = acc1;
-        }
+        for (int u = 0; u < TT; ++u) {
+            const int r = q * TT + u;
+            float acc[CE];
+            if constexpr (CE >= 2) {
 #pragma unroll
-        for (int c = 0; c < CE; ++c) lg[r * E + e0 + c] = acc[c];
-        if (t0 + r < T) {
-            float* dst = logits + (size_t)(t0 + r) * E + e0;
-            if constexpr (CE % 4 == 0) {
-#pragma unroll
-                for (int c = 0; c < CE; c += 4) *reinterpret_cast<float4*>(dst + c) = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
+                for (int c = 0; c < P; ++c) { acc[2 * c] = acc2[u][c].x; acc[2 * c + 1] = acc2[u][c].y; }
             } else {
+                acc[0] = acc1[u];
+            }
 #pragma unroll
-                for (int c = 0; c < CE; ++c) dst[c] = acc[c];
+            for (int c = 0; c < CE; ++c) lg[r * E + e0 + c] = acc[c];
+            if (t0 + r < T) {
+                float* dst = logits + (size_t)(t0 + r) * E + e0;
+                if constexpr (CE % 4 == 0) {
+#pragma unroll
+                    for (int c = 0; c < CE; c += 4) *reinterpret_cast<float4*>(dst + c) = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
+                } else {
+#pragma unroll
+                    for (int c = 0; c < CE; ++c) dst[c] = acc[c];
+                }
             }
         }
     }
     __syncthreads();
 
     const int tile0 = t0 / kScanTile;
-    if (tid < TB && t0 + tid < T) {
-        const int t = t0 + tid;
-        const float* l = lg + tid * E;
+    for (int rr = tid; rr < TB; rr += blockDim.x) {
+        const int t = t0 + rr;
+        if (t >= T) break;
+        const float* l = lg + rr * E;
         int sel[kMaxK];
 #pragma unroll
         for (int j = 0; j < kMaxK; ++j) {
@@ -351,7 +384,7 @@ int launch_routing(const RouteArgs& a, bool is_bf16, cudaStream_t s)
     cudaMemsetAsync(a.hist, 0, sizeof(int) * n_tiles * a.E, s);
     static bool attr_set = false;
     if (!attr_set) {
-#define SET(Elt, CE) cudaFuncSetAttribute(gate_topk_kernel<Elt, CE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)
+#define SET(Elt, CE) cudaFuncSetAttribute(gate_topk_kernel<Elt, CE, (CE >= 4 ? 2 : 1)>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)
         SET(bf16, 8); SET(bf16, 4); SET(bf16, 2); SET(bf16, 1);
         SET(float, 8); SET(float, 4); SET(float, 2); SET(float, 1);
 #undef SET
@@ -364,10 +397,10 @@ int launch_routing(const RouteArgs& a, bool is_bf16, cudaStream_t s)
 #define GATE_ARGS a.T, a.d, a.E, a.k, a.renorm, a.logits, a.idx, a.w, a.hist, n_tiles
 #define GATE_LAUNCH(Elt)                                                                                    \
     switch (g.ce) {                                                                                         \
-    case 8: gate_topk_kernel<Elt, 8><<<blocks, thr, g.smem, s>>>((const Elt*)a.x, a.wg, GATE_ARGS); break;  \
-    case 4: gate_topk_kernel<Elt, 4><<<blocks, thr, g.smem, s>>>((const Elt*)a.x, a.wg, GATE_ARGS); break;  \
-    case 2: gate_topk_kernel<Elt, 2><<<blocks, thr, g.smem, s>>>((const Elt*)a.x, a.wg, GATE_ARGS); break;  \
-    default: gate_topk_kernel<Elt, 1><<<blocks, thr, g.smem, s>>>((const Elt*)a.x, a.wg, GATE_ARGS); break; \
+    case 8: gate_topk_kernel<Elt, 8, 2><<<blocks, thr, g.smem, s>>>((const Elt*)a.x, a.wg, GATE_ARGS); break;  \
+    case 4: gate_topk_kernel<Elt, 4, 2><<<blocks, thr, g.smem, s>>>((const Elt*)a.x, a.wg, GATE_ARGS); break;  \
+    case 2: gate_topk_kernel<Elt, 2, 1><<<blocks, thr, g.smem, s>>>((const Elt*)a.x, a.wg, GATE_ARGS); break;  \
+    default: gate_topk_kernel<Elt, 1, 1><<<blocks, thr, g.smem, s>>>((const Elt*)a.x, a.wg, GATE_ARGS); break; \
     }
     if (is_bf16) { GATE_LAUNCH(bf16) } else { GATE_LAUNCH(float) }
 #undef GATE_LAUNCH

@@ -150,7 +150,8 @@ def test_tcgen05_gemm_matches_simt_gemm(T, d, f, E, k, n):
 
 @pytest.mark.parametrize("E,k", [(16, 2), (4, 1), (8, 4)])
 def test_gate_backward_paths(E, k):
-    # E <= 8: fused K6+K7 kernel; E > 8: two-kernel path (transposed Wg + dWg reduction)
+    # d % 256 != 0: the general K6 (Wg^T in shared memory) and K7 (partials over 64-token
+    # tiles) kernels, for E <= 8 and E > 8
     T, d, f = 900, 128, 256
     ins = inputs(T, d, f, E, k, beta=0.5, seed=E * 10 + k)
     g = run_gpu(ins, E, k, 1.0, 3)
@@ -158,3 +159,41 @@ def test_gate_backward_paths(E, k):
     assert_routing_exact(g, o)
     for key in ("y", "dx", "dwg", "dw1", "dw2"):
         assert normwise(g[key], o[key]) <= TOL["bf16"], key
+
+
+@pytest.mark.parametrize("T,d,E,k,dtype", [
+    (1999, 256, 8, 2, "bf16"),      # the GPT-MoE path shape class: E <= 8, d % 256 == 0
+    (1531, 512, 5, 1, "fp32"),      # odd E (padded to 8 in registers), top-1, fp32 storage
+    (2048, 256, 3, 3, "bf16"),      # k = 3 (ring slot sized for KK = 4), E padded to 4
+    (700, 2048, 2, 2, "bf16"),      # widest streamed row: 256 threads x 8 dims
+    (37, 256, 8, 2, "fp32"),        # fewer tokens than blocks
+])
+def test_gate_backward_streaming_paths(T, d, E, k, dtype):
+    # E <= 8, d % 256 == 0, d <= 2048: K6 with Wg^T in registers and K7 partials over
+    # contiguous token ranges, both fed by per-thread cp.async rings
+    f = 256
+    ins = inputs(T, d, f, E, k, beta=0.5, dtype=dtype, seed=T + E)
+    g = run_gpu(ins, E, k, 1.0, 2, dtype=dtype)
+    o = run_oracle(ins, k, 1.0, 2)
+    assert_routing_exact(g, o)
+    for key in ("y", "dx", "dwg", "dw1", "dw2"):
+        err = normwise(g[key], o[key])
+        assert err <= TOL[dtype], (key, err)
+
+
+@pytest.mark.parametrize("T,d,f,E,k", [
+    (3000, 256, 512, 4, 2),         # fc1 / dfc2 / dW2: 2 N tiles of 256 -> one multicast pair
+    (2100, 512, 1024, 2, 2),        # 4 / 2 N tiles; few, large groups
+])
+def test_gemm_multicast_is_bitwise_neutral(T, d, f, E, k):
+    # two CTA pairs sharing an A tile by TMA multicast issue the same MMAs in the same K order
+    # as one pair alone: every output must be bitwise identical
+    from paper_2404_19429_b200 import FLAG_GEMM_MULTICAST
+    ins = inputs(T, d, f, E, k, beta=0.5, seed=T)
+    mc = run_gpu(ins, E, k, 1.25, 2, flags=FLAG_GEMM_MULTICAST)
+    one = run_gpu(ins, E, k, 1.25, 2)
+    for key in ("y", "dx", "dwg", "dw1", "dw2"):
+        assert np.array_equal(mc[key], one[key]), key
+    o = run_oracle(ins, k, 1.25, 2)
+    for key in ("y", "dx", "dwg", "dw1", "dw2"):
+        assert normwise(mc[key], o[key]) <= TOL["bf16"], key
