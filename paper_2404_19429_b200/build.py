@@ -18,9 +18,11 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-BUILD = os.path.join(HERE, "build")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
-LIB = os.path.join(HERE, "liblancet_moe.so")
+# experiment variants (A/B builds): LANCET_BUILD_OUT=<lib path> LANCET_BUILD_DEFS="-DX -DY"
+LIB = os.environ.get("LANCET_BUILD_OUT") or os.path.join(HERE, "liblancet_moe.so")
+BUILD = os.path.join(HERE, "build") if LIB == os.path.join(HERE, "liblancet_moe.so") else LIB + ".objs"
+DEFS = os.environ.get("LANCET_BUILD_DEFS", "").split()
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -57,7 +59,7 @@ def compile_one(src: str, force: bool, verbose: bool) -> str:
     if not force and not _deps_newer(obj, src):
         return obj
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
-           "-I", CSRC, "-I", INCLUDE, "-I", nccl_inc, "--expt-relaxed-constexpr",
+           "-I", CSRC, "-I", INCLUDE, "-I", nccl_inc, "--expt-relaxed-constexpr", *DEFS,
            "-Xptxas", "-v" if verbose else "-O3", "-c", src, "-o", obj + ".tmp"]
     if src.endswith(".cpp"):
         cmd = [c for c in cmd if c not in ("--expt-relaxed-constexpr",)]

@@ -148,26 +148,22 @@ __device__ __forceinline__ void act_fwd_grad_fast(int act, float a, float& h, fl
     }
 }
 
-// Two elements at a time with the packed fp32 pipe (FFMA2 / FMUL2): same formula as
-// act_fwd_grad_fast, half the FP32 issue slots (tcgen05 fc1 epilogue).
-__device__ __forceinline__ void act_fwd_grad_fast2(int act, float2 a, float2& h, float2& g) {
-    if (act == ACT_RELU) {
-        h.x = a.x > 0.f ? a.x : 0.f; h.y = a.y > 0.f ? a.y : 0.f;
-        g.x = a.x > 0.f ? 1.f : 0.f; g.y = a.y > 0.f ? 1.f : 0.f;
-    } else {
-        const float2 c = make_float2(0.7978845608028654f, 0.7978845608028654f);
-        const float2 k1 = make_float2(0.044715f, 0.044715f);
-        const float2 k3 = make_float2(3.f * 0.044715f, 3.f * 0.044715f);
-        const float2 half = make_float2(0.5f, 0.5f), one = make_float2(1.f, 1.f);
-        const float2 a2 = __fmul2_rn(a, a);
-        const float2 u = __fmul2_rn(c, __ffma2_rn(__fmul2_rn(k1, a), a2, a));
-        const float2 th = make_float2(tanh_fast(u.x), tanh_fast(u.y));
-        const float2 hp = __ffma2_rn(half, th, half);                     // 0.5 (1 + th)
-        h = __fmul2_rn(a, hp);
-        const float2 om = __ffma2_rn(make_float2(-th.x, -th.y), th, one);  // 1 - th^2
-        const float2 r = __fmul2_rn(__fmul2_rn(half, c), __fmul2_rn(a, om));
-        g = __ffma2_rn(r, __ffma2_rn(k3, a2, one), hp);
-    }
+// GELU-tanh and its derivative for two elements at a time on the packed fp32 pipe
+// (FFMA2 / FMUL2), 9 paired ops + 2 SFU tanh:
+//   u = a (c + c k1 a^2),  th = tanh(u),  hp = (1 + th) / 2,  h = a hp,
+//   g = hp + a (1 - th^2) c (1 + 3 k1 a^2) / 2
+// (the tcgen05 fc1 epilogue; same formula as act_fwd_grad_fast).
+__device__ __forceinline__ void gelu_fwd_grad_fast2(float2 a, float2& h, float2& g) {
+    constexpr float c = 0.7978845608028654f, k1 = 0.044715f;
+    const float2 a2 = __fmul2_rn(a, a);
+    const float2 t = __ffma2_rn(make_float2(c * k1, c * k1), a2, make_float2(c, c));
+    const float2 u = __fmul2_rn(a, t);
+    const float2 th = make_float2(tanh_fast(u.x), tanh_fast(u.y));
+    const float2 hp = __ffma2_rn(make_float2(0.5f, 0.5f), th, make_float2(0.5f, 0.5f));
+    h = __fmul2_rn(a, hp);
+    const float2 om = __ffma2_rn(make_float2(-th.x, -th.y), th, make_float2(1.f, 1.f));
+    const float2 sd = __ffma2_rn(make_float2(1.5f * c * k1, 1.5f * c * k1), a2, make_float2(0.5f * c, 0.5f * c));
+    g = __ffma2_rn(__fmul2_rn(a, sd), om, hp);
 }
 
 }  // namespace lancet

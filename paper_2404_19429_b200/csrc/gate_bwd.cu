@@ -275,7 +275,7 @@ struct K6Geom {
 };
 
 // K6: dx_t = sum_j dX[prow_tj] + sum_e dlogit_te Wg[:, e]; Wg^T slice of the thread in registers
-template <typename Elt, int KK, int EE>
+template <typename Elt, int KK, int EE, int NTC>
 __global__ void __launch_bounds__(256)
 k6_stream_kernel(const Elt* __restrict__ dxe, const int* __restrict__ prow,
                  const float* __restrict__ dlogit, const float* __restrict__ wgT, int t0, int t1,
@@ -284,7 +284,7 @@ k6_stream_kernel(const Elt* __restrict__ dxe, const int* __restrict__ prow,
     using G = K6Geom<Elt, KK>;
     constexpr int NV = G::NV, U = G::U, S = kStreamStages;
     extern __shared__ __align__(16) uint4 ring[];          // [S][SLOT][NT]
-    const int NT = blockDim.x, tid = threadIdx.x;
+    const int NT = NTC > 0 ? NTC : (int)blockDim.x, tid = threadIdx.x;
     int* srow = reinterpret_cast<int*>(ring + (size_t)S * G::SLOT * NT);   // [tpb][KK]
     float* sdl = reinterpret_cast<float*>(srow + tpb * KK);                 // [tpb][EE]
     const int tb0 = t0 + blockIdx.x * tpb;
@@ -346,9 +346,18 @@ k6_stream_kernel(const Elt* __restrict__ dxe, const int* __restrict__ prow,
             float acc[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+            int rw[KK];
+#pragma unroll
+            for (int j = 0; j < KK; ++j) rw[j] = srow[r * KK + j];
+            float dlv[EE];
+#pragma unroll
+            for (int e = 0; e < EE; e += 2) {
+                const float2 v = *reinterpret_cast<const float2*>(sdl + r * EE + e);
+                dlv[e] = v.x; dlv[e + 1] = v.y;
+            }
 #pragma unroll
             for (int j = 0; j < KK; ++j) {
-                if (srow[r * KK + j] >= 0) {
+                if (rw[j] >= 0) {
                     uint4 raw[NV];
 #pragma unroll
                     for (int v = 0; v < NV; ++v) raw[v] = slot[((u * KK + j) * NV + v) * NT + tid];
@@ -362,8 +371,7 @@ k6_stream_kernel(const Elt* __restrict__ dxe, const int* __restrict__ prow,
                             make_float2(acc[4], acc[5]), make_float2(acc[6], acc[7])};
 #pragma unroll
             for (int e = 0; e < EE; ++e) {
-                const float dl = sdl[r * EE + e];
-                const float2 dl2 = make_float2(dl, dl);
+                const float2 dl2 = make_float2(dlv[e], dlv[e]);
 #pragma unroll
                 for (int p = 0; p < 4; ++p) a2[p] = __ffma2_rn(dl2, wg2[e][p], a2[p]);
             }
@@ -381,14 +389,14 @@ k6_stream_kernel(const Elt* __restrict__ dxe, const int* __restrict__ prow,
 }
 
 // K7 partials: block b sums x_t (x) dlogit_t over its contiguous token range -> partial[b][E][d]
-template <typename Elt, int EE>
+template <typename Elt, int EE, int NTC>
 __global__ void __launch_bounds__(256)
 dwg_stream_kernel(const Elt* __restrict__ x, const float* __restrict__ dlogit, int T, int d, int E,
                   int tpb, float* __restrict__ partial)
 {
     constexpr int NV = Dims8<Elt>::NV, U = 8 / NV, S = kStreamStages;
     extern __shared__ __align__(16) uint4 ring[];          // [S][U*NV][NT]
-    const int NT = blockDim.x, tid = threadIdx.x;
+    const int NT = NTC > 0 ? NTC : (int)blockDim.x, tid = threadIdx.x;
     float* sdl = reinterpret_cast<float*>(ring + (size_t)S * U * NV * NT);   // [tpb][EE]
     const int tb0 = blockIdx.x * tpb;
     const int nt = max(0, min(T, tb0 + tpb) - tb0);
@@ -551,11 +559,16 @@ static void launch_k6_stream(const DispatchArgs& a, const void* dxe, const int* 
     const size_t smem = (size_t)kStreamStages * G::SLOT * NT * 16 + (size_t)tpb * (KK + EE) * 4;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k6_stream_kernel<Elt, KK, EE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k6_stream_kernel<Elt, KK, EE, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k6_stream_kernel<Elt, KK, EE, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr = true;
     }
-    k6_stream_kernel<Elt, KK, EE><<<ceil_div(t1 - t0, tpb), NT, smem, s>>>(
-        (const Elt*)dxe, prow, dlogit, wgT, t0, t1, a.k, a.d, a.E, tpb, (Elt*)dx);
+    if (NT == 128)      // d = 1024: compile-time ring strides
+        k6_stream_kernel<Elt, KK, EE, 128><<<ceil_div(t1 - t0, tpb), NT, smem, s>>>(
+            (const Elt*)dxe, prow, dlogit, wgT, t0, t1, a.k, a.d, a.E, tpb, (Elt*)dx);
+    else
+        k6_stream_kernel<Elt, KK, EE, 0><<<ceil_div(t1 - t0, tpb), NT, smem, s>>>(
+            (const Elt*)dxe, prow, dlogit, wgT, t0, t1, a.k, a.d, a.E, tpb, (Elt*)dx);
 }
 
 int launch_unpermute_gate_bwd(const DispatchArgs& a, const void* dxe, const int* prow,
@@ -614,10 +627,12 @@ static void launch_dwg_stream(const Elt* x, const float* dlogit, int T, int d, i
     const size_t smem = (size_t)kStreamStages * U * NV * NT * 16 + (size_t)tpb * EE * 4;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(dwg_stream_kernel<Elt, EE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(dwg_stream_kernel<Elt, EE, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(dwg_stream_kernel<Elt, EE, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr = true;
     }
-    dwg_stream_kernel<Elt, EE><<<grid, NT, smem, s>>>(x, dlogit, T, d, E, tpb, partial);
+    if (NT == 128) dwg_stream_kernel<Elt, EE, 128><<<grid, NT, smem, s>>>(x, dlogit, T, d, E, tpb, partial);
+    else dwg_stream_kernel<Elt, EE, 0><<<grid, NT, smem, s>>>(x, dlogit, T, d, E, tpb, partial);
     dwg_reduce4_kernel<<<ceil_div(d * E, 32), 256, 0, s>>>(partial, grid, d * E, d, E, dwg);
 }
 

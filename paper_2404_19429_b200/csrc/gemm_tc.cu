@@ -45,8 +45,9 @@ constexpr size_t kSmemLimit = 232448;                     // 227 KiB opt-in per 
 template <int BN, bool A_MN, int CG>
 struct Cfg {
     static constexpr bool kStaged = !A_MN;                // M-grouped: bf16 out via TMA store
+                                                          // (K-grouped: fp32 out, also TMA)
     static constexpr uint32_t B_STAGE = BN * BK * 2 / CG; // this CTA's share of B
-    static constexpr size_t kEpi = kStaged ? (size_t)kEpiWarps * kWarpStage : 0;
+    static constexpr size_t kEpi = (size_t)kEpiWarps * kWarpStage;
     static constexpr size_t kFixed = 1024 + kEpi + kBarBytes + sizeof(int) * (3 * kMaxGroups + 1);
     static constexpr int STAGES_FIT = (int)((kSmemLimit - kFixed) / (A_STAGE + B_STAGE));
     static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
@@ -134,6 +135,12 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
                  "r"(smem_u32(src)), "r"(c0), "r"(c1)
                  : "memory");
 }
+// elementwise fp32 add of the shared box into global memory (dW accumulation across chunks)
+__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+    asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1)
+                 : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
@@ -173,6 +180,28 @@ __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t
             "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
             : "memory");
     }
+}
+// 32 lanes x 32 columns of 32-bit, issued without waiting: the registers are undefined until
+// tmem_wait_ld(v), which names them as in/out operands so no use can move above it
+__device__ __forceinline__ void tmem_ld32_issue(uint32_t addr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(addr));
+}
+__device__ __forceinline__ void tmem_wait_ld(uint32_t (&v)[32]) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),
+                   "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15]),
+                   "+r"(v[16]), "+r"(v[17]), "+r"(v[18]), "+r"(v[19]), "+r"(v[20]), "+r"(v[21]), "+r"(v[22]), "+r"(v[23]),
+                   "+r"(v[24]), "+r"(v[25]), "+r"(v[26]), "+r"(v[27]), "+r"(v[28]), "+r"(v[29]), "+r"(v[30]), "+r"(v[31])
+                 :
+                 : "memory");
 }
 // 32 lanes x 32 columns of 32-bit: thread t of the warp gets row (lane base + t), 32 columns
 __device__ __forceinline__ void tmem_ld32(uint32_t addr, uint32_t (&v)[32]) {
@@ -280,8 +309,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tmA);
         tma_prefetch(&tmB);
+        tma_prefetch(&tmC);
         if (CF::kStaged) {
-            tma_prefetch(&tmC);
             if (p.epi == EPI_ACT) tma_prefetch(&tmC2);
             if (p.epi == EPI_DACT) tma_prefetch(&tmX);
         }
@@ -429,13 +458,15 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 mbar_wait(&tfull[acc], acc_phase);
                 tc_fence_after();
                 if (live) {
-#pragma unroll 1
-                    for (int cc = cc0; cc < cc1; ++cc) {
-                        uint32_t v[32];
-                        tmem_ld32(tmem_base + acc * BN + cc * 32 + ((uint32_t)(q * 32) << 16), v);
+                    // chunk cc of this warp's columns: TMEM -> epilogue math -> staging -> TMA
+                    auto chunk = [&](int cc, uint32_t (&v)[32]) {
+                        if (!has_k) {                                   // uniform: empty reduction
+#pragma unroll
+                            for (int i = 0; i < 32; ++i) v[i] = 0u;
+                        }
                         float f[32];
 #pragma unroll
-                        for (int i = 0; i < 32; ++i) f[i] = has_k ? __uint_as_float(v[i]) : 0.f;
+                        for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
                         if (dact) {
                             mbar_wait(xbar, xphase);
                             xphase ^= 1;
@@ -444,7 +475,12 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                                 float a8[8];
                                 unpack16<bf16>(*reinterpret_cast<const uint4*>(sX + sw64(lane, j)), a8);
 #pragma unroll
-                                for (int i = 0; i < 8; ++i) f[8 * j + i] *= a8[i];
+                                for (int i = 0; i < 8; i += 2) {
+                                    const float2 r = __fmul2_rn(make_float2(f[8 * j + i], f[8 * j + i + 1]),
+                                                                make_float2(a8[i], a8[i + 1]));
+                                    f[8 * j + i] = r.x;
+                                    f[8 * j + i + 1] = r.y;
+                                }
                             }
                             __syncwarp();
                         }
@@ -457,12 +493,24 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                         }
                         if (p.epi == EPI_ACT) {
                             float h[32], gr[32];
+                            if (p.act == ACT_RELU) {                        // uniform branch
 #pragma unroll
-                            for (int i = 0; i < 32; i += 2) {
-                                float2 h2, g2;
-                                act_fwd_grad_fast2(p.act, make_float2(f[i], f[i + 1]), h2, g2);
-                                h[i] = h2.x; h[i + 1] = h2.y;
-                                gr[i] = g2.x; gr[i + 1] = g2.y;
+                                for (int i = 0; i < 32; ++i) {
+                                    h[i] = f[i] > 0.f ? f[i] : 0.f;
+                                    gr[i] = f[i] > 0.f ? 1.f : 0.f;
+                                }
+                            } else {
+#pragma unroll
+                                for (int i = 0; i < 32; i += 2) {
+                                    float2 h2, g2;
+#ifdef LANCET_EXP_NO_MATH
+                                    h2 = make_float2(f[i], f[i + 1]); g2 = h2;
+#else
+                                    gelu_fwd_grad_fast2(make_float2(f[i], f[i + 1]), h2, g2);
+#endif
+                                    h[i] = h2.x; h[i + 1] = h2.y;
+                                    gr[i] = g2.x; gr[i + 1] = g2.y;
+                                }
                             }
 #pragma unroll
                             for (int j = 0; j < 4; ++j) {
@@ -477,35 +525,60 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                         fence_proxy_async();
                         __syncwarp();
                         if (lane == 0) {
+#ifndef LANCET_EXP_NO_STORE
                             tma_store_2d(&tmC, sO0, n0 + cc * 32, row0);
+#ifndef LANCET_EXP_NO_G
                             if (p.epi == EPI_ACT) tma_store_2d(&tmC2, sO1, n0 + cc * 32, row0);
+#endif
+#endif
                             bulk_commit();
                         }
+                    };
+                    // TMEM loads one chunk ahead of the math (cc1 - cc0 is even)
+                    const uint32_t tbase = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16);
+                    uint32_t va[32], vb[32];
+                    tmem_ld32_issue(tbase + cc0 * 32, va);
+                    tmem_wait_ld(va);
+#pragma unroll 1
+                    for (int cc = cc0; cc < cc1; cc += 2) {
+                        tmem_ld32_issue(tbase + (cc + 1) * 32, vb);
+                        chunk(cc, va);
+                        tmem_wait_ld(vb);
+                        if (cc + 2 < cc1) tmem_ld32_issue(tbase + (cc + 2) * 32, va);
+                        chunk(cc + 1, vb);
+                        if (cc + 2 < cc1) tmem_wait_ld(va);
                     }
                 }
             } else {
                 mbar_wait(&tfull[acc], acc_phase);
                 tc_fence_after();
-                const long orow = (long)mt * MT + (int)rank * BM + q * 32 + lane;
+                // fp32 dW tile rows of this warp in the [n_groups * M][N] view of C
+                const int crow = g * p.M + mt * MT + (int)rank * BM + q * 32;
+                uint8_t* sF = sEpi + ew * kWarpStage;            // 32 x 32 fp32 box, SWIZZLE_128B
 #pragma unroll 1
                 for (int cc = cc0; cc < cc1; ++cc) {
                     uint32_t v[32];
                     tmem_ld32(tmem_base + acc * BN + cc * 32 + ((uint32_t)(q * 32) << 16), v);
-                    float f[32];
+                    if (!has_k) {
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) f[i] = has_k ? __uint_as_float(v[i]) : 0.f;
-                    float* C = reinterpret_cast<float*>(p.C) + (long)g * p.c_group_stride + orow * p.ldc + n0 + cc * 32;
-                    if (p.accumulate) {
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) {
-                            float o[4];
-                            unpack16<float>(ld_v4(C + 4 * i), o);
-#pragma unroll
-                            for (int j = 0; j < 4; ++j) f[4 * i + j] += o[j];
-                        }
+                        for (int i = 0; i < 32; ++i) v[i] = 0u;
                     }
+                    // the previous chunk's TMA store must have read the staging box
+                    if (lane == 0) bulk_wait_read0();
+                    __syncwarp();
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) st_v4(C + 4 * i, pack16<float>(f + 4 * i));
+                    for (int j = 0; j < 8; ++j)
+                        *reinterpret_cast<uint4*>(sF + lane * 128 + ((j ^ (lane & 7)) << 4)) =
+                            make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                    fence_proxy_async();
+                    __syncwarp();
+                    if (lane == 0) {
+                        // accumulate: TMA reduce-add (old + new, one rounding: same as a
+                        // read-add-write), else a plain store
+                        if (p.accumulate) tma_reduce_add_2d(&tmC, sF, n0 + cc * 32, crow);
+                        else tma_store_2d(&tmC, sF, n0 + cc * 32, crow);
+                        bulk_commit();
+                    }
                 }
             }
             tc_fence_before();
@@ -515,7 +588,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 else mbar_arrive_cluster(&tempty[acc], lead_rank); // the leader's MMA waits on it
             }
         }
-        if (CF::kStaged && lane == 0) bulk_wait0();
+        if (lane == 0) bulk_wait0();
     }
     tc_fence_before();
     if constexpr (CG * MC > 1) cluster_sync();
@@ -550,15 +623,16 @@ static EncodeFn get_encode()
 
 // 2D bf16 map: inner dimension `inner` (contiguous), `outer` rows of `stride_elems`.
 static bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t stride_elems,
-                     uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B)
+                     uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B,
+                     bool f32 = false)
 {
     EncodeFn enc = get_encode();
     if (!enc) return false;
     cuuint64_t dims[2] = {inner, outer};
-    cuuint64_t strides[1] = {stride_elems * 2};
+    cuuint64_t strides[1] = {stride_elems * (f32 ? 4 : 2)};
     cuuint32_t box[2] = {box_inner, box_outer};
     cuuint32_t es[2] = {1, 1};
-    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+    CUresult r = enc(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
@@ -583,6 +657,8 @@ static int launch_cfg(const GemmArgs& a, int num_sms, cudaStream_t s)
         ok = ok && make_map(&tcm, a.C, a.N, a.c_rows, a.ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
         if (a.epi == EPI_ACT) ok = ok && make_map(&tc2, a.C2, a.N, a.c_rows, a.ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
         if (a.epi == EPI_DACT) ok = ok && make_map(&tx, a.aux, a.N, a.c_rows, a.ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+    } else {   // fp32 C [n_groups][M][N] viewed as [n_groups * M][N]
+        ok = ok && make_map(&tcm, a.C, a.N, (uint64_t)a.n_groups * a.M, a.ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B, true);
     }
     if (!ok) return -1;
     Params p{a.mode, a.n_groups, a.gpw, a.n_weights > 0 ? a.n_weights : (1 << 30), a.epi, a.act, a.accumulate,
@@ -663,6 +739,7 @@ bool gemm_tc_supported(const GemmArgs& a)
         if (!a.a_mn || !a.b_mn) return false;
         if (a.M % tc::BM) return false;
         if (a.epi != EPI_F32) return false;
+        if (a.c_group_stride != (long)a.M * a.ldc || a.ldc % 4) return false;   // TMA store view
     }
     return a.a_rows > 0 && a.b_rows > 0;
 }

@@ -1,8 +1,10 @@
 #!/bin/bash
-# A/B: bench the in-tree library and gpurun_out/ab/libA.so alternately in one session
+# A/B: bench ablib/libA.so (variant A) and the in-tree library (B) alternately in one session
+# usage: FL=<flags> bash tools/ab.sh [rounds]
 mkdir -p gpurun_out/ab
-for i in 1 2; do
-  LANCET_LIB=$PWD/ablib/libA.so python bench.py --steps 30 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/ab/A$i.json 2>/dev/null
-  python bench.py --steps 30 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/ab/B$i.json 2>/dev/null
+FL=${FL:-0}
+R=${1:-3}
+for i in $(seq 1 $R); do
+  LANCET_LIB=$PWD/ablib/libA.so timeout 300 python bench.py --steps 40 --warmup 5 --no-cpu-baseline --no-e2e --flags $FL > gpurun_out/ab/A$i.json 2>/dev/null
+  timeout 300 python bench.py --steps 40 --warmup 5 --no-cpu-baseline --no-e2e --flags $FL > gpurun_out/ab/B$i.json 2>/dev/null
 done
-for f in A1 B1 A2 B2; do echo $f; python profiles/show_bench.py gpurun_out/ab/$f.json | head -8; done
