@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--flags", type=int, default=0, help="extra LANCET_FLAG_* bits")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-timeline", action="store_true",
+                    help="no per-op events in the timed region (A/B of their overhead)")
     a = ap.parse_args()
     a.warmup = max(a.warmup, 3)
     return a
@@ -307,7 +309,7 @@ def run_lancet(a, world, rank, local_rank):
     w1 = torch.from_numpy(ins["w1"]).to(dev, bf)
     w2 = torch.from_numpy(ins["w2"]).to(dev, bf)
     dy = torch.from_numpy(ins["dy"]).to(dev, bf)
-    flags = lancet.FLAG_TIMELINE | a.flags
+    flags = (0 if a.no_timeline else lancet.FLAG_TIMELINE) | a.flags
     cfg = lancet.LayerConfig(d_model=a.d, d_ffn=a.f, n_experts=a.experts, max_tokens=a.tokens,
                              max_k=a.k, max_chunks=max(8, a.chunks), dtype="bf16", flags=flags)
     ctx = lancet.Context(cfg, world=world, rank=rank, device=local_rank,

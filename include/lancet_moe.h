@@ -70,6 +70,9 @@ typedef enum {
     LANCET_ACT_IDENTITY_EXPERT = 2
 } lancet_act;
 
+/* SMs (= NCCL CTAs) reserved for the all-to-all at world > 1 (see gemm_sms). */
+#define LANCET_COMM_SMS 8
+
 /* Behaviour flags (lancet_layer_config.flags, or lancet_set_flags). */
 enum {
     LANCET_FLAG_RENORMALIZE = 1u << 0,  /* w = p[idx] / sum_j p[idx_j] (R3); default off     */
@@ -96,7 +99,11 @@ typedef struct {
     int32_t dtype;        /* lancet_dtype                                              */
     int32_t act;          /* lancet_act                                                */
     uint32_t flags;       /* LANCET_FLAG_*                                             */
-    int32_t gemm_sms;     /* SMs the persistent GEMMs may use (0 = all)                */
+    int32_t gemm_sms;     /* SMs the persistent GEMMs may use.  0 = all SMs at world 1;
+                             at world > 1 (NCCL) all but LANCET_COMM_SMS, which the NCCL
+                             communicator is created to use (ncclConfig_t.maxCTAs), so the
+                             all-to-all kernels always find free SMs beside the
+                             persistent GEMMs and overlap them instead of queueing      */
 } lancet_layer_config;
 
 /* Per-op record of the last forward/backward (LANCET_FLAG_TIMELINE).  Times are

@@ -65,14 +65,17 @@ int nccl_unique_id(void* out, std::string& err)
     return 0;
 }
 
-Transport* make_nccl_transport(int world, int rank, const void* id, std::string& err)
+Transport* make_nccl_transport(int world, int rank, const void* id, int max_ctas, std::string& err)
 {
     auto* t = new NcclTransport();
     t->world = world;
     t->rank = rank;
     ncclUniqueId uid;
     memcpy(&uid, id, sizeof(uid));
-    ncclResult_t r = ncclCommInitRank(&t->comm, world, uid, rank);
+    ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+    cfg.blocking = 1;
+    if (max_ctas > 0) cfg.maxCTAs = max_ctas;
+    ncclResult_t r = ncclCommInitRankConfig(&t->comm, world, uid, rank, &cfg);
     if (r != ncclSuccess) {
         err = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
         t->comm = nullptr;

@@ -33,7 +33,8 @@ struct Transport {
 };
 
 // NCCL (one process per GPU).  `id` is the 128-byte ncclUniqueId.
-Transport* make_nccl_transport(int world, int rank, const void* id, std::string& err);
+// max_ctas > 0: the communicator's kernels use at most that many CTAs (ncclConfig_t.maxCTAs)
+Transport* make_nccl_transport(int world, int rank, const void* id, int max_ctas, std::string& err);
 int nccl_unique_id(void* out, std::string& err);
 
 // In-process simulated ranks on one device.

@@ -242,6 +242,7 @@ __global__ void transpose_f32_kernel(const float* __restrict__ in, int rows, int
 // bounded by shared memory rather than registers, which is what these HBM-latency-bound
 // kernels need.  The packed rows / dlogit of the block's tokens are staged once up front.
 constexpr int kStreamStages = 4;
+constexpr int kDwgStages = 6;    // K7: 2 blocks per SM, ~5 x 16 KB of x in flight each
 
 template <typename Elt> struct Dims8 {                  // 8 elements = NV 16-byte vectors
     static constexpr int NV = 8 * (int)sizeof(Elt) / 16;
@@ -394,7 +395,7 @@ __global__ void __launch_bounds__(256)
 dwg_stream_kernel(const Elt* __restrict__ x, const float* __restrict__ dlogit, int T, int d, int E,
                   int tpb, float* __restrict__ partial)
 {
-    constexpr int NV = Dims8<Elt>::NV, U = 8 / NV, S = kStreamStages;
+    constexpr int NV = Dims8<Elt>::NV, U = 8 / NV, S = kDwgStages;
     extern __shared__ __align__(16) uint4 ring[];          // [S][U*NV][NT]
     const int NT = NTC > 0 ? NTC : (int)blockDim.x, tid = threadIdx.x;
     float* sdl = reinterpret_cast<float*>(ring + (size_t)S * U * NV * NT);   // [tpb][EE]
@@ -485,7 +486,7 @@ dwg_reduce4_kernel(const float* __restrict__ partial, int nb, int n_out, int d_m
     const int o = blockIdx.x * 32 + q4 * 4;                 // n_out % 4 == 0
     float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
     if (o < n_out) {
-#pragma unroll 8
+#pragma unroll 16
         for (int b = st; b < nb; b += 32) {
             const float4 v = __ldg(reinterpret_cast<const float4*>(partial + (size_t)b * n_out + o));
             s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
@@ -620,11 +621,11 @@ static void launch_dwg_stream(const Elt* x, const float* dlogit, int T, int d, i
 {
     constexpr int NV = Dims8<Elt>::NV, U = 8 / NV;
     const int NT = d / 8;
-    const int per_sm = std::max(1, 384 / NT);
+    const int per_sm = std::max(1, 256 / NT);       // fewer, fatter blocks: fewer partials
     const int nb = std::max(1, std::min({ceil_div(T, 2 * U), per_sm * num_sms, kDwgStreamMaxBlocks}));
     const int tpb = ceil_div(T, nb);
     const int grid = ceil_div(T, tpb);
-    const size_t smem = (size_t)kStreamStages * U * NV * NT * 16 + (size_t)tpb * EE * 4;
+    const size_t smem = (size_t)kDwgStages * U * NV * NT * 16 + (size_t)tpb * EE * 4;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(dwg_stream_kernel<Elt, EE, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);

@@ -143,7 +143,9 @@ lancet_status run_gemm(lancet_ctx* c, GemmArgs& a, cudaStream_t s, int* launches
     const bool use_tc = c->bf16 && !(c->cfg.flags & LANCET_FLAG_SIMT_GEMM) && gemm_tc_supported(a);
     if (use_tc) {
         a.multicast = (c->cfg.flags & LANCET_FLAG_GEMM_MULTICAST) != 0;
-        const int sms = c->cfg.gemm_sms > 0 ? std::min(c->cfg.gemm_sms, c->num_sms) : c->num_sms;
+        // at world > 1 (NCCL) leave LANCET_COMM_SMS SMs to the all-to-all kernels
+        const int all = (c->comm && c->comm->is_nccl()) ? c->num_sms - LANCET_COMM_SMS : c->num_sms;
+        const int sms = c->cfg.gemm_sms > 0 ? std::min(c->cfg.gemm_sms, c->num_sms) : all;
         *launches += launch_gemm_tc(a, sms, s);
     } else {
         *launches += launch_gemm_simt(a, c->bf16, s);
@@ -490,7 +492,7 @@ LANCET_API lancet_status lancet_create(lancet_ctx** out, int32_t world, int32_t 
     st = create_common(c, world, rank, cuda_device, cfg);
     if (!st && world > 1) {
         std::string err;
-        c->comm = make_nccl_transport(world, rank, nccl_id, err);
+        c->comm = make_nccl_transport(world, rank, nccl_id, LANCET_COMM_SMS, err);
         if (!c->comm) st = fail(c, LANCET_ERR_NCCL, err);
         else if (c->comm->check_same(cfg_hash(*cfg), c->s_comm, err)) st = fail(c, LANCET_ERR_ARG, err);
     }

@@ -40,7 +40,11 @@ struct GateGeom {
 
 __host__ __device__ inline int gate_ce(int E)
 {
+#ifdef LANCET_EXP_GATE_CE8
+    return (E % 8 == 0) ? 8 : (E % 4 == 0) ? 4 : (E % 2 == 0) ? 2 : 1;
+#else
     return (E % 8 == 0 && E >= 16) ? 8 : (E % 4 == 0) ? 4 : (E % 2 == 0) ? 2 : 1;
+#endif
 }
 
 // floats per expert group of the staged Wg tile (+4: groups start in different banks)
@@ -125,6 +129,47 @@ __device__ __forceinline__ void gate_load_tile(const Elt* __restrict__ x, const 
         for (int q = threadIdx.x; q < ilim * E; q += blockDim.x) {
             const int i = q / E, e = q % E;
             wb[(size_t)(e / CE) * gate_wg_stride(CE) + i * CE + (e % CE)] = __ldg(wsrc + q);
+        }
+    }
+}
+
+// Top-k selection (R2: logit desc, expert asc) and combine weights (R3) of token t from its
+// E fp32 logits l; counts the choices into the block's per-scan-tile histogram row.
+__device__ __forceinline__ void gate_select_token(const float* l, int t, int E, int k, int renorm,
+                                                  int* __restrict__ idx_out, float* __restrict__ w_out,
+                                                  int* sh_hist_row)
+{
+    int sel[kMaxK];
+#pragma unroll
+    for (int j = 0; j < kMaxK; ++j) {
+        if (j >= k) break;
+        int best = -1;
+        float bv = 0.f;
+        for (int e2 = 0; e2 < E; ++e2) {
+            bool taken = false;
+#pragma unroll
+            for (int jj = 0; jj < kMaxK; ++jj)
+                if (jj < j && sel[jj] == e2) taken = true;
+            if (taken) continue;
+            const float v = l[e2];
+            if (best < 0 || v > bv) { best = e2; bv = v; }   // strict >: ties -> lower e
+        }
+        sel[j] = best;
+    }
+    const float m = l[sel[0]];
+    float s = 0.f;
+    for (int e2 = 0; e2 < E; ++e2) s += expf(l[e2] - m);
+    float ev[kMaxK], ssel = 0.f;
+#pragma unroll
+    for (int j = 0; j < kMaxK; ++j)
+        if (j < k) { ev[j] = expf(l[sel[j]] - m); ssel += ev[j]; }
+    const float denom = renorm ? ssel : s;
+#pragma unroll
+    for (int j = 0; j < kMaxK; ++j) {
+        if (j < k) {
+            idx_out[(size_t)t * k + j] = sel[j];
+            w_out[(size_t)t * k + j] = ev[j] / denom;
+            atomicAdd(&sh_hist_row[sel[j]], 1);
         }
     }
 }
@@ -243,42 +288,122 @@ gate_topk_kernel(const Elt* __restrict__ x, const float* __restrict__ wg, int T,
     for (int rr = tid; rr < TB; rr += blockDim.x) {
         const int t = t0 + rr;
         if (t >= T) break;
-        const float* l = lg + rr * E;
-        int sel[kMaxK];
-#pragma unroll
-        for (int j = 0; j < kMaxK; ++j) {
-            if (j >= k) break;
-            int best = -1;
-            float bv = 0.f;
-            for (int e2 = 0; e2 < E; ++e2) {
-                bool taken = false;
-#pragma unroll
-                for (int jj = 0; jj < kMaxK; ++jj)
-                    if (jj < j && sel[jj] == e2) taken = true;
-                if (taken) continue;
-                const float v = l[e2];
-                if (best < 0 || v > bv) { best = e2; bv = v; }   // strict >: ties -> lower e
-            }
-            sel[j] = best;
-        }
-        const float m = l[sel[0]];
-        float s = 0.f;
-        for (int e2 = 0; e2 < E; ++e2) s += expf(l[e2] - m);
-        float ev[kMaxK], ssel = 0.f;
-#pragma unroll
-        for (int j = 0; j < kMaxK; ++j)
-            if (j < k) { ev[j] = expf(l[sel[j]] - m); ssel += ev[j]; }
-        const float denom = renorm ? ssel : s;
-        const int tile = t / kScanTile - tile0;
-#pragma unroll
-        for (int j = 0; j < kMaxK; ++j) {
-            if (j < k) {
-                idx_out[(size_t)t * k + j] = sel[j];
-                w_out[(size_t)t * k + j] = ev[j] / denom;
-                atomicAdd(&sh_hist[tile * E + sel[j]], 1);
-            }
-        }
+        gate_select_token(lg + rr * E, t, E, k, renorm, idx_out, w_out, sh_hist + (t / kScanTile - tile0) * E);
     }
+    __syncthreads();
+    for (int q = tid; q < 2 * E; q += blockDim.x) {
+        const int tile = tile0 + q / E;
+        if (sh_hist[q] && tile < n_tiles) atomicAdd(&hist[tile * E + (q % E)], sh_hist[q]);
+    }
+}
+
+
+// ---------------------------------------------------------------------------------------
+// K1, warp-streaming variant (E % 4 == 0, d % 64 == 0, Wg resident in shared memory): the
+// whole Wg is staged once per block (regrouped [E/4][d][4]); each warp then streams its own
+// tokens' x rows through a private cp.async ring of 64-dim slices and runs the R1 chains with
+// no block barrier in the loop.  Thread (token lane/tpt, experts 4*(lane%tpt)..+3), two
+// chains per fma.rn.f32x2.  4 warps per block; 2 blocks per SM at d = 1024, E = 8.
+constexpr int kGsWarps = 4, kGsDT = 64, kGsStages = 8;
+
+__host__ __device__ inline int gs_tpw(int E) { return 32 / (E / 4); }           // tokens per warp
+__host__ __device__ inline int gs_row_bytes(int elt) { return kGsDT * elt + 16; }
+__host__ __device__ inline size_t gs_wg_bytes(int d, int E) { return (size_t)(E / 4) * (d * 4 + 4) * 4; }
+__host__ __device__ inline size_t gs_smem(int d, int E, int elt)
+{
+    const size_t ring = (size_t)kGsWarps * kGsStages * gs_tpw(E) * gs_row_bytes(elt);
+    return gs_wg_bytes(d, E) + ring;       // a warp's logits [tpw][E] fit in its ring
+}
+static bool gs_ok(int d, int E, int elt)
+{
+    return E % 4 == 0 && E <= 32 && 32 % (E / 4) == 0 && d % kGsDT == 0 && gs_smem(d, E, elt) <= 110 * 1024;
+}
+
+template <typename Elt>
+__global__ void __launch_bounds__(kGsWarps * 32)
+gate_stream_kernel(const Elt* __restrict__ x, const float* __restrict__ wg, int T, int d, int E,
+                   int k, int renorm, float* __restrict__ logits, int* __restrict__ idx_out,
+                   float* __restrict__ w_out, int* __restrict__ hist, int n_tiles)
+{
+    extern __shared__ __align__(16) uint8_t gsm[];
+    __shared__ int sh_hist[2 * kMaxExperts];
+    constexpr int V = Vec16<Elt>::N;                   // dims per 16-byte chunk
+    constexpr int CPR = kGsDT / V;                     // chunks per row slice
+    constexpr int S = kGsStages;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tpt = E / 4, tpw = 32 / tpt;
+    const int RB = gs_row_bytes(sizeof(Elt));
+    const int gstride = d * 4 + 4;                     // floats per expert group (+4: bank offset)
+    float* swg = reinterpret_cast<float*>(gsm);
+    uint8_t* ring = gsm + gs_wg_bytes(d, E) + (size_t)warp * S * tpw * RB;
+    const int t0 = blockIdx.x * kGsWarps * tpw;
+    const int tw = t0 + warp * tpw;                    // this warp's first token
+
+    for (int i = tid; i < 2 * E; i += blockDim.x) sh_hist[i] = 0;
+    // Wg [d][E] -> swg[(e/4) * gstride + i * 4 + e % 4], 16-byte pieces
+    {
+        const int q4 = E / 4;
+        for (int q = tid; q < d * q4; q += blockDim.x) {
+            const int i = q / q4, e = (q % q4) * 4;
+            cp_async16(swg + (size_t)(e / 4) * gstride + i * 4, wg + (size_t)i * E + e);
+        }
+        cp_async_commit();
+    }
+    const int nst = d / kGsDT;
+    auto issue = [&](int st) {
+        uint8_t* slot = ring + (size_t)(st % S) * tpw * RB;
+        for (int q = lane; q < tpw * CPR; q += 32) {
+            const int rr = q / CPR, c = q % CPR, t = tw + rr;
+            if (t < T)
+                cp_async16(slot + rr * RB + c * 16,
+                           reinterpret_cast<const uint8_t*>(x + (size_t)t * d + st * kGsDT) + c * 16);
+        }
+    };
+#pragma unroll
+    for (int st = 0; st < S - 1; ++st) {
+        if (st < nst) issue(st);
+        cp_async_commit();
+    }
+    cp_async_wait<S - 1>();                            // Wg (the oldest group) has landed
+    __syncthreads();
+
+    const int r = lane / tpt, grp = lane % tpt;
+    const float* wbase = swg + (size_t)grp * gstride;
+    float2 acc0 = make_float2(0.f, 0.f), acc1 = acc0;
+    for (int st = 0; st < nst; ++st) {
+        if (st + S - 1 < nst) issue(st + S - 1);
+        cp_async_commit();
+        cp_async_wait<S - 1>();
+        __syncwarp();                                  // every lane's pieces of slice st landed
+        const uint4* xr = reinterpret_cast<const uint4*>(ring + (size_t)(st % S) * tpw * RB + r * RB);
+        const float* wp = wbase + st * kGsDT * 4;
+#pragma unroll
+        for (int c = 0; c < CPR; ++c) {
+            float xf[V];
+            unpack16<Elt>(xr[c], xf);
+#pragma unroll
+            for (int u = 0; u < V; ++u) {               // R1: increasing i, one fused step each
+                const float4 w4 = *reinterpret_cast<const float4*>(wp + (c * V + u) * 4);
+                ffma2(acc0, xf[u], make_float2(w4.x, w4.y));
+                ffma2(acc1, xf[u], make_float2(w4.z, w4.w));
+            }
+        }
+        __syncwarp();                                  // slice read by all lanes before refill
+    }
+    cp_async_wait<0>();
+    __syncwarp();
+    // logits of the warp's tokens -> shared [tpw][E] in the warp's own (now idle) ring, then
+    // top-k per token
+    float* lg = reinterpret_cast<float*>(ring);
+    const int t = tw + r;
+    *reinterpret_cast<float4*>(lg + r * E + grp * 4) = make_float4(acc0.x, acc0.y, acc1.x, acc1.y);
+    if (t < T)
+        *reinterpret_cast<float4*>(logits + (size_t)t * E + grp * 4) = make_float4(acc0.x, acc0.y, acc1.x, acc1.y);
+    __syncwarp();
+    const int tile0 = t0 / kScanTile;
+    if (lane < tpw && tw + lane < T)
+        gate_select_token(lg + lane * E, tw + lane, E, k, renorm, idx_out, w_out,
+                          sh_hist + ((tw + lane) / kScanTile - tile0) * E);
     __syncthreads();
     for (int q = tid; q < 2 * E; q += blockDim.x) {
         const int tile = tile0 + q / E;
@@ -391,7 +516,24 @@ int launch_routing(const RouteArgs& a, bool is_bf16, cudaStream_t s)
         cudaFuncSetAttribute(slot_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr_set = true;
     }
-    const GateGeom g = gate_geom(a.E, is_bf16 ? 2 : 4);
+    const int elt = is_bf16 ? 2 : 4;
+    if (gs_ok(a.d, a.E, elt)) {
+        static bool gs_attr = false;
+        if (!gs_attr) {
+            cudaFuncSetAttribute(gate_stream_kernel<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            cudaFuncSetAttribute(gate_stream_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            gs_attr = true;
+        }
+        const int per_block = kGsWarps * gs_tpw(a.E);
+        const size_t smem = gs_smem(a.d, a.E, elt);
+        if (is_bf16)
+            gate_stream_kernel<bf16><<<ceil_div(a.T, per_block), kGsWarps * 32, smem, s>>>(
+                (const bf16*)a.x, a.wg, a.T, a.d, a.E, a.k, a.renorm, a.logits, a.idx, a.w, a.hist, n_tiles);
+        else
+            gate_stream_kernel<float><<<ceil_div(a.T, per_block), kGsWarps * 32, smem, s>>>(
+                (const float*)a.x, a.wg, a.T, a.d, a.E, a.k, a.renorm, a.logits, a.idx, a.w, a.hist, n_tiles);
+    } else {
+    const GateGeom g = gate_geom(a.E, elt);
     const int blocks = ceil_div(a.T, g.TB);
     const int thr = round_up(g.threads, 32);
 #define GATE_ARGS a.T, a.d, a.E, a.k, a.renorm, a.logits, a.idx, a.w, a.hist, n_tiles
@@ -405,6 +547,7 @@ int launch_routing(const RouteArgs& a, bool is_bf16, cudaStream_t s)
     if (is_bf16) { GATE_LAUNCH(bf16) } else { GATE_LAUNCH(float) }
 #undef GATE_LAUNCH
 #undef GATE_ARGS
+    }
     const size_t smem2 = sizeof(int) * (a.E + 32 * a.E + 32 * a.E + a.E);
     slot_scan_kernel<<<n_tiles, kScanTile, smem2, s>>>(a.idx, a.T, a.k, a.E, a.C, a.n_chunks,
                                                        a.hist, n_tiles, a.slot, a.S, a.send_rows,

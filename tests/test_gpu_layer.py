@@ -27,6 +27,8 @@ def _lib():
     (777, 64, 3, 1, 0.0, 0.5, 5),          # odd E, top-1, capacity binding hard
     (1, 32, 8, 2, 0.5, 1.25, 1),           # single token
     (513, 32, 1, 1, 0.0, 1.0, 2),          # one expert
+    (1500, 192, 32, 2, 0.5, 1.25, 3),      # warp-streaming gate, 8 threads per token
+    (999, 320, 16, 3, 0.5, 1.0, 2),        # warp-streaming gate, 4 threads per token, ragged
 ])
 def test_routing_bit_exact(T, d, E, k, beta, cf, n):
     ins = inputs(T, d, 8, E, k, beta=beta, seed=T)
@@ -38,6 +40,7 @@ def test_routing_bit_exact(T, d, E, k, beta, cf, n):
 @pytest.mark.parametrize("dtype", ["bf16", "fp32"])
 @pytest.mark.parametrize("act", ["gelu_tanh", "relu"])
 def test_forward_backward_parity(dtype, act):
+    # d % 64 == 0, E = 8: the warp-streaming gate (bf16 and fp32 x); general K6/K7 (d % 256 != 0)
     T, d, f, E, k, cf, n = 1000, 128, 256, 8, 2, 1.0, 3
     ins = inputs(T, d, f, E, k, beta=0.5, dtype=dtype, seed=11)
     g = run_gpu(ins, E, k, cf, n, dtype=dtype, act=act)
