@@ -83,10 +83,12 @@ enum {
     LANCET_FLAG_NO_DW_OVERLAP = 1u << 4,/* backward: dW GEMMs after all a2a (ablation)       */
     LANCET_FLAG_NO_SIDE_STREAM = 1u << 5,/* world 1 backward: K6/K7 on the caller stream, in
                                            line with the GEMMs (A/B of the side stream)      */
-    LANCET_FLAG_GEMM_MULTICAST = 1u << 6/* tcgen05 GEMMs: clusters of two CTA pairs sharing each
+    LANCET_FLAG_GEMM_MULTICAST = 1u << 6,/* tcgen05 GEMMs: clusters of two CTA pairs sharing each
                                            A tile by TMA multicast.  Off by default: clusters
                                            of 4 fit on 132 of the 148 SMs, which costs more
                                            than the L2 traffic it saves (profiles/)          */
+    LANCET_FLAG_UNFUSED_GATE_BWD = 1u << 7 /* world 1 with NO_SIDE_STREAM: K6 and K7 as two
+                                           kernels even where the fused single pass applies  */
 };
 
 typedef struct {

@@ -475,6 +475,165 @@ dwg_stream_kernel(const Elt* __restrict__ x, const float* __restrict__ dlogit, i
     }
 }
 
+
+// K6 + K7 fused (world 1, one pass over all tokens): per token, dx_t from the k packed dX rows
+// and the gate term (Wg^T slice in registers), and dWg partials x_t (x) dlogit_t (dWg slice in
+// registers); dX rows and the x row stream through the per-thread cp.async ring together.
+constexpr int kFusedStages = 6;
+
+template <typename Elt, int KK>
+struct FusedGeom {
+    static constexpr int NV = Dims8<Elt>::NV;
+    static constexpr int U = (8 / ((KK + 1) * NV)) > 0 ? 8 / ((KK + 1) * NV) : 1;   // tokens per slot
+    static constexpr int SLOT = U * (KK + 1) * NV;                                    // 16-byte pieces
+};
+
+template <typename Elt, int KK, int EE, int NTC>
+__global__ void __launch_bounds__(256)
+gate_bwd_fused_kernel(const Elt* __restrict__ dxe, const int* __restrict__ prow,
+                      const float* __restrict__ dlogit, const float* __restrict__ wgT,
+                      const Elt* __restrict__ x, int T, int k, int d, int E, int tpb,
+                      Elt* __restrict__ dx, float* __restrict__ partial)
+{
+    using G = FusedGeom<Elt, KK>;
+    constexpr int NV = G::NV, U = G::U, S = kFusedStages, P = (KK + 1) * NV;   // P: pieces per token
+    extern __shared__ __align__(16) uint4 ring[];          // [S][SLOT][NT]
+    const int NT = NTC > 0 ? NTC : (int)blockDim.x, tid = threadIdx.x;
+    int* srow = reinterpret_cast<int*>(ring + (size_t)S * G::SLOT * NT);   // [tpb][KK]
+    float* sdl = reinterpret_cast<float*>(srow + tpb * KK);                 // [tpb][EE]
+    const int tb0 = blockIdx.x * tpb;
+    const int nt = max(0, min(T, tb0 + tpb) - tb0);
+    for (int q = tid; q < nt * KK; q += NT) {
+        const int r = q / KK, j = q % KK;
+        srow[q] = j < k ? prow[(size_t)(tb0 + r) * k + j] : -1;
+    }
+    for (int q = tid; q < nt * EE; q += NT) {
+        const int r = q / EE, e = q % EE;
+        sdl[q] = e < E ? dlogit[(size_t)(tb0 + r) * E + e] : 0.f;
+    }
+    const int i0 = tid * 8;
+    float2 wg2[EE][4];
+#pragma unroll
+    for (int e = 0; e < EE; ++e) {
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+        if (e < E) {
+            a = __ldg(reinterpret_cast<const float4*>(wgT + (size_t)e * d + i0));
+            b = __ldg(reinterpret_cast<const float4*>(wgT + (size_t)e * d + i0) + 1);
+        }
+        wg2[e][0] = make_float2(a.x, a.y); wg2[e][1] = make_float2(a.z, a.w);
+        wg2[e][2] = make_float2(b.x, b.y); wg2[e][3] = make_float2(b.z, b.w);
+    }
+    float2 acc[8][EE / 2];
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int p = 0; p < EE / 2; ++p) acc[a][p] = make_float2(0.f, 0.f);
+    __syncthreads();
+    const int ng = ceil_div(nt, U);
+    auto issue = [&](int g) {
+        uint4* slot = ring + (size_t)(g % S) * G::SLOT * NT;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int r = g * U + u;
+            if (r < nt) {
+#pragma unroll
+                for (int j = 0; j < KK; ++j) {
+                    const int row = srow[r * KK + j];
+                    if (row >= 0) {
+                        const uint4* src = reinterpret_cast<const uint4*>(dxe + (size_t)row * d + i0);
+#pragma unroll
+                        for (int v = 0; v < NV; ++v) cp_async16_s(slot + ((u * P) + j * NV + v) * NT + tid, src + v);
+                    }
+                }
+                const uint4* xs = reinterpret_cast<const uint4*>(x + (size_t)(tb0 + r) * d + i0);
+#pragma unroll
+                for (int v = 0; v < NV; ++v) cp_async16_s(slot + ((u * P) + KK * NV + v) * NT + tid, xs + v);
+            }
+        }
+    };
+#pragma unroll
+    for (int g = 0; g < S - 1; ++g) {
+        if (g < ng) issue(g);
+        cp_async_commit_s();
+    }
+    for (int g = 0; g < ng; ++g) {
+        if (g + S - 1 < ng) issue(g + S - 1);
+        cp_async_commit_s();
+        cp_async_wait_s<S - 1>();
+        const uint4* slot = ring + (size_t)(g % S) * G::SLOT * NT;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int r = g * U + u;
+            if (r >= nt) break;
+            float dlv[EE];
+#pragma unroll
+            for (int e = 0; e < EE; e += 2) {
+                const float2 v = *reinterpret_cast<const float2*>(sdl + r * EE + e);
+                dlv[e] = v.x; dlv[e + 1] = v.y;
+            }
+            // ---- K6: dx_t = sum_j dX[row_tj] (j order) + sum_e dlogit_te Wg[:, e] ----
+            float s8[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) s8[i] = 0.f;
+#pragma unroll
+            for (int j = 0; j < KK; ++j) {
+                if (srow[r * KK + j] >= 0) {
+                    uint4 raw[NV];
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) raw[v] = slot[((u * P) + j * NV + v) * NT + tid];
+                    float f[8];
+                    unpack8<Elt>(raw, f);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) s8[i] += f[i];
+                }
+            }
+            float2 a2[4] = {make_float2(s8[0], s8[1]), make_float2(s8[2], s8[3]),
+                            make_float2(s8[4], s8[5]), make_float2(s8[6], s8[7])};
+#pragma unroll
+            for (int e = 0; e < EE; ++e) {
+                const float2 dl2 = make_float2(dlv[e], dlv[e]);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) a2[q] = __ffma2_rn(dl2, wg2[e][q], a2[q]);
+            }
+            const float o[8] = {a2[0].x, a2[0].y, a2[1].x, a2[1].y, a2[2].x, a2[2].y, a2[3].x, a2[3].y};
+            Elt* dst = dx + (size_t)(tb0 + r) * d + i0;
+            if constexpr (sizeof(Elt) == 2) {
+                st_v4(dst, pack16<bf16>(o));
+            } else {
+                st_v4(dst, pack16<float>(o));
+                st_v4(dst + 4, pack16<float>(o + 4));
+            }
+            // ---- K7: dWg[i][e] += x_ti dlogit_te ----
+            uint4 xraw[NV];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) xraw[v] = slot[((u * P) + KK * NV + v) * NT + tid];
+            float xf[8];
+            unpack8<Elt>(xraw, xf);
+#pragma unroll
+            for (int a = 0; a < 8; ++a)
+#pragma unroll
+                for (int q = 0; q < EE / 2; ++q)
+                    acc[a][q] = __ffma2_rn(make_float2(xf[a], xf[a]), make_float2(dlv[2 * q], dlv[2 * q + 1]), acc[a][q]);
+        }
+    }
+    cp_async_wait_s<0>();
+    float* out = partial + (size_t)blockIdx.x * E * d + i0;     // partial[b][e][i]
+#pragma unroll
+    for (int q = 0; q < EE / 2; ++q) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int e = 2 * q + h;
+            if (e < E) {
+                float v[8];
+#pragma unroll
+                for (int a = 0; a < 8; ++a) v[a] = h ? acc[a][q].y : acc[a][q].x;
+                st_v4(out + (size_t)e * d, pack16<float>(v));
+                st_v4(out + (size_t)e * d + 4, pack16<float>(v + 4));
+            }
+        }
+    }
+}
+
 // Deterministic reduction of nb partials: block = 32 outputs (8 threads x float4) x 32 part
 // streams; stream s sums partials s, s+32, ... in order, the 32 stream sums are added in order.
 __global__ void __launch_bounds__(256)
@@ -659,6 +818,57 @@ int launch_dwg(const void* x, const float* dlogit, int T, int d, int E, float* p
     else
         dwg_partial_kernel<float><<<grid, kDwgThreads, 0, s>>>((const float*)x, dlogit, T, d, E, partial);
     dwg_reduce_kernel<<<ceil_div(d * E, 32), 256, 0, s>>>(partial, nb, d * E, dwg);
+    return 2;
+}
+
+
+template <typename Elt, int KK, int EE>
+static void launch_fused(const DispatchArgs& a, const void* dxe, const int* prow, const float* dlogit,
+                         const float* wgT, const void* x, void* dx, float* partial, float* dwg,
+                         int num_sms, cudaStream_t s)
+{
+    using G = FusedGeom<Elt, KK>;
+    const int NT = a.d / 8;
+    const int per_sm = std::max(1, 256 / NT);
+    const int nb = std::max(1, std::min({ceil_div(a.T, 4 * G::U), per_sm * num_sms, kDwgStreamMaxBlocks}));
+    const int tpb = ceil_div(a.T, nb);
+    const int grid = ceil_div(a.T, tpb);
+    const size_t smem = (size_t)kFusedStages * G::SLOT * NT * 16 + (size_t)tpb * (KK + EE) * 4;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(gate_bwd_fused_kernel<Elt, KK, EE, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(gate_bwd_fused_kernel<Elt, KK, EE, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+    }
+    if (NT == 128)
+        gate_bwd_fused_kernel<Elt, KK, EE, 128><<<grid, NT, smem, s>>>(
+            (const Elt*)dxe, prow, dlogit, wgT, (const Elt*)x, a.T, a.k, a.d, a.E, tpb, (Elt*)dx, partial);
+    else
+        gate_bwd_fused_kernel<Elt, KK, EE, 0><<<grid, NT, smem, s>>>(
+            (const Elt*)dxe, prow, dlogit, wgT, (const Elt*)x, a.T, a.k, a.d, a.E, tpb, (Elt*)dx, partial);
+    dwg_reduce4_kernel<<<ceil_div(a.d * a.E, 32), 256, 0, s>>>(partial, grid, a.d * a.E, a.d, a.E, dwg);
+}
+
+bool gate_bwd_fused_ok(int d, int E, int k) { return stream_ok(d, E) && k <= 4; }
+
+int launch_gate_bwd_fused(const DispatchArgs& a, const void* dxe, const int* prow, const float* dlogit,
+                          const float* wgT, const void* x, void* dx, float* partial, float* dwg,
+                          int num_sms, bool is_bf16, cudaStream_t s)
+{
+    if (!gate_bwd_fused_ok(a.d, a.E, a.k)) return -1;
+    const int ee = ee_of(a.E);
+#define FUS(Elt, KK)                                                                                                   \
+    do {                                                                                                               \
+        if (ee == 2) launch_fused<Elt, KK, 2>(a, dxe, prow, dlogit, wgT, x, dx, partial, dwg, num_sms, s);            \
+        else if (ee == 4) launch_fused<Elt, KK, 4>(a, dxe, prow, dlogit, wgT, x, dx, partial, dwg, num_sms, s);       \
+        else launch_fused<Elt, KK, 8>(a, dxe, prow, dlogit, wgT, x, dx, partial, dwg, num_sms, s);                    \
+    } while (0)
+    if (is_bf16) {
+        if (a.k == 1) FUS(bf16, 1); else if (a.k == 2) FUS(bf16, 2); else FUS(bf16, 4);
+    } else {
+        if (a.k == 1) FUS(float, 1); else if (a.k == 2) FUS(float, 2); else FUS(float, 4);
+    }
+#undef FUS
     return 2;
 }
 

@@ -47,6 +47,12 @@ int launch_unpermute_gate_bwd(const DispatchArgs& a, const void* dxe, const int*
 int launch_dwg(const void* x, const float* dlogit, int T, int d, int E, float* partial,
                float* dwg, bool is_bf16, int num_sms, cudaStream_t s);
 size_t dwg_partial_floats(int T, int d, int E);
+// K6 + K7 in one pass over all tokens (world 1; E <= 8, d % 256 == 0, d <= 2048, k <= 4):
+// dx and dWg (partials + deterministic reduction).  Returns launches, or -1 if unsupported.
+bool gate_bwd_fused_ok(int d, int E, int k);
+int launch_gate_bwd_fused(const DispatchArgs& a, const void* dxe, const int* prow, const float* dlogit,
+                          const float* wgT, const void* x, void* dx, float* partial, float* dwg,
+                          int num_sms, bool is_bf16, cudaStream_t s);
 // zero rows [off_g + rows_g, off_g + round_up(rows_g, 128)) of a packed buffer
 int launch_zero_pads(void* buf, int row_elems, const int* grp_off, const int* grp_rows,
                      int n_groups, int elt_bytes, cudaStream_t s);

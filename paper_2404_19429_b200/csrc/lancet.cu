@@ -809,15 +809,22 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
         CHECK_LAUNCH();
         const void* dxe = c->dcomb;
         const int max_rows = round_up(c->C, kRowAlign);
-        // K7 (dWg) needs only dlogit from K5, and K6 only dX: both run on a side stream beside
-        // the persistent GEMMs (one small block fits next to each GEMM CTA), so they hide under
-        // the dX / dW GEMMs instead of adding to the critical path
-        cudaStream_t sa = (c->cfg.flags & LANCET_FLAG_NO_SIDE_STREAM) ? s : c->s_comm;
+        // K6 (dx) and K7 (dWg).  Default: on a side stream beside the persistent GEMMs, K7 right
+        // after K5 (under the dX GEMMs) and K6 after the dX GEMMs (under the dW GEMMs) -- measured
+        // fastest.  With LANCET_FLAG_NO_SIDE_STREAM they run in line on the
+        // caller's stream, fused into one pass over the tokens after the dX GEMMs where the shape
+        // allows (LANCET_FLAG_UNFUSED_GATE_BWD keeps two kernels).
+        const bool inline_gate = (c->cfg.flags & LANCET_FLAG_NO_SIDE_STREAM) != 0;
+        cudaStream_t sa = inline_gate ? s : c->s_comm;
         cudaEvent_t ev_k5 = c->ev_pool[0], ev_dx = c->ev_pool[1], ev_side = c->ev_pool[2];
-        CK(cudaEventRecord(ev_k5, s));
-        CK(cudaStreamWaitEvent(sa, ev_k5, 0));
-        st = gate_backward_dwg(c, dwg, sa, &L);
-        if (st) return st;
+        const bool fused = inline_gate && !ident && gate_bwd_fused_ok(d, E, k) &&
+                           !(c->cfg.flags & LANCET_FLAG_UNFUSED_GATE_BWD);
+        if (!fused) {
+            CK(cudaEventRecord(ev_k5, s));
+            CK(cudaStreamWaitEvent(sa, ev_k5, 0));
+            st = gate_backward_dwg(c, dwg, sa, &L);
+            if (st) return st;
+        }
         if (!ident) {
             st = expert_backward_dx(c, c->dcomb, c->send_rows, c->send_off, E, max_rows, s, -1, &L);
             if (st) return st;
@@ -825,8 +832,16 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
         }
         CK(cudaEventRecord(ev_dx, s));
         CK(cudaStreamWaitEvent(sa, ev_dx, 0));
-        st = gate_backward_dx(c, da, dxe, dx, sa, 0, 1, &L);
-        if (st) return st;
+        if (fused) {
+            OpScope op(c, "gate_bwd_fused", sa == c->s_comp || sa == s ? 0 : 2, -1, sa);
+            L += launch_wg_transpose(c->wg, d, E, c->wgT, sa);
+            L += launch_gate_bwd_fused(da, dxe, c->prow, c->dlogit, c->wgT, c->x, dx, c->dwg_partial, dwg,
+                                       c->num_sms, c->bf16, sa);
+            CHECK_LAUNCH();
+        } else {
+            st = gate_backward_dx(c, da, dxe, dx, sa, 0, 1, &L);
+            if (st) return st;
+        }
         CK(cudaEventRecord(ev_side, sa));
         if (!ident) {
             st = expert_backward_dw(c, c->dcomb, c->send_rows, c->send_off, E, dw1, dw2, 0, s, -1, &L);

@@ -304,11 +304,16 @@ gate_topk_kernel(const Elt* __restrict__ x, const float* __restrict__ wg, int T,
 // tokens' x rows through a private cp.async ring of 64-dim slices and runs the R1 chains with
 // no block barrier in the loop.  Thread (token lane/tpt, experts 4*(lane%tpt)..+3), two
 // chains per fma.rn.f32x2.  4 warps per block; 2 blocks per SM at d = 1024, E = 8.
-constexpr int kGsWarps = 4, kGsDT = 64, kGsStages = 8;
+constexpr int kGsDT = 64, kGsStages = 8;
+#ifdef LANCET_EXP_GS_CE2
+constexpr int kGsCE = 2, kGsWarps = 8;  // experts (chains) per thread, warps per block
+#else
+constexpr int kGsCE = 4, kGsWarps = 4;
+#endif
 
-__host__ __device__ inline int gs_tpw(int E) { return 32 / (E / 4); }           // tokens per warp
+__host__ __device__ inline int gs_tpw(int E) { return 32 / (E / kGsCE); }       // tokens per warp
 __host__ __device__ inline int gs_row_bytes(int elt) { return kGsDT * elt + 16; }
-__host__ __device__ inline size_t gs_wg_bytes(int d, int E) { return (size_t)(E / 4) * (d * 4 + 4) * 4; }
+__host__ __device__ inline size_t gs_wg_bytes(int d, int E) { return (size_t)(E / kGsCE) * (d * kGsCE + 4) * 4; }
 __host__ __device__ inline size_t gs_smem(int d, int E, int elt)
 {
     const size_t ring = (size_t)kGsWarps * kGsStages * gs_tpw(E) * gs_row_bytes(elt);
@@ -316,7 +321,7 @@ __host__ __device__ inline size_t gs_smem(int d, int E, int elt)
 }
 static bool gs_ok(int d, int E, int elt)
 {
-    return E % 4 == 0 && E <= 32 && 32 % (E / 4) == 0 && d % kGsDT == 0 && gs_smem(d, E, elt) <= 110 * 1024;
+    return E % 4 == 0 && E / kGsCE <= 32 && 32 % (E / kGsCE) == 0 && d % kGsDT == 0 && gs_smem(d, E, elt) <= 110 * 1024;
 }
 
 template <typename Elt>
@@ -331,21 +336,28 @@ gate_stream_kernel(const Elt* __restrict__ x, const float* __restrict__ wg, int 
     constexpr int CPR = kGsDT / V;                     // chunks per row slice
     constexpr int S = kGsStages;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int tpt = E / 4, tpw = 32 / tpt;
+    constexpr int CE = kGsCE;
+    const int tpt = E / CE, tpw = 32 / tpt;
     const int RB = gs_row_bytes(sizeof(Elt));
-    const int gstride = d * 4 + 4;                     // floats per expert group (+4: bank offset)
+    const int gstride = d * CE + 4;                    // floats per expert group (+4: bank offset)
     float* swg = reinterpret_cast<float*>(gsm);
     uint8_t* ring = gsm + gs_wg_bytes(d, E) + (size_t)warp * S * tpw * RB;
     const int t0 = blockIdx.x * kGsWarps * tpw;
     const int tw = t0 + warp * tpw;                    // this warp's first token
 
     for (int i = tid; i < 2 * E; i += blockDim.x) sh_hist[i] = 0;
-    // Wg [d][E] -> swg[(e/4) * gstride + i * 4 + e % 4], 16-byte pieces
+    // Wg [d][E] -> swg[(e/CE) * gstride + i * CE + e % CE]
     {
         const int q4 = E / 4;
         for (int q = tid; q < d * q4; q += blockDim.x) {
             const int i = q / q4, e = (q % q4) * 4;
-            cp_async16(swg + (size_t)(e / 4) * gstride + i * 4, wg + (size_t)i * E + e);
+            if constexpr (CE == 4) {
+                cp_async16(swg + (size_t)(e / 4) * gstride + i * 4, wg + (size_t)i * E + e);
+            } else {
+                const float4 v = __ldg(reinterpret_cast<const float4*>(wg + (size_t)i * E + e));
+                *reinterpret_cast<float2*>(swg + (size_t)(e / 2) * gstride + i * 2) = make_float2(v.x, v.y);
+                *reinterpret_cast<float2*>(swg + (size_t)(e / 2 + 1) * gstride + i * 2) = make_float2(v.z, v.w);
+            }
         }
         cp_async_commit();
     }
@@ -376,16 +388,20 @@ gate_stream_kernel(const Elt* __restrict__ x, const float* __restrict__ wg, int 
         cp_async_wait<S - 1>();
         __syncwarp();                                  // every lane's pieces of slice st landed
         const uint4* xr = reinterpret_cast<const uint4*>(ring + (size_t)(st % S) * tpw * RB + r * RB);
-        const float* wp = wbase + st * kGsDT * 4;
+        const float* wp = wbase + st * kGsDT * CE;
 #pragma unroll
         for (int c = 0; c < CPR; ++c) {
             float xf[V];
             unpack16<Elt>(xr[c], xf);
 #pragma unroll
             for (int u = 0; u < V; ++u) {               // R1: increasing i, one fused step each
-                const float4 w4 = *reinterpret_cast<const float4*>(wp + (c * V + u) * 4);
-                ffma2(acc0, xf[u], make_float2(w4.x, w4.y));
-                ffma2(acc1, xf[u], make_float2(w4.z, w4.w));
+                if constexpr (CE == 4) {
+                    const float4 w4 = *reinterpret_cast<const float4*>(wp + (c * V + u) * 4);
+                    ffma2(acc0, xf[u], make_float2(w4.x, w4.y));
+                    ffma2(acc1, xf[u], make_float2(w4.z, w4.w));
+                } else {
+                    ffma2(acc0, xf[u], *reinterpret_cast<const float2*>(wp + (c * V + u) * 2));
+                }
             }
         }
         __syncwarp();                                  // slice read by all lanes before refill
@@ -396,9 +412,14 @@ gate_stream_kernel(const Elt* __restrict__ x, const float* __restrict__ wg, int 
     // top-k per token
     float* lg = reinterpret_cast<float*>(ring);
     const int t = tw + r;
-    *reinterpret_cast<float4*>(lg + r * E + grp * 4) = make_float4(acc0.x, acc0.y, acc1.x, acc1.y);
-    if (t < T)
-        *reinterpret_cast<float4*>(logits + (size_t)t * E + grp * 4) = make_float4(acc0.x, acc0.y, acc1.x, acc1.y);
+    if constexpr (CE == 4) {
+        *reinterpret_cast<float4*>(lg + r * E + grp * 4) = make_float4(acc0.x, acc0.y, acc1.x, acc1.y);
+        if (t < T)
+            *reinterpret_cast<float4*>(logits + (size_t)t * E + grp * 4) = make_float4(acc0.x, acc0.y, acc1.x, acc1.y);
+    } else {
+        *reinterpret_cast<float2*>(lg + r * E + grp * 2) = acc0;
+        if (t < T) *reinterpret_cast<float2*>(logits + (size_t)t * E + grp * 2) = acc0;
+    }
     __syncwarp();
     const int tile0 = t0 / kScanTile;
     if (lane < tpw && tw + lane < T)

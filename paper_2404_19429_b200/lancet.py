@@ -25,6 +25,7 @@ ACTS = {"gelu_tanh": 0, "relu": 1, "identity_expert": 2}
 FLAG_RENORMALIZE, FLAG_TIMELINE, FLAG_SERIAL, FLAG_SIMT_GEMM, FLAG_NO_DW_OVERLAP = 1, 2, 4, 8, 16
 FLAG_NO_SIDE_STREAM = 32
 FLAG_GEMM_MULTICAST = 64
+FLAG_UNFUSED_GATE_BWD = 128
 
 EXPORTS = ["lancet_abi_version", "lancet_last_error", "lancet_nccl_unique_id", "lancet_create",
            "lancet_local_group_create", "lancet_local_group_destroy", "lancet_create_local",

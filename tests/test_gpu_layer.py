@@ -200,3 +200,26 @@ def test_gemm_multicast_is_bitwise_neutral(T, d, f, E, k):
     o = run_oracle(ins, k, 1.25, 2)
     for key in ("y", "dx", "dwg", "dw1", "dw2"):
         assert normwise(mc[key], o[key]) <= TOL["bf16"], key
+
+
+@pytest.mark.parametrize("T,d,E,k,dtype", [
+    (3001, 256, 8, 2, "bf16"),
+    (1400, 512, 6, 1, "fp32"),
+    (900, 1024, 4, 4, "bf16"),
+])
+def test_fused_gate_backward_matches_two_kernel_path(T, d, E, k, dtype):
+    # world 1: K6 + K7 in one pass vs the two streaming kernels.  dx is the same arithmetic
+    # (row sum in j order, then the gate term in e order): bitwise.  dWg partials cover other
+    # token ranges: fp32 reassociation only.
+    from paper_2404_19429_b200 import FLAG_UNFUSED_GATE_BWD, FLAG_NO_SIDE_STREAM
+    f = 256
+    ins = inputs(T, d, f, E, k, beta=0.5, dtype=dtype, seed=T + d)
+    fu = run_gpu(ins, E, k, 1.0, 2, dtype=dtype, flags=FLAG_NO_SIDE_STREAM)
+    un = run_gpu(ins, E, k, 1.0, 2, dtype=dtype, flags=FLAG_NO_SIDE_STREAM | FLAG_UNFUSED_GATE_BWD)
+    side = run_gpu(ins, E, k, 1.0, 2, dtype=dtype)
+    assert np.array_equal(side["dx"], un["dx"]) and np.array_equal(side["dwg"], un["dwg"])
+    assert np.array_equal(fu["dx"], un["dx"])
+    assert normwise(fu["dwg"], un["dwg"]) <= 1e-6
+    o = run_oracle(ins, k, 1.0, 2)
+    for key in ("dx", "dwg"):
+        assert normwise(fu[key], o[key]) <= TOL[dtype], key
