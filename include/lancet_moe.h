@@ -87,8 +87,11 @@ enum {
                                            A tile by TMA multicast.  Off by default: clusters
                                            of 4 fit on 132 of the 148 SMs, which costs more
                                            than the L2 traffic it saves (profiles/)          */
-    LANCET_FLAG_UNFUSED_GATE_BWD = 1u << 7 /* world 1 with NO_SIDE_STREAM: K6 and K7 as two
+    LANCET_FLAG_UNFUSED_GATE_BWD = 1u << 7,/* world 1 with NO_SIDE_STREAM: K6 and K7 as two
                                            kernels even where the fused single pass applies  */
+    LANCET_FLAG_PDL = 1u << 8           /* programmatic dependent launch: each kernel may start
+                                           while its predecessor drains (every kernel waits
+                                           with griddepcontrol.wait before touching memory)  */
 };
 
 typedef struct {

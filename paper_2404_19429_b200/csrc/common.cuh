@@ -11,6 +11,12 @@
 
 namespace lancet {
 
+// Programmatic dependent launch: kernels may be launched before their stream predecessor has
+// finished (launch_k with PDL on); every kernel waits here before touching global memory the
+// predecessor writes or reads.  A no-op for normally launched kernels.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+
 using bf16 = __nv_bfloat16;
 
 constexpr int kRowAlign = 128;   // expert / (expert, chunk) row blocks start on 128-row

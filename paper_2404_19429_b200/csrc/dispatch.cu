@@ -52,6 +52,7 @@ permute_kernel(const Elt* __restrict__ x, const int* __restrict__ idx, const int
                int T, int k, int d, const int* __restrict__ send_off,
                const int* __restrict__ send_rows, Elt* __restrict__ xs, int tok_blocks)
 {
+    pdl_wait();   // programmatic dependent launch: predecessor's writes visible
     constexpr int V = Vec16<Elt>::N;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nvec = d / V;
@@ -97,6 +98,7 @@ combine_kernel(const Elt* __restrict__ comb, const int* __restrict__ idx,
                const int* __restrict__ send_off, int t0, int t1, int k, int d,
                Elt* __restrict__ y)
 {
+    pdl_wait();   // programmatic dependent launch: predecessor's writes visible
     constexpr int V = Vec16<Elt>::N;
     constexpr int U = 2;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -145,6 +147,7 @@ combine_bwd_kernel(const Elt* __restrict__ dy, const Elt* __restrict__ comb,
                    const float* __restrict__ logits, int E, int renorm, float* __restrict__ dlogit,
                    int* __restrict__ prow)
 {
+    pdl_wait();   // programmatic dependent launch: predecessor's writes visible
     constexpr int V = Vec16<Elt>::N;
     constexpr int U = 2;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -236,6 +239,7 @@ combine_bwd_kernel(const Elt* __restrict__ dy, const Elt* __restrict__ comb,
 __global__ void zero_pads_kernel(char* __restrict__ buf, int row_bytes,
                                  const int* __restrict__ grp_off, const int* __restrict__ grp_rows)
 {
+    pdl_wait();   // programmatic dependent launch: predecessor's writes visible
     const int g = blockIdx.x;
     const int r0 = grp_off[g] + grp_rows[g];
     const int r1 = grp_off[g] + round_up(grp_rows[g], kRowAlign);
@@ -262,10 +266,10 @@ int launch_permute(const DispatchArgs& a, const void* x, void* xs, bool is_bf16,
     const int grid = tok_blocks + a.E;
     LANCET_DISPATCH_K(a.k, {
         if (is_bf16)
-            permute_kernel<bf16, KK><<<grid, 256, 0, s>>>((const bf16*)x, a.idx, a.slot, a.T, a.k, a.d,
+            launch_k(permute_kernel<bf16, KK>, grid, 256, 0, s, (const bf16*)x, a.idx, a.slot, a.T, a.k, a.d,
                                                          a.send_off, a.send_rows, (bf16*)xs, tok_blocks);
         else
-            permute_kernel<float, KK><<<grid, 256, 0, s>>>((const float*)x, a.idx, a.slot, a.T, a.k, a.d,
+            launch_k(permute_kernel<float, KK>, grid, 256, 0, s, (const float*)x, a.idx, a.slot, a.T, a.k, a.d,
                                                           a.send_off, a.send_rows, (float*)xs, tok_blocks);
     });
     return 1;
@@ -278,10 +282,10 @@ int launch_combine(const DispatchArgs& a, const void* comb, void* y, int t0, int
     const int grid = ceil_div(t1 - t0, kWarpsPerBlock);
     LANCET_DISPATCH_K(a.k, {
         if (is_bf16)
-            combine_kernel<bf16, KK><<<grid, 256, 0, s>>>((const bf16*)comb, a.idx, a.slot, a.w, a.send_off,
+            launch_k(combine_kernel<bf16, KK>, grid, 256, 0, s, (const bf16*)comb, a.idx, a.slot, a.w, a.send_off,
                                                          t0, t1, a.k, a.d, (bf16*)y);
         else
-            combine_kernel<float, KK><<<grid, 256, 0, s>>>((const float*)comb, a.idx, a.slot, a.w,
+            launch_k(combine_kernel<float, KK>, grid, 256, 0, s, (const float*)comb, a.idx, a.slot, a.w,
                                                           a.send_off, t0, t1, a.k, a.d, (float*)y);
     });
     return 1;
@@ -296,12 +300,12 @@ int launch_combine_bwd(const DispatchArgs& a, const void* dy, const void* comb, 
     if (grid == 0) return 0;
     LANCET_DISPATCH_K(a.k, {
         if (is_bf16)
-            combine_bwd_kernel<bf16, KK><<<grid, 256, 0, s>>>((const bf16*)dy, (const bf16*)comb, a.idx,
+            launch_k(combine_bwd_kernel<bf16, KK>, grid, 256, 0, s, (const bf16*)dy, (const bf16*)comb, a.idx,
                                                              a.slot, a.w, a.send_off, a.send_rows, t0, t1,
                                                              a.k, a.d, g, (bf16*)dcomb, tok_blocks, logits, a.E,
                                                              renorm, dlogit, prow);
         else
-            combine_bwd_kernel<float, KK><<<grid, 256, 0, s>>>((const float*)dy, (const float*)comb, a.idx,
+            launch_k(combine_bwd_kernel<float, KK>, grid, 256, 0, s, (const float*)dy, (const float*)comb, a.idx,
                                                               a.slot, a.w, a.send_off, a.send_rows, t0, t1,
                                                               a.k, a.d, g, (float*)dcomb, tok_blocks, logits, a.E,
                                                               renorm, dlogit, prow);
@@ -313,7 +317,7 @@ int launch_zero_pads(void* buf, int row_elems, const int* grp_off, const int* gr
                      int n_groups, int elt_bytes, cudaStream_t s)
 {
     if (n_groups <= 0) return 0;
-    zero_pads_kernel<<<n_groups, 256, 0, s>>>((char*)buf, row_elems * elt_bytes, grp_off, grp_rows);
+    launch_k(zero_pads_kernel, n_groups, 256, 0, s, (char*)buf, row_elems * elt_bytes, grp_off, grp_rows);
     return 1;
 }
 

@@ -33,6 +33,7 @@ k6_gather_kernel(const Elt* __restrict__ dxe, const int* __restrict__ prow,
                  const float* __restrict__ dlogit, const float* __restrict__ wgT, int t0, int t1,
                  int k, int d, int E, Elt* __restrict__ dx)
 {
+    pdl_wait();   // programmatic dependent launch: predecessor's writes visible
     extern __shared__ __align__(16) float swt[];
     constexpr int V = Vec16<Elt>::N;                   // dims per 16-byte vector (8 bf16 / 4 fp32)
     constexpr int H = V / 4;                           // float4 pieces of Wg per vector
@@ -150,6 +151,7 @@ __global__ void __launch_bounds__(kDwgThreads)
 dwg_partial_kernel(const Elt* __restrict__ x, const float* __restrict__ dlogit, int T, int d,
                    int E, float* __restrict__ partial)
 {
+    pdl_wait();   // programmatic dependent launch: predecessor's writes visible
     using Q = Quad<Elt>;
     __shared__ __align__(16) float sdl[kDwgTok][kDwgE];
     const int i0 = (blockIdx.y * kDwgThreads + threadIdx.x) * 4;
@@ -202,6 +204,7 @@ dwg_partial_kernel(const Elt* __restrict__ x, const float* __restrict__ dlogit, 
 __global__ void __launch_bounds__(256)
 dwg_reduce_kernel(const float* __restrict__ partial, int nb, int n_out, float* __restrict__ dwg)
 {
+    pdl_wait();   // programmatic dependent launch: predecessor's writes visible
     __shared__ float red[8][32];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int q = blockIdx.x * 32 + lane;
@@ -227,6 +230,7 @@ dwg_reduce_kernel(const float* __restrict__ partial, int nb, int n_out, float* _
 __global__ void transpose_f32_kernel(const float* __restrict__ in, int rows, int cols,
                                      float* __restrict__ out)
 {
+    pdl_wait();   // programmatic dependent launch: predecessor's writes visible
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= rows * cols) return;
     const int r = q / cols, c = q % cols;
@@ -242,6 +246,7 @@ __global__ void transpose_f32_kernel(const float* __restrict__ in, int rows, int
 // bounded by shared memory rather than registers, which is what these HBM-latency-bound
 // kernels need.  The packed rows / dlogit of the block's tokens are staged once up front.
 constexpr int kStreamStages = 4;
+constexpr int kDwgStreamMaxBlocks = 512;   // partial blocks of the streaming dWg paths
 constexpr int kDwgStages = 6;    // K7: 2 blocks per SM, ~5 x 16 KB of x in flight each
 
 template <typename Elt> struct Dims8 {                  // 8 elements = NV 16-byte vectors
@@ -282,6 +287,7 @@ k6_stream_kernel(const Elt* __restrict__ dxe, const int* __restrict__ prow,
                  const float* __restrict__ dlogit, const float* __restrict__ wgT, int t0, int t1,
                  int k, int d, int E, int tpb, Elt* __restrict__ dx)
 {
+    pdl_wait();   // programmatic dependent launch: predecessor's writes visible
     using G = K6Geom<Elt, KK>;
     constexpr int NV = G::NV, U = G::U, S = kStreamStages;
     extern __shared__ __align__(16) uint4 ring[];          // [S][SLOT][NT]
@@ -395,6 +401,7 @@ __global__ void __launch_bounds__(256)
 dwg_stream_kernel(const Elt* __restrict__ x, const float* __restrict__ dlogit, int T, int d, int E,
                   int tpb, float* __restrict__ partial)
 {
+    pdl_wait();   // programmatic dependent launch: predecessor's writes visible
     constexpr int NV = Dims8<Elt>::NV, U = 8 / NV, S = kDwgStages;
     extern __shared__ __align__(16) uint4 ring[];          // [S][U*NV][NT]
     const int NT = NTC > 0 ? NTC : (int)blockDim.x, tid = threadIdx.x;
@@ -495,6 +502,7 @@ gate_bwd_fused_kernel(const Elt* __restrict__ dxe, const int* __restrict__ prow,
                       const Elt* __restrict__ x, int T, int k, int d, int E, int tpb,
                       Elt* __restrict__ dx, float* __restrict__ partial)
 {
+    pdl_wait();   // programmatic dependent launch: predecessor's writes visible
     using G = FusedGeom<Elt, KK>;
     constexpr int NV = G::NV, U = G::U, S = kFusedStages, P = (KK + 1) * NV;   // P: pieces per token
     extern __shared__ __align__(16) uint4 ring[];          // [S][SLOT][NT]
@@ -640,15 +648,24 @@ __global__ void __launch_bounds__(256)
 dwg_reduce4_kernel(const float* __restrict__ partial, int nb, int n_out, int d_model, int E,
                    float* __restrict__ dwg)
 {
+    pdl_wait();   // programmatic dependent launch: predecessor's writes visible
     __shared__ float4 red[32][8];
     const int q4 = threadIdx.x & 7, st = threadIdx.x >> 3;
     const int o = blockIdx.x * 32 + q4 * 4;                 // n_out % 4 == 0
     float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
     if (o < n_out) {
-#pragma unroll 16
-        for (int b = st; b < nb; b += 32) {
-            const float4 v = __ldg(reinterpret_cast<const float4*>(partial + (size_t)b * n_out + o));
-            s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+        // all of the stream's loads in flight at once (nb <= 32 * kRedMax), summed in b order
+        constexpr int kRedMax = kDwgStreamMaxBlocks / 32;
+        float4 v[kRedMax];
+#pragma unroll
+        for (int u = 0; u < kRedMax; ++u) {
+            const int b = st + 32 * u;
+            v[u] = b < nb ? __ldg(reinterpret_cast<const float4*>(partial + (size_t)b * n_out + o))
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < kRedMax; ++u) {
+            s.x += v[u].x; s.y += v[u].y; s.z += v[u].z; s.w += v[u].w;
         }
     }
     red[st][q4] = s;
@@ -680,7 +697,7 @@ dwg_reduce4_kernel(const float* __restrict__ partial, int nb, int n_out, int d_m
 
 int launch_wg_transpose(const float* wg, int d, int E, float* wgT, cudaStream_t s)
 {
-    transpose_f32_kernel<<<ceil_div(d * E, 256), 256, 0, s>>>(wg, d, E, wgT);
+    launch_k(transpose_f32_kernel, ceil_div(d * E, 256), 256, 0, s, wg, d, E, wgT);
     return 1;
 }
 
@@ -699,7 +716,7 @@ static void launch_k6(const DispatchArgs& a, const void* dxe, const int* prow, c
     }
     const int need = ceil_div(t1 - t0, kWarps * kK6T);
     const int grid = std::max(1, std::min(need, 4 * num_sms));
-    k6_gather_kernel<Elt, KK, SM><<<grid, kWarps * 32, smem, s>>>((const Elt*)dxe, prow, dlogit, wgT, t0, t1,
+    launch_k(k6_gather_kernel<Elt, KK, SM>, grid, kWarps * 32, smem, s, (const Elt*)dxe, prow, dlogit, wgT, t0, t1,
                                                                   a.k, a.d, a.E, (Elt*)dx);
 }
 
@@ -724,10 +741,10 @@ static void launch_k6_stream(const DispatchArgs& a, const void* dxe, const int* 
         attr = true;
     }
     if (NT == 128)      // d = 1024: compile-time ring strides
-        k6_stream_kernel<Elt, KK, EE, 128><<<ceil_div(t1 - t0, tpb), NT, smem, s>>>(
+        launch_k(k6_stream_kernel<Elt, KK, EE, 128>, ceil_div(t1 - t0, tpb), NT, smem, s, 
             (const Elt*)dxe, prow, dlogit, wgT, t0, t1, a.k, a.d, a.E, tpb, (Elt*)dx);
     else
-        k6_stream_kernel<Elt, KK, EE, 0><<<ceil_div(t1 - t0, tpb), NT, smem, s>>>(
+        launch_k(k6_stream_kernel<Elt, KK, EE, 0>, ceil_div(t1 - t0, tpb), NT, smem, s, 
             (const Elt*)dxe, prow, dlogit, wgT, t0, t1, a.k, a.d, a.E, tpb, (Elt*)dx);
 }
 
@@ -765,8 +782,6 @@ int launch_unpermute_gate_bwd(const DispatchArgs& a, const void* dxe, const int*
     return 1;
 }
 
-constexpr int kDwgStreamMaxBlocks = 512;
-
 size_t dwg_partial_floats(int T, int d, int E)
 {
     size_t n = (size_t)ceil_div(T, kDwgTok) * d * E;
@@ -791,9 +806,9 @@ static void launch_dwg_stream(const Elt* x, const float* dlogit, int T, int d, i
         cudaFuncSetAttribute(dwg_stream_kernel<Elt, EE, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr = true;
     }
-    if (NT == 128) dwg_stream_kernel<Elt, EE, 128><<<grid, NT, smem, s>>>(x, dlogit, T, d, E, tpb, partial);
-    else dwg_stream_kernel<Elt, EE, 0><<<grid, NT, smem, s>>>(x, dlogit, T, d, E, tpb, partial);
-    dwg_reduce4_kernel<<<ceil_div(d * E, 32), 256, 0, s>>>(partial, grid, d * E, d, E, dwg);
+    if (NT == 128) launch_k(dwg_stream_kernel<Elt, EE, 128>, grid, NT, smem, s, x, dlogit, T, d, E, tpb, partial);
+    else launch_k(dwg_stream_kernel<Elt, EE, 0>, grid, NT, smem, s, x, dlogit, T, d, E, tpb, partial);
+    launch_k(dwg_reduce4_kernel, ceil_div(d * E, 32), 256, 0, s, partial, grid, d * E, d, E, dwg);
 }
 
 int launch_dwg(const void* x, const float* dlogit, int T, int d, int E, float* partial,
@@ -814,10 +829,10 @@ int launch_dwg(const void* x, const float* dlogit, int T, int d, int E, float* p
     const int nb = ceil_div(T, kDwgTok);
     dim3 grid(nb, ceil_div(d, kDwgThreads * 4), ceil_div(E, kDwgE));
     if (is_bf16)
-        dwg_partial_kernel<bf16><<<grid, kDwgThreads, 0, s>>>((const bf16*)x, dlogit, T, d, E, partial);
+        launch_k(dwg_partial_kernel<bf16>, grid, kDwgThreads, 0, s, (const bf16*)x, dlogit, T, d, E, partial);
     else
-        dwg_partial_kernel<float><<<grid, kDwgThreads, 0, s>>>((const float*)x, dlogit, T, d, E, partial);
-    dwg_reduce_kernel<<<ceil_div(d * E, 32), 256, 0, s>>>(partial, nb, d * E, dwg);
+        launch_k(dwg_partial_kernel<float>, grid, kDwgThreads, 0, s, (const float*)x, dlogit, T, d, E, partial);
+    launch_k(dwg_reduce_kernel, ceil_div(d * E, 32), 256, 0, s, partial, nb, d * E, dwg);
     return 2;
 }
 
@@ -841,12 +856,12 @@ static void launch_fused(const DispatchArgs& a, const void* dxe, const int* prow
         attr = true;
     }
     if (NT == 128)
-        gate_bwd_fused_kernel<Elt, KK, EE, 128><<<grid, NT, smem, s>>>(
+        launch_k(gate_bwd_fused_kernel<Elt, KK, EE, 128>, grid, NT, smem, s, 
             (const Elt*)dxe, prow, dlogit, wgT, (const Elt*)x, a.T, a.k, a.d, a.E, tpb, (Elt*)dx, partial);
     else
-        gate_bwd_fused_kernel<Elt, KK, EE, 0><<<grid, NT, smem, s>>>(
+        launch_k(gate_bwd_fused_kernel<Elt, KK, EE, 0>, grid, NT, smem, s, 
             (const Elt*)dxe, prow, dlogit, wgT, (const Elt*)x, a.T, a.k, a.d, a.E, tpb, (Elt*)dx, partial);
-    dwg_reduce4_kernel<<<ceil_div(a.d * a.E, 32), 256, 0, s>>>(partial, grid, a.d * a.E, a.d, a.E, dwg);
+    launch_k(dwg_reduce4_kernel, ceil_div(a.d * a.E, 32), 256, 0, s, partial, grid, a.d * a.E, a.d, a.E, dwg);
 }
 
 bool gate_bwd_fused_ok(int d, int E, int k) { return stream_ok(d, E) && k <= 4; }

@@ -18,6 +18,7 @@ constexpr int SBM = 64, SBN = 64, SBK = 16;
 template <typename Elt, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(256) simt_gemm_kernel(GemmArgs p)
 {
+    pdl_wait();   // programmatic dependent launch: predecessor's writes visible
     __shared__ float As[SBK][SBM + 4];
     __shared__ float Bs[SBK][SBN + 4];
     const int g = blockIdx.z;
@@ -130,10 +131,10 @@ static void launch_t(const GemmArgs& a, cudaStream_t s)
 {
     const int mrows = a.mode == GEMM_M_GROUPED ? a.max_rows : a.M;
     dim3 grid(ceil_div(a.N, SBN), ceil_div(mrows, SBM), a.n_groups);
-    if (!a.a_mn && !a.b_mn) simt_gemm_kernel<Elt, false, false><<<grid, 256, 0, s>>>(a);
-    else if (!a.a_mn && a.b_mn) simt_gemm_kernel<Elt, false, true><<<grid, 256, 0, s>>>(a);
-    else if (a.a_mn && a.b_mn) simt_gemm_kernel<Elt, true, true><<<grid, 256, 0, s>>>(a);
-    else simt_gemm_kernel<Elt, true, false><<<grid, 256, 0, s>>>(a);
+    if (!a.a_mn && !a.b_mn) launch_k(simt_gemm_kernel<Elt, false, false>, grid, 256, 0, s, a);
+    else if (!a.a_mn && a.b_mn) launch_k(simt_gemm_kernel<Elt, false, true>, grid, 256, 0, s, a);
+    else if (a.a_mn && a.b_mn) launch_k(simt_gemm_kernel<Elt, true, true>, grid, 256, 0, s, a);
+    else launch_k(simt_gemm_kernel<Elt, true, false>, grid, 256, 0, s, a);
 }
 
 int launch_gemm_simt(const GemmArgs& a, bool is_bf16, cudaStream_t s)

@@ -262,6 +262,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2,
                const __grid_constant__ CUtensorMap tmX, Params p)
 {
+    pdl_wait();   // programmatic dependent launch: predecessor's writes visible
     using CF = Cfg<BN, A_MN, CG>;
     constexpr int STAGES = CF::STAGES;
     constexpr uint32_t B_STAGE = CF::B_STAGE;
@@ -700,13 +701,15 @@ static int launch_cfg(const GemmArgs& a, int num_sms, cudaStream_t s)
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute attrs[1];
+    cudaLaunchAttribute attrs[2];
     attrs[0].id = cudaLaunchAttributeClusterDimension;
     attrs[0].val.clusterDim.x = CG * MC;
     attrs[0].val.clusterDim.y = 1;
     attrs[0].val.clusterDim.z = 1;
+    attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attrs[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attrs;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = g_pdl ? 2 : 1;
     if (cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, A_MN, B_MN, CG, MC>, ta, tb, tcm, tc2, tx, p) != cudaSuccess)
         return -1;
     return 1;

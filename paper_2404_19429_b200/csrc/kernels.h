@@ -5,7 +5,30 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#include <utility>
+
 namespace lancet {
+
+// Kernel launch with optional programmatic dependent launch (PDL): with g_pdl set, the kernel
+// may start while its stream predecessor drains; every kernel of the library begins with
+// pdl_wait() (common.cuh), so it observes the predecessor's writes before touching memory.
+extern thread_local bool g_pdl;
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                            Args&&... args)
+{
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = g_pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // ---- K1 / K2: routing (routing.cu) -------------------------------------------------------
 struct RouteArgs {

@@ -451,6 +451,7 @@ lancet_status gate_backward_dwg(lancet_ctx* c, float* dwg, cudaStream_t s, int* 
 
 __global__ void send_counts_kernel(const int* __restrict__ S, int E, int n, int* __restrict__ out)
 {
+    pdl_wait();   // programmatic dependent launch: predecessor's writes visible
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= E * n) return;
     const int e = q / n, c = q % n;
@@ -579,6 +580,8 @@ LANCET_API lancet_status lancet_set_flags(lancet_ctx* c, uint32_t flags)
     return LANCET_OK;
 }
 
+namespace lancet { thread_local bool g_pdl = false; }
+
 LANCET_API lancet_status lancet_moe_forward(lancet_ctx* c, const void* x, const float* wg,
                                             const void* w1, const void* w2, int32_t T, int32_t k,
                                             float cf, int32_t n, void* y, int32_t* expert_idx,
@@ -595,6 +598,7 @@ LANCET_API lancet_status lancet_moe_forward(lancet_ctx* c, const void* x, const 
     if (!(cf > 0.f) || !std::isfinite(cf)) return fail(c, LANCET_ERR_ARG, "capacity_factor must be > 0");
     if (n < 1 || n > std::min<int>(T, c->cfg.max_chunks)) return fail(c, LANCET_ERR_ARG, "n_chunks must be in [1, min(T, max_chunks)]");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream_);
+    lancet::g_pdl = (c->cfg.flags & LANCET_FLAG_PDL) != 0;
     c->have_fwd = false;
     c->x = x; c->wg = wg; c->w1 = w1; c->w2 = w2;
     c->T = T; c->k = k; c->n = n; c->cf = cf;
@@ -643,7 +647,7 @@ LANCET_API lancet_status lancet_moe_forward(lancet_ctx* c, const void* x, const 
         { OpScope op(c, "gate", 0, -1, sc); L += launch_routing(ra, c->bf16, sc); }
         int* d_send = c->counts_dev;                       // [E][n]
         int* d_recv = c->counts_dev + E * n;               // [G][E_l][n]
-        send_counts_kernel<<<ceil_div(E * n, 256), 256, 0, sc>>>(c->S, E, n, d_send);
+        launch_k(send_counts_kernel, ceil_div(E * n, 256), 256, 0, sc, c->S, E, n, d_send);
         ++L;
         CHECK_LAUNCH();
         cudaEvent_t ev_route = next_ev();
@@ -795,6 +799,7 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
     const bool ident = c->cfg.act == LANCET_ACT_IDENTITY_EXPERT;
     if (!dy || !dx || !dwg || (!ident && (!dw1 || !dw2))) return fail(c, LANCET_ERR_ARG, "null required pointer");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream_);
+    lancet::g_pdl = (c->cfg.flags & LANCET_FLAG_PDL) != 0;
     const int E = c->cfg.n_experts, d = c->cfg.d_model, T = c->T, k = c->k, n = c->n;
     const int renorm = (c->cfg.flags & LANCET_FLAG_RENORMALIZE) ? 1 : 0;
     c->launches_bwd = 0;

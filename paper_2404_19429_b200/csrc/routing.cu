@@ -181,6 +181,7 @@ gate_topk_kernel(const Elt* __restrict__ x, const float* __restrict__ wg, int T,
                  int k, int renorm, float* __restrict__ logits, int* __restrict__ idx_out,
                  float* __restrict__ w_out, int* __restrict__ hist, int n_tiles)
 {
+    pdl_wait();   // programmatic dependent launch: predecessor's writes visible
     extern __shared__ __align__(16) uint8_t gsm[];
     __shared__ int sh_hist[2 * kMaxExperts];
     constexpr int V = Vec16<Elt>::N;                  // x values per 16-byte shared load
@@ -330,6 +331,7 @@ gate_stream_kernel(const Elt* __restrict__ x, const float* __restrict__ wg, int 
                    int k, int renorm, float* __restrict__ logits, int* __restrict__ idx_out,
                    float* __restrict__ w_out, int* __restrict__ hist, int n_tiles)
 {
+    pdl_wait();   // programmatic dependent launch: predecessor's writes visible
     extern __shared__ __align__(16) uint8_t gsm[];
     __shared__ int sh_hist[2 * kMaxExperts];
     constexpr int V = Vec16<Elt>::N;                   // dims per 16-byte chunk
@@ -432,12 +434,14 @@ gate_stream_kernel(const Elt* __restrict__ x, const float* __restrict__ wg, int 
     }
 }
 
-// One block per kScanTile tokens.  smem: base[E] | wcnt[32][E] | wbal[32][E] | adm[E]
+// One block per kScanTile tokens.  smem: base[E] | wcnt[32][E] | wbal[32][E] | adm[E] | hist copy
+constexpr int kScanHistMax = 8192;   // ints of the staged tile histograms
 __global__ void __launch_bounds__(kScanTile)
 slot_scan_kernel(const int* __restrict__ idx, int T, int k, int E, int C, int n,
                  const int* __restrict__ hist, int n_tiles, int* __restrict__ slot_out,
                  int* __restrict__ S, int* __restrict__ send_rows, int* __restrict__ send_off)
 {
+    pdl_wait();   // programmatic dependent launch: predecessor's writes visible
     extern __shared__ int ism[];
     int* base = ism;
     int* wcnt = base + E;
@@ -446,13 +450,22 @@ slot_scan_kernel(const int* __restrict__ idx, int T, int k, int E, int C, int n,
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int b = blockIdx.x;
 
+    // the per-tile histograms, all loads in flight at once (a serial prefix of dependent global
+    // loads would cost one L2 round trip per tile)
+    int* sh_h = adm + E;                                   // [n_tiles][E] when it fits
+    const bool staged = n_tiles * E <= kScanHistMax;
+    if (staged) {
+        for (int i = tid; i < n_tiles * E; i += blockDim.x) sh_h[i] = hist[i];
+        __syncthreads();
+    }
+    const int* hs = staged ? sh_h : hist;
     if (tid < E) {
         int s = 0;
-        for (int q = 0; q < b; ++q) s += hist[q * E + tid];
+        for (int q = 0; q < b; ++q) s += hs[q * E + tid];
         base[tid] = s;
         if (b == 0) {
             int tot = 0;
-            for (int q = 0; q < n_tiles; ++q) tot += hist[q * E + tid];
+            for (int q = 0; q < n_tiles; ++q) tot += hs[q * E + tid];
             const int a = min(C, tot);
             adm[tid] = a;
             S[tid * (n + 1)] = 0;
@@ -548,10 +561,10 @@ int launch_routing(const RouteArgs& a, bool is_bf16, cudaStream_t s)
         const int per_block = kGsWarps * gs_tpw(a.E);
         const size_t smem = gs_smem(a.d, a.E, elt);
         if (is_bf16)
-            gate_stream_kernel<bf16><<<ceil_div(a.T, per_block), kGsWarps * 32, smem, s>>>(
+            launch_k(gate_stream_kernel<bf16>, ceil_div(a.T, per_block), kGsWarps * 32, smem, s, 
                 (const bf16*)a.x, a.wg, a.T, a.d, a.E, a.k, a.renorm, a.logits, a.idx, a.w, a.hist, n_tiles);
         else
-            gate_stream_kernel<float><<<ceil_div(a.T, per_block), kGsWarps * 32, smem, s>>>(
+            launch_k(gate_stream_kernel<float>, ceil_div(a.T, per_block), kGsWarps * 32, smem, s, 
                 (const float*)a.x, a.wg, a.T, a.d, a.E, a.k, a.renorm, a.logits, a.idx, a.w, a.hist, n_tiles);
     } else {
     const GateGeom g = gate_geom(a.E, elt);
@@ -560,17 +573,18 @@ int launch_routing(const RouteArgs& a, bool is_bf16, cudaStream_t s)
 #define GATE_ARGS a.T, a.d, a.E, a.k, a.renorm, a.logits, a.idx, a.w, a.hist, n_tiles
 #define GATE_LAUNCH(Elt)                                                                                    \
     switch (g.ce) {                                                                                         \
-    case 8: gate_topk_kernel<Elt, 8, 2><<<blocks, thr, g.smem, s>>>((const Elt*)a.x, a.wg, GATE_ARGS); break;  \
-    case 4: gate_topk_kernel<Elt, 4, 2><<<blocks, thr, g.smem, s>>>((const Elt*)a.x, a.wg, GATE_ARGS); break;  \
-    case 2: gate_topk_kernel<Elt, 2, 1><<<blocks, thr, g.smem, s>>>((const Elt*)a.x, a.wg, GATE_ARGS); break;  \
-    default: gate_topk_kernel<Elt, 1, 1><<<blocks, thr, g.smem, s>>>((const Elt*)a.x, a.wg, GATE_ARGS); break; \
+    case 8: launch_k(gate_topk_kernel<Elt, 8, 2>, blocks, thr, g.smem, s, (const Elt*)a.x, a.wg, GATE_ARGS); break;  \
+    case 4: launch_k(gate_topk_kernel<Elt, 4, 2>, blocks, thr, g.smem, s, (const Elt*)a.x, a.wg, GATE_ARGS); break;  \
+    case 2: launch_k(gate_topk_kernel<Elt, 2, 1>, blocks, thr, g.smem, s, (const Elt*)a.x, a.wg, GATE_ARGS); break;  \
+    default: launch_k(gate_topk_kernel<Elt, 1, 1>, blocks, thr, g.smem, s, (const Elt*)a.x, a.wg, GATE_ARGS); break; \
     }
     if (is_bf16) { GATE_LAUNCH(bf16) } else { GATE_LAUNCH(float) }
 #undef GATE_LAUNCH
 #undef GATE_ARGS
     }
-    const size_t smem2 = sizeof(int) * (a.E + 32 * a.E + 32 * a.E + a.E);
-    slot_scan_kernel<<<n_tiles, kScanTile, smem2, s>>>(a.idx, a.T, a.k, a.E, a.C, a.n_chunks,
+    const size_t smem2 = sizeof(int) * (a.E + 32 * a.E + 32 * a.E + a.E +
+                                        (n_tiles * a.E <= kScanHistMax ? n_tiles * a.E : 0));
+    launch_k(slot_scan_kernel, n_tiles, kScanTile, smem2, s, a.idx, a.T, a.k, a.E, a.C, a.n_chunks,
                                                        a.hist, n_tiles, a.slot, a.S, a.send_rows,
                                                        a.send_off);
     return 2;

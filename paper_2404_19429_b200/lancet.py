@@ -26,6 +26,9 @@ FLAG_RENORMALIZE, FLAG_TIMELINE, FLAG_SERIAL, FLAG_SIMT_GEMM, FLAG_NO_DW_OVERLAP
 FLAG_NO_SIDE_STREAM = 32
 FLAG_GEMM_MULTICAST = 64
 FLAG_UNFUSED_GATE_BWD = 128
+FLAG_PDL = 256
+# LANCET_EXTRA_FLAGS: OR'ed into every context's flags (e.g. run the test suite under PDL)
+EXTRA_FLAGS = int(os.environ.get("LANCET_EXTRA_FLAGS", "0"), 0)
 
 EXPORTS = ["lancet_abi_version", "lancet_last_error", "lancet_nccl_unique_id", "lancet_create",
            "lancet_local_group_create", "lancet_local_group_destroy", "lancet_create_local",
@@ -125,8 +128,8 @@ class LayerConfig:
 
     def _c(self) -> _Config:
         return _Config(self.d_model, self.d_ffn, self.n_experts, self.max_tokens, self.max_k,
-                       self.max_chunks, DTYPES[self.dtype], ACTS[self.act], self.flags,
-                       self.gemm_sms)
+                       self.max_chunks, DTYPES[self.dtype], ACTS[self.act],
+                       self.flags | EXTRA_FLAGS, self.gemm_sms)
 
     @property
     def torch_dtype(self):
@@ -221,6 +224,7 @@ class Context:
             pass
 
     def set_flags(self, flags: int):
+        flags |= EXTRA_FLAGS
         _check(load_library().lancet_set_flags(self._p, flags), self._p)
         self.cfg.flags = flags
 
