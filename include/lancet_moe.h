@@ -89,9 +89,10 @@ enum {
                                            than the L2 traffic it saves (profiles/)          */
     LANCET_FLAG_UNFUSED_GATE_BWD = 1u << 7,/* world 1 with NO_SIDE_STREAM: K6 and K7 as two
                                            kernels even where the fused single pass applies  */
-    LANCET_FLAG_PDL = 1u << 8           /* programmatic dependent launch: each kernel may start
-                                           while its predecessor drains (every kernel waits
-                                           with griddepcontrol.wait before touching memory)  */
+    LANCET_FLAG_NO_PDL = 1u << 8        /* disable programmatic dependent launch (default on:
+                                           each kernel may start while its stream predecessor
+                                           drains; every kernel waits with griddepcontrol.wait
+                                           before touching memory; ~1 % per step)            */
 };
 
 typedef struct {

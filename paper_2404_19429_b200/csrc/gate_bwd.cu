@@ -284,7 +284,7 @@ struct K6Geom {
 template <typename Elt, int KK, int EE, int NTC>
 __global__ void __launch_bounds__(256)
 k6_stream_kernel(const Elt* __restrict__ dxe, const int* __restrict__ prow,
-                 const float* __restrict__ dlogit, const float* __restrict__ wgT, int t0, int t1,
+                 const float* __restrict__ dlogit, const float* __restrict__ wg, int t0, int t1,
                  int k, int d, int E, int tpb, Elt* __restrict__ dx)
 {
     pdl_wait();   // programmatic dependent launch: predecessor's writes visible
@@ -307,17 +307,15 @@ k6_stream_kernel(const Elt* __restrict__ dxe, const int* __restrict__ prow,
         sdl[q] = e < E ? dlogit[(size_t)(tb0 + r) * E + e] : 0.f;
     }
     const int i0 = tid * 8;
+    // this thread's Wg^T slice, read straight from Wg [d][E] (rows i0..i0+7 are contiguous)
     float2 wg2[EE][4];
 #pragma unroll
-    for (int e = 0; e < EE; ++e) {
-        float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
-        if (e < E) {
-            a = __ldg(reinterpret_cast<const float4*>(wgT + (size_t)e * d + i0));
-            b = __ldg(reinterpret_cast<const float4*>(wgT + (size_t)e * d + i0) + 1);
-        }
-        wg2[e][0] = make_float2(a.x, a.y); wg2[e][1] = make_float2(a.z, a.w);
-        wg2[e][2] = make_float2(b.x, b.y); wg2[e][3] = make_float2(b.z, b.w);
-    }
+    for (int e = 0; e < EE; ++e)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            wg2[e][q] = e < E ? make_float2(__ldg(wg + (size_t)(i0 + 2 * q) * E + e),
+                                            __ldg(wg + (size_t)(i0 + 2 * q + 1) * E + e))
+                              : make_float2(0.f, 0.f);
     __syncthreads();
     const int ng = ceil_div(nt, U);
     auto issue = [&](int g) {
@@ -498,7 +496,7 @@ struct FusedGeom {
 template <typename Elt, int KK, int EE, int NTC>
 __global__ void __launch_bounds__(256)
 gate_bwd_fused_kernel(const Elt* __restrict__ dxe, const int* __restrict__ prow,
-                      const float* __restrict__ dlogit, const float* __restrict__ wgT,
+                      const float* __restrict__ dlogit, const float* __restrict__ wg,
                       const Elt* __restrict__ x, int T, int k, int d, int E, int tpb,
                       Elt* __restrict__ dx, float* __restrict__ partial)
 {
@@ -520,17 +518,15 @@ gate_bwd_fused_kernel(const Elt* __restrict__ dxe, const int* __restrict__ prow,
         sdl[q] = e < E ? dlogit[(size_t)(tb0 + r) * E + e] : 0.f;
     }
     const int i0 = tid * 8;
+    // this thread's Wg^T slice, read straight from Wg [d][E] (rows i0..i0+7 are contiguous)
     float2 wg2[EE][4];
 #pragma unroll
-    for (int e = 0; e < EE; ++e) {
-        float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
-        if (e < E) {
-            a = __ldg(reinterpret_cast<const float4*>(wgT + (size_t)e * d + i0));
-            b = __ldg(reinterpret_cast<const float4*>(wgT + (size_t)e * d + i0) + 1);
-        }
-        wg2[e][0] = make_float2(a.x, a.y); wg2[e][1] = make_float2(a.z, a.w);
-        wg2[e][2] = make_float2(b.x, b.y); wg2[e][3] = make_float2(b.z, b.w);
-    }
+    for (int e = 0; e < EE; ++e)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            wg2[e][q] = e < E ? make_float2(__ldg(wg + (size_t)(i0 + 2 * q) * E + e),
+                                            __ldg(wg + (size_t)(i0 + 2 * q + 1) * E + e))
+                              : make_float2(0.f, 0.f);
     float2 acc[8][EE / 2];
 #pragma unroll
     for (int a = 0; a < 8; ++a)
@@ -701,7 +697,7 @@ int launch_wg_transpose(const float* wg, int d, int E, float* wgT, cudaStream_t 
     return 1;
 }
 
-bool gate_bwd_needs_wgT(int, int) { return true; }
+
 
 template <typename Elt, int KK, bool SM>
 static void launch_k6(const DispatchArgs& a, const void* dxe, const int* prow, const float* dlogit,
@@ -721,11 +717,12 @@ static void launch_k6(const DispatchArgs& a, const void* dxe, const int* prow, c
 }
 
 static bool stream_ok(int d, int E) { return E <= 8 && d % 256 == 0 && d <= 2048; }
+bool gate_bwd_needs_wgT(int d, int E) { return !stream_ok(d, E); }
 static int ee_of(int E) { return E <= 2 ? 2 : E <= 4 ? 4 : 8; }
 
 template <typename Elt, int KK, int EE>
 static void launch_k6_stream(const DispatchArgs& a, const void* dxe, const int* prow, const float* dlogit,
-                             const float* wgT, void* dx, int t0, int t1, int num_sms, cudaStream_t s)
+                             const float* wg, void* dx, int t0, int t1, int num_sms, cudaStream_t s)
 {
     using G = K6Geom<Elt, KK>;
     const int NT = a.d / 8;
@@ -742,14 +739,14 @@ static void launch_k6_stream(const DispatchArgs& a, const void* dxe, const int* 
     }
     if (NT == 128)      // d = 1024: compile-time ring strides
         launch_k(k6_stream_kernel<Elt, KK, EE, 128>, ceil_div(t1 - t0, tpb), NT, smem, s, 
-            (const Elt*)dxe, prow, dlogit, wgT, t0, t1, a.k, a.d, a.E, tpb, (Elt*)dx);
+            (const Elt*)dxe, prow, dlogit, wg, t0, t1, a.k, a.d, a.E, tpb, (Elt*)dx);
     else
         launch_k(k6_stream_kernel<Elt, KK, EE, 0>, ceil_div(t1 - t0, tpb), NT, smem, s, 
-            (const Elt*)dxe, prow, dlogit, wgT, t0, t1, a.k, a.d, a.E, tpb, (Elt*)dx);
+            (const Elt*)dxe, prow, dlogit, wg, t0, t1, a.k, a.d, a.E, tpb, (Elt*)dx);
 }
 
 int launch_unpermute_gate_bwd(const DispatchArgs& a, const void* dxe, const int* prow,
-                              const float* dlogit, const float* wgT, void* dx, int t0, int t1,
+                              const float* dlogit, const float* wg, const float* wgT, void* dx, int t0, int t1,
                               int num_sms, bool is_bf16, cudaStream_t s)
 {
     if (t1 <= t0) return 0;
@@ -757,9 +754,9 @@ int launch_unpermute_gate_bwd(const DispatchArgs& a, const void* dxe, const int*
         const int ee = ee_of(a.E);
 #define K6S(Elt, KK)                                                                                              \
     do {                                                                                                          \
-        if (ee == 2) launch_k6_stream<Elt, KK, 2>(a, dxe, prow, dlogit, wgT, dx, t0, t1, num_sms, s);            \
-        else if (ee == 4) launch_k6_stream<Elt, KK, 4>(a, dxe, prow, dlogit, wgT, dx, t0, t1, num_sms, s);       \
-        else launch_k6_stream<Elt, KK, 8>(a, dxe, prow, dlogit, wgT, dx, t0, t1, num_sms, s);                    \
+        if (ee == 2) launch_k6_stream<Elt, KK, 2>(a, dxe, prow, dlogit, wg, dx, t0, t1, num_sms, s);            \
+        else if (ee == 4) launch_k6_stream<Elt, KK, 4>(a, dxe, prow, dlogit, wg, dx, t0, t1, num_sms, s);       \
+        else launch_k6_stream<Elt, KK, 8>(a, dxe, prow, dlogit, wg, dx, t0, t1, num_sms, s);                    \
     } while (0)
         if (is_bf16) {
             if (a.k == 1) K6S(bf16, 1); else if (a.k == 2) K6S(bf16, 2); else K6S(bf16, 4);
@@ -839,7 +836,7 @@ int launch_dwg(const void* x, const float* dlogit, int T, int d, int E, float* p
 
 template <typename Elt, int KK, int EE>
 static void launch_fused(const DispatchArgs& a, const void* dxe, const int* prow, const float* dlogit,
-                         const float* wgT, const void* x, void* dx, float* partial, float* dwg,
+                         const float* wg, const void* x, void* dx, float* partial, float* dwg,
                          int num_sms, cudaStream_t s)
 {
     using G = FusedGeom<Elt, KK>;
@@ -857,26 +854,26 @@ static void launch_fused(const DispatchArgs& a, const void* dxe, const int* prow
     }
     if (NT == 128)
         launch_k(gate_bwd_fused_kernel<Elt, KK, EE, 128>, grid, NT, smem, s, 
-            (const Elt*)dxe, prow, dlogit, wgT, (const Elt*)x, a.T, a.k, a.d, a.E, tpb, (Elt*)dx, partial);
+            (const Elt*)dxe, prow, dlogit, wg, (const Elt*)x, a.T, a.k, a.d, a.E, tpb, (Elt*)dx, partial);
     else
         launch_k(gate_bwd_fused_kernel<Elt, KK, EE, 0>, grid, NT, smem, s, 
-            (const Elt*)dxe, prow, dlogit, wgT, (const Elt*)x, a.T, a.k, a.d, a.E, tpb, (Elt*)dx, partial);
+            (const Elt*)dxe, prow, dlogit, wg, (const Elt*)x, a.T, a.k, a.d, a.E, tpb, (Elt*)dx, partial);
     launch_k(dwg_reduce4_kernel, ceil_div(a.d * a.E, 32), 256, 0, s, partial, grid, a.d * a.E, a.d, a.E, dwg);
 }
 
 bool gate_bwd_fused_ok(int d, int E, int k) { return stream_ok(d, E) && k <= 4; }
 
 int launch_gate_bwd_fused(const DispatchArgs& a, const void* dxe, const int* prow, const float* dlogit,
-                          const float* wgT, const void* x, void* dx, float* partial, float* dwg,
+                          const float* wg, const void* x, void* dx, float* partial, float* dwg,
                           int num_sms, bool is_bf16, cudaStream_t s)
 {
     if (!gate_bwd_fused_ok(a.d, a.E, a.k)) return -1;
     const int ee = ee_of(a.E);
 #define FUS(Elt, KK)                                                                                                   \
     do {                                                                                                               \
-        if (ee == 2) launch_fused<Elt, KK, 2>(a, dxe, prow, dlogit, wgT, x, dx, partial, dwg, num_sms, s);            \
-        else if (ee == 4) launch_fused<Elt, KK, 4>(a, dxe, prow, dlogit, wgT, x, dx, partial, dwg, num_sms, s);       \
-        else launch_fused<Elt, KK, 8>(a, dxe, prow, dlogit, wgT, x, dx, partial, dwg, num_sms, s);                    \
+        if (ee == 2) launch_fused<Elt, KK, 2>(a, dxe, prow, dlogit, wg, x, dx, partial, dwg, num_sms, s);            \
+        else if (ee == 4) launch_fused<Elt, KK, 4>(a, dxe, prow, dlogit, wg, x, dx, partial, dwg, num_sms, s);       \
+        else launch_fused<Elt, KK, 8>(a, dxe, prow, dlogit, wg, x, dx, partial, dwg, num_sms, s);                    \
     } while (0)
     if (is_bf16) {
         if (a.k == 1) FUS(bf16, 1); else if (a.k == 2) FUS(bf16, 2); else FUS(bf16, 4);

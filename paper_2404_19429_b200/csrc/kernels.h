@@ -61,10 +61,11 @@ int launch_combine_bwd(const DispatchArgs& a, const void* dy, const void* comb, 
                        void* dcomb, int t0, int t1, bool zero_pads, const float* logits, int renorm,
                        float* dlogit, int* prow, bool is_bf16, cudaStream_t s);
 int launch_wg_transpose(const float* wg, int d, int E, float* wgT, cudaStream_t s);
-bool gate_bwd_needs_wgT(int d, int E);   // true: K6 reads Wg^T from global (too big for smem)
-// K6: dx_t = sum_j dX[prow_tj] + sum_e dlogit_te Wg[:, e]   (wgT = Wg transposed, [E][d])
+bool gate_bwd_needs_wgT(int d, int E);   // true: the general K6 reads Wg^T (launch_wg_transpose)
+// K6: dx_t = sum_j dX[prow_tj] + sum_e dlogit_te Wg[:, e]   (wg [d][E]; wgT = Wg transposed,
+// [E][d], only read by the general path)
 int launch_unpermute_gate_bwd(const DispatchArgs& a, const void* dxe, const int* prow,
-                              const float* dlogit, const float* wgT, void* dx, int t0, int t1,
+                              const float* dlogit, const float* wg, const float* wgT, void* dx, int t0, int t1,
                               int num_sms, bool is_bf16, cudaStream_t s);
 // dWg = x^T dlogit (K7); partial: [ceil(T/64)][d][E] fp32 scratch
 int launch_dwg(const void* x, const float* dlogit, int T, int d, int E, float* partial,
@@ -74,7 +75,7 @@ size_t dwg_partial_floats(int T, int d, int E);
 // dx and dWg (partials + deterministic reduction).  Returns launches, or -1 if unsupported.
 bool gate_bwd_fused_ok(int d, int E, int k);
 int launch_gate_bwd_fused(const DispatchArgs& a, const void* dxe, const int* prow, const float* dlogit,
-                          const float* wgT, const void* x, void* dx, float* partial, float* dwg,
+                          const float* wg, const void* x, void* dx, float* partial, float* dwg,
                           int num_sms, bool is_bf16, cudaStream_t s);
 // zero rows [off_g + rows_g, off_g + round_up(rows_g, 128)) of a packed buffer
 int launch_zero_pads(void* buf, int row_elems, const int* grp_off, const int* grp_rows,

@@ -434,8 +434,8 @@ lancet_status gate_backward_dx(lancet_ctx* c, const DispatchArgs& da, const void
     const int T = c->T, d = c->cfg.d_model, E = c->cfg.n_experts;
     const int t0 = chunk_start(T, nc, cc), t1 = chunk_start(T, nc, cc + 1);
     OpScope op(c, "unpermute_gate_bwd", s == c->s_comp ? 0 : 2, nc > 1 ? cc : -1, s);
-    if (cc == 0) *L += launch_wg_transpose(c->wg, d, E, c->wgT, s);
-    *L += launch_unpermute_gate_bwd(da, dxe, c->prow, c->dlogit, c->wgT, dx, t0, t1, c->num_sms, c->bf16, s);
+    if (cc == 0 && gate_bwd_needs_wgT(d, E)) *L += launch_wg_transpose(c->wg, d, E, c->wgT, s);
+    *L += launch_unpermute_gate_bwd(da, dxe, c->prow, c->dlogit, c->wg, c->wgT, dx, t0, t1, c->num_sms, c->bf16, s);
     CHECK_LAUNCH();
     return LANCET_OK;
 }
@@ -598,7 +598,7 @@ LANCET_API lancet_status lancet_moe_forward(lancet_ctx* c, const void* x, const 
     if (!(cf > 0.f) || !std::isfinite(cf)) return fail(c, LANCET_ERR_ARG, "capacity_factor must be > 0");
     if (n < 1 || n > std::min<int>(T, c->cfg.max_chunks)) return fail(c, LANCET_ERR_ARG, "n_chunks must be in [1, min(T, max_chunks)]");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream_);
-    lancet::g_pdl = (c->cfg.flags & LANCET_FLAG_PDL) != 0;
+    lancet::g_pdl = (c->cfg.flags & LANCET_FLAG_NO_PDL) == 0;
     c->have_fwd = false;
     c->x = x; c->wg = wg; c->w1 = w1; c->w2 = w2;
     c->T = T; c->k = k; c->n = n; c->cf = cf;
@@ -799,7 +799,7 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
     const bool ident = c->cfg.act == LANCET_ACT_IDENTITY_EXPERT;
     if (!dy || !dx || !dwg || (!ident && (!dw1 || !dw2))) return fail(c, LANCET_ERR_ARG, "null required pointer");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream_);
-    lancet::g_pdl = (c->cfg.flags & LANCET_FLAG_PDL) != 0;
+    lancet::g_pdl = (c->cfg.flags & LANCET_FLAG_NO_PDL) == 0;
     const int E = c->cfg.n_experts, d = c->cfg.d_model, T = c->T, k = c->k, n = c->n;
     const int renorm = (c->cfg.flags & LANCET_FLAG_RENORMALIZE) ? 1 : 0;
     c->launches_bwd = 0;
@@ -839,8 +839,7 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
         CK(cudaStreamWaitEvent(sa, ev_dx, 0));
         if (fused) {
             OpScope op(c, "gate_bwd_fused", sa == c->s_comp || sa == s ? 0 : 2, -1, sa);
-            L += launch_wg_transpose(c->wg, d, E, c->wgT, sa);
-            L += launch_gate_bwd_fused(da, dxe, c->prow, c->dlogit, c->wgT, c->x, dx, c->dwg_partial, dwg,
+            L += launch_gate_bwd_fused(da, dxe, c->prow, c->dlogit, c->wg, c->x, dx, c->dwg_partial, dwg,
                                        c->num_sms, c->bf16, sa);
             CHECK_LAUNCH();
         } else {

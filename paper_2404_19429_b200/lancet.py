@@ -26,7 +26,7 @@ FLAG_RENORMALIZE, FLAG_TIMELINE, FLAG_SERIAL, FLAG_SIMT_GEMM, FLAG_NO_DW_OVERLAP
 FLAG_NO_SIDE_STREAM = 32
 FLAG_GEMM_MULTICAST = 64
 FLAG_UNFUSED_GATE_BWD = 128
-FLAG_PDL = 256
+FLAG_NO_PDL = 256
 # LANCET_EXTRA_FLAGS: OR'ed into every context's flags (e.g. run the test suite under PDL)
 EXTRA_FLAGS = int(os.environ.get("LANCET_EXTRA_FLAGS", "0"), 0)
 
