@@ -358,12 +358,13 @@ def run_lancet(a, world, rank, local_rank):
     f_l, b_l = ctx.launch_counts()
     send, recv, C = ctx.counts(a.chunks)
     rows_expert = int(recv.sum())                     # rows this rank's experts processed
-    exposed_ms, comm_ms = exposure_per_step(tl, a.steps) if world > 1 else (0.0, 0.0)
+    ep = world > 1 or bool(flags & lancet.FLAG_FORCE_EP)      # expert-parallel path (a2a on)
+    exposed_ms, comm_ms = exposure_per_step(tl, a.steps) if ep else (0.0, 0.0)
     exposed_ms = max_over_ranks(exposed_ms)
 
     # ---- unoverlapped baseline (world > 1): serial schedule, one stream, chunks merged -------
     unoverlapped_ms = 0.0
-    if world > 1:
+    if ep:
         ctx.set_flags(flags | lancet.FLAG_SERIAL)
         for _ in range(2):
             step()

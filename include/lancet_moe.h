@@ -89,10 +89,15 @@ enum {
                                            than the L2 traffic it saves (profiles/)          */
     LANCET_FLAG_UNFUSED_GATE_BWD = 1u << 7,/* world 1 with NO_SIDE_STREAM: K6 and K7 as two
                                            kernels even where the fused single pass applies  */
-    LANCET_FLAG_NO_PDL = 1u << 8        /* disable programmatic dependent launch (default on:
+    LANCET_FLAG_NO_PDL = 1u << 8,       /* disable programmatic dependent launch (default on:
                                            each kernel may start while its stream predecessor
                                            drains; every kernel waits with griddepcontrol.wait
                                            before touching memory; ~1 % per step)            */
+    LANCET_FLAG_FORCE_EP = 1u << 9      /* run the expert-parallel path (chunked NCCL
+                                           exchanges, S1/S2 scheduler) even at world 1, over a
+                                           one-rank NCCL communicator (lancet_create needs an
+                                           NCCL id); set at creation.  Exercises the NCCL path
+                                           on a single GPU                                    */
 };
 
 typedef struct {

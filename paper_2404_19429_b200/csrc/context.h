@@ -29,6 +29,7 @@ struct OpEvent {
 struct lancet_ctx {
     // configuration
     int world = 1, rank = 0, device = 0, E_l = 0, num_sms = 0;
+    bool ep = false;           // expert-parallel path (world > 1, or LANCET_FLAG_FORCE_EP)
     lancet_layer_config cfg{};
     bool bf16 = true;
     size_t elt = 2;

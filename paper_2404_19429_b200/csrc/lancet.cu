@@ -165,7 +165,7 @@ lancet_status expert_forward(lancet_ctx* c, const int* grp_rows, const int* grp_
     a.c_rows = c->rows_exp;
     {   // fc1: H = act(X W1^T), G' = act'(X W1^T)
         OpScope op(c, "expert_fc1", 0, chunk, s);
-        a.A = c->world > 1 ? c->xe : c->xs; a.lda = d; a.a_rows = c->rows_exp;
+        a.A = c->ep ? c->xe : c->xs; a.lda = d; a.a_rows = c->rows_exp;
         a.B = c->w1; a.ldb = d; a.b_group_stride = (long)f * d; a.b_mn = false; a.a_mn = false;
         a.b_rows = (long)c->E_l * f;
         a.C = c->H; a.C2 = c->Gp; a.ldc = f; a.N = f; a.K = d; a.epi = EPI_ACT;
@@ -230,7 +230,7 @@ lancet_status expert_backward_dw(lancet_ctx* c, const void* dout, const int* grp
     }
     {
         OpScope op(c, "expert_dw1", 0, chunk, s);
-        a.A = c->dA; a.lda = f; a.B = c->world > 1 ? c->xe : c->xs; a.ldb = d;
+        a.A = c->dA; a.lda = f; a.B = c->ep ? c->xe : c->xs; a.ldb = d;
         a.C = dw1; a.ldc = d; a.c_group_stride = (long)f * d; a.M = f; a.N = d;
         return run_gemm(c, a, s, launches);
     }
@@ -254,6 +254,7 @@ lancet_status validate_cfg(const lancet_layer_config* cfg, int world)
 lancet_status create_common(lancet_ctx* c, int world, int rank, int device, const lancet_layer_config* cfg)
 {
     c->world = world;
+    c->ep = world > 1 || (cfg->flags & LANCET_FLAG_FORCE_EP);
     c->rank = rank;
     c->device = device;
     c->cfg = *cfg;
@@ -303,7 +304,7 @@ lancet_status create_common(lancet_ctx* c, int world, int rank, int device, cons
     const size_t rs = (size_t)c->rows_src * d * c->elt;
     AL(c->xs, rs);
     AL(c->dcomb, rs);
-    if (world == 1) {
+    if (!c->ep) {
         c->rows_exp = c->rows_src;
         c->xe = c->xs;
         c->comb = nullptr;                      // world 1: comb == out
@@ -486,12 +487,13 @@ LANCET_API lancet_status lancet_create(lancet_ctx** out, int32_t world, int32_t 
     if (!out) return fail(nullptr, LANCET_ERR_ARG, "out is NULL");
     *out = nullptr;
     if (world < 1 || rank < 0 || rank >= world) return fail(nullptr, LANCET_ERR_ARG, "bad world/rank");
-    if (world > 1 && !nccl_id) return fail(nullptr, LANCET_ERR_ARG, "world > 1 needs an NCCL id");
+    const bool ep = world > 1 || (cfg && (cfg->flags & LANCET_FLAG_FORCE_EP));
+    if (ep && !nccl_id) return fail(nullptr, LANCET_ERR_ARG, "world > 1 (or FORCE_EP) needs an NCCL id");
     lancet_status st = validate_cfg(cfg, world);
     if (st) return st;
     auto* c = new lancet_ctx();
     st = create_common(c, world, rank, cuda_device, cfg);
-    if (!st && world > 1) {
+    if (!st && ep) {
         std::string err;
         c->comm = make_nccl_transport(world, rank, nccl_id, LANCET_COMM_SMS, err);
         if (!c->comm) st = fail(c, LANCET_ERR_NCCL, err);
@@ -574,6 +576,8 @@ LANCET_API lancet_status lancet_destroy(lancet_ctx* c)
 LANCET_API lancet_status lancet_set_flags(lancet_ctx* c, uint32_t flags)
 {
     if (!c) return fail(nullptr, LANCET_ERR_ARG, "ctx is NULL");
+    if ((flags & LANCET_FLAG_FORCE_EP) != (c->cfg.flags & LANCET_FLAG_FORCE_EP))
+        return fail(c, LANCET_ERR_ARG, "FORCE_EP must be set at creation");
     if ((flags & LANCET_FLAG_RENORMALIZE) != (c->cfg.flags & LANCET_FLAG_RENORMALIZE) && c->world > 1)
         return fail(c, LANCET_ERR_ARG, "RENORMALIZE must be set at creation (checked across ranks)");
     c->cfg.flags = flags;
@@ -618,7 +622,7 @@ LANCET_API lancet_status lancet_moe_forward(lancet_ctx* c, const void* x, const 
     ra.S = c->S; ra.send_rows = c->send_rows; ra.send_off = c->send_off;
     DispatchArgs da{T, k, d, E, c->idx, c->slot, c->w, c->send_off, c->send_rows};
 
-    if (c->world == 1) {
+    if (!c->ep) {
         // ---- single GPU: no exchange, no host synchronisation --------------------------
         { OpScope op(c, "gate", 0, -1, s); L += launch_routing(ra, c->bf16, s); }
         CHECK_LAUNCH();
@@ -806,7 +810,7 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
     int& L = c->launches_bwd;
     DispatchArgs da{T, k, d, E, c->idx, c->slot, c->w, c->send_off, c->send_rows};
 
-    if (c->world == 1) {
+    if (!c->ep) {
         const void* comb = ident ? c->xs : c->out;
         { OpScope op(c, "combine_bwd", 0, -1, s);
           L += launch_combine_bwd(da, dy, comb, c->g, c->dcomb, 0, T, true, c->logits, renorm, c->dlogit,

@@ -27,6 +27,7 @@ FLAG_NO_SIDE_STREAM = 32
 FLAG_GEMM_MULTICAST = 64
 FLAG_UNFUSED_GATE_BWD = 128
 FLAG_NO_PDL = 256
+FLAG_FORCE_EP = 512
 # LANCET_EXTRA_FLAGS: OR'ed into every context's flags (e.g. run the test suite under PDL)
 EXTRA_FLAGS = int(os.environ.get("LANCET_EXTRA_FLAGS", "0"), 0)
 
@@ -206,6 +207,8 @@ class Context:
             nid = None
             if world > 1:
                 nid = ctypes.create_string_buffer(share_nccl_id(pg, rank), 128)
+            elif (cfg.flags | EXTRA_FLAGS) & FLAG_FORCE_EP:          # one-rank NCCL communicator
+                nid = ctypes.create_string_buffer(nccl_unique_id(), 128)
             _check(lib.lancet_create(ctypes.byref(self._p), world, rank, self.device, nid,
                                      ctypes.byref(c)))
         self.E_l = cfg.n_experts // world
