@@ -305,14 +305,16 @@ gate_topk_kernel(const Elt* __restrict__ x, const float* __restrict__ wg, int T,
 // tokens' x rows through a private cp.async ring of 64-dim slices and runs the R1 chains with
 // no block barrier in the loop.  Thread (token lane/tpt, experts 4*(lane%tpt)..+3), two
 // chains per fma.rn.f32x2.  4 warps per block; 2 blocks per SM at d = 1024, E = 8.
-constexpr int kGsDT = 64, kGsStages = 8;
-#ifdef LANCET_EXP_GS_CE2
-constexpr int kGsCE = 2, kGsWarps = 8;  // experts (chains) per thread, warps per block
+constexpr int kGsDT = 64;
+#if defined(LANCET_EXP_GS_CE2)
+constexpr int kGsCE = 2, kGsTT = 1, kGsWarps = 8, kGsStages = 8;  // chains/thread, tokens/thread
+#elif defined(LANCET_EXP_GS_TT2)
+constexpr int kGsCE = 4, kGsTT = 2, kGsWarps = 2, kGsStages = 4;
 #else
-constexpr int kGsCE = 4, kGsWarps = 4;
+constexpr int kGsCE = 4, kGsTT = 1, kGsWarps = 4, kGsStages = 8;
 #endif
 
-__host__ __device__ inline int gs_tpw(int E) { return 32 / (E / kGsCE); }       // tokens per warp
+__host__ __device__ inline int gs_tpw(int E) { return 32 / (E / kGsCE) * kGsTT; } // tokens per warp
 __host__ __device__ inline int gs_row_bytes(int elt) { return kGsDT * elt + 16; }
 __host__ __device__ inline size_t gs_wg_bytes(int d, int E) { return (size_t)(E / kGsCE) * (d * kGsCE + 4) * 4; }
 __host__ __device__ inline size_t gs_smem(int d, int E, int elt)
@@ -338,8 +340,8 @@ gate_stream_kernel(const Elt* __restrict__ x, const float* __restrict__ wg, int 
     constexpr int CPR = kGsDT / V;                     // chunks per row slice
     constexpr int S = kGsStages;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    constexpr int CE = kGsCE;
-    const int tpt = E / CE, tpw = 32 / tpt;
+    constexpr int CE = kGsCE, TT = kGsTT;
+    const int tpt = E / CE, tpw = 32 / tpt * TT;
     const int RB = gs_row_bytes(sizeof(Elt));
     const int gstride = d * CE + 4;                    // floats per expert group (+4: bank offset)
     float* swg = reinterpret_cast<float*>(gsm);
@@ -381,28 +383,37 @@ gate_stream_kernel(const Elt* __restrict__ x, const float* __restrict__ wg, int 
     cp_async_wait<S - 1>();                            // Wg (the oldest group) has landed
     __syncthreads();
 
-    const int r = lane / tpt, grp = lane % tpt;
+    const int r = lane / tpt, grp = lane % tpt;        // tokens r*TT .. r*TT+TT-1
     const float* wbase = swg + (size_t)grp * gstride;
-    float2 acc0 = make_float2(0.f, 0.f), acc1 = acc0;
+    float2 acc0[TT], acc1[TT];
+#pragma unroll
+    for (int u = 0; u < TT; ++u) acc0[u] = acc1[u] = make_float2(0.f, 0.f);
     for (int st = 0; st < nst; ++st) {
         if (st + S - 1 < nst) issue(st + S - 1);
         cp_async_commit();
         cp_async_wait<S - 1>();
         __syncwarp();                                  // every lane's pieces of slice st landed
-        const uint4* xr = reinterpret_cast<const uint4*>(ring + (size_t)(st % S) * tpw * RB + r * RB);
+        const uint8_t* xrow = ring + (size_t)(st % S) * tpw * RB + (size_t)(r * TT) * RB;
         const float* wp = wbase + st * kGsDT * CE;
 #pragma unroll
         for (int c = 0; c < CPR; ++c) {
-            float xf[V];
-            unpack16<Elt>(xr[c], xf);
+            float xf[TT][V];
+#pragma unroll
+            for (int tt = 0; tt < TT; ++tt)
+                unpack16<Elt>(reinterpret_cast<const uint4*>(xrow + tt * RB)[c], xf[tt]);
 #pragma unroll
             for (int u = 0; u < V; ++u) {               // R1: increasing i, one fused step each
                 if constexpr (CE == 4) {
                     const float4 w4 = *reinterpret_cast<const float4*>(wp + (c * V + u) * 4);
-                    ffma2(acc0, xf[u], make_float2(w4.x, w4.y));
-                    ffma2(acc1, xf[u], make_float2(w4.z, w4.w));
+#pragma unroll
+                    for (int tt = 0; tt < TT; ++tt) {
+                        ffma2(acc0[tt], xf[tt][u], make_float2(w4.x, w4.y));
+                        ffma2(acc1[tt], xf[tt][u], make_float2(w4.z, w4.w));
+                    }
                 } else {
-                    ffma2(acc0, xf[u], *reinterpret_cast<const float2*>(wp + (c * V + u) * 2));
+                    const float2 w2 = *reinterpret_cast<const float2*>(wp + (c * V + u) * 2);
+#pragma unroll
+                    for (int tt = 0; tt < TT; ++tt) ffma2(acc0[tt], xf[tt][u], w2);
                 }
             }
         }
@@ -413,20 +424,24 @@ gate_stream_kernel(const Elt* __restrict__ x, const float* __restrict__ wg, int 
     // logits of the warp's tokens -> shared [tpw][E] in the warp's own (now idle) ring, then
     // top-k per token
     float* lg = reinterpret_cast<float*>(ring);
-    const int t = tw + r;
-    if constexpr (CE == 4) {
-        *reinterpret_cast<float4*>(lg + r * E + grp * 4) = make_float4(acc0.x, acc0.y, acc1.x, acc1.y);
-        if (t < T)
-            *reinterpret_cast<float4*>(logits + (size_t)t * E + grp * 4) = make_float4(acc0.x, acc0.y, acc1.x, acc1.y);
-    } else {
-        *reinterpret_cast<float2*>(lg + r * E + grp * 2) = acc0;
-        if (t < T) *reinterpret_cast<float2*>(logits + (size_t)t * E + grp * 2) = acc0;
+#pragma unroll
+    for (int tt = 0; tt < TT; ++tt) {
+        const int rr = r * TT + tt, t = tw + rr;
+        if constexpr (CE == 4) {
+            const float4 v = make_float4(acc0[tt].x, acc0[tt].y, acc1[tt].x, acc1[tt].y);
+            *reinterpret_cast<float4*>(lg + rr * E + grp * 4) = v;
+            if (t < T) *reinterpret_cast<float4*>(logits + (size_t)t * E + grp * 4) = v;
+        } else {
+            *reinterpret_cast<float2*>(lg + rr * E + grp * 2) = acc0[tt];
+            if (t < T) *reinterpret_cast<float2*>(logits + (size_t)t * E + grp * 2) = acc0[tt];
+        }
     }
     __syncwarp();
     const int tile0 = t0 / kScanTile;
-    if (lane < tpw && tw + lane < T)
-        gate_select_token(lg + lane * E, tw + lane, E, k, renorm, idx_out, w_out,
-                          sh_hist + ((tw + lane) / kScanTile - tile0) * E);
+    for (int q = lane; q < tpw; q += 32)
+        if (tw + q < T)
+            gate_select_token(lg + q * E, tw + q, E, k, renorm, idx_out, w_out,
+                              sh_hist + ((tw + q) / kScanTile - tile0) * E);
     __syncthreads();
     for (int q = tid; q < 2 * E; q += blockDim.x) {
         const int tile = tile0 + q / E;
