@@ -280,9 +280,42 @@ def run_e2e(a, world, ins, ctx, wg, w1, w2, dwg, dw1, dw2, dev, barrier, max_ove
     ems = max_over_ranks(f0.elapsed_time(f1) / ne)
     ok = bool(torch.equal(yh[(ne - 1) & 1], yd[(ne - 1) & 1].cpu()))
     nb = xh.numel() * xh.element_size()
+    # the copies alone (no compute): the PCIe ceiling of this end-to-end loop
+    def copy_ms(fn, reps=5):
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        fn()
+        torch.cuda.synchronize()
+        c0.record(comp)
+        for _ in range(reps):
+            fn()
+        c1.record(comp)
+        torch.cuda.synchronize()
+        return c0.elapsed_time(c1) / reps
+
+    def h2d_only():
+        xd[0].copy_(xh, non_blocking=True)
+        dyd[0].copy_(dyh, non_blocking=True)
+
+    def d2h_only():
+        yh[0].copy_(yd[0], non_blocking=True)
+        dxh[0].copy_(dxd[0], non_blocking=True)
+
+    def both():
+        with torch.cuda.stream(s_in):
+            s_in.wait_stream(comp)
+            h2d_only()
+        with torch.cuda.stream(s_out):
+            s_out.wait_stream(comp)
+            d2h_only()
+        comp.wait_stream(s_in)
+        comp.wait_stream(s_out)
+
+    h_ms, d_ms, b_ms = copy_ms(h2d_only), copy_ms(d2h_only), copy_ms(both)
     return {"value": world * a.tokens / (ems / 1000.0), "unit": "tokens/s",
             "h2d_bytes_per_step": 2 * nb, "d2h_bytes_per_step": 2 * nb, "ms_per_step": ems,
             "readback_checked": ok,
+            "copies_alone_ms": {"h2d": h_ms, "d2h": d_ms, "both_directions": b_ms,
+                                "h2d_gbs": 2 * nb / (h_ms * 1e6), "d2h_gbs": 2 * nb / (d_ms * 1e6)},
             "path": "pinned host x, dy -> device (own stream) -> lancet_moe_forward + lancet_moe_backward "
                     "(C-ABI) -> y, dx -> pinned host (own stream); device buffers double-buffered so "
                     "copies overlap neighbouring steps' compute; every step's copies are inside the "
