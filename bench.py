@@ -471,6 +471,7 @@ def run_lancet(a, world, rank, local_rank):
                                "achieved = 12*rows*d*f algorithmic FLOP / summed CUDA-event time",
                      "peak_source": pk["src"] + " bf16_tflops_sustained"},
         "kernels": kernels,
+        "launch_groups": {o: v["launch_groups_per_step"] for o, v in ops.items()},
         "gpu_launches": (f_l + b_l) * a.steps,
         "clocks": clk,
         "routing": {"capacity": C, "admitted_pairs": adm, "dropped_pairs": a.tokens * a.k - adm,

@@ -18,9 +18,11 @@
 
 namespace lancet {
 
-constexpr int kGateDT = 128;     // d-tile staged in shared memory (cp.async ring)
-constexpr int kGateStages = 4;   // ring depth: ~3 tiles of x in flight per block (HBM latency)
-constexpr int kGateThreads = 128;
+// d-tile staged in shared memory (cp.async ring): 128 dims, 64 when 8 experts per thread (the
+// Wg tile, DT x E fp32, dominates the stage and bounds the blocks per SM)
+__host__ __device__ constexpr int gate_dt(int ce) { return ce >= 8 ? 64 : 128; }
+__host__ __device__ constexpr int gate_stages(int ce) { return ce >= 8 ? 3 : 4; }   // ring depth
+constexpr int kGateThreads = 256;
 constexpr int kGateMaxTB = 64;   // tokens per block (T=16k -> 256 blocks, all resident)
 
 // Thread (tokens r..r+TT-1, experts e0..e0+CE-1) runs TT*CE independent R1 chains, two at a
@@ -48,7 +50,7 @@ __host__ __device__ inline int gate_ce(int E)
 }
 
 // floats per expert group of the staged Wg tile (+4: groups start in different banks)
-__host__ __device__ constexpr int gate_wg_stride(int ce) { return kGateDT * ce + 4; }
+__host__ __device__ constexpr int gate_wg_stride(int ce) { return gate_dt(ce) * ce + 4; }
 
 __host__ __device__ inline GateGeom gate_geom(int E, int elt_bytes)
 {
@@ -60,10 +62,10 @@ __host__ __device__ inline GateGeom gate_geom(int E, int elt_bytes)
     if (g.TB > kGateMaxTB) g.TB = kGateMaxTB;
     if (g.TB < g.tt) g.TB = g.tt;
     g.threads = g.TB / g.tt * g.tpt;
-    g.row_bytes = kGateDT * elt_bytes + 16;
+    g.row_bytes = gate_dt(g.ce) * elt_bytes + 16;
     g.x_bytes = (size_t)g.TB * g.row_bytes;
     g.buf_bytes = g.x_bytes + (size_t)g.tpt * gate_wg_stride(g.ce) * 4;   // x tile | Wg tile [E/CE][DT][CE]
-    const size_t xs = kGateStages * g.buf_bytes;
+    const size_t xs = gate_stages(g.ce) * g.buf_bytes;
     const size_t lg = sizeof(float) * (size_t)g.TB * E;
     g.smem = xs > lg ? xs : lg;
     return g;
@@ -99,9 +101,10 @@ __device__ __forceinline__ void gate_load_tile(const Elt* __restrict__ x, const 
                                                int T, int d, int E, int t0, const GateGeom& geo,
                                                int i0, uint8_t* buf)
 {
-    const int ilim = min(kGateDT, d - i0);
-    constexpr int kFull = kGateDT * (int)sizeof(Elt) / 16;       // 16-byte chunks per full row
-    if (ilim == kGateDT) {
+    constexpr int DT = gate_dt(CE);
+    const int ilim = min(DT, d - i0);
+    constexpr int kFull = DT * (int)sizeof(Elt) / 16;            // 16-byte chunks per full row
+    if (ilim == DT) {
         for (int q = threadIdx.x; q < geo.TB * kFull; q += blockDim.x) {
             const int r = q / kFull, c = q % kFull, t = t0 + r;     // kFull: power of two
             if (t < T)
@@ -206,20 +209,21 @@ gate_topk_kernel(const Elt* __restrict__ x, const float* __restrict__ wg, int T,
         for (int c = 0; c < P; ++c) acc2[u][c] = make_float2(0.f, 0.f);
     }
 
-    const int ntiles = ceil_div(d, kGateDT);
+    constexpr int DT = gate_dt(CE), NS = gate_stages(CE);
+    const int ntiles = ceil_div(d, DT);
 #pragma unroll
-    for (int st = 0; st < kGateStages - 1; ++st) {             // prologue: tiles 0..S-2
-        if (st < ntiles) gate_load_tile<Elt, CE>(x, wg, T, d, E, t0, geo, st * kGateDT, gsm + st * geo.buf_bytes);
+    for (int st = 0; st < NS - 1; ++st) {                      // prologue: tiles 0..S-2
+        if (st < ntiles) gate_load_tile<Elt, CE>(x, wg, T, d, E, t0, geo, st * DT, gsm + st * geo.buf_bytes);
         cp_async_commit();
     }
     for (int it = 0; it < ntiles; ++it) {
-        uint8_t* cur = gsm + (it % kGateStages) * geo.buf_bytes;
-        const int nx = it + kGateStages - 1;                    // refill the slot freed last round
-        if (nx < ntiles) gate_load_tile<Elt, CE>(x, wg, T, d, E, t0, geo, nx * kGateDT, gsm + (nx % kGateStages) * geo.buf_bytes);
+        uint8_t* cur = gsm + (it % NS) * geo.buf_bytes;
+        const int nx = it + NS - 1;                             // refill the slot freed last round
+        if (nx < ntiles) gate_load_tile<Elt, CE>(x, wg, T, d, E, t0, geo, nx * DT, gsm + (nx % NS) * geo.buf_bytes);
         cp_async_commit();
-        cp_async_wait<kGateStages - 1>();
+        cp_async_wait<NS - 1>();
         __syncthreads();
-        const int ilim = min(kGateDT, d - it * kGateDT);        // multiple of 8 (d % 8 == 0)
+        const int ilim = min(DT, d - it * DT);        // multiple of 8 (d % 8 == 0)
         if (active) {
             const uint8_t* xrow = cur + (size_t)(q * TT) * geo.row_bytes;
             const float* wp = reinterpret_cast<const float*>(cur + geo.x_bytes) + (size_t)grp * gate_wg_stride(CE);
