@@ -281,7 +281,11 @@ struct K6Geom {
 };
 
 // K6: dx_t = sum_j dX[prow_tj] + sum_e dlogit_te Wg[:, e]; Wg^T slice of the thread in registers
-template <typename Elt, int KK, int EE, int NTC>
+// EG > 1 (E = 8 EG, E <= 64): EG adjacent lanes share a dim group, each holding the Wg^T
+// slice of 8 experts; their gate-term partials meet in an xor-shuffle tree; only the group's
+// first lane copies row pieces into the ring (the others read them after __syncwarp).  A block
+// covers 256 / EG dim groups (grid.y splits d).
+template <typename Elt, int KK, int EE, int NTC, int EG = 1>
 __global__ void __launch_bounds__(256)
 k6_stream_kernel(const Elt* __restrict__ dxe, const int* __restrict__ prow,
                  const float* __restrict__ dlogit, const float* __restrict__ wg, int t0, int t1,
@@ -290,10 +294,13 @@ k6_stream_kernel(const Elt* __restrict__ dxe, const int* __restrict__ prow,
     pdl_wait();   // programmatic dependent launch: predecessor's writes visible
     using G = K6Geom<Elt, KK>;
     constexpr int NV = G::NV, U = G::U, S = kStreamStages;
-    extern __shared__ __align__(16) uint4 ring[];          // [S][SLOT][NT]
-    const int NT = NTC > 0 ? NTC : (int)blockDim.x, tid = threadIdx.x;
-    int* srow = reinterpret_cast<int*>(ring + (size_t)S * G::SLOT * NT);   // [tpb][KK]
-    float* sdl = reinterpret_cast<float*>(srow + tpb * KK);                 // [tpb][EE]
+    constexpr int ET = EG == 1 ? EE : 8 * EG;              // experts staged per token
+    extern __shared__ __align__(16) uint4 ring[];          // [S][SLOT][NT / EG]
+    const int NT = NTC > 0 ? NTC : (int)blockDim.x;
+    const int NTD = NT / EG, dg = threadIdx.x / EG, eg = threadIdx.x % EG, tid = threadIdx.x;
+    const bool copier = eg == 0;
+    int* srow = reinterpret_cast<int*>(ring + (size_t)S * G::SLOT * NTD);  // [tpb][KK]
+    float* sdl = reinterpret_cast<float*>(srow + tpb * KK);                 // [tpb][ET]
     const int tb0 = t0 + blockIdx.x * tpb;
     const int tb1 = min(t1, tb0 + tpb);
     if (tb0 >= tb1) return;
@@ -302,24 +309,26 @@ k6_stream_kernel(const Elt* __restrict__ dxe, const int* __restrict__ prow,
         const int r = q / KK, j = q % KK;
         srow[q] = j < k ? prow[(size_t)(tb0 + r) * k + j] : -1;
     }
-    for (int q = tid; q < nt * EE; q += NT) {
-        const int r = q / EE, e = q % EE;
+    for (int q = tid; q < nt * ET; q += NT) {
+        const int r = q / ET, e = q % ET;
         sdl[q] = e < E ? dlogit[(size_t)(tb0 + r) * E + e] : 0.f;
     }
-    const int i0 = tid * 8;
+    const int i0 = (blockIdx.y * NTD + dg) * 8;
+    const int e0 = eg * 8;                                  // this lane's experts (EG > 1)
     // this thread's Wg^T slice, read straight from Wg [d][E] (rows i0..i0+7 are contiguous)
     float2 wg2[EE][4];
 #pragma unroll
     for (int e = 0; e < EE; ++e)
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-            wg2[e][q] = e < E ? make_float2(__ldg(wg + (size_t)(i0 + 2 * q) * E + e),
-                                            __ldg(wg + (size_t)(i0 + 2 * q + 1) * E + e))
-                              : make_float2(0.f, 0.f);
+            wg2[e][q] = e0 + e < E ? make_float2(__ldg(wg + (size_t)(i0 + 2 * q) * E + e0 + e),
+                                                 __ldg(wg + (size_t)(i0 + 2 * q + 1) * E + e0 + e))
+                                   : make_float2(0.f, 0.f);
     __syncthreads();
     const int ng = ceil_div(nt, U);
     auto issue = [&](int g) {
-        uint4* slot = ring + (size_t)(g % S) * G::SLOT * NT;
+        if (!copier) return;
+        uint4* slot = ring + (size_t)(g % S) * G::SLOT * NTD;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int r = g * U + u;
@@ -329,7 +338,7 @@ k6_stream_kernel(const Elt* __restrict__ dxe, const int* __restrict__ prow,
                 if (row >= 0) {
                     const uint4* src = reinterpret_cast<const uint4*>(dxe + (size_t)row * d + i0);
 #pragma unroll
-                    for (int v = 0; v < NV; ++v) cp_async16_s(slot + ((u * KK + j) * NV + v) * NT + tid, src + v);
+                    for (int v = 0; v < NV; ++v) cp_async16_s(slot + ((u * KK + j) * NV + v) * NTD + dg, src + v);
                 }
             }
         }
@@ -343,7 +352,8 @@ k6_stream_kernel(const Elt* __restrict__ dxe, const int* __restrict__ prow,
         if (g + S - 1 < ng) issue(g + S - 1);
         cp_async_commit_s();
         cp_async_wait_s<S - 1>();
-        const uint4* slot = ring + (size_t)(g % S) * G::SLOT * NT;
+        if constexpr (EG > 1) __syncwarp();                 // the group's copier has landed the slot
+        const uint4* slot = ring + (size_t)(g % S) * G::SLOT * NTD;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int r = g * U + u;
@@ -357,7 +367,7 @@ k6_stream_kernel(const Elt* __restrict__ dxe, const int* __restrict__ prow,
             float dlv[EE];
 #pragma unroll
             for (int e = 0; e < EE; e += 2) {
-                const float2 v = *reinterpret_cast<const float2*>(sdl + r * EE + e);
+                const float2 v = *reinterpret_cast<const float2*>(sdl + r * ET + e0 + e);
                 dlv[e] = v.x; dlv[e + 1] = v.y;
             }
 #pragma unroll
@@ -365,23 +375,41 @@ k6_stream_kernel(const Elt* __restrict__ dxe, const int* __restrict__ prow,
                 if (rw[j] >= 0) {
                     uint4 raw[NV];
 #pragma unroll
-                    for (int v = 0; v < NV; ++v) raw[v] = slot[((u * KK + j) * NV + v) * NT + tid];
+                    for (int v = 0; v < NV; ++v) raw[v] = slot[((u * KK + j) * NV + v) * NTD + dg];
                     float f[8];
                     unpack8<Elt>(raw, f);
 #pragma unroll
                     for (int i = 0; i < 8; ++i) acc[i] += f[i];
                 }
             }
-            float2 a2[4] = {make_float2(acc[0], acc[1]), make_float2(acc[2], acc[3]),
-                            make_float2(acc[4], acc[5]), make_float2(acc[6], acc[7])};
+            float2 a2[4];
+            if constexpr (EG == 1) {            // rows sum, then the gate term in e order
+                a2[0] = make_float2(acc[0], acc[1]); a2[1] = make_float2(acc[2], acc[3]);
+                a2[2] = make_float2(acc[4], acc[5]); a2[3] = make_float2(acc[6], acc[7]);
+            } else {                            // this lane's 8-expert partial of the gate term
+#pragma unroll
+                for (int p = 0; p < 4; ++p) a2[p] = make_float2(0.f, 0.f);
+            }
 #pragma unroll
             for (int e = 0; e < EE; ++e) {
                 const float2 dl2 = make_float2(dlv[e], dlv[e]);
 #pragma unroll
                 for (int p = 0; p < 4; ++p) a2[p] = __ffma2_rn(dl2, wg2[e][p], a2[p]);
             }
+            if constexpr (EG > 1) {             // partials of the EG lanes: fixed xor tree
+#pragma unroll
+                for (int m = 1; m < EG; m <<= 1)
+#pragma unroll
+                    for (int p = 0; p < 4; ++p) {
+                        a2[p].x += __shfl_xor_sync(0xffffffffu, a2[p].x, m);
+                        a2[p].y += __shfl_xor_sync(0xffffffffu, a2[p].y, m);
+                    }
+#pragma unroll
+                for (int p = 0; p < 4; ++p) a2[p] = make_float2(acc[2 * p] + a2[p].x, acc[2 * p + 1] + a2[p].y);
+            }
             const float o[8] = {a2[0].x, a2[0].y, a2[1].x, a2[1].y, a2[2].x, a2[2].y, a2[3].x, a2[3].y};
             Elt* dst = dx + (size_t)(tb0 + r) * d + i0;
+            if (!copier) continue;
             if constexpr (sizeof(Elt) == 2) {
                 st_v4(dst, pack16<bf16>(o));
             } else {
@@ -389,28 +417,34 @@ k6_stream_kernel(const Elt* __restrict__ dxe, const int* __restrict__ prow,
                 st_v4(dst + 4, pack16<float>(o + 4));
             }
         }
+        if constexpr (EG > 1) __syncwarp();                 // slot read by the group before refill
     }
     cp_async_wait_s<0>();
 }
 
 // K7 partials: block b sums x_t (x) dlogit_t over its contiguous token range -> partial[b][E][d]
-template <typename Elt, int EE, int NTC>
+// (EG > 1: E = 8 EG; EG adjacent lanes share a dim group, one group of 8 experts each; only
+// the group's first lane copies the x pieces.  grid.y splits d.)
+template <typename Elt, int EE, int NTC, int EG = 1>
 __global__ void __launch_bounds__(256)
 dwg_stream_kernel(const Elt* __restrict__ x, const float* __restrict__ dlogit, int T, int d, int E,
                   int tpb, float* __restrict__ partial)
 {
     pdl_wait();   // programmatic dependent launch: predecessor's writes visible
     constexpr int NV = Dims8<Elt>::NV, U = 8 / NV, S = kDwgStages;
-    extern __shared__ __align__(16) uint4 ring[];          // [S][U*NV][NT]
+    constexpr int ET = EG == 1 ? EE : 8 * EG;              // experts staged per token
+    extern __shared__ __align__(16) uint4 ring[];          // [S][U*NV][NT / EG]
     const int NT = NTC > 0 ? NTC : (int)blockDim.x, tid = threadIdx.x;
-    float* sdl = reinterpret_cast<float*>(ring + (size_t)S * U * NV * NT);   // [tpb][EE]
+    const int NTD = NT / EG, dg = tid / EG, eg = tid % EG;
+    const bool copier = eg == 0;
+    float* sdl = reinterpret_cast<float*>(ring + (size_t)S * U * NV * NTD);  // [tpb][ET]
     const int tb0 = blockIdx.x * tpb;
     const int nt = max(0, min(T, tb0 + tpb) - tb0);
-    for (int q = tid; q < nt * EE; q += NT) {
-        const int r = q / EE, e = q % EE;
+    for (int q = tid; q < nt * ET; q += NT) {
+        const int r = q / ET, e = q % ET;
         sdl[q] = e < E ? dlogit[(size_t)(tb0 + r) * E + e] : 0.f;
     }
-    const int i0 = tid * 8;
+    const int i0 = (blockIdx.y * NTD + dg) * 8, e0 = eg * 8;
     float2 acc[8][EE / 2];
 #pragma unroll
     for (int a = 0; a < 8; ++a)
@@ -419,14 +453,15 @@ dwg_stream_kernel(const Elt* __restrict__ x, const float* __restrict__ dlogit, i
     __syncthreads();
     const int ng = ceil_div(nt, U);
     auto issue = [&](int g) {
-        uint4* slot = ring + (size_t)(g % S) * U * NV * NT;
+        if (!copier) return;
+        uint4* slot = ring + (size_t)(g % S) * U * NV * NTD;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int r = g * U + u;
             if (r < nt) {
                 const uint4* src = reinterpret_cast<const uint4*>(x + (size_t)(tb0 + r) * d + i0);
 #pragma unroll
-                for (int v = 0; v < NV; ++v) cp_async16_s(slot + (u * NV + v) * NT + tid, src + v);
+                for (int v = 0; v < NV; ++v) cp_async16_s(slot + (u * NV + v) * NTD + dg, src + v);
             }
         }
     };
@@ -439,38 +474,40 @@ dwg_stream_kernel(const Elt* __restrict__ x, const float* __restrict__ dlogit, i
         if (g + S - 1 < ng) issue(g + S - 1);
         cp_async_commit_s();
         cp_async_wait_s<S - 1>();
-        const uint4* slot = ring + (size_t)(g % S) * U * NV * NT;
+        if constexpr (EG > 1) __syncwarp();                 // the group's copier has landed the slot
+        const uint4* slot = ring + (size_t)(g % S) * U * NV * NTD;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int r = g * U + u;
             if (r >= nt) break;
             uint4 raw[NV];
 #pragma unroll
-            for (int v = 0; v < NV; ++v) raw[v] = slot[(u * NV + v) * NT + tid];
+            for (int v = 0; v < NV; ++v) raw[v] = slot[(u * NV + v) * NTD + dg];
             float xf[8];
             unpack8<Elt>(raw, xf);
             float2 dl[EE / 2];
 #pragma unroll
-            for (int p = 0; p < EE / 2; ++p) dl[p] = *reinterpret_cast<const float2*>(sdl + r * EE + 2 * p);
+            for (int p = 0; p < EE / 2; ++p) dl[p] = *reinterpret_cast<const float2*>(sdl + r * ET + e0 + 2 * p);
 #pragma unroll
             for (int a = 0; a < 8; ++a)
 #pragma unroll
                 for (int p = 0; p < EE / 2; ++p) acc[a][p] = __ffma2_rn(make_float2(xf[a], xf[a]), dl[p], acc[a][p]);
         }
+        if constexpr (EG > 1) __syncwarp();                 // slot read by the group before refill
     }
     cp_async_wait_s<0>();
     // partial[b][e][i]: for each expert the block's threads store consecutive 32-byte runs
-    float* out = partial + (size_t)blockIdx.x * E * d + i0;
+    float* out = partial + (size_t)blockIdx.x * E * d + (size_t)e0 * d + i0;
 #pragma unroll
     for (int p = 0; p < EE / 2; ++p) {
-        if (2 * p < E) {
+        if (e0 + 2 * p < E) {
             float v[8];
 #pragma unroll
             for (int a = 0; a < 8; ++a) v[a] = acc[a][p].x;
             st_v4(out + (size_t)(2 * p) * d, pack16<float>(v));
             st_v4(out + (size_t)(2 * p) * d + 4, pack16<float>(v + 4));
         }
-        if (2 * p + 1 < E) {
+        if (e0 + 2 * p + 1 < E) {
             float v[8];
 #pragma unroll
             for (int a = 0; a < 8; ++a) v[a] = acc[a][p].y;
@@ -717,7 +754,16 @@ static void launch_k6(const DispatchArgs& a, const void* dxe, const int* prow, c
 }
 
 static bool stream_ok(int d, int E) { return E <= 8 && d % 256 == 0 && d <= 2048; }
-bool gate_bwd_needs_wgT(int d, int E) { return !stream_ok(d, E); }
+// E = 8 EG, EG in {2, 4, 8}: the wide streaming K6 / K7
+static bool wide_ok(int d, int E) { return (E == 16 || E == 32 || E == 64) && d % 256 == 0 && d <= 2048; }
+bool gate_bwd_needs_wgT(int d, int E) { return !stream_ok(d, E) && !(wide_ok(d, E) && E >= 32); }
+// dim groups per block for EG lanes per group (<= 256 threads, dividing d / 8)
+static int wide_ntd(int d, int EG)
+{
+    int ntd = 256 / EG;
+    while ((d / 8) % ntd) ntd /= 2;
+    return ntd;
+}
 static int ee_of(int E) { return E <= 2 ? 2 : E <= 4 ? 4 : 8; }
 
 template <typename Elt, int KK, int EE>
@@ -745,11 +791,45 @@ static void launch_k6_stream(const DispatchArgs& a, const void* dxe, const int* 
             (const Elt*)dxe, prow, dlogit, wg, t0, t1, a.k, a.d, a.E, tpb, (Elt*)dx);
 }
 
+template <typename Elt, int KK, int EG>
+static void launch_k6_wide(const DispatchArgs& a, const void* dxe, const int* prow, const float* dlogit,
+                           const float* wg, void* dx, int t0, int t1, int num_sms, cudaStream_t s)
+{
+    using G = K6Geom<Elt, KK>;
+    const int NTD = wide_ntd(a.d, EG), DS = a.d / 8 / NTD, NT = NTD * EG;
+    const int nb = std::max(1, std::min(ceil_div(t1 - t0, G::U), std::max(1, 3 * num_sms / DS)));
+    const int tpb = ceil_div(t1 - t0, nb);
+    const size_t smem = (size_t)kStreamStages * G::SLOT * NTD * 16 + (size_t)tpb * (KK + 8 * EG) * 4;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k6_stream_kernel<Elt, KK, 8, 0, EG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+    }
+    launch_k(k6_stream_kernel<Elt, KK, 8, 0, EG>, dim3(ceil_div(t1 - t0, tpb), DS), NT, smem, s,
+             (const Elt*)dxe, prow, dlogit, wg, t0, t1, a.k, a.d, a.E, tpb, (Elt*)dx);
+}
+
 int launch_unpermute_gate_bwd(const DispatchArgs& a, const void* dxe, const int* prow,
                               const float* dlogit, const float* wg, const float* wgT, void* dx, int t0, int t1,
                               int num_sms, bool is_bf16, cudaStream_t s)
 {
     if (t1 <= t0) return 0;
+    // wide K6 only from E = 32 (at E = 16 the shared-memory Wg^T kernel measured faster)
+    if (wide_ok(a.d, a.E) && a.E >= 32 && a.k <= 4) {
+#define K6W(Elt, KK)                                                                                              \
+    do {                                                                                                          \
+        if (a.E == 16) launch_k6_wide<Elt, KK, 2>(a, dxe, prow, dlogit, wg, dx, t0, t1, num_sms, s);             \
+        else if (a.E == 32) launch_k6_wide<Elt, KK, 4>(a, dxe, prow, dlogit, wg, dx, t0, t1, num_sms, s);        \
+        else launch_k6_wide<Elt, KK, 8>(a, dxe, prow, dlogit, wg, dx, t0, t1, num_sms, s);                       \
+    } while (0)
+        if (is_bf16) {
+            if (a.k == 1) K6W(bf16, 1); else if (a.k == 2) K6W(bf16, 2); else K6W(bf16, 4);
+        } else {
+            if (a.k == 1) K6W(float, 1); else if (a.k == 2) K6W(float, 2); else K6W(float, 4);
+        }
+#undef K6W
+        return 1;
+    }
     if (stream_ok(a.d, a.E) && a.k <= 4) {
         const int ee = ee_of(a.E);
 #define K6S(Elt, KK)                                                                                              \
@@ -782,7 +862,7 @@ int launch_unpermute_gate_bwd(const DispatchArgs& a, const void* dxe, const int*
 size_t dwg_partial_floats(int T, int d, int E)
 {
     size_t n = (size_t)ceil_div(T, kDwgTok) * d * E;
-    if (stream_ok(d, E)) n = std::max(n, (size_t)kDwgStreamMaxBlocks * d * E);
+    if (stream_ok(d, E) || wide_ok(d, E)) n = std::max(n, (size_t)kDwgStreamMaxBlocks * d * E);
     return n;
 }
 
@@ -808,9 +888,39 @@ static void launch_dwg_stream(const Elt* x, const float* dlogit, int T, int d, i
     launch_k(dwg_reduce4_kernel, ceil_div(d * E, 32), 256, 0, s, partial, grid, d * E, d, E, dwg);
 }
 
+template <typename Elt, int EG>
+static void launch_dwg_wide(const Elt* x, const float* dlogit, int T, int d, int E, float* partial,
+                            float* dwg, int num_sms, cudaStream_t s)
+{
+    constexpr int NV = Dims8<Elt>::NV, U = 8 / NV;
+    const int NTD = wide_ntd(d, EG), DS = d / 8 / NTD, NT = NTD * EG;
+    const int nb = std::max(1, std::min({ceil_div(T, 2 * U), std::max(1, 2 * num_sms / DS), kDwgStreamMaxBlocks}));
+    const int tpb = ceil_div(T, nb);
+    const int grid = ceil_div(T, tpb);
+    const size_t smem = (size_t)kDwgStages * U * NV * NTD * 16 + (size_t)tpb * 8 * EG * 4;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(dwg_stream_kernel<Elt, 8, 0, EG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+    }
+    launch_k(dwg_stream_kernel<Elt, 8, 0, EG>, dim3(grid, DS), NT, smem, s, x, dlogit, T, d, E, tpb, partial);
+    launch_k(dwg_reduce4_kernel, ceil_div(d * E, 32), 256, 0, s, partial, grid, d * E, d, E, dwg);
+}
+
 int launch_dwg(const void* x, const float* dlogit, int T, int d, int E, float* partial,
                float* dwg, bool is_bf16, int num_sms, cudaStream_t s)
 {
+    if (wide_ok(d, E)) {
+#define DWW(Elt)                                                                                                  \
+    do {                                                                                                          \
+        if (E == 16) launch_dwg_wide<Elt, 2>((const Elt*)x, dlogit, T, d, E, partial, dwg, num_sms, s);          \
+        else if (E == 32) launch_dwg_wide<Elt, 4>((const Elt*)x, dlogit, T, d, E, partial, dwg, num_sms, s);     \
+        else launch_dwg_wide<Elt, 8>((const Elt*)x, dlogit, T, d, E, partial, dwg, num_sms, s);                  \
+    } while (0)
+        if (is_bf16) DWW(bf16); else DWW(float);
+#undef DWW
+        return 2;
+    }
     if (stream_ok(d, E) && (d * E) % 4 == 0) {
         const int ee = ee_of(E);
 #define DWS(Elt)                                                                                                  \

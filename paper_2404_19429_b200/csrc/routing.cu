@@ -310,29 +310,34 @@ gate_topk_kernel(const Elt* __restrict__ x, const float* __restrict__ wg, int T,
 // no block barrier in the loop.  Thread (token lane/tpt, experts 4*(lane%tpt)..+3), two
 // chains per fma.rn.f32x2.  4 warps per block; 2 blocks per SM at d = 1024, E = 8.
 constexpr int kGsDT = 64;
-#if defined(LANCET_EXP_GS_CE2)
-constexpr int kGsCE = 2, kGsTT = 1, kGsWarps = 8, kGsStages = 8;  // chains/thread, tokens/thread
-#elif defined(LANCET_EXP_GS_TT2)
-constexpr int kGsCE = 4, kGsTT = 2, kGsWarps = 2, kGsStages = 4;
-#else
-constexpr int kGsCE = 4, kGsTT = 1, kGsWarps = 4, kGsStages = 8;
-#endif
+constexpr int kGsCE = 4, kGsTT = 1;   // experts per thread, tokens per thread (CE=2 / CE=8 /
+                                      // TT=2 measured slower)
+constexpr int kGsTokensPerBlock = 64; // 4 warps at E = 8, 8 at E = 16
+constexpr size_t kGsSmemMax = 110 * 1024;   // two blocks per SM
 
 __host__ __device__ inline int gs_tpw(int E) { return 32 / (E / kGsCE) * kGsTT; } // tokens per warp
 __host__ __device__ inline int gs_row_bytes(int elt) { return kGsDT * elt + 16; }
 __host__ __device__ inline size_t gs_wg_bytes(int d, int E) { return (size_t)(E / kGsCE) * (d * kGsCE + 4) * 4; }
-__host__ __device__ inline size_t gs_smem(int d, int E, int elt)
+__host__ __device__ inline int gs_warps(int E) { return kGsTokensPerBlock / gs_tpw(E) > 0 ? kGsTokensPerBlock / gs_tpw(E) : 1; }
+// ring depth: 8 slices if they fit beside the resident Wg, else 4
+static int gs_stages(int d, int E, int elt)
 {
-    const size_t ring = (size_t)kGsWarps * kGsStages * gs_tpw(E) * gs_row_bytes(elt);
-    return gs_wg_bytes(d, E) + ring;       // a warp's logits [tpw][E] fit in its ring
+    const size_t per_stage = (size_t)gs_warps(E) * gs_tpw(E) * gs_row_bytes(elt);
+    return gs_wg_bytes(d, E) + 8 * per_stage <= kGsSmemMax ? 8 : 4;
+}
+static size_t gs_smem(int d, int E, int elt)
+{
+    // a warp's logits [tpw][E] fit in its ring
+    return gs_wg_bytes(d, E) + (size_t)gs_stages(d, E, elt) * gs_warps(E) * gs_tpw(E) * gs_row_bytes(elt);
 }
 static bool gs_ok(int d, int E, int elt)
 {
-    return E % 4 == 0 && E / kGsCE <= 32 && 32 % (E / kGsCE) == 0 && d % kGsDT == 0 && gs_smem(d, E, elt) <= 110 * 1024;
+    return E % 4 == 0 && E / kGsCE <= 32 && 32 % (E / kGsCE) == 0 && d % kGsDT == 0 && gs_warps(E) <= 16 &&
+           gs_smem(d, E, elt) <= kGsSmemMax;
 }
 
-template <typename Elt>
-__global__ void __launch_bounds__(kGsWarps * 32)
+template <typename Elt, int S>
+__global__ void __launch_bounds__(512)
 gate_stream_kernel(const Elt* __restrict__ x, const float* __restrict__ wg, int T, int d, int E,
                    int k, int renorm, float* __restrict__ logits, int* __restrict__ idx_out,
                    float* __restrict__ w_out, int* __restrict__ hist, int n_tiles)
@@ -342,7 +347,6 @@ gate_stream_kernel(const Elt* __restrict__ x, const float* __restrict__ wg, int 
     __shared__ int sh_hist[2 * kMaxExperts];
     constexpr int V = Vec16<Elt>::N;                   // dims per 16-byte chunk
     constexpr int CPR = kGsDT / V;                     // chunks per row slice
-    constexpr int S = kGsStages;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     constexpr int CE = kGsCE, TT = kGsTT;
     const int tpt = E / CE, tpw = 32 / tpt * TT;
@@ -350,7 +354,7 @@ gate_stream_kernel(const Elt* __restrict__ x, const float* __restrict__ wg, int 
     const int gstride = d * CE + 4;                    // floats per expert group (+4: bank offset)
     float* swg = reinterpret_cast<float*>(gsm);
     uint8_t* ring = gsm + gs_wg_bytes(d, E) + (size_t)warp * S * tpw * RB;
-    const int t0 = blockIdx.x * kGsWarps * tpw;
+    const int t0 = blockIdx.x * (int)(blockDim.x >> 5) * tpw;
     const int tw = t0 + warp * tpw;                    // this warp's first token
 
     for (int i = tid; i < 2 * E; i += blockDim.x) sh_hist[i] = 0;
@@ -573,18 +577,20 @@ int launch_routing(const RouteArgs& a, bool is_bf16, cudaStream_t s)
     if (gs_ok(a.d, a.E, elt)) {
         static bool gs_attr = false;
         if (!gs_attr) {
-            cudaFuncSetAttribute(gate_stream_kernel<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-            cudaFuncSetAttribute(gate_stream_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            cudaFuncSetAttribute(gate_stream_kernel<bf16, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            cudaFuncSetAttribute(gate_stream_kernel<float, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            cudaFuncSetAttribute(gate_stream_kernel<bf16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            cudaFuncSetAttribute(gate_stream_kernel<float, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
             gs_attr = true;
         }
-        const int per_block = kGsWarps * gs_tpw(a.E);
+        const int W = gs_warps(a.E), per_block = W * gs_tpw(a.E), S = gs_stages(a.d, a.E, elt);
         const size_t smem = gs_smem(a.d, a.E, elt);
-        if (is_bf16)
-            launch_k(gate_stream_kernel<bf16>, ceil_div(a.T, per_block), kGsWarps * 32, smem, s, 
-                (const bf16*)a.x, a.wg, a.T, a.d, a.E, a.k, a.renorm, a.logits, a.idx, a.w, a.hist, n_tiles);
-        else
-            launch_k(gate_stream_kernel<float>, ceil_div(a.T, per_block), kGsWarps * 32, smem, s, 
-                (const float*)a.x, a.wg, a.T, a.d, a.E, a.k, a.renorm, a.logits, a.idx, a.w, a.hist, n_tiles);
+        const dim3 grid(ceil_div(a.T, per_block)), block(W * 32);
+#define GS(Elt, SS) launch_k(gate_stream_kernel<Elt, SS>, grid, block, smem, s, (const Elt*)a.x, a.wg, a.T, a.d, \
+                             a.E, a.k, a.renorm, a.logits, a.idx, a.w, a.hist, n_tiles)
+        if (is_bf16) { if (S == 8) GS(bf16, 8); else GS(bf16, 4); }
+        else { if (S == 8) GS(float, 8); else GS(float, 4); }
+#undef GS
     } else {
     const GateGeom g = gate_geom(a.E, elt);
     const int blocks = ceil_div(a.T, g.TB);

@@ -170,6 +170,10 @@ def test_gate_backward_paths(E, k):
     (2048, 256, 3, 3, "bf16"),      # k = 3 (ring slot sized for KK = 4), E padded to 4
     (700, 2048, 2, 2, "bf16"),      # widest streamed row: 256 threads x 8 dims
     (37, 256, 8, 2, "fp32"),        # fewer tokens than blocks
+    (1500, 256, 16, 2, "bf16"),     # wide: 2 lanes per dim group
+    (1200, 512, 32, 1, "fp32"),     # wide: 4 lanes per dim group, d split over 2 blocks
+    (900, 1024, 64, 4, "bf16"),     # wide: 8 lanes per dim group, d split over 4 blocks, k = 4
+    (333, 256, 64, 3, "bf16"),      # wide, k = 3, ragged
 ])
 def test_gate_backward_streaming_paths(T, d, E, k, dtype):
     # E <= 8, d % 256 == 0, d <= 2048: K6 with Wg^T in registers and K7 partials over
