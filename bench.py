@@ -50,10 +50,17 @@ def parse():
     ap.add_argument("--flags", type=int, default=0, help="extra LANCET_FLAG_* bits")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--transport", choices=["nccl", "peer"], default="nccl",
+                    help="world > 1: NCCL grouped send/recv, or copy-engine pulls over CUDA IPC")
+    ap.add_argument("--same-device", action="store_true",
+                    help="all ranks on GPU 0 (peer transport, gloo process group): a multi-process "
+                         "test of the exchange machinery on one GPU, not a scaling measurement")
     ap.add_argument("--no-timeline", action="store_true",
                     help="no per-op events in the timed region (A/B of their overhead)")
     a = ap.parse_args()
     a.warmup = max(a.warmup, 3)
+    if a.same_device:
+        a.transport = "peer"
     return a
 
 
@@ -64,6 +71,8 @@ def workload(a, world):
                     f"n_chunks={a.chunks} bf16",
         "tokens_per_gpu": a.tokens, "d_model": a.d, "d_ffn": a.f, "experts": a.experts,
         "top_k": a.k, "capacity_factor": a.cf, "n_chunks": a.chunks, "routing_skew_beta": a.beta,
+        "parallelism": f"ep{world}" + (f" ({a.transport} all-to-all)" if world > 1 else "")
+                       + (" all ranks on one GPU" if getattr(a, "same_device", False) else ""),
         "global_batch_tokens": a.tokens * world,
         "l2": "inputs larger than L2: per-step working set >= 1.4 GiB vs 126 MB L2 (no flush)",
     }
@@ -216,25 +225,28 @@ def run_e2e(a, world, ins, ctx, wg, w1, w2, dwg, dw1, dw2, dev, barrier, max_ove
 
     Every step copies its inputs x, dy from pinned host memory to the device and reads its
     results y, dx back to pinned host memory, inside the timed region.  Device inputs and
-    outputs are double-buffered and the copies run on their own streams, so step i+1's
-    host->device copy and step i's device->host copies overlap the compute of neighbouring
-    steps (a data-loader style pipeline); y's read-back overlaps the step's own backward."""
+    outputs are triple-buffered and the copies run on their own streams, so the host->device
+    copies of the next two steps and the device->host copies of earlier steps overlap the
+    compute (a data-loader style pipeline: PCIe moves 64 MB each way per step, about as long
+    as the step's compute, so a second step of slack absorbs the jitter); y's read-back
+    overlaps the step's own backward."""
     import torch
+    NB = 3
     bf = torch.bfloat16
     xh = torch.from_numpy(ins["x"]).to(bf).pin_memory()
     dyh = torch.from_numpy(ins["dy"]).to(bf).pin_memory()
-    yh = [torch.empty(xh.shape, dtype=bf).pin_memory() for _ in range(2)]
-    dxh = [torch.empty(xh.shape, dtype=bf).pin_memory() for _ in range(2)]
-    xd = [torch.empty(xh.shape, dtype=bf, device=dev) for _ in range(2)]
-    dyd = [torch.empty(xh.shape, dtype=bf, device=dev) for _ in range(2)]
-    yd = [torch.empty(xh.shape, dtype=bf, device=dev) for _ in range(2)]
-    dxd = [torch.empty(xh.shape, dtype=bf, device=dev) for _ in range(2)]
+    yh = [torch.empty(xh.shape, dtype=bf).pin_memory() for _ in range(NB)]
+    dxh = [torch.empty(xh.shape, dtype=bf).pin_memory() for _ in range(NB)]
+    xd = [torch.empty(xh.shape, dtype=bf, device=dev) for _ in range(NB)]
+    dyd = [torch.empty(xh.shape, dtype=bf, device=dev) for _ in range(NB)]
+    yd = [torch.empty(xh.shape, dtype=bf, device=dev) for _ in range(NB)]
+    dxd = [torch.empty(xh.shape, dtype=bf, device=dev) for _ in range(NB)]
     comp = torch.cuda.current_stream()
     s_in, s_out = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
-    ev_in = [torch.cuda.Event() for _ in range(2)]
-    ev_fwd = [torch.cuda.Event() for _ in range(2)]
-    ev_bwd = [torch.cuda.Event() for _ in range(2)]
-    ev_out = [torch.cuda.Event() for _ in range(2)]
+    ev_in = [torch.cuda.Event() for _ in range(NB)]
+    ev_fwd = [torch.cuda.Event() for _ in range(NB)]
+    ev_bwd = [torch.cuda.Event() for _ in range(NB)]
+    ev_out = [torch.cuda.Event() for _ in range(NB)]
 
     def h2d(b):
         with torch.cuda.stream(s_in):
@@ -244,20 +256,21 @@ def run_e2e(a, world, ins, ctx, wg, w1, w2, dwg, dw1, dw2, dev, barrier, max_ove
             ev_in[b].record(s_in)
 
     def run(n):
-        for b in range(2):
+        for b in range(NB):
             ev_bwd[b].record(comp)
             ev_out[b].record(s_out)
-        h2d(0)
+        for j in range(min(NB - 1, n)):
+            h2d(j)
         for i in range(n):
-            b = i & 1
+            b = i % NB
             comp.wait_event(ev_in[b])
-            comp.wait_event(ev_out[b])            # host buffers of step i-2 have been read
+            comp.wait_event(ev_out[b])            # host buffers of step i-NB have been read
             ctx.forward(xd[b], wg, w1, w2, a.k, a.cf, a.chunks, y=yd[b], routing=False)
             ev_fwd[b].record(comp)
             ctx.backward(dyd[b], dx=dxd[b], dwg=dwg, dw1=dw1, dw2=dw2)
             ev_bwd[b].record(comp)
-            if i + 1 < n:
-                h2d(1 - b)
+            if i + NB - 1 < n:
+                h2d((i + NB - 1) % NB)
             with torch.cuda.stream(s_out):
                 s_out.wait_event(ev_fwd[b])
                 yh[b].copy_(yd[b], non_blocking=True)
@@ -278,7 +291,7 @@ def run_e2e(a, world, ins, ctx, wg, w1, w2, dwg, dw1, dw2, dev, barrier, max_ove
     torch.cuda.synchronize()
     barrier()
     ems = max_over_ranks(f0.elapsed_time(f1) / ne)
-    ok = bool(torch.equal(yh[(ne - 1) & 1], yd[(ne - 1) & 1].cpu()))
+    ok = bool(torch.equal(yh[(ne - 1) % NB], yd[(ne - 1) % NB].cpu()))
     nb = xh.numel() * xh.element_size()
     # the copies alone (no compute): the PCIe ceiling of this end-to-end loop
     def copy_ms(fn, reps=5):
@@ -317,7 +330,7 @@ def run_e2e(a, world, ins, ctx, wg, w1, w2, dwg, dw1, dw2, dev, barrier, max_ove
             "copies_alone_ms": {"h2d": h_ms, "d2h": d_ms, "both_directions": b_ms,
                                 "h2d_gbs": 2 * nb / (h_ms * 1e6), "d2h_gbs": 2 * nb / (d_ms * 1e6)},
             "path": "pinned host x, dy -> device (own stream) -> lancet_moe_forward + lancet_moe_backward "
-                    "(C-ABI) -> y, dx -> pinned host (own stream); device buffers double-buffered so "
+                    "(C-ABI) -> y, dx -> pinned host (own stream); device buffers triple-buffered so "
                     "copies overlap neighbouring steps' compute; every step's copies are inside the "
                     "timed region (first H2D to last D2H)"}
 
@@ -346,7 +359,8 @@ def run_lancet(a, world, rank, local_rank):
     cfg = lancet.LayerConfig(d_model=a.d, d_ffn=a.f, n_experts=a.experts, max_tokens=a.tokens,
                              max_k=a.k, max_chunks=max(8, a.chunks), dtype="bf16", flags=flags)
     ctx = lancet.Context(cfg, world=world, rank=rank, device=local_rank,
-                         pg=dist.group.WORLD if world > 1 else None)
+                         pg=dist.group.WORLD if world > 1 else None,
+                         transport=a.transport if world > 1 else "nccl")
     stream = torch.cuda.current_stream()
     y = torch.empty_like(x)
     dx = torch.empty_like(x)
@@ -365,7 +379,7 @@ def run_lancet(a, world, rank, local_rank):
     def max_over_ranks(v):
         if world == 1:
             return v
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        t = torch.tensor([v], dtype=torch.float64, device="cpu" if a.same_device else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -500,9 +514,14 @@ def main():
         return
     import torch
     import torch.distributed as dist
+    if a.same_device:
+        local_rank = 0
     if world > 1:
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if a.same_device:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         run_lancet(a, world, rank, local_rank)
     finally:

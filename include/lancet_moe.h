@@ -151,6 +151,25 @@ lancet_status lancet_local_group_destroy(lancet_local_group* group);
 lancet_status lancet_create_local(lancet_ctx** out, lancet_local_group* group, int32_t rank,
                                   int32_t cuda_device, const lancet_layer_config* cfg);
 
+/* Copy-engine peer transport (no NCCL; one process per rank, all ranks' devices reachable by
+ * CUDA IPC -- one NVSwitch node, or several processes sharing one GPU).  Every rank maps its
+ * peers' pull-source buffers and copies the rows it needs into its own buffers with
+ * cudaMemcpyAsync on its comm stream (copy engines: no SMs taken from the expert GEMMs); the
+ * chunk readiness / buffer reuse across processes is ordered by sequence flags in device
+ * memory (stream wait-value / write-value operations).  Expert-side buffers are allocated at
+ * their bound (world * max_tokens * max_k rows) at creation.  Setup:
+ *   1. lancet_create_peer on every rank;
+ *   2. lancet_peer_export: this rank's blob (lancet_peer_blob_bytes() bytes, host);
+ *   3. the caller all-gathers the blobs (rank order) over its own channel;
+ *   4. lancet_peer_import with the world blobs (host, world * blob bytes).
+ * Then forward / backward as with NCCL (collective: every rank calls them in the same order).
+ * The blob holds CUDA IPC handles; it is only meaningful to processes of the same node. */
+lancet_status lancet_create_peer(lancet_ctx** out, int32_t world, int32_t rank, int32_t cuda_device,
+                                 const lancet_layer_config* cfg);
+size_t lancet_peer_blob_bytes(void);
+lancet_status lancet_peer_export(lancet_ctx* ctx, void* blob /* host, lancet_peer_blob_bytes() */);
+lancet_status lancet_peer_import(lancet_ctx* ctx, const void* blobs /* host, world blobs */);
+
 /* Destroy; aborts the communicator if the context is poisoned.  Safe on NULL. */
 lancet_status lancet_destroy(lancet_ctx* ctx);
 

@@ -18,6 +18,27 @@ struct DevBuf {
     size_t bytes = 0;
 };
 
+// Copy-engine peer transport (world > 1 without NCCL): every rank maps the pull sources of its
+// peers (CUDA IPC) and copies the rows it needs into its own buffers with cudaMemcpyAsync on
+// its comm stream (copy engines, no SMs); readiness and reuse are ordered by 32-bit sequence
+// flags in device memory (stream wait-value / write-value operations).
+enum PeerKind { PK_XS = 0, PK_OUT, PK_DCOMB, PK_DXE, PK_COUNTS, PK_N };
+struct PeerLinks {
+    int world = 0, n_max = 0;
+    std::vector<char*> src[PK_DXE + 1];   // per peer: its pull-source buffers (self: local)
+    std::vector<int*> counts;             // per peer: its count matrix [G][E][n]
+    std::vector<uint32_t*> flags;         // per peer: its flag array
+    int* my_counts = nullptr;             // [G][E][n_max] this rank's matrix
+    uint32_t* my_flags = nullptr;         // [2][PK_N][n_max][G]: ready | consumed
+    uint32_t seq = 0;                     // step counter (forward)
+    std::vector<void*> opened;            // IPC mappings to close
+    std::vector<int> matrix;              // host copy of the last count matrix [G][E][n]
+    int* h_matrix = nullptr;              // pinned staging of the matrix
+    size_t flag_index(int consumed, int kind, int chunk, int r) const {
+        return (((size_t)consumed * PK_N + kind) * n_max + chunk) * world + r;
+    }
+};
+
 struct OpEvent {
     std::string name;
     int lane, chunk;
@@ -36,6 +57,8 @@ struct lancet_ctx {
 
     // comm
     lancet::Transport* comm = nullptr;
+    lancet::PeerLinks* peer = nullptr;   // copy-engine peer transport (instead of comm)
+    bool peer_ready = false;             // peers imported
 
     // streams / events
     cudaStream_t s_comp = nullptr, s_comm = nullptr;

@@ -504,6 +504,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 #pragma unroll
                                 for (int i = 0; i < 32; i += 2) {
                                     float2 h2, g2;
+// LANCET_EXP_*: experiment switches for A/B builds only (LANCET_BUILD_DEFS, DESIGN.md §7's
+// power experiment); the library is never built with them.
 #ifdef LANCET_EXP_NO_MATH
                                     h2 = make_float2(f[i], f[i + 1]); g2 = h2;
 #else

@@ -25,6 +25,7 @@
 #include "common.cuh"
 #include "context.h"
 #include "kernels.h"
+#include "peer.h"
 
 #define LANCET_API extern "C" __attribute__((visibility("default")))
 
@@ -428,6 +429,54 @@ struct Plan {
     }
 };
 
+// Every rank's send and receive layout from the all-gathered count matrix M [G][E][n] (peer
+// transport: a pull needs the source rank's offsets).
+struct GlobalPlan {
+    int G = 0, E = 0, E_l = 0, n = 0;
+    std::vector<int> M;
+    std::vector<Plan> rank;     // rank[g] = g's Plan (its send counts and its receive counts)
+    void build(int G_, int E_, int E_l_, int n_, const int* m) {
+        G = G_; E = E_; E_l = E_l_; n = n_;
+        M.assign(m, m + (size_t)G * E * n);
+        rank.clear();
+        for (int g = 0; g < G; ++g) {
+            std::vector<int> recv((size_t)G * E_l * n);
+            for (int src = 0; src < G; ++src)
+                for (int el = 0; el < E_l; ++el)
+                    for (int c = 0; c < n; ++c)
+                        recv[((size_t)src * E_l + el) * n + c] = M[((size_t)src * E + g * E_l + el) * n + c];
+            Plan pl{E, E_l, G, n};
+            pl.build(&M[(size_t)g * E * n], recv.data());
+            rank.push_back(pl);
+        }
+    }
+    // pulls of rank `me` for chunks [c0, c1): toward_experts (dispatch-like: token-side source,
+    // expert-side destination `dst`) or back (combine-like: expert-side source, token-side `dst`)
+    std::vector<PeerCopy> pulls(int me, bool toward_experts, int c0, int c1, char* dst, size_t rowb) const {
+        std::vector<PeerCopy> v;
+        for (int p = 0; p < G; ++p)
+            for (int el = 0; el < E_l; ++el)
+                for (int ch = c0; ch < c1; ++ch) {
+                    if (toward_experts) {          // rows p admitted to my expert e
+                        const int e = me * E_l + el;
+                        const Plan& src = rank[p];
+                        const Plan& dstp = rank[me];
+                        v.push_back({p, (size_t)(src.send_off[e] + src.S[e * (n + 1) + ch]) * rowb,
+                                     dst + (size_t)(dstp.grp_off[ch * E_l + el] + dstp.src_off[(p * E_l + el) * n + ch]) * rowb,
+                                     (size_t)M[((size_t)p * E + e) * n + ch] * rowb});
+                    } else {                       // my rows back from expert e on rank p
+                        const int e = p * E_l + el;
+                        const Plan& src = rank[p];
+                        const Plan& dstp = rank[me];
+                        v.push_back({p, (size_t)(src.grp_off[ch * E_l + el] + src.src_off[(me * E_l + el) * n + ch]) * rowb,
+                                     dst + (size_t)(dstp.send_off[e] + dstp.S[e * (n + 1) + ch]) * rowb,
+                                     (size_t)M[((size_t)me * E + e) * n + ch] * rowb});
+                    }
+                }
+        return v;
+    }
+};
+
 // K6 for the tokens of chunk cc of nc (nc == 1: all tokens): dx = expert path + gate term.
 lancet_status gate_backward_dx(lancet_ctx* c, const DispatchArgs& da, const void* dxe, void* dx,
                                cudaStream_t s, int cc, int nc, int* L)
@@ -551,10 +600,70 @@ LANCET_API lancet_status lancet_create_local(lancet_ctx** out, lancet_local_grou
     return LANCET_OK;
 }
 
+LANCET_API lancet_status lancet_create_peer(lancet_ctx** out, int32_t world, int32_t rank,
+                                            int32_t cuda_device, const lancet_layer_config* cfg)
+{
+    if (!out) return fail(nullptr, LANCET_ERR_ARG, "out is NULL");
+    *out = nullptr;
+    if (world < 1 || rank < 0 || rank >= world) return fail(nullptr, LANCET_ERR_ARG, "bad world/rank");
+    lancet_status st = validate_cfg(cfg, world);
+    if (st) return st;
+    lancet_layer_config cf2 = *cfg;
+    cf2.flags |= LANCET_FLAG_FORCE_EP;                  // the expert-parallel path, even at world 1
+    auto* c = new lancet_ctx();
+    st = create_common(c, world, rank, cuda_device, &cf2);
+    if (!st) {
+        // the expert-side buffers are mapped by the peers: allocate them at their bound once
+        // (every source sends at most max_tokens * max_k rows; + 128-row padding per group)
+        const long rows = (long)world * cfg->max_tokens * cfg->max_k +
+                          (long)c->E_l * cfg->max_chunks * kRowAlign;
+        if (rows > (1L << 30)) st = fail(c, LANCET_ERR_ARG, "expert-side row bound too large");
+        else st = ensure_expert_rows(c, (int)rows);
+    }
+    if (!st) {
+        std::string err;
+        if (peer_init(c, err)) st = fail(c, LANCET_ERR_CUDA, err);
+    }
+    if (st) {
+        g_thread_err = c->err;
+        lancet_destroy(c);
+        return st;
+    }
+    *out = c;
+    return LANCET_OK;
+}
+
+LANCET_API size_t lancet_peer_blob_bytes(void) { return peer_blob_bytes(); }
+
+LANCET_API lancet_status lancet_peer_export(lancet_ctx* c, void* blob)
+{
+    lancet_status st = check_ready(c);
+    if (st) return st;
+    if (!c->peer || !blob) return fail(c, LANCET_ERR_ARG, "not a peer-transport context, or blob is NULL");
+    std::string err;
+    if (peer_export(c, blob, err)) return fail(c, LANCET_ERR_CUDA, err);
+    return LANCET_OK;
+}
+
+LANCET_API lancet_status lancet_peer_import(lancet_ctx* c, const void* blobs)
+{
+    lancet_status st = check_ready(c);
+    if (st) return st;
+    if (!c->peer || !blobs) return fail(c, LANCET_ERR_ARG, "not a peer-transport context, or blobs is NULL");
+    std::string err;
+    if (peer_import(c, blobs, err)) return fail(c, LANCET_ERR_CUDA, err);
+    c->peer_ready = true;
+    return LANCET_OK;
+}
+
 LANCET_API lancet_status lancet_destroy(lancet_ctx* c)
 {
     if (!c) return LANCET_OK;
     cudaSetDevice(c->device);
+    if (c->peer) {
+        cudaDeviceSynchronize();
+        peer_destroy(c);
+    }
     if (c->comm) {
         if (c->poisoned) c->comm->abort();
         else cudaDeviceSynchronize();
@@ -647,6 +756,13 @@ LANCET_API lancet_status lancet_moe_forward(lancet_ctx* c, const void* x, const 
         CK(cudaStreamWaitEvent(c->s_comm, c->ev_fork, 0));
         size_t ev_i = 0;
         auto next_ev = [&]() { return c->ev_pool[ev_i++]; };
+        lancet::PeerLinks* pr = c->peer;
+        if (pr) {
+            if (!c->peer_ready) return fail(c, LANCET_ERR_STATE, "peer transport: lancet_peer_import not called");
+            ++pr->seq;
+            // every peer has pulled the previous step's rows from this rank's pull sources
+            if (peer_wait_consumed(c, sc)) return fail(c, LANCET_ERR_CUDA, "cuStreamWaitValue32");
+        }
 
         { OpScope op(c, "gate", 0, -1, sc); L += launch_routing(ra, c->bf16, sc); }
         int* d_send = c->counts_dev;                       // [E][n]
@@ -659,24 +775,45 @@ LANCET_API lancet_status lancet_moe_forward(lancet_ctx* c, const void* x, const 
         {   // C1: size exchange, once for all chunks (R11)
             CK(cudaStreamWaitEvent(sm, ev_route, 0));
             OpScope op(c, "a2a_counts", 1, -1, sm);
-            std::vector<P2P> sends, recvs;
-            const size_t b = sizeof(int) * E_l * n;
-            for (int p = 0; p < G; ++p) {
-                sends.push_back({p, d_send + p * E_l * n, b});
-                recvs.push_back({p, d_recv + p * E_l * n, b});
-            }
             std::string err;
-            if (c->comm->exchange(sends, recvs, sm, err)) return fail(c, LANCET_ERR_NCCL, err);
-            CK(cudaMemcpyAsync(c->h_counts, c->counts_dev, sizeof(int) * (E * n + G * E_l * n),
-                               cudaMemcpyDeviceToHost, sm));
+            if (pr) {       // all-gather of the count matrix [G][E][n] through peer memory
+                if (peer_counts(c, d_send, n, sm, err)) return fail(c, LANCET_ERR_CUDA, err);
+                CK(cudaMemcpyAsync(pr->h_matrix, pr->my_counts, sizeof(int) * (size_t)G * E * n,
+                                   cudaMemcpyDeviceToHost, sm));
+            } else {
+                std::vector<P2P> sends, recvs;
+                const size_t b = sizeof(int) * E_l * n;
+                for (int p = 0; p < G; ++p) {
+                    sends.push_back({p, d_send + p * E_l * n, b});
+                    recvs.push_back({p, d_recv + p * E_l * n, b});
+                }
+                if (c->comm->exchange(sends, recvs, sm, err)) return fail(c, LANCET_ERR_NCCL, err);
+                CK(cudaMemcpyAsync(c->h_counts, c->counts_dev, sizeof(int) * (E * n + G * E_l * n),
+                                   cudaMemcpyDeviceToHost, sm));
+            }
             CK(cudaEventRecord(c->ev_counts, sm));
         }
         // K3 permute overlaps the size exchange
         { OpScope op(c, "permute", 0, -1, sc); L += launch_permute(da, x, c->xs, c->bf16, sc); }
         CHECK_LAUNCH();
+        const bool serial_ = c->cfg.flags & LANCET_FLAG_SERIAL;
+        const int nc_ = serial_ ? 1 : n;
+        if (pr)             // the dispatch sources of every chunk are ready
+            for (int cc = 0; cc < nc_; ++cc)
+                if (peer_signal(c, 0, lancet::PK_XS, cc, sc)) return fail(c, LANCET_ERR_CUDA, "cuStreamWriteValue32");
         cudaEvent_t ev_perm = next_ev();
         CK(cudaEventRecord(ev_perm, sc));
         CK(cudaEventSynchronize(c->ev_counts));            // the one host synchronisation
+        GlobalPlan gp;
+        if (pr) {           // this rank's send / recv counts out of the matrix
+            gp.build(G, E, E_l, n, pr->h_matrix);
+            pr->matrix = gp.M;
+            memcpy(c->h_counts, &gp.M[(size_t)c->rank * E * n], sizeof(int) * E * n);
+            for (int src = 0; src < G; ++src)
+                for (int el = 0; el < E_l; ++el)
+                    for (int ch = 0; ch < n; ++ch)
+                        c->h_counts[E * n + (src * E_l + el) * n + ch] = gp.M[((size_t)src * E + c->rank * E_l + el) * n + ch];
+        }
         Plan pl{E, E_l, G, n};
         pl.build(c->h_counts, c->h_counts + E * n);
         st = ensure_expert_rows(c, std::max(pl.rows_total, kRowAlign));
@@ -711,6 +848,16 @@ LANCET_API lancet_status lancet_moe_forward(lancet_ctx* c, const void* x, const 
             int c0, c1;
             chunk_range(cc, c0, c1);
             OpScope op(c, "a2a_dispatch", 1, serial ? -1 : cc, sm);
+            if (pr) {
+                std::string err;
+                if (peer_pull(c, lancet::PK_XS, cc, gp.pulls(c->rank, true, c0, c1, xe, rowb), cc == nc - 1, sm, err))
+                    return fail(c, LANCET_ERR_CUDA, err);
+                if (ident && peer_signal(c, 0, lancet::PK_OUT, cc, sm))   // identity: xe is the combine source
+                    return fail(c, LANCET_ERR_CUDA, "cuStreamWriteValue32");
+                ev_disp[cc] = next_ev();
+                CK(cudaEventRecord(ev_disp[cc], sm));
+                continue;
+            }
             std::vector<P2P> sends, recvs;
             for (int p = 0; p < G; ++p)
                 for (int i = 0; i < E_l; ++i) {
@@ -741,6 +888,7 @@ LANCET_API lancet_status lancet_moe_forward(lancet_ctx* c, const void* x, const 
                 st = expert_forward(c, d_grp_rows + c0 * E_l, d_grp_off + c0 * E_l, (c1 - c0) * E_l,
                                     std::max(mr, kRowAlign), sc, serial ? -1 : cc, &L);
                 if (st) return st;
+                if (pr && peer_signal(c, 0, lancet::PK_OUT, cc, sc)) return fail(c, LANCET_ERR_CUDA, "cuStreamWriteValue32");
             }
             ev_exp[cc] = next_ev();
             CK(cudaEventRecord(ev_exp[cc], sc));
@@ -752,6 +900,14 @@ LANCET_API lancet_status lancet_moe_forward(lancet_ctx* c, const void* x, const 
             chunk_range(cc, c0, c1);
             CK(cudaStreamWaitEvent(sm, ev_exp[cc], 0));
             OpScope op(c, "a2a_combine", 1, serial ? -1 : cc, sm);
+            if (pr) {
+                std::string err;
+                if (peer_pull(c, lancet::PK_OUT, cc, gp.pulls(c->rank, false, c0, c1, comb, rowb), cc == nc - 1, sm, err))
+                    return fail(c, LANCET_ERR_CUDA, err);
+                ev_comb[cc] = next_ev();
+                CK(cudaEventRecord(ev_comb[cc], sm));
+                continue;
+            }
             std::vector<P2P> sends, recvs;
             for (int p = 0; p < G; ++p)
                 for (int el = 0; el < E_l; ++el)
@@ -871,6 +1027,9 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
     auto next_ev = [&]() { return c->ev_pool[ev_i++]; };
     Plan pl{E, E_l, G, n};
     pl.build(c->host_send.data(), c->host_recv.data());
+    lancet::PeerLinks* pr = c->peer;
+    GlobalPlan gp;
+    if (pr) gp.build(G, E, E_l, n, pr->matrix.data());
     int* d_grp_rows = c->grp_dev;
     int* d_grp_off = c->grp_dev + n * E_l;
     const size_t rowb = (size_t)d * c->elt;
@@ -892,6 +1051,7 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
         OpScope op(c, "combine_bwd", 0, serial ? -1 : cc, sc);
         L += launch_combine_bwd(da, dy, comb, c->g, c->dcomb, t0, t1, cc == 0, c->logits, renorm, c->dlogit,
                                 c->prow, c->bf16, sc);
+        if (pr && peer_signal(c, 0, lancet::PK_DCOMB, cc, sc)) return fail(c, LANCET_ERR_CUDA, "cuStreamWriteValue32");
         ev_k5[cc] = next_ev();
         CK(cudaEventRecord(ev_k5[cc], sc));
     }
@@ -904,6 +1064,16 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
         chunk_range(cc, c0, c1);
         CK(cudaStreamWaitEvent(sm, ev_k5[cc], 0));
         OpScope op(c, "a2a_bwd_dispatch", 1, serial ? -1 : cc, sm);
+        if (pr) {
+            std::string err;
+            if (peer_pull(c, lancet::PK_DCOMB, cc, gp.pulls(c->rank, true, c0, c1, dout, rowb), cc == nc - 1, sm, err))
+                return fail(c, LANCET_ERR_CUDA, err);
+            if (ident && peer_signal(c, 0, lancet::PK_DXE, cc, sm))   // identity: dout is the source back
+                return fail(c, LANCET_ERR_CUDA, "cuStreamWriteValue32");
+            ev_b1[cc] = next_ev();
+            CK(cudaEventRecord(ev_b1[cc], sm));
+            continue;
+        }
         std::vector<P2P> sends, recvs;
         for (int p = 0; p < G; ++p)
             for (int i = 0; i < E_l; ++i) {
@@ -934,6 +1104,7 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
             st = expert_backward_dx(c, c->dout, d_grp_rows + c0 * E_l, d_grp_off + c0 * E_l,
                                     (c1 - c0) * E_l, std::max(mr, kRowAlign), sc, serial ? -1 : cc, &L);
             if (st) return st;
+            if (pr && peer_signal(c, 0, lancet::PK_DXE, cc, sc)) return fail(c, LANCET_ERR_CUDA, "cuStreamWriteValue32");
         }
         ev_dx[cc] = next_ev();
         CK(cudaEventRecord(ev_dx[cc], sc));
@@ -953,6 +1124,14 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
         chunk_range(cc, c0, c1);
         CK(cudaStreamWaitEvent(sm, ev_dx[cc], 0));
         OpScope op(c, "a2a_bwd_combine", 1, serial ? -1 : cc, sm);
+        if (pr) {
+            std::string err;
+            if (peer_pull(c, lancet::PK_DXE, cc, gp.pulls(c->rank, false, c0, c1, dxcomb, rowb), cc == nc - 1, sm, err))
+                return fail(c, LANCET_ERR_CUDA, err);
+            ev_b2[cc] = next_ev();
+            CK(cudaEventRecord(ev_b2[cc], sm));
+            continue;
+        }
         std::vector<P2P> sends, recvs;
         for (int p = 0; p < G; ++p)
             for (int el = 0; el < E_l; ++el)

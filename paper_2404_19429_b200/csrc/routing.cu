@@ -42,11 +42,7 @@ struct GateGeom {
 
 __host__ __device__ inline int gate_ce(int E)
 {
-#ifdef LANCET_EXP_GATE_CE8
-    return (E % 8 == 0) ? 8 : (E % 4 == 0) ? 4 : (E % 2 == 0) ? 2 : 1;
-#else
     return (E % 8 == 0 && E >= 16) ? 8 : (E % 4 == 0) ? 4 : (E % 2 == 0) ? 2 : 1;
-#endif
 }
 
 // floats per expert group of the staged Wg tile (+4: groups start in different banks)

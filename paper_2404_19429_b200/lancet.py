@@ -35,7 +35,8 @@ EXPORTS = ["lancet_abi_version", "lancet_last_error", "lancet_nccl_unique_id", "
            "lancet_local_group_create", "lancet_local_group_destroy", "lancet_create_local",
            "lancet_destroy", "lancet_set_flags", "lancet_moe_forward", "lancet_moe_backward",
            "lancet_get_counts", "lancet_timeline_begin", "lancet_last_timeline", "lancet_debug_copy",
-           "lancet_workspace_bytes", "lancet_launch_counts", "lancet_plan_exchange"]
+           "lancet_workspace_bytes", "lancet_launch_counts", "lancet_plan_exchange",
+           "lancet_create_peer", "lancet_peer_blob_bytes", "lancet_peer_export", "lancet_peer_import"]
 
 
 class LancetError(RuntimeError):
@@ -80,6 +81,10 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "lancet_local_group_create": ([ctypes.POINTER(P), I32], I32),
             "lancet_local_group_destroy": ([P], I32),
             "lancet_create_local": ([ctypes.POINTER(P), P, I32, I32, ctypes.POINTER(_Config)], I32),
+            "lancet_create_peer": ([ctypes.POINTER(P), I32, I32, I32, ctypes.POINTER(_Config)], I32),
+            "lancet_peer_blob_bytes": ([], ctypes.c_size_t),
+            "lancet_peer_export": ([P, P], I32),
+            "lancet_peer_import": ([P, P], I32),
             "lancet_destroy": ([P], I32),
             "lancet_set_flags": ([P, U32], I32),
             "lancet_moe_forward": ([P, P, P, P, P, I32, I32, F32, I32, P, P, P, P, P], I32),
@@ -193,14 +198,28 @@ class Context:
     """
 
     def __init__(self, cfg: LayerConfig, world: int = 1, rank: int = 0, device: int | None = None,
-                 pg=None, local_group: LocalGroup | None = None):
+                 pg=None, local_group: LocalGroup | None = None, transport: str = "nccl"):
+        """transport: "nccl" (world > 1: NCCL grouped send/recv) or "peer" (copy engines over
+        CUDA IPC; the blobs are all-gathered over the torch process group `pg`)."""
         lib = load_library()
         self.cfg = cfg
         self.world, self.rank = world, rank
         self.device = torch.cuda.current_device() if device is None else device
         self._p = ctypes.c_void_p()
         c = cfg._c()
-        if local_group is not None:
+        if transport == "peer":
+            import torch.distributed as dist
+            _check(lib.lancet_create_peer(ctypes.byref(self._p), world, rank, self.device, ctypes.byref(c)))
+            nb = lib.lancet_peer_blob_bytes()
+            blob = ctypes.create_string_buffer(nb)
+            _check(lib.lancet_peer_export(self._p, blob), self._p)
+            blobs = [bytes(blob.raw)]
+            if world > 1:
+                blobs = [None] * world
+                dist.all_gather_object(blobs, bytes(blob.raw), group=pg)
+            allb = ctypes.create_string_buffer(b"".join(blobs), nb * world)
+            _check(lib.lancet_peer_import(self._p, allb), self._p)
+        elif local_group is not None:
             _check(lib.lancet_create_local(ctypes.byref(self._p), local_group._p, rank, self.device,
                                            ctypes.byref(c)))
         else:

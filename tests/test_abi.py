@@ -89,3 +89,17 @@ def test_local_group_lifecycle_without_device(lib):
     g = ctypes.c_void_p()
     assert lib.lancet_local_group_create(ctypes.byref(g), 2) == 0
     assert lib.lancet_local_group_destroy(g) == 0
+
+
+def test_binding_flag_values_match_the_header():
+    # every LANCET_FLAG_* of the header has the same value in the Python binding
+    from paper_2404_19429_b200 import lancet
+    src = re.sub(r"/\*.*?\*/", "", open(HEADER).read(), flags=re.S)
+    flags = dict((name, 1 << int(bit)) for name, bit in
+                 re.findall(r"LANCET_FLAG_([A-Z_0-9]+)\s*=\s*1u\s*<<\s*(\d+)", src))
+    assert len(flags) >= 10
+    for name, val in flags.items():
+        assert getattr(lancet, "FLAG_" + name) == val, name
+    assert len(set(flags.values())) == len(flags), "flag bits collide"
+    comm = re.search(r"#define\s+LANCET_COMM_SMS\s+(\d+)", src)
+    assert comm and int(comm.group(1)) > 0

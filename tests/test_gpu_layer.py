@@ -248,3 +248,28 @@ def test_force_ep_nccl_path_matches_single_gpu_path(n, act):
     o = run_oracle(ins, k, 1.0, n, act=act)
     for key in ("y", "dx") + keys:
         assert normwise(ep[key], o[key]) <= TOL["bf16"], key
+
+
+def test_programmatic_dependent_launch_is_bitwise_neutral():
+    # PDL lets a kernel start while its predecessor drains; every kernel waits before touching
+    # memory, so the results must be bitwise those of plain stream ordering
+    from paper_2404_19429_b200 import FLAG_NO_PDL
+    T, d, f, E, k = 2500, 256, 512, 8, 2
+    ins = inputs(T, d, f, E, k, beta=0.5, seed=31)
+    a = run_gpu(ins, E, k, 1.0, 2)
+    b = run_gpu(ins, E, k, 1.0, 2, flags=FLAG_NO_PDL)
+    for key in ("idx", "slot", "y", "dx", "dwg", "dw1", "dw2"):
+        assert np.array_equal(a[key], b[key]), key
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+def test_force_ep_renormalized_and_fp32(dtype):
+    # the NCCL path with renormalised combine weights, and with fp32 storage (SIMT GEMMs)
+    from paper_2404_19429_b200 import FLAG_FORCE_EP, FLAG_RENORMALIZE
+    T, d, f, E, k = 1100, 128, 256, 4, 2
+    ins = inputs(T, d, f, E, k, beta=0.5, dtype=dtype, seed=5)
+    g = run_gpu(ins, E, k, 1.0, 3, dtype=dtype, flags=FLAG_FORCE_EP | FLAG_RENORMALIZE)
+    o = run_oracle(ins, k, 1.0, 3, renorm=True)
+    assert_routing_exact(g, o)
+    for key in ("y", "dx", "dwg", "dw1", "dw2"):
+        assert normwise(g[key], o[key]) <= TOL[dtype], key
