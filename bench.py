@@ -71,7 +71,7 @@ def workload(a, world):
                     f"n_chunks={a.chunks} bf16",
         "tokens_per_gpu": a.tokens, "d_model": a.d, "d_ffn": a.f, "experts": a.experts,
         "top_k": a.k, "capacity_factor": a.cf, "n_chunks": a.chunks, "routing_skew_beta": a.beta,
-        "parallelism": f"ep{world}" + (f" ({a.transport} all-to-all)" if world > 1 else "")
+        "parallelism": f"ep{world}" + (f" ({a.transport} all-to-all)" if world > 1 or a.transport == "peer" else "")
                        + (" all ranks on one GPU" if getattr(a, "same_device", False) else ""),
         "global_batch_tokens": a.tokens * world,
         "l2": "inputs larger than L2: per-step working set >= 1.4 GiB vs 126 MB L2 (no flush)",
@@ -360,7 +360,7 @@ def run_lancet(a, world, rank, local_rank):
                              max_k=a.k, max_chunks=max(8, a.chunks), dtype="bf16", flags=flags)
     ctx = lancet.Context(cfg, world=world, rank=rank, device=local_rank,
                          pg=dist.group.WORLD if world > 1 else None,
-                         transport=a.transport if world > 1 else "nccl")
+                         transport=a.transport)
     stream = torch.cuda.current_stream()
     y = torch.empty_like(x)
     dx = torch.empty_like(x)
@@ -405,7 +405,7 @@ def run_lancet(a, world, rank, local_rank):
     f_l, b_l = ctx.launch_counts()
     send, recv, C = ctx.counts(a.chunks)
     rows_expert = int(recv.sum())                     # rows this rank's experts processed
-    ep = world > 1 or bool(flags & lancet.FLAG_FORCE_EP)      # expert-parallel path (a2a on)
+    ep = world > 1 or bool(flags & lancet.FLAG_FORCE_EP) or a.transport == "peer"   # a2a on
     exposed_ms, comm_ms = exposure_per_step(tl, a.steps) if ep else (0.0, 0.0)
     exposed_ms = max_over_ranks(exposed_ms)
 

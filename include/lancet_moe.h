@@ -96,8 +96,9 @@ enum {
     LANCET_FLAG_FORCE_EP = 1u << 9      /* run the expert-parallel path (chunked NCCL
                                            exchanges, S1/S2 scheduler) even at world 1, over a
                                            one-rank NCCL communicator (lancet_create needs an
-                                           NCCL id); set at creation.  Exercises the NCCL path
-                                           on a single GPU                                    */
+                                           NCCL id); fixed at creation (lancet_set_flags keeps
+                                           the creation bit).  Exercises the NCCL path on a
+                                           single GPU                                         */
 };
 
 typedef struct {

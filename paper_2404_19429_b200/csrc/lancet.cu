@@ -685,8 +685,8 @@ LANCET_API lancet_status lancet_destroy(lancet_ctx* c)
 LANCET_API lancet_status lancet_set_flags(lancet_ctx* c, uint32_t flags)
 {
     if (!c) return fail(nullptr, LANCET_ERR_ARG, "ctx is NULL");
-    if ((flags & LANCET_FLAG_FORCE_EP) != (c->cfg.flags & LANCET_FLAG_FORCE_EP))
-        return fail(c, LANCET_ERR_ARG, "FORCE_EP must be set at creation");
+    // FORCE_EP is fixed at creation (the workspace layout depends on it): keep the creation bit
+    flags = (flags & ~(uint32_t)LANCET_FLAG_FORCE_EP) | (c->cfg.flags & LANCET_FLAG_FORCE_EP);
     if ((flags & LANCET_FLAG_RENORMALIZE) != (c->cfg.flags & LANCET_FLAG_RENORMALIZE) && c->world > 1)
         return fail(c, LANCET_ERR_ARG, "RENORMALIZE must be set at creation (checked across ranks)");
     c->cfg.flags = flags;

@@ -33,7 +33,7 @@ def inputs(T, d, f, E, k, beta=0.5, dtype="bf16", seed=0, G=1, rank=0):
 
 
 def run_gpu(ins, E, k, cf, n, dtype="bf16", act="gelu_tanh", flags=0, backward=True,
-            max_tokens=None, ctx=None):
+            max_tokens=None, ctx=None, transport="nccl"):
     from paper_2404_19429_b200 import lancet
     T, d = ins["x"].shape
     f = ins["w1"].shape[1]
@@ -42,7 +42,7 @@ def run_gpu(ins, E, k, cf, n, dtype="bf16", act="gelu_tanh", flags=0, backward=T
     if own:
         cfg = lancet.LayerConfig(d_model=d, d_ffn=f, n_experts=E, max_tokens=max_tokens or T,
                                  max_k=k, max_chunks=8, dtype=dtype, act=act, flags=flags)
-        ctx = lancet.Context(cfg)
+        ctx = lancet.Context(cfg, transport=transport)
     x = to_dev(ins["x"], tdt)
     wg = to_dev(ins["wg"], torch.float32)
     w1 = to_dev(ins["w1"], tdt)

@@ -229,8 +229,10 @@ def test_fused_gate_backward_matches_two_kernel_path(T, d, E, k, dtype):
         assert normwise(fu[key], o[key]) <= TOL[dtype], key
 
 
-@pytest.mark.parametrize("n,act", [(1, "gelu_tanh"), (4, "gelu_tanh"), (3, "identity_expert")])
-def test_force_ep_nccl_path_matches_single_gpu_path(n, act):
+@pytest.mark.parametrize("n,act,transport", [(1, "gelu_tanh", "nccl"), (4, "gelu_tanh", "nccl"),
+                                             (3, "identity_expert", "nccl"), (4, "gelu_tanh", "peer"),
+                                             (2, "identity_expert", "peer")])
+def test_force_ep_nccl_path_matches_single_gpu_path(n, act, transport):
     # the expert-parallel path (counts exchange, per-chunk grouped NCCL send/recv over a
     # one-rank communicator, S1/S2 chunk scheduler, per-chunk expert GEMMs) on one GPU: rows are
     # independent and K orders equal, so y / dx / routing are bitwise those of the single-GPU
@@ -238,7 +240,9 @@ def test_force_ep_nccl_path_matches_single_gpu_path(n, act):
     from paper_2404_19429_b200 import FLAG_FORCE_EP
     T, d, f, E, k = 2000, 256, 512, 8, 2
     ins = inputs(T, d, f, E, k, beta=0.5, seed=77 + n)
-    ep = run_gpu(ins, E, k, 1.0, n, act=act, flags=FLAG_FORCE_EP)
+    # "peer": the copy-engine transport over a one-rank peer group (self pulls)
+    ep = run_gpu(ins, E, k, 1.0, n, act=act, flags=FLAG_FORCE_EP if transport == "nccl" else 0,
+                 transport=transport)
     one = run_gpu(ins, E, k, 1.0, n, act=act)
     for key in ("idx", "slot", "y", "dx"):
         assert np.array_equal(ep[key], one[key]), key
