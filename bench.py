@@ -50,8 +50,9 @@ def parse():
     ap.add_argument("--flags", type=int, default=0, help="extra LANCET_FLAG_* bits")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--transport", choices=["nccl", "peer"], default="nccl",
-                    help="world > 1: NCCL grouped send/recv, or copy-engine pulls over CUDA IPC")
+    ap.add_argument("--transport", choices=["auto", "nccl", "peer"], default="auto",
+                    help="world > 1: NCCL grouped send/recv, copy-engine pulls over CUDA IPC, or "
+                         "auto (peer if every rank can set it up, else NCCL)")
     ap.add_argument("--same-device", action="store_true",
                     help="all ranks on GPU 0 (peer transport, gloo process group): a multi-process "
                          "test of the exchange machinery on one GPU, not a scaling measurement")
@@ -71,7 +72,8 @@ def workload(a, world):
                     f"n_chunks={a.chunks} bf16",
         "tokens_per_gpu": a.tokens, "d_model": a.d, "d_ffn": a.f, "experts": a.experts,
         "top_k": a.k, "capacity_factor": a.cf, "n_chunks": a.chunks, "routing_skew_beta": a.beta,
-        "parallelism": f"ep{world}" + (f" ({a.transport} all-to-all)" if world > 1 or a.transport == "peer" else "")
+        "parallelism": f"ep{world}" + (f" ({getattr(a, 'transport_used', a.transport)} all-to-all)"
+                                       if world > 1 or a.transport == "peer" else "")
                        + (" all ranks on one GPU" if getattr(a, "same_device", False) else ""),
         "global_batch_tokens": a.tokens * world,
         "l2": "inputs larger than L2: per-step working set >= 1.4 GiB vs 126 MB L2 (no flush)",
@@ -335,6 +337,36 @@ def run_e2e(a, world, ins, ctx, wg, w1, w2, dwg, dw1, dw2, dev, barrier, max_ove
                     "timed region (first H2D to last D2H)"}
 
 
+def make_context(a, lancet, cfg, world, rank, local_rank, dev):
+    """transport auto (world > 1): the copy-engine peer transport when every rank can set it up
+    (CUDA IPC between all ranks' devices, stream memory operations), else NCCL -- decided
+    collectively so all ranks use the same one."""
+    import torch
+    import torch.distributed as dist
+    pg = dist.group.WORLD if world > 1 else None
+    if a.transport != "auto":
+        a.transport_used = a.transport
+        return lancet.Context(cfg, world=world, rank=rank, device=local_rank, pg=pg, transport=a.transport)
+    if world == 1:
+        a.transport_used = "none"
+        return lancet.Context(cfg, world=1, rank=0, device=local_rank)
+    ctx, ok = None, 1.0
+    try:
+        ctx = lancet.Context(cfg, world=world, rank=rank, device=local_rank, pg=pg, transport="peer")
+    except Exception as e:  # noqa: BLE001
+        print(f"rank {rank}: peer transport unavailable ({e}); voting for NCCL", file=sys.stderr)
+        ok = 0.0
+    t = torch.tensor([ok], dtype=torch.float64, device="cpu" if a.same_device else dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    if t.item() == 1.0:
+        a.transport_used = "peer"
+        return ctx
+    if ctx is not None:
+        ctx.close()
+    a.transport_used = "nccl"
+    return lancet.Context(cfg, world=world, rank=rank, device=local_rank, pg=pg, transport="nccl")
+
+
 def run_lancet(a, world, rank, local_rank):
     import torch
     import torch.distributed as dist
@@ -358,9 +390,7 @@ def run_lancet(a, world, rank, local_rank):
     flags = (0 if a.no_timeline else lancet.FLAG_TIMELINE) | a.flags
     cfg = lancet.LayerConfig(d_model=a.d, d_ffn=a.f, n_experts=a.experts, max_tokens=a.tokens,
                              max_k=a.k, max_chunks=max(8, a.chunks), dtype="bf16", flags=flags)
-    ctx = lancet.Context(cfg, world=world, rank=rank, device=local_rank,
-                         pg=dist.group.WORLD if world > 1 else None,
-                         transport=a.transport)
+    ctx = make_context(a, lancet, cfg, world, rank, local_rank, dev)
     stream = torch.cuda.current_stream()
     y = torch.empty_like(x)
     dx = torch.empty_like(x)

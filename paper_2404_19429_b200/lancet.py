@@ -208,17 +208,7 @@ class Context:
         self._p = ctypes.c_void_p()
         c = cfg._c()
         if transport == "peer":
-            import torch.distributed as dist
-            _check(lib.lancet_create_peer(ctypes.byref(self._p), world, rank, self.device, ctypes.byref(c)))
-            nb = lib.lancet_peer_blob_bytes()
-            blob = ctypes.create_string_buffer(nb)
-            _check(lib.lancet_peer_export(self._p, blob), self._p)
-            blobs = [bytes(blob.raw)]
-            if world > 1:
-                blobs = [None] * world
-                dist.all_gather_object(blobs, bytes(blob.raw), group=pg)
-            allb = ctypes.create_string_buffer(b"".join(blobs), nb * world)
-            _check(lib.lancet_peer_import(self._p, allb), self._p)
+            self._create_peer(lib, c, world, rank, pg)
         elif local_group is not None:
             _check(lib.lancet_create_local(ctypes.byref(self._p), local_group._p, rank, self.device,
                                            ctypes.byref(c)))
@@ -232,6 +222,33 @@ class Context:
                                      ctypes.byref(c)))
         self.E_l = cfg.n_experts // world
         self._last = None
+
+    def _create_peer(self, lib, c, world, rank, pg):
+        """Copy-engine peer transport: create, export the IPC blob, all-gather the blobs over
+        `pg`, import.  Every rank takes part in both gathers even if its own step failed, so a
+        failure anywhere raises on every rank (no rank is left waiting in a collective)."""
+        import torch.distributed as dist
+
+        def agree(ok: bool, what: str):
+            if world > 1:
+                flags = [None] * world
+                dist.all_gather_object(flags, bool(ok), group=pg)
+                ok = all(flags)
+            if not ok:
+                self.close()
+                raise LancetError(6, f"peer transport: {what} failed on some rank")
+
+        nb = lib.lancet_peer_blob_bytes()
+        blob = ctypes.create_string_buffer(nb)
+        ok = lib.lancet_create_peer(ctypes.byref(self._p), world, rank, self.device, ctypes.byref(c)) == 0
+        ok = ok and lib.lancet_peer_export(self._p, blob) == 0
+        agree(ok, "create / export")
+        blobs = [bytes(blob.raw)]
+        if world > 1:
+            blobs = [None] * world
+            dist.all_gather_object(blobs, bytes(blob.raw), group=pg)
+        allb = ctypes.create_string_buffer(b"".join(blobs), nb * world)
+        agree(lib.lancet_peer_import(self._p, allb) == 0, "import")
 
     # -- lifecycle --------------------------------------------------------------------------
     def close(self):
