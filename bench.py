@@ -219,7 +219,8 @@ def op_stats(tl, steps):
 def exposure_per_step(tl, steps):
     from paper_2404_19429_b200.lancet import exposed_comm_us
     d = exposed_comm_us(tl)
-    return d["exposed_us"] / steps / 1000.0, d["comm_us"] / steps / 1000.0
+    return (d["exposed_us"] / steps / 1000.0, d["comm_us"] / steps / 1000.0,
+            d["exposed_counts_us"] / steps / 1000.0, d["exposed_data_us"] / steps / 1000.0)
 
 
 def run_e2e(a, world, ins, ctx, wg, w1, w2, dwg, dw1, dw2, dev, barrier, max_over_ranks):
@@ -436,7 +437,7 @@ def run_lancet(a, world, rank, local_rank):
     send, recv, C = ctx.counts(a.chunks)
     rows_expert = int(recv.sum())                     # rows this rank's experts processed
     ep = world > 1 or bool(flags & lancet.FLAG_FORCE_EP) or a.transport == "peer"   # a2a on
-    exposed_ms, comm_ms = exposure_per_step(tl, a.steps) if ep else (0.0, 0.0)
+    exposed_ms, comm_ms, exp_counts_ms, exp_data_ms = exposure_per_step(tl, a.steps) if ep else (0.0,) * 4
     exposed_ms = max_over_ranks(exposed_ms)
 
     # ---- unoverlapped baseline (world > 1): serial schedule, one stream, chunks merged -------
@@ -508,6 +509,7 @@ def run_lancet(a, world, rank, local_rank):
         "data": "synthetic (seeded; synthetic/ recipe, DESIGN.md)",
         "config": workload(a, world),
         "exposed_a2a_ms": exposed_ms, "a2a_ms_on_comm_lane": comm_ms,
+        "exposed_a2a_split_ms": {"counts": exp_counts_ms, "data": exp_data_ms},
         "unoverlapped_a2a_ms": unoverlapped_ms,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": pk["bf16_sus"], "unit": "TFLOP/s",
                      "frac": achieved / pk["bf16_sus"], "traffic": traffic,

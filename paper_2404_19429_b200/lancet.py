@@ -349,14 +349,21 @@ def exposed_comm_us(timeline) -> dict:
             else:
                 out.append([a, b])
         return out
+    def exposed(iv, cover):
+        tot = sum(b - a for a, b in iv)
+        ov = 0.0
+        for a, b in iv:
+            for c, d in cover:
+                lo, hi = max(a, c), min(b, d)
+                if hi > lo:
+                    ov += hi - lo
+        return tot, tot - ov
+
     comm = union([(r["start_us"], r["end_us"]) for r in timeline if r["lane"] == 1])
     comp = union([(r["start_us"], r["end_us"]) for r in timeline if r["lane"] != 1])
-    tot_comm = sum(b - a for a, b in comm)
-    overlap = 0.0
-    for a, b in comm:
-        for c, d in comp:
-            lo, hi = max(a, c), min(b, d)
-            if hi > lo:
-                overlap += hi - lo
-    return dict(exposed_us=tot_comm - overlap, comm_us=tot_comm,
-                compute_us=sum(b - a for a, b in comp))
+    tot_comm, exp = exposed(comm, comp)
+    # split: the size exchange (C1) and the data exchanges (C2)
+    cnt = union([(r["start_us"], r["end_us"]) for r in timeline if r["lane"] == 1 and r["name"].startswith("a2a_counts")])
+    dat = union([(r["start_us"], r["end_us"]) for r in timeline if r["lane"] == 1 and not r["name"].startswith("a2a_counts")])
+    return dict(exposed_us=exp, comm_us=tot_comm, compute_us=sum(b - a for a, b in comp),
+                exposed_counts_us=exposed(cnt, comp)[1], exposed_data_us=exposed(dat, comp)[1])
