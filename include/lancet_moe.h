@@ -93,12 +93,14 @@ enum {
                                            each kernel may start while its stream predecessor
                                            drains; every kernel waits with griddepcontrol.wait
                                            before touching memory; ~1 % per step)            */
-    LANCET_FLAG_FORCE_EP = 1u << 9      /* run the expert-parallel path (chunked NCCL
+    LANCET_FLAG_FORCE_EP = 1u << 9,     /* run the expert-parallel path (chunked NCCL
                                            exchanges, S1/S2 scheduler) even at world 1, over a
                                            one-rank NCCL communicator (lancet_create needs an
                                            NCCL id); fixed at creation (lancet_set_flags keeps
                                            the creation bit).  Exercises the NCCL path on a
                                            single GPU                                         */
+    LANCET_FLAG_TIMELINE_GEMM_ONLY = 1u << 10 /* with TIMELINE: events around the expert GEMM
+                                           launches only (the least perturbing roofline pass) */
 };
 
 typedef struct {

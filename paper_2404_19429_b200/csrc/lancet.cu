@@ -116,6 +116,7 @@ struct OpScope {
     OpScope(lancet_ctx* ctx, const char* name, int lane, int chunk, cudaStream_t st) : c(ctx), s(st) {
         i = (size_t)-1;
         if (!(c->cfg.flags & LANCET_FLAG_TIMELINE)) return;
+        if ((c->cfg.flags & LANCET_FLAG_TIMELINE_GEMM_ONLY) && strncmp(name, "expert_", 7) != 0) return;
         if (c->tl_used + 2 > c->tl_events.size()) {
             for (int q = 0; q < 64; ++q) {
                 cudaEvent_t e;
