@@ -164,11 +164,11 @@ def oracle_threads():
 
 
 def calibrate_sample(a, budget_s):
-    """Largest power-of-two token sample whose oracle fwd+bwd fits in ~budget_s seconds."""
-    T = 256
+    """Largest power-of-two token sample (>= 32) whose oracle fwd+bwd fits in ~budget_s s."""
+    T = 64
     dt = oracle_step(a, T, a.seed)
     per_tok = dt / T
-    Ts = 256
+    Ts = 32
     while Ts * 2 <= a.tokens and per_tok * Ts * 2 <= budget_s:
         Ts *= 2
     return Ts, per_tok
