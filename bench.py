@@ -286,7 +286,7 @@ def run_e2e(a, world, ins, ctx, wg, w1, w2, dwg, dw1, dw2, dev, barrier, max_ove
     run(2)
     torch.cuda.synchronize()
     barrier()
-    ne = max(3, min(a.steps, 20))
+    ne = max(3, a.steps)
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record(comp)
     s_in.wait_event(f0)

@@ -24,7 +24,7 @@ constexpr int kRowAlign = 128;   // expert / (expert, chunk) row blocks start on
 constexpr int kMaxK = 8;         // top-k bound on the device side
 constexpr int kMaxChunks = 64;
 constexpr int kMaxExperts = 256;
-constexpr int kScanTile = 1024;  // tokens per block of the slot scan (K2)
+constexpr int kScanTile = 256;   // tokens per block of the slot scan (K2); >= kMaxExperts
 
 __host__ __device__ inline int round_up(int a, int b) { return (a + b - 1) / b * b; }
 __host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }

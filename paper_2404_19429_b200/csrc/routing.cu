@@ -454,7 +454,7 @@ gate_stream_kernel(const Elt* __restrict__ x, const float* __restrict__ wg, int 
 }
 
 // One block per kScanTile tokens.  smem: base[E] | wcnt[32][E] | wbal[32][E] | adm[E] | hist copy
-constexpr int kScanHistMax = 8192;   // ints of the staged tile histograms
+constexpr int kScanHistMax = 16384;  // ints of the staged tile histograms (64 KiB)
 __global__ void __launch_bounds__(kScanTile)
 slot_scan_kernel(const int* __restrict__ idx, int T, int k, int E, int C, int n,
                  const int* __restrict__ hist, int n_tiles, int* __restrict__ slot_out,
@@ -521,7 +521,7 @@ slot_scan_kernel(const int* __restrict__ idx, int T, int k, int E, int C, int n,
     __syncthreads();
     if (tid < E) {
         int run = 0;
-        for (int ww = 0; ww < 32; ++ww) {
+        for (int ww = 0; ww < kScanTile / 32; ++ww) {
             const int c = wcnt[ww * E + tid];
             wcnt[ww * E + tid] = run;
             run += c;

@@ -1,10 +1,12 @@
 """GPU parity of the MoE layer step (single rank) against the oracle, through the C-ABI.
 
-Sizes span several tiles of every kernel (gate blocks of 128 tokens, 1024-token scan tiles,
+Sizes span several tiles of every kernel (gate blocks of 64 tokens, 256-token scan tiles,
 128-row GEMM tiles) with ragged tails; BASELINE.json configs[1] (the bench workload) is
 checked at full size on sampled outputs."""
 import numpy as np
 import pytest
+
+import torch
 
 from gpu_harness import (TOL, assert_routing_exact, inputs, normwise, run_gpu, run_oracle)
 
@@ -22,7 +24,7 @@ def _lib():
 
 @pytest.mark.parametrize("T,d,E,k,beta,cf,n", [
     (64, 16, 4, 2, 0.5, 1.25, 2),          # BASELINE configs[0] per-rank shape, 64 tokens
-    (2500, 256, 8, 2, 0.5, 1.25, 3),       # 3 scan tiles, ragged
+    (2500, 256, 8, 2, 0.5, 1.25, 3),       # 10 scan tiles, ragged
     (3001, 96, 64, 4, 1.0, 1.0, 8),        # many experts, k=4, drops
     (777, 64, 3, 1, 0.0, 0.5, 5),          # odd E, top-1, capacity binding hard
     (1, 32, 8, 2, 0.5, 1.25, 1),           # single token
@@ -277,3 +279,37 @@ def test_force_ep_renormalized_and_fp32(dtype):
     assert_routing_exact(g, o)
     for key in ("y", "dx", "dwg", "dw1", "dw2"):
         assert normwise(g[key], o[key]) <= TOL[dtype], key
+
+
+def test_context_reuse_across_shapes_and_chunk_counts():
+    # one context, successive steps with different T and n: each equals a fresh context's run
+    from paper_2404_19429_b200 import lancet
+    d, f, E, k = 256, 512, 8, 2
+    cfg = lancet.LayerConfig(d_model=d, d_ffn=f, n_experts=E, max_tokens=3000, max_k=k, max_chunks=8)
+    ctx = lancet.Context(cfg)
+    for T, n in ((3000, 4), (1234, 1), (2999, 8), (64, 2)):
+        ins = inputs(T, d, f, E, k, beta=0.5, seed=T)
+        a = run_gpu(ins, E, k, 1.0, n, ctx=ctx)
+        b = run_gpu(ins, E, k, 1.0, n, max_tokens=3000)
+        for key in ("idx", "slot", "y", "dx", "dwg", "dw1", "dw2"):
+            assert np.array_equal(a[key], b[key]), (T, n, key)
+    ctx.close()
+
+
+def test_peer_context_requires_import():
+    # the peer transport refuses to run before its peers are mapped (ERR_STATE, nothing enqueued)
+    import ctypes
+    from paper_2404_19429_b200 import lancet
+    lib = lancet.load_library()
+    cfg = lancet.LayerConfig(d_model=128, d_ffn=256, n_experts=4, max_tokens=256, max_k=2)
+    p = ctypes.c_void_p()
+    assert lib.lancet_create_peer(ctypes.byref(p), 1, 0, 0, ctypes.byref(cfg._c())) == 0
+    x = torch.zeros(256, 128, dtype=torch.bfloat16, device="cuda")
+    wg = torch.zeros(128, 4, device="cuda")
+    w1 = torch.zeros(4, 256, 128, dtype=torch.bfloat16, device="cuda")
+    w2 = torch.zeros(4, 128, 256, dtype=torch.bfloat16, device="cuda")
+    y = torch.empty_like(x)
+    st = lib.lancet_moe_forward(p, x.data_ptr(), wg.data_ptr(), w1.data_ptr(), w2.data_ptr(), 256, 2,
+                                ctypes.c_float(1.0), 2, y.data_ptr(), None, None, None, None)
+    assert st == 5                                               # ERR_STATE
+    assert lib.lancet_destroy(p) == 0
