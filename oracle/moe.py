@@ -101,6 +101,80 @@ def assign_slots(idx: np.ndarray, E: int, C: int, used=None):
     return slot, used
 
 
+def importance_scores(logits: np.ndarray, idx: np.ndarray) -> np.ndarray:
+    """Batch Prioritized Routing's importance score: "the sum of top-k largest gating
+    scores".  Gating score = the softmax probability p (R3), so
+    s_t = sum_j p[t, idx[t,j]], evaluated in fp64 as
+
+        s_t = (sum_j exp(l[t, idx_j] - m_t)) / (sum_e exp(l[t, e] - m_t)),  m_t = max_e l[t, e],
+
+    both sums sequential (j in rank order, e ascending) -- DESIGN.md R16.  The score decides
+    integers (who is dropped), so both sides evaluate it in fp64 in this order."""
+    l64 = logits.astype(np.float64)
+    T, E = l64.shape
+    m = l64.max(axis=1)
+    Z = np.zeros(T)
+    for e in range(E):
+        Z = Z + np.exp(l64[:, e] - m)
+    num = np.zeros(T)
+    for j in range(idx.shape[1]):
+        num = num + np.exp(l64[np.arange(T), idx[:, j]] - m)
+    return num / Z
+
+
+def assign_slots_bpr(idx: np.ndarray, score: np.ndarray, E: int, C: int):
+    """Batch Prioritized Routing (riquelme2021bpr) in Lancet's
+    partition-after-gate mode (L270-L271, fig:part_after_gate): the router "sorts tokens in a
+    batch first by their importance score ... and then assigns tokens to experts. So tokens
+    with lower scores would be dropped first."  Step by step (R16):
+
+      1. order the tokens by (score descending, token index ascending);
+      2. walk the tokens in that order, each token's choices j in rank order; expert e admits
+         a pair while it holds fewer than C ("any excess tokens ... are discarded", L119);
+      3. slot = the pair's position among e's ADMITTED pairs in token-major order (R7/R8), so
+         that chunk c's rows of e stay one contiguous slot range (the partition happens
+         after the gate; capacity passing is again the prefix at chunk boundaries).
+
+    Returns slot [T,k] int32 (-1 dropped)."""
+    T, k = idx.shape
+    order = sorted(range(T), key=lambda t: (-score[t], t))
+    used = [0] * E
+    admitted = np.zeros((T, k), dtype=bool)
+    for t in order:
+        for j in range(k):
+            e = int(idx[t, j])
+            if used[e] < C:
+                admitted[t, j] = True
+                used[e] += 1
+    slot = np.full((T, k), DROPPED, dtype=np.int32)
+    nxt = [0] * E
+    for t in range(T):
+        for j in range(k):
+            if admitted[t, j]:
+                e = int(idx[t, j])
+                slot[t, j] = nxt[e]
+                nxt[e] += 1
+    return slot
+
+
+def route_micro_bpr(idx: np.ndarray, score: np.ndarray, E: int, C: int, n_chunks: int):
+    """BPR applied per micro-batch with capacity passing -- what partitioning BEFORE the gate
+    would do (diagnostic only).  PAPER.md L270: "Splitting along batch dimension would thus
+    cause differences in token dropping" -- the reason BPR only allows partitioning after the
+    MoE gate.  Chunk c sorts only its own tokens and gets the capacity chunks 0..c-1 left."""
+    bounds = chunk_bounds(idx.shape[0], n_chunks)
+    used = [0] * E
+    admitted = np.zeros(idx.shape, dtype=bool)
+    for c in range(n_chunks):
+        for t in sorted(range(bounds[c], bounds[c + 1]), key=lambda t: (-score[t], t)):
+            for j in range(idx.shape[1]):
+                e = int(idx[t, j])
+                if used[e] < C:
+                    admitted[t, j] = True
+                    used[e] += 1
+    return admitted
+
+
 def chunk_bounds(T: int, n: int) -> list[int]:
     """Split T tokens into n contiguous chunks whose sizes differ by at most one, larger
     first (R9).  Returns the n+1 boundaries [t_0=0, ..., t_n=T]."""
@@ -226,11 +300,13 @@ class LayerResult:
     saved: dict = field(default_factory=dict)   # (rank, expert) -> (t, j, a, h, o)
 
 
-def route_rank(x, wg, k, cf, n_chunks, renormalize=False, gate_fp64=False) -> RankRouting:
+def route_rank(x, wg, k, cf, n_chunks, renormalize=False, gate_fp64=False,
+               gate="switch") -> RankRouting:
     """Routing of one rank's local batch (routing never crosses ranks: the gate is
     replicated, and C is per device).  `gate_fp64` replaces the R1 fp32
     chain by an fp64 product -- used only by the finite-difference pins of the backward,
-    which need a gate that is smooth at the 1e-6 scale."""
+    which need a gate that is smooth at the 1e-6 scale.  `gate`: "switch" (token-major
+    admission, R7) or "bpr" (Batch Prioritized Routing, assign_slots_bpr, R16)."""
     T = x.shape[0]
     E = wg.shape[1]
     if gate_fp64:
@@ -241,7 +317,12 @@ def route_rank(x, wg, k, cf, n_chunks, renormalize=False, gate_fp64=False) -> Ra
     p = softmax(logits)
     w = combine_weights(p, idx, renormalize)
     C = capacity(T, k, E, cf)
-    slot, _ = assign_slots(idx, E, C)
+    if gate == "bpr":
+        slot = assign_slots_bpr(idx, importance_scores(logits, idx), E, C)
+    elif gate == "switch":
+        slot, _ = assign_slots(idx, E, C)
+    else:
+        raise ValueError(gate)
     counts = chunk_counts(idx, slot, E, n_chunks)
     return RankRouting(logits, idx, p, w, slot, C, counts)
 
@@ -252,7 +333,7 @@ def expert_weights(w1_ranks, w2_ranks, e, E_l):
 
 
 def forward(xs, wg, w1_ranks, w2_ranks, k, cf, n_chunks, act="gelu_tanh",
-            renormalize=False, token_subset=None, gate_fp64=False) -> LayerResult:
+            renormalize=False, token_subset=None, gate_fp64=False, gate="switch") -> LayerResult:
     """The MoE layer forward over G = len(xs) ranks.
 
     xs[r]: [T_r, d] tokens of rank r; w1_ranks[r]: [E_l, f, d], w2_ranks[r]: [E_l, d, f].
@@ -270,7 +351,7 @@ def forward(xs, wg, w1_ranks, w2_ranks, k, cf, n_chunks, act="gelu_tanh",
     E_l = E // G
     res = LayerResult(routing=[], y=[])
     for r in range(G):
-        rt = route_rank(xs[r], wg, k, cf, n_chunks, renormalize, gate_fp64)
+        rt = route_rank(xs[r], wg, k, cf, n_chunks, renormalize, gate_fp64, gate)
         res.routing.append(rt)
         T, d = xs[r].shape
         keep = np.zeros(T, dtype=bool)
