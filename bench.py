@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--beta", type=float, default=0.25)
     ap.add_argument("--seed", type=int, default=2024)
     ap.add_argument("--flags", type=int, default=0, help="extra LANCET_FLAG_* bits")
+    ap.add_argument("--gate", choices=["switch", "bpr"], default="switch",
+                    help="capacity admission: token-major top-k (Switch/GShard-style) or Batch "
+                         "Prioritized Routing (PAPER.md L270; LANCET_FLAG_GATE_BPR)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--transport", choices=["auto", "nccl", "peer"], default="auto",
@@ -71,9 +74,10 @@ def workload(a, world):
     return {
         "workload": f"GPT-MoE layer fwd+bwd: d_model={a.d} ffn={a.f} experts={a.experts} "
                     f"({a.experts // world}/GPU) top-{a.k} cf={a.cf} {a.tokens} tokens/GPU "
-                    f"n_chunks={a.chunks} bf16",
+                    f"n_chunks={a.chunks} bf16" + (" gate=BPR" if a.gate == "bpr" else ""),
         "tokens_per_gpu": a.tokens, "d_model": a.d, "d_ffn": a.f, "experts": a.experts,
         "top_k": a.k, "capacity_factor": a.cf, "n_chunks": a.chunks, "routing_skew_beta": a.beta,
+        "gate": a.gate,
         "parallelism": f"ep{world}" + (f" ({getattr(a, 'transport_used', a.transport)} all-to-all)"
                                        if world > 1 or a.transport == "peer" else "")
                        + (" all ranks on one GPU" if getattr(a, "same_device", False) else ""),
@@ -149,7 +153,8 @@ def oracle_step(a, T, seed):
     sh = S.LayerShape(T=T, d=a.d, f=a.f, E=a.experts, G=1, k=a.k, cf=a.cf, n_chunks=1)
     ins = S.gen_rank_inputs(seed, 0, sh, beta=a.beta)
     t0 = time.perf_counter()
-    fwd = moe.forward([ins["x"]], ins["wg"], [ins["w1"]], [ins["w2"]], a.k, a.cf, a.chunks)
+    fwd = moe.forward([ins["x"]], ins["wg"], [ins["w1"]], [ins["w2"]], a.k, a.cf, a.chunks,
+                      gate=a.gate)
     moe.backward(fwd, [ins["x"]], ins["wg"], [ins["w1"]], [ins["w2"]], [ins["dy"]])
     return time.perf_counter() - t0
 
@@ -398,6 +403,8 @@ def run_lancet(a, world, rank, local_rank):
     # launch); the per-op breakdown, the GEMM roofline and the exposure come from a second,
     # instrumented pass of the same K steps right after it
     flags = a.flags & ~lancet.FLAG_TIMELINE
+    if a.gate == "bpr":
+        flags |= lancet.FLAG_GATE_BPR
     cfg = lancet.LayerConfig(d_model=a.d, d_ffn=a.f, n_experts=a.experts, max_tokens=a.tokens,
                              max_k=a.k, max_chunks=max(8, a.chunks), dtype="bf16", flags=flags)
     ctx = make_context(a, lancet, cfg, world, rank, local_rank, dev)

@@ -99,8 +99,18 @@ enum {
                                            NCCL id); fixed at creation (lancet_set_flags keeps
                                            the creation bit).  Exercises the NCCL path on a
                                            single GPU                                         */
-    LANCET_FLAG_TIMELINE_GEMM_ONLY = 1u << 10 /* with TIMELINE: events around the expert GEMM
+    LANCET_FLAG_TIMELINE_GEMM_ONLY = 1u << 10,/* with TIMELINE: events around the expert GEMM
                                            launches only (the least perturbing roofline pass) */
+    LANCET_FLAG_GATE_BPR = 1u << 11     /* Batch Prioritized Routing (DESIGN.md
+                                           R16) instead of token-major admission: the pairs of
+                                           each expert are admitted by the token's importance
+                                           score s_t = sum_j p[t, idx_tj] (fp64; descending,
+                                           ties to the lower token), so lower scores are dropped
+                                           first; admitted pairs then take token-major slots.
+                                           The gate sees the whole local batch and the chunks
+                                           partition after it (fig:part_after_gate, L271), so
+                                           chunked == unchunked as with the Switch gate.
+                                           Costs two more routing kernels per forward        */
 };
 
 typedef struct {

@@ -73,6 +73,8 @@ struct lancet_ctx {
     int rows_src = 0;
     float* logits = nullptr;  int* idx = nullptr;  float* w = nullptr;  int* slot = nullptr;
     int* hist = nullptr;  int* S = nullptr;  int* send_rows = nullptr;  int* send_off = nullptr;
+    double* bpr_score = nullptr;  int* bpr_list = nullptr;  unsigned char* bpr_adm = nullptr;
+    int* bpr_hist = nullptr;  int* bpr_meta = nullptr;   // Batch Prioritized Routing scratch (R16)
     void* xs = nullptr;        // [rows_src][d]  dispatch / send buffer
     void* comb = nullptr;      // [rows_src][d]  combined expert outputs (world > 1)
     void* dcomb = nullptr;     // [rows_src][d]  grad of expert outputs (source side)

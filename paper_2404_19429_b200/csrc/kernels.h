@@ -43,8 +43,16 @@ struct RouteArgs {
     int* S;               // [E][n+1] out: S[e][c] = min(C, P_e(t_c)) (capacity state)
     int* send_rows;       // [E]      out: admitted rows per expert
     int* send_off;        // [E]      out: 128-aligned packed row offset of expert e
+    // Batch Prioritized Routing (R16; bpr != 0): scratch of the three-pass admission
+    int bpr;
+    double* score;        // [T]      importance score (fp64)
+    int* list;            // [T*k]    pair ids grouped by expert, token order
+    unsigned char* bpr_adm; // [T*k]  1 = admitted by priority
+    int* hist2;           // [n_tiles][E] admitted pairs per token tile
+    int* bpr_meta;        // [E]      pairs routed to e
 };
-// Enqueues memset(hist) + K1 + K2.  Returns the number of kernels launched.
+// Enqueues memset(hist) + K1 + K2 (K2 = three kernels under BPR).  Returns the number of kernels
+// launched.
 int launch_routing(const RouteArgs& a, bool is_bf16, cudaStream_t s);
 
 // ---- K3..K6: dispatch / combine (dispatch.cu) --------------------------------------------

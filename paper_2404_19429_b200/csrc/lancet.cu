@@ -293,6 +293,11 @@ lancet_status create_common(lancet_ctx* c, int world, int rank, int device, cons
     AL(c->w, sizeof(float) * (size_t)T * K);
     AL(c->slot, sizeof(int) * (size_t)T * K);
     AL(c->hist, sizeof(int) * (size_t)n_tiles * E);
+    AL(c->bpr_score, sizeof(double) * (size_t)T);
+    AL(c->bpr_list, sizeof(int) * (size_t)T * K);
+    AL(c->bpr_adm, (size_t)T * K);
+    AL(c->bpr_hist, sizeof(int) * (size_t)n_tiles * E);
+    AL(c->bpr_meta, sizeof(int) * E);
     AL(c->S, sizeof(int) * (size_t)E * (kMaxChunks + 1));
     AL(c->send_rows, sizeof(int) * E);
     AL(c->send_off, sizeof(int) * E);
@@ -730,6 +735,9 @@ LANCET_API lancet_status lancet_moe_forward(lancet_ctx* c, const void* x, const 
     ra.renorm = (c->cfg.flags & LANCET_FLAG_RENORMALIZE) ? 1 : 0;
     ra.logits = c->logits; ra.idx = c->idx; ra.w = c->w; ra.slot = c->slot; ra.hist = c->hist;
     ra.S = c->S; ra.send_rows = c->send_rows; ra.send_off = c->send_off;
+    ra.bpr = (c->cfg.flags & LANCET_FLAG_GATE_BPR) ? 1 : 0;
+    ra.score = c->bpr_score; ra.list = c->bpr_list; ra.bpr_adm = c->bpr_adm; ra.hist2 = c->bpr_hist;
+    ra.bpr_meta = c->bpr_meta;
     DispatchArgs da{T, k, d, E, c->idx, c->slot, c->w, c->send_off, c->send_rows};
 
     if (!c->ep) {

@@ -453,12 +453,37 @@ gate_stream_kernel(const Elt* __restrict__ x, const float* __restrict__ wg, int 
     }
 }
 
-// One block per kScanTile tokens.  smem: base[E] | wcnt[32][E] | wbal[32][E] | adm[E] | hist copy
+// The slot scan (K2) runs in one of three modes:
+//   SCAN_SLOTS      token-major admission (R7): slot = P_e(t) if < C, capacity state S, offsets;
+//   SCAN_BPR_LIST   Batch Prioritized Routing, pass 1 (R16): the unclamped P_e(t) of every pair
+//                   places its pair id t*k+j at list[off_e + P_e(t)] (pairs grouped by expert, in
+//                   token order), and the token's fp64 importance score is written;
+//   SCAN_BPR_SLOTS  BPR pass 3: SCAN_SLOTS over the ADMITTED pairs only (bpr_adm), tile
+//                   histograms from bpr_select_kernel -- slot = token-major rank among admitted.
+enum ScanMode { SCAN_SLOTS = 0, SCAN_BPR_LIST = 1, SCAN_BPR_SLOTS = 2 };
+
+// BPR importance score ("the sum of top-k largest gating scores", R16):
+// s = (sum_j exp(l_idx_j - m)) / (sum_e exp(l_e - m)) in fp64, both sums sequential, m = the
+// top-1 logit (= the row maximum by R2).
+__device__ __forceinline__ double bpr_score(const float* __restrict__ lg, const int* mine, int E, int k)
+{
+    const double m = (double)lg[mine[0]];
+    double Z = 0.0, num = 0.0;
+    for (int e = 0; e < E; ++e) Z += exp((double)lg[e] - m);
+    for (int j = 0; j < k; ++j) num += exp((double)lg[mine[j]] - m);
+    return num / Z;
+}
+
+// One block per kScanTile tokens.  smem: base[E] | wcnt[32][E] | wbal[32][E] | adm[E] | offs[E] |
+// hist copy
 constexpr int kScanHistMax = 16384;  // ints of the staged tile histograms (64 KiB)
+template <int MODE>
 __global__ void __launch_bounds__(kScanTile)
 slot_scan_kernel(const int* __restrict__ idx, int T, int k, int E, int C, int n,
                  const int* __restrict__ hist, int n_tiles, int* __restrict__ slot_out,
-                 int* __restrict__ S, int* __restrict__ send_rows, int* __restrict__ send_off)
+                 int* __restrict__ S, int* __restrict__ send_rows, int* __restrict__ send_off,
+                 const float* __restrict__ logits, double* __restrict__ score, int* __restrict__ list,
+                 int* __restrict__ bpr_meta, const unsigned char* __restrict__ bpr_adm)
 {
     pdl_wait();   // programmatic dependent launch: predecessor's writes visible
     extern __shared__ int ism[];
@@ -466,12 +491,13 @@ slot_scan_kernel(const int* __restrict__ idx, int T, int k, int E, int C, int n,
     int* wcnt = base + E;
     unsigned* wbal = reinterpret_cast<unsigned*>(wcnt + 32 * E);
     int* adm = reinterpret_cast<int*>(wbal + 32 * E);
+    int* offs = adm + E;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int b = blockIdx.x;
 
     // the per-tile histograms, all loads in flight at once (a serial prefix of dependent global
     // loads would cost one L2 round trip per tile)
-    int* sh_h = adm + E;                                   // [n_tiles][E] when it fits
+    int* sh_h = offs + E;                                  // [n_tiles][E] when it fits
     const bool staged = n_tiles * E <= kScanHistMax;
     if (staged) {
         for (int i = tid; i < n_tiles * E; i += blockDim.x) sh_h[i] = hist[i];
@@ -482,7 +508,11 @@ slot_scan_kernel(const int* __restrict__ idx, int T, int k, int E, int C, int n,
         int s = 0;
         for (int q = 0; q < b; ++q) s += hs[q * E + tid];
         base[tid] = s;
-        if (b == 0) {
+        if (MODE == SCAN_BPR_LIST) {
+            int tot = 0;
+            for (int q = 0; q < n_tiles; ++q) tot += hs[q * E + tid];
+            adm[tid] = tot;                    // pairs routed to e (before any drop)
+        } else if (b == 0) {
             int tot = 0;
             for (int q = 0; q < n_tiles; ++q) tot += hs[q * E + tid];
             const int a = min(C, tot);
@@ -491,6 +521,14 @@ slot_scan_kernel(const int* __restrict__ idx, int T, int k, int E, int C, int n,
             S[tid * (n + 1) + n] = a;
             send_rows[tid] = a;
         }
+    }
+    if (MODE == SCAN_BPR_LIST) {
+        __syncthreads();
+        if (tid == 0) {
+            int o = 0;
+            for (int e = 0; e < E; ++e) { offs[e] = o; o += adm[e]; }
+        }
+        if (b == 0 && tid < E) bpr_meta[tid] = adm[tid];
     }
 
     const int t = b * kScanTile + tid;
@@ -501,7 +539,14 @@ slot_scan_kernel(const int* __restrict__ idx, int T, int k, int E, int C, int n,
         mine[j] = (valid && j < k) ? idx[(size_t)t * k + j] : -1;
         pre[j] = 0;
     }
-    const int cs = valid ? chunk_starting_at(T, n, t) : -1;
+    if (MODE == SCAN_BPR_LIST && valid) score[t] = bpr_score(logits + (size_t)t * E, mine, E, k);
+    if (MODE == SCAN_BPR_SLOTS) {
+        // dropped by priority: the pair takes no place in its expert's buffer
+#pragma unroll
+        for (int j = 0; j < kMaxK; ++j)
+            if (j < k && valid && !bpr_adm[(size_t)t * k + j]) mine[j] = -2;
+    }
+    const int cs = (MODE != SCAN_BPR_LIST && valid) ? chunk_starting_at(T, n, t) : -1;
     const bool warp_has_cs = __any_sync(0xffffffffu, cs >= 0);
     const unsigned lt = (1u << lane) - 1u;
     for (int e = 0; e < E; ++e) {
@@ -533,11 +578,18 @@ slot_scan_kernel(const int* __restrict__ idx, int T, int k, int E, int C, int n,
         for (int j = 0; j < kMaxK; ++j) {
             if (j < k) {
                 const int e = mine[j];
-                const int P = base[e] + wcnt[w * E + e] + pre[j];
-                slot_out[(size_t)t * k + j] = P < C ? P : -1;
+                if (MODE == SCAN_BPR_LIST) {
+                    list[offs[e] + base[e] + wcnt[w * E + e] + pre[j]] = t * k + j;
+                } else if (MODE == SCAN_BPR_SLOTS && e < 0) {
+                    slot_out[(size_t)t * k + j] = -1;
+                } else {
+                    const int P = base[e] + wcnt[w * E + e] + pre[j];
+                    slot_out[(size_t)t * k + j] = P < C ? P : -1;
+                }
             }
         }
     }
+    if (MODE == SCAN_BPR_LIST) return;
     if (cs >= 0) {
         for (int e = 0; e < E; ++e) {
             const int P = base[e] + wcnt[w * E + e] + __popc(wbal[w * E + e] & lt);
@@ -556,6 +608,147 @@ slot_scan_kernel(const int* __restrict__ idx, int T, int k, int E, int C, int n,
     }
 }
 
+// BPR pass 2 (R16): one block per expert.  Expert e's pairs sit in list[off_e, off_e + n_e) in
+// token order.  If n_e > C, an MSD radix select over the 64-bit patterns of the (positive)
+// fp64 scores (monotone in the score) finds the byte-granular prefix K* of the C-th largest
+// score and how many pairs sharing that prefix still fit; those go to the lower token indices
+// (ordered block scan).  The select starts at the highest byte where the smallest and largest
+// key differ (the scores share their exponent bytes) and stops as soon as the pairs sharing the
+// prefix all fit.  Writes bpr_adm for every pair of e and the per-tile admitted counts
+// hist2[tile][e] (every tile written: no memset needed).
+constexpr int kSelThreads = 1024;
+constexpr size_t kSelSmem = 200 * 1024;   // key cache + tile counts
+__global__ void __launch_bounds__(kSelThreads)
+bpr_select_kernel(const int* __restrict__ list, const int* __restrict__ bpr_meta,
+                  const double* __restrict__ score, int E, int k, int C, int n_tiles, int cap,
+                  unsigned char* __restrict__ bpr_adm, int* __restrict__ hist2)
+{
+    pdl_wait();
+    extern __shared__ unsigned long long kcache[];  // [cap] keys of the first cap pairs of e
+    int* tiles = reinterpret_cast<int*>(kcache + cap);   // [n_tiles] admitted pairs per token tile
+    __shared__ int hist[256];
+    __shared__ int wsum[kSelThreads / 32];
+    __shared__ unsigned long long wmin[kSelThreads / 32], wmax[kSelThreads / 32];
+    __shared__ unsigned long long s_prefix;
+    __shared__ int s_need, s_run, s_shift, s_done;
+    const int e = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    int off = 0;
+    for (int q = 0; q < e; ++q) off += bpr_meta[q];
+    const int ne = bpr_meta[e];
+    const int* L = list + off;
+    for (int q = tid; q < n_tiles; q += kSelThreads) tiles[q] = 0;
+    const bool all = ne <= C;
+    auto key_of = [&](int i) -> unsigned long long {
+        return i < cap ? kcache[i] : (unsigned long long)__double_as_longlong(score[L[i] / k]);
+    };
+    if (!all) {
+        // one gather pass stages the keys (the select passes and the admission re-read them;
+        // pairs beyond the cache are re-gathered from global memory) and finds min / max
+        unsigned long long mn = ~0ull, mx = 0ull;
+        for (int i = tid; i < ne; i += kSelThreads) {
+            const unsigned long long key = (unsigned long long)__double_as_longlong(score[L[i] / k]);
+            if (i < cap) kcache[i] = key;
+            mn = min(mn, key);
+            mx = max(mx, key);
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+            mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        }
+        if (lane == 0) { wmin[w] = mn; wmax[w] = mx; }
+        __syncthreads();
+        if (tid == 0) {
+            for (int q = 1; q < kSelThreads / 32; ++q) { mn = min(mn, wmin[q]); mx = max(mx, wmax[q]); }
+            mn = min(mn, wmin[0]); mx = max(mx, wmax[0]);
+            s_need = C;
+            s_run = 0;
+            if (mn == mx) {                    // one score for every pair: all ties
+                s_prefix = mn; s_shift = 0; s_done = 1;
+            } else {
+                const int hb = 63 - __clzll(mn ^ mx);          // highest differing bit
+                const int sh = (hb / 8) * 8;                    // first byte to select on
+                s_prefix = sh == 56 ? 0ull : (mn >> (sh + 8)) << (sh + 8);
+                s_shift = sh + 8;                               // bytes above are common
+                s_done = 0;
+            }
+        }
+        __syncthreads();
+        while (!s_done) {
+            const int shift = s_shift - 8;
+            for (int q = tid; q < 256; q += kSelThreads) hist[q] = 0;
+            __syncthreads();
+            const unsigned long long pre = s_prefix;
+            for (int i = tid; i < ne; i += kSelThreads) {
+                const unsigned long long key = key_of(i);
+                if (shift == 56 || (key >> (shift + 8)) == (pre >> (shift + 8)))
+                    atomicAdd(&hist[(key >> shift) & 255u], 1);
+            }
+            __syncthreads();
+            if (w == 0) {
+                // lane owns bins 255-8*lane .. 248-8*lane (descending); find the bin where the
+                // count of larger-or-equal keys reaches s_need
+                const int need = s_need;
+                int c[8], sum = 0;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) { c[q] = hist[255 - 8 * lane - q]; sum += c[q]; }
+                int ex = sum;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int v = __shfl_up_sync(0xffffffffu, ex, o);
+                    if (lane >= o) ex += v;
+                }
+                ex -= sum;
+                if (ex < need && need <= ex + sum) {
+                    int r = ex;
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        if (r < need && need <= r + c[q]) {
+                            s_prefix = pre | ((unsigned long long)(255 - 8 * lane - q) << shift);
+                            s_need = need - r;
+                            s_shift = shift;
+                            // every pair sharing the prefix fits, or no byte is left
+                            s_done = (need - r == c[q]) || shift == 0;
+                        }
+                        r += c[q];
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    } else if (tid == 0) {
+        s_prefix = 0ull; s_shift = 0; s_need = 0; s_run = 0;
+    }
+    __syncthreads();
+    // admission: key above the prefix K*, or sharing it among the first s_need such pairs in
+    // token order
+    const int fs = s_shift;
+    const unsigned long long kstar = fs == 64 ? 0ull : s_prefix >> fs;
+    const int need = s_need;
+    for (int i0 = 0; i0 < ne; i0 += kSelThreads) {
+        const int i = i0 + tid;
+        unsigned long long kh = 0;
+        if (i < ne && !all) kh = fs == 64 ? 0ull : key_of(i) >> fs;
+        const bool tie = i < ne && !all && kh == kstar;
+        const unsigned bal = __ballot_sync(0xffffffffu, tie);
+        if (lane == 0) wsum[w] = __popc(bal);
+        __syncthreads();
+        int before = s_run;
+        for (int q = 0; q < w; ++q) before += wsum[q];
+        before += __popc(bal & ((1u << lane) - 1u));
+        if (i < ne) {
+            const bool a = all || kh > kstar || (tie && before < need);
+            const int pid = L[i];
+            bpr_adm[pid] = a ? 1 : 0;
+            if (a) atomicAdd(&tiles[(pid / k) / kScanTile], 1);
+        }
+        __syncthreads();
+        if (tid == 0) for (int q = 0; q < kSelThreads / 32; ++q) s_run += wsum[q];
+        __syncthreads();
+    }
+    for (int q = tid; q < n_tiles; q += kSelThreads) hist2[q * E + e] = tiles[q];
+}
+
 int launch_routing(const RouteArgs& a, bool is_bf16, cudaStream_t s)
 {
     const int n_tiles = ceil_div(a.T, kScanTile);
@@ -566,7 +759,9 @@ int launch_routing(const RouteArgs& a, bool is_bf16, cudaStream_t s)
         SET(bf16, 8); SET(bf16, 4); SET(bf16, 2); SET(bf16, 1);
         SET(float, 8); SET(float, 4); SET(float, 2); SET(float, 1);
 #undef SET
-        cudaFuncSetAttribute(slot_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(slot_scan_kernel<SCAN_SLOTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(slot_scan_kernel<SCAN_BPR_LIST>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(slot_scan_kernel<SCAN_BPR_SLOTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr_set = true;
     }
     const int elt = is_bf16 ? 2 : 4;
@@ -603,12 +798,34 @@ int launch_routing(const RouteArgs& a, bool is_bf16, cudaStream_t s)
 #undef GATE_LAUNCH
 #undef GATE_ARGS
     }
-    const size_t smem2 = sizeof(int) * (a.E + 32 * a.E + 32 * a.E + a.E +
+    const size_t smem2 = sizeof(int) * (a.E + 32 * a.E + 32 * a.E + 2 * a.E +
                                         (n_tiles * a.E <= kScanHistMax ? n_tiles * a.E : 0));
-    launch_k(slot_scan_kernel, n_tiles, kScanTile, smem2, s, a.idx, a.T, a.k, a.E, a.C, a.n_chunks,
-                                                       a.hist, n_tiles, a.slot, a.S, a.send_rows,
-                                                       a.send_off);
-    return 2;
+    if (!a.bpr) {
+        launch_k(slot_scan_kernel<SCAN_SLOTS>, n_tiles, kScanTile, smem2, s, a.idx, a.T, a.k, a.E, a.C,
+                 a.n_chunks, (const int*)a.hist, n_tiles, a.slot, a.S, a.send_rows, a.send_off,
+                 (const float*)nullptr, (double*)nullptr, (int*)nullptr, (int*)nullptr,
+                 (const unsigned char*)nullptr);
+        return 2;
+    }
+    // Batch Prioritized Routing (R16): pairs grouped by expert + scores, per-expert priority
+    // admission, then the token-major scan over the admitted pairs
+    launch_k(slot_scan_kernel<SCAN_BPR_LIST>, n_tiles, kScanTile, smem2, s, a.idx, a.T, a.k, a.E, a.C,
+             a.n_chunks, (const int*)a.hist, n_tiles, a.slot, a.S, a.send_rows, a.send_off,
+             (const float*)a.logits, a.score, a.list, a.bpr_meta, (const unsigned char*)nullptr);
+    const int cap = std::min(a.T * a.k, (int)((kSelSmem - sizeof(int) * n_tiles) / 8));
+    static bool sel_attr = false;
+    if (!sel_attr) {
+        cudaFuncSetAttribute(bpr_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSelSmem);
+        sel_attr = true;
+    }
+    launch_k(bpr_select_kernel, a.E, kSelThreads, 8 * (size_t)cap + sizeof(int) * n_tiles, s,
+             (const int*)a.list, (const int*)a.bpr_meta, (const double*)a.score, a.E, a.k, a.C, n_tiles,
+             cap, a.bpr_adm, a.hist2);
+    launch_k(slot_scan_kernel<SCAN_BPR_SLOTS>, n_tiles, kScanTile, smem2, s, a.idx, a.T, a.k, a.E, a.C,
+             a.n_chunks, (const int*)a.hist2, n_tiles, a.slot, a.S, a.send_rows, a.send_off,
+             (const float*)nullptr, (double*)nullptr, (int*)nullptr, (int*)nullptr,
+             (const unsigned char*)a.bpr_adm);
+    return 4;
 }
 
 }  // namespace lancet

@@ -29,6 +29,7 @@ FLAG_UNFUSED_GATE_BWD = 128
 FLAG_NO_PDL = 256
 FLAG_FORCE_EP = 512
 FLAG_TIMELINE_GEMM_ONLY = 1024
+FLAG_GATE_BPR = 2048
 # LANCET_EXTRA_FLAGS: OR'ed into every context's flags (e.g. run the test suite under PDL)
 EXTRA_FLAGS = int(os.environ.get("LANCET_EXTRA_FLAGS", "0"), 0)
 

@@ -73,13 +73,13 @@ def run_group(G, ins, E, k, cf, n, flags=0, act="gelu_tanh", dtype="bf16", repea
     return out
 
 
-def oracle_group(ins, k, cf, n, act="gelu_tanh"):
+def oracle_group(ins, k, cf, n, act="gelu_tanh", gate="switch"):
     from oracle import moe
     xs = [i["x"] for i in ins]
     wg = ins[0]["wg"]
     w1 = [i["w1"] for i in ins]
     w2 = [i["w2"] for i in ins]
-    fwd = moe.forward(xs, wg, w1, w2, k, cf, n, act=act)
+    fwd = moe.forward(xs, wg, w1, w2, k, cf, n, act=act, gate=gate)
     b = moe.backward(fwd, xs, wg, w1, w2, [i["dy"] for i in ins], act=act)
     return fwd, b
 
