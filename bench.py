@@ -217,10 +217,12 @@ GEMM_OPS = ("expert_fc1", "expert_fc2", "expert_dfc2", "expert_dfc1", "expert_dw
 def op_stats(tl, steps):
     tot = {}
     for r in tl:
-        tot.setdefault(r["name"], [0.0, 0])
+        tot.setdefault(r["name"], [0.0, 0, set()])
         tot[r["name"]][0] += r["end_us"] - r["start_us"]
         tot[r["name"]][1] += 1
-    return {k: {"us_per_step": v[0] / steps, "launch_groups_per_step": v[1] / steps} for k, v in tot.items()}
+        tot[r["name"]][2].add(r["lane"])
+    return {k: {"us_per_step": v[0] / steps, "launch_groups_per_step": v[1] / steps,
+                "lanes": sorted(v[2])} for k, v in tot.items()}
 
 
 def exposure_per_step(tl, steps):
@@ -531,9 +533,20 @@ def run_lancet(a, world, rank, local_rank):
     }
     for o, b in mem_bytes.items():
         if o in ops and ops[o]["us_per_step"] > 0:
+            if 2 in ops[o]["lanes"]:
+                # side stream: the event span runs concurrently with the GEMMs (sharing SMs and
+                # waiting for them); it is not the kernel's duration, so no bandwidth is derived
+                # from it (isolated durations: the ncu launch list under profiles/)
+                kernels[o] = {"span_us": ops[o]["us_per_step"],
+                              "note": "side stream, concurrent with the expert GEMMs: event span, "
+                                      "not an isolated duration"}
+                continue
             kernels[o] = {"us": ops[o]["us_per_step"],
                           "gbs": b / (ops[o]["us_per_step"] * 1e-6) / 1e9,
                           "hbm_frac": b / (ops[o]["us_per_step"] * 1e-6) / 1e9 / pk["hbm"]}
+            if o == "gate":
+                kernels[o]["note"] = ("event span of K1 + K2 (gate, slot scan and the histogram "
+                                      "memset); bytes are the gate's")
     for o, v in ops.items():
         if o not in kernels:
             kernels[o] = {"us": v["us_per_step"]}

@@ -101,7 +101,7 @@ enum {
                                            single GPU                                         */
     LANCET_FLAG_TIMELINE_GEMM_ONLY = 1u << 10,/* with TIMELINE: events around the expert GEMM
                                            launches only (the least perturbing roofline pass) */
-    LANCET_FLAG_GATE_BPR = 1u << 11     /* Batch Prioritized Routing (DESIGN.md
+    LANCET_FLAG_GATE_BPR = 1u << 11,    /* Batch Prioritized Routing (DESIGN.md
                                            R16) instead of token-major admission: the pairs of
                                            each expert are admitted by the token's importance
                                            score s_t = sum_j p[t, idx_tj] (fp64; descending,
@@ -111,6 +111,13 @@ enum {
                                            partition after it (fig:part_after_gate, L271), so
                                            chunked == unchunked as with the Switch gate.
                                            Costs two more routing kernels per forward        */
+    LANCET_FLAG_DEFER_DW = 1u << 12     /* backward: do not enqueue this layer's dW GEMMs; they
+                                           stay pending (dW1 and dW2 separately) until
+                                           lancet_moe_backward_dw or another context's filler
+                                           slot enqueues them (cross-layer dW scheduling,
+                                           PAPER.md L156, L348-L398; R17).  The next
+                                           forward fails with LANCET_ERR_STATE while any are
+                                           pending                                           */
 };
 
 typedef struct {
@@ -218,6 +225,43 @@ lancet_status lancet_moe_forward(lancet_ctx* ctx, const void* x, const float* wg
  * Never blocks the host. */
 lancet_status lancet_moe_backward(lancet_ctx* ctx, const void* dy, void* dx, float* dwg,
                                   float* dw1, float* dw2, lancet_stream_t stream);
+
+/* Cross-layer dW scheduling (PAPER.md Opportunity 1, L156 "overlapped with any dWs in layer
+ * N+k"; Alg. 1 placement L359 "placing them right after their overlapping all-to-all
+ * instructions"; R17).
+ *
+ * lancet_moe_backward_dw: enqueue the pending dW GEMMs of `ctx`'s last backward (run with
+ *   LANCET_FLAG_DEFER_DW) on `stream`, ordered after that backward's dX GEMMs by an event.
+ *   which: bit 0 = dW1 (dA^T X), bit 1 = dW2 (dO^T H); both write the dw1 / dw2 pointers the
+ *   backward was given (fp32, all chunks, in chunk order).  LANCET_ERR_STATE if a requested
+ *   part is not pending.
+ * lancet_set_dw_fillers: for the NEXT backward of `ctx` only -- right after that backward
+ *   launches its all-to-all number a2a_index[i] (issue order: 0..n-1 = the per-chunk
+ *   dispatch of dO to the experts, n..2n-1 = the per-chunk return of dX), enqueue the pending
+ *   dW part which[i] of others[i] on the backward's compute stream.  An index the backward
+ *   never reaches (e.g. world 1: no all-to-all) is served at its end.  others[i] may be ctx
+ *   itself (its own dW placed under its own dX return).  Pointers are host arrays of n
+ *   entries, copied.  The other contexts must outlive the call and keep their forward's
+ *   buffers (no forward of theirs in between).
+ * lancet_dw_schedule: Alg. 1 on any instruction DAG (host only, no device).  kind[i]: 0 other,
+ *   1 all-to-all, 2 dW; cost[i] in any time unit; edges [n_edges][2] (src, dst) = dst
+ *   consumes src.  assign[i] (out) = the all-to-all instruction dW i overlaps, else -1.
+ *   Labelling: no directed path either way (L343); assignment: all-to-alls in program
+ *   order, while unoverlapped time t_u > 0 take the unused eligible dW minimising
+ *   |t_u - t_W| (ties -> lowest index).  LANCET_ERR_ARG on bad sizes / indices.
+ * lancet_stack_dw_plan: the backward program of an L-layer stack of this layer (layers in
+ *   forward order, backward runs L-1 first; per layer the per-chunk K5, dO a2a, dX GEMMs,
+ *   then dW2, dW1, the per-chunk dX a2a, K6, K7 -- DESIGN.md R17) scheduled by Alg. 1.
+ *   t_a2a [L][2n] (the layer's a2a in issue order), t_dw [L][2] (dW2, dW1).  Outputs per
+ *   (layer, part) [L][2] (part 0 = dW2, 1 = dW1): host_layer = the layer whose backward
+ *   carries it, host_a2a = the a2a index there, or -1 / -1 = unassigned (keep in place). */
+lancet_status lancet_moe_backward_dw(lancet_ctx* ctx, int32_t which, lancet_stream_t stream);
+lancet_status lancet_set_dw_fillers(lancet_ctx* ctx, int32_t n, lancet_ctx* const* others,
+                                    const int32_t* which, const int32_t* a2a_index);
+lancet_status lancet_dw_schedule(int32_t n_instr, const int32_t* kind, const double* cost,
+                                 int32_t n_edges, const int32_t* edges, int32_t* assign);
+lancet_status lancet_stack_dw_plan(int32_t L, int32_t n_chunks, const double* t_a2a,
+                                   const double* t_dw, int32_t* host_layer, int32_t* host_a2a);
 
 /* Routing sizes of the last forward (host arrays; synchronises with the forward):
  *   send_counts [E][n_chunks]         rows this rank admitted per expert per chunk

@@ -110,6 +110,13 @@ struct lancet_ctx {
     std::vector<int> host_send, host_recv, host_grp_rows, host_grp_off;  // world > 1
     int launches_fwd = 0, launches_bwd = 0;
 
+    // cross-layer dW scheduling (LANCET_FLAG_DEFER_DW, R17)
+    int dw_pending = 0;              // bit 0: dW1, bit 1: dW2 of the last backward not enqueued
+    float* pend_dw1 = nullptr;  float* pend_dw2 = nullptr;
+    cudaEvent_t ev_dw_ready = nullptr;   // after the last backward's dX GEMMs
+    struct Filler { lancet_ctx* other; int which; int a2a; };
+    std::vector<Filler> fillers;     // consumed by the next backward
+
     // errors
     bool poisoned = false;
     std::string err;

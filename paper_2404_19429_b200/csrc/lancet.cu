@@ -215,7 +215,7 @@ lancet_status expert_backward_dx(lancet_ctx* c, const void* dout, const int* grp
 // dW GEMMs (K-grouped over each group's token rows): dW2 (+)= dO^T H, dW1 (+)= dA^T X.
 lancet_status expert_backward_dw(lancet_ctx* c, const void* dout, const int* grp_rows,
                                  const int* grp_off, int ng, float* dw1, float* dw2,
-                                 int accumulate, cudaStream_t s, int chunk, int* launches)
+                                 int accumulate, cudaStream_t s, int chunk, int* launches, int which = 3)
 {
     const int d = c->cfg.d_model, f = c->cfg.d_ffn;
     GemmArgs a{};
@@ -223,19 +223,45 @@ lancet_status expert_backward_dw(lancet_ctx* c, const void* dout, const int* grp
     a.grp_rows = grp_rows; a.grp_off = grp_off; a.accumulate = accumulate;
     a.a_mn = true; a.b_mn = true; a.epi = EPI_F32; a.b_group_stride = 0;
     a.a_rows = c->rows_exp; a.b_rows = c->rows_exp;
-    {
+    if (which & 2) {
         OpScope op(c, "expert_dw2", 0, chunk, s);
         a.A = dout; a.lda = d; a.B = c->H; a.ldb = f;
         a.C = dw2; a.ldc = f; a.c_group_stride = (long)d * f; a.M = d; a.N = f;
         lancet_status st = run_gemm(c, a, s, launches);
         if (st) return st;
     }
-    {
+    if (which & 1) {
         OpScope op(c, "expert_dw1", 0, chunk, s);
         a.A = c->dA; a.lda = f; a.B = c->ep ? c->xe : c->xs; a.ldb = d;
         a.C = dw1; a.ldc = d; a.c_group_stride = (long)f * d; a.M = f; a.N = d;
         return run_gemm(c, a, s, launches);
     }
+    return LANCET_OK;
+}
+
+// Cross-layer dW scheduling (R17): enqueue the pending dW part(s) `which` of context o on
+// stream s, after o's dX GEMMs (o->ev_dw_ready), all chunks in chunk order.
+lancet_status enqueue_pending_dw(lancet_ctx* c, int which, cudaStream_t s, int* launches)
+{
+    if (which < 1 || which > 3) return fail(c, LANCET_ERR_ARG, "which must be 1 (dW1), 2 (dW2) or 3");
+    if ((c->dw_pending & which) != which) return fail(c, LANCET_ERR_STATE, "requested dW GEMMs are not pending");
+    CK(cudaStreamWaitEvent(s, c->ev_dw_ready, 0));
+    lancet_status st;
+    if (!c->ep) {
+        st = expert_backward_dw(c, c->dcomb, c->send_rows, c->send_off, c->cfg.n_experts, c->pend_dw1,
+                                c->pend_dw2, 0, s, -1, launches, which);
+    } else {
+        const int E_l = c->E_l, n = c->n;
+        const int* rows = c->grp_dev;
+        const int* off = c->grp_dev + n * E_l;
+        st = LANCET_OK;
+        for (int ch = 0; ch < n && !st; ++ch)
+            st = expert_backward_dw(c, c->dout, rows + ch * E_l, off + ch * E_l, E_l, c->pend_dw1, c->pend_dw2,
+                                    ch > 0, s, ch, launches, which);
+    }
+    if (st) return st;
+    c->dw_pending &= ~which;
+    return LANCET_OK;
 }
 
 lancet_status validate_cfg(const lancet_layer_config* cfg, int world)
@@ -276,6 +302,7 @@ lancet_status create_common(lancet_ctx* c, int world, int rank, int device, cons
     CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->ev_counts, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->ev_dw_ready, cudaEventDisableTiming));
     CK(cudaEventCreate(&c->ev_tl_base));
     for (int i = 0; i < 8 * kMaxChunks + 16; ++i) {
         cudaEvent_t e;
@@ -681,6 +708,7 @@ LANCET_API lancet_status lancet_destroy(lancet_ctx* c)
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->ev_counts) cudaEventDestroy(c->ev_counts);
+    if (c->ev_dw_ready) cudaEventDestroy(c->ev_dw_ready);
     if (c->ev_tl_base) cudaEventDestroy(c->ev_tl_base);
     if (c->s_comp) cudaStreamDestroy(c->s_comp);
     if (c->s_comm) cudaStreamDestroy(c->s_comm);
@@ -718,6 +746,7 @@ LANCET_API lancet_status lancet_moe_forward(lancet_ctx* c, const void* x, const 
     if (n < 1 || n > std::min<int>(T, c->cfg.max_chunks)) return fail(c, LANCET_ERR_ARG, "n_chunks must be in [1, min(T, max_chunks)]");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream_);
     lancet::g_pdl = (c->cfg.flags & LANCET_FLAG_NO_PDL) == 0;
+    if (c->dw_pending) return fail(c, LANCET_ERR_STATE, "deferred dW GEMMs of the last backward were never enqueued");
     c->have_fwd = false;
     c->x = x; c->wg = wg; c->w1 = w1; c->w2 = w2;
     c->T = T; c->k = k; c->n = n; c->cf = cf;
@@ -974,6 +1003,24 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
     c->launches_bwd = 0;
     int& L = c->launches_bwd;
     DispatchArgs da{T, k, d, E, c->idx, c->slot, c->w, c->send_off, c->send_rows};
+    const bool defer = (c->cfg.flags & LANCET_FLAG_DEFER_DW) && !ident;
+    if (c->dw_pending) return fail(c, LANCET_ERR_STATE, "the previous backward's deferred dW GEMMs were never enqueued");
+    // the fillers set for this backward, each served once right after its all-to-all's launch
+    std::vector<bool> served(c->fillers.size(), false);
+    struct ClearFillers { lancet_ctx* c; ~ClearFillers() { c->fillers.clear(); } } clear_fillers{c};
+    auto run_fillers = [&](lancet_ctx*, int lo, int hi, cudaStream_t fs, int* launches) -> lancet_status {
+        for (size_t i = 0; i < c->fillers.size(); ++i) {
+            const auto& fl = c->fillers[i];
+            if (served[i] || fl.a2a < lo || fl.a2a >= hi) continue;
+            served[i] = true;
+            lancet_status fst = enqueue_pending_dw(fl.other, fl.which, fs, launches);
+            if (fst) {
+                c->fillers.clear();
+                return fail(c, fst, std::string("dW filler: ") + fl.other->err);
+            }
+        }
+        return LANCET_OK;
+    };
 
     if (!c->ep) {
         const void* comb = ident ? c->xs : c->out;
@@ -1017,9 +1064,16 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
         }
         CK(cudaEventRecord(ev_side, sa));
         if (!ident) {
-            st = expert_backward_dw(c, c->dcomb, c->send_rows, c->send_off, E, dw1, dw2, 0, s, -1, &L);
-            if (st) return st;
+            if (defer) {
+                CK(cudaEventRecord(c->ev_dw_ready, s));
+                c->dw_pending = 3; c->pend_dw1 = dw1; c->pend_dw2 = dw2;
+            } else {
+                st = expert_backward_dw(c, c->dcomb, c->send_rows, c->send_off, E, dw1, dw2, 0, s, -1, &L);
+                if (st) return st;
+            }
         }
+        st = run_fillers(c, 0, 1 << 30, s, &L);       // no all-to-all at world 1
+        if (st) return st;
         CK(cudaStreamWaitEvent(s, ev_side, 0));
         return LANCET_OK;
     }
@@ -1101,6 +1155,10 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
         ev_b1[cc] = next_ev();
         CK(cudaEventRecord(ev_b1[cc], sm));
     }
+    // dW GEMMs of other layers placed under this layer's dO all-to-all (R17): on the compute
+    // stream ahead of the dX GEMMs, which wait for that all-to-all anyway
+    st = run_fillers(c, 0, n, sc, &L);
+    if (st) return st;
     // dX GEMMs per chunk, each followed immediately by the chunk's dW GEMMs
     for (int cc = 0; cc < nc; ++cc) {
         int c0, c1;
@@ -1117,13 +1175,17 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
         }
         ev_dx[cc] = next_ev();
         CK(cudaEventRecord(ev_dx[cc], sc));
-        if (!ident && !late_dw) {
+        if (!ident && !late_dw && !defer) {
             for (int ch = c0; ch < c1; ++ch) {
                 st = expert_backward_dw(c, c->dout, d_grp_rows + ch * E_l, d_grp_off + ch * E_l, E_l,
                                         dw1, dw2, ch > 0, sc, ch, &L);
                 if (st) return st;
             }
         }
+    }
+    if (defer) {                // this layer's dW GEMMs stay pending (R17)
+        CK(cudaEventRecord(c->ev_dw_ready, sc));
+        c->dw_pending = 3; c->pend_dw1 = dw1; c->pend_dw2 = dw2;
     }
     // backward a2a #2: dX rows back to the token owners (same plan as the combine)
     const char* dxe = ident ? (const char*)c->dout : (const char*)c->dXe;
@@ -1139,6 +1201,8 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
                 return fail(c, LANCET_ERR_CUDA, err);
             ev_b2[cc] = next_ev();
             CK(cudaEventRecord(ev_b2[cc], sm));
+            st = run_fillers(c, serial ? n : n + cc, serial ? 2 * n : n + cc + 1, sc, &L);
+            if (st) return st;
             continue;
         }
         std::vector<P2P> sends, recvs;
@@ -1158,8 +1222,12 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
         if (c->comm->exchange(sends, recvs, sm, err)) return fail(c, LANCET_ERR_NCCL, err);
         ev_b2[cc] = next_ev();
         CK(cudaEventRecord(ev_b2[cc], sm));
+        st = run_fillers(c, serial ? n : n + cc, serial ? 2 * n : n + cc + 1, sc, &L);
+        if (st) return st;
     }
-    if (!ident && late_dw) {    // ablation / serial baseline: all dW after the last a2a
+    st = run_fillers(c, 0, 1 << 30, sc, &L);     // indices this backward never reached
+    if (st) return st;
+    if (!ident && late_dw && !defer) {    // ablation / serial baseline: all dW after the last a2a
         for (int ch = 0; ch < n; ++ch) {
             st = expert_backward_dw(c, c->dout, d_grp_rows + ch * E_l, d_grp_off + ch * E_l, E_l,
                                     dw1, dw2, ch > 0, sc, ch, &L);
@@ -1180,6 +1248,34 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
         CK(cudaEventRecord(e2, sm));
         CK(cudaStreamWaitEvent(s, e2, 0));
     }
+    return LANCET_OK;
+}
+
+LANCET_API lancet_status lancet_moe_backward_dw(lancet_ctx* c, int32_t which, lancet_stream_t stream)
+{
+    lancet_status st = check_ready(c);
+    if (st) return st;
+    lancet::g_pdl = (c->cfg.flags & LANCET_FLAG_NO_PDL) == 0;
+    int L = 0;
+    st = enqueue_pending_dw(c, which, reinterpret_cast<cudaStream_t>(stream), &L);
+    if (st) return st;
+    CK(cudaGetLastError());
+    return LANCET_OK;
+}
+
+LANCET_API lancet_status lancet_set_dw_fillers(lancet_ctx* c, int32_t n, lancet_ctx* const* others,
+                                               const int32_t* which, const int32_t* a2a_index)
+{
+    lancet_status st = check_ready(c);
+    if (st) return st;
+    if (n < 0 || (n > 0 && (!others || !which || !a2a_index))) return fail(c, LANCET_ERR_ARG, "bad filler arrays");
+    std::vector<lancet_ctx::Filler> f;
+    for (int i = 0; i < n; ++i) {
+        if (!others[i] || which[i] < 1 || which[i] > 3 || a2a_index[i] < 0)
+            return fail(c, LANCET_ERR_ARG, "filler " + std::to_string(i) + ": null context, which not in 1..3 or negative index");
+        f.push_back({others[i], which[i], a2a_index[i]});
+    }
+    c->fillers = f;
     return LANCET_OK;
 }
 

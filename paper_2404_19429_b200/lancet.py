@@ -30,6 +30,7 @@ FLAG_NO_PDL = 256
 FLAG_FORCE_EP = 512
 FLAG_TIMELINE_GEMM_ONLY = 1024
 FLAG_GATE_BPR = 2048
+FLAG_DEFER_DW = 4096
 # LANCET_EXTRA_FLAGS: OR'ed into every context's flags (e.g. run the test suite under PDL)
 EXTRA_FLAGS = int(os.environ.get("LANCET_EXTRA_FLAGS", "0"), 0)
 
@@ -38,7 +39,8 @@ EXPORTS = ["lancet_abi_version", "lancet_last_error", "lancet_nccl_unique_id", "
            "lancet_destroy", "lancet_set_flags", "lancet_moe_forward", "lancet_moe_backward",
            "lancet_get_counts", "lancet_timeline_begin", "lancet_last_timeline", "lancet_debug_copy",
            "lancet_workspace_bytes", "lancet_launch_counts", "lancet_plan_exchange",
-           "lancet_create_peer", "lancet_peer_blob_bytes", "lancet_peer_export", "lancet_peer_import"]
+           "lancet_create_peer", "lancet_peer_blob_bytes", "lancet_peer_export", "lancet_peer_import",
+           "lancet_moe_backward_dw", "lancet_set_dw_fillers", "lancet_dw_schedule", "lancet_stack_dw_plan"]
 
 
 class LancetError(RuntimeError):
@@ -98,6 +100,10 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "lancet_workspace_bytes": ([P, ctypes.POINTER(ctypes.c_size_t)], I32),
             "lancet_launch_counts": ([P, ctypes.POINTER(I32), ctypes.POINTER(I32)], I32),
             "lancet_plan_exchange": ([I32, I32, I32, P, P, P, P, P, P, P, ctypes.POINTER(I32)], I32),
+            "lancet_moe_backward_dw": ([P, I32, P], I32),
+            "lancet_set_dw_fillers": ([P, I32, P, P, P], I32),
+            "lancet_dw_schedule": ([I32, P, P, I32, P, P], I32),
+            "lancet_stack_dw_plan": ([I32, I32, P, P, P, P], I32),
         }
         for name, (args, res) in sig.items():
             f = getattr(lib, name)
@@ -175,6 +181,33 @@ def plan_exchange(G: int, E_l: int, n: int, send_counts, recv_counts) -> dict:
                                                ctypes.byref(tot)))
     out["total_rows"] = tot.value
     return out
+
+
+def dw_schedule(kinds, costs, edges):
+    """Alg. 1 (lancet_dw_schedule) on an instruction DAG; returns assign[i] (a2a index or -1)."""
+    import numpy as np
+    kinds = np.ascontiguousarray(kinds, dtype=np.int32)
+    costs = np.ascontiguousarray(costs, dtype=np.float64)
+    ed = np.ascontiguousarray(np.asarray(edges, dtype=np.int32).reshape(-1, 2))
+    out = np.full(len(kinds), -1, dtype=np.int32)
+    p = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    _check(load_library().lancet_dw_schedule(len(kinds), p(kinds), p(costs), len(ed), p(ed), p(out)))
+    return out
+
+
+def stack_dw_plan(t_a2a, t_dw):
+    """Alg. 1 on the backward of an L-layer stack (lancet_stack_dw_plan).  t_a2a [L][2n] (each
+    layer's all-to-alls in issue order), t_dw [L][2] (dW2, dW1).  Returns (host_layer,
+    host_a2a), each [L][2] int32, -1 = unassigned."""
+    import numpy as np
+    t_a2a = np.ascontiguousarray(t_a2a, dtype=np.float64)
+    t_dw = np.ascontiguousarray(t_dw, dtype=np.float64)
+    L, n2 = t_a2a.shape
+    hl = np.full((L, 2), -1, dtype=np.int32)
+    ha = np.full((L, 2), -1, dtype=np.int32)
+    p = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    _check(load_library().lancet_stack_dw_plan(L, n2 // 2, p(t_a2a), p(t_dw), p(hl), p(ha)))
+    return hl, ha
 
 
 def share_nccl_id(pg=None, rank: int = 0) -> bytes:
@@ -298,6 +331,19 @@ class Context:
                                                 _ptr(dw2), _stream(stream))
         _check(st, self._p)
         return dx, dwg, dw1, dw2
+
+    # -- cross-layer dW scheduling (R17) ---------------------------------------------
+    def backward_dw(self, which: int = 3, stream=None):
+        """Enqueue this context's pending dW GEMMs (after a backward under FLAG_DEFER_DW)."""
+        _check(load_library().lancet_moe_backward_dw(self._p, which, _stream(stream)), self._p)
+
+    def set_dw_fillers(self, fillers):
+        """fillers: [(other Context, which (1 dW1 | 2 dW2), a2a index)] for the next backward."""
+        n = len(fillers)
+        others = (ctypes.c_void_p * max(n, 1))(*[f[0]._p.value for f in fillers])
+        which = (ctypes.c_int32 * max(n, 1))(*[f[1] for f in fillers])
+        idx = (ctypes.c_int32 * max(n, 1))(*[f[2] for f in fillers])
+        _check(load_library().lancet_set_dw_fillers(self._p, n, others, which, idx), self._p)
 
     # -- introspection ------------------------------------------------------------------------
     def counts(self, n_chunks: int):

@@ -10,5 +10,6 @@ if 'e2e' in d:
     print(f"e2e {d['e2e']['value']/1e6:.3f} M tok/s")
 for k, v in d.get('kernels', {}).items():
     extra = f"{v['tflops']:7.0f} TF/s" if 'tflops' in v else (f"{v['gbs']:7.0f} GB/s ({v['hbm_frac']:.2f})" if 'gbs' in v else "")
-    print(f"  {k:20s} {v['us']:8.1f} us  " + extra)
-print(f"  sum of ops {sum(v['us'] for v in d.get('kernels', {}).values()):.1f} us")
+    us = v.get('us', v.get('span_us', 0.0))
+    print(f"  {k:20s} {us:8.1f} us  " + (extra or ("(side-stream span)" if 'span_us' in v else "")))
+print(f"  sum of in-line ops {sum(v.get('us', 0.0) for v in d.get('kernels', {}).values()):.1f} us")
