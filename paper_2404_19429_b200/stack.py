@@ -20,7 +20,6 @@ class MoEStack:
     def __init__(self, ctxs: list[Context]):
         self.ctxs = ctxs
         self.L = len(ctxs)
-        self._base_flags = [c.cfg.flags & ~FLAG_DEFER_DW for c in ctxs]
 
     def forward(self, x, params, k, capacity_factor, n_chunks, stream=None):
         """params[l] = (wg, w1, w2).  Returns the per-layer outputs [y_0 .. y_L-1]."""
@@ -53,16 +52,17 @@ class MoEStack:
                     else:              # unassigned part keeps its place: after its own dX GEMMs
                         fill[m].append((self.ctxs[m], WHICH[w], n))
         dxs = [None] * L
+        base = [c.cfg.flags & ~FLAG_DEFER_DW for c in self.ctxs]
         for l in range(L - 1, -1, -1):
             ctx = self.ctxs[l]
-            ctx.set_flags(self._base_flags[l] | (FLAG_DEFER_DW if defer[l] else 0))
+            ctx.set_flags(base[l] | (FLAG_DEFER_DW if defer[l] else 0))
             ctx.set_dw_fillers(fill[l])
             dwg, dw1, dw2 = grads[l]
             dx, _, _, _ = ctx.backward(dy, dwg=dwg, dw1=dw1, dw2=dw2, stream=stream)
             dxs[l] = dx
             dy = dx
         for l in range(L):
-            self.ctxs[l].set_flags(self._base_flags[l])
+            self.ctxs[l].set_flags(base[l])
         return dxs
 
 
