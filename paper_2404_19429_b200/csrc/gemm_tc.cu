@@ -486,7 +486,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                             __syncwarp();
                         }
                         // the previous chunk's TMA stores must have read the staging buffers
+#ifndef LANCET_EXP_NO_WAIT
                         if (lane == 0) bulk_wait_read0();
+#endif
                         __syncwarp();
                         if (dact && cc + 1 < cc1 && lane == 0) {          // act'(A) of the next chunk
                             mbar_expect_tx(xbar, 2048);
