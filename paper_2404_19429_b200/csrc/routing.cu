@@ -24,12 +24,19 @@ __host__ __device__ constexpr int gate_dt(int ce) { return ce >= 8 ? 64 : 128; }
 __host__ __device__ constexpr int gate_stages(int ce) { return ce >= 8 ? 3 : 4; }   // ring depth
 constexpr int kGateThreads = 256;
 constexpr int kGateMaxTB = 64;   // tokens per block (T=16k -> 256 blocks, all resident)
+#ifndef LANCET_GATE_TT8
+#define LANCET_GATE_TT8 4
+#endif
+// tokens per thread at 8 experts per thread (E >= 16 on the tiled path): each staged Wg value
+// feeds 4 tokens.  ncu at d=1024 (round 1, session 3): E=64 T=16k 110 -> 92 us, T=64k 369 ->
+// 299 us; E=32 66 -> 62 / 209 -> 182 us against 2; 8 tokens per thread is slower (fewer warps)
+constexpr int kGateTT8 = LANCET_GATE_TT8;
 
 // Thread (tokens r..r+TT-1, experts e0..e0+CE-1) runs TT*CE independent R1 chains, two at a
 // time with the packed fp32 FMA (fma.rn.f32x2: two IEEE fused multiply-adds, each rounded once
-// -- bitwise the same as two fmaf).  CE = 8, 4, 2 or 1 (largest dividing E); TT = 2 tokens per
-// thread when CE >= 4, so each staged Wg value feeds two tokens (the kernel is bound by
-// shared-memory reads and FMA-chain latency, not by HBM).
+// -- bitwise the same as two fmaf).  CE = 8, 4, 2 or 1 (largest dividing E); TT = 4 tokens per
+// thread at CE = 8 and 2 at CE = 4, so each staged Wg value feeds several tokens (the kernel is
+// bound by shared-memory reads and FMA-chain latency, not by HBM).
 struct GateGeom {
     int ce;        // experts (R1 chains) per thread
     int tt;        // tokens per thread
@@ -52,7 +59,7 @@ __host__ __device__ inline GateGeom gate_geom(int E, int elt_bytes)
 {
     GateGeom g;
     g.ce = gate_ce(E);
-    g.tt = g.ce >= 4 ? 2 : 1;
+    g.tt = g.ce >= 8 ? kGateTT8 : (g.ce >= 4 ? 2 : 1);
     g.tpt = E / g.ce;
     g.TB = kGateThreads * g.tt / g.tpt;
     if (g.TB > kGateMaxTB) g.TB = kGateMaxTB;
@@ -755,7 +762,7 @@ int launch_routing(const RouteArgs& a, bool is_bf16, cudaStream_t s)
     cudaMemsetAsync(a.hist, 0, sizeof(int) * n_tiles * a.E, s);
     static bool attr_set = false;
     if (!attr_set) {
-#define SET(Elt, CE) cudaFuncSetAttribute(gate_topk_kernel<Elt, CE, (CE >= 4 ? 2 : 1)>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)
+#define SET(Elt, CE) cudaFuncSetAttribute(gate_topk_kernel<Elt, CE, (CE >= 8 ? kGateTT8 : CE >= 4 ? 2 : 1)>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)
         SET(bf16, 8); SET(bf16, 4); SET(bf16, 2); SET(bf16, 1);
         SET(float, 8); SET(float, 4); SET(float, 2); SET(float, 1);
 #undef SET
@@ -789,7 +796,7 @@ int launch_routing(const RouteArgs& a, bool is_bf16, cudaStream_t s)
 #define GATE_ARGS a.T, a.d, a.E, a.k, a.renorm, a.logits, a.idx, a.w, a.hist, n_tiles
 #define GATE_LAUNCH(Elt)                                                                                    \
     switch (g.ce) {                                                                                         \
-    case 8: launch_k(gate_topk_kernel<Elt, 8, 2>, blocks, thr, g.smem, s, (const Elt*)a.x, a.wg, GATE_ARGS); break;  \
+    case 8: launch_k(gate_topk_kernel<Elt, 8, kGateTT8>, blocks, thr, g.smem, s, (const Elt*)a.x, a.wg, GATE_ARGS); break;  \
     case 4: launch_k(gate_topk_kernel<Elt, 4, 2>, blocks, thr, g.smem, s, (const Elt*)a.x, a.wg, GATE_ARGS); break;  \
     case 2: launch_k(gate_topk_kernel<Elt, 2, 1>, blocks, thr, g.smem, s, (const Elt*)a.x, a.wg, GATE_ARGS); break;  \
     default: launch_k(gate_topk_kernel<Elt, 1, 1>, blocks, thr, g.smem, s, (const Elt*)a.x, a.wg, GATE_ARGS); break; \
