@@ -175,6 +175,36 @@ def route_micro_bpr(idx: np.ndarray, score: np.ndarray, E: int, C: int, n_chunks
     return admitted
 
 
+_GOLDEN_GAMMA = 0x9E3779B97F4A7C15
+_M64 = (1 << 64) - 1
+
+
+def splitmix64(key: int, seed: int) -> int:
+    """SplitMix64 output for counter `key` (0-based) of the stream seeded with `seed`: the
+    state after key + 1 increments of the golden-gamma Weyl sequence, through the SplitMix64
+    finaliser (Steele, Lea and Flood 2014).  DESIGN.md R18."""
+    z = (seed + (key + 1) * _GOLDEN_GAMMA) & _M64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+    return z ^ (z >> 31)
+
+
+def random_gate(T: int, E: int, k: int, seed: int):
+    """Random gating ("Random [zuo2022taming, chen2023sparse] gating", whose
+    "expert assignment can be decided from partial batches"), R18: token t's j-th
+    expert is the r-th smallest expert not chosen by draws 0..j-1, r = splitmix64(8 t + j,
+    seed) mod (E - j) (distinct experts, uniform up to a < 2^-50 modulo bias); combine weights
+    1/k.  The draw depends on the token index only, so any partition reproduces it.
+    Returns idx [T,k] int32 and w [T,k] f64."""
+    idx = np.zeros((T, k), dtype=np.int32)
+    for t in range(T):
+        free = list(range(E))
+        for j in range(k):
+            r = splitmix64(8 * t + j, seed) % (E - j)
+            idx[t, j] = free.pop(r)
+    return idx, np.full((T, k), 1.0 / k)
+
+
 def chunk_bounds(T: int, n: int) -> list[int]:
     """Split T tokens into n contiguous chunks whose sizes differ by at most one, larger
     first (R9).  Returns the n+1 boundaries [t_0=0, ..., t_n=T]."""
@@ -291,6 +321,7 @@ class RankRouting:
     slot: np.ndarray       # [T,k] i32 (-1 dropped)
     C: int
     counts: np.ndarray     # [E,n] admitted rows per expert per chunk
+    gate: str = "switch"   # "switch" | "bpr" | "random"
 
 
 @dataclass
@@ -301,7 +332,7 @@ class LayerResult:
 
 
 def route_rank(x, wg, k, cf, n_chunks, renormalize=False, gate_fp64=False,
-               gate="switch") -> RankRouting:
+               gate="switch", seed=0) -> RankRouting:
     """Routing of one rank's local batch (routing never crosses ranks: the gate is
     replicated, and C is per device).  `gate_fp64` replaces the R1 fp32
     chain by an fp64 product -- used only by the finite-difference pins of the backward,
@@ -309,6 +340,13 @@ def route_rank(x, wg, k, cf, n_chunks, renormalize=False, gate_fp64=False,
     admission, R7) or "bpr" (Batch Prioritized Routing, assign_slots_bpr, R16)."""
     T = x.shape[0]
     E = wg.shape[1]
+    if gate == "random":
+        # no gate network: logits are reported as zeros, and no gradient reaches Wg (R18)
+        idx, w = random_gate(T, E, k, seed)
+        C = capacity(T, k, E, cf)
+        slot, _ = assign_slots(idx, E, C)
+        return RankRouting(np.zeros((T, E), np.float32), idx, np.zeros((T, E)), w, slot, C,
+                           chunk_counts(idx, slot, E, n_chunks), gate="random")
     if gate_fp64:
         logits = x.astype(np.float64) @ wg.astype(np.float64)
     else:
@@ -324,7 +362,7 @@ def route_rank(x, wg, k, cf, n_chunks, renormalize=False, gate_fp64=False,
     else:
         raise ValueError(gate)
     counts = chunk_counts(idx, slot, E, n_chunks)
-    return RankRouting(logits, idx, p, w, slot, C, counts)
+    return RankRouting(logits, idx, p, w, slot, C, counts, gate=gate)
 
 
 def expert_weights(w1_ranks, w2_ranks, e, E_l):
@@ -333,7 +371,8 @@ def expert_weights(w1_ranks, w2_ranks, e, E_l):
 
 
 def forward(xs, wg, w1_ranks, w2_ranks, k, cf, n_chunks, act="gelu_tanh",
-            renormalize=False, token_subset=None, gate_fp64=False, gate="switch") -> LayerResult:
+            renormalize=False, token_subset=None, gate_fp64=False, gate="switch",
+            seed=0) -> LayerResult:
     """The MoE layer forward over G = len(xs) ranks.
 
     xs[r]: [T_r, d] tokens of rank r; w1_ranks[r]: [E_l, f, d], w2_ranks[r]: [E_l, d, f].
@@ -351,7 +390,7 @@ def forward(xs, wg, w1_ranks, w2_ranks, k, cf, n_chunks, act="gelu_tanh",
     E_l = E // G
     res = LayerResult(routing=[], y=[])
     for r in range(G):
-        rt = route_rank(xs[r], wg, k, cf, n_chunks, renormalize, gate_fp64, gate)
+        rt = route_rank(xs[r], wg, k, cf, n_chunks, renormalize, gate_fp64, gate, seed)
         res.routing.append(rt)
         T, d = xs[r].shape
         keep = np.zeros(T, dtype=bool)
@@ -426,7 +465,9 @@ def backward(fwd: LayerResult, xs, wg, w1_ranks, w2_ranks, dys, act="gelu_tanh",
             np.add.at(dx, t_sel, da @ w1e.astype(np.float64))
         dlogit = np.zeros((T, E))
         s = np.sum(g * rt.w, axis=1)                       # sum_j g_j w_j
-        if renormalize:
+        if rt.gate == "random":
+            pass                                           # no gate network (R18)
+        elif renormalize:
             for j in range(k):
                 dlogit[np.arange(T), rt.idx[:, j]] = rt.w[:, j] * (g[:, j] - s)
         else:
