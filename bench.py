@@ -50,9 +50,10 @@ def parse():
     ap.add_argument("--beta", type=float, default=0.25)
     ap.add_argument("--seed", type=int, default=2024)
     ap.add_argument("--flags", type=int, default=0, help="extra LANCET_FLAG_* bits")
-    ap.add_argument("--gate", choices=["switch", "bpr"], default="switch",
-                    help="capacity admission: token-major top-k (Switch/GShard-style) or Batch "
-                         "Prioritized Routing (PAPER.md L270; LANCET_FLAG_GATE_BPR)")
+    ap.add_argument("--gate", choices=["switch", "bpr", "random"], default="switch",
+                    help="token-major top-k (Switch/GShard-style), Batch Prioritized Routing "
+                         "(PAPER.md L270; LANCET_FLAG_GATE_BPR) or the Random gate (L271; "
+                         "LANCET_FLAG_GATE_RANDOM, seed 0)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--transport", choices=["auto", "nccl", "peer"], default="auto",
@@ -74,7 +75,7 @@ def workload(a, world):
     return {
         "workload": f"GPT-MoE layer fwd+bwd: d_model={a.d} ffn={a.f} experts={a.experts} "
                     f"({a.experts // world}/GPU) top-{a.k} cf={a.cf} {a.tokens} tokens/GPU "
-                    f"n_chunks={a.chunks} bf16" + (" gate=BPR" if a.gate == "bpr" else ""),
+                    f"n_chunks={a.chunks} bf16" + ("" if a.gate == "switch" else f" gate={a.gate}"),
         "tokens_per_gpu": a.tokens, "d_model": a.d, "d_ffn": a.f, "experts": a.experts,
         "top_k": a.k, "capacity_factor": a.cf, "n_chunks": a.chunks, "routing_skew_beta": a.beta,
         "gate": a.gate,
@@ -407,6 +408,8 @@ def run_lancet(a, world, rank, local_rank):
     flags = a.flags & ~lancet.FLAG_TIMELINE
     if a.gate == "bpr":
         flags |= lancet.FLAG_GATE_BPR
+    elif a.gate == "random":
+        flags |= lancet.FLAG_GATE_RANDOM
     cfg = lancet.LayerConfig(d_model=a.d, d_ffn=a.f, n_experts=a.experts, max_tokens=a.tokens,
                              max_k=a.k, max_chunks=max(8, a.chunks), dtype="bf16", flags=flags)
     ctx = make_context(a, lancet, cfg, world, rank, local_rank, dev)

@@ -111,13 +111,20 @@ enum {
                                            partition after it (fig:part_after_gate, L271), so
                                            chunked == unchunked as with the Switch gate.
                                            Costs two more routing kernels per forward        */
-    LANCET_FLAG_DEFER_DW = 1u << 12     /* backward: do not enqueue this layer's dW GEMMs; they
+    LANCET_FLAG_DEFER_DW = 1u << 12,    /* backward: do not enqueue this layer's dW GEMMs; they
                                            stay pending (dW1 and dW2 separately) until
                                            lancet_moe_backward_dw or another context's filler
                                            slot enqueues them (cross-layer dW scheduling,
                                            PAPER.md L156, L348-L398; R17).  The next
                                            forward fails with LANCET_ERR_STATE while any are
                                            pending                                           */
+    LANCET_FLAG_GATE_RANDOM = 1u << 13  /* Random gating (R18): token
+                                           t's j-th expert is drawn by SplitMix64 from counter
+                                           8t + j and the seed of lancet_set_gate_seed (distinct
+                                           experts, uniform), combine weights 1/k, token-major
+                                           admission.  No gate network: Wg is not read, logits
+                                           are reported as 0, dwg is 0 and dx has no gate term.
+                                           Exclusive with LANCET_FLAG_GATE_BPR (ERR_ARG)       */
 };
 
 typedef struct {
@@ -194,6 +201,9 @@ lancet_status lancet_peer_import(lancet_ctx* ctx, const void* blobs /* host, wor
 lancet_status lancet_destroy(lancet_ctx* ctx);
 
 lancet_status lancet_set_flags(lancet_ctx* ctx, uint32_t flags);
+
+/* Seed of the Random gate (LANCET_FLAG_GATE_RANDOM) for the following forwards; default 0. */
+lancet_status lancet_set_gate_seed(lancet_ctx* ctx, uint64_t seed);
 
 /* Forward of the MoE layer (collective when world > 1).
  *   x   [T][d]      dtype   caller-owned; must stay valid and unmodified until backward

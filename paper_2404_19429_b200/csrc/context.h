@@ -111,6 +111,7 @@ struct lancet_ctx {
     int launches_fwd = 0, launches_bwd = 0;
 
     // cross-layer dW scheduling (LANCET_FLAG_DEFER_DW, R17)
+    uint64_t gate_seed = 0;          // Random gate (LANCET_FLAG_GATE_RANDOM, R18)
     int dw_pending = 0;              // bit 0: dW1, bit 1: dW2 of the last backward not enqueued
     float* pend_dw1 = nullptr;  float* pend_dw2 = nullptr;
     cudaEvent_t ev_dw_ready = nullptr;   // after the last backward's dX GEMMs

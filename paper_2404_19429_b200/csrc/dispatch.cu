@@ -232,7 +232,9 @@ combine_bwd_kernel(const Elt* __restrict__ dy, const Elt* __restrict__ comb,
 #pragma unroll
         for (int j = 0; j < KK; ++j)
             if (j < k && ids[j] == e) { gt = gj[j]; wsel = wj[j]; sel = true; }
-        dlogit[(size_t)t * E + e] = renorm ? (sel ? wsel * (gt - sg) : 0.f) : (expf(lr[e] - m) / se) * (gt - sg);
+        // renorm == 2: Random gate, no gate network (R18)
+        dlogit[(size_t)t * E + e] = renorm == 2 ? 0.f
+                                  : renorm ? (sel ? wsel * (gt - sg) : 0.f) : (expf(lr[e] - m) / se) * (gt - sg);
     }
 }
 

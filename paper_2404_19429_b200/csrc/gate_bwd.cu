@@ -757,6 +757,15 @@ static bool stream_ok(int d, int E) { return E <= 8 && d % 256 == 0 && d <= 2048
 // E = 8 EG, EG in {2, 4, 8}: the wide streaming K6 / K7
 static bool wide_ok(int d, int E) { return (E == 16 || E == 32 || E == 64) && d % 256 == 0 && d <= 2048; }
 bool gate_bwd_needs_wgT(int d, int E) { return !stream_ok(d, E) && !(wide_ok(d, E) && E >= 32); }
+// Blocks for a per-block token range whose staged rows cost per_tok bytes of shared memory
+// beside a fixed ring: at least `want` blocks, more if the range would not fit (large T).
+static int blocks_for_smem(int ntok, int want, size_t ring, size_t per_tok)
+{
+    const size_t budget = 200 * 1024;
+    const int max_tpb = std::max(1, (int)((budget - std::min(ring, budget - per_tok)) / per_tok));
+    return std::max(want, ceil_div(ntok, max_tpb));
+}
+
 // dim groups per block for EG lanes per group (<= 256 threads, dividing d / 8)
 static int wide_ntd(int d, int EG)
 {
@@ -774,7 +783,8 @@ static void launch_k6_stream(const DispatchArgs& a, const void* dxe, const int* 
     const int NT = a.d / 8;
     // ~3 blocks per SM of 128 threads; a block's ring is kStreamStages slots of U tokens
     const int per_sm = std::max(1, 384 / NT);
-    const int nb = std::max(1, std::min(ceil_div(t1 - t0, G::U), per_sm * num_sms));
+    const int nb = blocks_for_smem(t1 - t0, std::max(1, std::min(ceil_div(t1 - t0, G::U), per_sm * num_sms)),
+                                   (size_t)kStreamStages * G::SLOT * NT * 16, (size_t)(KK + EE) * 4);
     const int tpb = ceil_div(t1 - t0, nb);
     const size_t smem = (size_t)kStreamStages * G::SLOT * NT * 16 + (size_t)tpb * (KK + EE) * 4;
     static bool attr = false;
@@ -797,7 +807,8 @@ static void launch_k6_wide(const DispatchArgs& a, const void* dxe, const int* pr
 {
     using G = K6Geom<Elt, KK>;
     const int NTD = wide_ntd(a.d, EG), DS = a.d / 8 / NTD, NT = NTD * EG;
-    const int nb = std::max(1, std::min(ceil_div(t1 - t0, G::U), std::max(1, 3 * num_sms / DS)));
+    const int nb = blocks_for_smem(t1 - t0, std::max(1, std::min(ceil_div(t1 - t0, G::U), std::max(1, 3 * num_sms / DS))),
+                                   (size_t)kStreamStages * G::SLOT * NTD * 16, (size_t)(KK + 8 * EG) * 4);
     const int tpb = ceil_div(t1 - t0, nb);
     const size_t smem = (size_t)kStreamStages * G::SLOT * NTD * 16 + (size_t)tpb * (KK + 8 * EG) * 4;
     static bool attr = false;
@@ -873,7 +884,10 @@ static void launch_dwg_stream(const Elt* x, const float* dlogit, int T, int d, i
     constexpr int NV = Dims8<Elt>::NV, U = 8 / NV;
     const int NT = d / 8;
     const int per_sm = std::max(1, 256 / NT);       // fewer, fatter blocks: fewer partials
-    const int nb = std::max(1, std::min({ceil_div(T, 2 * U), per_sm * num_sms, kDwgStreamMaxBlocks}));
+    const int nb = std::min(kDwgStreamMaxBlocks,
+                            blocks_for_smem(T, std::max(1, std::min({ceil_div(T, 2 * U), per_sm * num_sms,
+                                                                     kDwgStreamMaxBlocks})),
+                                            (size_t)kDwgStages * U * NV * NT * 16, (size_t)EE * 4));
     const int tpb = ceil_div(T, nb);
     const int grid = ceil_div(T, tpb);
     const size_t smem = (size_t)kDwgStages * U * NV * NT * 16 + (size_t)tpb * EE * 4;
@@ -894,7 +908,11 @@ static void launch_dwg_wide(const Elt* x, const float* dlogit, int T, int d, int
 {
     constexpr int NV = Dims8<Elt>::NV, U = 8 / NV;
     const int NTD = wide_ntd(d, EG), DS = d / 8 / NTD, NT = NTD * EG;
-    const int nb = std::max(1, std::min({ceil_div(T, 2 * U), std::max(1, 2 * num_sms / DS), kDwgStreamMaxBlocks}));
+    // the per-block dlogit rows must fit beside the ring (T = 64k at E = 64: 94 blocks, not 74)
+    const int nb = std::min(kDwgStreamMaxBlocks,
+                            blocks_for_smem(T, std::max(1, std::min({ceil_div(T, 2 * U), std::max(1, 2 * num_sms / DS),
+                                                                     kDwgStreamMaxBlocks})),
+                                            (size_t)kDwgStages * U * NV * NTD * 16, (size_t)8 * EG * 4));
     const int tpb = ceil_div(T, nb);
     const int grid = ceil_div(T, tpb);
     const size_t smem = (size_t)kDwgStages * U * NV * NTD * 16 + (size_t)tpb * 8 * EG * 4;
@@ -952,7 +970,10 @@ static void launch_fused(const DispatchArgs& a, const void* dxe, const int* prow
     using G = FusedGeom<Elt, KK>;
     const int NT = a.d / 8;
     const int per_sm = std::max(1, 256 / NT);
-    const int nb = std::max(1, std::min({ceil_div(a.T, 4 * G::U), per_sm * num_sms, kDwgStreamMaxBlocks}));
+    const int nb = std::min(kDwgStreamMaxBlocks,
+                            blocks_for_smem(a.T, std::max(1, std::min({ceil_div(a.T, 4 * G::U), per_sm * num_sms,
+                                                                       kDwgStreamMaxBlocks})),
+                                            (size_t)kFusedStages * G::SLOT * NT * 16, (size_t)(KK + EE) * 4));
     const int tpb = ceil_div(a.T, nb);
     const int grid = ceil_div(a.T, tpb);
     const size_t smem = (size_t)kFusedStages * G::SLOT * NT * 16 + (size_t)tpb * (KK + EE) * 4;

@@ -50,6 +50,9 @@ struct RouteArgs {
     unsigned char* bpr_adm; // [T*k]  1 = admitted by priority
     int* hist2;           // [n_tiles][E] admitted pairs per token tile
     int* bpr_meta;        // [E]      pairs routed to e
+    // Random gate (R18; random != 0): SplitMix64 draws instead of K1, x and Wg unused
+    int random;
+    unsigned long long seed;
 };
 // Enqueues memset(hist) + K1 + K2 (K2 = three kernels under BPR).  Returns the number of kernels
 // launched.

@@ -765,6 +765,9 @@ LANCET_API lancet_status lancet_moe_forward(lancet_ctx* c, const void* x, const 
     ra.logits = c->logits; ra.idx = c->idx; ra.w = c->w; ra.slot = c->slot; ra.hist = c->hist;
     ra.S = c->S; ra.send_rows = c->send_rows; ra.send_off = c->send_off;
     ra.bpr = (c->cfg.flags & LANCET_FLAG_GATE_BPR) ? 1 : 0;
+    ra.random = (c->cfg.flags & LANCET_FLAG_GATE_RANDOM) ? 1 : 0;
+    ra.seed = c->gate_seed;
+    if (ra.bpr && ra.random) return fail(c, LANCET_ERR_ARG, "LANCET_FLAG_GATE_BPR and LANCET_FLAG_GATE_RANDOM are exclusive");
     ra.score = c->bpr_score; ra.list = c->bpr_list; ra.bpr_adm = c->bpr_adm; ra.hist2 = c->bpr_hist;
     ra.bpr_meta = c->bpr_meta;
     DispatchArgs da{T, k, d, E, c->idx, c->slot, c->w, c->send_off, c->send_rows};
@@ -999,7 +1002,7 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream_);
     lancet::g_pdl = (c->cfg.flags & LANCET_FLAG_NO_PDL) == 0;
     const int E = c->cfg.n_experts, d = c->cfg.d_model, T = c->T, k = c->k, n = c->n;
-    const int renorm = (c->cfg.flags & LANCET_FLAG_RENORMALIZE) ? 1 : 0;
+    const int renorm = (c->cfg.flags & LANCET_FLAG_GATE_RANDOM) ? 2 : (c->cfg.flags & LANCET_FLAG_RENORMALIZE) ? 1 : 0;
     c->launches_bwd = 0;
     int& L = c->launches_bwd;
     DispatchArgs da{T, k, d, E, c->idx, c->slot, c->w, c->send_off, c->send_rows};
@@ -1248,6 +1251,14 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
         CK(cudaEventRecord(e2, sm));
         CK(cudaStreamWaitEvent(s, e2, 0));
     }
+    return LANCET_OK;
+}
+
+LANCET_API lancet_status lancet_set_gate_seed(lancet_ctx* c, uint64_t seed)
+{
+    lancet_status st = check_ready(c);
+    if (st) return st;
+    c->gate_seed = seed;
     return LANCET_OK;
 }
 

@@ -460,6 +460,49 @@ gate_stream_kernel(const Elt* __restrict__ x, const float* __restrict__ wg, int 
     }
 }
 
+// K1 for the Random gate (R18): thread per token, block = one scan
+// tile.  Draw j of token t: r = splitmix64(8t + j) mod (E - j), the r-th expert not drawn
+// before (walking the earlier draws in increasing order); weights 1/k; logits reported as 0.
+__device__ __forceinline__ unsigned long long splitmix64_at(unsigned long long key, unsigned long long seed)
+{
+    unsigned long long z = seed + (key + 1ull) * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__global__ void __launch_bounds__(kScanTile)
+random_gate_kernel(int T, int E, int k, unsigned long long seed, float* __restrict__ logits,
+                   int* __restrict__ idx_out, float* __restrict__ w_out, int* __restrict__ hist)
+{
+    pdl_wait();   // programmatic dependent launch: predecessor's writes visible
+    __shared__ int sh_hist[kMaxExperts];
+    const int tid = threadIdx.x;
+    for (int e = tid; e < E; e += blockDim.x) sh_hist[e] = 0;
+    __syncthreads();
+    const int t = blockIdx.x * kScanTile + tid;
+    if (t < T) {
+        int sorted[kMaxK];                              // earlier draws, ascending
+        const float wk = 1.0f / (float)k;
+        for (int j = 0; j < k; ++j) {
+            int e = (int)(splitmix64_at(8ull * (unsigned long long)t + (unsigned long long)j, seed) %
+                          (unsigned long long)(E - j));
+            int pos = 0;
+            for (int q = 0; q < j; ++q) {               // r-th free expert
+                if (sorted[q] <= e) { ++e; pos = q + 1; }
+            }
+            for (int q = j; q > pos; --q) sorted[q] = sorted[q - 1];
+            sorted[pos] = e;
+            idx_out[(size_t)t * k + j] = e;
+            w_out[(size_t)t * k + j] = wk;
+            atomicAdd(&sh_hist[e], 1);
+        }
+        for (int e = 0; e < E; ++e) logits[(size_t)t * E + e] = 0.f;
+    }
+    __syncthreads();
+    for (int e = tid; e < E; e += blockDim.x) hist[blockIdx.x * E + e] = sh_hist[e];
+}
+
 // The slot scan (K2) runs in one of three modes:
 //   SCAN_SLOTS      token-major admission (R7): slot = P_e(t) if < C, capacity state S, offsets;
 //   SCAN_BPR_LIST   Batch Prioritized Routing, pass 1 (R16): the unclamped P_e(t) of every pair
@@ -772,7 +815,10 @@ int launch_routing(const RouteArgs& a, bool is_bf16, cudaStream_t s)
         attr_set = true;
     }
     const int elt = is_bf16 ? 2 : 4;
-    if (gs_ok(a.d, a.E, elt)) {
+    if (a.random) {
+        launch_k(random_gate_kernel, n_tiles, kScanTile, 0, s, a.T, a.E, a.k, a.seed, a.logits, a.idx, a.w,
+                 a.hist);
+    } else if (gs_ok(a.d, a.E, elt)) {
         static bool gs_attr = false;
         if (!gs_attr) {
             cudaFuncSetAttribute(gate_stream_kernel<bf16, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);

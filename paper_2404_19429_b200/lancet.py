@@ -31,6 +31,7 @@ FLAG_FORCE_EP = 512
 FLAG_TIMELINE_GEMM_ONLY = 1024
 FLAG_GATE_BPR = 2048
 FLAG_DEFER_DW = 4096
+FLAG_GATE_RANDOM = 8192
 # LANCET_EXTRA_FLAGS: OR'ed into every context's flags (e.g. run the test suite under PDL)
 EXTRA_FLAGS = int(os.environ.get("LANCET_EXTRA_FLAGS", "0"), 0)
 
@@ -40,7 +41,8 @@ EXPORTS = ["lancet_abi_version", "lancet_last_error", "lancet_nccl_unique_id", "
            "lancet_get_counts", "lancet_timeline_begin", "lancet_last_timeline", "lancet_debug_copy",
            "lancet_workspace_bytes", "lancet_launch_counts", "lancet_plan_exchange",
            "lancet_create_peer", "lancet_peer_blob_bytes", "lancet_peer_export", "lancet_peer_import",
-           "lancet_moe_backward_dw", "lancet_set_dw_fillers", "lancet_dw_schedule", "lancet_stack_dw_plan"]
+           "lancet_moe_backward_dw", "lancet_set_dw_fillers", "lancet_dw_schedule", "lancet_stack_dw_plan",
+           "lancet_set_gate_seed"]
 
 
 class LancetError(RuntimeError):
@@ -101,6 +103,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "lancet_launch_counts": ([P, ctypes.POINTER(I32), ctypes.POINTER(I32)], I32),
             "lancet_plan_exchange": ([I32, I32, I32, P, P, P, P, P, P, P, ctypes.POINTER(I32)], I32),
             "lancet_moe_backward_dw": ([P, I32, P], I32),
+            "lancet_set_gate_seed": ([P, ctypes.c_uint64], I32),
             "lancet_set_dw_fillers": ([P, I32, P, P, P], I32),
             "lancet_dw_schedule": ([I32, P, P, I32, P, P], I32),
             "lancet_stack_dw_plan": ([I32, I32, P, P, P, P], I32),
@@ -331,6 +334,10 @@ class Context:
                                                 _ptr(dw2), _stream(stream))
         _check(st, self._p)
         return dx, dwg, dw1, dw2
+
+    def set_gate_seed(self, seed: int):
+        """Seed of the Random gate (FLAG_GATE_RANDOM) for the following forwards."""
+        _check(load_library().lancet_set_gate_seed(self._p, seed & ((1 << 64) - 1)), self._p)
 
     # -- cross-layer dW scheduling (DESIGN.md R17) ---------------------------------------------
     def backward_dw(self, which: int = 3, stream=None):

@@ -68,10 +68,10 @@ def run_gpu(ins, E, k, cf, n, dtype="bf16", act="gelu_tanh", flags=0, backward=T
 
 
 def run_oracle(ins, k, cf, n, act="gelu_tanh", renorm=False, backward=True, token_subset=None,
-               gate="switch"):
+               gate="switch", seed=0):
     from oracle import moe
     fwd = moe.forward([ins["x"]], ins["wg"], [ins["w1"]], [ins["w2"]], k, cf, n, act=act,
-                      renormalize=renorm, token_subset=token_subset, gate=gate)
+                      renormalize=renorm, token_subset=token_subset, gate=gate, seed=seed)
     out = dict(fwd=fwd, y=fwd.y[0], rt=fwd.routing[0])
     if backward:
         b = moe.backward(fwd, [ins["x"]], ins["wg"], [ins["w1"]], [ins["w2"]], [ins["dy"]],

@@ -313,3 +313,17 @@ def test_peer_context_requires_import():
                                 ctypes.c_float(1.0), 2, y.data_ptr(), None, None, None, None)
     assert st == 5                                               # ERR_STATE
     assert lib.lancet_destroy(p) == 0
+
+
+@pytest.mark.parametrize("E", [32, 64])
+def test_large_token_count_gate_backward(E):
+    # T = 64k with many experts: the streaming K6/K7 stage per-block dlogit rows in shared
+    # memory, which must be split over more blocks at this size (a launch once failed here);
+    # identity experts keep the oracle cheap (routing, y, dx, dWg against it)
+    T, d, k, cf, n = 65536, 1024, 2, 1.25, 4
+    ins = inputs(T, d, 8, E, k, beta=0.25, seed=64)
+    g = run_gpu(ins, E, k, cf, n, act="identity_expert")
+    o = run_oracle(ins, k, cf, n, act="identity_expert")
+    assert_routing_exact(g, o)
+    for key in ("y", "dx", "dwg"):
+        assert normwise(g[key], o[key]) <= TOL["bf16"], key
