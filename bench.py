@@ -550,6 +550,31 @@ def run_lancet(a, world, rank, local_rank):
             if o == "gate":
                 kernels[o]["note"] = ("event span of K1 + K2 (gate, slot scan and the histogram "
                                       "memset); bytes are the gate's")
+    # isolated durations of the same kernels from the committed ncu capture (cold cache,
+    # serialised, --clock-control none): the in-step event spans above include launch gaps
+    # and lose programmatic dependent launch at every event record
+    iso = os.path.join(ROOT, "profiles", "ncu_simt_traffic.json")
+    if os.path.exists(iso) and a.tokens == 16384 and a.experts == 8 and a.d == 1024:
+        try:
+            launches = json.load(open(iso))["launches"]
+            names = {"gate": ["gate_stream"], "permute": ["permute_kernel"], "combine": ["combine_kernel"],
+                     "combine_bwd": ["combine_bwd"], "unpermute_gate_bwd": ["k6_stream"],
+                     "gate_dwg": ["dwg_stream", "dwg_reduce4"]}
+            for o, pats in names.items():
+                if o not in kernels or o not in mem_bytes:
+                    continue
+                us = []
+                for pat in pats:
+                    m = [l["us"] for l in launches if pat in l["kernel"] and
+                         not (pat == "combine_kernel" and "bwd" in l["kernel"])]
+                    if m:
+                        us.append(min(m))
+                if len(us) == len(pats):
+                    t = sum(us)
+                    kernels[o]["ncu_isolated_us"] = t
+                    kernels[o]["hbm_frac_isolated"] = mem_bytes[o] / (t * 1e-6) / 1e9 / pk["hbm"]
+        except Exception:  # noqa: BLE001
+            pass
     for o, v in ops.items():
         if o not in kernels:
             kernels[o] = {"us": v["us_per_step"]}
