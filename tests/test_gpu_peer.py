@@ -47,7 +47,7 @@ def oracle(G, spec):
     xs = [i["x"] for i in ins]
     act = spec.get("act", "gelu_tanh")
     fwd = moe.forward(xs, ins[0]["wg"], [i["w1"] for i in ins], [i["w2"] for i in ins], spec["k"], spec["cf"],
-                      spec["n"], act=act)
+                      spec["n"], act=act, gate=spec.get("gate", "switch"))
     b = moe.backward(fwd, xs, ins[0]["wg"], [i["w1"] for i in ins], [i["w2"] for i in ins],
                      [i["dy"] for i in ins], act=act)
     return fwd, b
@@ -72,3 +72,21 @@ def test_peer_transport_matches_oracle(tmp_path, G, Ts, E, k, n, repeat, act):
             ref.update(dw1=b["dw1"][r], dw2=b["dw2"][r])
         for key in keys:
             assert normwise(res[r][key], ref[key]) <= TOL["bf16"], (r, key, normwise(res[r][key], ref[key]))
+
+
+@pytest.mark.parametrize("gate", ["bpr", "random"])
+def test_peer_transport_gate_variants(tmp_path, gate):
+    # Batch Prioritized and Random gates over two processes with binding capacity (drops)
+    from paper_2404_19429_b200 import FLAG_GATE_BPR, FLAG_GATE_RANDOM
+    G = 2
+    spec = dict(Ts=[640, 577], d=128, f=256, E=8, k=2, n=3, cf=0.75, seed=77, repeat=2, gate=gate,
+                flags=FLAG_GATE_BPR if gate == "bpr" else FLAG_GATE_RANDOM)
+    res = run_peer(tmp_path, G, **spec)
+    fwd, b = oracle(G, spec)
+    for r in range(G):
+        rt = fwd.routing[r]
+        assert np.any(rt.slot < 0)
+        assert np.array_equal(res[r]["idx"], rt.idx) and np.array_equal(res[r]["slot"], rt.slot)
+        for key, ref in (("y", fwd.y[r]), ("dx", b["dx"][r]), ("dwg", b["dwg"][r]),
+                         ("dw1", b["dw1"][r]), ("dw2", b["dw2"][r])):
+            assert normwise(res[r][key], ref) <= TOL["bf16"], (r, key)

@@ -84,3 +84,23 @@ def test_random_gate_excludes_bpr():
         run_gpu(ins, 4, 2, 1.0, 1, ctx=ctx, backward=False)
     assert e.value.status == 1
     ctx.close()
+
+
+def test_random_gate_expert_parallel_matches_oracle():
+    # two simulated ranks (lancet_local_group), seed 0 on every rank: the draws depend on the
+    # rank-local token index only (R18)
+    from oracle import moe
+    from paper_2404_19429_b200 import FLAG_GATE_RANDOM
+    from test_gpu_multirank import make_inputs, oracle_group, run_group
+    G, Ts, E, k, n = 2, [700, 513], 8, 2, 3
+    ins = make_inputs(G, Ts, 128, 256, E, k, seed=41)
+    g = run_group(G, ins, E, k, 0.75, n, flags=FLAG_GATE_RANDOM)
+    fwd, b = oracle_group(ins, k, 0.75, n, gate="random")
+    sends = [rt.counts for rt in fwd.routing]
+    for r in range(G):
+        rt = fwd.routing[r]
+        assert np.array_equal(g[r]["idx"], rt.idx) and np.array_equal(g[r]["slot"], rt.slot)
+        assert np.array_equal(g[r]["recv"], moe.recv_counts(sends, G, r))
+        assert np.all(g[r]["dwg"] == 0)
+        for key, ref in (("y", fwd.y[r]), ("dx", b["dx"][r]), ("dw1", b["dw1"][r]), ("dw2", b["dw2"][r])):
+            assert normwise(g[r][key], ref) <= TOL["bf16"], (r, key)
