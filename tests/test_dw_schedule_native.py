@@ -69,3 +69,12 @@ def test_native_stack_plan_hand_trace():
     hl, ha = lancet.stack_dw_plan([[65.0, 65.0], [65.0, 65.0]], [[230.0, 230.0], [230.0, 230.0]])
     assert hl.tolist() == [[0, -1], [1, 0]]
     assert ha.tolist() == [[1, -1], [1, 0]]
+
+
+def test_native_schedule_argument_errors():
+    import pytest
+    with pytest.raises(lancet.LancetError) as e:
+        lancet.dw_schedule([1, 2], [10.0, 5.0], [(0, 7)])          # edge to a missing instruction
+    assert e.value.status == 1
+    with pytest.raises(lancet.LancetError):
+        lancet.stack_dw_plan(np.zeros((0, 2)), np.zeros((0, 2)))     # no layers
