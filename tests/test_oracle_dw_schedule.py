@@ -140,3 +140,22 @@ def test_exact_guard():
     kinds = [D.A2A] * 5 + [D.DW]
     with pytest.raises(ValueError):
         D.exact_assign(kinds, [1.0] * 6, {a: [5] for a in range(5)})
+
+
+def test_stack_program_greedy_vs_exact():
+    # Alg. 1 on this layer's 2-layer stack program (4 a2a, 4 dW: inside the exact guard) with
+    # random costs: feasible, never above the optimum, and close to it on average
+    r = random.Random(21)
+    kinds, names, edges, idx = D.stack_backward_program(2, 1)
+    sets = D.label_overlappable(kinds, edges)
+    ratios = []
+    for trial in range(200):
+        cost = [0.0] * len(kinds)
+        for i, k in enumerate(kinds):
+            cost[i] = r.uniform(30, 150) if k == D.A2A else (r.uniform(50, 260) if k == D.DW else 5.0)
+        g = D.greedy_assign(kinds, cost, sets)
+        e = D.exact_assign(kinds, cost, sets)
+        og, oe = D.objective(kinds, cost, g), D.objective(kinds, cost, e)
+        assert og <= oe + 1e-9
+        ratios.append(og / oe)
+    assert sum(ratios) / len(ratios) >= 0.9
