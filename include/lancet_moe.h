@@ -118,13 +118,20 @@ enum {
                                            PAPER.md L156, L348-L398; R17).  The next
                                            forward fails with LANCET_ERR_STATE while any are
                                            pending                                           */
-    LANCET_FLAG_GATE_RANDOM = 1u << 13  /* Random gating (R18): token
+    LANCET_FLAG_GATE_RANDOM = 1u << 13, /* Random gating (R18): token
                                            t's j-th expert is drawn by SplitMix64 from counter
                                            8t + j and the seed of lancet_set_gate_seed (distinct
                                            experts, uniform), combine weights 1/k, token-major
                                            admission.  No gate network: Wg is not read, logits
                                            are reported as 0, dwg is 0 and dx has no gate term.
                                            Exclusive with LANCET_FLAG_GATE_BPR (ERR_ARG)       */
+    LANCET_FLAG_PEER_PUSH = 1u << 14    /* peer transport: the dispatch all-to-all is fused into
+                                           the permute kernel -- each admitted row is written
+                                           straight into the owning rank's receive buffer (IPC-
+                                           mapped peer memory; NVLink across GPUs) at its final
+                                           row, one launch per chunk, readiness signalled per
+                                           chunk by flags; no send buffer and no copy-engine
+                                           pass.  Must be set identically on every rank        */
 };
 
 typedef struct {

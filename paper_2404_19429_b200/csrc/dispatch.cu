@@ -91,6 +91,53 @@ permute_kernel(const Elt* __restrict__ x, const int* __restrict__ idx, const int
     }
 }
 
+// K3 + C2 dispatch fused over peer memory (LANCET_FLAG_PEER_PUSH): each admitted row x[t] is
+// written straight into the receive buffer of the rank that owns its expert (an IPC-mapped
+// pointer; over NVLink on a multi-GPU node), at its final row base[e] + slot -- no send buffer,
+// no copy-engine pass.  One launch per chunk (tokens [t0, t1), base = that chunk's table).
+template <typename Elt, int KK>
+__global__ void __launch_bounds__(256)
+permute_push_kernel(const Elt* __restrict__ x, const int* __restrict__ idx, const int* __restrict__ slot,
+                    int t0, int t1, int k, int d, int E_l, const int* __restrict__ base,
+                    char* const* __restrict__ xe_ptrs)
+{
+    pdl_wait();   // programmatic dependent launch: predecessor's writes visible
+    constexpr int V = Vec16<Elt>::N;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int t = t0 + blockIdx.x * kWarpsPerBlock + w;
+    if (t >= t1) return;
+    uint4* dst[KK];
+    int myidx = -1, mys = -1;
+    if (lane < k) {
+        myidx = idx[(size_t)t * k + lane];
+        mys = slot[(size_t)t * k + lane];
+    }
+#pragma unroll
+    for (int j = 0; j < KK; ++j) {
+        const int e = __shfl_sync(0xffffffffu, myidx, j);
+        const int sl = __shfl_sync(0xffffffffu, mys, j);
+        dst[j] = nullptr;
+        if (j < k && sl >= 0)
+            dst[j] = reinterpret_cast<uint4*>(xe_ptrs[e / E_l] + (size_t)(base[e] + sl) * d * sizeof(Elt));
+    }
+    const int nvec = d / V;
+    const uint4* src = reinterpret_cast<const uint4*>(x + (size_t)t * d);
+    constexpr int U = 4;
+    for (int v0 = lane; v0 < nvec; v0 += 32 * U) {
+        uint4 val[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (v0 + 32 * u < nvec) val[u] = ld_nc_v4(src + v0 + 32 * u);
+#pragma unroll
+        for (int j = 0; j < KK; ++j)
+            if (dst[j]) {
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (v0 + 32 * u < nvec) st_v4(dst[j] + v0 + 32 * u, val[u]);
+            }
+    }
+}
+
 template <typename Elt, int KK>
 __global__ void __launch_bounds__(256)
 combine_kernel(const Elt* __restrict__ comb, const int* __restrict__ idx,
@@ -273,6 +320,22 @@ int launch_permute(const DispatchArgs& a, const void* x, void* xs, bool is_bf16,
         else
             launch_k(permute_kernel<float, KK>, grid, 256, 0, s, (const float*)x, a.idx, a.slot, a.T, a.k, a.d,
                                                           a.send_off, a.send_rows, (float*)xs, tok_blocks);
+    });
+    return 1;
+}
+
+int launch_permute_push(const DispatchArgs& a, const void* x, int t0, int t1, int E_l, const int* base,
+                        char* const* xe_ptrs, bool is_bf16, cudaStream_t s)
+{
+    if (t1 <= t0) return 0;
+    const int grid = ceil_div(t1 - t0, kWarpsPerBlock);
+    LANCET_DISPATCH_K(a.k, {
+        if (is_bf16)
+            launch_k(permute_push_kernel<bf16, KK>, grid, 256, 0, s, (const bf16*)x, a.idx, a.slot, t0, t1, a.k,
+                     a.d, E_l, base, xe_ptrs);
+        else
+            launch_k(permute_push_kernel<float, KK>, grid, 256, 0, s, (const float*)x, a.idx, a.slot, t0, t1, a.k,
+                     a.d, E_l, base, xe_ptrs);
     });
     return 1;
 }

@@ -65,6 +65,10 @@ struct DispatchArgs {
     const int* send_off; const int* send_rows;
 };
 int launch_permute(const DispatchArgs& a, const void* x, void* xs, bool is_bf16, cudaStream_t s);
+// K3 fused with the dispatch all-to-all over peer memory: tokens [t0, t1) of one chunk, row
+// x[t] of choice (t, j) -> xe_ptrs[e / E_l] + (base[e] + slot) rows
+int launch_permute_push(const DispatchArgs& a, const void* x, int t0, int t1, int E_l, const int* base,
+                        char* const* xe_ptrs, bool is_bf16, cudaStream_t s);
 int launch_combine(const DispatchArgs& a, const void* comb, void* y, int t0, int t1, bool is_bf16,
                    cudaStream_t s);
 // K5: also writes dlogit [T][E] (softmax Jacobian) and prow [T][k] (packed row or -1)

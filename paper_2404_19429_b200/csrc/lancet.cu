@@ -798,11 +798,16 @@ LANCET_API lancet_status lancet_moe_forward(lancet_ctx* c, const void* x, const 
         size_t ev_i = 0;
         auto next_ev = [&]() { return c->ev_pool[ev_i++]; };
         lancet::PeerLinks* pr = c->peer;
+        const bool push = pr && (c->cfg.flags & LANCET_FLAG_PEER_PUSH);
         if (pr) {
             if (!c->peer_ready) return fail(c, LANCET_ERR_STATE, "peer transport: lancet_peer_import not called");
             ++pr->seq;
             // every peer has pulled the previous step's rows from this rank's pull sources
-            if (peer_wait_consumed(c, sc)) return fail(c, LANCET_ERR_CUDA, "cuStreamWaitValue32");
+            if (peer_wait_consumed(c, sc, push)) return fail(c, LANCET_ERR_CUDA, "cuStreamWaitValue32");
+            // push-dispatch: this rank's receive buffer is free for the step's pushes (its
+            // GEMMs of the previous step are behind on this stream, its pull readers done)
+            if (push && peer_signal(c, 0, lancet::PK_XEFREE, 0, sc))
+                return fail(c, LANCET_ERR_CUDA, "cuStreamWriteValue32");
         }
 
         { OpScope op(c, "gate", 0, -1, sc); L += launch_routing(ra, c->bf16, sc); }
@@ -834,14 +839,17 @@ LANCET_API lancet_status lancet_moe_forward(lancet_ctx* c, const void* x, const 
             }
             CK(cudaEventRecord(c->ev_counts, sm));
         }
-        // K3 permute overlaps the size exchange
-        { OpScope op(c, "permute", 0, -1, sc); L += launch_permute(da, x, c->xs, c->bf16, sc); }
-        CHECK_LAUNCH();
+        // K3 permute overlaps the size exchange (push-dispatch: permute fused with the
+        // exchange after the plan, below)
         const bool serial_ = c->cfg.flags & LANCET_FLAG_SERIAL;
         const int nc_ = serial_ ? 1 : n;
-        if (pr)             // the dispatch sources of every chunk are ready
-            for (int cc = 0; cc < nc_; ++cc)
-                if (peer_signal(c, 0, lancet::PK_XS, cc, sc)) return fail(c, LANCET_ERR_CUDA, "cuStreamWriteValue32");
+        if (!push) {
+            { OpScope op(c, "permute", 0, -1, sc); L += launch_permute(da, x, c->xs, c->bf16, sc); }
+            CHECK_LAUNCH();
+            if (pr)         // the dispatch sources of every chunk are ready
+                for (int cc = 0; cc < nc_; ++cc)
+                    if (peer_signal(c, 0, lancet::PK_XS, cc, sc)) return fail(c, LANCET_ERR_CUDA, "cuStreamWriteValue32");
+        }
         cudaEvent_t ev_perm = next_ev();
         CK(cudaEventRecord(ev_perm, sc));
         CK(cudaEventSynchronize(c->ev_counts));            // the one host synchronisation
@@ -871,6 +879,30 @@ LANCET_API lancet_status lancet_moe_forward(lancet_ctx* c, const void* x, const 
         CK(cudaMemcpyAsync(c->grp_dev, c->h_grp, sizeof(int) * 2 * n * E_l, cudaMemcpyHostToDevice, sc));
         L += launch_zero_pads(c->xe, d, d_grp_off, d_grp_rows, n * E_l, (int)c->elt, sc);
         CHECK_LAUNCH();
+        if (push) {
+            // K3 + C2 fused: each chunk's admitted rows go straight into the owners' receive
+            // buffers at their final rows: base[c][e] = (owner's group offset of (e, c)) +
+            // (this rank's row offset inside it, R12) - S[e][c]
+            const int me = c->rank;
+            std::vector<int> base((size_t)n * E);
+            for (int ch = 0; ch < n; ++ch)
+                for (int e = 0; e < E; ++e) {
+                    const int p = e / E_l, el = e % E_l;
+                    base[(size_t)ch * E + e] = gp.rank[p].grp_off[ch * E_l + el] +
+                                               gp.rank[p].src_off[(me * E_l + el) * n + ch] -
+                                               gp.rank[me].S[e * (n + 1) + ch];
+                }
+            CK(cudaMemcpyAsync(pr->d_push_base, base.data(), sizeof(int) * base.size(), cudaMemcpyHostToDevice, sc));
+            // every owner's receive buffer is free for this step
+            if (peer_wait_all(c, lancet::PK_XEFREE, 0, sc)) return fail(c, LANCET_ERR_CUDA, "cuStreamWaitValue32");
+            for (int ch = 0; ch < n; ++ch) {
+                OpScope op(c, "a2a_dispatch_push", 1, serial ? -1 : ch, sc);
+                L += launch_permute_push(da, x, chunk_start(T, n, ch), chunk_start(T, n, ch + 1), E_l,
+                                         pr->d_push_base + (size_t)ch * E, pr->d_xe, c->bf16, sc);
+                if (peer_signal(c, 0, lancet::PK_PUSH, ch, sc)) return fail(c, LANCET_ERR_CUDA, "cuStreamWriteValue32");
+            }
+            CHECK_LAUNCH();
+        }
         const size_t rowb = (size_t)d * c->elt;
         char* xs = (char*)c->xs;
         char* xe = (char*)c->xe;
@@ -889,6 +921,15 @@ LANCET_API lancet_status lancet_moe_forward(lancet_ctx* c, const void* x, const 
             int c0, c1;
             chunk_range(cc, c0, c1);
             OpScope op(c, "a2a_dispatch", 1, serial ? -1 : cc, sm);
+            if (push) {         // every rank's rows of these chunks have landed in xe
+                for (int ch = c0; ch < c1; ++ch)
+                    if (peer_wait_all(c, lancet::PK_PUSH, ch, sm)) return fail(c, LANCET_ERR_CUDA, "cuStreamWaitValue32");
+                if (ident && peer_signal(c, 0, lancet::PK_OUT, cc, sm))
+                    return fail(c, LANCET_ERR_CUDA, "cuStreamWriteValue32");
+                ev_disp[cc] = next_ev();
+                CK(cudaEventRecord(ev_disp[cc], sm));
+                continue;
+            }
             if (pr) {
                 std::string err;
                 if (peer_pull(c, lancet::PK_XS, cc, gp.pulls(c->rank, true, c0, c1, xe, rowb), cc == nc - 1, sm, err))

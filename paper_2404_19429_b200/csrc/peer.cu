@@ -53,7 +53,7 @@ const MemOps& memops()
     return ops;
 }
 
-constexpr int kBufs = 6;   // exported: xs, out-source, dcomb, dXe-source, counts, flags
+constexpr int kBufs = 7;   // exported: xs, out-source, dcomb, dXe-source, counts, flags, xe
 
 }  // namespace
 
@@ -81,6 +81,12 @@ int peer_init(lancet_ctx* c, std::string& err)
         return 1;
     }
     cudaMemset(pl->my_flags, 0, sizeof(uint32_t) * peer_flag_words(G, pl->n_max));
+    if (cudaMalloc(&pl->d_xe, sizeof(char*) * G) != cudaSuccess ||
+        cudaMalloc(&pl->d_push_base, sizeof(int) * (size_t)pl->n_max * E) != cudaSuccess) {
+        err = "cudaMalloc (push tables)";
+        return 1;
+    }
+    pl->xe.assign(G, nullptr);
     for (int k = 0; k <= PK_DXE; ++k) pl->src[k].assign(G, nullptr);
     pl->counts.assign(G, nullptr);
     pl->flags.assign(G, nullptr);
@@ -104,7 +110,7 @@ int peer_export(lancet_ctx* c, void* blob, std::string& err)
 {
     PeerLinks* pl = c->peer;
     void* bufs[kBufs] = {local_src(c, PK_XS), local_src(c, PK_OUT), local_src(c, PK_DCOMB),
-                         local_src(c, PK_DXE), pl->my_counts, pl->my_flags};
+                         local_src(c, PK_DXE), pl->my_counts, pl->my_flags, c->xe};
     auto* h = reinterpret_cast<cudaIpcMemHandle_t*>(blob);
     for (int i = 0; i < kBufs; ++i)
         if (cudaIpcGetMemHandle(&h[i], bufs[i]) != cudaSuccess) {
@@ -124,6 +130,7 @@ int peer_import(lancet_ctx* c, const void* blobs, std::string& err)
             for (int k = 0; k <= PK_DXE; ++k) m[k] = local_src(c, k);
             m[4] = pl->my_counts;
             m[5] = pl->my_flags;
+            m[6] = c->xe;
         } else {
             const auto* h = reinterpret_cast<const cudaIpcMemHandle_t*>(
                 reinterpret_cast<const char*>(blobs) + (size_t)p * peer_blob_bytes());
@@ -138,6 +145,11 @@ int peer_import(lancet_ctx* c, const void* blobs, std::string& err)
         for (int k = 0; k <= PK_DXE; ++k) pl->src[k][p] = reinterpret_cast<char*>(m[k]);
         pl->counts[p] = reinterpret_cast<int*>(m[4]);
         pl->flags[p] = reinterpret_cast<uint32_t*>(m[5]);
+        pl->xe[p] = reinterpret_cast<char*>(m[6]);
+    }
+    if (cudaMemcpy(pl->d_xe, pl->xe.data(), sizeof(char*) * G, cudaMemcpyHostToDevice) != cudaSuccess) {
+        err = "cudaMemcpy (peer receive-buffer table)";
+        return 1;
     }
     return 0;
 }
@@ -149,6 +161,8 @@ void peer_destroy(lancet_ctx* c)
     for (void* p : pl->opened) cudaIpcCloseMemHandle(p);
     if (pl->my_counts) cudaFree(pl->my_counts);
     if (pl->my_flags) cudaFree(pl->my_flags);
+    if (pl->d_xe) cudaFree(pl->d_xe);
+    if (pl->d_push_base) cudaFree(pl->d_push_base);
     if (pl->h_matrix) cudaFreeHost(pl->h_matrix);
     delete pl;
     c->peer = nullptr;
@@ -178,13 +192,25 @@ int peer_wait(lancet_ctx* c, int consumed, int kind, int chunk, int r, uint32_t 
 
 // before this step overwrites any pull source: every peer has pulled the previous step's rows
 // of every kind
-int peer_wait_consumed(lancet_ctx* c, cudaStream_t s)
+int peer_wait_consumed(lancet_ctx* c, cudaStream_t s, bool push)
 {
     PeerLinks* pl = c->peer;
     if (pl->seq <= 1) return 0;
-    for (int kind = 0; kind <= PK_DXE; ++kind)
+    for (int kind = 0; kind <= PK_DXE; ++kind) {
+        if (push && kind == PK_XS) continue;           // push-dispatch: nobody pulls the send rows
         for (int r = 0; r < pl->world; ++r)
             if (peer_wait(c, 1, kind, 0, r, pl->seq - 1, s)) return 1;
+    }
+    return 0;
+}
+
+// push-dispatch: wait until every peer's receive buffer is free for this step, and (after the
+// push of chunk `chunk`) until every peer's rows of chunk `chunk` have landed in ours
+int peer_wait_all(lancet_ctx* c, int kind, int chunk, cudaStream_t s)
+{
+    PeerLinks* pl = c->peer;
+    for (int r = 0; r < pl->world; ++r)
+        if (peer_wait(c, 0, kind, chunk, r, pl->seq, s)) return 1;
     return 0;
 }
 

@@ -32,6 +32,7 @@ FLAG_TIMELINE_GEMM_ONLY = 1024
 FLAG_GATE_BPR = 2048
 FLAG_DEFER_DW = 4096
 FLAG_GATE_RANDOM = 8192
+FLAG_PEER_PUSH = 16384
 # LANCET_EXTRA_FLAGS: OR'ed into every context's flags (e.g. run the test suite under PDL)
 EXTRA_FLAGS = int(os.environ.get("LANCET_EXTRA_FLAGS", "0"), 0)
 

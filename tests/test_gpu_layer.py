@@ -327,3 +327,27 @@ def test_large_token_count_gate_backward(E):
     assert_routing_exact(g, o)
     for key in ("y", "dx", "dwg"):
         assert normwise(g[key], o[key]) <= TOL["bf16"], key
+
+
+@pytest.mark.parametrize("n,act", [(1, "gelu_tanh"), (3, "gelu_tanh"), (2, "identity_expert")])
+def test_push_dispatch_is_bitwise_the_pull_path(n, act):
+    # LANCET_FLAG_PEER_PUSH: permute fused with the dispatch exchange (rows written straight into
+    # the owner's receive buffer) over a one-rank peer group: same rows at the same positions,
+    # so every output equals the copy-engine pull path bit for bit; two steps (buffer reuse)
+    from paper_2404_19429_b200 import FLAG_PEER_PUSH, lancet
+    T, d, f, E, k = 2000, 256, 512, 8, 2
+    ins = inputs(T, d, f, E, k, beta=0.5, seed=91 + n)
+    outs = {}
+    for name, fl in (("pull", 0), ("push", FLAG_PEER_PUSH)):
+        cfg = lancet.LayerConfig(d_model=d, d_ffn=f, n_experts=E, max_tokens=T, max_k=k, max_chunks=8,
+                                 act=act, flags=fl)
+        ctx = lancet.Context(cfg, transport="peer")
+        run_gpu(ins, E, k, 1.0, n, act=act, ctx=ctx)
+        outs[name] = run_gpu(ins, E, k, 1.0, n, act=act, ctx=ctx)
+        ctx.close()
+    keys = ("idx", "slot", "y", "dx", "dwg") + (() if act == "identity_expert" else ("dw1", "dw2"))
+    for key in keys:
+        assert np.array_equal(outs["push"][key], outs["pull"][key]), key
+    o = run_oracle(ins, k, 1.0, n, act=act)
+    for key in ("y", "dx"):
+        assert normwise(outs["push"][key], o[key]) <= TOL["bf16"], key

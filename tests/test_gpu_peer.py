@@ -90,3 +90,24 @@ def test_peer_transport_gate_variants(tmp_path, gate):
         for key, ref in (("y", fwd.y[r]), ("dx", b["dx"][r]), ("dwg", b["dwg"][r]),
                          ("dw1", b["dw1"][r]), ("dw2", b["dw2"][r])):
             assert normwise(res[r][key], ref) <= TOL["bf16"], (r, key)
+
+
+@pytest.mark.parametrize("G,Ts,n,act", [(2, [700, 513], 3, "gelu_tanh"), (4, [300, 420, 256, 333], 4, "gelu_tanh"),
+                                        (2, [500, 450], 2, "identity_expert")])
+def test_peer_push_dispatch_matches_oracle(tmp_path, G, Ts, n, act):
+    # LANCET_FLAG_PEER_PUSH across processes: each rank writes its admitted rows into the
+    # owners' receive buffers; two steps exercise the receive-buffer-free handshake
+    from paper_2404_19429_b200 import FLAG_PEER_PUSH
+    spec = dict(Ts=Ts, d=128, f=256, E=8, k=2, n=n, cf=1.0, seed=60 + G + n, repeat=2, act=act,
+                flags=FLAG_PEER_PUSH)
+    res = run_peer(tmp_path, G, **spec)
+    fwd, b = oracle(G, spec)
+    for r in range(G):
+        rt = fwd.routing[r]
+        assert np.array_equal(res[r]["idx"], rt.idx) and np.array_equal(res[r]["slot"], rt.slot)
+        keys = ("y", "dx", "dwg") + (() if act == "identity_expert" else ("dw1", "dw2"))
+        ref = {"y": fwd.y[r], "dx": b["dx"][r], "dwg": b["dwg"][r]}
+        if act != "identity_expert":
+            ref.update(dw1=b["dw1"][r], dw2=b["dw2"][r])
+        for key in keys:
+            assert normwise(res[r][key], ref[key]) <= TOL["bf16"], (r, key)
