@@ -59,6 +59,9 @@ def parse():
     ap.add_argument("--transport", choices=["auto", "nccl", "peer"], default="auto",
                     help="world > 1: NCCL grouped send/recv, copy-engine pulls over CUDA IPC, or "
                          "auto (peer if every rank can set it up, else NCCL)")
+    ap.add_argument("--no-push", action="store_true",
+                    help="peer transport: pull the dispatch rows with the copy engines instead of "
+                         "pushing them from the permute kernel (LANCET_FLAG_PEER_PUSH)")
     ap.add_argument("--same-device", action="store_true",
                     help="all ranks on GPU 0 (peer transport, gloo process group): a multi-process "
                          "test of the exchange machinery on one GPU, not a scaling measurement")
@@ -79,7 +82,9 @@ def workload(a, world):
         "tokens_per_gpu": a.tokens, "d_model": a.d, "d_ffn": a.f, "experts": a.experts,
         "top_k": a.k, "capacity_factor": a.cf, "n_chunks": a.chunks, "routing_skew_beta": a.beta,
         "gate": a.gate,
-        "parallelism": f"ep{world}" + (f" ({getattr(a, 'transport_used', a.transport)} all-to-all)"
+        "parallelism": f"ep{world}" + (f" ({getattr(a, 'transport_used', a.transport)}"
+                                       + (" push" if getattr(a, "transport_used", "") == "peer" and not a.no_push else "")
+                                       + " all-to-all)"
                                        if world > 1 or a.transport == "peer" else "")
                        + (" all ranks on one GPU" if getattr(a, "same_device", False) else ""),
         "global_batch_tokens": a.tokens * world,
@@ -413,6 +418,11 @@ def run_lancet(a, world, rank, local_rank):
     cfg = lancet.LayerConfig(d_model=a.d, d_ffn=a.f, n_experts=a.experts, max_tokens=a.tokens,
                              max_k=a.k, max_chunks=max(8, a.chunks), dtype="bf16", flags=flags)
     ctx = make_context(a, lancet, cfg, world, rank, local_rank, dev)
+    if a.transport_used == "peer" and not a.no_push:
+        # dispatch all-to-all fused into the permute kernel (rows written straight into the
+        # owners' receive buffers; DESIGN.md §8 "push dispatch")
+        flags |= lancet.FLAG_PEER_PUSH
+        ctx.set_flags(flags)
     stream = torch.cuda.current_stream()
     y = torch.empty_like(x)
     dx = torch.empty_like(x)
