@@ -131,7 +131,9 @@ enum {
                                            mapped peer memory; NVLink across GPUs) at its final
                                            row, one launch per chunk, readiness signalled per
                                            chunk by flags; no send buffer and no copy-engine
-                                           pass.  Must be set identically on every rank        */
+                                           pass.  Likewise the backward's first all-to-all:
+                                           K5 writes its dO rows straight into the owners' dO
+                                           buffers.  Must be set identically on every rank     */
 };
 
 typedef struct {

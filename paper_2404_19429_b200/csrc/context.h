@@ -24,13 +24,17 @@ struct DevBuf {
 // flags in device memory (stream wait-value / write-value operations).
 // PK_PUSH: "my rows of chunk c are in your receive buffer" (push-dispatch, LANCET_FLAG_PEER_PUSH);
 // PK_XEFREE: "my receive buffer may be written for this step" (its previous readers are done).
-enum PeerKind { PK_XS = 0, PK_OUT, PK_DCOMB, PK_DXE, PK_COUNTS, PK_PUSH, PK_XEFREE, PK_N };
+// PK_PUSH2 / PK_DOUTFREE: the same for the dO rows pushed by K5 into the owners' dout.
+enum PeerKind { PK_XS = 0, PK_OUT, PK_DCOMB, PK_DXE, PK_COUNTS, PK_PUSH, PK_XEFREE, PK_PUSH2, PK_DOUTFREE,
+                PK_N };
 struct PeerLinks {
     int world = 0, n_max = 0;
     std::vector<char*> src[PK_DXE + 1];   // per peer: its pull-source buffers (self: local)
     std::vector<int*> counts;             // per peer: its count matrix [G][E][n]
     std::vector<char*> xe;                // per peer: its expert-side receive buffer (push-dispatch)
     char** d_xe = nullptr;                // device copy of `xe` [G]
+    std::vector<char*> dout;              // per peer: its expert-side dO buffer (push, backward)
+    char** d_dout = nullptr;              // device copy of `dout` [G]
     int* d_push_base = nullptr;           // [n_max][E] push row base per (chunk, expert)
     std::vector<uint32_t*> flags;         // per peer: its flag array
     int* my_counts = nullptr;             // [G][E][n_max] this rank's matrix

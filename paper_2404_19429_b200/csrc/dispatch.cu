@@ -192,7 +192,8 @@ combine_bwd_kernel(const Elt* __restrict__ dy, const Elt* __restrict__ comb,
                    const int* __restrict__ send_rows, int t0, int t1, int k, int d,
                    float* __restrict__ g, Elt* __restrict__ dcomb, int tok_blocks,
                    const float* __restrict__ logits, int E, int renorm, float* __restrict__ dlogit,
-                   int* __restrict__ prow)
+                   int* __restrict__ prow, const int* __restrict__ push_base, char* const* __restrict__ push_dst,
+                   int E_l)
 {
     pdl_wait();   // programmatic dependent launch: predecessor's writes visible
     constexpr int V = Vec16<Elt>::N;
@@ -216,6 +217,22 @@ combine_bwd_kernel(const Elt* __restrict__ dy, const Elt* __restrict__ comb,
     load_choices<KK>(idx, slot, wts, send_off, t, k, lane, rows, wj, ids);
 #pragma unroll
     for (int j = 0; j < KK; ++j) part[j] = 0.f;
+    // dO row of choice j: this rank's dcomb, or (push, LANCET_FLAG_PEER_PUSH) its final row in
+    // the owning rank's receive buffer -- backward all-to-all #1 fused into this kernel
+    Elt* drow[KK];
+#pragma unroll
+    for (int j = 0; j < KK; ++j) {
+        drow[j] = nullptr;
+        if (rows[j] >= 0) {
+            if (push_base) {
+                const int e = ids[j];
+                drow[j] = reinterpret_cast<Elt*>(push_dst[e / E_l] +
+                                                 (size_t)(push_base[e] + rows[j] - send_off[e]) * d * sizeof(Elt));
+            } else {
+                drow[j] = dcomb + (size_t)rows[j] * d;
+            }
+        }
+    }
     const uint4* dyr = reinterpret_cast<const uint4*>(dy + (size_t)t * d);
     for (int v0 = lane; v0 < nvec; v0 += 32 * U) {
         uint4 rdy[U], ro[U][KK];
@@ -244,7 +261,7 @@ combine_bwd_kernel(const Elt* __restrict__ dy, const Elt* __restrict__ comb,
                         part[j] = fmaf(fdy[q], fo[q], part[j]);
                         sc[q] = wj[j] * fdy[q];
                     }
-                    st_v4(reinterpret_cast<uint4*>(dcomb + (size_t)rows[j] * d) + v0 + 32 * u, pack16<Elt>(sc));
+                    st_v4(reinterpret_cast<uint4*>(drow[j]) + v0 + 32 * u, pack16<Elt>(sc));
                 }
             }
         }
@@ -358,7 +375,8 @@ int launch_combine(const DispatchArgs& a, const void* comb, void* y, int t0, int
 
 int launch_combine_bwd(const DispatchArgs& a, const void* dy, const void* comb, float* g,
                        void* dcomb, int t0, int t1, bool zero_pads, const float* logits, int renorm,
-                       float* dlogit, int* prow, bool is_bf16, cudaStream_t s)
+                       float* dlogit, int* prow, bool is_bf16, cudaStream_t s, const int* push_base,
+                       char* const* push_dst, int E_l)
 {
     const int tok_blocks = ceil_div(t1 - t0, kWarpsPerBlock);
     const int grid = tok_blocks + (zero_pads ? a.E : 0);
@@ -368,12 +386,12 @@ int launch_combine_bwd(const DispatchArgs& a, const void* dy, const void* comb, 
             launch_k(combine_bwd_kernel<bf16, KK>, grid, 256, 0, s, (const bf16*)dy, (const bf16*)comb, a.idx,
                                                              a.slot, a.w, a.send_off, a.send_rows, t0, t1,
                                                              a.k, a.d, g, (bf16*)dcomb, tok_blocks, logits, a.E,
-                                                             renorm, dlogit, prow);
+                                                             renorm, dlogit, prow, push_base, push_dst, E_l);
         else
             launch_k(combine_bwd_kernel<float, KK>, grid, 256, 0, s, (const float*)dy, (const float*)comb, a.idx,
                                                               a.slot, a.w, a.send_off, a.send_rows, t0, t1,
                                                               a.k, a.d, g, (float*)dcomb, tok_blocks, logits, a.E,
-                                                              renorm, dlogit, prow);
+                                                              renorm, dlogit, prow, push_base, push_dst, E_l);
     });
     return 1;
 }

@@ -1152,13 +1152,32 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
     L += launch_zero_pads(c->dout, d, d_grp_off, d_grp_rows, n * E_l, (int)c->elt, sc);
     const void* comb = c->comb;     // o_tj returned by the combine all-to-all (source side)
     std::vector<cudaEvent_t> ev_k5(nc), ev_b1(nc), ev_dx(nc), ev_b2(nc);
+    const bool push = pr && (c->cfg.flags & LANCET_FLAG_PEER_PUSH);
+    if (push) {
+        // K5 pushes its dO rows into the owners' dout (backward all-to-all #1 fused, same row
+        // bases as the forward's push): this rank's dout is free (its readers of the previous
+        // step are behind it on this stream), and so must every owner's be
+        if (peer_signal(c, 0, lancet::PK_DOUTFREE, 0, sc) || peer_wait_all(c, lancet::PK_DOUTFREE, 0, sc))
+            return fail(c, LANCET_ERR_CUDA, "cuStream{Write,Wait}Value32");
+    }
     for (int cc = 0; cc < nc; ++cc) {
         int t0, t1;
         tok_range(cc, t0, t1);
-        OpScope op(c, "combine_bwd", 0, serial ? -1 : cc, sc);
-        L += launch_combine_bwd(da, dy, comb, c->g, c->dcomb, t0, t1, cc == 0, c->logits, renorm, c->dlogit,
-                                c->prow, c->bf16, sc);
-        if (pr && peer_signal(c, 0, lancet::PK_DCOMB, cc, sc)) return fail(c, LANCET_ERR_CUDA, "cuStreamWriteValue32");
+        OpScope op(c, push ? "combine_bwd_push" : "combine_bwd", 0, serial ? -1 : cc, sc);
+        if (push) {
+            int c0, c1;
+            chunk_range(cc, c0, c1);
+            for (int ch = c0; ch < c1; ++ch) {
+                L += launch_combine_bwd(da, dy, comb, c->g, c->dcomb, chunk_start(T, n, ch), chunk_start(T, n, ch + 1),
+                                        false, c->logits, renorm, c->dlogit, c->prow, c->bf16, sc,
+                                        pr->d_push_base + (size_t)ch * E, pr->d_dout, E_l);
+                if (peer_signal(c, 0, lancet::PK_PUSH2, ch, sc)) return fail(c, LANCET_ERR_CUDA, "cuStreamWriteValue32");
+            }
+        } else {
+            L += launch_combine_bwd(da, dy, comb, c->g, c->dcomb, t0, t1, cc == 0, c->logits, renorm, c->dlogit,
+                                    c->prow, c->bf16, sc);
+            if (pr && peer_signal(c, 0, lancet::PK_DCOMB, cc, sc)) return fail(c, LANCET_ERR_CUDA, "cuStreamWriteValue32");
+        }
         ev_k5[cc] = next_ev();
         CK(cudaEventRecord(ev_k5[cc], sc));
     }
@@ -1171,6 +1190,15 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
         chunk_range(cc, c0, c1);
         CK(cudaStreamWaitEvent(sm, ev_k5[cc], 0));
         OpScope op(c, "a2a_bwd_dispatch", 1, serial ? -1 : cc, sm);
+        if (push) {         // every rank's dO rows of these chunks have landed in dout
+            for (int ch = c0; ch < c1; ++ch)
+                if (peer_wait_all(c, lancet::PK_PUSH2, ch, sm)) return fail(c, LANCET_ERR_CUDA, "cuStreamWaitValue32");
+            if (ident && peer_signal(c, 0, lancet::PK_DXE, cc, sm))   // identity: dout is the source back
+                return fail(c, LANCET_ERR_CUDA, "cuStreamWriteValue32");
+            ev_b1[cc] = next_ev();
+            CK(cudaEventRecord(ev_b1[cc], sm));
+            continue;
+        }
         if (pr) {
             std::string err;
             if (peer_pull(c, lancet::PK_DCOMB, cc, gp.pulls(c->rank, true, c0, c1, dout, rowb), cc == nc - 1, sm, err))

@@ -53,7 +53,7 @@ const MemOps& memops()
     return ops;
 }
 
-constexpr int kBufs = 7;   // exported: xs, out-source, dcomb, dXe-source, counts, flags, xe
+constexpr int kBufs = 8;   // exported: xs, out-source, dcomb, dXe-source, counts, flags, xe, dout
 
 }  // namespace
 
@@ -82,11 +82,13 @@ int peer_init(lancet_ctx* c, std::string& err)
     }
     cudaMemset(pl->my_flags, 0, sizeof(uint32_t) * peer_flag_words(G, pl->n_max));
     if (cudaMalloc(&pl->d_xe, sizeof(char*) * G) != cudaSuccess ||
+        cudaMalloc(&pl->d_dout, sizeof(char*) * G) != cudaSuccess ||
         cudaMalloc(&pl->d_push_base, sizeof(int) * (size_t)pl->n_max * E) != cudaSuccess) {
         err = "cudaMalloc (push tables)";
         return 1;
     }
     pl->xe.assign(G, nullptr);
+    pl->dout.assign(G, nullptr);
     for (int k = 0; k <= PK_DXE; ++k) pl->src[k].assign(G, nullptr);
     pl->counts.assign(G, nullptr);
     pl->flags.assign(G, nullptr);
@@ -110,7 +112,7 @@ int peer_export(lancet_ctx* c, void* blob, std::string& err)
 {
     PeerLinks* pl = c->peer;
     void* bufs[kBufs] = {local_src(c, PK_XS), local_src(c, PK_OUT), local_src(c, PK_DCOMB),
-                         local_src(c, PK_DXE), pl->my_counts, pl->my_flags, c->xe};
+                         local_src(c, PK_DXE), pl->my_counts, pl->my_flags, c->xe, c->dout};
     auto* h = reinterpret_cast<cudaIpcMemHandle_t*>(blob);
     for (int i = 0; i < kBufs; ++i)
         if (cudaIpcGetMemHandle(&h[i], bufs[i]) != cudaSuccess) {
@@ -131,6 +133,7 @@ int peer_import(lancet_ctx* c, const void* blobs, std::string& err)
             m[4] = pl->my_counts;
             m[5] = pl->my_flags;
             m[6] = c->xe;
+            m[7] = c->dout;
         } else {
             const auto* h = reinterpret_cast<const cudaIpcMemHandle_t*>(
                 reinterpret_cast<const char*>(blobs) + (size_t)p * peer_blob_bytes());
@@ -146,8 +149,10 @@ int peer_import(lancet_ctx* c, const void* blobs, std::string& err)
         pl->counts[p] = reinterpret_cast<int*>(m[4]);
         pl->flags[p] = reinterpret_cast<uint32_t*>(m[5]);
         pl->xe[p] = reinterpret_cast<char*>(m[6]);
+        pl->dout[p] = reinterpret_cast<char*>(m[7]);
     }
-    if (cudaMemcpy(pl->d_xe, pl->xe.data(), sizeof(char*) * G, cudaMemcpyHostToDevice) != cudaSuccess) {
+    if (cudaMemcpy(pl->d_xe, pl->xe.data(), sizeof(char*) * G, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(pl->d_dout, pl->dout.data(), sizeof(char*) * G, cudaMemcpyHostToDevice) != cudaSuccess) {
         err = "cudaMemcpy (peer receive-buffer table)";
         return 1;
     }
@@ -162,6 +167,7 @@ void peer_destroy(lancet_ctx* c)
     if (pl->my_counts) cudaFree(pl->my_counts);
     if (pl->my_flags) cudaFree(pl->my_flags);
     if (pl->d_xe) cudaFree(pl->d_xe);
+    if (pl->d_dout) cudaFree(pl->d_dout);
     if (pl->d_push_base) cudaFree(pl->d_push_base);
     if (pl->h_matrix) cudaFreeHost(pl->h_matrix);
     delete pl;
@@ -197,7 +203,7 @@ int peer_wait_consumed(lancet_ctx* c, cudaStream_t s, bool push)
     PeerLinks* pl = c->peer;
     if (pl->seq <= 1) return 0;
     for (int kind = 0; kind <= PK_DXE; ++kind) {
-        if (push && kind == PK_XS) continue;           // push-dispatch: nobody pulls the send rows
+        if (push && (kind == PK_XS || kind == PK_DCOMB)) continue;   // pushed, never pulled
         for (int r = 0; r < pl->world; ++r)
             if (peer_wait(c, 1, kind, 0, r, pl->seq - 1, s)) return 1;
     }
