@@ -35,6 +35,7 @@ struct PeerLinks {
     char** d_xe = nullptr;                // device copy of `xe` [G]
     std::vector<char*> dout;              // per peer: its expert-side dO buffer (push, backward)
     char** d_dout = nullptr;              // device copy of `dout` [G]
+    char** d_outsrc = nullptr;            // device copy of src[PK_OUT] [G] (fused combine reads)
     int* d_push_base = nullptr;           // [n_max][E] push row base per (chunk, expert)
     std::vector<uint32_t*> flags;         // per peer: its flag array
     int* my_counts = nullptr;             // [G][E][n_max] this rank's matrix
@@ -121,6 +122,9 @@ struct lancet_ctx {
 
     // cross-layer dW scheduling (LANCET_FLAG_DEFER_DW, R17)
     uint64_t gate_seed = 0;          // Random gate (LANCET_FLAG_GATE_RANDOM, R18)
+    uint32_t bwd_seq = 0;             // peer: step (PeerLinks::seq) of the last backward
+    bool out_consume_pending = false; // push: the owners' outputs read by K4 are not yet released
+                                      // (K5 releases them; a forward without backward does)
     int dw_pending = 0;              // bit 0: dW1, bit 1: dW2 of the last backward not enqueued
     float* pend_dw1 = nullptr;  float* pend_dw2 = nullptr;
     cudaEvent_t ev_dw_ready = nullptr;   // after the last backward's dX GEMMs

@@ -143,7 +143,8 @@ __global__ void __launch_bounds__(256)
 combine_kernel(const Elt* __restrict__ comb, const int* __restrict__ idx,
                const int* __restrict__ slot, const float* __restrict__ wts,
                const int* __restrict__ send_off, int t0, int t1, int k, int d,
-               Elt* __restrict__ y)
+               Elt* __restrict__ y, const int* __restrict__ src_base, const char* const* __restrict__ src_tab,
+               int E_l)
 {
     pdl_wait();   // programmatic dependent launch: predecessor's writes visible
     constexpr int V = Vec16<Elt>::N;
@@ -154,6 +155,17 @@ combine_kernel(const Elt* __restrict__ comb, const int* __restrict__ idx,
     int rows[KK], ids[KK];
     float wj[KK];
     load_choices<KK>(idx, slot, wts, send_off, t, k, lane, rows, wj, ids);
+    // o row of choice j: the returned row in this rank's comb, or (fused combine exchange,
+    // LANCET_FLAG_PEER_PUSH) the expert output row itself in the owner's buffer over peer memory
+    const Elt* orow[KK];
+#pragma unroll
+    for (int j = 0; j < KK; ++j) {
+        orow[j] = nullptr;
+        if (rows[j] >= 0)
+            orow[j] = src_base ? reinterpret_cast<const Elt*>(src_tab[ids[j] / E_l] +
+                                                               (size_t)(src_base[ids[j]] + rows[j] - send_off[ids[j]]) * d * sizeof(Elt))
+                               : comb + (size_t)rows[j] * d;
+    }
     const int nvec = d / V;
     uint4* dst = reinterpret_cast<uint4*>(y + (size_t)t * d);
     for (int v0 = lane; v0 < nvec; v0 += 32 * U) {
@@ -163,7 +175,7 @@ combine_kernel(const Elt* __restrict__ comb, const int* __restrict__ idx,
 #pragma unroll
             for (int j = 0; j < KK; ++j)
                 if (rows[j] >= 0 && v0 + 32 * u < nvec)
-                    raw[u][j] = ld_nc_v4(reinterpret_cast<const uint4*>(comb + (size_t)rows[j] * d) + v0 + 32 * u);
+                    raw[u][j] = ld_nc_v4(reinterpret_cast<const uint4*>(orow[j]) + v0 + 32 * u);
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             if (v0 + 32 * u >= nvec) break;
@@ -193,7 +205,7 @@ combine_bwd_kernel(const Elt* __restrict__ dy, const Elt* __restrict__ comb,
                    float* __restrict__ g, Elt* __restrict__ dcomb, int tok_blocks,
                    const float* __restrict__ logits, int E, int renorm, float* __restrict__ dlogit,
                    int* __restrict__ prow, const int* __restrict__ push_base, char* const* __restrict__ push_dst,
-                   int E_l)
+                   int E_l, const char* const* __restrict__ src_tab)
 {
     pdl_wait();   // programmatic dependent launch: predecessor's writes visible
     constexpr int V = Vec16<Elt>::N;
@@ -220,9 +232,16 @@ combine_bwd_kernel(const Elt* __restrict__ dy, const Elt* __restrict__ comb,
     // dO row of choice j: this rank's dcomb, or (push, LANCET_FLAG_PEER_PUSH) its final row in
     // the owning rank's receive buffer -- backward all-to-all #1 fused into this kernel
     Elt* drow[KK];
+    const Elt* orow[KK];                               // o rows (fused combine: the owner's)
 #pragma unroll
     for (int j = 0; j < KK; ++j) {
         drow[j] = nullptr;
+        orow[j] = nullptr;
+        if (rows[j] >= 0)
+            orow[j] = (push_base && src_tab)
+                          ? reinterpret_cast<const Elt*>(src_tab[ids[j] / E_l] +
+                                                         (size_t)(push_base[ids[j]] + rows[j] - send_off[ids[j]]) * d * sizeof(Elt))
+                          : comb + (size_t)rows[j] * d;
         if (rows[j] >= 0) {
             if (push_base) {
                 const int e = ids[j];
@@ -243,7 +262,7 @@ combine_bwd_kernel(const Elt* __restrict__ dy, const Elt* __restrict__ comb,
 #pragma unroll
                 for (int j = 0; j < KK; ++j)
                     if (rows[j] >= 0)
-                        ro[u][j] = ld_nc_v4(reinterpret_cast<const uint4*>(comb + (size_t)rows[j] * d) + v0 + 32 * u);
+                        ro[u][j] = ld_nc_v4(reinterpret_cast<const uint4*>(orow[j]) + v0 + 32 * u);
             }
         }
 #pragma unroll
@@ -358,17 +377,18 @@ int launch_permute_push(const DispatchArgs& a, const void* x, int t0, int t1, in
 }
 
 int launch_combine(const DispatchArgs& a, const void* comb, void* y, int t0, int t1, bool is_bf16,
-                   cudaStream_t s)
+                   cudaStream_t s, const int* src_base, const char* const* src_tab, int E_l)
 {
     if (t1 <= t0) return 0;
     const int grid = ceil_div(t1 - t0, kWarpsPerBlock);
     LANCET_DISPATCH_K(a.k, {
         if (is_bf16)
             launch_k(combine_kernel<bf16, KK>, grid, 256, 0, s, (const bf16*)comb, a.idx, a.slot, a.w, a.send_off,
-                                                         t0, t1, a.k, a.d, (bf16*)y);
+                                                         t0, t1, a.k, a.d, (bf16*)y, src_base, src_tab, E_l);
         else
             launch_k(combine_kernel<float, KK>, grid, 256, 0, s, (const float*)comb, a.idx, a.slot, a.w,
-                                                          a.send_off, t0, t1, a.k, a.d, (float*)y);
+                                                          a.send_off, t0, t1, a.k, a.d, (float*)y, src_base, src_tab,
+                                                          E_l);
     });
     return 1;
 }
@@ -376,7 +396,7 @@ int launch_combine(const DispatchArgs& a, const void* comb, void* y, int t0, int
 int launch_combine_bwd(const DispatchArgs& a, const void* dy, const void* comb, float* g,
                        void* dcomb, int t0, int t1, bool zero_pads, const float* logits, int renorm,
                        float* dlogit, int* prow, bool is_bf16, cudaStream_t s, const int* push_base,
-                       char* const* push_dst, int E_l)
+                       char* const* push_dst, int E_l, const char* const* src_tab)
 {
     const int tok_blocks = ceil_div(t1 - t0, kWarpsPerBlock);
     const int grid = tok_blocks + (zero_pads ? a.E : 0);
@@ -386,12 +406,12 @@ int launch_combine_bwd(const DispatchArgs& a, const void* dy, const void* comb, 
             launch_k(combine_bwd_kernel<bf16, KK>, grid, 256, 0, s, (const bf16*)dy, (const bf16*)comb, a.idx,
                                                              a.slot, a.w, a.send_off, a.send_rows, t0, t1,
                                                              a.k, a.d, g, (bf16*)dcomb, tok_blocks, logits, a.E,
-                                                             renorm, dlogit, prow, push_base, push_dst, E_l);
+                                                             renorm, dlogit, prow, push_base, push_dst, E_l, src_tab);
         else
             launch_k(combine_bwd_kernel<float, KK>, grid, 256, 0, s, (const float*)dy, (const float*)comb, a.idx,
                                                               a.slot, a.w, a.send_off, a.send_rows, t0, t1,
                                                               a.k, a.d, g, (float*)dcomb, tok_blocks, logits, a.E,
-                                                              renorm, dlogit, prow, push_base, push_dst, E_l);
+                                                              renorm, dlogit, prow, push_base, push_dst, E_l, src_tab);
     });
     return 1;
 }

@@ -69,15 +69,18 @@ int launch_permute(const DispatchArgs& a, const void* x, void* xs, bool is_bf16,
 // x[t] of choice (t, j) -> xe_ptrs[e / E_l] + (base[e] + slot) rows
 int launch_permute_push(const DispatchArgs& a, const void* x, int t0, int t1, int E_l, const int* base,
                         char* const* xe_ptrs, bool is_bf16, cudaStream_t s);
+// src_base / src_tab (fused combine exchange, optional): o rows read from src_tab[e / E_l] at
+// rows src_base[e] + slot (the owners' expert outputs over peer memory) instead of comb
 int launch_combine(const DispatchArgs& a, const void* comb, void* y, int t0, int t1, bool is_bf16,
-                   cudaStream_t s);
+                   cudaStream_t s, const int* src_base = nullptr, const char* const* src_tab = nullptr,
+                   int E_l = 1);
 // K5: also writes dlogit [T][E] (softmax Jacobian) and prow [T][k] (packed row or -1)
 // push_base / push_dst (peer push, optional): the dO rows go to push_dst[e / E_l] at rows
 // push_base[e] + slot instead of dcomb (backward all-to-all #1 fused into K5)
 int launch_combine_bwd(const DispatchArgs& a, const void* dy, const void* comb, float* g,
                        void* dcomb, int t0, int t1, bool zero_pads, const float* logits, int renorm,
                        float* dlogit, int* prow, bool is_bf16, cudaStream_t s, const int* push_base = nullptr,
-                       char* const* push_dst = nullptr, int E_l = 1);
+                       char* const* push_dst = nullptr, int E_l = 1, const char* const* src_tab = nullptr);
 int launch_wg_transpose(const float* wg, int d, int E, float* wgT, cudaStream_t s);
 bool gate_bwd_needs_wgT(int d, int E);   // true: the general K6 reads Wg^T (launch_wg_transpose)
 // K6: dx_t = sum_j dX[prow_tj] + sum_e dlogit_te Wg[:, e]   (wg [d][E]; wgT = Wg transposed,

@@ -802,8 +802,15 @@ LANCET_API lancet_status lancet_moe_forward(lancet_ctx* c, const void* x, const 
         if (pr) {
             if (!c->peer_ready) return fail(c, LANCET_ERR_STATE, "peer transport: lancet_peer_import not called");
             ++pr->seq;
-            // every peer has pulled the previous step's rows from this rank's pull sources
-            if (peer_wait_consumed(c, sc, push)) return fail(c, LANCET_ERR_CUDA, "cuStreamWaitValue32");
+            // a forward without backward: release the owners' outputs the last forward read
+            if (push && c->out_consume_pending) {
+                if (peer_signal(c, 1, lancet::PK_OUT, 0, sc)) return fail(c, LANCET_ERR_CUDA, "cuStreamWriteValue32");
+                c->out_consume_pending = false;
+            }
+            // every peer has pulled the previous step's rows from this rank's pull sources (the
+            // backward's only if that step had a backward: a forward may follow a forward)
+            if (peer_wait_consumed(c, sc, push, c->bwd_seq == pr->seq - 1))
+                return fail(c, LANCET_ERR_CUDA, "cuStreamWaitValue32");
             // push-dispatch: this rank's receive buffer is free for the step's pushes (its
             // GEMMs of the previous step are behind on this stream, its pull readers done)
             if (push && peer_signal(c, 0, lancet::PK_XEFREE, 0, sc))
@@ -977,7 +984,7 @@ LANCET_API lancet_status lancet_moe_forward(lancet_ctx* c, const void* x, const 
         }
         // combine all-to-alls C0..C(n-1)
         const char* eout = ident ? xe : (const char*)c->out;
-        for (int cc = 0; cc < nc; ++cc) {
+        for (int cc = 0; cc < nc && !push; ++cc) {
             int c0, c1;
             chunk_range(cc, c0, c1);
             CK(cudaStreamWaitEvent(sm, ev_exp[cc], 0));
@@ -1008,8 +1015,21 @@ LANCET_API lancet_status lancet_moe_forward(lancet_ctx* c, const void* x, const 
             ev_comb[cc] = next_ev();
             CK(cudaEventRecord(ev_comb[cc], sm));
         }
+        // push: the combine exchange is fused into the gather -- K4 reads each expert output row
+        // where its owner's fc2 wrote it (peer memory), once every owner has finished chunk c
+        for (int cc = 0; cc < nc && push; ++cc) {
+            int c0, c1;
+            chunk_range(cc, c0, c1);
+            for (int ch = c0; ch < c1; ++ch) {
+                if (peer_wait_all(c, lancet::PK_OUT, ch, sc)) return fail(c, LANCET_ERR_CUDA, "cuStreamWaitValue32");
+                OpScope op(c, "combine_fused", 0, ch, sc);
+                L += launch_combine(da, comb, y, chunk_start(T, n, ch), chunk_start(T, n, ch + 1), c->bf16, sc,
+                                    pr->d_push_base + (size_t)ch * E, pr->d_outsrc, E_l);
+            }
+            c->out_consume_pending = true;
+        }
         // gather per chunk (chunk c's tokens are final as soon as combine c lands)
-        for (int cc = 0; cc < nc; ++cc) {
+        for (int cc = 0; cc < nc && !push; ++cc) {
             CK(cudaStreamWaitEvent(sc, ev_comb[cc], 0));
             const int t0 = serial ? 0 : chunk_start(T, n, cc), t1 = serial ? T : chunk_start(T, n, cc + 1);
             OpScope op(c, "combine", 0, serial ? -1 : cc, sc);
@@ -1170,7 +1190,7 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
             for (int ch = c0; ch < c1; ++ch) {
                 L += launch_combine_bwd(da, dy, comb, c->g, c->dcomb, chunk_start(T, n, ch), chunk_start(T, n, ch + 1),
                                         false, c->logits, renorm, c->dlogit, c->prow, c->bf16, sc,
-                                        pr->d_push_base + (size_t)ch * E, pr->d_dout, E_l);
+                                        pr->d_push_base + (size_t)ch * E, pr->d_dout, E_l, pr->d_outsrc);
                 if (peer_signal(c, 0, lancet::PK_PUSH2, ch, sc)) return fail(c, LANCET_ERR_CUDA, "cuStreamWriteValue32");
             }
         } else {
@@ -1180,6 +1200,11 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
         }
         ev_k5[cc] = next_ev();
         CK(cudaEventRecord(ev_k5[cc], sc));
+    }
+    // push: K4 and K5 read the owners' expert outputs in place; they are consumed now
+    if (push) {
+        if (peer_signal(c, 1, lancet::PK_OUT, 0, sc)) return fail(c, LANCET_ERR_CUDA, "cuStreamWriteValue32");
+        c->out_consume_pending = false;
     }
     CHECK_LAUNCH();
     char* dcomb = (char*)c->dcomb;
@@ -1313,6 +1338,7 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
     }
     st = gate_backward_dwg(c, dwg, sc, &L);
     if (st) return st;
+    if (pr) c->bwd_seq = pr->seq;
     CK(cudaEventRecord(c->ev_join, sc));
     CK(cudaStreamWaitEvent(s, c->ev_join, 0));
     if (sm != sc) {

@@ -83,6 +83,7 @@ int peer_init(lancet_ctx* c, std::string& err)
     cudaMemset(pl->my_flags, 0, sizeof(uint32_t) * peer_flag_words(G, pl->n_max));
     if (cudaMalloc(&pl->d_xe, sizeof(char*) * G) != cudaSuccess ||
         cudaMalloc(&pl->d_dout, sizeof(char*) * G) != cudaSuccess ||
+        cudaMalloc(&pl->d_outsrc, sizeof(char*) * G) != cudaSuccess ||
         cudaMalloc(&pl->d_push_base, sizeof(int) * (size_t)pl->n_max * E) != cudaSuccess) {
         err = "cudaMalloc (push tables)";
         return 1;
@@ -152,7 +153,8 @@ int peer_import(lancet_ctx* c, const void* blobs, std::string& err)
         pl->dout[p] = reinterpret_cast<char*>(m[7]);
     }
     if (cudaMemcpy(pl->d_xe, pl->xe.data(), sizeof(char*) * G, cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemcpy(pl->d_dout, pl->dout.data(), sizeof(char*) * G, cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaMemcpy(pl->d_dout, pl->dout.data(), sizeof(char*) * G, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(pl->d_outsrc, pl->src[PK_OUT].data(), sizeof(char*) * G, cudaMemcpyHostToDevice) != cudaSuccess) {
         err = "cudaMemcpy (peer receive-buffer table)";
         return 1;
     }
@@ -168,6 +170,7 @@ void peer_destroy(lancet_ctx* c)
     if (pl->my_flags) cudaFree(pl->my_flags);
     if (pl->d_xe) cudaFree(pl->d_xe);
     if (pl->d_dout) cudaFree(pl->d_dout);
+    if (pl->d_outsrc) cudaFree(pl->d_outsrc);
     if (pl->d_push_base) cudaFree(pl->d_push_base);
     if (pl->h_matrix) cudaFreeHost(pl->h_matrix);
     delete pl;
@@ -198,12 +201,14 @@ int peer_wait(lancet_ctx* c, int consumed, int kind, int chunk, int r, uint32_t 
 
 // before this step overwrites any pull source: every peer has pulled the previous step's rows
 // of every kind
-int peer_wait_consumed(lancet_ctx* c, cudaStream_t s, bool push)
+int peer_wait_consumed(lancet_ctx* c, cudaStream_t s, bool push, bool prev_backward)
 {
     PeerLinks* pl = c->peer;
     if (pl->seq <= 1) return 0;
     for (int kind = 0; kind <= PK_DXE; ++kind) {
         if (push && (kind == PK_XS || kind == PK_DCOMB)) continue;   // pushed, never pulled
+        // a forward that was not followed by a backward produced no backward rows to consume
+        if (!prev_backward && (kind == PK_DCOMB || kind == PK_DXE)) continue;
         for (int r = 0; r < pl->world; ++r)
             if (peer_wait(c, 1, kind, 0, r, pl->seq - 1, s)) return 1;
     }

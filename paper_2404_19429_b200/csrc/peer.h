@@ -25,7 +25,7 @@ int peer_export(lancet_ctx* c, void* blob, std::string& err);
 int peer_import(lancet_ctx* c, const void* blobs, std::string& err);   // world blobs, rank order
 void peer_destroy(lancet_ctx* c);
 int peer_signal(lancet_ctx* c, int consumed, int kind, int chunk, cudaStream_t s);
-int peer_wait_consumed(lancet_ctx* c, cudaStream_t s, bool push = false);
+int peer_wait_consumed(lancet_ctx* c, cudaStream_t s, bool push = false, bool prev_backward = true);
 int peer_wait_all(lancet_ctx* c, int kind, int chunk, cudaStream_t s);
 int peer_pull(lancet_ctx* c, int kind, int chunk, const std::vector<PeerCopy>& copies, bool last,
               cudaStream_t s, std::string& err);

@@ -351,3 +351,22 @@ def test_push_dispatch_is_bitwise_the_pull_path(n, act):
     o = run_oracle(ins, k, 1.0, n, act=act)
     for key in ("y", "dx"):
         assert normwise(outs["push"][key], o[key]) <= TOL["bf16"], key
+
+
+def test_push_forward_without_backward_releases_the_outputs():
+    # with the fused combine, K4 and K5 read the owners' expert outputs in place and K5 releases
+    # them; a forward that is not followed by a backward must release them at the next forward
+    # (no stall), and the step after it is unchanged
+    from paper_2404_19429_b200 import FLAG_PEER_PUSH, lancet
+    T, d, f, E, k, n = 1000, 128, 256, 8, 2, 2
+    ins = inputs(T, d, f, E, k, beta=0.5, seed=5)
+    cfg = lancet.LayerConfig(d_model=d, d_ffn=f, n_experts=E, max_tokens=T, max_k=k, max_chunks=8,
+                             flags=FLAG_PEER_PUSH)
+    ctx = lancet.Context(cfg, transport="peer")
+    ref = run_gpu(ins, E, k, 1.0, n, ctx=ctx)
+    run_gpu(ins, E, k, 1.0, n, ctx=ctx, backward=False)          # forward only
+    run_gpu(ins, E, k, 1.0, n, ctx=ctx, backward=False)          # and again
+    got = run_gpu(ins, E, k, 1.0, n, ctx=ctx)
+    ctx.close()
+    for key in ("y", "dx", "dwg", "dw1", "dw2"):
+        assert np.array_equal(got[key], ref[key]), key
