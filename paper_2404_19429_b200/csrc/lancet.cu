@@ -1020,8 +1020,9 @@ LANCET_API lancet_status lancet_moe_forward(lancet_ctx* c, const void* x, const 
         for (int cc = 0; cc < nc && push; ++cc) {
             int c0, c1;
             chunk_range(cc, c0, c1);
+            // the owners signal their outputs per chunk group cc (all chunks at once when serial)
+            if (peer_wait_all(c, lancet::PK_OUT, cc, sc)) return fail(c, LANCET_ERR_CUDA, "cuStreamWaitValue32");
             for (int ch = c0; ch < c1; ++ch) {
-                if (peer_wait_all(c, lancet::PK_OUT, ch, sc)) return fail(c, LANCET_ERR_CUDA, "cuStreamWaitValue32");
                 OpScope op(c, "combine_fused", 0, ch, sc);
                 L += launch_combine(da, comb, y, chunk_start(T, n, ch), chunk_start(T, n, ch + 1), c->bf16, sc,
                                     pr->d_push_base + (size_t)ch * E, pr->d_outsrc, E_l);

@@ -329,16 +329,19 @@ def test_large_token_count_gate_backward(E):
         assert normwise(g[key], o[key]) <= TOL["bf16"], key
 
 
-@pytest.mark.parametrize("n,act", [(1, "gelu_tanh"), (3, "gelu_tanh"), (2, "identity_expert")])
-def test_push_dispatch_is_bitwise_the_pull_path(n, act):
+@pytest.mark.parametrize("n,act,serial", [(1, "gelu_tanh", False), (3, "gelu_tanh", False),
+                                          (2, "identity_expert", False), (4, "gelu_tanh", True),
+                                          (3, "identity_expert", True)])
+def test_push_dispatch_is_bitwise_the_pull_path(n, act, serial):
     # LANCET_FLAG_PEER_PUSH: permute fused with the dispatch exchange (rows written straight into
     # the owner's receive buffer) over a one-rank peer group: same rows at the same positions,
     # so every output equals the copy-engine pull path bit for bit; two steps (buffer reuse)
-    from paper_2404_19429_b200 import FLAG_PEER_PUSH, lancet
+    from paper_2404_19429_b200 import FLAG_PEER_PUSH, FLAG_SERIAL, lancet
     T, d, f, E, k = 2000, 256, 512, 8, 2
     ins = inputs(T, d, f, E, k, beta=0.5, seed=91 + n)
     outs = {}
-    for name, fl in (("pull", 0), ("push", FLAG_PEER_PUSH)):
+    sf = FLAG_SERIAL if serial else 0        # serial baseline: chunks merged into one group
+    for name, fl in (("pull", sf), ("push", FLAG_PEER_PUSH | sf)):
         cfg = lancet.LayerConfig(d_model=d, d_ffn=f, n_experts=E, max_tokens=T, max_k=k, max_chunks=8,
                                  act=act, flags=fl)
         ctx = lancet.Context(cfg, transport="peer")
