@@ -133,7 +133,9 @@ enum {
                                            chunk by flags; no send buffer and no copy-engine
                                            pass.  Likewise the backward's first all-to-all:
                                            K5 writes its dO rows straight into the owners' dO
-                                           buffers.  Must be set identically on every rank     */
+                                           buffers; and the combine: K4 / K5 read the expert
+                                           outputs in place from the owners' buffers.  Must be
+                                           set identically on every rank                       */
 };
 
 typedef struct {
