@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define LANCET_ABI_VERSION 1
+#define LANCET_ABI_VERSION 2
 
 typedef struct lancet_ctx lancet_ctx;                 /* opaque, library-owned */
 typedef struct lancet_local_group lancet_local_group; /* opaque, library-owned */
@@ -125,7 +125,7 @@ enum {
                                            admission.  No gate network: Wg is not read, logits
                                            are reported as 0, dwg is 0 and dx has no gate term.
                                            Exclusive with LANCET_FLAG_GATE_BPR (ERR_ARG)       */
-    LANCET_FLAG_PEER_PUSH = 1u << 14    /* peer transport: the dispatch all-to-all is fused into
+    LANCET_FLAG_PEER_PUSH = 1u << 14,   /* peer transport: the dispatch all-to-all is fused into
                                            the permute kernel -- each admitted row is written
                                            straight into the owning rank's receive buffer (IPC-
                                            mapped peer memory; NVLink across GPUs) at its final
@@ -134,8 +134,22 @@ enum {
                                            pass.  Likewise the backward's first all-to-all:
                                            K5 writes its dO rows straight into the owners' dO
                                            buffers; and the combine: K4 / K5 read the expert
-                                           outputs in place from the owners' buffers.  Must be
-                                           set identically on every rank                       */
+                                           outputs in place from the owners' buffers, and K6
+                                           reads the dX rows in place from the owners' dX
+                                           buffers (backward #2).  The exchange plan is built on
+                                           the device from the gathered count matrix and every
+                                           readiness flag is a kernel, so the step never waits on
+                                           the host and can be captured in a CUDA graph.  The
+                                           fused kernels run on the comm stream beside the
+                                           expert GEMMs (which leave LANCET_COMM_SMS SMs free).
+                                           Fixed at creation (lancet_set_flags keeps the creation
+                                           bit); checked identical on every rank at
+                                           lancet_peer_import                                   */
+    LANCET_FLAG_NO_COMM = 1u << 15      /* TIMING ONLY (results are wrong): skip the data
+                                           exchanges (NCCL / copy-engine: the C2 copies; push
+                                           mode: the four fused exchange kernels) but keep every
+                                           other op and wait -- T_step - T_step(NO_COMM) bounds
+                                           the exposed exchange time from above  */
 };
 
 typedef struct {
@@ -207,8 +221,26 @@ lancet_status lancet_create_peer(lancet_ctx** out, int32_t world, int32_t rank, 
 size_t lancet_peer_blob_bytes(void);
 lancet_status lancet_peer_export(lancet_ctx* ctx, void* blob /* host, lancet_peer_blob_bytes() */);
 lancet_status lancet_peer_import(lancet_ctx* ctx, const void* blobs /* host, world blobs */);
+/* Import checks every blob's configuration hash (d_model, d_ffn, n_experts, max_tokens, max_k,
+ * max_chunks, dtype, act, RENORMALIZE, PEER_PUSH, world) and rank: LANCET_ERR_CUDA with a
+ * message naming the disagreeing rank otherwise.
+ *
+ * Failure handling of the peer transport.  Push mode (LANCET_FLAG_PEER_PUSH): every wait is
+ * a kernel that gives up after the timeout (default 60 s, env LANCET_PEER_TIMEOUT_MS, or
+ * lancet_set_peer_timeout_ms) and records which rank / flag it missed; the step's results are
+ * then undefined and every later call on the context returns LANCET_ERR_STATE naming the
+ * flag.  lancet_peer_abort (any mode, e.g. from a watchdog thread of the caller): sets every
+ * flag of this rank so that all its pending waits -- stream wait-value operations of the
+ * copy-engine mode included -- return, and poisons the context.  lancet_peer_status: the
+ * context's asynchronous error state without blocking (LANCET_OK, or LANCET_ERR_STATE). */
+lancet_status lancet_set_peer_timeout_ms(lancet_ctx* ctx, int64_t ms);
+lancet_status lancet_peer_abort(lancet_ctx* ctx);
+lancet_status lancet_peer_status(lancet_ctx* ctx);
 
-/* Destroy; aborts the communicator if the context is poisoned.  Safe on NULL. */
+/* Destroy; aborts the communicator if the context is poisoned.  Safe on NULL.  Peer
+ * transport: collective -- peers read this rank's buffers over IPC, so destroy first waits
+ * (bounded by the peer timeout) until every peer has signalled that it consumed this rank's
+ * rows of the last step, then unmaps and frees; call it on every rank after the last step. */
 lancet_status lancet_destroy(lancet_ctx* ctx);
 
 lancet_status lancet_set_flags(lancet_ctx* ctx, uint32_t flags);
@@ -221,19 +253,21 @@ lancet_status lancet_set_gate_seed(lancet_ctx* ctx, uint64_t seed);
  *   wg  [d][E]      fp32    replicated gate
  *   w1  [E_l][f][d] dtype   this rank's experts e = rank*E_l + i; valid until backward
  *   w2  [E_l][d][f] dtype
- *   T in [1, max_tokens]; k in [1, min(E, max_k)]; capacity_factor > 0;
+ *   T in [1, max_tokens]; k in [1, min(E, max_k)]; capacity_factor > 0 (double: the
+ *   capacity C = max(1, min(T, ceil(cf k T / E))) is evaluated in double, R4);
  *   n_chunks in [1, min(T, max_chunks)]
  *   y          [T][d] dtype  out
  *   expert_idx [T][k] int32  out or NULL   (rank order; idx[:,0] is the best expert)
  *   slot       [T][k] int32  out or NULL   (position in the expert's buffer; -1 = dropped)
  *   combine_w  [T][k] fp32   out or NULL
- * world > 1: blocks the host once (the counts exchange of P:L525 must reach the host to
- * size the NCCL sends).  world == 1: never blocks.
+ * world > 1 over NCCL or the copy-engine peer transport: blocks the host once (the counts
+ * exchange of P:L525 must reach the host to size the NCCL sends / the copies).  world == 1
+ * and the push mode of the peer transport: never blocks (plan built on the device).
  * One outstanding forward per context: a second forward before backward is allowed (the
  * first is discarded); backward without forward returns LANCET_ERR_STATE. */
 lancet_status lancet_moe_forward(lancet_ctx* ctx, const void* x, const float* wg,
                                  const void* w1, const void* w2, int32_t T, int32_t k,
-                                 float capacity_factor, int32_t n_chunks, void* y,
+                                 double capacity_factor, int32_t n_chunks, void* y,
                                  int32_t* expert_idx, int32_t* slot, float* combine_w,
                                  lancet_stream_t stream);
 

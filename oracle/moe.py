@@ -372,7 +372,7 @@ def expert_weights(w1_ranks, w2_ranks, e, E_l):
 
 def forward(xs, wg, w1_ranks, w2_ranks, k, cf, n_chunks, act="gelu_tanh",
             renormalize=False, token_subset=None, gate_fp64=False, gate="switch",
-            seed=0) -> LayerResult:
+            seed=0, experts=None) -> LayerResult:
     """The MoE layer forward over G = len(xs) ranks.
 
     xs[r]: [T_r, d] tokens of rank r; w1_ranks[r]: [E_l, f, d], w2_ranks[r]: [E_l, d, f].
@@ -380,7 +380,9 @@ def forward(xs, wg, w1_ranks, w2_ranks, k, cf, n_chunks, act="gelu_tanh",
     "restores the received tokens back to their original order"; dropped choices
     contribute zero, R6).  `token_subset` (list per rank of token ids, or None) restricts
     the expert math to those tokens (routing is always over the whole batch); y rows of
-    other tokens are NaN.
+    other tokens are NaN.  `experts` (global expert ids, or None) restricts the expert math
+    to those experts -- a cost restriction for large shapes: y then holds only their
+    contributions, and backward() gives the full dW1 / dW2 of exactly those experts.
 
     The all-to-all is pure data movement: a token's expert output depends only
     on the token and the expert's weights, so the oracle evaluates each expert on the rows
@@ -397,7 +399,7 @@ def forward(xs, wg, w1_ranks, w2_ranks, k, cf, n_chunks, act="gelu_tanh",
         keep[np.arange(T) if token_subset is None else np.asarray(token_subset[r], dtype=np.int64)] = True
         y = np.full((T, d), np.nan)
         y[keep] = 0.0
-        for e in range(E):
+        for e in (range(E) if experts is None else sorted(set(experts))):
             # admitted pairs of expert e, in token-major (buffer slot) order
             t_sel, j_sel = np.nonzero((rt.idx == e) & (rt.slot >= 0) & keep[:, None])
             if t_sel.size == 0:

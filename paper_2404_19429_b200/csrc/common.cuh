@@ -24,6 +24,8 @@ constexpr int kRowAlign = 128;   // expert / (expert, chunk) row blocks start on
 constexpr int kMaxK = 8;         // top-k bound on the device side
 constexpr int kMaxChunks = 64;
 constexpr int kMaxExperts = 256;
+constexpr int kPeerRowBits = 24; // push mode: K5 hands K6 (owner rank << 24) | row in the owner's
+                                 // dX buffer (lancet_create_peer bounds rows and world)
 constexpr int kScanTile = 256;   // tokens per block of the slot scan (K2); >= kMaxExperts
 
 __host__ __device__ inline int round_up(int a, int b) { return (a + b - 1) / b * b; }

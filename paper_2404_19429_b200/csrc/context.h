@@ -44,6 +44,20 @@ struct PeerLinks {
     std::vector<void*> opened;            // IPC mappings to close
     std::vector<int> matrix;              // host copy of the last count matrix [G][E][n]
     int* h_matrix = nullptr;              // pinned staging of the matrix
+    // device-side protocol of the push mode (peer.cu dev_*): the step counter lives on the
+    // device so flag values are never baked into the host's enqueue (graph-capturable), and
+    // waits are kernels that give up after timeout_ns and record why in err (poison)
+    uint32_t* d_seq = nullptr;            // [0] step (bumped by each forward), [1] step of the
+                                          // last backward
+    uint32_t** d_flag_tab = nullptr;      // [G] device copy of `flags`
+    int** d_counts_tab = nullptr;         // [G] device copy of `counts`
+    char** d_dxesrc = nullptr;            // [G] device copy of src[PK_DXE] (K6 reads in place)
+    int* d_plan_scratch = nullptr;        // [2][E][n_max] owner group rows / offsets
+    uint32_t* h_err = nullptr;            // mapped pinned word: 0, or the first failed wait
+    uint32_t* d_err = nullptr;            //   (device alias of h_err)
+    unsigned long long timeout_ns = 60ull * 1000 * 1000 * 1000;
+    unsigned long long cfg_hash = 0;      // exported in the blob, checked by every importer
+    int rows_cap = 0;                     // expert-side rows allocated (pushes are bounded by it)
     size_t flag_index(int consumed, int kind, int chunk, int r) const {
         return (((size_t)consumed * PK_N + kind) * n_max + chunk) * world + r;
     }
@@ -69,6 +83,7 @@ struct lancet_ctx {
     lancet::Transport* comm = nullptr;
     lancet::PeerLinks* peer = nullptr;   // copy-engine peer transport (instead of comm)
     bool peer_ready = false;             // peers imported
+    bool push = false;                   // LANCET_FLAG_PEER_PUSH, fixed at creation
 
     // streams / events
     cudaStream_t s_comp = nullptr, s_comm = nullptr;
@@ -115,7 +130,7 @@ struct lancet_ctx {
     bool have_fwd = false;
     const void* x = nullptr; const float* wg = nullptr; const void* w1 = nullptr; const void* w2 = nullptr;
     int T = 0, k = 0, n = 0, C = 0;
-    float cf = 0.f;
+    double cf = 0.0;
     int n_groups = 0;          // expert-side GEMM groups of the last forward
     std::vector<int> host_send, host_recv, host_grp_rows, host_grp_off;  // world > 1
     int launches_fwd = 0, launches_bwd = 0;

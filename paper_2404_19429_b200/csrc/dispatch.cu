@@ -296,7 +296,11 @@ combine_bwd_kernel(const Elt* __restrict__ dy, const Elt* __restrict__ comb,
             gj[j] = rows[j] >= 0 ? s : 0.f;
             if (lane == 0) g[(size_t)t * k + j] = gj[j];
             sg = fmaf(gj[j], wj[j], sg);
-            if (lane == j) myrow = rows[j];
+            // push mode: where K6 will read this choice's dX row -- (owner, row in its buffer)
+            if (lane == j)
+                myrow = (push_base && rows[j] >= 0)
+                            ? (((ids[j] / E_l) << kPeerRowBits) | (push_base[ids[j]] + rows[j] - send_off[ids[j]]))
+                            : rows[j];
         }
     }
     // inputs of the gate backward (K6/K7): packed source rows and dlogit from the softmax

@@ -27,11 +27,22 @@ constexpr size_t kSmemWgMax = 64 * 1024;
 // gate does not fit in shared memory.
 constexpr int kK6T = 2;
 
+// dX row of a choice: local (dxe + row d), or -- push mode, the backward's second all-to-all
+// fused into K6 -- row (row & mask) of the owner's dX buffer tab[row >> kPeerRowBits], read in
+// place over peer memory
+template <typename Elt>
+__device__ __forceinline__ const Elt* dx_row(const Elt* dxe, const char* const* tab, int row, int d)
+{
+    if (tab)
+        return reinterpret_cast<const Elt*>(tab[row >> kPeerRowBits]) + (size_t)(row & ((1 << kPeerRowBits) - 1)) * d;
+    return dxe + (size_t)row * d;
+}
+
 template <typename Elt, int KK, bool SMEM_WG>
 __global__ void __launch_bounds__(kWarps * 32)
 k6_gather_kernel(const Elt* __restrict__ dxe, const int* __restrict__ prow,
                  const float* __restrict__ dlogit, const float* __restrict__ wgT, int t0, int t1,
-                 int k, int d, int E, Elt* __restrict__ dx)
+                 int k, int d, int E, Elt* __restrict__ dx, const char* const* __restrict__ src_tab)
 {
     pdl_wait();   // programmatic dependent launch: predecessor's writes visible
     extern __shared__ __align__(16) float swt[];
@@ -71,7 +82,7 @@ k6_gather_kernel(const Elt* __restrict__ dxe, const int* __restrict__ prow,
 #pragma unroll
                     for (int j = 0; j < KK; ++j)
                         if (rows[q][j] >= 0 && v0 + 32 * u < nvec)
-                            raw[q][u][j] = ld_nc_v4(reinterpret_cast<const uint4*>(dxe + (size_t)rows[q][j] * d) + v0 + 32 * u);
+                            raw[q][u][j] = ld_nc_v4(reinterpret_cast<const uint4*>(dx_row(dxe, src_tab, rows[q][j], d)) + v0 + 32 * u);
             float acc[kK6T][U][V];
 #pragma unroll
             for (int q = 0; q < kK6T; ++q)
@@ -289,7 +300,7 @@ template <typename Elt, int KK, int EE, int NTC, int EG = 1>
 __global__ void __launch_bounds__(256)
 k6_stream_kernel(const Elt* __restrict__ dxe, const int* __restrict__ prow,
                  const float* __restrict__ dlogit, const float* __restrict__ wg, int t0, int t1,
-                 int k, int d, int E, int tpb, Elt* __restrict__ dx)
+                 int k, int d, int E, int tpb, Elt* __restrict__ dx, const char* const* __restrict__ src_tab)
 {
     pdl_wait();   // programmatic dependent launch: predecessor's writes visible
     using G = K6Geom<Elt, KK>;
@@ -336,7 +347,7 @@ k6_stream_kernel(const Elt* __restrict__ dxe, const int* __restrict__ prow,
             for (int j = 0; j < KK; ++j) {
                 const int row = r < nt ? srow[r * KK + j] : -1;
                 if (row >= 0) {
-                    const uint4* src = reinterpret_cast<const uint4*>(dxe + (size_t)row * d + i0);
+                    const uint4* src = reinterpret_cast<const uint4*>(dx_row(dxe, src_tab, row, d) + i0);
 #pragma unroll
                     for (int v = 0; v < NV; ++v) cp_async16_s(slot + ((u * KK + j) * NV + v) * NTD + dg, src + v);
                 }
@@ -738,7 +749,8 @@ int launch_wg_transpose(const float* wg, int d, int E, float* wgT, cudaStream_t 
 
 template <typename Elt, int KK, bool SM>
 static void launch_k6(const DispatchArgs& a, const void* dxe, const int* prow, const float* dlogit,
-                      const float* wgT, void* dx, int t0, int t1, int num_sms, cudaStream_t s)
+                      const float* wgT, void* dx, int t0, int t1, int num_sms, cudaStream_t s,
+                      const char* const* src_tab)
 {
     const size_t smem = SM ? sizeof(float) * (size_t)a.d * a.E : 0;
     static bool attr = false;
@@ -750,7 +762,7 @@ static void launch_k6(const DispatchArgs& a, const void* dxe, const int* prow, c
     const int need = ceil_div(t1 - t0, kWarps * kK6T);
     const int grid = std::max(1, std::min(need, 4 * num_sms));
     launch_k(k6_gather_kernel<Elt, KK, SM>, grid, kWarps * 32, smem, s, (const Elt*)dxe, prow, dlogit, wgT, t0, t1,
-                                                                  a.k, a.d, a.E, (Elt*)dx);
+                                                                  a.k, a.d, a.E, (Elt*)dx, src_tab);
 }
 
 static bool stream_ok(int d, int E) { return E <= 8 && d % 256 == 0 && d <= 2048; }
@@ -777,7 +789,8 @@ static int ee_of(int E) { return E <= 2 ? 2 : E <= 4 ? 4 : 8; }
 
 template <typename Elt, int KK, int EE>
 static void launch_k6_stream(const DispatchArgs& a, const void* dxe, const int* prow, const float* dlogit,
-                             const float* wg, void* dx, int t0, int t1, int num_sms, cudaStream_t s)
+                             const float* wg, void* dx, int t0, int t1, int num_sms, cudaStream_t s,
+                             const char* const* src_tab)
 {
     using G = K6Geom<Elt, KK>;
     const int NT = a.d / 8;
@@ -795,15 +808,16 @@ static void launch_k6_stream(const DispatchArgs& a, const void* dxe, const int* 
     }
     if (NT == 128)      // d = 1024: compile-time ring strides
         launch_k(k6_stream_kernel<Elt, KK, EE, 128>, ceil_div(t1 - t0, tpb), NT, smem, s, 
-            (const Elt*)dxe, prow, dlogit, wg, t0, t1, a.k, a.d, a.E, tpb, (Elt*)dx);
+            (const Elt*)dxe, prow, dlogit, wg, t0, t1, a.k, a.d, a.E, tpb, (Elt*)dx, src_tab);
     else
         launch_k(k6_stream_kernel<Elt, KK, EE, 0>, ceil_div(t1 - t0, tpb), NT, smem, s, 
-            (const Elt*)dxe, prow, dlogit, wg, t0, t1, a.k, a.d, a.E, tpb, (Elt*)dx);
+            (const Elt*)dxe, prow, dlogit, wg, t0, t1, a.k, a.d, a.E, tpb, (Elt*)dx, src_tab);
 }
 
 template <typename Elt, int KK, int EG>
 static void launch_k6_wide(const DispatchArgs& a, const void* dxe, const int* prow, const float* dlogit,
-                           const float* wg, void* dx, int t0, int t1, int num_sms, cudaStream_t s)
+                           const float* wg, void* dx, int t0, int t1, int num_sms, cudaStream_t s,
+                           const char* const* src_tab)
 {
     using G = K6Geom<Elt, KK>;
     const int NTD = wide_ntd(a.d, EG), DS = a.d / 8 / NTD, NT = NTD * EG;
@@ -817,21 +831,21 @@ static void launch_k6_wide(const DispatchArgs& a, const void* dxe, const int* pr
         attr = true;
     }
     launch_k(k6_stream_kernel<Elt, KK, 8, 0, EG>, dim3(ceil_div(t1 - t0, tpb), DS), NT, smem, s,
-             (const Elt*)dxe, prow, dlogit, wg, t0, t1, a.k, a.d, a.E, tpb, (Elt*)dx);
+             (const Elt*)dxe, prow, dlogit, wg, t0, t1, a.k, a.d, a.E, tpb, (Elt*)dx, src_tab);
 }
 
 int launch_unpermute_gate_bwd(const DispatchArgs& a, const void* dxe, const int* prow,
                               const float* dlogit, const float* wg, const float* wgT, void* dx, int t0, int t1,
-                              int num_sms, bool is_bf16, cudaStream_t s)
+                              int num_sms, bool is_bf16, cudaStream_t s, const char* const* src_tab)
 {
     if (t1 <= t0) return 0;
     // wide K6 only from E = 32 (at E = 16 the shared-memory Wg^T kernel measured faster)
     if (wide_ok(a.d, a.E) && a.E >= 32 && a.k <= 4) {
 #define K6W(Elt, KK)                                                                                              \
     do {                                                                                                          \
-        if (a.E == 16) launch_k6_wide<Elt, KK, 2>(a, dxe, prow, dlogit, wg, dx, t0, t1, num_sms, s);             \
-        else if (a.E == 32) launch_k6_wide<Elt, KK, 4>(a, dxe, prow, dlogit, wg, dx, t0, t1, num_sms, s);        \
-        else launch_k6_wide<Elt, KK, 8>(a, dxe, prow, dlogit, wg, dx, t0, t1, num_sms, s);                       \
+        if (a.E == 16) launch_k6_wide<Elt, KK, 2>(a, dxe, prow, dlogit, wg, dx, t0, t1, num_sms, s, src_tab);             \
+        else if (a.E == 32) launch_k6_wide<Elt, KK, 4>(a, dxe, prow, dlogit, wg, dx, t0, t1, num_sms, s, src_tab);        \
+        else launch_k6_wide<Elt, KK, 8>(a, dxe, prow, dlogit, wg, dx, t0, t1, num_sms, s, src_tab);                       \
     } while (0)
         if (is_bf16) {
             if (a.k == 1) K6W(bf16, 1); else if (a.k == 2) K6W(bf16, 2); else K6W(bf16, 4);
@@ -845,9 +859,9 @@ int launch_unpermute_gate_bwd(const DispatchArgs& a, const void* dxe, const int*
         const int ee = ee_of(a.E);
 #define K6S(Elt, KK)                                                                                              \
     do {                                                                                                          \
-        if (ee == 2) launch_k6_stream<Elt, KK, 2>(a, dxe, prow, dlogit, wg, dx, t0, t1, num_sms, s);            \
-        else if (ee == 4) launch_k6_stream<Elt, KK, 4>(a, dxe, prow, dlogit, wg, dx, t0, t1, num_sms, s);       \
-        else launch_k6_stream<Elt, KK, 8>(a, dxe, prow, dlogit, wg, dx, t0, t1, num_sms, s);                    \
+        if (ee == 2) launch_k6_stream<Elt, KK, 2>(a, dxe, prow, dlogit, wg, dx, t0, t1, num_sms, s, src_tab);            \
+        else if (ee == 4) launch_k6_stream<Elt, KK, 4>(a, dxe, prow, dlogit, wg, dx, t0, t1, num_sms, s, src_tab);       \
+        else launch_k6_stream<Elt, KK, 8>(a, dxe, prow, dlogit, wg, dx, t0, t1, num_sms, s, src_tab);                    \
     } while (0)
         if (is_bf16) {
             if (a.k == 1) K6S(bf16, 1); else if (a.k == 2) K6S(bf16, 2); else K6S(bf16, 4);
@@ -860,11 +874,11 @@ int launch_unpermute_gate_bwd(const DispatchArgs& a, const void* dxe, const int*
     const bool sm = (size_t)a.d * a.E * 4 <= kSmemWgMax;
     LANCET_DISPATCH_K(a.k, {
         if (is_bf16) {
-            if (sm) launch_k6<bf16, KK, true>(a, dxe, prow, dlogit, wgT, dx, t0, t1, num_sms, s);
-            else launch_k6<bf16, KK, false>(a, dxe, prow, dlogit, wgT, dx, t0, t1, num_sms, s);
+            if (sm) launch_k6<bf16, KK, true>(a, dxe, prow, dlogit, wgT, dx, t0, t1, num_sms, s, src_tab);
+            else launch_k6<bf16, KK, false>(a, dxe, prow, dlogit, wgT, dx, t0, t1, num_sms, s, src_tab);
         } else {
-            if (sm) launch_k6<float, KK, true>(a, dxe, prow, dlogit, wgT, dx, t0, t1, num_sms, s);
-            else launch_k6<float, KK, false>(a, dxe, prow, dlogit, wgT, dx, t0, t1, num_sms, s);
+            if (sm) launch_k6<float, KK, true>(a, dxe, prow, dlogit, wgT, dx, t0, t1, num_sms, s, src_tab);
+            else launch_k6<float, KK, false>(a, dxe, prow, dlogit, wgT, dx, t0, t1, num_sms, s, src_tab);
         }
     });
     return 1;

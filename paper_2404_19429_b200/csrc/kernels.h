@@ -85,9 +85,11 @@ int launch_wg_transpose(const float* wg, int d, int E, float* wgT, cudaStream_t 
 bool gate_bwd_needs_wgT(int d, int E);   // true: the general K6 reads Wg^T (launch_wg_transpose)
 // K6: dx_t = sum_j dX[prow_tj] + sum_e dlogit_te Wg[:, e]   (wg [d][E]; wgT = Wg transposed,
 // [E][d], only read by the general path)
+// src_tab (push mode, optional): prow holds (owner << kPeerRowBits) | row and the dX rows are
+// read in place from src_tab[owner] (the owners' dX buffers over peer memory) instead of dxe
 int launch_unpermute_gate_bwd(const DispatchArgs& a, const void* dxe, const int* prow,
                               const float* dlogit, const float* wg, const float* wgT, void* dx, int t0, int t1,
-                              int num_sms, bool is_bf16, cudaStream_t s);
+                              int num_sms, bool is_bf16, cudaStream_t s, const char* const* src_tab = nullptr);
 // dWg = x^T dlogit (K7); partial: [ceil(T/64)][d][E] fp32 scratch
 int launch_dwg(const void* x, const float* dlogit, int T, int d, int E, float* partial,
                float* dwg, bool is_bf16, int num_sms, cudaStream_t s);

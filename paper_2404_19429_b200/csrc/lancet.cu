@@ -66,10 +66,10 @@ lancet_status fail(lancet_ctx* c, lancet_status st, const std::string& msg)
                                                 cudaGetErrorString(e_));                \
     } while (0)
 
-int capacity_of(int T, int k, int E, float cf)
+int capacity_of(int T, int k, int E, double cf)
 {
     // R4: C = max(1, min(T, ceil(cf*k*T/E))) in double
-    const double v = std::ceil((double)cf * (double)k * (double)T / (double)E);
+    const double v = std::ceil(cf * (double)k * (double)T / (double)E);
     long c = (long)v;
     if (c > T) c = T;
     if (c < 1) c = 1;
@@ -142,13 +142,23 @@ struct OpScope {
 // ---- grouped GEMM dispatch ---------------------------------------------------------------
 lancet_status run_gemm(lancet_ctx* c, GemmArgs& a, cudaStream_t s, int* launches)
 {
-    const bool use_tc = c->bf16 && !(c->cfg.flags & LANCET_FLAG_SIMT_GEMM) && gemm_tc_supported(a);
-    if (use_tc) {
+    if (c->bf16 && !(c->cfg.flags & LANCET_FLAG_SIMT_GEMM)) {
         a.multicast = (c->cfg.flags & LANCET_FLAG_GEMM_MULTICAST) != 0;
-        // at world > 1 (NCCL) leave LANCET_COMM_SMS SMs to the all-to-all kernels
-        const int all = (c->comm && c->comm->is_nccl()) ? c->num_sms - LANCET_COMM_SMS : c->num_sms;
+        // leave LANCET_COMM_SMS SMs to the exchange kernels running beside the persistent GEMMs:
+        // NCCL's (world > 1) and the fused push kernels on the comm stream (push mode)
+        const bool reserve = (c->comm && c->comm->is_nccl()) ||
+                             (c->push && !(c->cfg.flags & LANCET_FLAG_SERIAL));
+        const int all = reserve ? c->num_sms - LANCET_COMM_SMS : c->num_sms;
         const int sms = c->cfg.gemm_sms > 0 ? std::min(c->cfg.gemm_sms, c->num_sms) : all;
-        *launches += launch_gemm_tc(a, sms, s);
+        const int r = launch_gemm_tc(a, sms, s);
+        if (r < 0) {
+            CHECK_LAUNCH();
+            return fail(c, LANCET_ERR_UNSUPPORTED,
+                        "tcgen05 GEMM: shape or layout not supported (N=" + std::to_string(a.N) + " K=" +
+                            std::to_string(a.K) + " M=" + std::to_string(a.M) + " groups=" +
+                            std::to_string(a.n_groups) + ") or tensor-map encoding failed");
+        }
+        *launches += r;
     } else {
         *launches += launch_gemm_simt(a, c->bf16, s);
     }
@@ -367,6 +377,10 @@ lancet_status create_common(lancet_ctx* c, int world, int rank, int device, cons
 lancet_status ensure_expert_rows(lancet_ctx* c, int rows)
 {
     if (rows <= c->rows_exp) return LANCET_OK;
+    // peers map these buffers (CUDA IPC): never reallocate under them
+    if (c->peer) return fail(c, LANCET_ERR_ARG, "peer transport: the step needs " + std::to_string(rows) +
+                                                    " expert-side rows, more than the " + std::to_string(c->rows_exp) +
+                                                    " allocated at creation");
     const int d = c->cfg.d_model, f = c->cfg.d_ffn;
     const int newrows = round_up(std::max(rows, c->rows_exp + c->rows_exp / 4), kRowAlign);
     CK(cudaDeviceSynchronize());
@@ -396,6 +410,10 @@ lancet_status check_ready(lancet_ctx* c)
 {
     if (!c) return fail(nullptr, LANCET_ERR_ARG, "ctx is NULL");
     if (c->poisoned) return fail(c, LANCET_ERR_STATE, "context poisoned by an earlier error: " + c->err);
+    if (const uint32_t pe = lancet::peer_error(c)) {
+        c->poisoned = true;
+        return fail(c, LANCET_ERR_STATE, "context poisoned: " + lancet::peer_error_text(pe));
+    }
     cudaError_t e = cudaSetDevice(c->device);
     if (e != cudaSuccess) return fail(c, LANCET_ERR_CUDA, cudaGetErrorString(e));
     return LANCET_OK;
@@ -541,6 +559,215 @@ __global__ void send_counts_kernel(const int* __restrict__ S, int E, int n, int*
     out[q] = S[e * (n + 1) + c + 1] - S[e * (n + 1) + c];
 }
 
+
+// ---- push mode (LANCET_FLAG_PEER_PUSH on the peer transport) -------------------------------
+// All four exchanges are fused into the token kernels over peer memory: K3 writes each admitted
+// row into the owner's receive buffer (dispatch), K4 reads the expert outputs where the owners'
+// fc2 wrote them (combine), K5 writes its dO rows into the owners' dO buffers (backward #1) and
+// K6 reads the dX rows where the owners' dfc1 wrote them (backward #2).  The exchange plan is
+// built on the device from the gathered count matrix and every flag is a kernel (peer.cu
+// dev_*), so nothing waits on the host: the step is graph-capturable.
+//
+// Streams (S1 / S2): the compute stream runs routing, the plan and
+// the expert GEMMs of chunk after chunk; the comm stream runs the fused exchange kernels --
+// chunk c+1's push and chunk c-1's combine under chunk c's GEMMs, on the SMs the persistent
+// GEMMs leave free (gemm_sms = all - LANCET_COMM_SMS by default).  LANCET_FLAG_SERIAL puts
+// everything on one stream with the chunks merged (the unoverlapped baseline).
+
+#define DEV(call)                                                                       \
+    do {                                                                                \
+        if (call) return fail(c, LANCET_ERR_CUDA, std::string(#call) + ": " +           \
+                                                     cudaGetErrorString(cudaGetLastError())); \
+    } while (0)
+
+int push_group_rows_bound(const lancet_ctx* c)
+{
+    // a group (e_l, c) holds at most min(C, T) <= max_tokens rows of each source rank
+    return std::min(c->rows_exp, round_up(c->world * c->cfg.max_tokens, kRowAlign));
+}
+
+lancet_status forward_push(lancet_ctx* c, const RouteArgs& ra, const DispatchArgs& da, const void* x,
+                           void* y, cudaStream_t s, int& L)
+{
+    lancet::PeerLinks* pr = c->peer;
+    const int E = c->cfg.n_experts, E_l = c->E_l, n = c->n, T = c->T;
+    const bool ident = c->cfg.act == LANCET_ACT_IDENTITY_EXPERT;
+    const bool serial = c->cfg.flags & LANCET_FLAG_SERIAL;
+    const bool nocomm = c->cfg.flags & LANCET_FLAG_NO_COMM;
+    cudaStream_t sc = c->s_comp, sm = serial ? c->s_comp : c->s_comm;
+    using namespace lancet;
+    CK(cudaEventRecord(c->ev_fork, s));
+    CK(cudaStreamWaitEvent(sc, c->ev_fork, 0));
+    CK(cudaStreamWaitEvent(c->s_comm, c->ev_fork, 0));
+    // a forward without backward: release the owners' outputs the last forward read (with
+    // that step's number: before the bump)
+    if (c->out_consume_pending) {
+        DEV(dev_signal(c, 1, PK_OUT, 0, sc));
+        c->out_consume_pending = false;
+    }
+    ++pr->seq;
+    DEV(dev_seq_bump(c, sc));
+    // this rank's receive buffer is free for the step's pushes: its readers (the previous
+    // step's GEMMs) are behind on this stream
+    DEV(dev_signal(c, 0, PK_XEFREE, 0, sc));
+    { OpScope op(c, "gate", 0, -1, sc); L += launch_routing(ra, c->bf16, sc); }
+    int* d_send = c->counts_dev;
+    launch_k(send_counts_kernel, ceil_div(E * n, 256), 256, 0, sc, c->S, E, n, d_send);
+    ++L;
+    CHECK_LAUNCH();
+    {   // C1: the size exchange -- the count matrix all-gathered through peer memory
+        OpScope op(c, "a2a_counts", 1, -1, sc);
+        DEV(dev_counts(c, d_send, n, sc));
+        L += 2;
+    }
+    DEV(dev_plan(c, n, sc));
+    ++L;
+    int* d_grp_rows = c->grp_dev;
+    int* d_grp_off = c->grp_dev + n * E_l;
+    L += launch_zero_pads(c->xe, c->cfg.d_model, d_grp_off, d_grp_rows, n * E_l, (int)c->elt, sc);
+    CHECK_LAUNCH();
+    cudaEvent_t ev_plan = c->ev_pool[0];
+    CK(cudaEventRecord(ev_plan, sc));
+    CK(cudaStreamWaitEvent(sm, ev_plan, 0));
+    // K3 + C2-d fused: chunk c's rows go straight to the owners' receive buffers
+    DEV(dev_wait(c, 0, PK_XEFREE, 0, TGT_STEP, sm));
+    for (int ch = 0; ch < n; ++ch) {
+        {
+            OpScope op(c, "a2a_dispatch_push", 1, serial ? -1 : ch, sm);
+            if (!nocomm)
+                L += launch_permute_push(da, x, chunk_start(T, n, ch), chunk_start(T, n, ch + 1), E_l,
+                                         pr->d_push_base + (size_t)ch * E, pr->d_xe, c->bf16, sm);
+        }
+        CHECK_LAUNCH();
+        DEV(dev_signal(c, 0, PK_PUSH, ch, sm));
+    }
+    const int nc = serial ? 1 : n;
+    const int mr = push_group_rows_bound(c);
+    for (int cc = 0; cc < nc; ++cc) {
+        const int c0 = serial ? 0 : cc, c1 = serial ? n : cc + 1;
+        for (int ch = c0; ch < c1; ++ch) DEV(dev_wait(c, 0, PK_PUSH, ch, TGT_STEP, sc));
+        if (cc == 0) DEV(dev_wait(c, 1, PK_OUT, 0, TGT_PREV, sc));   // peers done with last step's outputs
+        if (!ident) {
+            lancet_status st = expert_forward(c, d_grp_rows + c0 * E_l, d_grp_off + c0 * E_l, (c1 - c0) * E_l,
+                                              mr, sc, serial ? -1 : cc, &L);
+            if (st) return st;
+        }
+        DEV(dev_signal(c, 0, PK_OUT, cc, sc));
+    }
+    // C2-c + K4 fused: chunk c's tokens gather the expert outputs from the owners' buffers
+    for (int cc = 0; cc < nc; ++cc) {
+        const int c0 = serial ? 0 : cc, c1 = serial ? n : cc + 1;
+        DEV(dev_wait(c, 0, PK_OUT, cc, TGT_STEP, sm));
+        for (int ch = c0; ch < c1; ++ch) {
+            OpScope op(c, "a2a_combine_fused", 1, serial ? -1 : ch, sm);
+            if (nocomm) continue;
+            L += launch_combine(da, c->comb, y, chunk_start(T, n, ch), chunk_start(T, n, ch + 1), c->bf16, sm,
+                                pr->d_push_base + (size_t)ch * E, pr->d_outsrc, E_l);
+        }
+        CHECK_LAUNCH();
+    }
+    c->out_consume_pending = true;
+    CK(cudaEventRecord(c->ev_join, sc));
+    CK(cudaStreamWaitEvent(s, c->ev_join, 0));
+    if (sm != sc) {
+        cudaEvent_t e2 = c->ev_pool[1];
+        CK(cudaEventRecord(e2, sm));
+        CK(cudaStreamWaitEvent(s, e2, 0));
+    }
+    return LANCET_OK;
+}
+
+lancet_status backward_push(lancet_ctx* c, const DispatchArgs& da, const void* dy, void* dx, float* dwg,
+                            float* dw1, float* dw2, int renorm, cudaStream_t s, int& L)
+{
+    using namespace lancet;
+    lancet::PeerLinks* pr = c->peer;
+    const int E = c->cfg.n_experts, E_l = c->E_l, n = c->n, T = c->T, d = c->cfg.d_model;
+    const bool ident = c->cfg.act == LANCET_ACT_IDENTITY_EXPERT;
+    const bool serial = c->cfg.flags & LANCET_FLAG_SERIAL;
+    const bool late_dw = serial || (c->cfg.flags & LANCET_FLAG_NO_DW_OVERLAP);
+    const bool nocomm = c->cfg.flags & LANCET_FLAG_NO_COMM;
+    cudaStream_t sc = c->s_comp, sm = serial ? c->s_comp : c->s_comm;
+    CK(cudaEventRecord(c->ev_fork, s));
+    CK(cudaStreamWaitEvent(sc, c->ev_fork, 0));
+    CK(cudaStreamWaitEvent(c->s_comm, c->ev_fork, 0));
+    int* d_grp_rows = c->grp_dev;
+    int* d_grp_off = c->grp_dev + n * E_l;
+    // this rank's dO buffer is free (its readers, the previous step's GEMMs, are behind on
+    // this stream); its pads must be zero for the K-grouped dW GEMMs
+    DEV(dev_signal(c, 0, PK_DOUTFREE, 0, sc));
+    L += launch_zero_pads(c->dout, d, d_grp_off, d_grp_rows, n * E_l, (int)c->elt, sc);
+    CHECK_LAUNCH();
+    cudaEvent_t ev0 = c->ev_pool[0];
+    CK(cudaEventRecord(ev0, sc));
+    CK(cudaStreamWaitEvent(sm, ev0, 0));
+    // K5 + C2-b1 fused: dO rows straight into the owners' dO buffers; o read in place
+    DEV(dev_wait(c, 0, PK_DOUTFREE, 0, TGT_STEP, sm));
+    for (int ch = 0; ch < n; ++ch) {
+        {
+            OpScope op(c, "a2a_bwd_dispatch_push", 1, serial ? -1 : ch, sm);
+            L += launch_combine_bwd(da, dy, c->comb, c->g, c->dcomb, chunk_start(T, n, ch), chunk_start(T, n, ch + 1),
+                                    false, c->logits, renorm, c->dlogit, c->prow, c->bf16, sm,
+                                    nocomm ? nullptr : pr->d_push_base + (size_t)ch * E, pr->d_dout, E_l,
+                                    nocomm ? nullptr : pr->d_outsrc);
+        }
+        CHECK_LAUNCH();
+        DEV(dev_signal(c, 0, PK_PUSH2, ch, sm));
+    }
+    DEV(dev_signal(c, 1, PK_OUT, 0, sm));   // the owners' outputs are consumed (K4 and K5 done)
+    c->out_consume_pending = false;
+    lancet_status st = gate_backward_dwg(c, dwg, sm, &L);     // K7 beside the dX GEMMs
+    if (st) return st;
+    // dX GEMMs per chunk, each followed by its dW GEMMs
+    const int nc = serial ? 1 : n;
+    const int mr = push_group_rows_bound(c);
+    for (int cc = 0; cc < nc; ++cc) {
+        const int c0 = serial ? 0 : cc, c1 = serial ? n : cc + 1;
+        for (int ch = c0; ch < c1; ++ch) DEV(dev_wait(c, 0, PK_PUSH2, ch, TGT_STEP, sc));
+        if (cc == 0) DEV(dev_wait(c, 1, PK_DXE, 0, TGT_LAST_BWD, sc));   // last backward's K6 readers done
+        if (!ident) {
+            st = expert_backward_dx(c, c->dout, d_grp_rows + c0 * E_l, d_grp_off + c0 * E_l, (c1 - c0) * E_l, mr, sc,
+                                    serial ? -1 : cc, &L);
+            if (st) return st;
+        }
+        DEV(dev_signal(c, 0, PK_DXE, cc, sc));
+        if (!ident && !late_dw)
+            for (int ch = c0; ch < c1; ++ch) {
+                st = expert_backward_dw(c, c->dout, d_grp_rows + ch * E_l, d_grp_off + ch * E_l, E_l, dw1, dw2,
+                                        ch > 0, sc, ch, &L);
+                if (st) return st;
+            }
+    }
+    if (!ident && late_dw)
+        for (int ch = 0; ch < n; ++ch) {
+            st = expert_backward_dw(c, c->dout, d_grp_rows + ch * E_l, d_grp_off + ch * E_l, E_l, dw1, dw2, ch > 0,
+                                    sc, ch, &L);
+            if (st) return st;
+        }
+    // C2-b2 + K6 fused: chunk c's tokens sum their dX rows where the owners' dfc1 wrote them
+    for (int cc = 0; cc < nc; ++cc) {
+        const int c0 = serial ? 0 : cc, c1 = serial ? n : cc + 1;
+        DEV(dev_wait(c, 0, PK_DXE, cc, TGT_STEP, sm));
+        for (int ch = c0; ch < c1; ++ch) {
+            const int t0 = chunk_start(T, n, ch), t1 = chunk_start(T, n, ch + 1);
+            OpScope op(c, "a2a_bwd_combine_fused", 1, serial ? -1 : ch, sm);
+            if (ch == 0 && gate_bwd_needs_wgT(d, E)) L += launch_wg_transpose(c->wg, d, E, c->wgT, sm);
+            L += launch_unpermute_gate_bwd(da, c->dxcomb, c->prow, c->dlogit, c->wg, c->wgT, dx, t0, t1, c->num_sms,
+                                           c->bf16, sm, nocomm ? nullptr : (const char* const*)pr->d_dxesrc);
+        }
+        CHECK_LAUNCH();
+    }
+    DEV(dev_signal(c, 1, PK_DXE, 0, sm, /*mark_bwd=*/true));
+    c->bwd_seq = pr->seq;
+    CK(cudaEventRecord(c->ev_join, sc));
+    CK(cudaStreamWaitEvent(s, c->ev_join, 0));
+    if (sm != sc) {
+        cudaEvent_t e2 = c->ev_pool[1];
+        CK(cudaEventRecord(e2, sm));
+        CK(cudaStreamWaitEvent(s, e2, 0));
+    }
+    return LANCET_OK;
+}
 }  // namespace
 
 // =========================================================================================
@@ -644,7 +871,14 @@ LANCET_API lancet_status lancet_create_peer(lancet_ctx** out, int32_t world, int
     lancet_layer_config cf2 = *cfg;
     cf2.flags |= LANCET_FLAG_FORCE_EP;                  // the expert-parallel path, even at world 1
     auto* c = new lancet_ctx();
+    c->push = (cfg->flags & LANCET_FLAG_PEER_PUSH) != 0;
     st = create_common(c, world, rank, cuda_device, &cf2);
+    if (!st && c->push) {
+        // push mode: K5 hands K6 (owner, row) packed in one int32 (lancet::kPeerRowBits)
+        const long rows = (long)world * cfg->max_tokens * cfg->max_k + (long)c->E_l * cfg->max_chunks * kRowAlign;
+        if (rows >= (1L << kPeerRowBits) || world > (1 << (31 - kPeerRowBits)))
+            st = fail(c, LANCET_ERR_ARG, "push mode: world * max_tokens * max_k must stay below 2^24 rows and world <= 128");
+    }
     if (!st) {
         // the expert-side buffers are mapped by the peers: allocate them at their bound once
         // (every source sends at most max_tokens * max_k rows; + 128-row padding per group)
@@ -656,6 +890,15 @@ LANCET_API lancet_status lancet_create_peer(lancet_ctx** out, int32_t world, int
     if (!st) {
         std::string err;
         if (peer_init(c, err)) st = fail(c, LANCET_ERR_CUDA, err);
+        else {
+            unsigned long long h = cfg_hash(*cfg);
+            for (long v : {(long)cfg->max_tokens, (long)(cfg->flags & LANCET_FLAG_PEER_PUSH), (long)world}) {
+                h ^= (unsigned long long)v;
+                h *= 1099511628211ull;
+            }
+            c->peer->cfg_hash = h;
+            c->peer->rows_cap = c->rows_exp;
+        }
     }
     if (st) {
         g_thread_err = c->err;
@@ -695,6 +938,7 @@ LANCET_API lancet_status lancet_destroy(lancet_ctx* c)
     cudaSetDevice(c->device);
     if (c->peer) {
         cudaDeviceSynchronize();
+        if (!c->poisoned && c->peer_ready) lancet::peer_quiesce(c);
         peer_destroy(c);
     }
     if (c->comm) {
@@ -716,11 +960,39 @@ LANCET_API lancet_status lancet_destroy(lancet_ctx* c)
     return LANCET_OK;
 }
 
+LANCET_API lancet_status lancet_set_peer_timeout_ms(lancet_ctx* c, int64_t ms)
+{
+    lancet_status st = check_ready(c);
+    if (st) return st;
+    if (!c->peer || ms <= 0) return fail(c, LANCET_ERR_ARG, "not a peer-transport context, or ms <= 0");
+    c->peer->timeout_ns = (unsigned long long)ms * 1000000ull;
+    return LANCET_OK;
+}
+
+LANCET_API lancet_status lancet_peer_abort(lancet_ctx* c)
+{
+    if (!c) return fail(nullptr, LANCET_ERR_ARG, "ctx is NULL");
+    if (!c->peer) return fail(c, LANCET_ERR_ARG, "not a peer-transport context");
+    cudaSetDevice(c->device);
+    if (lancet::peer_poison(c, 0xFFFFFFFFu)) return fail(c, LANCET_ERR_CUDA, "peer abort: cudaMemsetAsync of the flags failed");
+    c->poisoned = true;
+    c->err = "peer transport aborted (lancet_peer_abort)";
+    return LANCET_OK;
+}
+
+LANCET_API lancet_status lancet_peer_status(lancet_ctx* c)
+{
+    return check_ready(c);
+}
+
 LANCET_API lancet_status lancet_set_flags(lancet_ctx* c, uint32_t flags)
 {
     if (!c) return fail(nullptr, LANCET_ERR_ARG, "ctx is NULL");
     // FORCE_EP is fixed at creation (the workspace layout depends on it): keep the creation bit
-    flags = (flags & ~(uint32_t)LANCET_FLAG_FORCE_EP) | (c->cfg.flags & LANCET_FLAG_FORCE_EP);
+    // FORCE_EP and PEER_PUSH are fixed at creation (the workspace layout and the peer protocol
+    // depend on them): keep the creation bits
+    const uint32_t fixed = LANCET_FLAG_FORCE_EP | LANCET_FLAG_PEER_PUSH;
+    flags = (flags & ~fixed) | (c->cfg.flags & fixed);
     if ((flags & LANCET_FLAG_RENORMALIZE) != (c->cfg.flags & LANCET_FLAG_RENORMALIZE) && c->world > 1)
         return fail(c, LANCET_ERR_ARG, "RENORMALIZE must be set at creation (checked across ranks)");
     c->cfg.flags = flags;
@@ -731,7 +1003,7 @@ namespace lancet { thread_local bool g_pdl = false; }
 
 LANCET_API lancet_status lancet_moe_forward(lancet_ctx* c, const void* x, const float* wg,
                                             const void* w1, const void* w2, int32_t T, int32_t k,
-                                            float cf, int32_t n, void* y, int32_t* expert_idx,
+                                            double cf, int32_t n, void* y, int32_t* expert_idx,
                                             int32_t* slot_out, float* combine_w,
                                             lancet_stream_t stream_)
 {
@@ -742,7 +1014,7 @@ LANCET_API lancet_status lancet_moe_forward(lancet_ctx* c, const void* x, const 
     if (!x || !wg || !y || (!ident && (!w1 || !w2))) return fail(c, LANCET_ERR_ARG, "null required pointer");
     if (T < 1 || T > c->cfg.max_tokens) return fail(c, LANCET_ERR_ARG, "T must be in [1, max_tokens]");
     if (k < 1 || k > c->cfg.max_k || k > E) return fail(c, LANCET_ERR_ARG, "k must be in [1, min(E, max_k)]");
-    if (!(cf > 0.f) || !std::isfinite(cf)) return fail(c, LANCET_ERR_ARG, "capacity_factor must be > 0");
+    if (!(cf > 0.0) || !std::isfinite(cf)) return fail(c, LANCET_ERR_ARG, "capacity_factor must be > 0");
     if (n < 1 || n > std::min<int>(T, c->cfg.max_chunks)) return fail(c, LANCET_ERR_ARG, "n_chunks must be in [1, min(T, max_chunks)]");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream_);
     lancet::g_pdl = (c->cfg.flags & LANCET_FLAG_NO_PDL) == 0;
@@ -772,7 +1044,11 @@ LANCET_API lancet_status lancet_moe_forward(lancet_ctx* c, const void* x, const 
     ra.bpr_meta = c->bpr_meta;
     DispatchArgs da{T, k, d, E, c->idx, c->slot, c->w, c->send_off, c->send_rows};
 
-    if (!c->ep) {
+    if (c->ep && c->push) {
+        if (!c->peer_ready) return fail(c, LANCET_ERR_STATE, "peer transport: lancet_peer_import not called");
+        st = forward_push(c, ra, da, x, y, s, L);
+        if (st) return st;
+    } else if (!c->ep) {
         // ---- single GPU: no exchange, no host synchronisation --------------------------
         { OpScope op(c, "gate", 0, -1, s); L += launch_routing(ra, c->bf16, s); }
         CHECK_LAUNCH();
@@ -798,23 +1074,13 @@ LANCET_API lancet_status lancet_moe_forward(lancet_ctx* c, const void* x, const 
         size_t ev_i = 0;
         auto next_ev = [&]() { return c->ev_pool[ev_i++]; };
         lancet::PeerLinks* pr = c->peer;
-        const bool push = pr && (c->cfg.flags & LANCET_FLAG_PEER_PUSH);
         if (pr) {
             if (!c->peer_ready) return fail(c, LANCET_ERR_STATE, "peer transport: lancet_peer_import not called");
             ++pr->seq;
-            // a forward without backward: release the owners' outputs the last forward read
-            if (push && c->out_consume_pending) {
-                if (peer_signal(c, 1, lancet::PK_OUT, 0, sc)) return fail(c, LANCET_ERR_CUDA, "cuStreamWriteValue32");
-                c->out_consume_pending = false;
-            }
             // every peer has pulled the previous step's rows from this rank's pull sources (the
             // backward's only if that step had a backward: a forward may follow a forward)
-            if (peer_wait_consumed(c, sc, push, c->bwd_seq == pr->seq - 1))
+            if (peer_wait_consumed(c, sc, false, c->bwd_seq == pr->seq - 1))
                 return fail(c, LANCET_ERR_CUDA, "cuStreamWaitValue32");
-            // push-dispatch: this rank's receive buffer is free for the step's pushes (its
-            // GEMMs of the previous step are behind on this stream, its pull readers done)
-            if (push && peer_signal(c, 0, lancet::PK_XEFREE, 0, sc))
-                return fail(c, LANCET_ERR_CUDA, "cuStreamWriteValue32");
         }
 
         { OpScope op(c, "gate", 0, -1, sc); L += launch_routing(ra, c->bf16, sc); }
@@ -846,15 +1112,12 @@ LANCET_API lancet_status lancet_moe_forward(lancet_ctx* c, const void* x, const 
             }
             CK(cudaEventRecord(c->ev_counts, sm));
         }
-        // K3 permute overlaps the size exchange (push-dispatch: permute fused with the
-        // exchange after the plan, below)
-        const bool serial_ = c->cfg.flags & LANCET_FLAG_SERIAL;
-        const int nc_ = serial_ ? 1 : n;
-        if (!push) {
+        // K3 permute overlaps the size exchange
+        {
             { OpScope op(c, "permute", 0, -1, sc); L += launch_permute(da, x, c->xs, c->bf16, sc); }
             CHECK_LAUNCH();
             if (pr)         // the dispatch sources of every chunk are ready
-                for (int cc = 0; cc < nc_; ++cc)
+                for (int cc = 0; cc < (serial ? 1 : n); ++cc)
                     if (peer_signal(c, 0, lancet::PK_XS, cc, sc)) return fail(c, LANCET_ERR_CUDA, "cuStreamWriteValue32");
         }
         cudaEvent_t ev_perm = next_ev();
@@ -886,30 +1149,6 @@ LANCET_API lancet_status lancet_moe_forward(lancet_ctx* c, const void* x, const 
         CK(cudaMemcpyAsync(c->grp_dev, c->h_grp, sizeof(int) * 2 * n * E_l, cudaMemcpyHostToDevice, sc));
         L += launch_zero_pads(c->xe, d, d_grp_off, d_grp_rows, n * E_l, (int)c->elt, sc);
         CHECK_LAUNCH();
-        if (push) {
-            // K3 + C2 fused: each chunk's admitted rows go straight into the owners' receive
-            // buffers at their final rows: base[c][e] = (owner's group offset of (e, c)) +
-            // (this rank's row offset inside it, R12) - S[e][c]
-            const int me = c->rank;
-            std::vector<int> base((size_t)n * E);
-            for (int ch = 0; ch < n; ++ch)
-                for (int e = 0; e < E; ++e) {
-                    const int p = e / E_l, el = e % E_l;
-                    base[(size_t)ch * E + e] = gp.rank[p].grp_off[ch * E_l + el] +
-                                               gp.rank[p].src_off[(me * E_l + el) * n + ch] -
-                                               gp.rank[me].S[e * (n + 1) + ch];
-                }
-            CK(cudaMemcpyAsync(pr->d_push_base, base.data(), sizeof(int) * base.size(), cudaMemcpyHostToDevice, sc));
-            // every owner's receive buffer is free for this step
-            if (peer_wait_all(c, lancet::PK_XEFREE, 0, sc)) return fail(c, LANCET_ERR_CUDA, "cuStreamWaitValue32");
-            for (int ch = 0; ch < n; ++ch) {
-                OpScope op(c, "a2a_dispatch_push", 1, serial ? -1 : ch, sc);
-                L += launch_permute_push(da, x, chunk_start(T, n, ch), chunk_start(T, n, ch + 1), E_l,
-                                         pr->d_push_base + (size_t)ch * E, pr->d_xe, c->bf16, sc);
-                if (peer_signal(c, 0, lancet::PK_PUSH, ch, sc)) return fail(c, LANCET_ERR_CUDA, "cuStreamWriteValue32");
-            }
-            CHECK_LAUNCH();
-        }
         const size_t rowb = (size_t)d * c->elt;
         char* xs = (char*)c->xs;
         char* xe = (char*)c->xe;
@@ -928,15 +1167,6 @@ LANCET_API lancet_status lancet_moe_forward(lancet_ctx* c, const void* x, const 
             int c0, c1;
             chunk_range(cc, c0, c1);
             OpScope op(c, "a2a_dispatch", 1, serial ? -1 : cc, sm);
-            if (push) {         // every rank's rows of these chunks have landed in xe
-                for (int ch = c0; ch < c1; ++ch)
-                    if (peer_wait_all(c, lancet::PK_PUSH, ch, sm)) return fail(c, LANCET_ERR_CUDA, "cuStreamWaitValue32");
-                if (ident && peer_signal(c, 0, lancet::PK_OUT, cc, sm))
-                    return fail(c, LANCET_ERR_CUDA, "cuStreamWriteValue32");
-                ev_disp[cc] = next_ev();
-                CK(cudaEventRecord(ev_disp[cc], sm));
-                continue;
-            }
             if (pr) {
                 std::string err;
                 if (peer_pull(c, lancet::PK_XS, cc, gp.pulls(c->rank, true, c0, c1, xe, rowb), cc == nc - 1, sm, err))
@@ -984,7 +1214,7 @@ LANCET_API lancet_status lancet_moe_forward(lancet_ctx* c, const void* x, const 
         }
         // combine all-to-alls C0..C(n-1)
         const char* eout = ident ? xe : (const char*)c->out;
-        for (int cc = 0; cc < nc && !push; ++cc) {
+        for (int cc = 0; cc < nc; ++cc) {
             int c0, c1;
             chunk_range(cc, c0, c1);
             CK(cudaStreamWaitEvent(sm, ev_exp[cc], 0));
@@ -1015,22 +1245,8 @@ LANCET_API lancet_status lancet_moe_forward(lancet_ctx* c, const void* x, const 
             ev_comb[cc] = next_ev();
             CK(cudaEventRecord(ev_comb[cc], sm));
         }
-        // push: the combine exchange is fused into the gather -- K4 reads each expert output row
-        // where its owner's fc2 wrote it (peer memory), once every owner has finished chunk c
-        for (int cc = 0; cc < nc && push; ++cc) {
-            int c0, c1;
-            chunk_range(cc, c0, c1);
-            // the owners signal their outputs per chunk group cc (all chunks at once when serial)
-            if (peer_wait_all(c, lancet::PK_OUT, cc, sc)) return fail(c, LANCET_ERR_CUDA, "cuStreamWaitValue32");
-            for (int ch = c0; ch < c1; ++ch) {
-                OpScope op(c, "combine_fused", 0, ch, sc);
-                L += launch_combine(da, comb, y, chunk_start(T, n, ch), chunk_start(T, n, ch + 1), c->bf16, sc,
-                                    pr->d_push_base + (size_t)ch * E, pr->d_outsrc, E_l);
-            }
-            c->out_consume_pending = true;
-        }
         // gather per chunk (chunk c's tokens are final as soon as combine c lands)
-        for (int cc = 0; cc < nc && !push; ++cc) {
+        for (int cc = 0; cc < nc; ++cc) {
             CK(cudaStreamWaitEvent(sc, ev_comb[cc], 0));
             const int t0 = serial ? 0 : chunk_start(T, n, cc), t1 = serial ? T : chunk_start(T, n, cc + 1);
             OpScope op(c, "combine", 0, serial ? -1 : cc, sc);
@@ -1144,6 +1360,7 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
     }
 
     // ---- expert parallel (S2) ---------------------------------------------------------------
+    if (c->push) return backward_push(c, da, dy, dx, dwg, dw1, dw2, renorm, s, L);
     const int G = c->world, E_l = c->E_l;
     const bool serial = c->cfg.flags & LANCET_FLAG_SERIAL;
     const bool late_dw = serial || (c->cfg.flags & LANCET_FLAG_NO_DW_OVERLAP);
@@ -1173,39 +1390,15 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
     L += launch_zero_pads(c->dout, d, d_grp_off, d_grp_rows, n * E_l, (int)c->elt, sc);
     const void* comb = c->comb;     // o_tj returned by the combine all-to-all (source side)
     std::vector<cudaEvent_t> ev_k5(nc), ev_b1(nc), ev_dx(nc), ev_b2(nc);
-    const bool push = pr && (c->cfg.flags & LANCET_FLAG_PEER_PUSH);
-    if (push) {
-        // K5 pushes its dO rows into the owners' dout (backward all-to-all #1 fused, same row
-        // bases as the forward's push): this rank's dout is free (its readers of the previous
-        // step are behind it on this stream), and so must every owner's be
-        if (peer_signal(c, 0, lancet::PK_DOUTFREE, 0, sc) || peer_wait_all(c, lancet::PK_DOUTFREE, 0, sc))
-            return fail(c, LANCET_ERR_CUDA, "cuStream{Write,Wait}Value32");
-    }
     for (int cc = 0; cc < nc; ++cc) {
         int t0, t1;
         tok_range(cc, t0, t1);
-        OpScope op(c, push ? "combine_bwd_push" : "combine_bwd", 0, serial ? -1 : cc, sc);
-        if (push) {
-            int c0, c1;
-            chunk_range(cc, c0, c1);
-            for (int ch = c0; ch < c1; ++ch) {
-                L += launch_combine_bwd(da, dy, comb, c->g, c->dcomb, chunk_start(T, n, ch), chunk_start(T, n, ch + 1),
-                                        false, c->logits, renorm, c->dlogit, c->prow, c->bf16, sc,
-                                        pr->d_push_base + (size_t)ch * E, pr->d_dout, E_l, pr->d_outsrc);
-                if (peer_signal(c, 0, lancet::PK_PUSH2, ch, sc)) return fail(c, LANCET_ERR_CUDA, "cuStreamWriteValue32");
-            }
-        } else {
-            L += launch_combine_bwd(da, dy, comb, c->g, c->dcomb, t0, t1, cc == 0, c->logits, renorm, c->dlogit,
-                                    c->prow, c->bf16, sc);
-            if (pr && peer_signal(c, 0, lancet::PK_DCOMB, cc, sc)) return fail(c, LANCET_ERR_CUDA, "cuStreamWriteValue32");
-        }
+        OpScope op(c, "combine_bwd", 0, serial ? -1 : cc, sc);
+        L += launch_combine_bwd(da, dy, comb, c->g, c->dcomb, t0, t1, cc == 0, c->logits, renorm, c->dlogit,
+                                c->prow, c->bf16, sc);
+        if (pr && peer_signal(c, 0, lancet::PK_DCOMB, cc, sc)) return fail(c, LANCET_ERR_CUDA, "cuStreamWriteValue32");
         ev_k5[cc] = next_ev();
         CK(cudaEventRecord(ev_k5[cc], sc));
-    }
-    // push: K4 and K5 read the owners' expert outputs in place; they are consumed now
-    if (push) {
-        if (peer_signal(c, 1, lancet::PK_OUT, 0, sc)) return fail(c, LANCET_ERR_CUDA, "cuStreamWriteValue32");
-        c->out_consume_pending = false;
     }
     CHECK_LAUNCH();
     char* dcomb = (char*)c->dcomb;
@@ -1216,15 +1409,6 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
         chunk_range(cc, c0, c1);
         CK(cudaStreamWaitEvent(sm, ev_k5[cc], 0));
         OpScope op(c, "a2a_bwd_dispatch", 1, serial ? -1 : cc, sm);
-        if (push) {         // every rank's dO rows of these chunks have landed in dout
-            for (int ch = c0; ch < c1; ++ch)
-                if (peer_wait_all(c, lancet::PK_PUSH2, ch, sm)) return fail(c, LANCET_ERR_CUDA, "cuStreamWaitValue32");
-            if (ident && peer_signal(c, 0, lancet::PK_DXE, cc, sm))   // identity: dout is the source back
-                return fail(c, LANCET_ERR_CUDA, "cuStreamWriteValue32");
-            ev_b1[cc] = next_ev();
-            CK(cudaEventRecord(ev_b1[cc], sm));
-            continue;
-        }
         if (pr) {
             std::string err;
             if (peer_pull(c, lancet::PK_DCOMB, cc, gp.pulls(c->rank, true, c0, c1, dout, rowb), cc == nc - 1, sm, err))
@@ -1401,8 +1585,18 @@ LANCET_API lancet_status lancet_get_counts(lancet_ctx* c, int32_t* send_counts,
         for (int ch = 0; ch < n; ++ch) send[e * n + ch] = S[e * (n + 1) + ch + 1] - S[e * (n + 1) + ch];
     if (send_counts) memcpy(send_counts, send.data(), sizeof(int) * E * n);
     if (recv_counts) {
-        if (G == 1) memcpy(recv_counts, send.data(), sizeof(int) * E * n);
-        else memcpy(recv_counts, c->host_recv.data(), sizeof(int) * G * E_l * n);
+        if (c->push) {          // the plan lives on the device: recv from the gathered matrix
+            std::vector<int> M((size_t)G * E * n);
+            CK(cudaMemcpy(M.data(), c->peer->my_counts, sizeof(int) * M.size(), cudaMemcpyDeviceToHost));
+            for (int src = 0; src < G; ++src)
+                for (int el = 0; el < E_l; ++el)
+                    for (int ch = 0; ch < n; ++ch)
+                        recv_counts[(src * E_l + el) * n + ch] = M[((size_t)src * E + c->rank * E_l + el) * n + ch];
+        } else if (G == 1 && !c->ep) {
+            memcpy(recv_counts, send.data(), sizeof(int) * E * n);
+        } else {
+            memcpy(recv_counts, c->host_recv.data(), sizeof(int) * G * E_l * n);
+        }
     }
     if (capacity) *capacity = c->C;
     return LANCET_OK;

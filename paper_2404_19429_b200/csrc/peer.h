@@ -30,5 +30,29 @@ int peer_wait_all(lancet_ctx* c, int kind, int chunk, cudaStream_t s);
 int peer_pull(lancet_ctx* c, int kind, int chunk, const std::vector<PeerCopy>& copies, bool last,
               cudaStream_t s, std::string& err);
 int peer_counts(lancet_ctx* c, const int* d_send, int n, cudaStream_t s, std::string& err);
+// this rank's flags all set to a value every wait accepts, and the error word set: every
+// stream-memop and kernel wait on this rank returns (lancet_peer_abort)
+int peer_poison(lancet_ctx* c, uint32_t code);
+int peer_quiesce(lancet_ctx* c);   // 0: peers done with this rank's buffers; 1: timed out
+
+// ---- device-side protocol (push mode, LANCET_FLAG_PEER_PUSH) ------------------------------
+// Flags carry the step number read from the device counter (d_seq), waits are single-warp
+// kernels that spin with ld.acquire.sys and give up after timeout_ns (recording the failed
+// flag in the error word, which poisons the context at its next call).  No value is baked
+// into the host's enqueue, so a step can be captured in a CUDA graph and replayed.
+enum WaitTarget { TGT_STEP = 0, TGT_PREV = 1, TGT_LAST_BWD = 2 };
+int dev_seq_bump(lancet_ctx* c, cudaStream_t s);
+// this rank's flag (consumed?, kind, chunk) := step in every peer's array; mark_bwd also
+// records the step as "last backward" (d_seq[1])
+int dev_signal(lancet_ctx* c, int consumed, int kind, int chunk, cudaStream_t s, bool mark_bwd = false);
+// wait until every rank's flag (consumed?, kind, chunk) in this rank's array reaches the target
+int dev_wait(lancet_ctx* c, int consumed, int kind, int chunk, int target, cudaStream_t s);
+// count matrix all-gather ([G][E][n], this rank's row written into every peer's) + wait
+int dev_counts(lancet_ctx* c, const int* d_send, int n, cudaStream_t s);
+// expert-side group table (c->grp_dev, [n][E_l] rows | offsets) and the push row bases
+// [n][E] of this rank, from the gathered matrix
+int dev_plan(lancet_ctx* c, int n, cudaStream_t s);
+uint32_t peer_error(const lancet_ctx* c);      // 0 or the error word
+std::string peer_error_text(uint32_t code);
 
 }  // namespace lancet

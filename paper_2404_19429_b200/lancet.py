@@ -33,6 +33,7 @@ FLAG_GATE_BPR = 2048
 FLAG_DEFER_DW = 4096
 FLAG_GATE_RANDOM = 8192
 FLAG_PEER_PUSH = 16384
+FLAG_NO_COMM = 32768          # timing only: the data exchanges are skipped (results are wrong)
 # LANCET_EXTRA_FLAGS: OR'ed into every context's flags (e.g. run the test suite under PDL)
 EXTRA_FLAGS = int(os.environ.get("LANCET_EXTRA_FLAGS", "0"), 0)
 
@@ -43,7 +44,7 @@ EXPORTS = ["lancet_abi_version", "lancet_last_error", "lancet_nccl_unique_id", "
            "lancet_workspace_bytes", "lancet_launch_counts", "lancet_plan_exchange",
            "lancet_create_peer", "lancet_peer_blob_bytes", "lancet_peer_export", "lancet_peer_import",
            "lancet_moe_backward_dw", "lancet_set_dw_fillers", "lancet_dw_schedule", "lancet_stack_dw_plan",
-           "lancet_set_gate_seed"]
+           "lancet_set_gate_seed", "lancet_set_peer_timeout_ms", "lancet_peer_abort", "lancet_peer_status"]
 
 
 class LancetError(RuntimeError):
@@ -94,7 +95,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "lancet_peer_import": ([P, P], I32),
             "lancet_destroy": ([P], I32),
             "lancet_set_flags": ([P, U32], I32),
-            "lancet_moe_forward": ([P, P, P, P, P, I32, I32, F32, I32, P, P, P, P, P], I32),
+            "lancet_moe_forward": ([P, P, P, P, P, I32, I32, ctypes.c_double, I32, P, P, P, P, P], I32),
             "lancet_moe_backward": ([P, P, P, P, P, P, P], I32),
             "lancet_get_counts": ([P, P, P, P], I32),
             "lancet_timeline_begin": ([P, P], I32),
@@ -108,6 +109,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "lancet_set_dw_fillers": ([P, I32, P, P, P], I32),
             "lancet_dw_schedule": ([I32, P, P, I32, P, P], I32),
             "lancet_stack_dw_plan": ([I32, I32, P, P, P, P], I32),
+            "lancet_set_peer_timeout_ms": ([P, ctypes.c_int64], I32),
+            "lancet_peer_abort": ([P], I32),
+            "lancet_peer_status": ([P], I32),
         }
         for name, (args, res) in sig.items():
             f = getattr(lib, name)
@@ -335,6 +339,18 @@ class Context:
                                                 _ptr(dw2), _stream(stream))
         _check(st, self._p)
         return dx, dwg, dw1, dw2
+
+    # -- peer transport failure handling (include/lancet_moe.h) ---------------------------------
+    def set_peer_timeout_ms(self, ms: int):
+        _check(load_library().lancet_set_peer_timeout_ms(self._p, int(ms)), self._p)
+
+    def peer_abort(self):
+        _check(load_library().lancet_peer_abort(self._p), self._p)
+
+    def status(self):
+        """Raise LancetError if an asynchronous failure (a timed-out peer wait) poisoned the
+        context; never blocks."""
+        _check(load_library().lancet_peer_status(self._p), self._p)
 
     def set_gate_seed(self, seed: int):
         """Seed of the Random gate (FLAG_GATE_RANDOM) for the following forwards."""

@@ -41,7 +41,7 @@ def test_every_declared_symbol_is_exported(lib):
 
 
 def test_abi_version(lib):
-    assert lib.lancet_abi_version() == 1
+    assert lib.lancet_abi_version() == 2
 
 
 def test_create_rejects_bad_config_without_a_device(lib):

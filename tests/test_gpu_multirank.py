@@ -158,3 +158,38 @@ def test_chunking_invariance_across_ranks_and_repeats():
                 assert np.array_equal(g[r][key], ref[r][key]), (n, r, key)
             for key in ("dw1", "dw2", "dwg"):
                 assert normwise(g[r][key], ref[r][key]) <= 1e-5, (n, r, key)
+
+
+def test_eight_simulated_ranks_at_configs1_full_size():
+    # the layout the 8-GPU run executes: G = 8, E = 8 (E_l = 1), T = 16384 per rank, d = 1024,
+    # f = 4096, top-2, cf = 1.25, n = 4 -- 8 simulated ranks on one device.  Routing, send and
+    # receive counts bit-exact on every rank; y / dx on 64 sampled tokens per rank; the full
+    # dW1 / dW2 of expert 0 (all its rows from all 8 ranks) and rank 0's full dWg
+    G, T, d, f, E, k, cf, n = 8, 16384, 1024, 4096, 8, 2, 1.25, 4
+    ins = make_inputs(G, [T] * G, d, f, E, k, seed=2025, beta=0.25)
+    g = run_group(G, ins, E, k, cf, n)
+    from oracle import moe
+    rng = np.random.default_rng(1)
+    sample = [np.sort(rng.choice(T, 64, replace=False)) for _ in range(G)]
+    sample[0] = np.arange(T)                      # rank 0 in full: its dWg needs every g
+    xs, wg = [i["x"] for i in ins], ins[0]["wg"]
+    w1, w2, dys = [i["w1"] for i in ins], [i["w2"] for i in ins], [i["dy"] for i in ins]
+    fs = moe.forward(xs, wg, w1, w2, k, cf, n, token_subset=sample)
+    bs = moe.backward(fs, xs, wg, w1, w2, dys)
+    sends = [rt.counts for rt in fs.routing]
+    for r in range(G):
+        rt = fs.routing[r]
+        assert np.array_equal(g[r]["idx"], rt.idx) and np.array_equal(g[r]["slot"], rt.slot), r
+        assert g[r]["C"] == rt.C == 5120
+        assert np.array_equal(g[r]["send"], rt.counts), r
+        assert np.array_equal(g[r]["recv"], moe.recv_counts(sends, G, r)), r
+        tok = sample[r]
+        for key, ref in (("y", fs.y[r][tok]), ("dx", bs["dx"][r][tok])):
+            e = normwise(g[r][key][tok], ref)
+            assert e <= TOL["bf16"], (r, key, e)
+    assert normwise(g[0]["dwg"], bs["dwg"][0]) <= TOL["bf16"]
+    fe = moe.forward(xs, wg, w1, w2, k, cf, n, experts=[0])
+    be = moe.backward(fe, xs, wg, w1, w2, dys)
+    for key in ("dw1", "dw2"):
+        e = normwise(g[0][key], be[key][0])
+        assert e <= TOL["bf16"], (key, e)

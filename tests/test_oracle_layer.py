@@ -99,6 +99,27 @@ def test_token_subset_matches_full():
         assert np.allclose(part.y[r][sub[r]], full.y[r][sub[r]], rtol=1e-12, atol=1e-18)
 
 
+def test_expert_restriction_partitions_the_layer():
+    # experts=[...] (the cost restriction of the full-size GPU tests): the per-expert forwards
+    # sum to the full y, and each restricted backward gives exactly the full dW of its experts
+    xs, wg, w1, w2, dys = _inputs(2, 64, 8, 16, 4)
+    full = moe.forward(xs, wg, w1, w2, 2, 1.25, 2)
+    gfull = moe.backward(full, xs, wg, w1, w2, dys)
+    ysum = [np.zeros_like(y) for y in full.y]
+    for e in range(4):
+        part = moe.forward(xs, wg, w1, w2, 2, 1.25, 2, experts=[e])
+        gp = moe.backward(part, xs, wg, w1, w2, dys)
+        for r in range(2):
+            ysum[r] += part.y[r]
+        r, el = e // 2, e % 2
+        assert np.allclose(gp["dw1"][r][el], gfull["dw1"][r][el], rtol=1e-12, atol=1e-18)
+        assert np.allclose(gp["dw2"][r][el], gfull["dw2"][r][el], rtol=1e-12, atol=1e-18)
+        other = 1 - el
+        assert not np.any(gp["dw1"][r][other]) and not np.any(gp["dw2"][r][other])
+    for r in range(2):
+        assert np.allclose(ysum[r], full.y[r], rtol=1e-12, atol=1e-15)
+
+
 # ---------------------------------------------------------------- backward by FD -------
 
 def _loss(xs, wg, w1, w2, dys, k, cf, act, renorm, ref_routing=None):
