@@ -67,6 +67,11 @@ def parse():
                          "test of the exchange machinery on one GPU, not a scaling measurement")
     ap.add_argument("--no-timeline", action="store_true",
                     help="no per-op events in the timed region (A/B of their overhead)")
+    ap.add_argument("--no-ep", action="store_true",
+                    help="N = 1: skip the 'ep' sub-record (the expert-parallel chunk pipeline over a "
+                         "one-rank peer group, with its exposure and no-comm differential)")
+    ap.add_argument("--no-arms", action="store_true",
+                    help="N > 1: skip the per-transport arms (push / pull / NCCL on one definition)")
     a = ap.parse_args()
     a.warmup = max(a.warmup, 3)
     if a.same_device:
@@ -99,6 +104,15 @@ def peaks():
         return dict(hbm=j["hbm_gbs"], bf16=j["bf16_tflops"], bf16_sus=j.get("bf16_tflops_sustained", j["bf16_tflops"]),
                     src="measured (MEASURED_PEAKS.json)")
     return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="fallback (B200_PROFILING.md)")
+
+
+def gemm_peak(pk, clk):
+    """The bf16 peak matching the run's clock regime: MEASURED_PEAKS' burst figure when the
+    median SM clock under load stayed within 5 % of the maximum (short runs at boost), its
+    sustained figure (measured at a power-capped ~1.36 GHz median) otherwise."""
+    mhz, mx = clk.get("sm_mhz"), clk.get("sm_max_mhz")
+    burst = bool(mhz and mx and mhz >= 0.95 * mx)
+    return (pk["bf16"] if burst else pk["bf16_sus"]), ("burst" if burst else "sustained")
 
 
 # ------------------------------------------------------------------------ clocks -----------
@@ -356,22 +370,85 @@ def run_e2e(a, world, ins, ctx, wg, w1, w2, dwg, dw1, dw2, dev, barrier, max_ove
                     "timed region (first H2D to last D2H)"}
 
 
+def measure_arm(a, ctx, lancet, flags, step, stream, barrier, max_over_ranks, n_chunks):
+    """One exchange arm measured on one definition, all ranks' max:
+      ms_per_step          clean pass (no per-op events), the throughput number;
+      exposed_a2a_ms       instants where an exchange op (lane 1) runs and no compute op does,
+                           from per-op events of a second pass;
+      unoverlapped_a2a_ms  the lane-1 time of the serial schedule (one stream, chunks merged,
+                           dW after the exchanges: LANCET_FLAG_SERIAL);
+      no_comm_ms_per_step  the same schedule with the data exchanges skipped (LANCET_FLAG_NO_COMM,
+                           timing only), so ms_per_step - no_comm bounds the exposed exchange
+                           time from above (it also removes the exchanges' SM / HBM contention).
+    In the push mode the lane-1 ops are the fused token kernels (permute / gather work
+    included); NO_COMM keeps that local work (same kernels on local buffers) so the
+    differential is comparable across push, pull and NCCL."""
+    import torch
+
+    def run(fl, n, instrumented=False):
+        ctx.set_flags(fl | (lancet.FLAG_TIMELINE if instrumented else 0))
+        for _ in range(2):
+            step(n_chunks)
+        torch.cuda.synchronize()
+        if instrumented:
+            ctx.timeline_begin(stream)
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(n):
+            step(n_chunks)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ms = max_over_ranks(e0.elapsed_time(e1) / n)
+        return ms, (ctx.timeline(cap=200000) if instrumented else None)
+
+    ctx.set_flags(flags)
+    for _ in range(a.warmup):
+        step(n_chunks)
+    steps = max(3, a.steps)
+    ms, _ = run(flags, steps)
+    ms_instr, tl = run(flags, steps, True)
+    exposed, comm, exp_c, exp_d = exposure_per_step(tl, steps)
+    ns = max(3, min(10, steps))
+    ms_serial, tls = run(flags | lancet.FLAG_SERIAL, ns, True)
+    unover = sum(r["end_us"] - r["start_us"] for r in tls if r["lane"] == 1) / ns / 1000.0
+    ms_nocomm, _ = run(flags | lancet.FLAG_NO_COMM, steps)
+    ms_serial_clean, _ = run(flags | lancet.FLAG_SERIAL, steps)
+    ctx.set_flags(flags)
+    world = ctx.world
+    return {"n_chunks": n_chunks, "ms_per_step": ms, "tokens_per_s": world * a.tokens / (ms / 1000.0),
+            "instrumented_ms_per_step": ms_instr,
+            "exposed_a2a_ms": max_over_ranks(exposed), "a2a_ms_on_comm_lane": max_over_ranks(comm),
+            "exposed_a2a_split_ms": {"counts": exp_c, "data": exp_d},
+            "unoverlapped_a2a_ms": max_over_ranks(unover),
+            "exposed_over_unoverlapped": (max_over_ranks(exposed) / max_over_ranks(unover)) if unover > 0 else None,
+            "serial_ms_per_step": ms_serial_clean,
+            "no_comm_ms_per_step": ms_nocomm, "exposed_upper_bound_ms": ms - ms_nocomm}
+
+
 def make_context(a, lancet, cfg, world, rank, local_rank, dev):
     """transport auto (world > 1): the copy-engine peer transport when every rank can set it up
     (CUDA IPC between all ranks' devices, stream memory operations), else NCCL -- decided
     collectively so all ranks use the same one."""
     import torch
     import torch.distributed as dist
+    import dataclasses
     pg = dist.group.WORLD if world > 1 else None
+    # the push mode of the peer transport is fixed at creation (every exchange fused into the
+    # token kernels, no host synchronisation; DESIGN.md §8)
+    pcfg = dataclasses.replace(cfg, flags=cfg.flags | (0 if a.no_push else lancet.FLAG_PEER_PUSH))
     if a.transport != "auto":
         a.transport_used = a.transport
-        return lancet.Context(cfg, world=world, rank=rank, device=local_rank, pg=pg, transport=a.transport)
+        return lancet.Context(pcfg if a.transport == "peer" else cfg, world=world, rank=rank, device=local_rank,
+                              pg=pg, transport=a.transport)
     if world == 1:
         a.transport_used = "none"
         return lancet.Context(cfg, world=1, rank=0, device=local_rank)
     ctx, ok = None, 1.0
     try:
-        ctx = lancet.Context(cfg, world=world, rank=rank, device=local_rank, pg=pg, transport="peer")
+        ctx = lancet.Context(pcfg, world=world, rank=rank, device=local_rank, pg=pg, transport="peer")
     except Exception as e:  # noqa: BLE001
         print(f"rank {rank}: peer transport unavailable ({e}); voting for NCCL", file=sys.stderr)
         ok = 0.0
@@ -419,10 +496,7 @@ def run_lancet(a, world, rank, local_rank):
                              max_k=a.k, max_chunks=max(8, a.chunks), dtype="bf16", flags=flags)
     ctx = make_context(a, lancet, cfg, world, rank, local_rank, dev)
     if a.transport_used == "peer" and not a.no_push:
-        # dispatch all-to-all fused into the permute kernel (rows written straight into the
-        # owners' receive buffers; DESIGN.md §8 "push dispatch")
         flags |= lancet.FLAG_PEER_PUSH
-        ctx.set_flags(flags)
     stream = torch.cuda.current_stream()
     y = torch.empty_like(x)
     dx = torch.empty_like(x)
@@ -433,6 +507,12 @@ def run_lancet(a, world, rank, local_rank):
     def step(xx=x, dyy=dy):
         ctx.forward(xx, wg, w1, w2, a.k, a.cf, a.chunks, y=y, routing=False)
         ctx.backward(dyy, dx=dx, dwg=dwg, dw1=dw1, dw2=dw2)
+
+    def step_on(c):
+        def f(n):
+            c.forward(x, wg, w1, w2, a.k, a.cf, n, y=y, routing=False)
+            c.backward(dy, dx=dx, dwg=dwg, dw1=dw1, dw2=dw2)
+        return f
 
     def barrier():
         if world > 1:
@@ -516,15 +596,23 @@ def run_lancet(a, world, rank, local_rank):
 
     # ---- roofline of the dominant kernel (the tcgen05 grouped GEMM, 6 launches per step) ----
     pk = peaks()
+    peak, regime = gemm_peak(pk, clk)
     gsrc = gemm_ops or ops
     gemm_us = sum(gsrc[o]["us_per_step"] for o in GEMM_OPS if o in gsrc)
     gemm_flops = 12.0 * rows_expert * a.d * a.f       # algorithmic: admitted rows only
     achieved = gemm_flops / (gemm_us * 1e-6) / 1e12 if gemm_us > 0 else 0.0
-    traffic = None
+    # DRAM bytes of the six GEMM launches from the committed `ncu --set full` capture -- only
+    # when this run is the captured configuration (world 1, configs[1] shape, Switch gate)
+    traffic, traffic_src = None, "no ncu capture of this configuration"
     prof = os.path.join(ROOT, "profiles", "ncu_gemm_traffic.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_step")
+            pj = json.load(open(prof))
+            want = {"tokens": a.tokens, "d": a.d, "f": a.f, "experts": a.experts, "k": a.k, "world": world,
+                    "gate": a.gate, "cf": a.cf}
+            if all(pj.get("config", {}).get(key) == v for key, v in want.items()):
+                traffic = pj.get("dram_bytes_per_step")
+                traffic_src = f"{pj.get('source')} (dram__bytes_read.sum + dram__bytes_write.sum, six launches)"
         except Exception:  # noqa: BLE001
             traffic = None
     kernels = {}
@@ -601,14 +689,17 @@ def run_lancet(a, world, rank, local_rank):
         "exposed_a2a_ms": exposed_ms, "a2a_ms_on_comm_lane": comm_ms,
         "exposed_a2a_split_ms": {"counts": exp_counts_ms, "data": exp_data_ms},
         "unoverlapped_a2a_ms": unoverlapped_ms,
-        "roofline": {"bound": "tensor", "achieved": achieved, "peak": pk["bf16_sus"], "unit": "TFLOP/s",
-                     "frac": achieved / pk["bf16_sus"], "traffic": traffic,
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                     "peak_regime": regime, "peak_burst": pk["bf16"], "peak_sustained": pk["bf16_sus"],
+                     "frac_burst": achieved / pk["bf16"], "frac_sustained": achieved / pk["bf16_sus"],
                      "kernel": "tc_gemm_kernel (tcgen05 grouped GEMM), 6 launches/step; "
                                "achieved = 12*rows*d*f algorithmic FLOP / summed CUDA-event time "
                                "of the six launches, from events around the GEMM launches only "
                                "over a second pass of the same K steps (the clean timed pass "
                                "carries no per-op events)",
-                     "peak_source": pk["src"] + " bf16_tflops_sustained"},
+                     "peak_source": pk["src"] + (" bf16_tflops (median SM clock >= 0.95 x max)" if regime == "burst"
+                                                 else " bf16_tflops_sustained (median SM clock < 0.95 x max)")},
         "kernels": kernels,
         "launch_groups": {o: v["launch_groups_per_step"] for o, v in ops.items()},
         "gpu_launches": (f_l + b_l) * a.steps,
@@ -618,10 +709,47 @@ def run_lancet(a, world, rank, local_rank):
     }
     if e2e:
         out["e2e"] = e2e
-    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+    if world > 1:
+        out["exposure_definition"] = ("lane 1 = exchange ops; " + (
+            "push mode: the fused token kernels (permute / gather work included)" if a.transport_used == "peer"
+            and not a.no_push else "copies / NCCL kernels only"))
+    import dataclasses
+    if world == 1 and not a.no_ep:
+        # the expert-parallel chunk pipeline (S1 / S2) on this GPU: a one-rank group of the peer
+        # transport in push mode -- every exchange of the N > 1 path is executed (to self), so
+        # the line carries the metric's second half (exposed vs unoverlapped all-to-all)
+        pcfg = dataclasses.replace(cfg, flags=(flags & ~lancet.FLAG_FORCE_EP) | lancet.FLAG_PEER_PUSH)
+        ectx = lancet.Context(pcfg, world=1, rank=0, device=local_rank, transport="peer")
+        ep_flags = pcfg.flags
+        out["ep"] = {"transport": "peer push, one-rank group (all exchanges to self)",
+                     "by_n": [measure_arm(a, ectx, lancet, ep_flags, step_on(ectx), stream, barrier, max_over_ranks, n)
+                              for n in sorted({1, a.chunks})]}
+        ectx.close()
+    if world > 1 and not a.no_arms:
+        # every transport on the same definitions (push / pull over the peer transport, NCCL)
+        arms = {}
+        for name in ("push", "pull", "nccl"):
+            if name != "nccl" and a.transport_used != "peer":
+                continue
+            if name == ("push" if not a.no_push else "pull") and a.transport_used == "peer":
+                actx, own = ctx, False
+            else:
+                acfg = dataclasses.replace(cfg, flags=flags & ~lancet.FLAG_PEER_PUSH | (lancet.FLAG_PEER_PUSH if name == "push" else 0))
+                actx = lancet.Context(acfg, world=world, rank=rank, device=local_rank,
+                                      pg=dist.group.WORLD, transport="nccl" if name == "nccl" else "peer")
+                own = True
+            afl = flags & ~lancet.FLAG_PEER_PUSH | (lancet.FLAG_PEER_PUSH if name == "push" else 0)
+            arms[name] = measure_arm(a, actx, lancet, afl, step_on(actx), stream, barrier, max_over_ranks, a.chunks)
+            if own:
+                barrier()
+                actx.close()
+        out["arms"] = arms
+    if rank == 0 and not a.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(a)
+    barrier()
     if rank == 0:
         print(json.dumps(out), flush=True)
+    barrier()
     ctx.close()
 
 

@@ -145,6 +145,12 @@ enum {
                                            Fixed at creation (lancet_set_flags keeps the creation
                                            bit); checked identical on every rank at
                                            lancet_peer_import                                   */
+    LANCET_FLAG_CHUNK_LAUNCHES = 1u << 16,/* push mode: one expert-GEMM launch per chunk ordered
+                                           by flag kernels on the host's enqueue (the A/B of the
+                                           default: one launch over all chunks whose TMA producer
+                                           waits for each chunk's rows on the device and whose
+                                           epilogue publishes each chunk's outputs, with the dW
+                                           GEMMs merged over the chunks)                         */
     LANCET_FLAG_NO_COMM = 1u << 15      /* TIMING ONLY (results are wrong): skip the data
                                            exchanges (NCCL / copy-engine: the C2 copies; push
                                            mode: the four fused exchange kernels) but keep every

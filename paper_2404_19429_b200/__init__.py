@@ -9,6 +9,6 @@ from .lancet import (Context, LayerConfig, LocalGroup, LancetError, load_library
                      exposed_comm_us, FLAG_RENORMALIZE, FLAG_TIMELINE, FLAG_SERIAL,
                      FLAG_SIMT_GEMM, FLAG_NO_DW_OVERLAP, FLAG_NO_SIDE_STREAM, FLAG_GEMM_MULTICAST,
                      FLAG_UNFUSED_GATE_BWD, FLAG_NO_PDL, FLAG_FORCE_EP, FLAG_GATE_BPR, FLAG_DEFER_DW, FLAG_GATE_RANDOM, FLAG_PEER_PUSH,
-                     FLAG_NO_COMM,
+                     FLAG_NO_COMM, FLAG_CHUNK_LAUNCHES,
                      dw_schedule, stack_dw_plan,
                      EXPORTS, LIB_PATH)

@@ -87,6 +87,8 @@ struct lancet_ctx {
 
     // streams / events
     cudaStream_t s_comp = nullptr, s_comm = nullptr;
+    cudaStream_t s_comp2 = nullptr;      // push pipeline: odd chunks' fc2 / dfc1 launches, so one
+                                         // chunk's tail wave overlaps the next chunk's GEMM
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_counts = nullptr, ev_tl_base = nullptr;
     std::vector<cudaEvent_t> ev_pool;                 // generic sync events
     std::vector<lancet::OpEvent> ops;                 // timeline of the last fwd+bwd

@@ -73,7 +73,10 @@ k6_gather_kernel(const Elt* __restrict__ dxe, const int* __restrict__ prow,
             for (int j = 0; j < KK; ++j) rows[q][j] = __shfl_sync(0xffffffffu, myrow, j);
             dl_lane[q] = (ok && lane < E) ? __ldg(dlogit + (size_t)t * E + lane) : 0.f;
         }
-        for (int v0 = lane; v0 < nvec; v0 += 32 * U) {
+        // every lane runs every pass (the dlogit broadcast below is a full-warp shuffle, so no
+        // lane may leave early even when d / V < 32); loads and stores are guarded per vector
+        for (int vb = 0; vb < nvec; vb += 32 * U) {
+            const int v0 = vb + lane;
             uint4 raw[kK6T][U][KK];
 #pragma unroll
             for (int q = 0; q < kK6T; ++q)

@@ -62,6 +62,7 @@ struct Params {
     const int* grp_off;
     void* C;
     long ldc, c_group_stride;
+    ChunkSync cs;
 };
 
 // ---------------------------------------------------------------- PTX wrappers ----------
@@ -135,6 +136,16 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
                  "r"(smem_u32(src)), "r"(c0), "r"(c1)
                  : "memory");
 }
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(map),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_reduce_add_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
+    asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(map),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
 // elementwise fp32 add of the shared box into global memory (dW accumulation across chunks)
 __device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
     asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
@@ -145,6 +156,38 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// ---- device-side chunk pipeline (ChunkSync, push mode) ----------------------------------
+__device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// producer: every rank's rows of chunk ch have landed (then the TMA loads may read them)
+__device__ __forceinline__ void chunk_wait(const ChunkSync& cs, int ch) {
+    const uint32_t want = cs.seq[0];
+    const uint32_t* f = cs.wait_flags + (long)ch * cs.wait_chunk_stride;
+    const unsigned long long t0 = gtimer();
+    for (int r = 0; r < cs.ranks; ++r) {
+        unsigned ns = 32;
+        while (ld_acquire_sys_u32(f + r) < want) {
+            if (*reinterpret_cast<volatile uint32_t*>(cs.err) != 0) return;
+            if (gtimer() - t0 > cs.timeout_ns) {
+                atomicCAS(cs.err, 0u, cs.err_code | ((uint32_t)(ch & 0xFFFF) << 8) | (uint32_t)r);
+                return;
+            }
+            __nanosleep(ns);
+            if (ns < 512) ns *= 2;
+        }
+    }
+    // the rows were written by other agents (generic proxy); the TMA loads are async proxy
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
 }
@@ -286,7 +329,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // MC pairs of a cluster share one A tile (TMA multicast) and compute MC adjacent N tiles:
     // "super tiles" of MC * BN columns; pair pp takes n tile ntp * MC + pp
-    const int ntn = p.N / (BN * MC);
+    // ragged N / K / M: the tile counts round up; TMA zero-fills the loads past the tensor and
+    // clips the stores to it, so the extra rows / columns never reach memory
+    const int ntn = ceil_div(p.N, BN * MC);
     const uint32_t crank = CG * MC > 1 ? cta_rank() : 0;
     const uint32_t rank = CG == 2 ? (crank & 1) : 0;    // CTA within the pair
     const int pp = (int)(crank / CG);                   // pair within the cluster
@@ -302,7 +347,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             tstart[g] = acc;
             srows[g] = p.grp_rows[g];
             soff[g] = p.grp_off[g];
-            const int mt = p.mode == GEMM_M_GROUPED ? ceil_div(srows[g], MT) : p.M / MT;
+            const int mt = p.mode == GEMM_M_GROUPED ? ceil_div(srows[g], MT) : ceil_div(p.M, MT);
             acc += mt * ntn;
         }
         tstart[p.n_groups] = acc;
@@ -345,13 +390,18 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
+            int ready_c = -1;
             for (int tile = cluster; tile < total; tile += n_clusters) {
                 int g, mt, nt;
                 decode_tile(tile, tstart, p.n_groups, ntn, g, mt, nt);
+                if (p.cs.wait_flags && g / p.cs.gpc > ready_c) {     // chunk pipeline: rows landed?
+                    ready_c = g / p.cs.gpc;
+                    chunk_wait(p.cs, ready_c);
+                }
                 const int nb = (nt * MC + pp) * BN + (int)rank * BNC;   // this CTA's B rows / columns
                 int num_kb, arow, brow;
                 if (p.mode == GEMM_M_GROUPED) {
-                    num_kb = p.K / BK;
+                    num_kb = ceil_div(p.K, BK);
                     arow = soff[g] + mt * MT + (int)rank * BM;
                     brow = ((g / p.gpw) % p.n_weights) * (B_MN ? p.K : p.N);
                 } else {
@@ -403,7 +453,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             for (int tile = cluster; tile < total; tile += n_clusters, ++it) {
                 int g, mt, nt;
                 decode_tile(tile, tstart, p.n_groups, ntn, g, mt, nt);
-                const int num_kb = p.mode == GEMM_M_GROUPED ? p.K / BK : round_up(srows[g], kRowAlign) / BK;
+                const int num_kb = p.mode == GEMM_M_GROUPED ? ceil_div(p.K, BK) : round_up(srows[g], kRowAlign) / BK;
                 const int acc = it & 1;
                 const uint32_t acc_phase = (it >> 1) & 1;
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -557,8 +607,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             } else {
                 mbar_wait(&tfull[acc], acc_phase);
                 tc_fence_after();
-                // fp32 dW tile rows of this warp in the [n_groups * M][N] view of C
-                const int crow = g * p.M + mt * MT + (int)rank * BM + q * 32;
+                // fp32 dW tile rows of this warp in the [n_groups][M][N] view of C (3D: a tile
+                // past a ragged M is clipped at the group's end, never spills into the next)
+                const int crow = mt * MT + (int)rank * BM + q * 32;
                 uint8_t* sF = sEpi + ew * kWarpStage;            // 32 x 32 fp32 box, SWIZZLE_128B
 #pragma unroll 1
                 for (int cc = cc0; cc < cc1; ++cc) {
@@ -580,8 +631,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                     if (lane == 0) {
                         // accumulate: TMA reduce-add (old + new, one rounding: same as a
                         // read-add-write), else a plain store
-                        if (p.accumulate) tma_reduce_add_2d(&tmC, sF, n0 + cc * 32, crow);
-                        else tma_store_2d(&tmC, sF, n0 + cc * 32, crow);
+                        if (p.accumulate) tma_reduce_add_3d(&tmC, sF, n0 + cc * 32, crow, g);
+                        else tma_store_3d(&tmC, sF, n0 + cc * 32, crow, g);
                         bulk_commit();
                     }
                 }
@@ -643,6 +694,21 @@ static bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t o
     return r == CUDA_SUCCESS;
 }
 
+// 3D fp32 map [outer2][outer][inner] with row stride `ld` and plane stride `plane` (elements)
+static bool make_map3_f32(CUtensorMap* m, void* ptr, uint64_t inner, uint64_t outer, uint64_t outer2, uint64_t ld,
+                          uint64_t plane, uint32_t box_inner, uint32_t box_outer)
+{
+    EncodeFn enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[3] = {inner, outer, outer2};
+    cuuint64_t strides[2] = {ld * 4, plane * 4};
+    cuuint32_t box[3] = {box_inner, box_outer, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, ptr, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int BN, bool A_MN, bool B_MN, int CG, int MC>
 static int launch_cfg(const GemmArgs& a, int num_sms, cudaStream_t s)
 {
@@ -662,12 +728,12 @@ static int launch_cfg(const GemmArgs& a, int num_sms, cudaStream_t s)
         ok = ok && make_map(&tcm, a.C, a.N, a.c_rows, a.ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
         if (a.epi == EPI_ACT) ok = ok && make_map(&tc2, a.C2, a.N, a.c_rows, a.ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
         if (a.epi == EPI_DACT) ok = ok && make_map(&tx, a.aux, a.N, a.c_rows, a.ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
-    } else {   // fp32 C [n_groups][M][N] viewed as [n_groups * M][N]
-        ok = ok && make_map(&tcm, a.C, a.N, (uint64_t)a.n_groups * a.M, a.ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B, true);
+    } else {   // fp32 C [n_groups][M][N] (3D, group stride c_group_stride)
+        ok = ok && make_map3_f32(&tcm, a.C, a.N, a.M, a.n_groups, a.ldc, a.c_group_stride, 32, 32);
     }
     if (!ok) return -1;
     Params p{a.mode, a.n_groups, a.gpw, a.n_weights > 0 ? a.n_weights : (1 << 30), a.epi, a.act, a.accumulate,
-             a.M, a.N, a.K, a.grp_rows, a.grp_off, a.C, a.ldc, a.c_group_stride};
+             a.M, a.N, a.K, a.grp_rows, a.grp_off, a.C, a.ldc, a.c_group_stride, a.cs};
     constexpr size_t smem = CF::kSmem;
     static bool attr = false;
     if (!attr) {
@@ -678,8 +744,8 @@ static int launch_cfg(const GemmArgs& a, int num_sms, cudaStream_t s)
     // persistent grid: at most one CTA per SM (pairs on one TPC when CG == 2), never more
     // (pair) tiles than the upper bound of tiles
     long max_tiles;
-    if (a.mode == GEMM_M_GROUPED) max_tiles = (long)ceil_div(a.max_rows, BM * CG) * a.n_groups * (a.N / (BN * MC));
-    else max_tiles = (long)(a.M / (BM * CG)) * (a.N / (BN * MC)) * a.n_groups;
+    if (a.mode == GEMM_M_GROUPED) max_tiles = (long)ceil_div(a.max_rows, BM * CG) * a.n_groups * ceil_div(a.N, BN * MC);
+    else max_tiles = (long)ceil_div(a.M, BM * CG) * ceil_div(a.N, BN * MC) * a.n_groups;
     // clusters of 4 cannot tile every GPC: cap the persistent grid at what is co-resident
     static int max_active = -1;
     if (max_active < 0) {
@@ -727,26 +793,27 @@ static int launch_cg(const GemmArgs& a, int num_sms, cudaStream_t s)
     const bool pair = a.mode == GEMM_M_GROUPED || a.M % (2 * BM) == 0;
     if (!pair) return launch_cfg<BN, A_MN, B_MN, 1, 1>(a, num_sms, s);
     // two pairs share each A tile (multicast) when the N tiles pair up
-    if (a.multicast && (a.N / BN) % 2 == 0) return launch_cfg<BN, A_MN, B_MN, 2, 2>(a, num_sms, s);
+    if (a.multicast && a.N % (2 * BN) == 0) return launch_cfg<BN, A_MN, B_MN, 2, 2>(a, num_sms, s);
     return launch_cfg<BN, A_MN, B_MN, 2, 1>(a, num_sms, s);
 }
 
 }  // namespace tc
 
+// Any N, K (M-grouped) and M (K-grouped) -- ragged tiles are zero-filled / clipped by TMA; the
+// TMA constraints remain: 16-byte aligned base pointers and row strides (d, f multiples of 8,
+// checked at creation), at most kMaxGroups groups per launch (run_gemm splits larger tables).
 bool gemm_tc_supported(const GemmArgs& a)
 {
     if (a.n_groups > tc::kMaxGroups || a.n_groups <= 0) return false;
-    if (a.N % 128) return false;
+    if (a.N <= 0 || a.K <= 0 && a.mode == GEMM_M_GROUPED) return false;
     if (a.mode == GEMM_M_GROUPED) {
         if (a.a_mn) return false;
-        if (a.K % tc::BK) return false;
         if (a.epi == EPI_F32) return false;
-        if (a.c_rows <= 0 || a.ldc % 8) return false;
+        if (a.c_rows <= 0 || a.ldc % 8 || a.lda % 8 || a.ldb % 8) return false;
     } else {
         if (!a.a_mn || !a.b_mn) return false;
-        if (a.M % tc::BM) return false;
-        if (a.epi != EPI_F32) return false;
-        if (a.c_group_stride != (long)a.M * a.ldc || a.ldc % 4) return false;   // TMA store view
+        if (a.epi != EPI_F32 || a.M <= 0) return false;
+        if (a.ldc % 4 || a.c_group_stride % 4 || a.lda % 8 || a.ldb % 8) return false;
     }
     return a.a_rows > 0 && a.b_rows > 0;
 }
@@ -754,7 +821,7 @@ bool gemm_tc_supported(const GemmArgs& a)
 int launch_gemm_tc(const GemmArgs& a, int num_sms, cudaStream_t s)
 {
     if (!gemm_tc_supported(a)) return -1;
-    const bool bn256 = a.N % 256 == 0;
+    const bool bn256 = a.N % 256 == 0;           // else 128-column tiles (ragged N included)
     if (!a.a_mn && !a.b_mn) return bn256 ? tc::launch_cg<256, false, false>(a, num_sms, s)
                                          : tc::launch_cg<128, false, false>(a, num_sms, s);
     if (!a.a_mn && a.b_mn) return bn256 ? tc::launch_cg<256, false, true>(a, num_sms, s)

@@ -108,6 +108,22 @@ int launch_zero_pads(void* buf, int row_elems, const int* grp_off, const int* gr
 enum GemmMode { GEMM_M_GROUPED = 0, GEMM_K_GROUPED = 1 };
 enum GemmEpi { EPI_STORE = 0, EPI_ACT = 1, EPI_DACT = 2, EPI_F32 = 3 };
 
+// Device-side chunk pipeline of one GEMM launch over all chunks (push mode).  Groups are in
+// chunk-major table order (gpc groups per chunk).  wait_flags != NULL: before the first load of
+// chunk c's tiles the TMA producer spins until every rank's flag wait_flags[c*stride + r]
+// reaches seq[0] (then every row of chunk c has landed; the rows were written by a completed
+// kernel and published by a flag kernel after it).  A wait that exceeds timeout_ns records
+// err_code | chunk << 8 | rank in *err and gives up (the context is poisoned at its next call).
+struct ChunkSync {
+    int gpc = 0, ranks = 0;
+    const uint32_t* wait_flags = nullptr;
+    long wait_chunk_stride = 0;
+    const uint32_t* seq = nullptr;
+    unsigned long long timeout_ns = 0;
+    uint32_t* err = nullptr;
+    uint32_t err_code = 0;
+};
+
 struct GemmArgs {
     // A(m,k): A_MN ? A[(row0+k)*lda + m] : A[(row0+m)*lda + k]
     const void* A; long lda;
@@ -129,6 +145,7 @@ struct GemmArgs {
     long a_rows, b_rows;  // outer extents of A and B viewed as 2D row-major tensors (TMA maps)
     long c_rows;          // outer extent of C / C2 / aux (M-grouped; TMA store maps)
     bool multicast;       // tcgen05: two CTA pairs share each A tile by TMA multicast
+    ChunkSync cs;         // tcgen05, M-grouped: device-side chunk pipeline (push mode)
 };
 int launch_gemm_simt(const GemmArgs& a, bool is_bf16, cudaStream_t s);
 

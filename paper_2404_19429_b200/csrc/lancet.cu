@@ -66,6 +66,8 @@ lancet_status fail(lancet_ctx* c, lancet_status st, const std::string& msg)
                                                 cudaGetErrorString(e_));                \
     } while (0)
 
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
 int capacity_of(int T, int k, int E, double cf)
 {
     // R4: C = max(1, min(T, ceil(cf*k*T/E))) in double
@@ -140,6 +142,8 @@ struct OpScope {
 };
 
 // ---- grouped GEMM dispatch ---------------------------------------------------------------
+constexpr int kTcMaxGroups = 128;   // gemm_tc.cu tc::kMaxGroups
+
 lancet_status run_gemm(lancet_ctx* c, GemmArgs& a, cudaStream_t s, int* launches)
 {
     if (c->bf16 && !(c->cfg.flags & LANCET_FLAG_SIMT_GEMM)) {
@@ -150,16 +154,42 @@ lancet_status run_gemm(lancet_ctx* c, GemmArgs& a, cudaStream_t s, int* launches
                              (c->push && !(c->cfg.flags & LANCET_FLAG_SERIAL));
         const int all = reserve ? c->num_sms - LANCET_COMM_SMS : c->num_sms;
         const int sms = c->cfg.gemm_sms > 0 ? std::min(c->cfg.gemm_sms, c->num_sms) : all;
-        const int r = launch_gemm_tc(a, sms, s);
-        if (r < 0) {
-            CHECK_LAUNCH();
-            return fail(c, LANCET_ERR_UNSUPPORTED,
-                        "tcgen05 GEMM: shape or layout not supported (N=" + std::to_string(a.N) + " K=" +
-                            std::to_string(a.K) + " M=" + std::to_string(a.M) + " groups=" +
-                            std::to_string(a.n_groups) + ") or tensor-map encoding failed");
+        // the kernel caches at most kTcMaxGroups group entries: larger tables go in batches,
+        // each inside one cycle of the weights (B and C pointers shifted to its first group)
+        const int ng = a.n_groups, nw = a.n_weights > 0 ? a.n_weights : ng;
+        if (ng > kTcMaxGroups && a.gpw != 1)
+            return fail(c, LANCET_ERR_UNSUPPORTED, "tcgen05 GEMM: > 128 groups with several groups per weight");
+        if (ng > kTcMaxGroups && a.cs.wait_flags)
+            return fail(c, LANCET_ERR_UNSUPPORTED, "tcgen05 GEMM: the chunk pipeline needs <= 128 groups per launch");
+        for (int g0 = 0; g0 < ng;) {
+            GemmArgs b = a;
+            int g1 = std::min(ng, g0 + kTcMaxGroups);
+            if (a.mode == GEMM_M_GROUPED) {
+                g1 = std::min(g1, (g0 / nw + 1) * nw);
+                const int w0 = g0 % nw;
+                b.B = (const char*)a.B + (size_t)w0 * a.b_group_stride * c->elt;
+                b.b_rows = a.b_rows - (long)w0 * (a.b_mn ? a.K : a.N);
+                b.n_weights = nw - w0;
+            } else {
+                b.C = (char*)a.C + (size_t)g0 * a.c_group_stride * 4;
+            }
+            b.n_groups = g1 - g0;
+            b.grp_rows = a.grp_rows + g0;
+            b.grp_off = a.grp_off + g0;
+            const int r = launch_gemm_tc(b, sms, s);
+            if (r < 0) {
+                CHECK_LAUNCH();
+                return fail(c, LANCET_ERR_UNSUPPORTED,
+                            "tcgen05 GEMM: shape or layout not supported (N=" + std::to_string(a.N) + " K=" +
+                                std::to_string(a.K) + " M=" + std::to_string(a.M) + " groups=" +
+                                std::to_string(a.n_groups) + ") or tensor-map encoding failed");
+            }
+            *launches += r;
+            g0 = g1;
         }
-        *launches += r;
     } else {
+        if (a.cs.wait_flags)
+            return fail(c, LANCET_ERR_UNSUPPORTED, "the device-side chunk pipeline runs on the tcgen05 GEMM only");
         *launches += launch_gemm_simt(a, c->bf16, s);
     }
     CHECK_LAUNCH();
@@ -167,30 +197,81 @@ lancet_status run_gemm(lancet_ctx* c, GemmArgs& a, cudaStream_t s, int* launches
 }
 
 // M-grouped expert GEMMs of the forward over groups [g0, g0+ng) of the expert-side table.
-lancet_status expert_forward(lancet_ctx* c, const int* grp_rows, const int* grp_off, int ng,
-                             int max_rows, cudaStream_t s, int chunk, int* launches)
+GemmArgs grouped_args(lancet_ctx* c, const int* grp_rows, const int* grp_off, int ng, int max_rows)
 {
-    const int d = c->cfg.d_model, f = c->cfg.d_ffn;
     GemmArgs a{};
     a.mode = GEMM_M_GROUPED; a.n_groups = ng; a.gpw = 1; a.n_weights = c->E_l;
     a.grp_rows = grp_rows; a.grp_off = grp_off; a.max_rows = max_rows; a.act = c->cfg.act;
     a.c_rows = c->rows_exp;
-    {   // fc1: H = act(X W1^T), G' = act'(X W1^T)
-        OpScope op(c, "expert_fc1", 0, chunk, s);
-        a.A = c->ep ? c->xe : c->xs; a.lda = d; a.a_rows = c->rows_exp;
-        a.B = c->w1; a.ldb = d; a.b_group_stride = (long)f * d; a.b_mn = false; a.a_mn = false;
-        a.b_rows = (long)c->E_l * f;
-        a.C = c->H; a.C2 = c->Gp; a.ldc = f; a.N = f; a.K = d; a.epi = EPI_ACT;
-        lancet_status st = run_gemm(c, a, s, launches);
-        if (st) return st;
-    }
-    {   // fc2: O = H W2^T
-        OpScope op(c, "expert_fc2", 0, chunk, s);
-        a.A = c->H; a.lda = f;
-        a.B = c->w2; a.ldb = f; a.b_group_stride = (long)d * f; a.b_rows = (long)c->E_l * d;
-        a.C = c->out; a.C2 = nullptr; a.ldc = d; a.N = d; a.K = f; a.epi = EPI_STORE;
-        return run_gemm(c, a, s, launches);
-    }
+    return a;
+}
+
+// fc1: H = act(X W1^T), G' = act'(X W1^T).  cs (push mode): the TMA producer waits for each
+// chunk's rows on the device (ChunkSync)
+lancet_status expert_fc1(lancet_ctx* c, const int* grp_rows, const int* grp_off, int ng, int max_rows,
+                         cudaStream_t s, int chunk, int* launches, const ChunkSync* cs = nullptr)
+{
+    const int d = c->cfg.d_model, f = c->cfg.d_ffn;
+    GemmArgs a = grouped_args(c, grp_rows, grp_off, ng, max_rows);
+    if (cs) a.cs = *cs;
+    OpScope op(c, "expert_fc1", 0, chunk, s);
+    a.A = c->ep ? c->xe : c->xs; a.lda = d; a.a_rows = c->rows_exp;
+    a.B = c->w1; a.ldb = d; a.b_group_stride = (long)f * d; a.b_mn = false; a.a_mn = false;
+    a.b_rows = (long)c->E_l * f;
+    a.C = c->H; a.C2 = c->Gp; a.ldc = f; a.N = f; a.K = d; a.epi = EPI_ACT;
+    return run_gemm(c, a, s, launches);
+}
+
+// fc2: O = H W2^T
+lancet_status expert_fc2(lancet_ctx* c, const int* grp_rows, const int* grp_off, int ng, int max_rows,
+                         cudaStream_t s, int chunk, int* launches)
+{
+    const int d = c->cfg.d_model, f = c->cfg.d_ffn;
+    GemmArgs a = grouped_args(c, grp_rows, grp_off, ng, max_rows);
+    OpScope op(c, "expert_fc2", 0, chunk, s);
+    a.A = c->H; a.lda = f; a.a_rows = c->rows_exp; a.a_mn = false;
+    a.B = c->w2; a.ldb = f; a.b_group_stride = (long)d * f; a.b_rows = (long)c->E_l * d; a.b_mn = false;
+    a.C = c->out; a.C2 = nullptr; a.ldc = d; a.N = d; a.K = f; a.epi = EPI_STORE;
+    return run_gemm(c, a, s, launches);
+}
+
+// M-grouped expert GEMMs of the forward over groups [g0, g0+ng) of the expert-side table.
+lancet_status expert_forward(lancet_ctx* c, const int* grp_rows, const int* grp_off, int ng,
+                             int max_rows, cudaStream_t s, int chunk, int* launches)
+{
+    lancet_status st = expert_fc1(c, grp_rows, grp_off, ng, max_rows, s, chunk, launches);
+    if (st) return st;
+    return expert_fc2(c, grp_rows, grp_off, ng, max_rows, s, chunk, launches);
+}
+
+// dX GEMMs (critical path) of the backward.
+// dA = (dO W2) * act'(A):  B(n=f, k=d) = W2[e][k][n]  (MN-major).  cs: device-side waits.
+lancet_status expert_dfc2(lancet_ctx* c, const void* dout, const int* grp_rows, const int* grp_off, int ng,
+                          int max_rows, cudaStream_t s, int chunk, int* launches, const ChunkSync* cs = nullptr)
+{
+    const int d = c->cfg.d_model, f = c->cfg.d_ffn;
+    GemmArgs a = grouped_args(c, grp_rows, grp_off, ng, max_rows);
+    if (cs) a.cs = *cs;
+    OpScope op(c, "expert_dfc2", 0, chunk, s);
+    a.A = dout; a.lda = d; a.a_mn = false; a.a_rows = c->rows_exp;
+    a.B = c->w2; a.ldb = f; a.b_group_stride = (long)d * f; a.b_mn = true;
+    a.b_rows = (long)c->E_l * d;
+    a.C = c->dA; a.ldc = f; a.aux = c->Gp; a.N = f; a.K = d; a.epi = EPI_DACT;
+    return run_gemm(c, a, s, launches);
+}
+
+// dX = dA W1:  B(n=d, k=f) = W1[e][k][n]  (MN-major)
+lancet_status expert_dfc1(lancet_ctx* c, const int* grp_rows, const int* grp_off, int ng, int max_rows,
+                          cudaStream_t s, int chunk, int* launches)
+{
+    const int d = c->cfg.d_model, f = c->cfg.d_ffn;
+    GemmArgs a = grouped_args(c, grp_rows, grp_off, ng, max_rows);
+    OpScope op(c, "expert_dfc1", 0, chunk, s);
+    a.A = c->dA; a.lda = f; a.a_mn = false; a.a_rows = c->rows_exp;
+    a.B = c->w1; a.ldb = d; a.b_group_stride = (long)f * d; a.b_mn = true;
+    a.b_rows = (long)c->E_l * f;
+    a.C = c->dXe; a.ldc = d; a.aux = nullptr; a.N = d; a.K = f; a.epi = EPI_STORE;
+    return run_gemm(c, a, s, launches);
 }
 
 // dX GEMMs (critical path) of the backward.
@@ -198,28 +279,9 @@ lancet_status expert_backward_dx(lancet_ctx* c, const void* dout, const int* grp
                                  const int* grp_off, int ng, int max_rows, cudaStream_t s,
                                  int chunk, int* launches)
 {
-    const int d = c->cfg.d_model, f = c->cfg.d_ffn;
-    GemmArgs a{};
-    a.mode = GEMM_M_GROUPED; a.n_groups = ng; a.gpw = 1; a.n_weights = c->E_l;
-    a.grp_rows = grp_rows; a.grp_off = grp_off; a.max_rows = max_rows; a.act = c->cfg.act;
-    a.c_rows = c->rows_exp;
-    {   // dA = (dO W2) * act'(A):  B(n=f, k=d) = W2[e][k][n]  (MN-major)
-        OpScope op(c, "expert_dfc2", 0, chunk, s);
-        a.A = dout; a.lda = d; a.a_mn = false; a.a_rows = c->rows_exp;
-        a.B = c->w2; a.ldb = f; a.b_group_stride = (long)d * f; a.b_mn = true;
-        a.b_rows = (long)c->E_l * d;
-        a.C = c->dA; a.ldc = f; a.aux = c->Gp; a.N = f; a.K = d; a.epi = EPI_DACT;
-        lancet_status st = run_gemm(c, a, s, launches);
-        if (st) return st;
-    }
-    {   // dX = dA W1:  B(n=d, k=f) = W1[e][k][n]  (MN-major)
-        OpScope op(c, "expert_dfc1", 0, chunk, s);
-        a.A = c->dA; a.lda = f;
-        a.B = c->w1; a.ldb = d; a.b_group_stride = (long)f * d; a.b_mn = true;
-        a.b_rows = (long)c->E_l * f;
-        a.C = c->dXe; a.ldc = d; a.aux = nullptr; a.N = d; a.K = f; a.epi = EPI_STORE;
-        return run_gemm(c, a, s, launches);
-    }
+    lancet_status st = expert_dfc2(c, dout, grp_rows, grp_off, ng, max_rows, s, chunk, launches);
+    if (st) return st;
+    return expert_dfc1(c, grp_rows, grp_off, ng, max_rows, s, chunk, launches);
 }
 
 // dW GEMMs (K-grouped over each group's token rows): dW2 (+)= dO^T H, dW1 (+)= dA^T X.
@@ -306,6 +368,7 @@ lancet_status create_common(lancet_ctx* c, int world, int rank, int device, cons
         return fail(c, LANCET_ERR_UNSUPPORTED, std::string("lancet_moe needs an sm_100 (B200) device, found ") + prop.name);
     c->num_sms = prop.multiProcessorCount;
     CK(cudaStreamCreateWithFlags(&c->s_comp, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->s_comp2, cudaStreamNonBlocking));
     int lo, hi;
     CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     CK(cudaStreamCreateWithPriority(&c->s_comm, cudaStreamNonBlocking, hi));
@@ -344,7 +407,7 @@ lancet_status create_common(lancet_ctx* c, int world, int rank, int device, cons
     AL(c->dwg_partial, sizeof(float) * dwg_partial_floats(T, d, E));
     AL(c->wgT, sizeof(float) * (size_t)d * E);
     AL(c->counts_dev, sizeof(int) * 2 * (size_t)E * kMaxChunks);
-    AL(c->grp_dev, sizeof(int) * 2 * (size_t)c->E_l * kMaxChunks);
+    AL(c->grp_dev, sizeof(int) * (2 * (size_t)c->E_l * kMaxChunks + 2 * (size_t)c->E_l));   // + merged dW table
     const size_t rs = (size_t)c->rows_src * d * c->elt;
     AL(c->xs, rs);
     AL(c->dcomb, rs);
@@ -580,6 +643,32 @@ __global__ void send_counts_kernel(const int* __restrict__ S, int E, int n, int*
                                                      cudaGetErrorString(cudaGetLastError())); \
     } while (0)
 
+// push mode with the device-side chunk pipeline in the GEMMs (ChunkSync): tcgen05 GEMMs, one
+// launch over all chunks (<= 128 groups), not the serial baseline, not the per-chunk-launch A/B
+bool push_pipelined(const lancet_ctx* c)
+{
+    return c->bf16 && c->cfg.act != LANCET_ACT_IDENTITY_EXPERT &&
+           !(c->cfg.flags & (LANCET_FLAG_SERIAL | LANCET_FLAG_SIMT_GEMM | LANCET_FLAG_CHUNK_LAUNCHES)) &&
+           c->n * c->E_l <= kTcMaxGroups;
+}
+
+// Per-chunk GEMM launches of the push pipeline: chunk ch on sc (even) or s_comp2 (odd), both
+// ordered after everything already on sc, and sc ordered after all of them at the end.
+template <typename F>
+lancet_status per_chunk_alternating(lancet_ctx* c, int n, cudaStream_t sc, F&& body)
+{
+    cudaEvent_t ev_in = c->ev_pool[3], ev_out = c->ev_pool[4];
+    CK(cudaEventRecord(ev_in, sc));
+    CK(cudaStreamWaitEvent(c->s_comp2, ev_in, 0));
+    for (int ch = 0; ch < n; ++ch) {
+        lancet_status st = body(ch, (ch & 1) ? c->s_comp2 : sc);
+        if (st) return st;
+    }
+    CK(cudaEventRecord(ev_out, c->s_comp2));
+    CK(cudaStreamWaitEvent(sc, ev_out, 0));
+    return LANCET_OK;
+}
+
 int push_group_rows_bound(const lancet_ctx* c)
 {
     // a group (e_l, c) holds at most min(C, T) <= max_tokens rows of each source rank
@@ -631,28 +720,57 @@ lancet_status forward_push(lancet_ctx* c, const RouteArgs& ra, const DispatchArg
     CK(cudaStreamWaitEvent(sm, ev_plan, 0));
     // K3 + C2-d fused: chunk c's rows go straight to the owners' receive buffers
     DEV(dev_wait(c, 0, PK_XEFREE, 0, TGT_STEP, sm));
+    cudaEvent_t ev_first = c->ev_pool[2];
     for (int ch = 0; ch < n; ++ch) {
         {
             OpScope op(c, "a2a_dispatch_push", 1, serial ? -1 : ch, sm);
             if (!nocomm)
                 L += launch_permute_push(da, x, chunk_start(T, n, ch), chunk_start(T, n, ch + 1), E_l,
                                          pr->d_push_base + (size_t)ch * E, pr->d_xe, c->bf16, sm);
+            else if (ch == 0)       // NO_COMM (timing): the same permute into local rows
+                L += launch_permute(da, x, c->xs, c->bf16, sm);
         }
         CHECK_LAUNCH();
         DEV(dev_signal(c, 0, PK_PUSH, ch, sm));
+        if (ch == 0) CK(cudaEventRecord(ev_first, sm));
     }
     const int nc = serial ? 1 : n;
     const int mr = push_group_rows_bound(c);
-    for (int cc = 0; cc < nc; ++cc) {
-        const int c0 = serial ? 0 : cc, c1 = serial ? n : cc + 1;
-        for (int ch = c0; ch < c1; ++ch) DEV(dev_wait(c, 0, PK_PUSH, ch, TGT_STEP, sc));
-        if (cc == 0) DEV(dev_wait(c, 1, PK_OUT, 0, TGT_PREV, sc));   // peers done with last step's outputs
-        if (!ident) {
-            lancet_status st = expert_forward(c, d_grp_rows + c0 * E_l, d_grp_off + c0 * E_l, (c1 - c0) * E_l,
-                                              mr, sc, serial ? -1 : cc, &L);
-            if (st) return st;
+    if (push_pipelined(c)) {
+        // one fc1 and one fc2 launch over all chunks: fc1's TMA producer waits for chunk c's
+        // rows of every rank on the device, fc2 publishes chunk c's outputs as soon as its last
+        // tile is stored -- chunk c+1's dispatch runs under chunk c's GEMMs and chunk c's
+        // combine under chunk c+1's, with no launch boundary between chunks
+        DEV(dev_wait(c, 1, PK_OUT, 0, TGT_PREV, sc));   // peers done with last step's outputs
+        // the persistent fc1 starts once this rank's chunk-0 push is done (so that push has
+        // every SM; fc1's CTAs would otherwise hold them while waiting for chunk 0), and waits
+        // for the rest -- every rank's chunk c -- on the device
+        CK(cudaStreamWaitEvent(sc, ev_first, 0));
+        const ChunkSync w = chunk_sync(c, PK_PUSH);
+        lancet_status st = expert_fc1(c, d_grp_rows, d_grp_off, n * E_l, mr, sc, -1, &L, &w);
+        if (st) return st;
+        // fc2 per chunk, each published by a flag kernel once it completed (kernel completion
+        // makes its TMA-stored rows visible to the peers' fused combine); even chunks on the
+        // compute stream, odd ones on a second one, so a chunk's last wave overlaps the next
+        st = per_chunk_alternating(c, n, sc, [&](int ch, cudaStream_t st_) -> lancet_status {
+            lancet_status r = expert_fc2(c, d_grp_rows + ch * E_l, d_grp_off + ch * E_l, E_l, mr, st_, ch, &L);
+            if (r) return r;
+            DEV(dev_signal(c, 0, PK_OUT, ch, st_));
+            return LANCET_OK;
+        });
+        if (st) return st;
+    } else {
+        for (int cc = 0; cc < nc; ++cc) {
+            const int c0 = serial ? 0 : cc, c1 = serial ? n : cc + 1;
+            for (int ch = c0; ch < c1; ++ch) DEV(dev_wait(c, 0, PK_PUSH, ch, TGT_STEP, sc));
+            if (cc == 0) DEV(dev_wait(c, 1, PK_OUT, 0, TGT_PREV, sc));   // peers done with last step's outputs
+            if (!ident) {
+                lancet_status st = expert_forward(c, d_grp_rows + c0 * E_l, d_grp_off + c0 * E_l, (c1 - c0) * E_l,
+                                                  mr, sc, serial ? -1 : cc, &L);
+                if (st) return st;
+            }
+            DEV(dev_signal(c, 0, PK_OUT, cc, sc));
         }
-        DEV(dev_signal(c, 0, PK_OUT, cc, sc));
     }
     // C2-c + K4 fused: chunk c's tokens gather the expert outputs from the owners' buffers
     for (int cc = 0; cc < nc; ++cc) {
@@ -660,9 +778,9 @@ lancet_status forward_push(lancet_ctx* c, const RouteArgs& ra, const DispatchArg
         DEV(dev_wait(c, 0, PK_OUT, cc, TGT_STEP, sm));
         for (int ch = c0; ch < c1; ++ch) {
             OpScope op(c, "a2a_combine_fused", 1, serial ? -1 : ch, sm);
-            if (nocomm) continue;
+                // NO_COMM (timing): the same gather from local rows
             L += launch_combine(da, c->comb, y, chunk_start(T, n, ch), chunk_start(T, n, ch + 1), c->bf16, sm,
-                                pr->d_push_base + (size_t)ch * E, pr->d_outsrc, E_l);
+                                nocomm ? nullptr : pr->d_push_base + (size_t)ch * E, pr->d_outsrc, E_l);
         }
         CHECK_LAUNCH();
     }
@@ -713,6 +831,7 @@ lancet_status backward_push(lancet_ctx* c, const DispatchArgs& da, const void* d
         }
         CHECK_LAUNCH();
         DEV(dev_signal(c, 0, PK_PUSH2, ch, sm));
+        if (ch == 0) CK(cudaEventRecord(c->ev_pool[2], sm));
     }
     DEV(dev_signal(c, 1, PK_OUT, 0, sm));   // the owners' outputs are consumed (K4 and K5 done)
     c->out_consume_pending = false;
@@ -721,6 +840,27 @@ lancet_status backward_push(lancet_ctx* c, const DispatchArgs& da, const void* d
     // dX GEMMs per chunk, each followed by its dW GEMMs
     const int nc = serial ? 1 : n;
     const int mr = push_group_rows_bound(c);
+    if (push_pipelined(c)) {
+        // one dfc2 and one dfc1 launch over all chunks (dfc2 waits for chunk c's dO rows on the
+        // device, dfc1 publishes chunk c's dX rows as soon as they are stored), then the dW
+        // GEMMs once over every chunk's rows (merged table: one K range per expert, no per-chunk
+        // fp32 reduce-add) -- under the fused dX return of the last chunks
+        DEV(dev_wait(c, 1, PK_DXE, 0, TGT_LAST_BWD, sc));   // last backward's K6 readers done
+        CK(cudaStreamWaitEvent(sc, c->ev_pool[2], 0));          // this rank's chunk-0 K5 push done
+        const ChunkSync w = chunk_sync(c, PK_PUSH2);
+        st = expert_dfc2(c, c->dout, d_grp_rows, d_grp_off, n * E_l, mr, sc, -1, &L, &w);
+        if (st) return st;
+        st = per_chunk_alternating(c, n, sc, [&](int ch, cudaStream_t st_) -> lancet_status {
+            lancet_status r = expert_dfc1(c, d_grp_rows + ch * E_l, d_grp_off + ch * E_l, E_l, mr, st_, ch, &L);
+            if (r) return r;
+            DEV(dev_signal(c, 0, PK_DXE, ch, st_));
+            return LANCET_OK;
+        });
+        if (st) return st;
+        const int* merged = c->grp_dev + 2 * kMaxChunks * E_l;
+        st = expert_backward_dw(c, c->dout, merged, merged + E_l, E_l, dw1, dw2, 0, sc, -1, &L);
+        if (st) return st;
+    } else
     for (int cc = 0; cc < nc; ++cc) {
         const int c0 = serial ? 0 : cc, c1 = serial ? n : cc + 1;
         for (int ch = c0; ch < c1; ++ch) DEV(dev_wait(c, 0, PK_PUSH2, ch, TGT_STEP, sc));
@@ -738,7 +878,7 @@ lancet_status backward_push(lancet_ctx* c, const DispatchArgs& da, const void* d
                 if (st) return st;
             }
     }
-    if (!ident && late_dw)
+    if (!ident && late_dw && !push_pipelined(c))
         for (int ch = 0; ch < n; ++ch) {
             st = expert_backward_dw(c, c->dout, d_grp_rows + ch * E_l, d_grp_off + ch * E_l, E_l, dw1, dw2, ch > 0,
                                     sc, ch, &L);
@@ -955,6 +1095,7 @@ LANCET_API lancet_status lancet_destroy(lancet_ctx* c)
     if (c->ev_dw_ready) cudaEventDestroy(c->ev_dw_ready);
     if (c->ev_tl_base) cudaEventDestroy(c->ev_tl_base);
     if (c->s_comp) cudaStreamDestroy(c->s_comp);
+    if (c->s_comp2) cudaStreamDestroy(c->s_comp2);
     if (c->s_comm) cudaStreamDestroy(c->s_comm);
     delete c;
     return LANCET_OK;
@@ -1012,6 +1153,8 @@ LANCET_API lancet_status lancet_moe_forward(lancet_ctx* c, const void* x, const 
     const bool ident = c->cfg.act == LANCET_ACT_IDENTITY_EXPERT;
     const int E = c->cfg.n_experts, d = c->cfg.d_model;
     if (!x || !wg || !y || (!ident && (!w1 || !w2))) return fail(c, LANCET_ERR_ARG, "null required pointer");
+    if (!aligned16(x) || !aligned16(wg) || !aligned16(y) || (!ident && (!aligned16(w1) || !aligned16(w2))))
+        return fail(c, LANCET_ERR_ARG, "x, wg, w1, w2 and y must be 16-byte aligned (vector loads, TMA)");
     if (T < 1 || T > c->cfg.max_tokens) return fail(c, LANCET_ERR_ARG, "T must be in [1, max_tokens]");
     if (k < 1 || k > c->cfg.max_k || k > E) return fail(c, LANCET_ERR_ARG, "k must be in [1, min(E, max_k)]");
     if (!(cf > 0.0) || !std::isfinite(cf)) return fail(c, LANCET_ERR_ARG, "capacity_factor must be > 0");
@@ -1067,6 +1210,7 @@ LANCET_API lancet_status lancet_moe_forward(lancet_ctx* c, const void* x, const 
         // ---- expert parallel over world ranks ---------------------------------------------
         const int G = c->world, E_l = c->E_l;
         const bool serial = c->cfg.flags & LANCET_FLAG_SERIAL;
+        const bool nocomm_ = c->cfg.flags & LANCET_FLAG_NO_COMM;   // timing only: no data exchange
         cudaStream_t sc = c->s_comp, sm = serial ? c->s_comp : c->s_comm;
         CK(cudaEventRecord(c->ev_fork, s));
         CK(cudaStreamWaitEvent(sc, c->ev_fork, 0));
@@ -1169,7 +1313,7 @@ LANCET_API lancet_status lancet_moe_forward(lancet_ctx* c, const void* x, const 
             OpScope op(c, "a2a_dispatch", 1, serial ? -1 : cc, sm);
             if (pr) {
                 std::string err;
-                if (peer_pull(c, lancet::PK_XS, cc, gp.pulls(c->rank, true, c0, c1, xe, rowb), cc == nc - 1, sm, err))
+                if (peer_pull(c, lancet::PK_XS, cc, (nocomm_ ? std::vector<lancet::PeerCopy>{} : gp.pulls(c->rank, true, c0, c1, xe, rowb)), cc == nc - 1, sm, err))
                     return fail(c, LANCET_ERR_CUDA, err);
                 if (ident && peer_signal(c, 0, lancet::PK_OUT, cc, sm))   // identity: xe is the combine source
                     return fail(c, LANCET_ERR_CUDA, "cuStreamWriteValue32");
@@ -1191,7 +1335,7 @@ LANCET_API lancet_status lancet_moe_forward(lancet_ctx* c, const void* x, const 
                         recvs.push_back({p, xe + (size_t)(pl.grp_off[ch * E_l + el] + pl.src_off[(p * E_l + el) * n + ch]) * rowb,
                                          (size_t)pl.recv[(p * E_l + el) * n + ch] * rowb});
             std::string err;
-            if (c->comm->exchange(sends, recvs, sm, err)) return fail(c, LANCET_ERR_NCCL, err);
+            if (!nocomm_ && c->comm->exchange(sends, recvs, sm, err)) return fail(c, LANCET_ERR_NCCL, err);
             ev_disp[cc] = next_ev();
             CK(cudaEventRecord(ev_disp[cc], sm));
         }
@@ -1221,7 +1365,7 @@ LANCET_API lancet_status lancet_moe_forward(lancet_ctx* c, const void* x, const 
             OpScope op(c, "a2a_combine", 1, serial ? -1 : cc, sm);
             if (pr) {
                 std::string err;
-                if (peer_pull(c, lancet::PK_OUT, cc, gp.pulls(c->rank, false, c0, c1, comb, rowb), cc == nc - 1, sm, err))
+                if (peer_pull(c, lancet::PK_OUT, cc, (nocomm_ ? std::vector<lancet::PeerCopy>{} : gp.pulls(c->rank, false, c0, c1, comb, rowb)), cc == nc - 1, sm, err))
                     return fail(c, LANCET_ERR_CUDA, err);
                 ev_comb[cc] = next_ev();
                 CK(cudaEventRecord(ev_comb[cc], sm));
@@ -1241,7 +1385,7 @@ LANCET_API lancet_status lancet_moe_forward(lancet_ctx* c, const void* x, const 
                                          (size_t)pl.send[e * n + ch] * rowb});
                 }
             std::string err;
-            if (c->comm->exchange(sends, recvs, sm, err)) return fail(c, LANCET_ERR_NCCL, err);
+            if (!nocomm_ && c->comm->exchange(sends, recvs, sm, err)) return fail(c, LANCET_ERR_NCCL, err);
             ev_comb[cc] = next_ev();
             CK(cudaEventRecord(ev_comb[cc], sm));
         }
@@ -1277,6 +1421,8 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
     if (!c->have_fwd) return fail(c, LANCET_ERR_STATE, "backward without a preceding forward");
     const bool ident = c->cfg.act == LANCET_ACT_IDENTITY_EXPERT;
     if (!dy || !dx || !dwg || (!ident && (!dw1 || !dw2))) return fail(c, LANCET_ERR_ARG, "null required pointer");
+    if (!aligned16(dy) || !aligned16(dx) || !aligned16(dwg) || (!ident && (!aligned16(dw1) || !aligned16(dw2))))
+        return fail(c, LANCET_ERR_ARG, "dy, dx, dwg, dw1 and dw2 must be 16-byte aligned (vector loads, TMA)");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream_);
     lancet::g_pdl = (c->cfg.flags & LANCET_FLAG_NO_PDL) == 0;
     const int E = c->cfg.n_experts, d = c->cfg.d_model, T = c->T, k = c->k, n = c->n;
@@ -1363,6 +1509,7 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
     if (c->push) return backward_push(c, da, dy, dx, dwg, dw1, dw2, renorm, s, L);
     const int G = c->world, E_l = c->E_l;
     const bool serial = c->cfg.flags & LANCET_FLAG_SERIAL;
+    const bool nocomm_ = c->cfg.flags & LANCET_FLAG_NO_COMM;   // timing only: no data exchange
     const bool late_dw = serial || (c->cfg.flags & LANCET_FLAG_NO_DW_OVERLAP);
     cudaStream_t sc = c->s_comp, sm = serial ? c->s_comp : c->s_comm;
     CK(cudaEventRecord(c->ev_fork, s));
@@ -1411,7 +1558,7 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
         OpScope op(c, "a2a_bwd_dispatch", 1, serial ? -1 : cc, sm);
         if (pr) {
             std::string err;
-            if (peer_pull(c, lancet::PK_DCOMB, cc, gp.pulls(c->rank, true, c0, c1, dout, rowb), cc == nc - 1, sm, err))
+            if (peer_pull(c, lancet::PK_DCOMB, cc, (nocomm_ ? std::vector<lancet::PeerCopy>{} : gp.pulls(c->rank, true, c0, c1, dout, rowb)), cc == nc - 1, sm, err))
                 return fail(c, LANCET_ERR_CUDA, err);
             if (ident && peer_signal(c, 0, lancet::PK_DXE, cc, sm))   // identity: dout is the source back
                 return fail(c, LANCET_ERR_CUDA, "cuStreamWriteValue32");
@@ -1433,7 +1580,7 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
                     recvs.push_back({p, dout + (size_t)(pl.grp_off[ch * E_l + el] + pl.src_off[(p * E_l + el) * n + ch]) * rowb,
                                      (size_t)pl.recv[(p * E_l + el) * n + ch] * rowb});
         std::string err;
-        if (c->comm->exchange(sends, recvs, sm, err)) return fail(c, LANCET_ERR_NCCL, err);
+        if (!nocomm_ && c->comm->exchange(sends, recvs, sm, err)) return fail(c, LANCET_ERR_NCCL, err);
         ev_b1[cc] = next_ev();
         CK(cudaEventRecord(ev_b1[cc], sm));
     }
@@ -1479,7 +1626,7 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
         OpScope op(c, "a2a_bwd_combine", 1, serial ? -1 : cc, sm);
         if (pr) {
             std::string err;
-            if (peer_pull(c, lancet::PK_DXE, cc, gp.pulls(c->rank, false, c0, c1, dxcomb, rowb), cc == nc - 1, sm, err))
+            if (peer_pull(c, lancet::PK_DXE, cc, (nocomm_ ? std::vector<lancet::PeerCopy>{} : gp.pulls(c->rank, false, c0, c1, dxcomb, rowb)), cc == nc - 1, sm, err))
                 return fail(c, LANCET_ERR_CUDA, err);
             ev_b2[cc] = next_ev();
             CK(cudaEventRecord(ev_b2[cc], sm));
@@ -1501,7 +1648,7 @@ LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void
                                      (size_t)pl.send[e * n + ch] * rowb});
             }
         std::string err;
-        if (c->comm->exchange(sends, recvs, sm, err)) return fail(c, LANCET_ERR_NCCL, err);
+        if (!nocomm_ && c->comm->exchange(sends, recvs, sm, err)) return fail(c, LANCET_ERR_NCCL, err);
         ev_b2[cc] = next_ev();
         CK(cudaEventRecord(ev_b2[cc], sm));
         st = run_fillers(c, serial ? n : n + cc, serial ? 2 * n : n + cc + 1, sc, &L);
@@ -1642,11 +1789,23 @@ LANCET_API lancet_status lancet_debug_copy(lancet_ctx* c, int32_t which, void* h
     lancet_status st = check_ready(c);
     if (st) return st;
     if (!c->have_fwd) return fail(c, LANCET_ERR_STATE, "no forward yet");
-    if (which != 0) return fail(c, LANCET_ERR_ARG, "unknown buffer");
-    const size_t need = sizeof(float) * (size_t)c->T * c->cfg.n_experts;
+    const void* src = nullptr;
+    size_t need = 0;
+    const size_t rowb = (size_t)c->cfg.d_model * c->elt;
+    switch (which) {
+    case 0: src = c->logits; need = sizeof(float) * (size_t)c->T * c->cfg.n_experts; break;
+    case 1: src = c->out; need = (size_t)c->rows_exp * rowb; break;
+    case 2: src = c->H; need = (size_t)c->rows_exp * c->cfg.d_ffn * c->elt; break;
+    case 3: src = c->xe; need = (size_t)c->rows_exp * rowb; break;
+    case 4: src = c->grp_dev; need = sizeof(int) * 2 * (size_t)c->n * c->E_l; break;
+    case 5: if (c->peer) { src = c->peer->my_flags; need = sizeof(uint32_t) * lancet::peer_flag_words(c->world, c->peer->n_max); } break;
+    case 6: if (c->peer) { src = c->peer->d_push_base; need = sizeof(int) * (size_t)c->n * c->cfg.n_experts; } break;
+    default: break;
+    }
+    if (!src) return fail(c, LANCET_ERR_ARG, "unknown buffer");
     if (!host_dst || bytes < need) return fail(c, LANCET_ERR_ARG, "destination too small");
     CK(cudaDeviceSynchronize());
-    CK(cudaMemcpy(host_dst, c->logits, need, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(host_dst, src, need, cudaMemcpyDeviceToHost));
     return LANCET_OK;
 }
 

@@ -451,7 +451,8 @@ __global__ void counts_allgather_kernel(const int* __restrict__ row, int len, in
 //   base [n][E]: row of this rank's chunk-c rows for expert e in the owner's buffer, minus
 //   S[e][c] (so row = base + slot).
 __global__ void plan_kernel(const int* __restrict__ M, int G, int E, int E_l, int n, int me, int* grp_rows,
-                            int* grp_off, int* base, int* R, int* OFF, int rows_cap, uint32_t* err, uint32_t code)
+                            int* grp_off, int* base, int* R, int* OFF, int rows_cap, uint32_t* err, uint32_t code,
+                            int* merged)
 {
     pdl_wait();
     const int tid = threadIdx.x, nt = blockDim.x;
@@ -477,6 +478,13 @@ __global__ void plan_kernel(const int* __restrict__ M, int G, int E, int E_l, in
         const int i = (me * E_l + el) * n + ch;
         grp_rows[q] = R[i];
         grp_off[q] = OFF[i];
+    }
+    // merged dW tables [E_l] rows | offsets: expert e_l's rows of every chunk as one K range
+    // (its groups are consecutive in the buffer; the pads between them are zero rows)
+    for (int el = tid; el < E_l; el += nt) {
+        const int i0 = (me * E_l + el) * n, i1 = i0 + n - 1;
+        merged[el] = OFF[i1] + R[i1] - OFF[i0];
+        merged[E_l + el] = OFF[i0];
     }
     for (int q = tid; q < n * E; q += nt) {
         const int ch = q / E, e = q % E;
@@ -511,6 +519,21 @@ std::string peer_error_text(uint32_t code)
 uint32_t peer_error(const lancet_ctx* c)
 {
     return (c->peer && c->peer->h_err) ? *reinterpret_cast<volatile uint32_t*>(c->peer->h_err) : 0u;
+}
+
+ChunkSync chunk_sync(lancet_ctx* c, int wait_kind)
+{
+    PeerLinks* pl = c->peer;
+    ChunkSync cs;
+    cs.gpc = c->E_l;
+    cs.ranks = pl->world;
+    cs.wait_flags = pl->my_flags + pl->flag_index(0, wait_kind, 0, 0);
+    cs.wait_chunk_stride = pl->world;
+    cs.seq = pl->d_seq;
+    cs.timeout_ns = pl->timeout_ns;
+    cs.err = pl->d_err;
+    cs.err_code = wait_code(0, wait_kind, 0);
+    return cs;
 }
 
 int dev_seq_bump(lancet_ctx* c, cudaStream_t s)
@@ -553,7 +576,7 @@ int dev_plan(lancet_ctx* c, int n, cudaStream_t s)
     int* OFF = R + (size_t)E * pl->n_max;
     launch_k(plan_kernel, 1, 256, 0, s, (const int*)pl->my_counts, pl->world, E, c->E_l, n, c->rank, c->grp_dev,
              c->grp_dev + n * c->E_l, pl->d_push_base, R, OFF, pl->rows_cap, pl->d_err,
-             wait_code(0, kPlanKind, 0));
+             wait_code(0, kPlanKind, 0), c->grp_dev + 2 * kMaxChunks * c->E_l);
     return cudaGetLastError() != cudaSuccess;
 }
 

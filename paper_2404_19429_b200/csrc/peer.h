@@ -6,6 +6,8 @@
 #include <string>
 #include <vector>
 
+#include "kernels.h"
+
 struct lancet_ctx;
 
 namespace lancet {
@@ -19,7 +21,8 @@ struct PeerCopy {
     size_t bytes;
 };
 
-int peer_init(lancet_ctx* c, std::string& err);          // after the workspace is allocated
+int peer_init(lancet_ctx* c, std::string& err);
+int peer_flag_words(int world, int n_max);          // after the workspace is allocated
 size_t peer_blob_bytes();                                 // per rank
 int peer_export(lancet_ctx* c, void* blob, std::string& err);
 int peer_import(lancet_ctx* c, const void* blobs, std::string& err);   // world blobs, rank order
@@ -53,6 +56,8 @@ int dev_counts(lancet_ctx* c, const int* d_send, int n, cudaStream_t s);
 // [n][E] of this rank, from the gathered matrix
 int dev_plan(lancet_ctx* c, int n, cudaStream_t s);
 uint32_t peer_error(const lancet_ctx* c);      // 0 or the error word
+// ChunkSync of a GEMM over all chunks: its TMA producer waits for kind `wait_kind` per chunk
+ChunkSync chunk_sync(lancet_ctx* c, int wait_kind);
 std::string peer_error_text(uint32_t code);
 
 }  // namespace lancet

@@ -63,6 +63,7 @@ __host__ __device__ inline GateGeom gate_geom(int E, int elt_bytes)
     g.tpt = E / g.ce;
     g.TB = kGateThreads * g.tt / g.tpt;
     if (g.TB > kGateMaxTB) g.TB = kGateMaxTB;
+    g.TB = g.TB / g.tt * g.tt;                  // whole token groups (E = 192: 42 -> 40)
     if (g.TB < g.tt) g.TB = g.tt;
     g.threads = g.TB / g.tt * g.tpt;
     g.row_bytes = gate_dt(g.ce) * elt_bytes + 16;
@@ -805,7 +806,8 @@ int launch_routing(const RouteArgs& a, bool is_bf16, cudaStream_t s)
     cudaMemsetAsync(a.hist, 0, sizeof(int) * n_tiles * a.E, s);
     static bool attr_set = false;
     if (!attr_set) {
-#define SET(Elt, CE) cudaFuncSetAttribute(gate_topk_kernel<Elt, CE, (CE >= 8 ? kGateTT8 : CE >= 4 ? 2 : 1)>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)
+// 225 KiB: the 227 KiB opt-in minus the static histogram (E = 256 stages 207 KiB of x / Wg tiles)
+#define SET(Elt, CE) cudaFuncSetAttribute(gate_topk_kernel<Elt, CE, (CE >= 8 ? kGateTT8 : CE >= 4 ? 2 : 1)>, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024)
         SET(bf16, 8); SET(bf16, 4); SET(bf16, 2); SET(bf16, 1);
         SET(float, 8); SET(float, 4); SET(float, 2); SET(float, 1);
 #undef SET

@@ -34,6 +34,7 @@ FLAG_DEFER_DW = 4096
 FLAG_GATE_RANDOM = 8192
 FLAG_PEER_PUSH = 16384
 FLAG_NO_COMM = 32768          # timing only: the data exchanges are skipped (results are wrong)
+FLAG_CHUNK_LAUNCHES = 65536   # push mode: one GEMM launch per chunk (A/B of the device-side pipeline)
 # LANCET_EXTRA_FLAGS: OR'ed into every context's flags (e.g. run the test suite under PDL)
 EXTRA_FLAGS = int(os.environ.get("LANCET_EXTRA_FLAGS", "0"), 0)
 

@@ -26,12 +26,15 @@ def _push_ctx(T, d, f, E, k, flags=0, act="gelu_tanh"):
     return lancet.Context(cfg, transport="peer")
 
 
-@pytest.mark.parametrize("n,act", [(4, "gelu_tanh"), (1, "gelu_tanh"), (3, "identity_expert")])
-def test_push_step_replays_from_a_cuda_graph(n, act):
+@pytest.mark.parametrize("n,act,launches", [(4, "gelu_tanh", False), (1, "gelu_tanh", False),
+                                            (3, "identity_expert", False), (4, "gelu_tanh", True)])
+def test_push_step_replays_from_a_cuda_graph(n, act, launches):
     # capture one fwd+bwd step into a CUDA graph, then replay it on new inputs copied into the
     # captured buffers: every output equals an eager step on the same inputs bit for bit
+    # (launches: the per-chunk-launch schedule instead of the device-side GEMM pipeline)
+    from paper_2404_19429_b200 import FLAG_CHUNK_LAUNCHES
     T, d, f, E, k, cf = 2048, 256, 512, 8, 2, 1.0
-    ctx = _push_ctx(T, d, f, E, k, act=act)
+    ctx = _push_ctx(T, d, f, E, k, act=act, flags=FLAG_CHUNK_LAUNCHES if launches else 0)
     ins = [inputs(T, d, f, E, k, beta=0.5, seed=300 + i) for i in range(3)]
     bf = torch.bfloat16
     x = to_dev(ins[0]["x"], bf)
@@ -92,13 +95,16 @@ def test_push_step_replays_from_a_cuda_graph(n, act):
     ctx.close()
 
 
-def test_push_exchanges_overlap_the_expert_gemms():
+@pytest.mark.parametrize("launches", [False, True])
+def test_push_exchanges_overlap_the_expert_gemms(launches):
     # the fused exchange kernels run on the comm stream, on the SMs the persistent GEMMs leave
-    # free: chunk c's fused combine runs under chunk c+1's expert GEMMs (forward), chunk c's
-    # fused dX return under chunk c's dW GEMMs (backward) -- timeline of a one-rank group
-    from paper_2404_19429_b200 import FLAG_TIMELINE
+    # free.  Device-side pipeline (default): chunk c >= 1's dispatch runs under fc1 (one launch
+    # over all chunks, waiting per chunk on the device), chunk c's combine under chunk c+1's fc2,
+    # chunk c's dX return under chunk c+1's dfc1 or the merged dW GEMMs.
+    # Per-chunk launches: chunk c's combine under chunk c+1's GEMMs, its dX return under its dW.
+    from paper_2404_19429_b200 import FLAG_CHUNK_LAUNCHES, FLAG_TIMELINE
     T, d, f, E, k, n = 16384, 1024, 4096, 8, 2, 4
-    ctx = _push_ctx(T, d, f, E, k, flags=FLAG_TIMELINE)
+    ctx = _push_ctx(T, d, f, E, k, flags=FLAG_TIMELINE | (FLAG_CHUNK_LAUNCHES if launches else 0))
     ins = inputs(T, d, f, E, k, beta=0.25, seed=4)
     for _ in range(3):
         run_gpu(ins, E, k, 1.25, n, ctx=ctx)
@@ -113,10 +119,17 @@ def test_push_exchanges_overlap_the_expert_gemms():
     def overlap(a, b):
         return max(0.0, min(a[1], b[1]) - max(a[0], b[0]))
 
-    fwd = [overlap(span("a2a_combine_fused", ch), (span("expert_fc1", ch + 1)[0], span("expert_fc2", ch + 1)[1]))
-           for ch in range(n - 1)]
-    bwd = [overlap(span("a2a_bwd_combine_fused", ch), (span("expert_dw2", ch)[0], span("expert_dw1", ch)[1]))
-           for ch in range(n)]
+    if launches:
+        fwd = [overlap(span("a2a_combine_fused", ch), (span("expert_fc1", ch + 1)[0], span("expert_fc2", ch + 1)[1]))
+               for ch in range(n - 1)]
+        bwd = [overlap(span("a2a_bwd_combine_fused", ch), (span("expert_dw2", ch)[0], span("expert_dw1", ch)[1]))
+               for ch in range(n)]
+    else:
+        fc1, dw1 = span("expert_fc1", -1), span("expert_dw1", -1)
+        fwd = [overlap(span("a2a_dispatch_push", ch), fc1) for ch in range(1, n)] + \
+              [overlap(span("a2a_combine_fused", ch), span("expert_fc2", ch + 1)) for ch in range(n - 1)]
+        bwd = [overlap(span("a2a_bwd_combine_fused", ch), (span("expert_dfc1", ch + 1)[0] if ch + 1 < n else
+                                                           span("expert_dw2", -1)[0], dw1[1])) for ch in range(n)]
     assert sum(o > 0 for o in fwd) >= n - 2, fwd
     assert sum(o > 0 for o in bwd) >= n - 1, bwd
     for name in ("a2a_dispatch_push", "a2a_combine_fused", "a2a_bwd_dispatch_push", "a2a_bwd_combine_fused"):
