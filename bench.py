@@ -418,7 +418,9 @@ def measure_arm(a, ctx, lancet, flags, step, stream, barrier, max_over_ranks, n_
     ms_serial_clean, _ = run(flags | lancet.FLAG_SERIAL, steps)
     ctx.set_flags(flags)
     world = ctx.world
+    from paper_2404_19429_b200.chunk_tuner import profile_ops
     return {"n_chunks": n_chunks, "ms_per_step": ms, "tokens_per_s": world * a.tokens / (ms / 1000.0),
+            "op_profile_us": [round(v, 3) for v in profile_ops(tl, steps, n_chunks)],
             "instrumented_ms_per_step": ms_instr,
             "exposed_a2a_ms": max_over_ranks(exposed), "a2a_ms_on_comm_lane": max_over_ranks(comm),
             "exposed_a2a_split_ms": {"counts": exp_c, "data": exp_d},
@@ -426,6 +428,31 @@ def measure_arm(a, ctx, lancet, flags, step, stream, barrier, max_over_ranks, n_
             "exposed_over_unoverlapped": (max_over_ranks(exposed) / max_over_ranks(unover)) if unover > 0 else None,
             "serial_ms_per_step": ms_serial_clean,
             "no_comm_ms_per_step": ms_nocomm, "exposed_upper_bound_ms": ms - ms_nocomm}
+
+
+def tuner_record(a, ctx, lancet, flags, step_fn, stream, barrier, max_over_ranks, schedule, bytes_full,
+                 ns=(1, 2, 4, 8), fit_on=(1, 4)):
+    """Every n of `ns` measured on one definition (measure_arm), and the chunk-count tuner
+    (lancet_tune_chunks, NEXT-3) fitted on the op profiles of `fit_on` predicting n = 1..8:
+    predicted vs measured step time per n, the tuner's pick and the measured best."""
+    from paper_2404_19429_b200.chunk_tuner import tune
+    import numpy as np
+    by_n = [measure_arm(a, ctx, lancet, flags, step_fn, stream, barrier, max_over_ranks, n) for n in ns]
+    prof = {r["n_chunks"]: np.array(r["op_profile_us"]) for r in by_n if r["n_chunks"] in fit_on}
+    best, pred, expo = tune(prof, bytes_full, schedule, max_chunks=max(8, max(ns)))
+    meas = {r["n_chunks"]: r["ms_per_step"] * 1000.0 for r in by_n}
+    pts = [{"n": n, "measured_us": meas[n], "predicted_us": float(pred[n - 1]),
+            "error": float((pred[n - 1] - meas[n]) / meas[n]), "predicted_exposed_us": float(expo[n - 1])}
+           for n in ns]
+    return {"by_n": by_n,
+            "tuner": {"schedule": "push pipeline" if schedule == 1 else "per-chunk launches",
+                      "profiled_n": sorted(prof), "predicted_us_n1_to_8": [round(float(v), 1) for v in pred],
+                      "points": pts, "mean_abs_error": float(np.mean([abs(p["error"]) for p in pts])),
+                      "pick": int(best), "measured_best": int(min(meas, key=meas.get)),
+                      "model": "DP over partition counts (P:L405-L414) scored by the two-lane stage "
+                               "simulator (P:L488-L499) on lancet.cu's schedule; ops from the per-op "
+                               "timelines at the profiled n (caching profiler, P:L322-L323); exchanges "
+                               "from the size-interpolated cost model at C/n (P:L325-L328)"}}
 
 
 def make_context(a, lancet, cfg, world, rank, local_rank, dev):
@@ -721,9 +748,9 @@ def run_lancet(a, world, rank, local_rank):
         pcfg = dataclasses.replace(cfg, flags=(flags & ~lancet.FLAG_FORCE_EP) | lancet.FLAG_PEER_PUSH)
         ectx = lancet.Context(pcfg, world=1, rank=0, device=local_rank, transport="peer")
         ep_flags = pcfg.flags
-        out["ep"] = {"transport": "peer push, one-rank group (all exchanges to self)",
-                     "by_n": [measure_arm(a, ectx, lancet, ep_flags, step_on(ectx), stream, barrier, max_over_ranks, n)
-                              for n in sorted({1, a.chunks})]}
+        rec = tuner_record(a, ectx, lancet, ep_flags, step_on(ectx), stream, barrier, max_over_ranks, 1,
+                           float(adm * rowb), ns=sorted({1, 2, 4, 8, a.chunks}))
+        out["ep"] = {"transport": "peer push, one-rank group (all exchanges to self)", **rec}
         ectx.close()
     if world > 1 and not a.no_arms:
         # every transport on the same definitions (push / pull over the peer transport, NCCL)
@@ -744,6 +771,10 @@ def run_lancet(a, world, rank, local_rank):
                 barrier()
                 actx.close()
         out["arms"] = arms
+        # the chunk-count tuner on the main arm: n = 1, 2, 4, 8 measured, predicted from n = 1, 4
+        sched = 1 if (a.transport_used == "peer" and not a.no_push) else 0
+        out["chunk_tuner"] = tuner_record(a, ctx, lancet, flags, step_on(ctx), stream, barrier, max_over_ranks,
+                                          sched, float(adm * rowb))["tuner"]
     if rank == 0 and not a.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(a)
     barrier()

@@ -324,6 +324,48 @@ lancet_status lancet_dw_schedule(int32_t n_instr, const int32_t* kind, const dou
 lancet_status lancet_stack_dw_plan(int32_t L, int32_t n_chunks, const double* t_a2a,
                                    const double* t_dw, int32_t* host_layer, int32_t* host_a2a);
 
+/* Chunk-count tuner (host only, no device): Lancet's partition-count
+ * search reduced to one MoE layer.  The DP over partition ranges has a
+ * single range here, so it is a scan over n = 1..max_chunks; each n is scored by the pipeline
+ * scheduler of L488-L499 (stages of every chunk on a computation and a communication lane in
+ * their scheduled order; an op starts at the later of its dependencies' end and its lane's
+ * previous op; step = end of the last op), run on the schedule lancet.cu enqueues
+ * (schedule 0: per-chunk launches of the copy-engine / NCCL paths; 1: the push pipeline).
+ * Op costs come from a caching profiler (L322-L323): prof_us[i][op] = the op's duration per
+ * chunk (per step for GATE, COUNTS, K7) measured with prof_n[i] chunks (n_prof >= 2, e.g. the
+ * timeline of one step at n = 1, 2, 4).  Communication follows the cost model of L325-L328:
+ * (bytes, us) points at the profiled message sizes bytes_full / prof_n[i], linearly
+ * interpolated, and an n-partitioned exchange costs the model at bytes_full / n (the C/n
+ * approximation); computation is interpolated linearly in 1/n.  bytes_full: bytes of one data
+ * exchange at n = 1.  Outputs: pred_us[n-1] (step time), pred_exposed_us[n-1] (exposed
+ * communication; may be NULL), *best_n.  LANCET_ERR_ARG on bad sizes. */
+enum {
+    LANCET_OP_GATE = 0,      /* once: routing (gate, slot scan; + permute on the pull / NCCL paths) */
+    LANCET_OP_COUNTS,        /* once, comm: the size exchange                     */
+    LANCET_OP_DISPATCH,      /* comm: dispatch exchange of a chunk (push: fused permute)   */
+    LANCET_OP_FC1, LANCET_OP_FC2,
+    LANCET_OP_COMBINE,       /* comm: combine exchange of a chunk (push: fused with K4)    */
+    LANCET_OP_GATHER,        /* K4 (pull / NCCL)                                           */
+    LANCET_OP_K5,            /* combine backward (pull / NCCL)                             */
+    LANCET_OP_BWD_DISPATCH,  /* comm: dO rows to the experts (push: fused with K5)         */
+    LANCET_OP_DFC2, LANCET_OP_DFC1,
+    LANCET_OP_DW,            /* dW2 + dW1 (per chunk; push: merged, profiled as total / n) */
+    LANCET_OP_BWD_COMBINE,   /* comm: dX rows back (push: fused with K6)                   */
+    LANCET_OP_K6,            /* dispatch backward + gate term (pull / NCCL)                */
+    LANCET_OP_K7,            /* once: dWg                                                  */
+    LANCET_OP_N
+};
+typedef struct {
+    int32_t schedule;
+    int32_t n_prof;
+    const int32_t* prof_n;   /* [n_prof]               */
+    const double* prof_us;   /* [n_prof][LANCET_OP_N]  */
+    double bytes_full;
+    int32_t max_chunks;      /* 1..64                  */
+} lancet_tune_input;
+lancet_status lancet_tune_chunks(const lancet_tune_input* in, double* pred_us, double* pred_exposed_us,
+                                 int32_t* best_n);
+
 /* Routing sizes of the last forward (host arrays; synchronises with the forward):
  *   send_counts [E][n_chunks]         rows this rank admitted per expert per chunk
  *   recv_counts [G][E_l][n_chunks]    rows this rank's experts receive per source rank

@@ -45,7 +45,8 @@ EXPORTS = ["lancet_abi_version", "lancet_last_error", "lancet_nccl_unique_id", "
            "lancet_workspace_bytes", "lancet_launch_counts", "lancet_plan_exchange",
            "lancet_create_peer", "lancet_peer_blob_bytes", "lancet_peer_export", "lancet_peer_import",
            "lancet_moe_backward_dw", "lancet_set_dw_fillers", "lancet_dw_schedule", "lancet_stack_dw_plan",
-           "lancet_set_gate_seed", "lancet_set_peer_timeout_ms", "lancet_peer_abort", "lancet_peer_status"]
+           "lancet_set_gate_seed", "lancet_set_peer_timeout_ms", "lancet_peer_abort", "lancet_peer_status",
+           "lancet_tune_chunks"]
 
 
 class LancetError(RuntimeError):

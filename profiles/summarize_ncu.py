@@ -3,9 +3,10 @@
   python profiles/summarize_ncu.py launches LAUNCHES.csv STEPS OUT.md
       per-kernel share of the device time from an `ncu --metrics gpu__time_duration.sum`
       launch list (cold-cache, serialised; compare SHARES, not absolutes)
-  python profiles/summarize_ncu.py full REPORT.ncu-rep OUT.json OUT.md
+  python profiles/summarize_ncu.py full REPORT.ncu-rep OUT.json OUT.md [CONFIG_JSON]
       per-launch duration, DRAM bytes, tensor-pipe %, issue % and top stall reasons of a
-      `--set full` capture; OUT.json holds the GEMM DRAM traffic per step read by bench.py
+      `--set full` capture; OUT.json holds the GEMM DRAM traffic per step read by bench.py,
+      with the captured configuration (bench.py attaches the traffic only to that config)
 """
 import collections
 import csv
@@ -39,7 +40,7 @@ def launches(path, steps, out):
     print("\n".join(lines))
 
 
-def full(rep, out_json, out_md):
+def full(rep, out_json, out_md, config=None):
     txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     h = rows[0]
@@ -61,6 +62,8 @@ def full(rep, out_json, out_md):
             top_stalls=[f"{k} {v:.2f}" for v, k in top]))
     gemms = [r for r in recs if "tc_gemm" in r["kernel"]]
     summary = {"source": rep, "launches": recs}
+    if config:
+        summary["config"] = json.loads(config)
     if len(gemms) == 6:
         for name, r in zip(GEMM_NAMES, gemms):
             r["op"] = name
@@ -82,4 +85,4 @@ if __name__ == "__main__":
     if sys.argv[1] == "launches":
         launches(sys.argv[2], sys.argv[3], sys.argv[4])
     else:
-        full(sys.argv[2], sys.argv[3], sys.argv[4])
+        full(sys.argv[2], sys.argv[3], sys.argv[4], sys.argv[5] if len(sys.argv) > 5 else None)

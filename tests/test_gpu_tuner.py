@@ -1,0 +1,70 @@
+"""GPU check of the chunk-count tuner (lancet_tune_chunks) on the
+expert-parallel push path of one B200 (a one-rank peer group at the configs[1] shape): fitted on
+the op profiles of n = 1 and 4, its pick among n = 1..8 must be (within the run-to-run noise)
+the measured best of n = 1, 2, 4, 8, and its predictions close to the measured step times."""
+import numpy as np
+import pytest
+import torch
+
+from gpu_harness import inputs, to_dev
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2404_19429_b200 import build
+    build.build()
+
+
+def test_tuner_pick_is_the_measured_best_on_the_push_path():
+    from paper_2404_19429_b200 import FLAG_PEER_PUSH, FLAG_TIMELINE, lancet
+    from paper_2404_19429_b200.chunk_tuner import profile_ops, tune
+    T, d, f, E, k, cf = 16384, 1024, 4096, 8, 2, 1.25
+    ins = inputs(T, d, f, E, k, beta=0.25, seed=21)
+    bf = torch.bfloat16
+    x, dy = to_dev(ins["x"], bf), to_dev(ins["dy"], bf)
+    wg, w1, w2 = to_dev(ins["wg"], torch.float32), to_dev(ins["w1"], bf), to_dev(ins["w2"], bf)
+    y, dx = torch.empty_like(x), torch.empty_like(x)
+    dwg = torch.empty_like(wg)
+    dw1, dw2 = torch.empty(w1.shape, device="cuda"), torch.empty(w2.shape, device="cuda")
+    cfg = lancet.LayerConfig(d_model=d, d_ffn=f, n_experts=E, max_tokens=T, max_k=k, max_chunks=8, flags=FLAG_PEER_PUSH)
+    ctx = lancet.Context(cfg, transport="peer")
+
+    def step(n):
+        ctx.forward(x, wg, w1, w2, k, cf, n, y=y, routing=False)
+        ctx.backward(dy, dx=dx, dwg=dwg, dw1=dw1, dw2=dw2)
+
+    meas, prof = {}, {}
+    for rnd in range(2):                          # two interleaved rounds, best of
+        for n in (1, 2, 4, 8):
+            ctx.set_flags(FLAG_PEER_PUSH)
+            for _ in range(5):
+                step(n)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(15):
+                step(n)
+            e1.record()
+            torch.cuda.synchronize()
+            meas[n] = min(meas.get(n, 1e30), e0.elapsed_time(e1) / 15 * 1000.0)
+            if rnd == 0 and n in (1, 4):
+                ctx.set_flags(FLAG_PEER_PUSH | FLAG_TIMELINE)
+                step(n)
+                torch.cuda.synchronize()
+                ctx.timeline_begin()
+                for _ in range(3):
+                    step(n)
+                prof[n] = profile_ops(ctx.timeline(cap=100000), 3, n)
+    send, _, _ = ctx.counts(4)
+    ctx.close()
+    best, pred, _ = tune(prof, float(send.sum()) * d * 2, schedule=1, max_chunks=8)
+    mbest = min(meas, key=meas.get)
+    errs = {n: (pred[n - 1] - meas[n]) / meas[n] for n in meas}
+    assert np.mean([abs(e) for e in errs.values()]) <= 0.15, (errs, meas, list(pred))
+    # the pick, measured if it is one of the four, else its neighbours bound it
+    t_pick = meas.get(best, min(meas[n] for n in meas if n >= best) if best < 8 else meas[8])
+    assert t_pick <= 1.05 * meas[mbest], (best, mbest, meas, list(pred))
