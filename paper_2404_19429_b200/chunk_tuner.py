@@ -41,13 +41,26 @@ class _TuneInput(ctypes.Structure):
 
 def profile_ops(timeline, steps: int, n: int) -> np.ndarray:
     """Per-chunk cost of every op kind (per step for GATE, COUNTS, K7) from the timeline of
-    `steps` fwd+bwd steps run with n chunks: each kind's total event time per step, divided by
-    n for the chunked kinds (a launch over all chunks counts as n chunks' worth)."""
-    tot = np.zeros(N_OPS)
+    `steps` fwd+bwd steps run with n chunks: the measure of the union of each kind's event
+    intervals per step (launches of one kind that run concurrently -- the push pipeline's fc2 /
+    dfc1 on two streams -- count once), divided by n for the chunked kinds (a launch over all
+    chunks counts as n chunks' worth)."""
+    iv = {}
     for r in timeline:
         k = TIMELINE_TO_OP.get(r["name"])
         if k is not None:
-            tot[OPS.index(k)] += r["end_us"] - r["start_us"]
+            iv.setdefault(k, []).append((r["start_us"], r["end_us"]))
+    tot = np.zeros(N_OPS)
+    for k, v in iv.items():
+        v.sort()
+        s, e, acc = v[0][0], v[0][1], 0.0
+        for a, b in v[1:]:
+            if a <= e:
+                e = max(e, b)
+            else:
+                acc += e - s
+                s, e = a, b
+        tot[OPS.index(k)] = acc + (e - s)
     tot /= steps
     for i, k in enumerate(OPS):
         if k not in ONCE:

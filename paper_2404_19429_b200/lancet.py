@@ -328,6 +328,7 @@ class Context:
             n_chunks, _ptr(y), _ptr(idx), _ptr(slot), _ptr(w), _stream(stream))
         _check(st, self._p)
         self._last = (x, wg, w1, w2)       # the library keeps pointers until backward
+        self._last_n = n_chunks
         return y, idx, slot, w
 
     def backward(self, dy, dx=None, dwg=None, dw1=None, dw2=None, stream=None):
@@ -372,8 +373,16 @@ class Context:
         _check(load_library().lancet_set_dw_fillers(self._p, n, others, which, idx), self._p)
 
     # -- introspection ------------------------------------------------------------------------
-    def counts(self, n_chunks: int):
+    def counts(self, n_chunks: int | None = None):
+        """(send [E][n], recv [G][E_l][n], C) of the last forward; n is that forward's chunk
+        count (the host arrays are sized by it)."""
         import numpy as np
+        last = getattr(self, "_last_n", None)
+        if last is None:
+            raise LancetError(5, "no forward yet")
+        if n_chunks is not None and n_chunks != last:
+            raise LancetError(1, f"counts({n_chunks}): the last forward ran {last} chunks")
+        n_chunks = last
         E, G = self.cfg.n_experts, self.world
         send = np.zeros((E, n_chunks), dtype=np.int32)
         recv = np.zeros((G, self.E_l, n_chunks), dtype=np.int32)

@@ -77,12 +77,14 @@ def test_comm_model_interpolates_sizes_and_uses_c_over_n():
 def test_profile_from_timeline():
     tl = [dict(name="expert_fc1", start_us=0.0, end_us=80.0), dict(name="expert_fc1", start_us=100.0, end_us=180.0),
           dict(name="gate", start_us=0.0, end_us=30.0), dict(name="a2a_dispatch_push", start_us=0.0, end_us=10.0),
-          dict(name="expert_dw2", start_us=0.0, end_us=50.0), dict(name="expert_dw1", start_us=0.0, end_us=70.0)]
+          dict(name="expert_dw2", start_us=0.0, end_us=50.0), dict(name="expert_dw1", start_us=50.0, end_us=120.0),
+          dict(name="expert_fc2", start_us=0.0, end_us=40.0), dict(name="expert_fc2", start_us=20.0, end_us=60.0)]
     p = profile_ops(tl, steps=1, n=2)
     assert p[OPS.index("FC1")] == pytest.approx(80.0)
     assert p[OPS.index("GATE")] == pytest.approx(30.0)
     assert p[OPS.index("DISPATCH")] == pytest.approx(5.0)
     assert p[OPS.index("DW")] == pytest.approx(60.0)
+    assert p[OPS.index("FC2")] == pytest.approx(30.0)      # concurrent launches count once (union)
 
 
 def test_bad_arguments():

@@ -59,7 +59,7 @@ def test_tuner_pick_is_the_measured_best_on_the_push_path():
                 for _ in range(3):
                     step(n)
                 prof[n] = profile_ops(ctx.timeline(cap=100000), 3, n)
-    send, _, _ = ctx.counts(4)
+    send, _, _ = ctx.counts()
     ctx.close()
     best, pred, _ = tune(prof, float(send.sum()) * d * 2, schedule=1, max_chunks=8)
     mbest = min(meas, key=meas.get)
