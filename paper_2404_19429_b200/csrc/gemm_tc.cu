@@ -379,11 +379,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         }
     }
     tc_fence_before();
-    // the cluster barrier orders the tcgen05.alloc write of tmem_slot for the whole cluster; the
-    // CTA barrier after it is redundant for the hardware but is the one compute-sanitizer's
-    // racecheck models (with barrier.cluster alone it reports the slot read as a hazard)
     if constexpr (CG * MC > 1) cluster_sync();
-    __syncthreads();
+    else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     const int total = tstart[p.n_groups];
