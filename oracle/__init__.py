@@ -8,8 +8,10 @@ Contents
   moe.py           routing, expert FFN, layer forward/backward over G simulated ranks (fp64)
   gate_logits.c    the fp32 fma-chain gate logits of DESIGN.md R1 (bit-exact routing)
   _native.py       gcc build + ctypes loader for gate_logits.c
+  block.py         GPT-MoE block (LN, causal attention, MoE) and its pre-MoE partitioned form
 Each function cites the PAPER.md passage it follows; DESIGN.md lists the readings (R1-R14)
 taken where the paper is silent, and the CPU tests that pin every function.
 """
 from . import moe  # noqa: F401
+from . import block  # noqa: F401
 from ._native import build  # noqa: F401

@@ -29,11 +29,13 @@ import numpy as np
 
 __all__ = [
     "LayerShape", "round_to_bf16", "gen_u", "gen_tokens", "gen_gate", "gen_experts",
-    "gen_dy", "gen_rank_inputs", "TINY", "CFG2",
+    "gen_dy", "gen_rank_inputs", "TINY", "CFG2", "BlockShape", "CFG4", "TINY_BLOCK",
+    "gen_block_params", "gen_block_rank_inputs",
 ]
 
 _TID_X, _TID_DY = 1, 2
 _TID_U, _TID_WG, _TID_W1, _TID_W2 = 100, 101, 102, 103
+_TID_LN1G, _TID_LN1B, _TID_LN2G, _TID_LN2B, _TID_WQKV, _TID_WO = 104, 105, 106, 107, 108, 109
 
 
 @dataclass(frozen=True)
@@ -53,9 +55,46 @@ class LayerShape:
         return self.E // self.G
 
 
+@dataclass(frozen=True)
+class BlockShape:
+    """Per-rank shape of one GPT-MoE block (BASELINE.json configs[3]): T = n_seq * seq_len
+    tokens per rank, causal self-attention with n_heads heads, then the MoE layer."""
+    n_seq: int        # sequences per rank (the batch dimension B, P:L245)
+    seq_len: int      # S
+    d: int            # d_model
+    n_heads: int
+    f: int            # expert ffn width
+    E: int            # experts in total
+    G: int            # ranks
+    k: int            # top-k (1: Switch)
+    cf: float
+    n_chunks: int     # batch chunks (whole sequences; n_chunks divides n_seq)
+
+    @property
+    def T(self) -> int:
+        return self.n_seq * self.seq_len
+
+    @property
+    def E_l(self) -> int:
+        return self.E // self.G
+
+    @property
+    def head_dim(self) -> int:
+        return self.d // self.n_heads
+
+    def layer(self) -> LayerShape:
+        return LayerShape(T=self.T, d=self.d, f=self.f, E=self.E, G=self.G, k=self.k, cf=self.cf,
+                          n_chunks=self.n_chunks)
+
+
 # BASELINE.json configs[0] (64 tokens over 2 ranks) and configs[1] (GPT-MoE layer).
 TINY = LayerShape(T=32, d=16, f=32, E=4, G=2, k=2, cf=1.25, n_chunks=2)
 CFG2 = LayerShape(T=16384, d=1024, f=4096, E=8, G=8, k=2, cf=1.25, n_chunks=4)
+# configs[3]: full GPT-MoE block, d = 2048, 16 heads, 32 experts (4 per GPU), Switch top-1,
+# seq 1024 x 8 sequences per GPU; f = 4 d (SURVEY.md §8(d) "Config 4")
+CFG4 = BlockShape(n_seq=8, seq_len=1024, d=2048, n_heads=16, f=8192, E=32, G=8, k=1, cf=1.25, n_chunks=4)
+# a small block for the CPU oracle tests (head_dim 128 as on the GPU path)
+TINY_BLOCK = BlockShape(n_seq=4, seq_len=32, d=256, n_heads=2, f=256, E=4, G=2, k=1, cf=1.25, n_chunks=2)
 
 
 def round_to_bf16(a: np.ndarray) -> np.ndarray:
@@ -127,4 +166,28 @@ def gen_rank_inputs(base: int, rank: int, shape: LayerShape, beta: float = 0.5,
                wg=gen_gate(base, shape.d, shape.E, beta), w1=w1, w2=w2)
     if with_dy:
         out["dy"] = gen_dy(base, rank, shape.T, shape.d, dtype)
+    return out
+
+
+def gen_block_params(base: int, d: int, dtype: str = "bf16", std: float = 0.02) -> dict:
+    """Non-MoE parameters of a GPT-MoE block: LayerNorm gains / biases (fp32; gain 1 + 0.1 z,
+    bias 0.1 z), the fused QKV projection W_qkv [3d, d] (rows: q | k | v, head h at rows
+    h*hd .. h*hd+hd-1 of each) and the output projection W_o [d, d], both N(0, std^2)
+    (GPT-2 init scale), stored in `dtype`."""
+    def ln(tid):
+        return (1.0 + 0.1 * _rng(base + tid).standard_normal(d)).astype(np.float32)
+
+    def bias(tid):
+        return (0.1 * _rng(base + tid).standard_normal(d)).astype(np.float32)
+    w_qkv = _rng(base + _TID_WQKV).standard_normal((3 * d, d), dtype=np.float32) * std
+    w_o = _rng(base + _TID_WO).standard_normal((d, d), dtype=np.float32) * std
+    return dict(ln1_g=ln(_TID_LN1G), ln1_b=bias(_TID_LN1B), ln2_g=ln(_TID_LN2G), ln2_b=bias(_TID_LN2B),
+                w_qkv=_store(w_qkv, dtype), w_o=_store(w_o, dtype))
+
+
+def gen_block_rank_inputs(base: int, rank: int, shape: BlockShape, beta: float = 0.5,
+                          dtype: str = "bf16", with_dy: bool = True) -> dict:
+    """Everything rank `rank` passes to lancet_block_forward / backward (numpy arrays)."""
+    out = gen_rank_inputs(base, rank, shape.layer(), beta, dtype, with_dy)
+    out.update(gen_block_params(base, shape.d, dtype))
     return out
