@@ -277,6 +277,23 @@ lancet_status lancet_moe_forward(lancet_ctx* ctx, const void* x, const float* wg
                                  int32_t* expert_idx, int32_t* slot, float* combine_w,
                                  lancet_stream_t stream);
 
+/* Forward with Lancet's partition BEFORE the gate (fig:part_all; the MoE
+ * stage of lancet_block_forward, include/lancet_block.h): every chunk of the batch is gated on
+ * its own, with the capacity left over by the earlier chunks ("capacity passing", L255), its
+ * sizes exchanged (L525) and its rows pushed / computed / combined before later chunks are
+ * gated.  Same arguments and results as lancet_moe_forward -- routing, drops and y equal the
+ * unpartitioned layer (L256) -- plus resid [T][d] (optional): y = resid + MoE(x), the block's
+ * residual fused into the combine.  Needs the peer transport in push mode; the experts'
+ * receive buffers must hold E_l static regions of world * C(max_tokens) + 127 * n_chunks rows
+ * (LANCET_ERR_ARG otherwise; lancet_block_create_peer sizes them).  Batch Prioritized Routing
+ * needs the whole batch: LANCET_ERR_UNSUPPORTED (L270-L271).  lancet_moe_backward follows as
+ * usual.  Never blocks the host. */
+lancet_status lancet_moe_forward_partitioned(lancet_ctx* ctx, const void* x, const float* wg,
+                                             const void* w1, const void* w2, int32_t T, int32_t k,
+                                             double capacity_factor, int32_t n_chunks, const void* resid,
+                                             void* y, int32_t* expert_idx, int32_t* slot, float* combine_w,
+                                             lancet_stream_t stream);
+
 /* Backward of the last forward (collective when world > 1).  Gradient of <dy, y>:
  *   dy  [T][d]      dtype  in
  *   dx  [T][d]      dtype  out (overwritten)

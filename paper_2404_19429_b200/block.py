@@ -1,0 +1,142 @@
+"""Thin Python binding of the GPT-MoE block (include/lancet_block.h).
+
+Argument marshalling only: LN, the projections, attention and the MoE layer all run in
+liblancet_moe.so's kernels.  The block's MoE layer is a peer-transport push context
+(`Block.moe`, a borrowed lancet.Context: counts, timeline, flags, and the MoE backward)."""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import torch
+
+from . import lancet as L
+
+_BLOCK_SIG = {
+    "lancet_block_create_peer": None,
+    "lancet_block_moe": None,
+    "lancet_block_destroy": None,
+    "lancet_block_forward": None,
+    "lancet_block_debug_copy": None,
+}
+EXPORTS = list(_BLOCK_SIG)
+
+
+class _BlockConfig(ctypes.Structure):
+    _fields_ = [("moe", L._Config), ("n_heads", ctypes.c_int32), ("seq_len", ctypes.c_int32),
+                ("max_capacity_factor", ctypes.c_double)]
+
+
+_loaded = False
+
+
+def _lib():
+    global _loaded
+    lib = L.load_library()
+    if not _loaded:
+        P, I32 = ctypes.c_void_p, ctypes.c_int32
+        lib.lancet_block_create_peer.argtypes = [ctypes.POINTER(P), I32, I32, I32, ctypes.POINTER(_BlockConfig)]
+        lib.lancet_block_create_peer.restype = I32
+        lib.lancet_block_moe.argtypes = [P]
+        lib.lancet_block_moe.restype = P
+        lib.lancet_block_destroy.argtypes = [P]
+        lib.lancet_block_destroy.restype = I32
+        lib.lancet_block_forward.argtypes = [P] + [P] * 10 + [I32, I32, ctypes.c_double, I32, P, P]
+        lib.lancet_block_forward.restype = I32
+        lib.lancet_block_debug_copy.argtypes = [P, I32, P, ctypes.c_size_t]
+        lib.lancet_block_debug_copy.restype = I32
+        _loaded = True
+    return lib
+
+
+@dataclass
+class BlockConfig:
+    moe: L.LayerConfig
+    n_heads: int
+    seq_len: int
+    max_capacity_factor: float = 2.0
+
+    def _c(self) -> _BlockConfig:
+        return _BlockConfig(self.moe._c(), self.n_heads, self.seq_len, float(self.max_capacity_factor))
+
+
+PARAMS = ("ln1_g", "ln1_b", "w_qkv", "w_o", "ln2_g", "ln2_b", "wg", "w1", "w2")
+
+
+class Block:
+    """One rank's lancet_block (world 1: a one-rank peer group; world > 1: the blobs are
+    all-gathered over the torch process group `pg`)."""
+
+    def __init__(self, cfg: BlockConfig, world: int = 1, rank: int = 0, device: int | None = None, pg=None):
+        import torch.distributed as dist
+        lib = _lib()
+        self.cfg = cfg
+        self.world, self.rank = world, rank
+        self.device = torch.cuda.current_device() if device is None else device
+        self._p = ctypes.c_void_p()
+        ok = lib.lancet_block_create_peer(ctypes.byref(self._p), world, rank, self.device, ctypes.byref(cfg._c())) == 0
+        if world > 1:
+            flags = [None] * world
+            dist.all_gather_object(flags, bool(ok), group=pg)
+            ok = all(flags)
+        if not ok:
+            msg = lib.lancet_last_error(None)
+            self.close()
+            raise L.LancetError(6, f"block creation failed on some rank: {msg.decode() if msg else ''}")
+        moe = L.Context.__new__(L.Context)
+        moe.cfg, moe.world, moe.rank, moe.device = cfg.moe, world, rank, self.device
+        moe._p = ctypes.c_void_p(lib.lancet_block_moe(self._p))
+        moe._borrowed = True
+        moe.E_l = cfg.moe.n_experts // world
+        moe._last = None
+        self.moe = moe
+        nb = lib.lancet_peer_blob_bytes()
+        blob = ctypes.create_string_buffer(nb)
+        L._check(lib.lancet_peer_export(moe._p, blob), moe._p)
+        blobs = [bytes(blob.raw)]
+        if world > 1:
+            blobs = [None] * world
+            dist.all_gather_object(blobs, bytes(blob.raw), group=pg)
+        L._check(lib.lancet_peer_import(moe._p, ctypes.create_string_buffer(b"".join(blobs), nb * world)), moe._p)
+        self._last = None
+
+    def close(self):
+        if self._p:
+            _lib().lancet_block_destroy(self._p)
+            self._p = ctypes.c_void_p()
+            if hasattr(self, "moe"):
+                self.moe._p = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def forward(self, x, p: dict, k: int, capacity_factor: float, n_chunks: int, out=None, stream=None):
+        """out = h + MoE(LN2(h)), h = x + Attn(LN1(x)).  p: the PARAMS tensors (ln* fp32 [d],
+        w_qkv [3d][d], w_o [d][d] bf16, wg [d][E] fp32, w1 [E_l][f][d], w2 [E_l][d][f] bf16)."""
+        T = x.shape[0]
+        out = torch.empty_like(x) if out is None else out
+        st = _lib().lancet_block_forward(self._p, L._ptr(x), *[L._ptr(p[n]) for n in PARAMS], T, k,
+                                         float(capacity_factor), n_chunks, L._ptr(out), L._stream(stream))
+        L._check(st, self.moe._p)
+        self._last = (x, p)
+        self._k = k
+        self.moe._last = (None, p["wg"], p["w1"], p["w2"])     # the MoE layer's backward
+        self.moe._last_n = n_chunks
+        return out
+
+    def debug(self, which: str, T: int):
+        """An intermediate of the last forward as a torch CPU tensor: h, u, att, qkv, a1 (bf16),
+        lse (fp32 [H][T], log2 domain), idx / slot (int32 [T][k], the MoE layer's routing)."""
+        d = self.cfg.moe.d_model
+        k = self._k
+        shapes = {"h": (0, (T, d)), "u": (1, (T, d)), "att": (2, (T, d)), "qkv": (3, (T, 3 * d)),
+                  "a1": (4, (T, d)), "lse": (5, (self.cfg.n_heads, T)), "idx": (6, (T, k)), "slot": (7, (T, k))}
+        w, shape = shapes[which]
+        dt = {"lse": torch.float32, "idx": torch.int32, "slot": torch.int32}.get(which, torch.bfloat16)
+        t = torch.empty(shape, dtype=dt)
+        L._check(_lib().lancet_block_debug_copy(self._p, w, ctypes.c_void_p(t.data_ptr()),
+                                                t.numel() * t.element_size()), self.moe._p)
+        return t

@@ -1,0 +1,228 @@
+// block.cu -- C-ABI of the GPT-MoE block (include/lancet_block.h): the non-MoE part of the
+// block (LN1, fused q|k|v projection, causal attention, output projection, residual + LN2) and
+// Lancet's pre-MoE partition of it into the MoE layer's all-to-all pipeline.
+//
+// "if we partition non-MoE computations and integrate them into the computation-communication
+// pipeline, we can create additional opportunities to overlap operations with the all-to-all
+// communication" (fig:part_all).  Per chunk of whole sequences (the batch
+// dimension, L252; R20) the block's stream runs LN1 -> QKV GEMM -> attention -> O GEMM ->
+// residual + LN2 and hands the chunk's rows to the MoE layer, which gates them with the carried
+// capacity state (L255) and exchanges / computes / combines them on its own streams
+// (lancet::moe_forward_chunked) while the block's stream already works on the next chunk.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "../../include/lancet_block.h"
+#include "common.cuh"
+#include "context.h"
+#include "internal.h"
+#include "kernels.h"
+
+#define LANCET_API extern "C" __attribute__((visibility("default")))
+
+struct lancet_block {
+    lancet_ctx* moe = nullptr;
+    int world = 1, rank = 0, device = 0, d = 0, H = 0, S = 0, max_tokens = 0;
+    double cf_max = 0.0;
+    cudaStream_t s_pre = nullptr;
+    std::vector<void*> allocs;
+    void *a1 = nullptr, *qkv = nullptr, *att = nullptr, *o = nullptr, *h = nullptr, *u = nullptr;
+    float *mu1 = nullptr, *rs1 = nullptr, *mu2 = nullptr, *rs2 = nullptr, *lse = nullptr;
+    int* tok_tab = nullptr;     // [2][kMaxChunks]: rows | first row of each chunk (projection GEMMs)
+    int T_last = 0;
+};
+
+namespace {
+
+using namespace lancet;
+
+thread_local std::string g_block_err;
+
+lancet_status bfail(lancet_block* b, lancet_status st, const std::string& msg)
+{
+    g_block_err = msg;
+    return record_error(b ? b->moe : nullptr, st, msg);     // lancet_last_error(ctx or NULL)
+}
+
+#define BCK(call)                                                                                   \
+    do {                                                                                            \
+        cudaError_t e_ = (call);                                                                    \
+        if (e_ != cudaSuccess) return bfail(b, LANCET_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+__global__ void tok_tab_kernel(int* tab, int n, int Tc)
+{
+    pdl_wait();
+    const int c = threadIdx.x;
+    if (c < n) {
+        tab[c] = Tc;
+        tab[kMaxChunks + c] = c * Tc;
+    }
+}
+
+bool aligned(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+}  // namespace
+
+LANCET_API lancet_status lancet_block_create_peer(lancet_block** out, int32_t world, int32_t rank, int32_t dev,
+                                                  const lancet_block_config* cfg)
+{
+    if (!out || !cfg) return bfail(nullptr, LANCET_ERR_ARG, "out / cfg is NULL");
+    *out = nullptr;
+    const lancet_layer_config& m = cfg->moe;
+    if (m.dtype != LANCET_BF16) return bfail(nullptr, LANCET_ERR_UNSUPPORTED, "the block runs in bf16");
+    if (m.act == LANCET_ACT_IDENTITY_EXPERT) return bfail(nullptr, LANCET_ERR_UNSUPPORTED, "the block needs FFN experts");
+    if (cfg->n_heads <= 0 || m.d_model != cfg->n_heads * 128)
+        return bfail(nullptr, LANCET_ERR_UNSUPPORTED, "attention: d_model must be n_heads * 128 (head_dim 128)");
+    if (m.d_model > 4096) return bfail(nullptr, LANCET_ERR_UNSUPPORTED, "LayerNorm: d_model <= 4096");
+    if (cfg->seq_len <= 0 || cfg->seq_len % 128) return bfail(nullptr, LANCET_ERR_ARG, "seq_len must be a positive multiple of 128");
+    if (m.max_tokens % cfg->seq_len) return bfail(nullptr, LANCET_ERR_ARG, "max_tokens must be a multiple of seq_len");
+    if (!(cfg->max_capacity_factor > 0.0)) return bfail(nullptr, LANCET_ERR_ARG, "max_capacity_factor must be > 0");
+    if (world < 1 || rank < 0 || rank >= world || m.n_experts % world)
+        return bfail(nullptr, LANCET_ERR_ARG, "bad world / rank");
+    lancet_layer_config mc = m;
+    mc.flags |= LANCET_FLAG_PEER_PUSH;
+    auto* b = new lancet_block();
+    b->world = world; b->rank = rank; b->device = dev; b->d = m.d_model; b->H = cfg->n_heads; b->S = cfg->seq_len;
+    b->max_tokens = m.max_tokens; b->cf_max = cfg->max_capacity_factor;
+    // the experts' receive buffers hold every chunk group in place: E_l static regions of
+    // world * C(max_tokens, cf_max) rows + 127 pad rows per chunk (moe_forward_chunked)
+    const int E_l = m.n_experts / world;
+    const long Cb = capacity_rows(m.max_tokens, m.max_k, m.n_experts, cfg->max_capacity_factor);
+    const long min_rows = (long)E_l * round_up((int)std::min<long>((long)world * Cb + 127L * m.max_chunks, 1L << 28), kRowAlign);
+    lancet_status st = create_peer_ctx(&b->moe, world, rank, dev, &mc, min_rows);
+    if (st) {
+        g_block_err = lancet_last_error(nullptr);
+        delete b;
+        return st;
+    }
+    const size_t T = m.max_tokens, d = m.d_model;
+    auto al = [&](void** p, size_t bytes) -> bool {
+        if (cudaMalloc(p, bytes) != cudaSuccess) return false;
+        b->allocs.push_back(*p);
+        return true;
+    };
+    bool ok = al(&b->a1, T * d * 2) && al(&b->qkv, T * 3 * d * 2) && al(&b->att, T * d * 2) && al(&b->o, T * d * 2) &&
+              al(&b->h, T * d * 2) && al(&b->u, T * d * 2) && al((void**)&b->mu1, T * 4) && al((void**)&b->rs1, T * 4) &&
+              al((void**)&b->mu2, T * 4) && al((void**)&b->rs2, T * 4) && al((void**)&b->lse, T * 4 * cfg->n_heads) &&
+              al((void**)&b->tok_tab, sizeof(int) * 2 * kMaxChunks);
+    if (!ok || cudaStreamCreateWithFlags(&b->s_pre, cudaStreamNonBlocking) != cudaSuccess) {
+        lancet_block_destroy(b);
+        return bfail(nullptr, LANCET_ERR_NOMEM, "block workspace allocation failed");
+    }
+    *out = b;
+    return LANCET_OK;
+}
+
+LANCET_API lancet_ctx* lancet_block_moe(lancet_block* b) { return b ? b->moe : nullptr; }
+
+LANCET_API lancet_status lancet_block_destroy(lancet_block* b)
+{
+    if (!b) return LANCET_OK;
+    lancet_status st = LANCET_OK;
+    if (b->moe) st = lancet_destroy(b->moe);
+    cudaSetDevice(b->device);
+    for (void* p : b->allocs) cudaFree(p);
+    if (b->s_pre) cudaStreamDestroy(b->s_pre);
+    delete b;
+    return st;
+}
+
+LANCET_API lancet_status lancet_block_forward(lancet_block* b, const void* x, const float* ln1_g, const float* ln1_b,
+                                              const void* w_qkv, const void* w_o, const float* ln2_g,
+                                              const float* ln2_b, const float* wg, const void* w1, const void* w2,
+                                              int32_t T, int32_t k, double cf, int32_t n, void* out,
+                                              lancet_stream_t stream_)
+{
+    if (!b) return bfail(nullptr, LANCET_ERR_ARG, "block is NULL");
+    lancet_ctx* c = b->moe;
+    lancet_status st = ctx_ready(c);
+    if (st) return st;
+    const void* ptrs[] = {x, ln1_g, ln1_b, w_qkv, w_o, ln2_g, ln2_b, wg, w1, w2, out};
+    for (const void* p : ptrs) {
+        if (!p) return bfail(b, LANCET_ERR_ARG, "null required pointer");
+        if (!aligned(p)) return bfail(b, LANCET_ERR_ARG, "every tensor must be 16-byte aligned (vector loads, TMA)");
+    }
+    if (T < b->S || T > b->max_tokens || T % b->S) return bfail(b, LANCET_ERR_ARG, "T must be n_seq * seq_len <= max_tokens");
+    const int n_seq = T / b->S;
+    if (n < 1 || n > c->cfg.max_chunks || n_seq % n) return bfail(b, LANCET_ERR_ARG, "n_chunks must divide the sequences (R20)");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream_);
+    const int d = b->d, Tc = T / n, seq_c = n_seq / n;
+    std::vector<int> bounds(n + 1);
+    for (int ch = 0; ch <= n; ++ch) bounds[ch] = ch * Tc;
+    // the projection GEMMs' group tables (on the caller's stream: every internal stream forks
+    // from it after this)
+    launch_k(tok_tab_kernel, 1, 64, 0, s, b->tok_tab, n, Tc);
+    BCK(cudaGetLastError());
+    const size_t row = (size_t)d * 2;
+    int extra = 1;
+    ChunkedInput in;
+    in.n = n;
+    in.bounds = bounds.data();
+    in.resid = b->h;
+    in.s_pre = b->s_pre;
+    in.cf_max = b->cf_max;
+    in.produce = [&](int ch, int t0, int t1, cudaStream_t sp) -> lancet_status {
+        const int rows = t1 - t0;
+        const int* tr = b->tok_tab + ch;
+        const int* to = b->tok_tab + kMaxChunks + ch;
+        const char* xs = (const char*)x + t0 * row;
+        size_t op = op_begin(c, "ln1", 0, ch, sp);
+        int r = launch_layer_norm(xs, nullptr, nullptr, ln1_g, ln1_b, (char*)b->a1 + t0 * row, b->mu1 + t0, b->rs1 + t0,
+                                  rows, d, sp);
+        op_end(c, op, sp);
+        if (r < 0) return bfail(b, LANCET_ERR_UNSUPPORTED, "LayerNorm shape");
+        op = op_begin(c, "qkv_proj", 0, ch, sp);
+        lancet_status e = dense_gemm(c, b->a1, T, w_qkv, 3 * d, d, b->qkv, T, tr, to, 1, Tc, sp, &extra);
+        op_end(c, op, sp);
+        if (e) return e;
+        op = op_begin(c, "attention", 0, ch, sp);
+        r = launch_attention_fwd(b->qkv, b->att, b->lse, t0, seq_c, b->S, b->H, d, T, sp);
+        op_end(c, op, sp);
+        if (r < 0) return bfail(b, LANCET_ERR_UNSUPPORTED, "attention: unsupported shape or tensor-map encoding failed");
+        op = op_begin(c, "o_proj", 0, ch, sp);
+        e = dense_gemm(c, b->att, T, w_o, d, d, b->o, T, tr, to, 1, Tc, sp, &extra);
+        op_end(c, op, sp);
+        if (e) return e;
+        op = op_begin(c, "ln2", 0, ch, sp);
+        r = launch_layer_norm(xs, (const char*)b->o + t0 * row, (char*)b->h + t0 * row, ln2_g, ln2_b,
+                              (char*)b->u + t0 * row, b->mu2 + t0, b->rs2 + t0, rows, d, sp);
+        op_end(c, op, sp);
+        if (r < 0) return bfail(b, LANCET_ERR_UNSUPPORTED, "LayerNorm shape");
+        extra += 3;
+        cudaError_t ce = cudaGetLastError();
+        if (ce != cudaSuccess) return bfail(b, LANCET_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(ce));
+        return LANCET_OK;
+    };
+    st = moe_forward_chunked(c, b->u, wg, w1, w2, T, k, cf, out, in, s);
+    if (st) return st;
+    c->launches_fwd += extra;
+    b->T_last = T;
+    return LANCET_OK;
+}
+
+LANCET_API lancet_status lancet_block_debug_copy(lancet_block* b, int32_t which, void* host, size_t bytes)
+{
+    if (!b || !host) return bfail(b, LANCET_ERR_ARG, "null argument");
+    const size_t T = b->T_last, d = b->d;
+    const void* src = nullptr;
+    size_t need = 0;
+    switch (which) {
+    case 0: src = b->h; need = T * d * 2; break;
+    case 1: src = b->u; need = T * d * 2; break;
+    case 2: src = b->att; need = T * d * 2; break;
+    case 3: src = b->qkv; need = T * 3 * d * 2; break;
+    case 4: src = b->a1; need = T * d * 2; break;
+    case 5: src = b->lse; need = (size_t)b->H * T * 4; break;    // [H][T] of the last forward
+    case 6: src = b->moe->idx; need = T * b->moe->k * 4; break;   // the MoE layer's routing
+    case 7: src = b->moe->slot; need = T * b->moe->k * 4; break;
+    default: return bfail(b, LANCET_ERR_ARG, "bad `which`");
+    }
+    if (bytes != need) return bfail(b, LANCET_ERR_ARG, "bytes must match the buffer");
+    if (cudaDeviceSynchronize() != cudaSuccess) return bfail(b, LANCET_ERR_CUDA, "synchronize");
+    if (cudaMemcpy(host, src, need, cudaMemcpyDeviceToHost) != cudaSuccess) return bfail(b, LANCET_ERR_CUDA, "copy");
+    return LANCET_OK;
+}

@@ -87,6 +87,7 @@ struct lancet_ctx {
 
     // streams / events
     cudaStream_t s_comp = nullptr, s_comm = nullptr;
+    cudaStream_t s_gate = nullptr;       // partitioned forward: the chunks' gates (producer stream)
     cudaStream_t s_comp2 = nullptr;      // push pipeline: odd chunks' fc2 / dfc1 launches, so one
                                          // chunk's tail wave overlaps the next chunk's GEMM
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_counts = nullptr, ev_tl_base = nullptr;
@@ -110,6 +111,8 @@ struct lancet_ctx {
     float* wgT = nullptr;      // [E][d] transposed gate (backward, coalesced dx gate term)
     int* prow = nullptr;       // [T][k] packed source row of each choice (-1 dropped), from K5
     int* counts_dev = nullptr;   // [E][n] send counts, then [G][E_l][n] recv counts
+    int* carry = nullptr;        // [max_chunks + 1][E] capacity state carried across separately
+                                 // gated chunks (block mode): pairs routed to e before chunk c
     int* grp_dev = nullptr;      // expert-side group table: rows[n_groups] | off[n_groups]
 
     // expert-side workspace (rows_exp rows; == rows_src when world == 1)

@@ -144,7 +144,7 @@ combine_kernel(const Elt* __restrict__ comb, const int* __restrict__ idx,
                const int* __restrict__ slot, const float* __restrict__ wts,
                const int* __restrict__ send_off, int t0, int t1, int k, int d,
                Elt* __restrict__ y, const int* __restrict__ src_base, const char* const* __restrict__ src_tab,
-               int E_l)
+               int E_l, const Elt* __restrict__ resid)
 {
     pdl_wait();   // programmatic dependent launch: predecessor's writes visible
     constexpr int V = Vec16<Elt>::N;
@@ -180,8 +180,12 @@ combine_kernel(const Elt* __restrict__ comb, const int* __restrict__ idx,
         for (int u = 0; u < U; ++u) {
             if (v0 + 32 * u >= nvec) break;
             float acc[V];
+            if (resid) {   // the block's residual: y = h + sum_j w_j o_j (the chain starts at h)
+                unpack16<Elt>(ld_nc_v4(reinterpret_cast<const uint4*>(resid + (size_t)t * d) + v0 + 32 * u), acc);
+            } else {
 #pragma unroll
-            for (int q = 0; q < V; ++q) acc[q] = 0.f;
+                for (int q = 0; q < V; ++q) acc[q] = 0.f;
+            }
 #pragma unroll
             for (int j = 0; j < KK; ++j) {
                 if (rows[j] >= 0) {
@@ -381,18 +385,19 @@ int launch_permute_push(const DispatchArgs& a, const void* x, int t0, int t1, in
 }
 
 int launch_combine(const DispatchArgs& a, const void* comb, void* y, int t0, int t1, bool is_bf16,
-                   cudaStream_t s, const int* src_base, const char* const* src_tab, int E_l)
+                   cudaStream_t s, const int* src_base, const char* const* src_tab, int E_l, const void* resid)
 {
     if (t1 <= t0) return 0;
     const int grid = ceil_div(t1 - t0, kWarpsPerBlock);
     LANCET_DISPATCH_K(a.k, {
         if (is_bf16)
             launch_k(combine_kernel<bf16, KK>, grid, 256, 0, s, (const bf16*)comb, a.idx, a.slot, a.w, a.send_off,
-                                                         t0, t1, a.k, a.d, (bf16*)y, src_base, src_tab, E_l);
+                                                         t0, t1, a.k, a.d, (bf16*)y, src_base, src_tab, E_l,
+                                                         (const bf16*)resid);
         else
             launch_k(combine_kernel<float, KK>, grid, 256, 0, s, (const float*)comb, a.idx, a.slot, a.w,
                                                           a.send_off, t0, t1, a.k, a.d, (float*)y, src_base, src_tab,
-                                                          E_l);
+                                                          E_l, (const float*)resid);
     });
     return 1;
 }

@@ -53,6 +53,16 @@ struct RouteArgs {
     // Random gate (R18; random != 0): SplitMix64 draws instead of K1, x and Wg unused
     int random;
     unsigned long long seed;
+    int t_base = 0;        // global index of token 0 of this launch (Random gate counters)
+    // Capacity passing across separately gated chunks (the block's pre-MoE partition, PAPER.md
+    // L255; carry_in != NULL): the launch covers one chunk `carry_chunk` of `carry_n`; pair
+    // positions continue from carry_in[e] (pairs routed to e by earlier chunks), block 0 writes
+    // carry_out[e] = carry_in[e] + this chunk's pairs, S[e][c], S[e][c+1] and the chunk's
+    // admitted counts carry_counts[e * carry_n + c]; send_rows / send_off are not written.
+    const int* carry_in = nullptr;
+    int* carry_out = nullptr;
+    int carry_chunk = 0, carry_n = 1;
+    int* carry_counts = nullptr;
 };
 // Enqueues memset(hist) + K1 + K2 (K2 = three kernels under BPR).  Returns the number of kernels
 // launched.
@@ -71,9 +81,10 @@ int launch_permute_push(const DispatchArgs& a, const void* x, int t0, int t1, in
                         char* const* xe_ptrs, bool is_bf16, cudaStream_t s);
 // src_base / src_tab (fused combine exchange, optional): o rows read from src_tab[e / E_l] at
 // rows src_base[e] + slot (the owners' expert outputs over peer memory) instead of comb
+// resid (optional, [T][d]): y = resid + sum_j w_j o_j, the block's residual add (fp32 chain from resid)
 int launch_combine(const DispatchArgs& a, const void* comb, void* y, int t0, int t1, bool is_bf16,
                    cudaStream_t s, const int* src_base = nullptr, const char* const* src_tab = nullptr,
-                   int E_l = 1);
+                   int E_l = 1, const void* resid = nullptr);
 // K5: also writes dlogit [T][E] (softmax Jacobian) and prow [T][k] (packed row or -1)
 // push_base / push_dst (peer push, optional): the dO rows go to push_dst[e / E_l] at rows
 // push_base[e] + slot instead of dcomb (backward all-to-all #1 fused into K5)
@@ -103,6 +114,17 @@ int launch_gate_bwd_fused(const DispatchArgs& a, const void* dxe, const int* pro
 // zero rows [off_g + rows_g, off_g + round_up(rows_g, 128)) of a packed buffer
 int launch_zero_pads(void* buf, int row_elems, const int* grp_off, const int* grp_rows,
                      int n_groups, int elt_bytes, cudaStream_t s);
+
+// ---- the GPT-MoE block's non-MoE kernels (attention.cu) ----------------------------------
+// Causal self-attention, head_dim 128, S % 128 == 0, d = H * 128: qkv [T_all][3d] (q | k | v),
+// the n_seq sequences starting at token tok0; att [T_all][d] and lse [H][T_all] (log2 domain)
+// written for those tokens.  Returns -1 if unsupported or the tensor maps fail.
+int launch_attention_fwd(const void* qkv, void* att, float* lse, int tok0, int n_seq, int S, int H, int d,
+                         int T_all, cudaStream_t s);
+// LayerNorm over rows of d (d % 256 == 0, d <= 4096): y = (x - mean) rstd g + b, bf16; with
+// resid != NULL the row is first h = bf16(a + resid), stored to hout.  mean / rstd [rows] out.
+int launch_layer_norm(const void* a, const void* resid, void* hout, const float* g, const float* b, void* y,
+                      float* mean, float* rstd, int rows, int d, cudaStream_t s);
 
 // ---- grouped GEMMs (gemm_simt.cu, gemm_tc.cu) --------------------------------------------
 enum GemmMode { GEMM_M_GROUPED = 0, GEMM_K_GROUPED = 1 };

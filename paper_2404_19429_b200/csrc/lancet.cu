@@ -26,6 +26,7 @@
 #include "context.h"
 #include "kernels.h"
 #include "peer.h"
+#include "internal.h"
 
 #define LANCET_API extern "C" __attribute__((visibility("default")))
 
@@ -369,6 +370,7 @@ lancet_status create_common(lancet_ctx* c, int world, int rank, int device, cons
     c->num_sms = prop.multiProcessorCount;
     CK(cudaStreamCreateWithFlags(&c->s_comp, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&c->s_comp2, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->s_gate, cudaStreamNonBlocking));
     int lo, hi;
     CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     CK(cudaStreamCreateWithPriority(&c->s_comm, cudaStreamNonBlocking, hi));
@@ -407,6 +409,7 @@ lancet_status create_common(lancet_ctx* c, int world, int rank, int device, cons
     AL(c->dwg_partial, sizeof(float) * dwg_partial_floats(T, d, E));
     AL(c->wgT, sizeof(float) * (size_t)d * E);
     AL(c->counts_dev, sizeof(int) * 2 * (size_t)E * kMaxChunks);
+    AL(c->carry, sizeof(int) * (size_t)E * (kMaxChunks + 1));
     AL(c->grp_dev, sizeof(int) * (2 * (size_t)c->E_l * kMaxChunks + 2 * (size_t)c->E_l));   // + merged dW table
     const size_t rs = (size_t)c->rows_src * d * c->elt;
     AL(c->xs, rs);
@@ -432,6 +435,8 @@ lancet_status create_common(lancet_ctx* c, int world, int rank, int device, cons
 #undef AL
     CK(cudaMemset(c->xs, 0, rs));
     CK(cudaMemset(c->dcomb, 0, rs));
+    CK(cudaMemset(c->send_off, 0, sizeof(int) * E));     // block mode never writes them; the
+    CK(cudaMemset(c->send_rows, 0, sizeof(int) * E));    // push kernels' row arithmetic cancels them
     CK(cudaDeviceSynchronize());
     return LANCET_OK;
 }
@@ -910,6 +915,195 @@ lancet_status backward_push(lancet_ctx* c, const DispatchArgs& da, const void* d
 }
 }  // namespace
 
+
+// =========================================================================================
+// Block mode (internal.h): the MoE forward whose input arrives chunk by chunk
+// =========================================================================================
+namespace lancet {
+
+lancet_status record_error(lancet_ctx* c, lancet_status st, const std::string& msg) { return fail(c, st, msg); }
+lancet_status ctx_ready(lancet_ctx* c) { return check_ready(c); }
+int capacity_rows(int T, int k, int E, double cf) { return capacity_of(T, k, E, cf); }
+
+size_t op_begin(lancet_ctx* c, const char* name, int lane, int chunk, cudaStream_t s)
+{
+    OpScope op(c, name, lane, chunk, s);
+    const size_t h = op.i;
+    op.i = (size_t)-1;          // the end event is recorded by op_end
+    return h;
+}
+
+void op_end(lancet_ctx* c, size_t h, cudaStream_t s)
+{
+    if (h != (size_t)-1) cudaEventRecord(c->ops[h].end, s);
+}
+
+lancet_status dense_gemm(lancet_ctx* c, const void* A, long a_rows, const void* B, int N, int K, void* C,
+                         long c_rows, const int* grp_rows, const int* grp_off, int n_groups, int max_rows,
+                         cudaStream_t s, int* launches)
+{
+    GemmArgs a{};
+    a.mode = GEMM_M_GROUPED; a.n_groups = n_groups; a.gpw = n_groups; a.n_weights = 1;
+    a.grp_rows = grp_rows; a.grp_off = grp_off; a.max_rows = max_rows; a.act = 0;
+    a.A = A; a.lda = K; a.a_rows = a_rows; a.a_mn = false;
+    a.B = B; a.ldb = K; a.b_group_stride = 0; a.b_rows = N; a.b_mn = false;
+    a.C = C; a.C2 = nullptr; a.ldc = N; a.c_rows = c_rows; a.N = N; a.K = K; a.epi = EPI_STORE;
+    return run_gemm(c, a, s, launches);
+}
+
+// Forward of the MoE layer in block mode (push transport; LANCET_FLAG_PEER_PUSH).  Per chunk
+// ch, stage by stage (S1 with the non-MoE part in the pipeline, fig:part_all):
+//   producer stream:  produce(ch) [the block's LN1 / attention / projections / LN2], then the
+//                     gate of chunk ch with the carried capacity state (K1 + K2 in carry mode);
+//   comm stream:      size exchange of chunk ch (column ch of the count matrix), the
+//                     chunk's plan (static regions: final before later chunks are gated), pad
+//                     zeroing, and the fused permute + dispatch push of chunk ch;
+//   compute stream:   once every rank's rows of chunk ch landed: fc1, fc2 of chunk ch;
+//   combine stream:   once every owner's outputs of chunk ch are stored: the fused combine
+//                     (+ residual) of chunk ch.
+// The producer never waits for the exchange: chunk ch+1's attention runs while chunk ch is
+// exchanged and its experts run.  The resulting routing, plan tables, buffers and flags are
+// those of forward_push, so lancet_moe_backward works unchanged.
+lancet_status moe_forward_chunked(lancet_ctx* c, const void* x, const float* wg, const void* w1, const void* w2,
+                                  int T, int k, double cf, void* y, const ChunkedInput& in, cudaStream_t s)
+{
+    lancet_status st = check_ready(c);
+    if (st) return st;
+    const int E = c->cfg.n_experts, d = c->cfg.d_model, E_l = c->E_l, n = in.n;
+    if (!c->ep || !c->push || !c->peer) return fail(c, LANCET_ERR_UNSUPPORTED, "block mode needs the peer transport in push mode");
+    if (!c->peer_ready) return fail(c, LANCET_ERR_STATE, "peer transport: lancet_peer_import not called");
+    if (!c->bf16 || c->cfg.act == LANCET_ACT_IDENTITY_EXPERT) return fail(c, LANCET_ERR_UNSUPPORTED, "block mode: bf16 experts only");
+    if (c->cfg.flags & LANCET_FLAG_GATE_BPR)
+        return fail(c, LANCET_ERR_UNSUPPORTED, "Batch Prioritized Routing needs the whole batch: no partition before the gate (PAPER.md L270-L271)");
+    if (T < 1 || T > c->cfg.max_tokens) return fail(c, LANCET_ERR_ARG, "T must be in [1, max_tokens]");
+    if (k < 1 || k > c->cfg.max_k || k > E) return fail(c, LANCET_ERR_ARG, "k must be in [1, min(E, max_k)]");
+    if (!(cf > 0.0) || !std::isfinite(cf) || cf > in.cf_max) return fail(c, LANCET_ERR_ARG, "capacity_factor must be in (0, max_capacity_factor]");
+    if (n < 1 || n > c->cfg.max_chunks || in.bounds[0] != 0 || in.bounds[n] != T)
+        return fail(c, LANCET_ERR_ARG, "bad chunk bounds");
+    for (int ch = 0; ch < n; ++ch)
+        if (in.bounds[ch + 1] - in.bounds[ch] != chunk_start(T, n, ch + 1) - chunk_start(T, n, ch))
+            return fail(c, LANCET_ERR_ARG, "block chunks must be the layer's chunks (R9)");
+    if (c->dw_pending) return fail(c, LANCET_ERR_STATE, "deferred dW GEMMs of the last backward were never enqueued");
+    // static receive regions per local expert: every source admits <= C(max_tokens) rows of an
+    // expert over all chunks, plus < 128 pad rows per chunk group
+    const int Cb = capacity_of(c->cfg.max_tokens, k, E, cf);
+    const long region = round_up((int)std::min<long>((long)c->world * Cb + 127L * n, 1L << 28), kRowAlign);
+    if ((long)E_l * region > c->peer->rows_cap)
+        return fail(c, LANCET_ERR_ARG, "block mode: the expert-side buffers hold " + std::to_string(c->peer->rows_cap) +
+                                           " rows, the static regions need " + std::to_string((long)E_l * region));
+    lancet::g_pdl = (c->cfg.flags & LANCET_FLAG_NO_PDL) == 0;
+    c->have_fwd = false;
+    c->x = x; c->wg = wg; c->w1 = w1; c->w2 = w2;
+    c->T = T; c->k = k; c->n = n; c->cf = cf;
+    c->C = capacity_of(T, k, E, cf);
+    c->launches_fwd = 0;
+    int& L = c->launches_fwd;
+    if (!c->tl_accumulate) {
+        c->ops.clear();
+        c->tl_used = 0;
+        if (c->cfg.flags & LANCET_FLAG_TIMELINE) CK(cudaEventRecord(c->ev_tl_base, s));
+    }
+    lancet::PeerLinks* pr = c->peer;
+    const bool serial = c->cfg.flags & LANCET_FLAG_SERIAL;
+    const bool nocomm = c->cfg.flags & LANCET_FLAG_NO_COMM;
+    cudaStream_t sp = serial ? c->s_comp : in.s_pre;
+    cudaStream_t sm = serial ? c->s_comp : c->s_comm;
+    cudaStream_t sc = c->s_comp;
+    cudaStream_t sb = serial ? c->s_comp : c->s_comp2;
+    size_t ev_i = 0;
+    auto next_ev = [&]() { return c->ev_pool[ev_i++]; };
+    CK(cudaEventRecord(c->ev_fork, s));
+    for (cudaStream_t q : {sp, sm, sc, sb}) CK(cudaStreamWaitEvent(q, c->ev_fork, 0));
+    if (c->out_consume_pending) {
+        DEV(dev_signal(c, 1, PK_OUT, 0, sc));
+        c->out_consume_pending = false;
+    }
+    ++pr->seq;
+    DEV(dev_seq_bump(c, sc));
+    DEV(dev_signal(c, 0, PK_XEFREE, 0, sc));    // this rank's receive buffer is free for the step
+    int* carry = c->carry;
+    CK(cudaMemsetAsync(carry, 0, sizeof(int) * E, sc));
+    cudaEvent_t ev_start = next_ev();
+    CK(cudaEventRecord(ev_start, sc));
+    for (cudaStream_t q : {sp, sm, sb}) CK(cudaStreamWaitEvent(q, ev_start, 0));
+
+    RouteArgs ra{};
+    ra.wg = wg; ra.d = d; ra.E = E; ra.k = k; ra.C = c->C; ra.n_chunks = 1;
+    ra.renorm = (c->cfg.flags & LANCET_FLAG_RENORMALIZE) ? 1 : 0;
+    ra.hist = c->hist; ra.S = c->S; ra.send_rows = c->send_rows; ra.send_off = c->send_off;
+    ra.random = (c->cfg.flags & LANCET_FLAG_GATE_RANDOM) ? 1 : 0;
+    ra.seed = c->gate_seed;
+    ra.carry_n = n; ra.carry_counts = c->counts_dev;
+    DispatchArgs da{T, k, d, E, c->idx, c->slot, c->w, c->send_off, c->send_rows};
+    int* d_grp_rows = c->grp_dev;
+    int* d_grp_off = c->grp_dev + n * E_l;
+    const int mr = push_group_rows_bound(c);
+    const size_t xrow = (size_t)d * c->elt;
+    for (int ch = 0; ch < n; ++ch) {
+        const int t0 = in.bounds[ch], t1 = in.bounds[ch + 1];
+        // ---- producer: the chunk's MoE input, then its gate with the carried capacity state
+        st = in.produce(ch, t0, t1, sp);
+        if (st) return st;
+        ra.x = (const char*)x + (size_t)t0 * xrow;
+        ra.T = t1 - t0; ra.t_base = t0;
+        ra.logits = c->logits + (size_t)t0 * E; ra.idx = c->idx + (size_t)t0 * k; ra.w = c->w + (size_t)t0 * k;
+        ra.slot = c->slot + (size_t)t0 * k;
+        ra.carry_in = carry + (size_t)ch * E; ra.carry_out = carry + (size_t)(ch + 1) * E; ra.carry_chunk = ch;
+        { OpScope op(c, "gate", 0, ch, sp); L += launch_routing(ra, c->bf16, sp); }
+        CHECK_LAUNCH();
+        cudaEvent_t ev_route = next_ev();
+        CK(cudaEventRecord(ev_route, sp));
+        // ---- comm: sizes of chunk ch, its plan, the fused permute + dispatch push
+        CK(cudaStreamWaitEvent(sm, ev_route, 0));
+        {
+            OpScope op(c, "a2a_counts", 1, ch, sm);
+            DEV(dev_counts_chunk(c, c->counts_dev, n, ch, sm));
+            L += 2;
+        }
+        DEV(dev_plan_chunk(c, n, ch, (int)region, sm));
+        ++L;
+        L += launch_zero_pads(c->xe, d, d_grp_off + ch * E_l, d_grp_rows + ch * E_l, E_l, (int)c->elt, sm);
+        CHECK_LAUNCH();
+        cudaEvent_t ev_plan = next_ev();
+        CK(cudaEventRecord(ev_plan, sm));
+        if (ch == 0) DEV(dev_wait(c, 0, PK_XEFREE, 0, TGT_STEP, sm));
+        {
+            OpScope op(c, "a2a_dispatch_push", 1, ch, sm);
+            if (!nocomm)
+                L += launch_permute_push(da, x, t0, t1, E_l, pr->d_push_base + (size_t)ch * E, pr->d_xe, c->bf16, sm);
+        }
+        CHECK_LAUNCH();
+        DEV(dev_signal(c, 0, PK_PUSH, ch, sm));
+        // ---- compute: the experts of chunk ch once every rank's rows landed
+        CK(cudaStreamWaitEvent(sc, ev_plan, 0));
+        DEV(dev_wait(c, 0, PK_PUSH, ch, TGT_STEP, sc));
+        if (ch == 0) DEV(dev_wait(c, 1, PK_OUT, 0, TGT_PREV, sc));   // peers done with last step's outputs
+        st = expert_forward(c, d_grp_rows + ch * E_l, d_grp_off + ch * E_l, E_l, mr, sc, ch, &L);
+        if (st) return st;
+        DEV(dev_signal(c, 0, PK_OUT, ch, sc));
+        // ---- combine: chunk ch's tokens gather their outputs from the owners (+ residual)
+        CK(cudaStreamWaitEvent(sb, ev_plan, 0));
+        DEV(dev_wait(c, 0, PK_OUT, ch, TGT_STEP, sb));
+        {
+            OpScope op(c, "a2a_combine_fused", 1, ch, sb);
+            L += launch_combine(da, c->comb, y, t0, t1, c->bf16, sb, nocomm ? nullptr : pr->d_push_base + (size_t)ch * E,
+                                pr->d_outsrc, E_l, in.resid);
+        }
+        CHECK_LAUNCH();
+    }
+    c->out_consume_pending = true;
+    c->n_groups = n * E_l;
+    for (cudaStream_t q : {sp, sm, sc, sb}) {
+        cudaEvent_t e = next_ev();
+        CK(cudaEventRecord(e, q));
+        CK(cudaStreamWaitEvent(s, e, 0));
+    }
+    c->have_fwd = true;
+    return LANCET_OK;
+}
+
+}  // namespace lancet
+
 // =========================================================================================
 // C-ABI
 // =========================================================================================
@@ -1003,6 +1197,12 @@ LANCET_API lancet_status lancet_create_local(lancet_ctx** out, lancet_local_grou
 LANCET_API lancet_status lancet_create_peer(lancet_ctx** out, int32_t world, int32_t rank,
                                             int32_t cuda_device, const lancet_layer_config* cfg)
 {
+    return lancet::create_peer_ctx(out, world, rank, cuda_device, cfg, 0);
+}
+
+lancet_status lancet::create_peer_ctx(lancet_ctx** out, int world, int rank, int cuda_device,
+                                      const lancet_layer_config* cfg, long min_rows)
+{
     if (!out) return fail(nullptr, LANCET_ERR_ARG, "out is NULL");
     *out = nullptr;
     if (world < 1 || rank < 0 || rank >= world) return fail(nullptr, LANCET_ERR_ARG, "bad world/rank");
@@ -1022,9 +1222,10 @@ LANCET_API lancet_status lancet_create_peer(lancet_ctx** out, int32_t world, int
     if (!st) {
         // the expert-side buffers are mapped by the peers: allocate them at their bound once
         // (every source sends at most max_tokens * max_k rows; + 128-row padding per group)
-        const long rows = (long)world * cfg->max_tokens * cfg->max_k +
-                          (long)c->E_l * cfg->max_chunks * kRowAlign;
-        if (rows > (1L << 30)) st = fail(c, LANCET_ERR_ARG, "expert-side row bound too large");
+        const long rows = std::max(min_rows, (long)world * cfg->max_tokens * cfg->max_k +
+                                                 (long)c->E_l * cfg->max_chunks * kRowAlign);
+        if (rows > (1L << 30) || (c->push && rows >= (1L << kPeerRowBits)))
+            st = fail(c, LANCET_ERR_ARG, "expert-side row bound too large");
         else st = ensure_expert_rows(c, (int)rows);
     }
     if (!st) {
@@ -1032,7 +1233,7 @@ LANCET_API lancet_status lancet_create_peer(lancet_ctx** out, int32_t world, int
         if (peer_init(c, err)) st = fail(c, LANCET_ERR_CUDA, err);
         else {
             unsigned long long h = cfg_hash(*cfg);
-            for (long v : {(long)cfg->max_tokens, (long)(cfg->flags & LANCET_FLAG_PEER_PUSH), (long)world}) {
+            for (long v : {(long)cfg->max_tokens, (long)(cfg->flags & LANCET_FLAG_PEER_PUSH), (long)world, min_rows}) {
                 h ^= (unsigned long long)v;
                 h *= 1099511628211ull;
             }
@@ -1096,6 +1297,7 @@ LANCET_API lancet_status lancet_destroy(lancet_ctx* c)
     if (c->ev_tl_base) cudaEventDestroy(c->ev_tl_base);
     if (c->s_comp) cudaStreamDestroy(c->s_comp);
     if (c->s_comp2) cudaStreamDestroy(c->s_comp2);
+    if (c->s_gate) cudaStreamDestroy(c->s_gate);
     if (c->s_comm) cudaStreamDestroy(c->s_comm);
     delete c;
     return LANCET_OK;
@@ -1410,6 +1612,37 @@ LANCET_API lancet_status lancet_moe_forward(lancet_ctx* c, const void* x, const 
     if (slot_out) CK(cudaMemcpyAsync(slot_out, c->slot, tk * sizeof(int), cudaMemcpyDeviceToDevice, s));
     if (combine_w) CK(cudaMemcpyAsync(combine_w, c->w, tk * sizeof(float), cudaMemcpyDeviceToDevice, s));
     c->have_fwd = true;
+    return LANCET_OK;
+}
+
+LANCET_API lancet_status lancet_moe_forward_partitioned(lancet_ctx* c, const void* x, const float* wg,
+                                                        const void* w1, const void* w2, int32_t T, int32_t k,
+                                                        double cf, int32_t n, const void* resid, void* y,
+                                                        int32_t* expert_idx, int32_t* slot_out, float* combine_w,
+                                                        lancet_stream_t stream_)
+{
+    lancet_status st = check_ready(c);
+    if (st) return st;
+    if (!x || !wg || !w1 || !w2 || !y) return fail(c, LANCET_ERR_ARG, "null required pointer");
+    if (!aligned16(x) || !aligned16(wg) || !aligned16(y) || !aligned16(w1) || !aligned16(w2) || (resid && !aligned16(resid)))
+        return fail(c, LANCET_ERR_ARG, "x, wg, w1, w2, resid and y must be 16-byte aligned (vector loads, TMA)");
+    if (n < 1 || n > std::min<int>(T, c->cfg.max_chunks)) return fail(c, LANCET_ERR_ARG, "n_chunks must be in [1, min(T, max_chunks)]");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream_);
+    std::vector<int> bounds(n + 1);
+    for (int ch = 0; ch <= n; ++ch) bounds[ch] = chunk_start(T, n, ch);
+    lancet::ChunkedInput in;
+    in.n = n;
+    in.bounds = bounds.data();
+    in.resid = resid;
+    in.s_pre = c->s_gate;      // the input is resident: the producer stream only gates
+    in.cf_max = cf;
+    in.produce = [](int, int, int, cudaStream_t) { return LANCET_OK; };
+    st = lancet::moe_forward_chunked(c, x, wg, w1, w2, T, k, cf, y, in, s);
+    if (st) return st;
+    const size_t tk = (size_t)T * k;
+    if (expert_idx) CK(cudaMemcpyAsync(expert_idx, c->idx, tk * sizeof(int), cudaMemcpyDeviceToDevice, s));
+    if (slot_out) CK(cudaMemcpyAsync(slot_out, c->slot, tk * sizeof(int), cudaMemcpyDeviceToDevice, s));
+    if (combine_w) CK(cudaMemcpyAsync(combine_w, c->w, tk * sizeof(float), cudaMemcpyDeviceToDevice, s));
     return LANCET_OK;
 }
 

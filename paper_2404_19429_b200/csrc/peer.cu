@@ -495,6 +495,60 @@ __global__ void plan_kernel(const int* __restrict__ M, int G, int E, int E_l, in
     }
 }
 
+// Per-chunk size exchange of the block's pre-MoE partition (each chunk is gated separately,
+// PAPER.md L255-L257): column `ch` of this rank's count row ([E][n]) into row `rank` of every
+// peer's matrix, then the PK_COUNTS flag of chunk ch in every peer's array.
+__global__ void counts_col_kernel(const int* __restrict__ counts, int E, int n, int ch, int* const* mats, int G,
+                                  int rank, uint32_t* const* tab, size_t idx, const uint32_t* seq)
+{
+    pdl_wait();
+    for (int p = 0; p < G; ++p)
+        for (int e = threadIdx.x; e < E; e += blockDim.x)
+            mats[p][((size_t)rank * E + e) * n + ch] = counts[e * n + ch];
+    __threadfence_system();
+    __syncthreads();
+    const uint32_t v = seq[0];
+    for (int p = threadIdx.x; p < G; p += blockDim.x) st_release_sys(tab[p] + idx, v);
+}
+
+// The exchange plan of chunk ch when every chunk is gated on its own (block mode): owner p's
+// receive buffer gives local expert e_l a static region of `region` rows starting at
+// e_l * region; inside it the groups (e_l, 0), (e_l, 1), ... follow each other 128-row aligned
+// (so an expert's rows over all chunks stay one K range for the merged dW GEMM), rows of a
+// group ordered by source rank (R12).  Only the columns 0..ch of M are read: chunk ch's plan is
+// final before any later chunk is gated.  Writes this rank's group ch (grp_rows / grp_off
+// [n][E_l]), its push bases of chunk ch (base[ch][e] = row of its first chunk-ch row in the
+// owner's group minus S[e][ch], so row = base + slot) and, at the last chunk, the merged dW table.
+__global__ void plan_chunk_kernel(const int* __restrict__ M, int G, int E, int E_l, int n, int me, int ch,
+                                  int region, int* grp_rows, int* grp_off, int* base, uint32_t* err, uint32_t code,
+                                  int* merged)
+{
+    pdl_wait();
+    for (int e = threadIdx.x; e < E; e += blockDim.x) {
+        const int p = e / E_l, el = e % E_l;
+        int off = el * region;
+        int R = 0;
+        for (int c = 0; c <= ch; ++c) {
+            R = 0;
+            for (int src = 0; src < G; ++src) R += M[((size_t)src * E + e) * n + c];
+            if (c < ch) off += round_up(R, kRowAlign);
+        }
+        if (off + round_up(R, kRowAlign) > (el + 1) * region) atomicCAS(err, 0u, code | (uint32_t)p);
+        int src_off = 0, Sme = 0;
+        for (int src = 0; src < me; ++src) src_off += M[((size_t)src * E + e) * n + ch];
+        for (int c = 0; c < ch; ++c) Sme += M[((size_t)me * E + e) * n + c];
+        base[ch * E + e] = off + src_off - Sme;
+        if (p == me) {
+            grp_rows[ch * E_l + el] = R;
+            grp_off[ch * E_l + el] = off;
+            if (ch == n - 1) {
+                merged[el] = off + R - el * region;
+                merged[E_l + el] = el * region;
+            }
+        }
+    }
+}
+
 constexpr uint32_t kErrBit = 0x80000000u;
 uint32_t wait_code(int consumed, int kind, int chunk)
 {
@@ -577,6 +631,26 @@ int dev_plan(lancet_ctx* c, int n, cudaStream_t s)
     launch_k(plan_kernel, 1, 256, 0, s, (const int*)pl->my_counts, pl->world, E, c->E_l, n, c->rank, c->grp_dev,
              c->grp_dev + n * c->E_l, pl->d_push_base, R, OFF, pl->rows_cap, pl->d_err,
              wait_code(0, kPlanKind, 0), c->grp_dev + 2 * kMaxChunks * c->E_l);
+    return cudaGetLastError() != cudaSuccess;
+}
+
+int dev_counts_chunk(lancet_ctx* c, const int* d_counts, int n, int ch, cudaStream_t s)
+{
+    PeerLinks* pl = c->peer;
+    const int E = c->cfg.n_experts;
+    launch_k(counts_col_kernel, 1, 256, 0, s, d_counts, E, n, ch, pl->d_counts_tab, pl->world, c->rank, pl->d_flag_tab,
+             pl->flag_index(0, PK_COUNTS, ch, c->rank), (const uint32_t*)pl->d_seq);
+    if (cudaGetLastError() != cudaSuccess) return 1;
+    return dev_wait(c, 0, PK_COUNTS, ch, TGT_STEP, s);
+}
+
+int dev_plan_chunk(lancet_ctx* c, int n, int ch, int region, cudaStream_t s)
+{
+    PeerLinks* pl = c->peer;
+    const int E = c->cfg.n_experts;
+    launch_k(plan_chunk_kernel, 1, 256, 0, s, (const int*)pl->my_counts, pl->world, E, c->E_l, n, c->rank, ch, region,
+             c->grp_dev, c->grp_dev + n * c->E_l, pl->d_push_base, pl->d_err, wait_code(0, kPlanKind, ch),
+             c->grp_dev + 2 * kMaxChunks * c->E_l);
     return cudaGetLastError() != cudaSuccess;
 }
 

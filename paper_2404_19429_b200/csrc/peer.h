@@ -55,6 +55,10 @@ int dev_counts(lancet_ctx* c, const int* d_send, int n, cudaStream_t s);
 // expert-side group table (c->grp_dev, [n][E_l] rows | offsets) and the push row bases
 // [n][E] of this rank, from the gathered matrix
 int dev_plan(lancet_ctx* c, int n, cudaStream_t s);
+// block mode (every chunk gated on its own): the size exchange of chunk ch (column ch of the
+// [E][n] counts) + wait, and the plan of chunk ch in the static-region layout (peer.cu)
+int dev_counts_chunk(lancet_ctx* c, const int* d_counts, int n, int ch, cudaStream_t s);
+int dev_plan_chunk(lancet_ctx* c, int n, int ch, int region, cudaStream_t s);
 uint32_t peer_error(const lancet_ctx* c);      // 0 or the error word
 // ChunkSync of a GEMM over all chunks: its TMA producer waits for kind `wait_kind` per chunk
 ChunkSync chunk_sync(lancet_ctx* c, int wait_kind);

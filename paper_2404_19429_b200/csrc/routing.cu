@@ -474,7 +474,7 @@ __device__ __forceinline__ unsigned long long splitmix64_at(unsigned long long k
 
 __global__ void __launch_bounds__(kScanTile)
 random_gate_kernel(int T, int E, int k, unsigned long long seed, float* __restrict__ logits,
-                   int* __restrict__ idx_out, float* __restrict__ w_out, int* __restrict__ hist)
+                   int* __restrict__ idx_out, float* __restrict__ w_out, int* __restrict__ hist, int t_base)
 {
     pdl_wait();   // programmatic dependent launch: predecessor's writes visible
     __shared__ int sh_hist[kMaxExperts];
@@ -486,7 +486,7 @@ random_gate_kernel(int T, int E, int k, unsigned long long seed, float* __restri
         int sorted[kMaxK];                              // earlier draws, ascending
         const float wk = 1.0f / (float)k;
         for (int j = 0; j < k; ++j) {
-            int e = (int)(splitmix64_at(8ull * (unsigned long long)t + (unsigned long long)j, seed) %
+            int e = (int)(splitmix64_at(8ull * (unsigned long long)(t + t_base) + (unsigned long long)j, seed) %
                           (unsigned long long)(E - j));
             int pos = 0;
             for (int q = 0; q < j; ++q) {               // r-th free expert
@@ -534,7 +534,9 @@ slot_scan_kernel(const int* __restrict__ idx, int T, int k, int E, int C, int n,
                  const int* __restrict__ hist, int n_tiles, int* __restrict__ slot_out,
                  int* __restrict__ S, int* __restrict__ send_rows, int* __restrict__ send_off,
                  const float* __restrict__ logits, double* __restrict__ score, int* __restrict__ list,
-                 int* __restrict__ bpr_meta, const unsigned char* __restrict__ bpr_adm)
+                 int* __restrict__ bpr_meta, const unsigned char* __restrict__ bpr_adm,
+                 const int* __restrict__ carry_in, int* __restrict__ carry_out, int carry_chunk,
+                 int* __restrict__ carry_counts)
 {
     pdl_wait();   // programmatic dependent launch: predecessor's writes visible
     extern __shared__ int ism[];
@@ -556,10 +558,21 @@ slot_scan_kernel(const int* __restrict__ idx, int T, int k, int E, int C, int n,
     }
     const int* hs = staged ? sh_h : hist;
     if (tid < E) {
-        int s = 0;
+        int s = carry_in ? carry_in[tid] : 0;    // capacity passing from earlier chunks (L255)
         for (int q = 0; q < b; ++q) s += hs[q * E + tid];
         base[tid] = s;
-        if (MODE == SCAN_BPR_LIST) {
+        if (MODE == SCAN_SLOTS && carry_in) {
+            if (b == 0) {
+                int tot = 0;
+                for (int q = 0; q < n_tiles; ++q) tot += hs[q * E + tid];
+                const int p0 = carry_in[tid], p1 = p0 + tot;
+                const int s0 = min(C, p0), s1 = min(C, p1);
+                carry_out[tid] = p1;
+                S[tid * (n + 1) + carry_chunk] = s0;
+                S[tid * (n + 1) + carry_chunk + 1] = s1;
+                carry_counts[tid * n + carry_chunk] = s1 - s0;
+            }
+        } else if (MODE == SCAN_BPR_LIST) {
             int tot = 0;
             for (int q = 0; q < n_tiles; ++q) tot += hs[q * E + tid];
             adm[tid] = tot;                    // pairs routed to e (before any drop)
@@ -597,7 +610,7 @@ slot_scan_kernel(const int* __restrict__ idx, int T, int k, int E, int C, int n,
         for (int j = 0; j < kMaxK; ++j)
             if (j < k && valid && !bpr_adm[(size_t)t * k + j]) mine[j] = -2;
     }
-    const int cs = (MODE != SCAN_BPR_LIST && valid) ? chunk_starting_at(T, n, t) : -1;
+    const int cs = (MODE != SCAN_BPR_LIST && valid && !carry_in) ? chunk_starting_at(T, n, t) : -1;
     const bool warp_has_cs = __any_sync(0xffffffffu, cs >= 0);
     const unsigned lt = (1u << lane) - 1u;
     for (int e = 0; e < E; ++e) {
@@ -647,7 +660,7 @@ slot_scan_kernel(const int* __restrict__ idx, int T, int k, int E, int C, int n,
             S[e * (n + 1) + cs] = min(C, P);
         }
     }
-    if (b == 0) {
+    if (b == 0 && !carry_in) {
         __syncthreads();
         if (tid == 0) {
             int off = 0;
@@ -819,7 +832,7 @@ int launch_routing(const RouteArgs& a, bool is_bf16, cudaStream_t s)
     const int elt = is_bf16 ? 2 : 4;
     if (a.random) {
         launch_k(random_gate_kernel, n_tiles, kScanTile, 0, s, a.T, a.E, a.k, a.seed, a.logits, a.idx, a.w,
-                 a.hist);
+                 a.hist, a.t_base);
     } else if (gs_ok(a.d, a.E, elt)) {
         static bool gs_attr = false;
         if (!gs_attr) {
@@ -857,16 +870,17 @@ int launch_routing(const RouteArgs& a, bool is_bf16, cudaStream_t s)
                                         (n_tiles * a.E <= kScanHistMax ? n_tiles * a.E : 0));
     if (!a.bpr) {
         launch_k(slot_scan_kernel<SCAN_SLOTS>, n_tiles, kScanTile, smem2, s, a.idx, a.T, a.k, a.E, a.C,
-                 a.n_chunks, (const int*)a.hist, n_tiles, a.slot, a.S, a.send_rows, a.send_off,
-                 (const float*)nullptr, (double*)nullptr, (int*)nullptr, (int*)nullptr,
-                 (const unsigned char*)nullptr);
+                 a.carry_in ? a.carry_n : a.n_chunks, (const int*)a.hist, n_tiles, a.slot, a.S, a.send_rows,
+                 a.send_off, (const float*)nullptr, (double*)nullptr, (int*)nullptr, (int*)nullptr,
+                 (const unsigned char*)nullptr, a.carry_in, a.carry_out, a.carry_chunk, a.carry_counts);
         return 2;
     }
     // Batch Prioritized Routing (R16): pairs grouped by expert + scores, per-expert priority
     // admission, then the token-major scan over the admitted pairs
     launch_k(slot_scan_kernel<SCAN_BPR_LIST>, n_tiles, kScanTile, smem2, s, a.idx, a.T, a.k, a.E, a.C,
              a.n_chunks, (const int*)a.hist, n_tiles, a.slot, a.S, a.send_rows, a.send_off,
-             (const float*)a.logits, a.score, a.list, a.bpr_meta, (const unsigned char*)nullptr);
+             (const float*)a.logits, a.score, a.list, a.bpr_meta, (const unsigned char*)nullptr,
+             (const int*)nullptr, (int*)nullptr, 0, (int*)nullptr);
     const int cap = std::min(a.T * a.k, (int)((kSelSmem - sizeof(int) * n_tiles) / 8));
     static bool sel_attr = false;
     if (!sel_attr) {
@@ -879,7 +893,7 @@ int launch_routing(const RouteArgs& a, bool is_bf16, cudaStream_t s)
     launch_k(slot_scan_kernel<SCAN_BPR_SLOTS>, n_tiles, kScanTile, smem2, s, a.idx, a.T, a.k, a.E, a.C,
              a.n_chunks, (const int*)a.hist2, n_tiles, a.slot, a.S, a.send_rows, a.send_off,
              (const float*)nullptr, (double*)nullptr, (int*)nullptr, (int*)nullptr,
-             (const unsigned char*)a.bpr_adm);
+             (const unsigned char*)a.bpr_adm, (const int*)nullptr, (int*)nullptr, 0, (int*)nullptr);
     return 4;
 }
 

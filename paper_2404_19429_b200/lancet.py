@@ -46,7 +46,7 @@ EXPORTS = ["lancet_abi_version", "lancet_last_error", "lancet_nccl_unique_id", "
            "lancet_create_peer", "lancet_peer_blob_bytes", "lancet_peer_export", "lancet_peer_import",
            "lancet_moe_backward_dw", "lancet_set_dw_fillers", "lancet_dw_schedule", "lancet_stack_dw_plan",
            "lancet_set_gate_seed", "lancet_set_peer_timeout_ms", "lancet_peer_abort", "lancet_peer_status",
-           "lancet_tune_chunks"]
+           "lancet_tune_chunks", "lancet_moe_forward_partitioned"]
 
 
 class LancetError(RuntimeError):
@@ -99,6 +99,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "lancet_set_flags": ([P, U32], I32),
             "lancet_moe_forward": ([P, P, P, P, P, I32, I32, ctypes.c_double, I32, P, P, P, P, P], I32),
             "lancet_moe_backward": ([P, P, P, P, P, P, P], I32),
+            "lancet_moe_forward_partitioned": ([P, P, P, P, P, I32, I32, ctypes.c_double, I32, P, P, P, P, P, P],
+                                               I32),
             "lancet_get_counts": ([P, P, P, P], I32),
             "lancet_timeline_begin": ([P, P], I32),
             "lancet_last_timeline": ([P, ctypes.POINTER(_OpRecord), I32, ctypes.POINTER(I32)], I32),
@@ -297,9 +299,9 @@ class Context:
 
     # -- lifecycle --------------------------------------------------------------------------
     def close(self):
-        if self._p:
+        if self._p and not getattr(self, "_borrowed", False):
             load_library().lancet_destroy(self._p)
-            self._p = ctypes.c_void_p()
+        self._p = ctypes.c_void_p()
 
     def __del__(self):
         try:
@@ -328,6 +330,26 @@ class Context:
             n_chunks, _ptr(y), _ptr(idx), _ptr(slot), _ptr(w), _stream(stream))
         _check(st, self._p)
         self._last = (x, wg, w1, w2)       # the library keeps pointers until backward
+        self._last_n = n_chunks
+        return y, idx, slot, w
+
+    def forward_partitioned(self, x, wg, w1, w2, k: int, capacity_factor: float, n_chunks: int,
+                            resid=None, y=None, stream=None, routing: bool = True):
+        """lancet_moe_forward_partitioned: every chunk gated on its own with the carried capacity
+        state (the block's pre-MoE partition); y = resid + MoE(x)."""
+        T = x.shape[0]
+        dev = x.device
+        y = torch.empty_like(x) if y is None else y
+        idx = slot = w = None
+        if routing:
+            idx = torch.empty((T, k), dtype=torch.int32, device=dev)
+            slot = torch.empty((T, k), dtype=torch.int32, device=dev)
+            w = torch.empty((T, k), dtype=torch.float32, device=dev)
+        st = load_library().lancet_moe_forward_partitioned(
+            self._p, _ptr(x), _ptr(wg), _ptr(w1), _ptr(w2), T, k, float(capacity_factor), n_chunks,
+            _ptr(resid), _ptr(y), _ptr(idx), _ptr(slot), _ptr(w), _stream(stream))
+        _check(st, self._p)
+        self._last = (x, wg, w1, w2)
         self._last_n = n_chunks
         return y, idx, slot, w
 

@@ -10,6 +10,7 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 HEADER = os.path.join(ROOT, "include", "lancet_moe.h")
+BLOCK_HEADER = os.path.join(ROOT, "include", "lancet_block.h")
 PKG = os.path.join(ROOT, "paper_2404_19429_b200")
 
 
@@ -21,8 +22,8 @@ def lib():
     return lancet.load_library()
 
 
-def declared_functions():
-    src = open(HEADER).read()
+def declared_functions(path=HEADER):
+    src = open(path).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     return sorted(set(re.findall(r"\b(lancet_[a-z_0-9]+)\s*\(", src)))
 
@@ -34,10 +35,29 @@ def test_header_declares_the_north_star_entry_points():
 
 
 def test_every_declared_symbol_is_exported(lib):
-    from paper_2404_19429_b200 import lancet
+    from paper_2404_19429_b200 import block, lancet
     for name in declared_functions():
         assert hasattr(lib, name), name
     assert set(declared_functions()) == set(lancet.EXPORTS)
+    # the GPT-MoE block (include/lancet_block.h)
+    for name in declared_functions(BLOCK_HEADER):
+        assert hasattr(lib, name), name
+    assert set(declared_functions(BLOCK_HEADER)) == set(block.EXPORTS)
+
+
+def test_block_create_rejects_bad_config_without_a_device(lib):
+    from paper_2404_19429_b200 import block, lancet
+    b = ctypes.c_void_p()
+    good = dict(d_model=256, d_ffn=512, n_experts=4, max_tokens=512)
+    for moe_kw, heads, seq in [(dict(good), 3, 128),                          # head_dim != 128
+                               (dict(good), 2, 100),                          # seq % 128
+                               (dict(good, max_tokens=500), 2, 128),          # max_tokens % seq
+                               (dict(good, act="identity_expert"), 2, 128),
+                               (dict(good, dtype="fp32"), 2, 128)]:
+        cfg = block.BlockConfig(lancet.LayerConfig(**moe_kw), n_heads=heads, seq_len=seq)
+        st = block._lib().lancet_block_create_peer(ctypes.byref(b), 1, 0, 0, ctypes.byref(cfg._c()))
+        assert st in (1, 6), (moe_kw, heads, seq, st)
+        assert not b.value
 
 
 def test_abi_version(lib):
