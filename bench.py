@@ -70,6 +70,11 @@ def parse():
     ap.add_argument("--no-ep", action="store_true",
                     help="N = 1: skip the 'ep' sub-record (the expert-parallel chunk pipeline over a "
                          "one-rank peer group, with its exposure and no-comm differential)")
+    ap.add_argument("--no-block", action="store_true",
+                    help="skip the 'block' sub-record (BASELINE configs[3]: the GPT-MoE block forward "
+                         "with the pre-MoE partition, NEXT-1)")
+    ap.add_argument("--only-block", action="store_true",
+                    help="measure and print only the 'block' record")
     ap.add_argument("--no-arms", action="store_true",
                     help="N > 1: skip the per-transport arms (push / pull / NCCL on one definition)")
     a = ap.parse_args()
@@ -455,6 +460,105 @@ def tuner_record(a, ctx, lancet, flags, step_fn, stream, barrier, max_over_ranks
                                "from the size-interpolated cost model at C/n (P:L325-L328)"}}
 
 
+BLOCK_OPS_NONMOE = ("ln1", "qkv_proj", "attention", "o_proj", "ln2")
+
+
+def block_record(a, world, rank, local_rank, stream, barrier, max_over_ranks, ns=(1, 2, 4, 8)):
+    """BASELINE configs[3]: the full GPT-MoE block (pre-LN GPT-2 block with the MoE layer as its
+    MLP) forward with Lancet's pre-MoE partition (fig:part_all), per
+    GPU: 8 sequences x 1024 tokens, d_model 2048, 16 heads, ffn 8192, 32 experts (32/N per GPU),
+    Switch top-1, cf 1.25.  Per chunk count n: the pipelined forward (clean pass), its exposed /
+    unoverlapped exchange time (instrumented pass; LANCET_FLAG_SERIAL = one stream, chunks
+    merged, no overlap) and the no-comm differential; per-op times of the n = 4 pass and the
+    attention kernel's roofline."""
+    import dataclasses
+    import torch
+    import synthetic as S
+    from paper_2404_19429_b200 import block as B
+    from paper_2404_19429_b200 import lancet
+    sh = S.BlockShape(n_seq=8, seq_len=1024, d=2048, n_heads=16, f=8192, E=32, G=world, k=1, cf=1.25, n_chunks=4)
+    ins = S.gen_block_rank_inputs(a.seed + 7, rank, sh, beta=a.beta, with_dy=False)
+    dev = torch.device("cuda", local_rank)
+    bf = torch.bfloat16
+    p = {key: torch.from_numpy(ins[key]).to(dev, torch.float32 if key in ("ln1_g", "ln1_b", "ln2_g", "ln2_b", "wg")
+                                            else bf) for key in B.PARAMS}
+    x = torch.from_numpy(ins["x"]).to(dev, bf)
+    del ins
+    out = torch.empty_like(x)
+    moe = lancet.LayerConfig(d_model=sh.d, d_ffn=sh.f, n_experts=sh.E, max_tokens=sh.T, max_k=sh.k, max_chunks=8)
+    import torch.distributed as dist
+    blk = B.Block(B.BlockConfig(moe, n_heads=sh.n_heads, seq_len=sh.seq_len, max_capacity_factor=sh.cf),
+                  world=world, rank=rank, device=local_rank, pg=dist.group.WORLD if world > 1 else None)
+    base = blk.moe.cfg.flags
+
+    def run(n, fl, steps, instrumented=False):
+        blk.moe.set_flags(base | fl | (lancet.FLAG_TIMELINE if instrumented else 0))
+        for _ in range(3):
+            blk.forward(x, p, sh.k, sh.cf, n, out=out)
+        torch.cuda.synchronize()
+        if instrumented:
+            blk.moe.timeline_begin(stream)
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            blk.forward(x, p, sh.k, sh.cf, n, out=out)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        return max_over_ranks(e0.elapsed_time(e1) / steps), (blk.moe.timeline(cap=200000) if instrumented else None)
+
+    steps = max(5, min(a.steps, 30))
+    for _ in range(max(3, min(a.warmup, 20))):
+        blk.forward(x, p, sh.k, sh.cf, 4, out=out)
+    by_n, ops4 = [], None
+    for n in ns:
+        ms, _ = run(n, 0, steps)
+        _, tl = run(n, 0, steps, True)
+        exposed, comm, _, _ = exposure_per_step(tl, steps)
+        _, tls = run(n, lancet.FLAG_SERIAL, 3, True)
+        unover = sum(r["end_us"] - r["start_us"] for r in tls if r["lane"] == 1) / 3 / 1000.0
+        ms_serial, _ = run(n, lancet.FLAG_SERIAL, steps)
+        ms_nocomm, _ = run(n, lancet.FLAG_NO_COMM, steps)
+        by_n.append({"n_chunks": n, "ms_per_step": ms, "tokens_per_s": world * sh.T / (ms / 1000.0),
+                     "exposed_a2a_ms": max_over_ranks(exposed), "a2a_ms_on_comm_lane": max_over_ranks(comm),
+                     "unoverlapped_a2a_ms": max_over_ranks(unover), "serial_ms_per_step": ms_serial,
+                     "no_comm_ms_per_step": ms_nocomm, "exposed_upper_bound_ms": ms - ms_nocomm})
+        if n == 4:
+            ops4 = op_stats(tl, steps)
+    blk.moe.set_flags(base)
+    best = min(by_n, key=lambda r: r["ms_per_step"])
+    pk = peaks()
+    # attention: algorithmic causal FLOPs 2 * 2 * S^2 / 2 * hd per (sequence, head); the kernel
+    # also recomputes Q K^T (two-pass exact softmax) and evaluates 2 exp2 per unmasked score
+    att_flops = sh.n_seq * sh.n_heads * 2.0 * sh.seq_len ** 2 * (sh.d // sh.n_heads)
+    att_us = ops4["attention"]["us_per_step"] if ops4 and "attention" in ops4 else None
+    proj_flops = 2.0 * sh.T * sh.d * (3 * sh.d) + 2.0 * sh.T * sh.d * sh.d
+    proj_us = sum(ops4[o]["us_per_step"] for o in ("qkv_proj", "o_proj") if ops4 and o in ops4) or None
+    rec = {
+        "workload": f"GPT-MoE block forward (BASELINE configs[3]): {sh.n_seq}x{sh.seq_len} tokens/GPU, d_model={sh.d}, "
+                    f"{sh.n_heads} heads, ffn={sh.f}, experts={sh.E} ({sh.E // world}/GPU), Switch top-1, cf={sh.cf}, "
+                    f"bf16; MoE over the peer push transport" + (" (one-rank group: exchanges to self)" if world == 1 else ""),
+        "metric": "block forward tokens/s; exposed all-to-all ms/iter", "unit": "tokens/s",
+        "value": world * sh.T / (best["ms_per_step"] / 1000.0), "best_n_chunks": best["n_chunks"],
+        "by_n": by_n,
+        "ops_us_per_step_n4": {o: round(v["us_per_step"], 2) for o, v in (ops4 or {}).items()},
+        "attention_roofline": {
+            "bound": "tensor", "achieved": att_flops / (att_us * 1e-6) / 1e12 if att_us else None,
+            "peak": pk["bf16_sus"], "unit": "TFLOP/s",
+            "frac": (att_flops / (att_us * 1e-6) / 1e12 / pk["bf16_sus"]) if att_us else None,
+            "flops": att_flops, "us": att_us,
+            "note": "algorithmic causal FLOPs (QK^T and PV on the unmasked half) / summed event time of the "
+                    "per-chunk attention launches (n = 4, instrumented pass); the two-pass kernel executes 1.5x "
+                    "the MMA work and 2 exp2 per score on the SFU"},
+        "projection_gemms": {"achieved_tflops": proj_flops / (proj_us * 1e-6) / 1e12 if proj_us else None,
+                             "us": proj_us, "flops": proj_flops},
+    }
+    blk.close()
+    return rec
+
+
 def make_context(a, lancet, cfg, world, rank, local_rank, dev):
     """transport auto (world > 1): the copy-engine peer transport when every rank can set it up
     (CUDA IPC between all ranks' devices, stream memory operations), else NCCL -- decided
@@ -551,6 +655,15 @@ def run_lancet(a, world, rank, local_rank):
         t = torch.tensor([v], dtype=torch.float64, device="cpu" if a.same_device else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
+
+    if a.only_block:
+        clocks = ClockSampler(local_rank).start()
+        rec = block_record(a, world, rank, local_rank, torch.cuda.current_stream(), barrier, max_over_ranks)
+        rec["clocks"] = clocks.stop()
+        if rank == 0:
+            print(json.dumps({"block": rec}), flush=True)
+        ctx.close()
+        return
 
     clocks = ClockSampler(local_rank).start()
     for _ in range(a.warmup):
@@ -775,6 +888,8 @@ def run_lancet(a, world, rank, local_rank):
         sched = 1 if (a.transport_used == "peer" and not a.no_push) else 0
         out["chunk_tuner"] = tuner_record(a, ctx, lancet, flags, step_on(ctx), stream, barrier, max_over_ranks,
                                           sched, float(adm * rowb))["tuner"]
+    if not a.no_block:
+        out["block"] = block_record(a, world, rank, local_rank, stream, barrier, max_over_ranks)
     if rank == 0 and not a.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(a)
     barrier()

@@ -13,8 +13,10 @@
 // correction step.  The extra Q K^T costs 1/3 more MMA work, which the tensor core has to spare
 // here (the kernel is bound by the exponentials on the SFU: 2 x 128 x 128 per key tile).
 //
-// Roles (256 threads): warp 0 TMA producer | warp 1 MMA issuer (one thread) | warp 2 TMEM
-// allocator | warp 3 idle | warps 4-7 softmax + epilogue (thread = query row, TMEM lane).
+// Roles (384 threads): warp 0 TMA producer | warp 1 MMA issuer (one thread) | warp 2 TMEM
+// allocator | warp 3 idle | warps 4-11 softmax + epilogue: thread = query row (TMEM lane
+// quadrant warp % 4), column half (warp - 4) / 4 -- two warps per row share the exponentials;
+// their pass-1 row statistics meet once, in shared memory, after the last key tile.
 // Shared memory: Q 32 KiB | K ring 2 x 32 KiB | V ring 2 x 32 KiB | P 2 x 32 KiB.
 // TMEM: S double buffer (2 x 128 columns) + O (128 columns) of a 512-column allocation.
 #include <cuda.h>
@@ -31,7 +33,7 @@ using namespace lancet::tc;
 constexpr int HD = 128;                 // head dim
 constexpr int TQ = 128;                 // query rows per CTA
 constexpr int TK = 128;                 // keys per tile
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;
 constexpr uint32_t TILE_BYTES = 128 * 128 * 2;     // one 128 x 128 bf16 operand = 32 KiB
 constexpr uint32_t BOX_BYTES = 128 * 64 * 2;       // a [128 rows][64] K-major box = 16 KiB
 constexpr size_t kSmem = 1024 + 7 * (size_t)TILE_BYTES + 256;
@@ -78,6 +80,8 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQK, const __grid_constant_
     uint64_t* p_empty = bars + 15;
     uint64_t* o_full = bars + 17;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
+    // [2 halves][m | l][128] row statistics of pass 1, in P buffer 1 (untouched until pass 2)
+    float* red = reinterpret_cast<float*>(sP + TILE_BYTES);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nq = S / TQ;
@@ -97,8 +101,8 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQK, const __grid_constant_
         for (int i = 0; i < 2; ++i) {
             mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1);
             mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1);
-            mbar_init(&s_full[i], 1); mbar_init(&s_empty[i], 4);
-            mbar_init(&p_full[i], 4); mbar_init(&p_empty[i], 1);
+            mbar_init(&s_full[i], 1); mbar_init(&s_empty[i], 8);
+            mbar_init(&p_full[i], 8); mbar_init(&p_empty[i], 1);
         }
         mbar_init(o_full, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -181,21 +185,22 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQK, const __grid_constant_
             tc_commit<1>(o_full);
         }
     } else if (warp >= 4) {
-        // ===================== softmax + epilogue (thread = query row) =====================
-        const int quad = warp & 3;
+        // ===================== softmax + epilogue (thread = query row, column half) =====
+        const int quad = warp & 3, half = (warp - 4) >> 2;
         const int r = quad * 32 + lane;
         const int q_pos = qi * TQ + r;                 // query position in the sequence
         const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
         float m = -INFINITY, l = 0.f;
         uint32_t v[32];
-        // pass 1: row max and normaliser
+        // pass 1: this half's row max and normaliser
         for (int it = 0; it < n; ++it) {
             const int b = it & 1;
             mbar_wait(&s_full[b], (it >> 1) & 1);
             tc_fence_after();
             const bool diag = it == qi;
 #pragma unroll 1
-            for (int cc = 0; cc < 4; ++cc) {
+            for (int c2 = 0; c2 < 2; ++c2) {
+                const int cc = 2 * half + c2;
                 tmem_ld32(tmem + lane_off + 128 * b + 32 * cc, v);
                 float cm = -INFINITY;
 #pragma unroll
@@ -206,27 +211,41 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQK, const __grid_constant_
                     cm = fmaxf(cm, x);
                 }
                 const float mn = fmaxf(m, cm);
-                float s = 0.f;
+                if (mn != -INFINITY) {
+                    float sum = 0.f;
 #pragma unroll
-                for (int i = 0; i < 32; ++i) s += ex2(__uint_as_float(v[i]) - mn);
-                l = l * ex2(m - mn) + s;
-                m = mn;
+                    for (int i = 0; i < 32; ++i) sum += ex2(__uint_as_float(v[i]) - mn);
+                    l = l * ex2(m - mn) + sum;
+                    m = mn;
+                }
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&s_empty[b]);
         }
+        // the two halves' statistics of each row meet (named barrier of the 8 softmax warps)
+        red[(half * 2 + 0) * 128 + r] = m;
+        red[(half * 2 + 1) * 128 + r] = l;
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        {
+            const float mo = red[((half ^ 1) * 2 + 0) * 128 + r], lo = red[((half ^ 1) * 2 + 1) * 128 + r];
+            const float mm = fmaxf(m, mo);
+            l = (m == -INFINITY ? 0.f : l * ex2(m - mm)) + (mo == -INFINITY ? 0.f : lo * ex2(mo - mm));
+            m = mm;
+        }
+        asm volatile("bar.sync 1, 256;" ::: "memory");     // every read done before P buffer 1 is written
         const float inv_l = 1.f / l;
-        // pass 2: P = exp2(s - m) / l into shared memory (K-major SW128: two [128][64] boxes)
+        // pass 2: P = exp2(s - m) / l into shared memory (K-major SW128: box `half` of P)
         for (int j = 0; j < n; ++j) {
             const int it = n + j, b = it & 1, pb = j & 1;
             mbar_wait(&s_full[b], (it >> 1) & 1);
             mbar_wait(&p_empty[pb], ((j >> 1) & 1) ^ 1);
             tc_fence_after();
             const bool diag = j == qi;
-            uint8_t* prow = sP + pb * TILE_BYTES + r * 128;
+            uint8_t* box = sP + pb * TILE_BYTES + half * BOX_BYTES + r * 128;
 #pragma unroll 1
-            for (int cc = 0; cc < 4; ++cc) {
+            for (int c2 = 0; c2 < 2; ++c2) {
+                const int cc = 2 * half + c2;
                 tmem_ld32(tmem + lane_off + 128 * b + 32 * cc, v);
                 uint32_t pk[16];
 #pragma unroll
@@ -238,10 +257,9 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQK, const __grid_constant_
                     __nv_bfloat162 hv = __floats2bfloat162_rn(p0, p1);
                     pk[i] = *reinterpret_cast<uint32_t*>(&hv);
                 }
-                uint8_t* box = prow + (cc >> 1) * BOX_BYTES;
 #pragma unroll
                 for (int c4 = 0; c4 < 4; ++c4) {
-                    const int c16 = (cc & 1) * 4 + c4;
+                    const int c16 = c2 * 4 + c4;
                     st_v4(box + ((c16 ^ (r & 7)) << 4), make_uint4(pk[4 * c4], pk[4 * c4 + 1], pk[4 * c4 + 2], pk[4 * c4 + 3]));
                 }
             }
@@ -253,13 +271,14 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQK, const __grid_constant_
                 mbar_arrive(&s_empty[b]);
             }
         }
-        // epilogue: O (TMEM columns 256..383) -> bf16 rows of att
+        // epilogue: this half's 64 columns of O (TMEM columns 256..383) -> bf16 rows of att
         mbar_wait(o_full, 0);
         tc_fence_after();
         const long tok = (long)seq_row0 + qi * TQ + r;
         bf16* orow = att + tok * d + h * HD;
 #pragma unroll 1
-        for (int cc = 0; cc < 4; ++cc) {
+        for (int c2 = 0; c2 < 2; ++c2) {
+            const int cc = 2 * half + c2;
             tmem_ld32(tmem + lane_off + 256 + 32 * cc, v);
             uint32_t pk[16];
 #pragma unroll
@@ -271,7 +290,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQK, const __grid_constant_
             for (int c4 = 0; c4 < 4; ++c4)
                 st_v4(orow + 32 * cc + 8 * c4, make_uint4(pk[4 * c4], pk[4 * c4 + 1], pk[4 * c4 + 2], pk[4 * c4 + 3]));
         }
-        lse[(long)h * T_all + tok] = m + __log2f(l);
+        if (half == 0) lse[(long)h * T_all + tok] = m + __log2f(l);
     }
     tc_fence_before();
     __syncthreads();
