@@ -463,7 +463,7 @@ def tuner_record(a, ctx, lancet, flags, step_fn, stream, barrier, max_over_ranks
 BLOCK_OPS_NONMOE = ("ln1", "qkv_proj", "attention", "o_proj", "ln2")
 
 
-def block_record(a, world, rank, local_rank, stream, barrier, max_over_ranks, ns=(1, 2, 4, 8)):
+def block_record(a, world, rank, local_rank, stream, barrier, max_over_ranks, ns=(1, 2, 4, 8), experts=32):
     """BASELINE configs[3]: the full GPT-MoE block (pre-LN GPT-2 block with the MoE layer as its
     MLP) forward with Lancet's pre-MoE partition (fig:part_all), per
     GPU: 8 sequences x 1024 tokens, d_model 2048, 16 heads, ffn 8192, 32 experts (32/N per GPU),
@@ -476,7 +476,7 @@ def block_record(a, world, rank, local_rank, stream, barrier, max_over_ranks, ns
     import synthetic as S
     from paper_2404_19429_b200 import block as B
     from paper_2404_19429_b200 import lancet
-    sh = S.BlockShape(n_seq=8, seq_len=1024, d=2048, n_heads=16, f=8192, E=32, G=world, k=1, cf=1.25, n_chunks=4)
+    sh = S.BlockShape(n_seq=8, seq_len=1024, d=2048, n_heads=16, f=8192, E=experts, G=world, k=1, cf=1.25, n_chunks=4)
     ins = S.gen_block_rank_inputs(a.seed + 7, rank, sh, beta=a.beta, with_dy=False)
     dev = torch.device("cuda", local_rank)
     bf = torch.bfloat16
@@ -659,6 +659,9 @@ def run_lancet(a, world, rank, local_rank):
     if a.only_block:
         clocks = ClockSampler(local_rank).start()
         rec = block_record(a, world, rank, local_rank, torch.cuda.current_stream(), barrier, max_over_ranks)
+        if world == 1:
+            rec["ep8_expert_shapes"] = block_record(a, world, rank, local_rank, torch.cuda.current_stream(), barrier,
+                                                    max_over_ranks, experts=4)
         rec["clocks"] = clocks.stop()
         if rank == 0:
             print(json.dumps({"block": rec}), flush=True)
@@ -890,6 +893,12 @@ def run_lancet(a, world, rank, local_rank):
                                           sched, float(adm * rowb))["tuner"]
     if not a.no_block:
         out["block"] = block_record(a, world, rank, local_rank, stream, barrier, max_over_ranks)
+        if world == 1:
+            # the per-GPU expert shapes of the 8-GPU run (4 local experts receiving 8192 rows per
+            # step) on this GPU: the same block with E = 4 experts in a one-rank group -- with
+            # E_l = 32 every chunk splits each expert's ~256 rows into tiny GEMM groups
+            out["block"]["ep8_expert_shapes"] = block_record(a, world, rank, local_rank, stream, barrier,
+                                                             max_over_ranks, experts=4)
     if rank == 0 and not a.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(a)
     barrier()
