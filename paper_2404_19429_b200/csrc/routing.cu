@@ -47,22 +47,27 @@ struct GateGeom {
     size_t x_bytes, buf_bytes, smem;
 };
 
-__host__ __device__ inline int gate_ce(int E)
+// experts (chains) per thread: 8 (x 4 tokens: each staged Wg value feeds 4 chains) where the
+// batch still gives >= 4 warps per SM with them; else 4 (x 2 tokens), which quadruples the
+// threads -- at T = 8192, E = 32 (configs[3]) 8 x 4 left 128 blocks of 2 warps for 148 SMs
+constexpr int kGateMinThreads8 = 148 * 64;
+__host__ __device__ inline int gate_ce(int E, int T)
 {
-    return (E % 8 == 0 && E >= 16) ? 8 : (E % 4 == 0) ? 4 : (E % 2 == 0) ? 2 : 1;
+    if (E % 8 == 0 && E >= 16 && (long)T * E / (8 * kGateTT8) >= kGateMinThreads8) return 8;
+    return (E % 4 == 0) ? 4 : (E % 2 == 0) ? 2 : 1;
 }
 
 // floats per expert group of the staged Wg tile (+4: groups start in different banks)
 __host__ __device__ constexpr int gate_wg_stride(int ce) { return gate_dt(ce) * ce + 4; }
 
-__host__ __device__ inline GateGeom gate_geom(int E, int elt_bytes)
+__host__ __device__ inline GateGeom gate_geom(int E, int elt_bytes, int ce, int tb_max)
 {
     GateGeom g;
-    g.ce = gate_ce(E);
+    g.ce = ce;
     g.tt = g.ce >= 8 ? kGateTT8 : (g.ce >= 4 ? 2 : 1);
     g.tpt = E / g.ce;
     g.TB = kGateThreads * g.tt / g.tpt;
-    if (g.TB > kGateMaxTB) g.TB = kGateMaxTB;
+    if (g.TB > tb_max) g.TB = tb_max;
     g.TB = g.TB / g.tt * g.tt;                  // whole token groups (E = 192: 42 -> 40)
     if (g.TB < g.tt) g.TB = g.tt;
     g.threads = g.TB / g.tt * g.tpt;
@@ -186,14 +191,14 @@ template <typename Elt, int CE, int TT>
 __global__ void __launch_bounds__(kGateThreads)
 gate_topk_kernel(const Elt* __restrict__ x, const float* __restrict__ wg, int T, int d, int E,
                  int k, int renorm, float* __restrict__ logits, int* __restrict__ idx_out,
-                 float* __restrict__ w_out, int* __restrict__ hist, int n_tiles)
+                 float* __restrict__ w_out, int* __restrict__ hist, int n_tiles, int tb_max)
 {
     pdl_wait();   // programmatic dependent launch: predecessor's writes visible
     extern __shared__ __align__(16) uint8_t gsm[];
     __shared__ int sh_hist[2 * kMaxExperts];
     constexpr int V = Vec16<Elt>::N;                  // x values per 16-byte shared load
     constexpr int P = CE >= 2 ? CE / 2 : 1;           // packed chain pairs
-    const GateGeom geo = gate_geom(E, sizeof(Elt));
+    const GateGeom geo = gate_geom(E, sizeof(Elt), CE, tb_max);
     const int TB = geo.TB;
     const int tid = threadIdx.x;
     const int q = tid / geo.tpt;                      // token group: rows q*TT .. q*TT+TT-1
@@ -851,10 +856,13 @@ int launch_routing(const RouteArgs& a, bool is_bf16, cudaStream_t s)
         else { if (S == 8) GS(float, 8); else GS(float, 4); }
 #undef GS
     } else {
-    const GateGeom g = gate_geom(a.E, elt);
+    // 64 tokens per block (32 measured slower even where it doubles the blocks: each block
+    // stages the whole Wg, so fewer tokens per block means more Wg traffic per FMA)
+    const int tb_max = kGateMaxTB;
+    const GateGeom g = gate_geom(a.E, elt, gate_ce(a.E, a.T), tb_max);
     const int blocks = ceil_div(a.T, g.TB);
     const int thr = round_up(g.threads, 32);
-#define GATE_ARGS a.T, a.d, a.E, a.k, a.renorm, a.logits, a.idx, a.w, a.hist, n_tiles
+#define GATE_ARGS a.T, a.d, a.E, a.k, a.renorm, a.logits, a.idx, a.w, a.hist, n_tiles, tb_max
 #define GATE_LAUNCH(Elt)                                                                                    \
     switch (g.ce) {                                                                                         \
     case 8: launch_k(gate_topk_kernel<Elt, 8, kGateTT8>, blocks, thr, g.smem, s, (const Elt*)a.x, a.wg, GATE_ARGS); break;  \
