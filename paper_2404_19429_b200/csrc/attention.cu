@@ -21,6 +21,8 @@
 // TMEM: S double buffer (2 x 128 columns) + O (128 columns) of a 512-column allocation.
 #include <cuda.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "tc_common.cuh"
@@ -54,12 +56,16 @@ __device__ __forceinline__ float ex2(float x) {
 
 // qkv [T][3d] bf16 (q | k | v, head h at columns h*128 of each); att [T][d] bf16 out;
 // lse [H][T] fp32 out: log2 of the row normaliser in the scaled (log2) domain, m + log2(l).
-// Tokens [tok0, tok0 + n_seq * S) are processed; CTA b -> (query tile, head, sequence), the
-// longest (last) query tiles first.
+// Tokens [tok0, tok0 + n_seq * S) are processed.  Persistent: CTA b takes work items b,
+// b + gridDim.x, ... (item -> (query tile, head, sequence), the longest (last) query tiles
+// first); every barrier phase runs on counters that continue across items, so the next item's
+// K / V loads and Q K^T start while the current item's softmax and P V finish (Q is reloaded
+// once the current item's last Q K^T has completed; O is drained before the next item's first
+// P V).
 __global__ void __launch_bounds__(kThreads, 1)
 attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQK, const __grid_constant__ CUtensorMap tmV,
                 bf16* __restrict__ att, float* __restrict__ lse, int tok0, int S, int H, int d, int T_all,
-                float scale_log2)
+                float scale_log2, int n_items)
 {
     pdl_wait();
     extern __shared__ uint8_t smem_raw[];
@@ -79,18 +85,21 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQK, const __grid_constant_
     uint64_t* p_full = bars + 13;
     uint64_t* p_empty = bars + 15;
     uint64_t* o_full = bars + 17;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
-    // [2 halves][m | l][128] row statistics of pass 1, in P buffer 1 (untouched until pass 2)
+    uint64_t* q_empty = bars + 18;
+    uint64_t* o_empty = bars + 19;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
+    // [2 halves][m | l][128] row statistics of pass 1, in P buffer 1 (no P V reads it then)
     float* red = reinterpret_cast<float*>(sP + TILE_BYTES);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nq = S / TQ;
-    const int bh = gridDim.x / nq;                 // (sequence, head) pairs
-    const int qi = nq - 1 - (int)blockIdx.x / bh;  // longest tiles first
-    const int rem = (int)blockIdx.x % bh;
-    const int h = rem % H, sq = rem / H;
-    const int seq_row0 = tok0 + sq * S;            // first token of the sequence
-    const int n = qi + 1;                          // key tiles (causal)
+    const int bh = n_items / nq;                   // (sequence, head) pairs
+    auto decode = [&](int item, int& qi, int& h, int& row0) {
+        qi = nq - 1 - item / bh;                   // longest tiles first
+        const int rem = item % bh;
+        h = rem % H;
+        row0 = tok0 + (rem / H) * S;               // first token of the sequence
+    };
 
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tmQK);
@@ -98,6 +107,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQK, const __grid_constant_
     }
     if (warp == 1 && lane == 0) {
         mbar_init(q_full, 1);
+        mbar_init(q_empty, 1);
         for (int i = 0; i < 2; ++i) {
             mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1);
             mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1);
@@ -105,6 +115,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQK, const __grid_constant_
             mbar_init(&p_full[i], 8); mbar_init(&p_empty[i], 1);
         }
         mbar_init(o_full, 1);
+        mbar_init(o_empty, 8);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 2) {
@@ -120,28 +131,36 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQK, const __grid_constant_
     if (warp == 0) {
         // ===================== TMA producer =====================
         if (lane == 0) {
-            const int qcol = h * HD, kcol = d + h * HD, vcol = 2 * d + h * HD;
-            mbar_expect_tx(q_full, TILE_BYTES);
-            tma_load_2d(&tmQK, q_full, sQ, qcol, seq_row0 + qi * TQ);
-            tma_load_2d(&tmQK, q_full, sQ + BOX_BYTES, qcol + 64, seq_row0 + qi * TQ);
-            for (int it = 0; it < 2 * n; ++it) {
-                const int j = it < n ? it : it - n;
-                const int ks = it & 1;
-                mbar_wait(&k_empty[ks], ((it >> 1) & 1) ^ 1);
-                mbar_expect_tx(&k_full[ks], TILE_BYTES);
-                uint8_t* kd = sK + ks * TILE_BYTES;
-                tma_load_2d(&tmQK, &k_full[ks], kd, kcol, seq_row0 + j * TK);
-                tma_load_2d(&tmQK, &k_full[ks], kd + BOX_BYTES, kcol + 64, seq_row0 + j * TK);
-                if (it >= n) {
-                    const int vs = j & 1;
-                    mbar_wait(&v_empty[vs], ((j >> 1) & 1) ^ 1);
-                    mbar_expect_tx(&v_full[vs], TILE_BYTES);
-                    uint8_t* vd = sV + vs * TILE_BYTES;
-                    // MN-major B operand: boxes of [64 keys][64 head dims], (key half, dim half)
-                    for (int kb = 0; kb < 2; ++kb)
-                        for (int nb = 0; nb < 2; ++nb)
-                            tma_load_2d(&tmV, &v_full[vs], vd + (kb * 2 + nb) * 8192, vcol + 64 * nb,
-                                        seq_row0 + j * TK + 64 * kb);
+            uint32_t kc = 0, vc = 0, ni = 0;            // K tiles, V tiles, items so far
+            for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++ni) {
+                int qi, h, row0;
+                decode(item, qi, h, row0);
+                const int n = qi + 1;
+                const int qcol = h * HD, kcol = d + h * HD, vcol = 2 * d + h * HD;
+                mbar_wait(q_empty, (ni & 1) ^ 1);       // the last item's Q K^T are done
+                mbar_expect_tx(q_full, TILE_BYTES);
+                tma_load_2d(&tmQK, q_full, sQ, qcol, row0 + qi * TQ);
+                tma_load_2d(&tmQK, q_full, sQ + BOX_BYTES, qcol + 64, row0 + qi * TQ);
+                for (int it = 0; it < 2 * n; ++it, ++kc) {
+                    const int j = it < n ? it : it - n;
+                    const int ks = kc & 1;
+                    mbar_wait(&k_empty[ks], ((kc >> 1) & 1) ^ 1);
+                    mbar_expect_tx(&k_full[ks], TILE_BYTES);
+                    uint8_t* kd = sK + ks * TILE_BYTES;
+                    tma_load_2d(&tmQK, &k_full[ks], kd, kcol, row0 + j * TK);
+                    tma_load_2d(&tmQK, &k_full[ks], kd + BOX_BYTES, kcol + 64, row0 + j * TK);
+                    if (it >= n) {
+                        const int vs = vc & 1;
+                        mbar_wait(&v_empty[vs], ((vc >> 1) & 1) ^ 1);
+                        mbar_expect_tx(&v_full[vs], TILE_BYTES);
+                        uint8_t* vd = sV + vs * TILE_BYTES;
+                        // MN-major B operand: boxes of [64 keys][64 head dims], (key half, dim half)
+                        for (int kb = 0; kb < 2; ++kb)
+                            for (int nb = 0; nb < 2; ++nb)
+                                tma_load_2d(&tmV, &v_full[vs], vd + (kb * 2 + nb) * 8192, vcol + 64 * nb,
+                                            row0 + j * TK + 64 * kb);
+                        ++vc;
+                    }
                 }
             }
         }
@@ -149,11 +168,15 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQK, const __grid_constant_
         // ===================== MMA issuer =====================
         if (lane == 0) {
             const uint32_t sq_addr = smem_u32(sQ);
-            mbar_wait(q_full, 0);
+            uint32_t kc = 0, pc = 0, ni = 0;        // S tiles (= K tiles), P V tiles, items
             auto pv = [&](int jp) {
-                const int pb = jp & 1;
-                mbar_wait(&p_full[pb], (jp >> 1) & 1);
-                mbar_wait(&v_full[pb], (jp >> 1) & 1);
+                const int pb = pc & 1;
+                if (jp == 0) {
+                    mbar_wait(o_empty, (ni & 1) ^ 1);   // the last item's O has been read
+                    tc_fence_after();
+                }
+                mbar_wait(&p_full[pb], (pc >> 1) & 1);
+                mbar_wait(&v_full[pb], (pc >> 1) & 1);
                 tc_fence_after();
                 const uint32_t pa = smem_u32(sP + pb * TILE_BYTES), va = smem_u32(sV + pb * TILE_BYTES);
 #pragma unroll
@@ -164,133 +187,160 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQK, const __grid_constant_
                 }
                 tc_commit<1>(&v_empty[pb]);
                 tc_commit<1>(&p_empty[pb]);
+                ++pc;
             };
-            for (int it = 0; it < 2 * n; ++it) {
-                const int b = it & 1, ks = it & 1;
-                mbar_wait(&s_empty[b], ((it >> 1) & 1) ^ 1);
-                mbar_wait(&k_full[ks], (it >> 1) & 1);
-                tc_fence_after();
-                const uint32_t ka = smem_u32(sK + ks * TILE_BYTES);
+            for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++ni) {
+                int qi, h, row0;
+                decode(item, qi, h, row0);
+                const int n = qi + 1;
+                mbar_wait(q_full, ni & 1);
+                for (int it = 0; it < 2 * n; ++it, ++kc) {
+                    const int b = kc & 1;
+                    mbar_wait(&s_empty[b], ((kc >> 1) & 1) ^ 1);
+                    mbar_wait(&k_full[b], (kc >> 1) & 1);
+                    tc_fence_after();
+                    const uint32_t ka = smem_u32(sK + b * TILE_BYTES);
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    const uint64_t ad = make_desc(sq_addr + (kk >> 2) * BOX_BYTES + (kk & 3) * 32, 16, 1024);
-                    const uint64_t bd = make_desc(ka + (kk >> 2) * BOX_BYTES + (kk & 3) * 32, 16, 1024);
-                    tc_mma<1>(tmem + 128 * b, ad, bd, idesc(false), kk > 0 ? 1u : 0u);
+                    for (int kk = 0; kk < 8; ++kk) {
+                        const uint64_t ad = make_desc(sq_addr + (kk >> 2) * BOX_BYTES + (kk & 3) * 32, 16, 1024);
+                        const uint64_t bd = make_desc(ka + (kk >> 2) * BOX_BYTES + (kk & 3) * 32, 16, 1024);
+                        tc_mma<1>(tmem + 128 * b, ad, bd, idesc(false), kk > 0 ? 1u : 0u);
+                    }
+                    tc_commit<1>(&k_empty[b]);
+                    tc_commit<1>(&s_full[b]);
+                    if (it == 2 * n - 1) tc_commit<1>(q_empty);   // Q is free for the next item
+                    if (it > n) pv(it - 1 - n);  // P_(j-1) V_(j-1) behind S_j: the softmax of j-1 overlaps S_j
                 }
-                tc_commit<1>(&k_empty[ks]);
-                tc_commit<1>(&s_full[b]);
-                if (it > n) pv(it - 1 - n);     // P_(j-1) V_(j-1) behind S_j: the softmax of j-1 overlaps S_j
+                pv(n - 1);
+                tc_commit<1>(o_full);
             }
-            pv(n - 1);
-            tc_commit<1>(o_full);
         }
     } else if (warp >= 4) {
         // ===================== softmax + epilogue (thread = query row, column half) =====
         const int quad = warp & 3, half = (warp - 4) >> 2;
         const int r = quad * 32 + lane;
-        const int q_pos = qi * TQ + r;                 // query position in the sequence
         const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-        float m = -INFINITY, l = 0.f;
+        uint32_t sc = 0, pc = 0, ni = 0;              // S tiles, P tiles, items
         uint32_t v[32];
-        // pass 1: this half's row max and normaliser
-        for (int it = 0; it < n; ++it) {
-            const int b = it & 1;
-            mbar_wait(&s_full[b], (it >> 1) & 1);
-            tc_fence_after();
-            const bool diag = it == qi;
-#pragma unroll 1
-            for (int c2 = 0; c2 < 2; ++c2) {
-                const int cc = 2 * half + c2;
-                tmem_ld32(tmem + lane_off + 128 * b + 32 * cc, v);
-                float cm = -INFINITY;
+        for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++ni) {
+            int qi, h, row0;
+            decode(item, qi, h, row0);
+            const int n = qi + 1;
+            const int q_pos = qi * TQ + r;             // query position in the sequence
+            float m = -INFINITY, l = 0.f;
+            // pass 1: this half's row max and normaliser (both 32-column chunks loaded at once;
+            // 4 independent max / sum chains: the serial reductions were the latency limit)
+            for (int it = 0; it < n; ++it, ++sc) {
+                const int b = sc & 1;
+                mbar_wait(&s_full[b], (sc >> 1) & 1);
+                tc_fence_after();
+                const bool diag = it == qi;
+                uint32_t w2[32];
+                tmem_ld32_issue(tmem + lane_off + 128 * b + 32 * (2 * half), v);
+                tmem_ld32_issue(tmem + lane_off + 128 * b + 32 * (2 * half + 1), w2);
+                tmem_wait_ld(v);
+                tmem_wait_ld(w2);
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&s_empty[b]);    // S buffer b is in registers
+                float cm[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    float x = __uint_as_float(v[i]) * scale_log2;
-                    if (diag && it * TK + 32 * cc + i > q_pos) x = -INFINITY;
-                    v[i] = __float_as_uint(x);
-                    cm = fmaxf(cm, x);
+                for (int i = 0; i < 64; ++i) {
+                    const uint32_t raw = i < 32 ? v[i] : w2[i - 32];
+                    float x = __uint_as_float(raw) * scale_log2;
+                    if (diag && it * TK + 64 * half + i > q_pos) x = -INFINITY;
+                    if (i < 32) v[i] = __float_as_uint(x); else w2[i - 32] = __float_as_uint(x);
+                    cm[i & 3] = fmaxf(cm[i & 3], x);
                 }
-                const float mn = fmaxf(m, cm);
+                const float mn = fmaxf(m, fmaxf(fmaxf(cm[0], cm[1]), fmaxf(cm[2], cm[3])));
                 if (mn != -INFINITY) {
-                    float sum = 0.f;
+                    float su[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) sum += ex2(__uint_as_float(v[i]) - mn);
-                    l = l * ex2(m - mn) + sum;
+                    for (int i = 0; i < 64; ++i)
+                        su[i & 3] += ex2(__uint_as_float(i < 32 ? v[i] : w2[i - 32]) - mn);
+                    l = l * ex2(m - mn) + ((su[0] + su[1]) + (su[2] + su[3]));
                     m = mn;
                 }
             }
+            // the two halves' statistics of each row meet (named barrier of the 8 softmax warps)
+            red[(half * 2 + 0) * 128 + r] = m;
+            red[(half * 2 + 1) * 128 + r] = l;
+            asm volatile("bar.sync 1, 256;" ::: "memory");
+            {
+                const float mo = red[((half ^ 1) * 2 + 0) * 128 + r], lo = red[((half ^ 1) * 2 + 1) * 128 + r];
+                const float mm = fmaxf(m, mo);
+                l = (m == -INFINITY ? 0.f : l * ex2(m - mm)) + (mo == -INFINITY ? 0.f : lo * ex2(mo - mm));
+                m = mm;
+            }
+            asm volatile("bar.sync 1, 256;" ::: "memory");     // every read done before P buffer 1 is written
+            const float inv_l = 1.f / l;
+            // pass 2: P = exp2(s - m) / l into shared memory (K-major SW128: box `half` of P)
+            for (int j = 0; j < n; ++j, ++sc, ++pc) {
+                const int b = sc & 1, pb = pc & 1;
+                mbar_wait(&s_full[b], (sc >> 1) & 1);
+                mbar_wait(&p_empty[pb], ((pc >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const bool diag = j == qi;
+                uint8_t* box = sP + pb * TILE_BYTES + half * BOX_BYTES + r * 128;
+                uint32_t w2[32];
+                tmem_ld32_issue(tmem + lane_off + 128 * b + 32 * (2 * half), v);
+                tmem_ld32_issue(tmem + lane_off + 128 * b + 32 * (2 * half + 1), w2);
+                tmem_wait_ld(v);
+                tmem_wait_ld(w2);
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&s_empty[b]);    // S buffer b is in registers
+#pragma unroll
+                for (int c2 = 0; c2 < 2; ++c2) {
+                    const int cc = 2 * half + c2;
+                    uint32_t pk[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const uint32_t r0 = c2 ? w2[2 * i] : v[2 * i], r1 = c2 ? w2[2 * i + 1] : v[2 * i + 1];
+                        float p0 = ex2(__uint_as_float(r0) * scale_log2 - m) * inv_l;
+                        float p1 = ex2(__uint_as_float(r1) * scale_log2 - m) * inv_l;
+                        if (diag && j * TK + 32 * cc + 2 * i > q_pos) p0 = 0.f;
+                        if (diag && j * TK + 32 * cc + 2 * i + 1 > q_pos) p1 = 0.f;
+                        __nv_bfloat162 hv = __floats2bfloat162_rn(p0, p1);
+                        pk[i] = *reinterpret_cast<uint32_t*>(&hv);
+                    }
+#pragma unroll
+                    for (int c4 = 0; c4 < 4; ++c4) {
+                        const int c16 = c2 * 4 + c4;
+                        st_v4(box + ((c16 ^ (r & 7)) << 4), make_uint4(pk[4 * c4], pk[4 * c4 + 1], pk[4 * c4 + 2], pk[4 * c4 + 3]));
+                    }
+                }
+                fence_proxy_async();            // generic-proxy stores -> visible to the tensor core
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&p_full[pb]);
+            }
+            // epilogue: this half's 64 columns of O (TMEM columns 256..383) -> bf16 rows of att
+            mbar_wait(o_full, ni & 1);
+            tc_fence_after();
+            uint32_t o2[2][32];
+            tmem_ld32(tmem + lane_off + 256 + 32 * (2 * half), o2[0]);
+            tmem_ld32(tmem + lane_off + 256 + 32 * (2 * half + 1), o2[1]);
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&s_empty[b]);
-        }
-        // the two halves' statistics of each row meet (named barrier of the 8 softmax warps)
-        red[(half * 2 + 0) * 128 + r] = m;
-        red[(half * 2 + 1) * 128 + r] = l;
-        asm volatile("bar.sync 1, 256;" ::: "memory");
-        {
-            const float mo = red[((half ^ 1) * 2 + 0) * 128 + r], lo = red[((half ^ 1) * 2 + 1) * 128 + r];
-            const float mm = fmaxf(m, mo);
-            l = (m == -INFINITY ? 0.f : l * ex2(m - mm)) + (mo == -INFINITY ? 0.f : lo * ex2(mo - mm));
-            m = mm;
-        }
-        asm volatile("bar.sync 1, 256;" ::: "memory");     // every read done before P buffer 1 is written
-        const float inv_l = 1.f / l;
-        // pass 2: P = exp2(s - m) / l into shared memory (K-major SW128: box `half` of P)
-        for (int j = 0; j < n; ++j) {
-            const int it = n + j, b = it & 1, pb = j & 1;
-            mbar_wait(&s_full[b], (it >> 1) & 1);
-            mbar_wait(&p_empty[pb], ((j >> 1) & 1) ^ 1);
-            tc_fence_after();
-            const bool diag = j == qi;
-            uint8_t* box = sP + pb * TILE_BYTES + half * BOX_BYTES + r * 128;
-#pragma unroll 1
+            if (lane == 0) mbar_arrive(o_empty);        // the next item's first P V may overwrite O
+            const long tok = (long)row0 + qi * TQ + r;
+            bf16* orow = att + tok * d + h * HD;
+#pragma unroll
             for (int c2 = 0; c2 < 2; ++c2) {
                 const int cc = 2 * half + c2;
-                tmem_ld32(tmem + lane_off + 128 * b + 32 * cc, v);
                 uint32_t pk[16];
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
-                    float p0 = ex2(__uint_as_float(v[2 * i]) * scale_log2 - m) * inv_l;
-                    float p1 = ex2(__uint_as_float(v[2 * i + 1]) * scale_log2 - m) * inv_l;
-                    if (diag && j * TK + 32 * cc + 2 * i > q_pos) p0 = 0.f;
-                    if (diag && j * TK + 32 * cc + 2 * i + 1 > q_pos) p1 = 0.f;
-                    __nv_bfloat162 hv = __floats2bfloat162_rn(p0, p1);
+                    __nv_bfloat162 hv = __floats2bfloat162_rn(__uint_as_float(o2[c2][2 * i]), __uint_as_float(o2[c2][2 * i + 1]));
                     pk[i] = *reinterpret_cast<uint32_t*>(&hv);
                 }
 #pragma unroll
-                for (int c4 = 0; c4 < 4; ++c4) {
-                    const int c16 = c2 * 4 + c4;
-                    st_v4(box + ((c16 ^ (r & 7)) << 4), make_uint4(pk[4 * c4], pk[4 * c4 + 1], pk[4 * c4 + 2], pk[4 * c4 + 3]));
-                }
+                for (int c4 = 0; c4 < 4; ++c4)
+                    st_v4(orow + 32 * cc + 8 * c4, make_uint4(pk[4 * c4], pk[4 * c4 + 1], pk[4 * c4 + 2], pk[4 * c4 + 3]));
             }
-            fence_proxy_async();            // generic-proxy stores -> visible to the tensor core
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(&p_full[pb]);
-                mbar_arrive(&s_empty[b]);
-            }
+            if (half == 0) lse[(long)h * T_all + tok] = m + __log2f(l);
         }
-        // epilogue: this half's 64 columns of O (TMEM columns 256..383) -> bf16 rows of att
-        mbar_wait(o_full, 0);
-        tc_fence_after();
-        const long tok = (long)seq_row0 + qi * TQ + r;
-        bf16* orow = att + tok * d + h * HD;
-#pragma unroll 1
-        for (int c2 = 0; c2 < 2; ++c2) {
-            const int cc = 2 * half + c2;
-            tmem_ld32(tmem + lane_off + 256 + 32 * cc, v);
-            uint32_t pk[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                __nv_bfloat162 hv = __floats2bfloat162_rn(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
-                pk[i] = *reinterpret_cast<uint32_t*>(&hv);
-            }
-#pragma unroll
-            for (int c4 = 0; c4 < 4; ++c4)
-                st_v4(orow + 32 * cc + 8 * c4, make_uint4(pk[4 * c4], pk[4 * c4 + 1], pk[4 * c4 + 2], pk[4 * c4 + 3]));
-        }
-        if (half == 0) lse[(long)h * T_all + tok] = m + __log2f(l);
     }
     tc_fence_before();
     __syncthreads();
@@ -316,10 +366,17 @@ int launch_attention_fwd(const void* qkv, void* att, float* lse, int tok0, int n
         cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
         attr = true;
     }
-    const int grid = n_seq * H * (S / TQ);
+    static int num_sms = 0;
+    if (!num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int items = n_seq * H * (S / TQ);
+    const int grid = std::min(items, num_sms);      // persistent: one CTA per SM
     const float scale_log2 = 1.4426950408889634f / sqrtf((float)HD);
     if (launch_k(attn_fwd_kernel, grid, kThreads, kSmem, s, tqk, tv, (bf16*)att, lse, tok0, S, H, d, T_all,
-                 scale_log2) != cudaSuccess)
+                 scale_log2, items) != cudaSuccess)
         return -1;
     return 1;
 }

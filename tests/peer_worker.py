@@ -9,6 +9,10 @@ Special modes (spec["mode"]):
               context poisoned (lancet_peer_status), and writes the message.
   "mismatch"  rank 1 creates its context with another max_tokens; import must fail on every
               rank, and each rank writes the error.
+  "partitioned"  lancet_moe_forward_partitioned (every chunk gated on its own with the carried
+              capacity state, per-chunk size exchange and plan) instead of lancet_moe_forward.
+  "block"     the GPT-MoE block (lancet_block_*) of spec n_seq x S tokens per rank: saves out,
+              h, u and the routing of each step.
 """
 import json
 import os
@@ -55,6 +59,9 @@ def main():
         dist.barrier()
         dist.destroy_process_group()
         return
+    if mode == "block":
+        run_block(spec, r, G, dev, out_dir)
+        return
     ctx = lancet.Context(cfg, world=G, rank=r, device=dev.index, pg=dist.group.WORLD, transport="peer")
     if mode == "timeout":
         ctx.set_peer_timeout_ms(spec.get("timeout_ms", 1500))
@@ -85,7 +92,8 @@ def main():
         w1 = torch.from_numpy(ins["w1"]).to(dev, bf)
         w2 = torch.from_numpy(ins["w2"]).to(dev, bf)
         dy = torch.from_numpy(ins["dy"]).to(dev, bf)
-        y, idx, slot, w = ctx.forward(x, wg, w1, w2, k, spec["cf"], n)
+        fw = ctx.forward_partitioned if mode == "partitioned" else ctx.forward
+        y, idx, slot, w = fw(x, wg, w1, w2, k, spec["cf"], n)
         dx, dwg, dw1, dw2 = ctx.backward(dy)
         torch.cuda.synchronize()
         send, recv, C = ctx.counts(n)
@@ -103,6 +111,32 @@ def main():
     np.savez(os.path.join(out_dir, f"rank{r}.npz"), **res)
     dist.barrier()          # no rank unmaps or frees while a peer may still read its buffers
     ctx.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def run_block(spec, r, G, dev, out_dir):
+    from paper_2404_19429_b200 import block as B
+    bf = torch.bfloat16
+    sh = S.BlockShape(n_seq=spec["n_seq"], seq_len=spec["S"], d=spec["d"], n_heads=spec["H"], f=spec["f"],
+                      E=spec["E"], G=G, k=spec["k"], cf=spec["cf"], n_chunks=spec["n"])
+    moe = lancet.LayerConfig(d_model=sh.d, d_ffn=sh.f, n_experts=sh.E, max_tokens=sh.T, max_k=sh.k, max_chunks=8)
+    blk = B.Block(B.BlockConfig(moe, n_heads=sh.n_heads, seq_len=sh.seq_len, max_capacity_factor=sh.cf),
+                  world=G, rank=r, device=dev.index, pg=dist.group.WORLD)
+    res = {}
+    for step in range(spec.get("repeat", 1)):
+        ins = S.gen_block_rank_inputs(spec["seed"] + step, r, sh, beta=spec.get("beta", 0.5), with_dy=False)
+        p = {key: torch.from_numpy(ins[key]).to(dev, torch.float32 if key in ("ln1_g", "ln1_b", "ln2_g", "ln2_b", "wg")
+                                                else bf) for key in B.PARAMS}
+        out = blk.forward(torch.from_numpy(ins["x"]).to(dev, bf), p, sh.k, sh.cf, sh.n_chunks)
+        torch.cuda.synchronize()
+        _, _, C = blk.moe.counts()
+        res.update({f"out_s{step}": out.float().cpu().numpy(), f"u_s{step}": blk.debug("u", sh.T).float().numpy(),
+                    f"h_s{step}": blk.debug("h", sh.T).float().numpy(), f"idx_s{step}": blk.debug("idx", sh.T).numpy(),
+                    f"slot_s{step}": blk.debug("slot", sh.T).numpy(), f"C_s{step}": np.array(C)})
+    np.savez(os.path.join(out_dir, f"rank{r}.npz"), **res)
+    dist.barrier()
+    blk.close()
     dist.barrier()
     dist.destroy_process_group()
 

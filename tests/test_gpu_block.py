@@ -322,3 +322,55 @@ def test_block_configs3_full_size_sampled(n_chunks):
     assert normwise(got[same], ref[same]) <= TOL["bf16"]
     assert (rt.slot < 0).any()          # capacity binds at this skew
     blk.close()
+
+
+# ---------------------------------------------------------------------------------------------
+# several processes (ranks) on one GPU over the peer transport
+# ---------------------------------------------------------------------------------------------
+
+def _run_peer(tmp_path, G, **spec):
+    from test_gpu_peer import run_peer
+    return run_peer(tmp_path, G, **spec)
+
+
+@pytest.mark.parametrize("G,Ts,E,k,n", [(2, [700, 513], 8, 2, 3), (4, [300, 420, 256, 333], 8, 2, 4),
+                                         (2, [1024, 1024], 4, 1, 2)])
+def test_partitioned_forward_over_processes_matches_the_oracle(tmp_path, G, Ts, E, k, n):
+    """Per-chunk size exchange (column c of the count matrix into every peer's), per-chunk
+    plan with the static regions and the push over G processes: routing and every output of
+    two steps (new inputs each) against the oracle."""
+    from paper_2404_19429_b200 import FLAG_PEER_PUSH
+    from test_gpu_peer import check_steps
+    spec = dict(Ts=Ts, d=128, f=256, E=E, k=k, n=n, cf=1.0, seed=31, repeat=2, mode="partitioned",
+                flags=FLAG_PEER_PUSH)
+    res = _run_peer(tmp_path, G, **spec)
+    check_steps(res, G, spec)
+
+
+@pytest.mark.parametrize("G,n", [(2, 2), (4, 4)])
+def test_block_over_processes_matches_the_oracle(tmp_path, G, n):
+    """The block at world G (E_l = E / G experts per rank, every rank 4 sequences of 128
+    tokens), two steps: h, u and out against the oracle block over G ranks, routing by the
+    margin rule of _routing_check."""
+    from oracle import block as OB
+    spec = dict(n_seq=4, S=128, d=256, H=2, f=256, E=8, k=2, cf=1.0, n=n, seed=37, repeat=2, mode="block",
+                Ts=[512] * G)
+    res = _run_peer(tmp_path, G, **spec)
+    for step in range(2):
+        sh = S.BlockShape(n_seq=4, seq_len=128, d=256, n_heads=2, f=256, E=8, G=G, k=2, cf=1.0, n_chunks=n)
+        ins = [S.gen_block_rank_inputs(37 + step, r, sh, beta=0.5, with_dy=False) for r in range(G)]
+        prm = {key: ins[0][key] for key in ("ln1_g", "ln1_b", "ln2_g", "ln2_b", "w_qkv", "w_o")}
+        ref = OB.block_forward([i["x"] for i in ins], prm, ins[0]["wg"], [i["w1"] for i in ins],
+                               [i["w2"] for i in ins], 2, 128, 2, 1.0, n)
+        for r in range(G):
+            g = res[r]
+            assert normwise(g[f"u_s{step}"], ref.u[r]) <= TOL["bf16"]
+            assert normwise(g[f"h_s{step}"], ref.h[r]) <= TOL["bf16"]
+            rt = ref.moe.routing[r]
+            assert int(g[f"C_s{step}"]) == rt.C
+            assert np.array_equal(g[f"slot_s{step}"], _admit(g[f"idx_s{step}"], rt.C, sh.E))
+            _routing_check(g[f"idx_s{step}"], g[f"slot_s{step}"], rt.logits, rt.idx, rt.slot,
+                           g[f"u_s{step}"].astype(np.float64) - ref.u[r], ins[0]["wg"], sh.k)
+            same = np.all(g[f"idx_s{step}"] == rt.idx, axis=1) & np.all((g[f"slot_s{step}"] >= 0) == (rt.slot >= 0), axis=1)
+            assert same.mean() > 0.95
+            assert normwise(g[f"out_s{step}"][same], ref.out[r][same]) <= TOL["bf16"]
