@@ -68,10 +68,23 @@ lancet_status lancet_block_forward(lancet_block* b, const void* x, const float* 
                                    const float* wg, const void* w1, const void* w2, int32_t T, int32_t k,
                                    double capacity_factor, int32_t n_chunks, void* out, lancet_stream_t stream);
 
+/* Backward of the last block forward (collective when world > 1): gradients of <dout, out>.
+ *   dout [T][d] bf16 in;  dx [T][d] bf16 out;  dln1_g, dln1_b, dln2_g, dln2_b [d] fp32 out;
+ *   dw_qkv [3d][d] fp32 out;  dw_o [d][d] fp32 out;  dwg [d][E] fp32 out (local, as
+ *   lancet_moe_backward);  dw1 [E_l][f][d], dw2 [E_l][d][f] fp32 out.  All overwritten.
+ * Runs the MoE layer's backward (its dW GEMMs overlap its all-to-alls),
+ * then LN2', the output projection's gradients, the attention backward (dK/dV per key tile,
+ * dQ per query tile, P recomputed from the forward's row normaliser), the q|k|v projection's
+ * gradients and LN1'.  Never blocks the host.  LANCET_ERR_STATE without a preceding forward. */
+lancet_status lancet_block_backward(lancet_block* b, const void* dout, void* dx, float* dln1_g, float* dln1_b,
+                                    float* dw_qkv, float* dw_o, float* dln2_g, float* dln2_b, float* dwg,
+                                    float* dw1, float* dw2, lancet_stream_t stream);
+
 /* Copy an intermediate of the last forward to host (tests; synchronises).  which: 0 h [T][d],
  * 1 u = LN2(h) [T][d], 2 att [T][d], 3 qkv [T][3d], 4 a1 = LN1(x) [T][d] (all bf16), 5 lse
  * [H][T] fp32 (log2 of the attention row normaliser in the scaled log2 domain), 6 expert_idx
- * [T][k] int32, 7 slot [T][k] int32 (-1 = dropped).  bytes must match. */
+ * [T][k] int32, 7 slot [T][k] int32 (-1 = dropped); of the last backward: 8 dqkv [T][3d],
+ * 9 dh [T][d], 10 datt [T][d] (bf16).  bytes must match. */
 lancet_status lancet_block_debug_copy(lancet_block* b, int32_t which, void* host_dst, size_t bytes);
 
 #ifdef __cplusplus

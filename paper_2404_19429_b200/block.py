@@ -18,6 +18,7 @@ _BLOCK_SIG = {
     "lancet_block_destroy": None,
     "lancet_block_forward": None,
     "lancet_block_debug_copy": None,
+    "lancet_block_backward": None,
 }
 EXPORTS = list(_BLOCK_SIG)
 
@@ -43,6 +44,8 @@ def _lib():
         lib.lancet_block_destroy.restype = I32
         lib.lancet_block_forward.argtypes = [P] + [P] * 10 + [I32, I32, ctypes.c_double, I32, P, P]
         lib.lancet_block_forward.restype = I32
+        lib.lancet_block_backward.argtypes = [P] * 13
+        lib.lancet_block_backward.restype = I32
         lib.lancet_block_debug_copy.argtypes = [P, I32, P, ctypes.c_size_t]
         lib.lancet_block_debug_copy.restype = I32
         _loaded = True
@@ -127,13 +130,34 @@ class Block:
         self.moe._last_n = n_chunks
         return out
 
+    def backward(self, dout, stream=None):
+        """Gradients of <dout, out> of the last forward: dict(dx, dln1_g, dln1_b, dw_qkv, dw_o,
+        dln2_g, dln2_b, dwg, dw1, dw2)."""
+        x, p = self._last
+        dev = dout.device
+        f32 = torch.float32
+        g = dict(dx=torch.empty_like(dout), dln1_g=torch.empty(p["ln1_g"].shape, dtype=f32, device=dev),
+                 dln1_b=torch.empty(p["ln1_b"].shape, dtype=f32, device=dev),
+                 dw_qkv=torch.empty(p["w_qkv"].shape, dtype=f32, device=dev),
+                 dw_o=torch.empty(p["w_o"].shape, dtype=f32, device=dev),
+                 dln2_g=torch.empty(p["ln2_g"].shape, dtype=f32, device=dev),
+                 dln2_b=torch.empty(p["ln2_b"].shape, dtype=f32, device=dev),
+                 dwg=torch.empty(p["wg"].shape, dtype=f32, device=dev),
+                 dw1=torch.empty(p["w1"].shape, dtype=f32, device=dev),
+                 dw2=torch.empty(p["w2"].shape, dtype=f32, device=dev))
+        order = ("dx", "dln1_g", "dln1_b", "dw_qkv", "dw_o", "dln2_g", "dln2_b", "dwg", "dw1", "dw2")
+        st = _lib().lancet_block_backward(self._p, L._ptr(dout), *[L._ptr(g[n]) for n in order], L._stream(stream))
+        L._check(st, self.moe._p)
+        return g
+
     def debug(self, which: str, T: int):
         """An intermediate of the last forward as a torch CPU tensor: h, u, att, qkv, a1 (bf16),
         lse (fp32 [H][T], log2 domain), idx / slot (int32 [T][k], the MoE layer's routing)."""
         d = self.cfg.moe.d_model
         k = self._k
         shapes = {"h": (0, (T, d)), "u": (1, (T, d)), "att": (2, (T, d)), "qkv": (3, (T, 3 * d)),
-                  "a1": (4, (T, d)), "lse": (5, (self.cfg.n_heads, T)), "idx": (6, (T, k)), "slot": (7, (T, k))}
+                  "a1": (4, (T, d)), "lse": (5, (self.cfg.n_heads, T)), "idx": (6, (T, k)), "slot": (7, (T, k)),
+                  "dqkv": (8, (T, 3 * d)), "dh": (9, (T, d)), "datt": (10, (T, d))}
         w, shape = shapes[which]
         dt = {"lse": torch.float32, "idx": torch.int32, "slot": torch.int32}.get(which, torch.bfloat16)
         t = torch.empty(shape, dtype=dt)

@@ -31,8 +31,16 @@ struct lancet_block {
     std::vector<void*> allocs;
     void *a1 = nullptr, *qkv = nullptr, *att = nullptr, *o = nullptr, *h = nullptr, *u = nullptr;
     float *mu1 = nullptr, *rs1 = nullptr, *mu2 = nullptr, *rs2 = nullptr, *lse = nullptr;
-    int* tok_tab = nullptr;     // [2][kMaxChunks]: rows | first row of each chunk (projection GEMMs)
+    int* tok_tab = nullptr;     // [2][kMaxChunks]: rows | first row of each chunk (projection GEMMs),
+                                // then [2]: rows | first row of the whole batch (weight gradients)
     int T_last = 0;
+    // backward workspace and the last forward's arguments (pointers only; the caller keeps them)
+    void *du = nullptr, *dh = nullptr, *datt = nullptr, *dqkv = nullptr, *da1 = nullptr;
+    float *Dbuf = nullptr, *ln_partial = nullptr;
+    const void *x = nullptr, *w_qkv = nullptr, *w_o = nullptr;
+    const float *ln1_g = nullptr, *ln2_g = nullptr;
+    int n_last = 0;
+    bool have_fwd = false;
 };
 
 namespace {
@@ -60,6 +68,10 @@ __global__ void tok_tab_kernel(int* tab, int n, int Tc)
     if (c < n) {
         tab[c] = Tc;
         tab[kMaxChunks + c] = c * Tc;
+    }
+    if (c == 0) {
+        tab[2 * kMaxChunks] = n * Tc;
+        tab[2 * kMaxChunks + 1] = 0;
     }
 }
 
@@ -108,7 +120,10 @@ LANCET_API lancet_status lancet_block_create_peer(lancet_block** out, int32_t wo
     bool ok = al(&b->a1, T * d * 2) && al(&b->qkv, T * 3 * d * 2) && al(&b->att, T * d * 2) && al(&b->o, T * d * 2) &&
               al(&b->h, T * d * 2) && al(&b->u, T * d * 2) && al((void**)&b->mu1, T * 4) && al((void**)&b->rs1, T * 4) &&
               al((void**)&b->mu2, T * 4) && al((void**)&b->rs2, T * 4) && al((void**)&b->lse, T * 4 * cfg->n_heads) &&
-              al((void**)&b->tok_tab, sizeof(int) * 2 * kMaxChunks);
+              al((void**)&b->tok_tab, sizeof(int) * (2 * kMaxChunks + 2)) && al(&b->du, T * d * 2) &&
+              al(&b->dh, T * d * 2) && al(&b->datt, T * d * 2) && al(&b->dqkv, T * 3 * d * 2) && al(&b->da1, T * d * 2) &&
+              al((void**)&b->Dbuf, T * 4 * cfg->n_heads) &&
+              al((void**)&b->ln_partial, sizeof(float) * ln_bwd_partial_floats((int)T, (int)d));
     if (!ok || cudaStreamCreateWithFlags(&b->s_pre, cudaStreamNonBlocking) != cudaSuccess) {
         lancet_block_destroy(b);
         return bfail(nullptr, LANCET_ERR_NOMEM, "block workspace allocation failed");
@@ -197,10 +212,84 @@ LANCET_API lancet_status lancet_block_forward(lancet_block* b, const void* x, co
         if (ce != cudaSuccess) return bfail(b, LANCET_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(ce));
         return LANCET_OK;
     };
+    b->have_fwd = false;
     st = moe_forward_chunked(c, b->u, wg, w1, w2, T, k, cf, out, in, s);
     if (st) return st;
     c->launches_fwd += extra;
     b->T_last = T;
+    b->n_last = n;
+    b->x = x; b->w_qkv = w_qkv; b->w_o = w_o; b->ln1_g = ln1_g; b->ln2_g = ln2_g;
+    b->have_fwd = true;
+    return LANCET_OK;
+}
+
+// Backward of the block (the chain rule of lancet_block.h's forward, R19), on the
+// caller's stream after the MoE layer's own backward (which overlaps
+// its all-to-alls with its dW GEMMs):
+//   du = the MoE layer's input gradient (lancet_moe_backward of dy = dout)
+//   dh = dout + LN2'(du);  dW_o = dh^T att;  datt = dh W_o;  dqkv = Attn'(datt)
+//   dW_qkv = dqkv^T a1;  da1 = dqkv W_qkv;  dx = dh + LN1'(da1)
+// The projection weight gradients run on the compute stream after their input-gradient GEMM
+// (nothing downstream waits for them).
+LANCET_API lancet_status lancet_block_backward(lancet_block* b, const void* dout, void* dx, float* dln1_g,
+                                               float* dln1_b, float* dw_qkv, float* dw_o, float* dln2_g,
+                                               float* dln2_b, float* dwg, float* dw1, float* dw2,
+                                               lancet_stream_t stream_)
+{
+    if (!b) return bfail(nullptr, LANCET_ERR_ARG, "block is NULL");
+    lancet_ctx* c = b->moe;
+    lancet_status st = ctx_ready(c);
+    if (st) return st;
+    if (!b->have_fwd) return bfail(b, LANCET_ERR_STATE, "block backward without a block forward");
+    const void* ptrs[] = {dout, dx, dln1_g, dln1_b, dw_qkv, dw_o, dln2_g, dln2_b, dwg, dw1, dw2};
+    for (const void* p : ptrs) {
+        if (!p) return bfail(b, LANCET_ERR_ARG, "null required pointer");
+        if (!aligned(p)) return bfail(b, LANCET_ERR_ARG, "every tensor must be 16-byte aligned");
+    }
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream_);
+    const int T = b->T_last, d = b->d, H = b->H;
+    st = moe_backward_into(c, dout, b->du, dwg, dw1, dw2, s);
+    if (st) return st;
+    b->have_fwd = false;
+    int L = 0;
+    const int* all_rows = b->tok_tab + 2 * kMaxChunks;
+    const int* all_off = all_rows + 1;
+    size_t op = op_begin(c, "ln2_bwd", 0, -1, s);
+    int r = launch_layer_norm_bwd(b->du, b->h, b->mu2, b->rs2, b->ln2_g, dout, b->dh, b->ln_partial, dln2_g, dln2_b,
+                                  T, d, s);
+    op_end(c, op, s);
+    if (r < 0) return bfail(b, LANCET_ERR_UNSUPPORTED, "LayerNorm backward shape");
+    L += r;
+    op = op_begin(c, "o_proj_dx", 0, -1, s);
+    st = dense_gemm_bmn(c, b->dh, T, b->w_o, d, d, b->datt, T, all_rows, all_off, 1, T, s, &L);
+    op_end(c, op, s);
+    if (st) return st;
+    op = op_begin(c, "o_proj_dw", 0, -1, s);
+    st = dense_wgrad(c, b->dh, d, b->att, d, d, d, T, all_rows, all_off, dw_o, s, &L);
+    op_end(c, op, s);
+    if (st) return st;
+    op = op_begin(c, "attention_bwd", 0, -1, s);
+    r = launch_attention_bwd(b->qkv, b->att, b->datt, b->lse, b->Dbuf, b->dqkv, 0, T / b->S, b->S, H, d, T, s);
+    op_end(c, op, s);
+    if (r < 0) return bfail(b, LANCET_ERR_UNSUPPORTED, "attention backward: shape or tensor maps");
+    L += r;
+    op = op_begin(c, "qkv_proj_dx", 0, -1, s);
+    st = dense_gemm_bmn(c, b->dqkv, T, b->w_qkv, d, 3 * d, b->da1, T, all_rows, all_off, 1, T, s, &L);
+    op_end(c, op, s);
+    if (st) return st;
+    op = op_begin(c, "qkv_proj_dw", 0, -1, s);
+    st = dense_wgrad(c, b->dqkv, 3 * d, b->a1, d, 3 * d, d, T, all_rows, all_off, dw_qkv, s, &L);
+    op_end(c, op, s);
+    if (st) return st;
+    op = op_begin(c, "ln1_bwd", 0, -1, s);
+    r = launch_layer_norm_bwd(b->da1, b->x, b->mu1, b->rs1, b->ln1_g, b->dh, dx, b->ln_partial, dln1_g, dln1_b, T, d,
+                              s);
+    op_end(c, op, s);
+    if (r < 0) return bfail(b, LANCET_ERR_UNSUPPORTED, "LayerNorm backward shape");
+    L += r;
+    cudaError_t ce = cudaGetLastError();
+    if (ce != cudaSuccess) return bfail(b, LANCET_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(ce));
+    c->launches_bwd += L;
     return LANCET_OK;
 }
 
@@ -219,6 +308,9 @@ LANCET_API lancet_status lancet_block_debug_copy(lancet_block* b, int32_t which,
     case 5: src = b->lse; need = (size_t)b->H * T * 4; break;    // [H][T] of the last forward
     case 6: src = b->moe->idx; need = T * b->moe->k * 4; break;   // the MoE layer's routing
     case 7: src = b->moe->slot; need = T * b->moe->k * 4; break;
+    case 8: src = b->dqkv; need = T * 3 * d * 2; break;          // the last backward's
+    case 9: src = b->dh; need = T * d * 2; break;
+    case 10: src = b->datt; need = T * d * 2; break;
     default: return bfail(b, LANCET_ERR_ARG, "bad `which`");
     }
     if (bytes != need) return bfail(b, LANCET_ERR_ARG, "bytes must match the buffer");

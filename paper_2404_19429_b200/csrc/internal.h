@@ -35,6 +35,18 @@ lancet_status dense_gemm(lancet_ctx* c, const void* A, long a_rows, const void* 
                          long c_rows, const int* grp_rows, const int* grp_off, int n_groups, int max_rows,
                          cudaStream_t s, int* launches);
 
+// C[rows] = A[rows] B for B stored [K][N] row-major (read as an MN-major operand): the
+// projections' input gradients dX = dY W
+lancet_status dense_gemm_bmn(lancet_ctx* c, const void* A, long a_rows, const void* B, int N, int K, void* C,
+                             long c_rows, const int* grp_rows, const int* grp_off, int n_groups, int max_rows,
+                             cudaStream_t s, int* launches);
+// C[M][N] (fp32, overwritten) = sum over the group's rows t of A[t][m] B[t][n] (K-grouped, one
+// group): the projections' weight gradients dW = dY^T X
+lancet_status dense_wgrad(lancet_ctx* c, const void* A, int lda, const void* B, int ldb, int M, int N, long rows_ext,
+                          const int* grp_rows, const int* grp_off, float* C, cudaStream_t s, int* launches);
+lancet_status moe_backward_into(lancet_ctx* c, const void* dy, void* dx, float* dwg, float* dw1, float* dw2,
+                                cudaStream_t s);
+
 // timeline records of the context (LANCET_FLAG_TIMELINE): begin returns a handle for end
 size_t op_begin(lancet_ctx* c, const char* name, int lane, int chunk, cudaStream_t s);
 void op_end(lancet_ctx* c, size_t h, cudaStream_t s);

@@ -126,6 +126,18 @@ int launch_attention_fwd(const void* qkv, void* att, float* lse, int tok0, int n
 int launch_layer_norm(const void* a, const void* resid, void* hout, const float* g, const float* b, void* y,
                       float* mean, float* rstd, int rows, int d, cudaStream_t s);
 
+// Backward of the causal attention (attention_bwd.cu): dqkv [T_all][3d] bf16 (dq | dk | dv) of
+// the n_seq sequences starting at tok0, from qkv, att (= O), datt (= dO), lse (forward's, log2
+// domain); Dbuf [H][T_all] fp32 scratch (D = rowsum(dO O)).  Returns launches or -1.
+int launch_attention_bwd(const void* qkv, const void* att, const void* datt, const float* lse, float* Dbuf,
+                         void* dqkv, int tok0, int n_seq, int S, int H, int d, int T_all, cudaStream_t s);
+// LayerNorm backward: out = resid + dLN/dx (bf16), dg / db [d] fp32 (overwritten); x is the LN
+// input (bf16), mean / rstd the forward's; partial: ln_bwd_partial_floats(rows, d) fp32 scratch.
+int launch_layer_norm_bwd(const void* dy, const void* x, const float* mean, const float* rstd, const float* g,
+                          const void* resid, void* out, float* partial, float* dg, float* db, int rows, int d,
+                          cudaStream_t s);
+size_t ln_bwd_partial_floats(int rows, int d);
+
 // ---- grouped GEMMs (gemm_simt.cu, gemm_tc.cu) --------------------------------------------
 enum GemmMode { GEMM_M_GROUPED = 0, GEMM_K_GROUPED = 1 };
 enum GemmEpi { EPI_STORE = 0, EPI_ACT = 1, EPI_DACT = 2, EPI_F32 = 3 };

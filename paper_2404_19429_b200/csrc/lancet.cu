@@ -951,6 +951,32 @@ lancet_status dense_gemm(lancet_ctx* c, const void* A, long a_rows, const void* 
     return run_gemm(c, a, s, launches);
 }
 
+lancet_status dense_gemm_bmn(lancet_ctx* c, const void* A, long a_rows, const void* B, int N, int K, void* C,
+                             long c_rows, const int* grp_rows, const int* grp_off, int n_groups, int max_rows,
+                             cudaStream_t s, int* launches)
+{
+    GemmArgs a{};
+    a.mode = GEMM_M_GROUPED; a.n_groups = n_groups; a.gpw = n_groups; a.n_weights = 1;
+    a.grp_rows = grp_rows; a.grp_off = grp_off; a.max_rows = max_rows; a.act = 0;
+    a.A = A; a.lda = K; a.a_rows = a_rows; a.a_mn = false;
+    a.B = B; a.ldb = N; a.b_group_stride = 0; a.b_rows = K; a.b_mn = true;
+    a.C = C; a.C2 = nullptr; a.ldc = N; a.c_rows = c_rows; a.N = N; a.K = K; a.epi = EPI_STORE;
+    return run_gemm(c, a, s, launches);
+}
+
+lancet_status dense_wgrad(lancet_ctx* c, const void* A, int lda, const void* B, int ldb, int M, int N, long rows_ext,
+                          const int* grp_rows, const int* grp_off, float* C, cudaStream_t s, int* launches)
+{
+    GemmArgs a{};
+    a.mode = GEMM_K_GROUPED; a.n_groups = 1; a.gpw = 1; a.n_weights = 1;
+    a.grp_rows = grp_rows; a.grp_off = grp_off; a.accumulate = 0;
+    a.a_mn = true; a.b_mn = true; a.epi = EPI_F32; a.b_group_stride = 0;
+    a.a_rows = rows_ext; a.b_rows = rows_ext;
+    a.A = A; a.lda = lda; a.B = B; a.ldb = ldb;
+    a.C = C; a.ldc = N; a.c_group_stride = (long)M * N; a.M = M; a.N = N;
+    return run_gemm(c, a, s, launches);
+}
+
 // Forward of the MoE layer in block mode (push transport; LANCET_FLAG_PEER_PUSH).  Per chunk
 // ch, stage by stage (S1 with the non-MoE part in the pipeline, fig:part_all):
 //   producer stream:  produce(ch) [the block's LN1 / attention / projections / LN2], then the
@@ -1645,6 +1671,14 @@ LANCET_API lancet_status lancet_moe_forward_partitioned(lancet_ctx* c, const voi
     if (combine_w) CK(cudaMemcpyAsync(combine_w, c->w, tk * sizeof(float), cudaMemcpyDeviceToDevice, s));
     return LANCET_OK;
 }
+
+namespace lancet {
+lancet_status moe_backward_into(lancet_ctx* c, const void* dy, void* dx, float* dwg, float* dw1, float* dw2,
+                                cudaStream_t s)
+{
+    return lancet_moe_backward(c, dy, dx, dwg, dw1, dw2, reinterpret_cast<lancet_stream_t>(s));
+}
+}  // namespace lancet
 
 LANCET_API lancet_status lancet_moe_backward(lancet_ctx* c, const void* dy, void* dx, float* dwg,
                                              float* dw1, float* dw2, lancet_stream_t stream_)

@@ -374,3 +374,73 @@ def test_block_over_processes_matches_the_oracle(tmp_path, G, n):
             same = np.all(g[f"idx_s{step}"] == rt.idx, axis=1) & np.all((g[f"slot_s{step}"] >= 0) == (rt.slot >= 0), axis=1)
             assert same.mean() > 0.95
             assert normwise(g[f"out_s{step}"][same], ref.out[r][same]) <= TOL["bf16"]
+
+
+def _margin_mask(logits, u, wg, k):
+    """Tokens whose top-(k+1) logit margins (oracle side only) exceed an 8-sigma bound of what a
+    one-ulp bf16 difference of the gate input u can move: their routing is the same on both
+    sides."""
+    d = wg.shape[0]
+    diff_rms = max(np.sqrt(np.mean((wg[:, a] - wg[:, b]) ** 2))
+                   for a in range(wg.shape[1]) for b in range(a + 1, wg.shape[1]))
+    du_rms = 2.0 ** -8 * np.sqrt(np.mean(u ** 2))
+    bound = 8 * du_rms * np.sqrt(d) * diff_rms
+    srt = -np.sort(-logits.astype(np.float64), axis=1)
+    kk = min(k + 1, srt.shape[1])
+    return np.min(srt[:, :kk - 1] - srt[:, 1:kk], axis=1) > bound
+
+
+@pytest.mark.parametrize("n_seq,S_,d,H,f,E,k,n,seed", [(4, 256, 256, 2, 512, 4, 2, 2, 11),
+                                                        (2, 384, 384, 3, 256, 8, 1, 2, 12),
+                                                        (8, 128, 256, 2, 256, 4, 1, 4, 13)])
+def test_block_backward_matches_the_oracle(n_seq, S_, d, H, f, E, k, n, seed):
+    """lancet_block_backward vs oracle/block.py block_backward: dx, both LayerNorms' gains and
+    biases, W_qkv, W_o, Wg, W1, W2 (normwise, bf16 bar).  Capacity not binding (cf = E / k: no
+    drops, so a token's routing affects only its own output) and dout = 0 on the tokens whose
+    oracle-side top-k margin is within reach of bf16 rounding of the gate input (_margin_mask),
+    so every remaining token routes the same way on both sides (checked) and the aggregated
+    gradients are comparable."""
+    from oracle import block as OB
+    cf = E / k
+    sh = S.BlockShape(n_seq=n_seq, seq_len=S_, d=d, n_heads=H, f=f, E=E, G=1, k=k, cf=cf, n_chunks=n)
+    ins = S.gen_block_rank_inputs(seed, 0, sh, beta=0.5)
+    prm = {key: ins[key] for key in ("ln1_g", "ln1_b", "ln2_g", "ln2_b", "w_qkv", "w_o")}
+    ref = OB.block_forward([ins["x"]], prm, ins["wg"], [ins["w1"]], [ins["w2"]], H, S_, k, cf, n)
+    rt = ref.moe.routing[0]
+    keep = _margin_mask(rt.logits, ref.u[0], ins["wg"], k)
+    dout = S.gen_dy(seed + 1, 0, sh.T, d) * keep[:, None]
+    blk = _block(sh, cf_max=cf)
+    p = _dev_params(ins)
+    blk.forward(to_dev(ins["x"], bf), p, k, cf, n)
+    g = blk.backward(to_dev(dout, bf))
+    torch.cuda.synchronize()
+    assert np.array_equal(blk.debug("idx", sh.T).numpy()[keep], rt.idx[keep])
+    assert keep.mean() > 0.75
+    rb = OB.block_backward(ref, [ins["x"]], prm, ins["wg"], [ins["w1"]], [ins["w2"]], [dout], H, S_)
+    for key in ("dx", "dln1_g", "dln1_b", "dw_qkv", "dw_o", "dln2_g", "dln2_b", "dwg", "dw1", "dw2"):
+        got = g[key].float().cpu().numpy()
+        e = normwise(got, rb[key][0])
+        assert e <= TOL["bf16"], (key, e)
+    blk.close()
+
+
+def test_block_backward_chunk_invariance():
+    """The backward of a forward with n = 1 and with n = 4 chunks gives the same input and LN /
+    projection gradients bit for bit, the expert weight gradients within fp32 reassociation (the
+    merged dW GEMMs see another receive layout)."""
+    sh = S.BlockShape(n_seq=4, seq_len=256, d=256, n_heads=2, f=512, E=8, G=1, k=2, cf=1.0, n_chunks=1)
+    ins = S.gen_block_rank_inputs(29, 0, sh, beta=0.5)
+    dout = to_dev(S.gen_dy(30, 0, sh.T, sh.d), bf)
+    res = []
+    for n in (1, 4):
+        blk = _block(sh)
+        p = _dev_params(ins)
+        blk.forward(to_dev(ins["x"], bf), p, sh.k, sh.cf, n)
+        g = blk.backward(dout)
+        torch.cuda.synchronize()
+        res.append({key: v.cpu() for key, v in g.items()})
+        blk.close()
+    for key in ("dx", "dln1_g", "dln1_b", "dw_qkv", "dw_o", "dln2_g", "dln2_b", "dwg"):
+        assert torch.equal(res[0][key], res[1][key]), key
+    for key in ("dw1", "dw2"):
+        assert normwise(res[1][key].numpy(), res[0][key].numpy()) <= 1e-5
