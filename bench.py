@@ -491,10 +491,17 @@ def block_record(a, world, rank, local_rank, stream, barrier, max_over_ranks, ns
                   world=world, rank=rank, device=local_rank, pg=dist.group.WORLD if world > 1 else None)
     base = blk.moe.cfg.flags
 
-    def run(n, fl, steps, instrumented=False):
+    dout = torch.randn(x.shape, generator=torch.Generator(device=dev).manual_seed(a.seed + 8), device=dev).to(bf)
+
+    def one(n, bwd):
+        blk.forward(x, p, sh.k, sh.cf, n, out=out)
+        if bwd:
+            blk.backward(dout)
+
+    def run(n, fl, steps, instrumented=False, bwd=False):
         blk.moe.set_flags(base | fl | (lancet.FLAG_TIMELINE if instrumented else 0))
         for _ in range(3):
-            blk.forward(x, p, sh.k, sh.cf, n, out=out)
+            one(n, bwd)
         torch.cuda.synchronize()
         if instrumented:
             blk.moe.timeline_begin(stream)
@@ -503,7 +510,7 @@ def block_record(a, world, rank, local_rank, stream, barrier, max_over_ranks, ns
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(steps):
-            blk.forward(x, p, sh.k, sh.cf, n, out=out)
+            one(n, bwd)
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -512,7 +519,7 @@ def block_record(a, world, rank, local_rank, stream, barrier, max_over_ranks, ns
     steps = max(5, min(a.steps, 30))
     for _ in range(max(3, min(a.warmup, 20))):
         blk.forward(x, p, sh.k, sh.cf, 4, out=out)
-    by_n, ops4 = [], None
+    by_n, ops4, opsb = [], None, None
     for n in ns:
         ms, _ = run(n, 0, steps)
         _, tl = run(n, 0, steps, True)
@@ -521,12 +528,16 @@ def block_record(a, world, rank, local_rank, stream, barrier, max_over_ranks, ns
         unover = sum(r["end_us"] - r["start_us"] for r in tls if r["lane"] == 1) / 3 / 1000.0
         ms_serial, _ = run(n, lancet.FLAG_SERIAL, steps)
         ms_nocomm, _ = run(n, lancet.FLAG_NO_COMM, steps)
+        ms_fb, _ = run(n, 0, steps, bwd=True)
         by_n.append({"n_chunks": n, "ms_per_step": ms, "tokens_per_s": world * sh.T / (ms / 1000.0),
+                     "fwd_bwd_ms_per_step": ms_fb, "fwd_bwd_tokens_per_s": world * sh.T / (ms_fb / 1000.0),
                      "exposed_a2a_ms": max_over_ranks(exposed), "a2a_ms_on_comm_lane": max_over_ranks(comm),
                      "unoverlapped_a2a_ms": max_over_ranks(unover), "serial_ms_per_step": ms_serial,
                      "no_comm_ms_per_step": ms_nocomm, "exposed_upper_bound_ms": ms - ms_nocomm})
         if n == 4:
             ops4 = op_stats(tl, steps)
+            _, tlb = run(n, 0, steps, True, bwd=True)
+            opsb = op_stats(tlb, steps)
     blk.moe.set_flags(base)
     best = min(by_n, key=lambda r: r["ms_per_step"])
     pk = peaks()
@@ -540,10 +551,13 @@ def block_record(a, world, rank, local_rank, stream, barrier, max_over_ranks, ns
         "workload": f"GPT-MoE block forward (BASELINE configs[3]): {sh.n_seq}x{sh.seq_len} tokens/GPU, d_model={sh.d}, "
                     f"{sh.n_heads} heads, ffn={sh.f}, experts={sh.E} ({sh.E // world}/GPU), Switch top-1, cf={sh.cf}, "
                     f"bf16; MoE over the peer push transport" + (" (one-rank group: exchanges to self)" if world == 1 else ""),
-        "metric": "block forward tokens/s; exposed all-to-all ms/iter", "unit": "tokens/s",
+        "metric": "block forward tokens/s (fwd_bwd_value: forward + backward); exposed all-to-all ms/iter",
+        "unit": "tokens/s",
         "value": world * sh.T / (best["ms_per_step"] / 1000.0), "best_n_chunks": best["n_chunks"],
         "by_n": by_n,
         "ops_us_per_step_n4": {o: round(v["us_per_step"], 2) for o, v in (ops4 or {}).items()},
+        "fwd_bwd_ops_us_per_step_n4": {o: round(v["us_per_step"], 2) for o, v in (opsb or {}).items()},
+        "fwd_bwd_value": world * sh.T / (min(r["fwd_bwd_ms_per_step"] for r in by_n) / 1000.0),
         "attention_roofline": {
             "bound": "tensor", "achieved": att_flops / (att_us * 1e-6) / 1e12 if att_us else None,
             "peak": pk["bf16_sus"], "unit": "TFLOP/s",

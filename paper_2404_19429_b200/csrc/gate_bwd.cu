@@ -314,7 +314,8 @@ k6_stream_kernel(const Elt* __restrict__ dxe, const int* __restrict__ prow,
     const int NTD = NT / EG, dg = threadIdx.x / EG, eg = threadIdx.x % EG, tid = threadIdx.x;
     const bool copier = eg == 0;
     int* srow = reinterpret_cast<int*>(ring + (size_t)S * G::SLOT * NTD);  // [tpb][KK]
-    float* sdl = reinterpret_cast<float*>(srow + tpb * KK);                 // [tpb][ET]
+    // [tpb][ET], 16-byte aligned (float2 reads): tpb * KK ints rounded up to 4
+    float* sdl = reinterpret_cast<float*>(srow + round_up(tpb * KK, 4));
     const int tb0 = t0 + blockIdx.x * tpb;
     const int tb1 = min(t1, tb0 + tpb);
     if (tb0 >= tb1) return;
@@ -557,7 +558,7 @@ gate_bwd_fused_kernel(const Elt* __restrict__ dxe, const int* __restrict__ prow,
     extern __shared__ __align__(16) uint4 ring[];          // [S][SLOT][NT]
     const int NT = NTC > 0 ? NTC : (int)blockDim.x, tid = threadIdx.x;
     int* srow = reinterpret_cast<int*>(ring + (size_t)S * G::SLOT * NT);   // [tpb][KK]
-    float* sdl = reinterpret_cast<float*>(srow + tpb * KK);                 // [tpb][EE]
+    float* sdl = reinterpret_cast<float*>(srow + round_up(tpb * KK, 4));    // [tpb][EE], 16 B aligned
     const int tb0 = blockIdx.x * tpb;
     const int nt = max(0, min(T, tb0 + tpb) - tb0);
     for (int q = tid; q < nt * KK; q += NT) {
@@ -776,7 +777,7 @@ bool gate_bwd_needs_wgT(int d, int E) { return !stream_ok(d, E) && !(wide_ok(d, 
 // beside a fixed ring: at least `want` blocks, more if the range would not fit (large T).
 static int blocks_for_smem(int ntok, int want, size_t ring, size_t per_tok)
 {
-    const size_t budget = 200 * 1024;
+    const size_t budget = 200 * 1024 - 16;     // - 16: the 16-byte alignment of the staged dlogit
     const int max_tpb = std::max(1, (int)((budget - std::min(ring, budget - per_tok)) / per_tok));
     return std::max(want, ceil_div(ntok, max_tpb));
 }
@@ -802,7 +803,7 @@ static void launch_k6_stream(const DispatchArgs& a, const void* dxe, const int* 
     const int nb = blocks_for_smem(t1 - t0, std::max(1, std::min(ceil_div(t1 - t0, G::U), per_sm * num_sms)),
                                    (size_t)kStreamStages * G::SLOT * NT * 16, (size_t)(KK + EE) * 4);
     const int tpb = ceil_div(t1 - t0, nb);
-    const size_t smem = (size_t)kStreamStages * G::SLOT * NT * 16 + (size_t)tpb * (KK + EE) * 4;
+    const size_t smem = (size_t)kStreamStages * G::SLOT * NT * 16 + ((size_t)round_up(tpb * KK, 4) + (size_t)tpb * EE) * 4;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k6_stream_kernel<Elt, KK, EE, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -827,7 +828,7 @@ static void launch_k6_wide(const DispatchArgs& a, const void* dxe, const int* pr
     const int nb = blocks_for_smem(t1 - t0, std::max(1, std::min(ceil_div(t1 - t0, G::U), std::max(1, 3 * num_sms / DS))),
                                    (size_t)kStreamStages * G::SLOT * NTD * 16, (size_t)(KK + 8 * EG) * 4);
     const int tpb = ceil_div(t1 - t0, nb);
-    const size_t smem = (size_t)kStreamStages * G::SLOT * NTD * 16 + (size_t)tpb * (KK + 8 * EG) * 4;
+    const size_t smem = (size_t)kStreamStages * G::SLOT * NTD * 16 + ((size_t)round_up(tpb * KK, 4) + (size_t)tpb * 8 * EG) * 4;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k6_stream_kernel<Elt, KK, 8, 0, EG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -993,7 +994,7 @@ static void launch_fused(const DispatchArgs& a, const void* dxe, const int* prow
                                             (size_t)kFusedStages * G::SLOT * NT * 16, (size_t)(KK + EE) * 4));
     const int tpb = ceil_div(a.T, nb);
     const int grid = ceil_div(a.T, tpb);
-    const size_t smem = (size_t)kFusedStages * G::SLOT * NT * 16 + (size_t)tpb * (KK + EE) * 4;
+    const size_t smem = (size_t)kFusedStages * G::SLOT * NT * 16 + ((size_t)round_up(tpb * KK, 4) + (size_t)tpb * EE) * 4;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(gate_bwd_fused_kernel<Elt, KK, EE, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);

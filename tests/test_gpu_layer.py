@@ -352,6 +352,20 @@ def test_large_token_count_gate_backward(E):
         assert normwise(g[key], o[key]) <= TOL["bf16"], key
 
 
+@pytest.mark.parametrize("T,E,k", [(4097, 32, 1), (2053, 16, 1), (3001, 32, 3)])
+def test_gate_backward_odd_tokens_per_block(T, E, k):
+    # the wide / streaming K6 stage an odd number of (tokens x choices) row ids in front of the
+    # dlogit rows they read as float2: the dlogit staging is 16-byte aligned (an odd count once
+    # faulted at E = 32, k = 1, d = 2048 -- found by compute-sanitizer on the block backward)
+    d = 2048
+    ins = inputs(T, d, 8, E, k, beta=0.25, seed=65)
+    g = run_gpu(ins, E, k, 1.0, 2, act="identity_expert")
+    o = run_oracle(ins, k, 1.0, 2, act="identity_expert")
+    assert_routing_exact(g, o)
+    for key in ("y", "dx", "dwg"):
+        assert normwise(g[key], o[key]) <= TOL["bf16"], key
+
+
 @pytest.mark.parametrize("n,act,serial", [(1, "gelu_tanh", False), (3, "gelu_tanh", False),
                                           (2, "identity_expert", False), (4, "gelu_tanh", True),
                                           (3, "identity_expert", True)])
