@@ -426,6 +426,7 @@ ln_bwd_rows_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ x, cons
     const long base = (long)row * d;
     const float mu = mean[row], rs = rstd[row];
     float s1 = 0.f, s2 = 0.f;
+#pragma unroll 4
     for (int col = lane * 8; col < d; col += 256) {
         float xv[8], dv[8], gg[8];
         unpack16<bf16>(ld_v4(x + base + col), xv);
@@ -440,6 +441,7 @@ ln_bwd_rows_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ x, cons
         }
     }
     const float m1 = warp_sum(s1) / (float)d, m2 = warp_sum(s2) / (float)d;
+#pragma unroll 4
     for (int col = lane * 8; col < d; col += 256) {
         float xv[8], dv[8], gg[8], rv[8], o[8];
         unpack16<bf16>(ld_v4(x + base + col), xv);
@@ -453,40 +455,65 @@ ln_bwd_rows_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ x, cons
     }
 }
 
-constexpr int kLnColChunk = 256;   // rows per column-partial block
+constexpr int kLnColChunk = 32;    // rows per column-partial block
+// thread = 8 consecutive columns (16-byte loads), block = 2048 columns x 32 rows
 __global__ void __launch_bounds__(256)
 ln_bwd_cols_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ x, const float* __restrict__ mean,
                    const float* __restrict__ rstd, float* __restrict__ partial, int rows, int d)
 {
     pdl_wait();
-    const int col = blockIdx.x * 256 + threadIdx.x;
+    const int col = (blockIdx.x * 256 + threadIdx.x) * 8;
     if (col >= d) return;
     const int r0 = blockIdx.y * kLnColChunk, r1 = min(rows, r0 + kLnColChunk);
-    float a = 0.f, b = 0.f;
+    float a[8], b[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = b[i] = 0.f;
+#pragma unroll 4
     for (int r = r0; r < r1; ++r) {
-        const float dv = __bfloat162float(dy[(long)r * d + col]);
-        const float xh = (__bfloat162float(x[(long)r * d + col]) - mean[r]) * rstd[r];
-        a = fmaf(dv, xh, a);
-        b += dv;
+        float dv[8], xv[8];
+        unpack16<bf16>(ld_nc_v4(dy + (long)r * d + col), dv);
+        unpack16<bf16>(ld_nc_v4(x + (long)r * d + col), xv);
+        const float mu = __ldg(mean + r), rs = __ldg(rstd + r);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            a[i] = fmaf(dv[i], (xv[i] - mu) * rs, a[i]);
+            b[i] += dv[i];
+        }
     }
-    partial[((size_t)blockIdx.y * 2 + 0) * d + col] = a;
-    partial[((size_t)blockIdx.y * 2 + 1) * d + col] = b;
+    float* pa = partial + ((size_t)blockIdx.y * 2 + 0) * d + col;
+    float* pb = partial + ((size_t)blockIdx.y * 2 + 1) * d + col;
+    *reinterpret_cast<float4*>(pa) = make_float4(a[0], a[1], a[2], a[3]);
+    *reinterpret_cast<float4*>(pa + 4) = make_float4(a[4], a[5], a[6], a[7]);
+    *reinterpret_cast<float4*>(pb) = make_float4(b[0], b[1], b[2], b[3]);
+    *reinterpret_cast<float4*>(pb + 4) = make_float4(b[4], b[5], b[6], b[7]);
 }
 
-// dg[c] = sum_q partial[q][0][c], db[c] = sum_q partial[q][1][c] (fixed order)
-__global__ void ln_bwd_reduce_kernel(const float* __restrict__ partial, int nb, int d, float* __restrict__ dg,
-                                     float* __restrict__ db)
+// dg[c] = sum_q partial[q][0][c], db[c] = sum_q partial[q][1][c]: block = 32 columns x 8 chunk
+// groups (group g sums chunks g, g + 8, ...), the 8 group sums added in order (deterministic)
+__global__ void __launch_bounds__(256)
+ln_bwd_reduce_kernel(const float* __restrict__ partial, int nb, int d, float* __restrict__ dg,
+                     float* __restrict__ db)
 {
     pdl_wait();
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= d) return;
+    __shared__ float sa[8][32], sb[8][32];
+    const int cl = threadIdx.x & 31, grp = threadIdx.x >> 5;
+    const int c = blockIdx.x * 32 + cl;
     float a = 0.f, b = 0.f;
-    for (int q = 0; q < nb; ++q) {
-        a += partial[((size_t)q * 2 + 0) * d + c];
-        b += partial[((size_t)q * 2 + 1) * d + c];
+    if (c < d)
+        for (int q = grp; q < nb; q += 8) {
+            a += partial[((size_t)q * 2 + 0) * d + c];
+            b += partial[((size_t)q * 2 + 1) * d + c];
+        }
+    sa[grp][cl] = a;
+    sb[grp][cl] = b;
+    __syncthreads();
+    if (grp == 0 && c < d) {
+        float ta = 0.f, tb = 0.f;
+#pragma unroll
+        for (int g = 0; g < 8; ++g) { ta += sa[g][cl]; tb += sb[g][cl]; }
+        dg[c] = ta;
+        db[c] = tb;
     }
-    dg[c] = a;
-    db[c] = b;
 }
 
 size_t ln_bwd_partial_floats(int rows, int d) { return (size_t)ceil_div(rows, kLnColChunk) * 2 * d; }
@@ -499,9 +526,9 @@ int launch_layer_norm_bwd(const void* dy, const void* x, const float* mean, cons
     launch_k(ln_bwd_rows_kernel, ceil_div(rows * 32, 256), 256, 0, s, (const bf16*)dy, (const bf16*)x, mean, rstd, g,
              (const bf16*)resid, (bf16*)out, rows, d);
     const int nb = ceil_div(rows, kLnColChunk);
-    launch_k(ln_bwd_cols_kernel, dim3(ceil_div(d, 256), nb), 256, 0, s, (const bf16*)dy, (const bf16*)x, mean, rstd,
+    launch_k(ln_bwd_cols_kernel, dim3(ceil_div(d, 2048), nb), 256, 0, s, (const bf16*)dy, (const bf16*)x, mean, rstd,
              partial, rows, d);
-    launch_k(ln_bwd_reduce_kernel, ceil_div(d, 256), 256, 0, s, (const float*)partial, nb, d, dg, db);
+    launch_k(ln_bwd_reduce_kernel, ceil_div(d, 32), 256, 0, s, (const float*)partial, nb, d, dg, db);
     return 3;
 }
 
