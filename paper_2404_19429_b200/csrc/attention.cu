@@ -243,21 +243,25 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQK, const __grid_constant_
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&s_empty[b]);    // S buffer b is in registers
+                if (diag) {                                   // keys after the query: -inf (raw s)
+#pragma unroll
+                    for (int i = 0; i < 64; ++i)
+                        if (it * TK + 64 * half + i > q_pos) {
+                            if (i < 32) v[i] = __float_as_uint(-INFINITY);
+                            else w2[i - 32] = __float_as_uint(-INFINITY);
+                        }
+                }
+                // max on the raw scores (scale_log2 > 0), then exp2(s * scale - m) as one FFMA
                 float cm[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-                for (int i = 0; i < 64; ++i) {
-                    const uint32_t raw = i < 32 ? v[i] : w2[i - 32];
-                    float x = __uint_as_float(raw) * scale_log2;
-                    if (diag && it * TK + 64 * half + i > q_pos) x = -INFINITY;
-                    if (i < 32) v[i] = __float_as_uint(x); else w2[i - 32] = __float_as_uint(x);
-                    cm[i & 3] = fmaxf(cm[i & 3], x);
-                }
-                const float mn = fmaxf(m, fmaxf(fmaxf(cm[0], cm[1]), fmaxf(cm[2], cm[3])));
+                for (int i = 0; i < 64; ++i)
+                    cm[i & 3] = fmaxf(cm[i & 3], __uint_as_float(i < 32 ? v[i] : w2[i - 32]));
+                const float mn = fmaxf(m, fmaxf(fmaxf(cm[0], cm[1]), fmaxf(cm[2], cm[3])) * scale_log2);
                 if (mn != -INFINITY) {
                     float su[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
                     for (int i = 0; i < 64; ++i)
-                        su[i & 3] += ex2(__uint_as_float(i < 32 ? v[i] : w2[i - 32]) - mn);
+                        su[i & 3] += ex2(fmaf(__uint_as_float(i < 32 ? v[i] : w2[i - 32]), scale_log2, -mn));
                     l = l * ex2(m - mn) + ((su[0] + su[1]) + (su[2] + su[3]));
                     m = mn;
                 }
@@ -273,7 +277,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQK, const __grid_constant_
                 m = mm;
             }
             asm volatile("bar.sync 1, 256;" ::: "memory");     // every read done before P buffer 1 is written
-            const float inv_l = 1.f / l;
+            const float mlog = m + __log2f(l);           // P = exp2(s * scale - m) / l in one FFMA + EX2
             // pass 2: P = exp2(s - m) / l into shared memory (K-major SW128: box `half` of P)
             for (int j = 0; j < n; ++j, ++sc, ++pc) {
                 const int b = sc & 1, pb = pc & 1;
@@ -290,17 +294,22 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQK, const __grid_constant_
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&s_empty[b]);    // S buffer b is in registers
+                if (diag) {
+#pragma unroll
+                    for (int i = 0; i < 64; ++i)
+                        if (j * TK + 64 * half + i > q_pos) {
+                            if (i < 32) v[i] = __float_as_uint(-INFINITY);
+                            else w2[i - 32] = __float_as_uint(-INFINITY);
+                        }
+                }
 #pragma unroll
                 for (int c2 = 0; c2 < 2; ++c2) {
-                    const int cc = 2 * half + c2;
                     uint32_t pk[16];
 #pragma unroll
                     for (int i = 0; i < 16; ++i) {
                         const uint32_t r0 = c2 ? w2[2 * i] : v[2 * i], r1 = c2 ? w2[2 * i + 1] : v[2 * i + 1];
-                        float p0 = ex2(__uint_as_float(r0) * scale_log2 - m) * inv_l;
-                        float p1 = ex2(__uint_as_float(r1) * scale_log2 - m) * inv_l;
-                        if (diag && j * TK + 32 * cc + 2 * i > q_pos) p0 = 0.f;
-                        if (diag && j * TK + 32 * cc + 2 * i + 1 > q_pos) p1 = 0.f;
+                        const float p0 = ex2(fmaf(__uint_as_float(r0), scale_log2, -mlog));
+                        const float p1 = ex2(fmaf(__uint_as_float(r1), scale_log2, -mlog));
                         __nv_bfloat162 hv = __floats2bfloat162_rn(p0, p1);
                         pk[i] = *reinterpret_cast<uint32_t*>(&hv);
                     }
@@ -339,7 +348,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQK, const __grid_constant_
                 for (int c4 = 0; c4 < 4; ++c4)
                     st_v4(orow + 32 * cc + 8 * c4, make_uint4(pk[4 * c4], pk[4 * c4 + 1], pk[4 * c4 + 2], pk[4 * c4 + 3]));
             }
-            if (half == 0) lse[(long)h * T_all + tok] = m + __log2f(l);
+            if (half == 0) lse[(long)h * T_all + tok] = mlog;
         }
     }
     tc_fence_before();

@@ -217,11 +217,15 @@ attn_bwd_kv_kernel(const __grid_constant__ CUtensorMap tmQKV, const __grid_const
             if (lane == 0) mbar_arrive(s_empty);
             const float* lq = lse + (size_t)h * T_all + qtok;
             const float* dq = Dv + (size_t)h * T_all + qtok;
+            if (i == j) {                               // diagonal tile: key after query -> P = 0
+#pragma unroll
+                for (int c = 0; c < 64; ++c)
+                    if (i * TQ + 64 * half + c < kpos) st[c] = -INFINITY;
+            }
 #pragma unroll
             for (int c = 0; c < 64; ++c) {
                 const float l2 = __ldg(lq + c), dd = __ldg(dq + c);
-                float p = ex2(st[c] * scale_log2 - l2);
-                if (i == j && i * TQ + 64 * half + c < kpos) p = 0.f;     // key after query: masked
+                const float p = ex2(fmaf(st[c], scale_log2, -l2));
                 st[c] = p;
                 dp[c] = p * (dp[c] - dd);
             }
@@ -353,12 +357,13 @@ attn_bwd_q_kernel(const __grid_constant__ CUtensorMap tmQKV, const __grid_consta
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(s_empty);
+            if (jj == i) {                              // diagonal tile: key after query -> P = 0
 #pragma unroll
-            for (int c = 0; c < 64; ++c) {
-                float p = ex2(s[c] * scale_log2 - l2);
-                if (jj == i && jj * TK + 64 * half + c > qpos) p = 0.f;
-                dp[c] = p * (dp[c] - dd);
+                for (int c = 0; c < 64; ++c)
+                    if (jj * TK + 64 * half + c > qpos) s[c] = -INFINITY;
             }
+#pragma unroll
+            for (int c = 0; c < 64; ++c) dp[c] = ex2(fmaf(s[c], scale_log2, -l2)) * (dp[c] - dd);
             mbar_wait(ds_empty, (jj & 1) ^ 1);
             st_row64(sDS + half * BOX + r * 128, r, dp);
             fence_proxy_async();

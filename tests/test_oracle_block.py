@@ -11,8 +11,6 @@ import synthetic as S
 from oracle import block as B
 from oracle import moe as M
 
-torch.set_default_dtype(torch.float64)
-
 
 def _rng(seed):
     return np.random.default_rng(seed)
