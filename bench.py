@@ -539,6 +539,35 @@ def block_record(a, world, rank, local_rank, stream, barrier, max_over_ranks, ns
             _, tlb = run(n, 0, steps, True, bwd=True)
             opsb = op_stats(tlb, steps)
     blk.moe.set_flags(base)
+    # a stack of two blocks (same parameters, own buffers): consecutive forwards vs the chunk
+    # pipeline across the blocks (lancet_block_forward_stack: block 2's chunk c starts once block
+    # 1 has combined chunk c)
+    blk2 = B.Block(B.BlockConfig(moe, n_heads=sh.n_heads, seq_len=sh.seq_len, max_capacity_factor=sh.cf),
+                   world=world, rank=rank, device=local_rank, pg=dist.group.WORLD if world > 1 else None)
+    out2 = [torch.empty_like(x), torch.empty_like(x)]
+    stack = []
+    for n in (1, 2, 4):
+        def cons():
+            blk.forward(x, p, sh.k, sh.cf, n, out=out2[0])
+            blk2.forward(out2[0], p, sh.k, sh.cf, n, out=out2[1])
+
+        def pipe():
+            B.forward_stack([blk, blk2], x, [p, p], sh.k, sh.cf, n, outs=out2)
+        tm = {}
+        for name, fn in (("consecutive", cons), ("stack_pipelined", pipe)):
+            for _ in range(3):
+                fn()
+            torch.cuda.synchronize()
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(steps):
+                fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            tm[name] = max_over_ranks(e0.elapsed_time(e1) / steps)
+        stack.append({"n_chunks": n, "consecutive_ms": tm["consecutive"], "stack_ms": tm["stack_pipelined"]})
+    blk2.close()
     best = min(by_n, key=lambda r: r["ms_per_step"])
     pk = peaks()
     # attention: algorithmic causal FLOPs 2 * 2 * S^2 / 2 * hd per (sequence, head); the kernel
@@ -558,6 +587,7 @@ def block_record(a, world, rank, local_rank, stream, barrier, max_over_ranks, ns
         "ops_us_per_step_n4": {o: round(v["us_per_step"], 2) for o, v in (ops4 or {}).items()},
         "fwd_bwd_ops_us_per_step_n4": {o: round(v["us_per_step"], 2) for o, v in (opsb or {}).items()},
         "fwd_bwd_value": world * sh.T / (min(r["fwd_bwd_ms_per_step"] for r in by_n) / 1000.0),
+        "two_block_stack_forward": stack,
         "attention_roofline": {
             "bound": "tensor", "achieved": att_flops / (att_us * 1e-6) / 1e12 if att_us else None,
             "peak": pk["bf16_sus"], "unit": "TFLOP/s",

@@ -68,6 +68,20 @@ lancet_status lancet_block_forward(lancet_block* b, const void* x, const float* 
                                    const float* wg, const void* w1, const void* w2, int32_t T, int32_t k,
                                    double capacity_factor, int32_t n_chunks, void* out, lancet_stream_t stream);
 
+/* Forward of a stack of L blocks (collective when world > 1), block l's output feeding block
+ * l+1, with the chunk pipeline running across the blocks: block l+1's LN1 / attention of chunk
+ * c starts once block l has combined chunk c (the non-MoE computation after
+ * the MoE layer -- the following Transformer layer -- joins the pipeline, fig:part_after_gate).
+ *   blocks [L]; x [T][d] bf16 in; params [L][9] device pointers per block in the order ln1_g,
+ *   ln1_b, w_qkv, w_o, ln2_g, ln2_b, wg, w1, w2 (as lancet_block_forward); outs [L] [T][d] bf16
+ *   out (every block's output; each block's backward needs its own input = the previous out).
+ *   The blocks must be distinct (own buffers) and share T, k, capacity_factor, n_chunks.
+ * Results are bitwise those of L consecutive lancet_block_forward calls.  Never blocks. */
+lancet_status lancet_block_forward_stack(lancet_block* const* blocks, int32_t L, const void* x,
+                                         const void* const* params, int32_t T, int32_t k,
+                                         double capacity_factor, int32_t n_chunks, void* const* outs,
+                                         lancet_stream_t stream);
+
 /* Backward of the last block forward (collective when world > 1): gradients of <dout, out>.
  *   dout [T][d] bf16 in;  dx [T][d] bf16 out;  dln1_g, dln1_b, dln2_g, dln2_b [d] fp32 out;
  *   dw_qkv [3d][d] fp32 out;  dw_o [d][d] fp32 out;  dwg [d][E] fp32 out (local, as

@@ -19,6 +19,7 @@ _BLOCK_SIG = {
     "lancet_block_forward": None,
     "lancet_block_debug_copy": None,
     "lancet_block_backward": None,
+    "lancet_block_forward_stack": None,
 }
 EXPORTS = list(_BLOCK_SIG)
 
@@ -44,6 +45,8 @@ def _lib():
         lib.lancet_block_destroy.restype = I32
         lib.lancet_block_forward.argtypes = [P] + [P] * 10 + [I32, I32, ctypes.c_double, I32, P, P]
         lib.lancet_block_forward.restype = I32
+        lib.lancet_block_forward_stack.argtypes = [P, I32, P, P, I32, I32, ctypes.c_double, I32, P, P]
+        lib.lancet_block_forward_stack.restype = I32
         lib.lancet_block_backward.argtypes = [P] * 13
         lib.lancet_block_backward.restype = I32
         lib.lancet_block_debug_copy.argtypes = [P, I32, P, ctypes.c_size_t]
@@ -164,3 +167,23 @@ class Block:
         L._check(_lib().lancet_block_debug_copy(self._p, w, ctypes.c_void_p(t.data_ptr()),
                                                 t.numel() * t.element_size()), self.moe._p)
         return t
+
+
+def forward_stack(blocks, x, params, k: int, capacity_factor: float, n_chunks: int, outs=None, stream=None):
+    """lancet_block_forward_stack: blocks[l] with params[l] (PARAMS dicts); returns the list of
+    every block's output (outs[l] = block l's out, block l+1's input)."""
+    nl = len(blocks)
+    T = x.shape[0]
+    outs = [torch.empty_like(x) for _ in range(nl)] if outs is None else outs
+    bp = (ctypes.c_void_p * nl)(*[b._p.value for b in blocks])
+    pp = (ctypes.c_void_p * (9 * nl))(*[params[l][n].data_ptr() for l in range(nl) for n in PARAMS])
+    op = (ctypes.c_void_p * nl)(*[o.data_ptr() for o in outs])
+    st = _lib().lancet_block_forward_stack(bp, nl, ctypes.c_void_p(x.data_ptr()), pp, T, k,
+                                           float(capacity_factor), n_chunks, op, L._stream(stream))
+    L._check(st, blocks[0].moe._p)
+    for l, b in enumerate(blocks):
+        b._last = (x if l == 0 else outs[l - 1], params[l])
+        b._k = k
+        b.moe._last = (None, params[l]["wg"], params[l]["w1"], params[l]["w2"])
+        b.moe._last_n = n_chunks
+    return outs

@@ -41,6 +41,7 @@ struct lancet_block {
     const float *ln1_g = nullptr, *ln2_g = nullptr;
     int n_last = 0;
     bool have_fwd = false;
+    std::vector<cudaEvent_t> ev_out;   // [kMaxChunks]: chunk c of the last forward's out is stored
 };
 
 namespace {
@@ -124,6 +125,11 @@ LANCET_API lancet_status lancet_block_create_peer(lancet_block** out, int32_t wo
               al(&b->dh, T * d * 2) && al(&b->datt, T * d * 2) && al(&b->dqkv, T * 3 * d * 2) && al(&b->da1, T * d * 2) &&
               al((void**)&b->Dbuf, T * 4 * cfg->n_heads) &&
               al((void**)&b->ln_partial, sizeof(float) * ln_bwd_partial_floats((int)T, (int)d));
+    for (int i = 0; ok && i < kMaxChunks; ++i) {
+        cudaEvent_t e;
+        ok = cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
+        if (ok) b->ev_out.push_back(e);
+    }
     if (!ok || cudaStreamCreateWithFlags(&b->s_pre, cudaStreamNonBlocking) != cudaSuccess) {
         lancet_block_destroy(b);
         return bfail(nullptr, LANCET_ERR_NOMEM, "block workspace allocation failed");
@@ -141,16 +147,20 @@ LANCET_API lancet_status lancet_block_destroy(lancet_block* b)
     if (b->moe) st = lancet_destroy(b->moe);
     cudaSetDevice(b->device);
     for (void* p : b->allocs) cudaFree(p);
+    for (cudaEvent_t e : b->ev_out) cudaEventDestroy(e);
     if (b->s_pre) cudaStreamDestroy(b->s_pre);
     delete b;
     return st;
 }
 
-LANCET_API lancet_status lancet_block_forward(lancet_block* b, const void* x, const float* ln1_g, const float* ln1_b,
-                                              const void* w_qkv, const void* w_o, const float* ln2_g,
-                                              const float* ln2_b, const float* wg, const void* w1, const void* w2,
-                                              int32_t T, int32_t k, double cf, int32_t n, void* out,
-                                              lancet_stream_t stream_)
+namespace {
+// One block's forward.  ev_in (optional, [n]): chunk c's input rows are ready once ev_in[c] has
+// fired (the previous block of a stack); the block's chunk-c output records b->ev_out[c]; join =
+// false leaves the internal streams un-joined (the stack joins them at its end).
+lancet_status block_forward_impl(lancet_block* b, const void* x, const float* ln1_g, const float* ln1_b,
+                                 const void* w_qkv, const void* w_o, const float* ln2_g, const float* ln2_b,
+                                 const float* wg, const void* w1, const void* w2, int32_t T, int32_t k, double cf,
+                                 int32_t n, void* out, cudaStream_t s, const cudaEvent_t* ev_in, bool join)
 {
     if (!b) return bfail(nullptr, LANCET_ERR_ARG, "block is NULL");
     lancet_ctx* c = b->moe;
@@ -164,7 +174,6 @@ LANCET_API lancet_status lancet_block_forward(lancet_block* b, const void* x, co
     if (T < b->S || T > b->max_tokens || T % b->S) return bfail(b, LANCET_ERR_ARG, "T must be n_seq * seq_len <= max_tokens");
     const int n_seq = T / b->S;
     if (n < 1 || n > c->cfg.max_chunks || n_seq % n) return bfail(b, LANCET_ERR_ARG, "n_chunks must divide the sequences (R20)");
-    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream_);
     const int d = b->d, Tc = T / n, seq_c = n_seq / n;
     std::vector<int> bounds(n + 1);
     for (int ch = 0; ch <= n; ++ch) bounds[ch] = ch * Tc;
@@ -180,6 +189,9 @@ LANCET_API lancet_status lancet_block_forward(lancet_block* b, const void* x, co
     in.resid = b->h;
     in.s_pre = b->s_pre;
     in.cf_max = b->cf_max;
+    in.ev_in = ev_in;
+    in.ev_out = b->ev_out.data();
+    in.join = join;
     in.produce = [&](int ch, int t0, int t1, cudaStream_t sp) -> lancet_status {
         const int rows = t1 - t0;
         const int* tr = b->tok_tab + ch;
@@ -220,6 +232,48 @@ LANCET_API lancet_status lancet_block_forward(lancet_block* b, const void* x, co
     b->n_last = n;
     b->x = x; b->w_qkv = w_qkv; b->w_o = w_o; b->ln1_g = ln1_g; b->ln2_g = ln2_g;
     b->have_fwd = true;
+    return LANCET_OK;
+}
+}  // namespace
+
+LANCET_API lancet_status lancet_block_forward(lancet_block* b, const void* x, const float* ln1_g, const float* ln1_b,
+                                              const void* w_qkv, const void* w_o, const float* ln2_g,
+                                              const float* ln2_b, const float* wg, const void* w1, const void* w2,
+                                              int32_t T, int32_t k, double cf, int32_t n, void* out,
+                                              lancet_stream_t stream_)
+{
+    return block_forward_impl(b, x, ln1_g, ln1_b, w_qkv, w_o, ln2_g, ln2_b, wg, w1, w2, T, k, cf, n, out,
+                              reinterpret_cast<cudaStream_t>(stream_), nullptr, true);
+}
+
+// A stack of L blocks (block l's output is block l+1's input) with the chunk pipeline running
+// across the blocks: block l+1's LN1 / attention of chunk c starts as soon as block l has
+// combined chunk c ("the non-MoE computation ... after (e.g., the following Transformer layer)
+// the MoE layer", fig:part_after_gate + fig:part_all) instead of after
+// block l's whole forward.  params: [L][9] device pointers in the order ln1_g, ln1_b, w_qkv,
+// w_o, ln2_g, ln2_b, wg, w1, w2 (as lancet_block_forward); outs: [L] outputs [T][d].
+LANCET_API lancet_status lancet_block_forward_stack(lancet_block* const* blocks, int32_t L, const void* x,
+                                                    const void* const* params, int32_t T, int32_t k, double cf,
+                                                    int32_t n, void* const* outs, lancet_stream_t stream_)
+{
+    if (!blocks || !params || !outs || L < 1) return bfail(nullptr, LANCET_ERR_ARG, "bad stack arguments");
+    for (int l = 0; l < L; ++l)
+        if (!blocks[l]) return bfail(nullptr, LANCET_ERR_ARG, "null block");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream_);
+    for (int l = 0; l < L; ++l) {
+        lancet_block* b = blocks[l];
+        const void* const* p = params + 9 * l;
+        const void* in = l == 0 ? x : outs[l - 1];
+        lancet_status st = block_forward_impl(b, in, (const float*)p[0], (const float*)p[1], p[2], p[3],
+                                              (const float*)p[4], (const float*)p[5], (const float*)p[6], p[7],
+                                              p[8], T, k, cf, n, outs[l], s,
+                                              l == 0 ? nullptr : blocks[l - 1]->ev_out.data(), false);
+        if (st) return st;
+    }
+    for (int l = 0; l < L; ++l) {
+        lancet_status st = moe_join(blocks[l]->moe, blocks[l]->s_pre, s);
+        if (st) return st;
+    }
     return LANCET_OK;
 }
 

@@ -24,7 +24,16 @@ struct ChunkedInput {
     const void* resid = nullptr;
     cudaStream_t s_pre = nullptr;    // the producer's stream
     double cf_max = 0.0;             // bound of the capacity factor (static receive regions)
+    // chunk pipeline across consecutive layers (a stack of blocks): the producer of chunk c
+    // first waits for ev_in[c] (the previous block's chunk-c output is stored), the combine of
+    // chunk c records ev_out[c]; join = false leaves the internal streams un-joined to the
+    // caller's stream (the stack joins every block at its end: moe_join)
+    const cudaEvent_t* ev_in = nullptr;
+    cudaEvent_t* ev_out = nullptr;
+    bool join = true;
 };
+// make `s` wait for everything the context's streams (and `extra`) have enqueued
+lancet_status moe_join(lancet_ctx* c, cudaStream_t extra, cudaStream_t s);
 lancet_status moe_forward_chunked(lancet_ctx* c, const void* x, const float* wg, const void* w1, const void* w2,
                                   int T, int k, double cf, void* y, const ChunkedInput& in, cudaStream_t s);
 

@@ -1068,6 +1068,7 @@ lancet_status moe_forward_chunked(lancet_ctx* c, const void* x, const float* wg,
     for (int ch = 0; ch < n; ++ch) {
         const int t0 = in.bounds[ch], t1 = in.bounds[ch + 1];
         // ---- producer: the chunk's MoE input, then its gate with the carried capacity state
+        if (in.ev_in) CK(cudaStreamWaitEvent(sp, in.ev_in[ch], 0));
         st = in.produce(ch, t0, t1, sp);
         if (st) return st;
         ra.x = (const char*)x + (size_t)t0 * xrow;
@@ -1116,15 +1117,30 @@ lancet_status moe_forward_chunked(lancet_ctx* c, const void* x, const float* wg,
                                 pr->d_outsrc, E_l, in.resid);
         }
         CHECK_LAUNCH();
+        if (in.ev_out) CK(cudaEventRecord(in.ev_out[ch], sb));
     }
     c->out_consume_pending = true;
     c->n_groups = n * E_l;
-    for (cudaStream_t q : {sp, sm, sc, sb}) {
-        cudaEvent_t e = next_ev();
+    if (in.join) {
+        for (cudaStream_t q : {sp, sm, sc, sb}) {
+            cudaEvent_t e = next_ev();
+            CK(cudaEventRecord(e, q));
+            CK(cudaStreamWaitEvent(s, e, 0));
+        }
+    }
+    c->have_fwd = true;
+    return LANCET_OK;
+}
+
+lancet_status moe_join(lancet_ctx* c, cudaStream_t extra, cudaStream_t s)
+{
+    int i = (int)c->ev_pool.size() - 6;
+    for (cudaStream_t q : {extra, c->s_comp, c->s_comm, c->s_comp2, c->s_gate}) {
+        if (!q) continue;
+        cudaEvent_t e = c->ev_pool[i++];
         CK(cudaEventRecord(e, q));
         CK(cudaStreamWaitEvent(s, e, 0));
     }
-    c->have_fwd = true;
     return LANCET_OK;
 }
 

@@ -444,3 +444,55 @@ def test_block_backward_chunk_invariance():
         assert torch.equal(res[0][key], res[1][key]), key
     for key in ("dw1", "dw2"):
         assert normwise(res[1][key].numpy(), res[0][key].numpy()) <= 1e-5
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_block_stack_pipeline_is_bitwise_consecutive_blocks(n):
+    """lancet_block_forward_stack (block l+1's chunk c starts once block l combined chunk c) gives
+    every block's output bit for bit as consecutive lancet_block_forward calls, and the stack's
+    backward (blocks in reverse, each fed the next one's dx) matches the consecutive one; the
+    3-block output is checked against the chained oracle blocks (routing margin rule)."""
+    from paper_2404_19429_b200 import block as B
+    from oracle import block as OB
+    sh = S.BlockShape(n_seq=4, seq_len=256, d=256, n_heads=2, f=512, E=8, G=1, k=2, cf=1.0, n_chunks=n)
+    L = 3
+    insl = [S.gen_block_rank_inputs(50 + l, 0, sh, beta=0.5) for l in range(L)]
+    x = to_dev(insl[0]["x"], bf)
+    res = {}
+    for mode in ("consecutive", "stack"):
+        blks = [_block(sh) for _ in range(L)]
+        ps = [_dev_params(i) for i in insl]
+        if mode == "stack":
+            outs = B.forward_stack(blks, x, ps, sh.k, sh.cf, n)
+        else:
+            outs, cur = [], x
+            for b, p in zip(blks, ps):
+                cur = b.forward(cur, p, sh.k, sh.cf, n)
+                outs.append(cur)
+        dout = to_dev(S.gen_dy(70, 0, sh.T, sh.d), bf)
+        grads = []
+        for b in reversed(blks):
+            g = b.backward(dout)
+            grads.append(g)
+            dout = g["dx"]
+        torch.cuda.synchronize()
+        res[mode] = ([o.cpu() for o in outs], [{key: v.cpu() for key, v in g.items()} for g in grads])
+        for b in blks:
+            b.close()
+    for a, b in zip(res["consecutive"][0], res["stack"][0]):
+        assert torch.equal(a, b)
+    for ga, gb in zip(res["consecutive"][1], res["stack"][1]):
+        for key in ga:
+            if key in ("dw1", "dw2"):
+                assert normwise(gb[key].numpy(), ga[key].numpy()) <= 1e-5
+            else:
+                assert torch.equal(ga[key], gb[key]), key
+    # the chained oracle: each block's oracle on the previous oracle block's output
+    cur = insl[0]["x"]
+    for l in range(L):
+        i = insl[l]
+        prm = {key: i[key] for key in ("ln1_g", "ln1_b", "ln2_g", "ln2_b", "w_qkv", "w_o")}
+        ref = OB.block_forward([cur], prm, i["wg"], [i["w1"]], [i["w2"]], sh.n_heads, sh.seq_len, sh.k, sh.cf, n)
+        cur = ref.out[0].astype(np.float32)
+    got = res["stack"][0][-1].float().numpy()
+    assert normwise(got, cur) <= 3 * TOL["bf16"]
