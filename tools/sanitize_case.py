@@ -1,5 +1,7 @@
 """One tiny fwd+bwd (two steps, different inputs) of a path, for compute-sanitizer runs
-(tools/sanitize.sh): world1 | local2 | peer1push | peer1pull | peer2push (under torchrun)."""
+(tools/sanitize.sh): world1 | local2 | peer1push | peer1pull | peer2push (under torchrun) |
+partitioned (lancet_moe_forward_partitioned + backward) | block (block forward + backward, and a
+two-block stack forward)."""
 import os
 import sys
 import threading
@@ -62,6 +64,38 @@ def main():
         [t.join() for t in th]
         g.close()
         assert not errs, errs
+    elif mode == "partitioned":
+        c = lancet.Context(mk(FLAG_PEER_PUSH), transport="peer")
+        dev = torch.device("cuda", 0)
+        for s_ in range(2):
+            sh = S.LayerShape(T=T, d=d, f=f, E=E, G=1, k=k, cf=1.0, n_chunks=n)
+            ins = S.gen_rank_inputs(5 + s_, 0, sh, beta=0.5)
+            x, wg, w1, w2, dy = (torch.from_numpy(ins[key]).to(dev, torch.float32 if key == "wg" else torch.bfloat16)
+                                 for key in ("x", "wg", "w1", "w2", "dy"))
+            c.forward_partitioned(x, wg, w1, w2, k, 1.0, n)
+            c.backward(dy)
+            torch.cuda.synchronize()
+        c.close()
+    elif mode == "block":
+        from paper_2404_19429_b200 import block as B
+        sh = S.BlockShape(n_seq=2, seq_len=128, d=256, n_heads=2, f=256, E=4, G=1, k=2, cf=1.0, n_chunks=2)
+        ins = S.gen_block_rank_inputs(9, 0, sh, beta=0.5)
+        dev = torch.device("cuda", 0)
+        p = {key: torch.from_numpy(ins[key]).to(dev, torch.float32 if key in ("ln1_g", "ln1_b", "ln2_g", "ln2_b", "wg")
+                                                else torch.bfloat16) for key in B.PARAMS}
+        moe = lancet.LayerConfig(d_model=sh.d, d_ffn=sh.f, n_experts=sh.E, max_tokens=sh.T, max_k=sh.k, max_chunks=4)
+        blks = [B.Block(B.BlockConfig(moe, n_heads=sh.n_heads, seq_len=sh.seq_len, max_capacity_factor=1.0))
+                for _ in range(2)]
+        x = torch.from_numpy(ins["x"]).to(dev, torch.bfloat16)
+        out = blks[0].forward(x, p, sh.k, sh.cf, 2)
+        blks[0].backward(torch.from_numpy(ins["dy"]).to(dev, torch.bfloat16))
+        outs = B.forward_stack(blks, x, [p, p], sh.k, sh.cf, 2)
+        g = blks[1].backward(outs[1])
+        blks[0].backward(g["dx"])
+        torch.cuda.synchronize()
+        for b_ in blks:
+            b_.close()
+        del out
     elif mode == "peer2push":
         import torch.distributed as dist
         dist.init_process_group("gloo")
