@@ -51,7 +51,11 @@ struct Cfg {
     static constexpr size_t kEpi = (size_t)kEpiWarps * kWarpStage;
     static constexpr size_t kFixed = 1024 + kEpi + kBarBytes + sizeof(int) * (3 * kMaxGroups + 1);
     static constexpr int STAGES_FIT = (int)((kSmemLimit - kFixed) / (A_STAGE + B_STAGE));
+#ifdef LANCET_EXP_STAGES
+    static constexpr int STAGES = STAGES_FIT > LANCET_EXP_STAGES ? LANCET_EXP_STAGES : STAGES_FIT;
+#else
     static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
+#endif
     static constexpr size_t kRing = (size_t)STAGES * (A_STAGE + B_STAGE);
     static constexpr size_t kSmem = kFixed + kRing;
 };
@@ -330,7 +334,11 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 }
                 mbar_wait(&tfull[acc], acc_phase);
                 tc_fence_after();
+#ifdef LANCET_EXP_NO_EPI
+                if (false) {
+#else
                 if (live) {
+#endif
                     // chunk cc of this warp's columns: TMEM -> epilogue math -> staging -> TMA
                     auto chunk = [&](int cc, uint32_t (&v)[32]) {
                         if (!has_k) {                                   // uniform: empty reduction
@@ -389,11 +397,20 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                                     gr[i] = g2.x; gr[i + 1] = g2.y;
                                 }
                             }
+#ifdef LANCET_EXP_NO_STS
+                            {
+                                uint32_t acc_ = 0;
+#pragma unroll
+                                for (int j = 0; j < 4; ++j) { const uint4 a_ = pack16<bf16>(h + 8 * j), b_ = pack16<bf16>(gr + 8 * j); acc_ ^= a_.x ^ a_.y ^ a_.z ^ a_.w ^ b_.x ^ b_.y ^ b_.z ^ b_.w; }
+                                if (acc_ == 0x12345678u && lane == 40) *reinterpret_cast<uint32_t*>(sO0) = acc_;
+                            }
+#else
 #pragma unroll
                             for (int j = 0; j < 4; ++j) {
                                 *reinterpret_cast<uint4*>(sO0 + sw64(lane, j)) = pack16<bf16>(h + 8 * j);
                                 *reinterpret_cast<uint4*>(sO1 + sw64(lane, j)) = pack16<bf16>(gr + 8 * j);
                             }
+#endif
                         } else {
 #pragma unroll
                             for (int j = 0; j < 4; ++j)
@@ -414,17 +431,26 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                     // TMEM loads one chunk ahead of the math (cc1 - cc0 is even)
                     const uint32_t tbase = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16);
                     uint32_t va[32], vb[32];
-                    tmem_ld32_issue(tbase + cc0 * 32, va);
-                    tmem_wait_ld(va);
+#ifdef LANCET_EXP_NO_TMEM
+#define TLD(addr, v) do { for (int i_ = 0; i_ < 32; ++i_) v[i_] = __float_as_uint((float)(lane + i_) * 0.01f + (float)(addr & 255)); } while (0)
+#define TWAIT(v) do {} while (0)
+#else
+#define TLD(addr, v) tmem_ld32_issue(addr, v)
+#define TWAIT(v) tmem_wait_ld(v)
+#endif
+                    TLD(tbase + cc0 * 32, va);
+                    TWAIT(va);
 #pragma unroll 1
                     for (int cc = cc0; cc < cc1; cc += 2) {
-                        tmem_ld32_issue(tbase + (cc + 1) * 32, vb);
+                        TLD(tbase + (cc + 1) * 32, vb);
                         chunk(cc, va);
-                        tmem_wait_ld(vb);
-                        if (cc + 2 < cc1) tmem_ld32_issue(tbase + (cc + 2) * 32, va);
+                        TWAIT(vb);
+                        if (cc + 2 < cc1) TLD(tbase + (cc + 2) * 32, va);
                         chunk(cc + 1, vb);
-                        if (cc + 2 < cc1) tmem_wait_ld(va);
+                        if (cc + 2 < cc1) TWAIT(va);
                     }
+#undef TLD
+#undef TWAIT
                 }
             } else {
                 mbar_wait(&tfull[acc], acc_phase);
