@@ -15,6 +15,7 @@
 #include "kernels.h"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace lancet {
 
@@ -316,36 +317,44 @@ gate_topk_kernel(const Elt* __restrict__ x, const float* __restrict__ wg, int T,
 // K1, warp-streaming variant (E % 4 == 0, d % 64 == 0, Wg resident in shared memory): the
 // whole Wg is staged once per block (regrouped [E/4][d][4]); each warp then streams its own
 // tokens' x rows through a private cp.async ring of 64-dim slices and runs the R1 chains with
-// no block barrier in the loop.  Thread (token lane/tpt, experts 4*(lane%tpt)..+3), two
-// chains per fma.rn.f32x2.  4 warps per block; 2 blocks per SM at d = 1024, E = 8.
+// no block barrier in the loop.  Thread (tokens TT*(lane/tpt)..+TT-1, experts
+// 4*(lane%tpt)..+3), two chains per fma.rn.f32x2 and token; 64 tokens per block.
 constexpr int kGsDT = 64;
-constexpr int kGsCE = 4, kGsTT = 1;   // experts per thread, tokens per thread (CE=2 / CE=8 /
-                                      // TT=2 measured slower)
-constexpr int kGsTokensPerBlock = 64; // 4 warps at E = 8, 8 at E = 16
+constexpr int kGsCE = 4;              // experts per thread (CE=2 / CE=8 measured slower)
+constexpr int kGsTokensPerBlock = 64; // E = 8: 4 warps (1 token per thread) or 2 (2 tokens)
 constexpr size_t kGsSmemMax = 110 * 1024;   // two blocks per SM
 
-__host__ __device__ inline int gs_tpw(int E) { return 32 / (E / kGsCE) * kGsTT; } // tokens per warp
+// tokens per thread: 2 where the batch still gives every SM a block (each staged Wg value
+// then feeds two tokens: half the shared-memory bytes per FMA; E = 8 / 16 at T = 16k:
+// -12 % / -31 %), else 1 (more warps)
+static int gs_tt(int T, int E)
+{
+    static const int forced = [] { const char* e = getenv("LANCET_GATE_TT"); return e ? atoi(e) : 0; }();
+    if (forced == 1 || forced == 2) return forced;   // A/B runs
+    return (E <= 16 && T >= 148 * kGsTokensPerBlock) ? 2 : 1;
+}
+__host__ __device__ inline int gs_tpw(int E, int tt) { return 32 / (E / kGsCE) * tt; } // tokens per warp
 __host__ __device__ inline int gs_row_bytes(int elt) { return kGsDT * elt + 16; }
 __host__ __device__ inline size_t gs_wg_bytes(int d, int E) { return (size_t)(E / kGsCE) * (d * kGsCE + 4) * 4; }
-__host__ __device__ inline int gs_warps(int E) { return kGsTokensPerBlock / gs_tpw(E) > 0 ? kGsTokensPerBlock / gs_tpw(E) : 1; }
+__host__ __device__ inline int gs_warps(int E, int tt) { return kGsTokensPerBlock / gs_tpw(E, tt) > 0 ? kGsTokensPerBlock / gs_tpw(E, tt) : 1; }
 // ring depth: 8 slices if they fit beside the resident Wg, else 4
-static int gs_stages(int d, int E, int elt)
+static int gs_stages(int d, int E, int elt, int tt)
 {
-    const size_t per_stage = (size_t)gs_warps(E) * gs_tpw(E) * gs_row_bytes(elt);
+    const size_t per_stage = (size_t)gs_warps(E, tt) * gs_tpw(E, tt) * gs_row_bytes(elt);
     return gs_wg_bytes(d, E) + 8 * per_stage <= kGsSmemMax ? 8 : 4;
 }
-static size_t gs_smem(int d, int E, int elt)
+static size_t gs_smem(int d, int E, int elt, int tt)
 {
     // a warp's logits [tpw][E] fit in its ring
-    return gs_wg_bytes(d, E) + (size_t)gs_stages(d, E, elt) * gs_warps(E) * gs_tpw(E) * gs_row_bytes(elt);
+    return gs_wg_bytes(d, E) + (size_t)gs_stages(d, E, elt, tt) * gs_warps(E, tt) * gs_tpw(E, tt) * gs_row_bytes(elt);
 }
-static bool gs_ok(int d, int E, int elt)
+static bool gs_ok(int d, int E, int elt, int tt)
 {
-    return E % 4 == 0 && E / kGsCE <= 32 && 32 % (E / kGsCE) == 0 && d % kGsDT == 0 && gs_warps(E) <= 16 &&
-           gs_smem(d, E, elt) <= kGsSmemMax;
+    return E % 4 == 0 && E / kGsCE <= 32 && 32 % (E / kGsCE) == 0 && d % kGsDT == 0 && gs_warps(E, tt) <= 16 &&
+           gs_smem(d, E, elt, tt) <= kGsSmemMax;
 }
 
-template <typename Elt, int S>
+template <typename Elt, int S, int TT>
 __global__ void __launch_bounds__(512)
 gate_stream_kernel(const Elt* __restrict__ x, const float* __restrict__ wg, int T, int d, int E,
                    int k, int renorm, float* __restrict__ logits, int* __restrict__ idx_out,
@@ -357,7 +366,7 @@ gate_stream_kernel(const Elt* __restrict__ x, const float* __restrict__ wg, int 
     constexpr int V = Vec16<Elt>::N;                   // dims per 16-byte chunk
     constexpr int CPR = kGsDT / V;                     // chunks per row slice
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    constexpr int CE = kGsCE, TT = kGsTT;
+    constexpr int CE = kGsCE;
     const int tpt = E / CE, tpw = 32 / tpt * TT;
     const int RB = gs_row_bytes(sizeof(Elt));
     const int gstride = d * CE + 4;                    // floats per expert group (+4: bank offset)
@@ -367,30 +376,24 @@ gate_stream_kernel(const Elt* __restrict__ x, const float* __restrict__ wg, int 
     const int tw = t0 + warp * tpw;                    // this warp's first token
 
     for (int i = tid; i < 2 * E; i += blockDim.x) sh_hist[i] = 0;
-    // Wg [d][E] -> swg[(e/CE) * gstride + i * CE + e % CE]
-    {
-        const int q4 = E / 4;
-        for (int q = tid; q < d * q4; q += blockDim.x) {
-            const int i = q / q4, e = (q % q4) * 4;
-            if constexpr (CE == 4) {
-                cp_async16(swg + (size_t)(e / 4) * gstride + i * 4, wg + (size_t)i * E + e);
-            } else {
-                const float4 v = __ldg(reinterpret_cast<const float4*>(wg + (size_t)i * E + e));
-                *reinterpret_cast<float2*>(swg + (size_t)(e / 2) * gstride + i * 2) = make_float2(v.x, v.y);
-                *reinterpret_cast<float2*>(swg + (size_t)(e / 2 + 1) * gstride + i * 2) = make_float2(v.z, v.w);
-            }
-        }
-        cp_async_commit();
-    }
+    // Wg [d][E] -> swg[(e/4) * gstride + i * 4 + e % 4] (no integer division in the copy loop:
+    // it showed up as ~15 % of the kernel's stall samples)
+    for (int e4 = 0; e4 < E / 4; ++e4)
+        for (int i = tid; i < d; i += blockDim.x)
+            cp_async16(swg + (size_t)e4 * gstride + i * 4, wg + (size_t)i * E + e4 * 4);
+    cp_async_commit();
     const int nst = d / kGsDT;
+    // lane copies 16-byte column cl of rows rl, rl + RSTEP, ... of each slice (pointers stepped,
+    // no per-copy 64-bit index arithmetic)
+    constexpr int RSTEP = 32 / CPR;
+    const int cl = lane % CPR, rl = lane / CPR;
+    const uint8_t* xl = reinterpret_cast<const uint8_t*>(x) + (size_t)(tw + rl) * d * sizeof(Elt) + cl * 16;
+    const size_t xstep = (size_t)RSTEP * d * sizeof(Elt);
     auto issue = [&](int st) {
-        uint8_t* slot = ring + (size_t)(st % S) * tpw * RB;
-        for (int q = lane; q < tpw * CPR; q += 32) {
-            const int rr = q / CPR, c = q % CPR, t = tw + rr;
-            if (t < T)
-                cp_async16(slot + rr * RB + c * 16,
-                           reinterpret_cast<const uint8_t*>(x + (size_t)t * d + st * kGsDT) + c * 16);
-        }
+        uint8_t* sl = ring + (size_t)(st % S) * tpw * RB + rl * RB + cl * 16;
+        const uint8_t* g = xl + (size_t)st * kGsDT * sizeof(Elt);
+        for (int rr = rl; rr < tpw; rr += RSTEP, sl += RSTEP * RB, g += xstep)
+            if (tw + rr < T) cp_async16(sl, g);
     };
 #pragma unroll
     for (int st = 0; st < S - 1; ++st) {
@@ -420,17 +423,11 @@ gate_stream_kernel(const Elt* __restrict__ x, const float* __restrict__ wg, int 
                 unpack16<Elt>(reinterpret_cast<const uint4*>(xrow + tt * RB)[c], xf[tt]);
 #pragma unroll
             for (int u = 0; u < V; ++u) {               // R1: increasing i, one fused step each
-                if constexpr (CE == 4) {
-                    const float4 w4 = *reinterpret_cast<const float4*>(wp + (c * V + u) * 4);
+                const float4 w4 = *reinterpret_cast<const float4*>(wp + (c * V + u) * CE);
 #pragma unroll
-                    for (int tt = 0; tt < TT; ++tt) {
-                        ffma2(acc0[tt], xf[tt][u], make_float2(w4.x, w4.y));
-                        ffma2(acc1[tt], xf[tt][u], make_float2(w4.z, w4.w));
-                    }
-                } else {
-                    const float2 w2 = *reinterpret_cast<const float2*>(wp + (c * V + u) * 2);
-#pragma unroll
-                    for (int tt = 0; tt < TT; ++tt) ffma2(acc0[tt], xf[tt][u], w2);
+                for (int tt = 0; tt < TT; ++tt) {
+                    ffma2(acc0[tt], xf[tt][u], make_float2(w4.x, w4.y));
+                    ffma2(acc1[tt], xf[tt][u], make_float2(w4.z, w4.w));
                 }
             }
         }
@@ -838,22 +835,28 @@ int launch_routing(const RouteArgs& a, bool is_bf16, cudaStream_t s)
     if (a.random) {
         launch_k(random_gate_kernel, n_tiles, kScanTile, 0, s, a.T, a.E, a.k, a.seed, a.logits, a.idx, a.w,
                  a.hist, a.t_base);
-    } else if (gs_ok(a.d, a.E, elt)) {
+    } else if (gs_ok(a.d, a.E, elt, gs_tt(a.T, a.E))) {
         static bool gs_attr = false;
         if (!gs_attr) {
-            cudaFuncSetAttribute(gate_stream_kernel<bf16, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-            cudaFuncSetAttribute(gate_stream_kernel<float, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-            cudaFuncSetAttribute(gate_stream_kernel<bf16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-            cudaFuncSetAttribute(gate_stream_kernel<float, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+#define GSA(Elt, SS, TTT) cudaFuncSetAttribute(gate_stream_kernel<Elt, SS, TTT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)
+            GSA(bf16, 8, 1); GSA(bf16, 4, 1); GSA(float, 8, 1); GSA(float, 4, 1);
+            GSA(bf16, 8, 2); GSA(bf16, 4, 2); GSA(float, 8, 2); GSA(float, 4, 2);
+#undef GSA
             gs_attr = true;
         }
-        const int W = gs_warps(a.E), per_block = W * gs_tpw(a.E), S = gs_stages(a.d, a.E, elt);
-        const size_t smem = gs_smem(a.d, a.E, elt);
+        const int tt = gs_tt(a.T, a.E);
+        const int W = gs_warps(a.E, tt), per_block = W * gs_tpw(a.E, tt), S = gs_stages(a.d, a.E, elt, tt);
+        const size_t smem = gs_smem(a.d, a.E, elt, tt);
         const dim3 grid(ceil_div(a.T, per_block)), block(W * 32);
-#define GS(Elt, SS) launch_k(gate_stream_kernel<Elt, SS>, grid, block, smem, s, (const Elt*)a.x, a.wg, a.T, a.d, \
-                             a.E, a.k, a.renorm, a.logits, a.idx, a.w, a.hist, n_tiles)
-        if (is_bf16) { if (S == 8) GS(bf16, 8); else GS(bf16, 4); }
-        else { if (S == 8) GS(float, 8); else GS(float, 4); }
+#define GS(Elt, SS, TTT) launch_k(gate_stream_kernel<Elt, SS, TTT>, grid, block, smem, s, (const Elt*)a.x, a.wg, a.T, a.d, \
+                                  a.E, a.k, a.renorm, a.logits, a.idx, a.w, a.hist, n_tiles)
+        if (tt == 2) {
+            if (is_bf16) { if (S == 8) GS(bf16, 8, 2); else GS(bf16, 4, 2); }
+            else { if (S == 8) GS(float, 8, 2); else GS(float, 4, 2); }
+        } else {
+            if (is_bf16) { if (S == 8) GS(bf16, 8, 1); else GS(bf16, 4, 1); }
+            else { if (S == 8) GS(float, 8, 1); else GS(float, 4, 1); }
+        }
 #undef GS
     } else {
     // 64 tokens per block (32 measured slower even where it doubles the blocks: each block
