@@ -287,6 +287,35 @@ __device__ __forceinline__ void cp_async_commit_s() { asm volatile("cp.async.com
 template <int N>
 __device__ __forceinline__ void cp_async_wait_s() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// Wg^T slice of a thread: wg2[e][q] = (Wg[i0+2q][e0+e], Wg[i0+2q+1][e0+e]) for e < EE.  With 8
+// experts per lane and E % 4 == 0 the 8 rows are read as two 16-byte vectors each (the 64
+// scalar loads of the general form were ~25 % of K6's stall samples: LSU throttle in the
+// prologue of a one-wave grid)
+template <int EE>
+__device__ __forceinline__ void load_wgT(const float* __restrict__ wg, int E, int i0, int e0, float2 (&wg2)[EE][4])
+{
+    if (EE == 8 && E % 4 == 0 && e0 + 8 <= E) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const float4* ra = reinterpret_cast<const float4*>(wg + (size_t)(i0 + 2 * q) * E + e0);
+            const float4* rb = reinterpret_cast<const float4*>(wg + (size_t)(i0 + 2 * q + 1) * E + e0);
+            const float4 a0 = __ldg(ra), a1 = __ldg(ra + 1), b0 = __ldg(rb), b1 = __ldg(rb + 1);
+            const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+            for (int e = 0; e < EE; ++e) wg2[e][q] = make_float2(av[e & 7], bv[e & 7]);
+        }
+    } else {
+#pragma unroll
+        for (int e = 0; e < EE; ++e)
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                wg2[e][q] = e0 + e < E ? make_float2(__ldg(wg + (size_t)(i0 + 2 * q) * E + e0 + e),
+                                                     __ldg(wg + (size_t)(i0 + 2 * q + 1) * E + e0 + e))
+                                       : make_float2(0.f, 0.f);
+    }
+}
+
 template <typename Elt, int KK>
 struct K6Geom {
     static constexpr int NV = Dims8<Elt>::NV;
@@ -330,15 +359,9 @@ k6_stream_kernel(const Elt* __restrict__ dxe, const int* __restrict__ prow,
     }
     const int i0 = (blockIdx.y * NTD + dg) * 8;
     const int e0 = eg * 8;                                  // this lane's experts (EG > 1)
-    // this thread's Wg^T slice, read straight from Wg [d][E] (rows i0..i0+7 are contiguous)
+    // this thread's Wg^T slice, read straight from Wg [d][E] (rows i0..i0+7)
     float2 wg2[EE][4];
-#pragma unroll
-    for (int e = 0; e < EE; ++e)
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-            wg2[e][q] = e0 + e < E ? make_float2(__ldg(wg + (size_t)(i0 + 2 * q) * E + e0 + e),
-                                                 __ldg(wg + (size_t)(i0 + 2 * q + 1) * E + e0 + e))
-                                   : make_float2(0.f, 0.f);
+    load_wgT<EE>(wg, E, i0, e0, wg2);
     __syncthreads();
     const int ng = ceil_div(nt, U);
     auto issue = [&](int g) {
@@ -455,17 +478,7 @@ dwg_stream_kernel(const Elt* __restrict__ x, const float* __restrict__ dlogit, i
     float* sdl = reinterpret_cast<float*>(ring + (size_t)S * U * NV * NTD);  // [tpb][ET]
     const int tb0 = blockIdx.x * tpb;
     const int nt = max(0, min(T, tb0 + tpb) - tb0);
-    for (int q = tid; q < nt * ET; q += NT) {
-        const int r = q / ET, e = q % ET;
-        sdl[q] = e < E ? dlogit[(size_t)(tb0 + r) * E + e] : 0.f;
-    }
     const int i0 = (blockIdx.y * NTD + dg) * 8, e0 = eg * 8;
-    float2 acc[8][EE / 2];
-#pragma unroll
-    for (int a = 0; a < 8; ++a)
-#pragma unroll
-        for (int p = 0; p < EE / 2; ++p) acc[a][p] = make_float2(0.f, 0.f);
-    __syncthreads();
     const int ng = ceil_div(nt, U);
     auto issue = [&](int g) {
         if (!copier) return;
@@ -480,11 +493,23 @@ dwg_stream_kernel(const Elt* __restrict__ x, const float* __restrict__ dlogit, i
             }
         }
     };
+    // the x ring fills while dlogit is staged (one round trip of latency instead of two in a
+    // one-wave grid)
 #pragma unroll
     for (int g = 0; g < S - 1; ++g) {
         if (g < ng) issue(g);
         cp_async_commit_s();
     }
+    for (int q = tid; q < nt * ET; q += NT) {
+        const int r = q / ET, e = q % ET;
+        sdl[q] = e < E ? dlogit[(size_t)(tb0 + r) * E + e] : 0.f;
+    }
+    float2 acc[8][EE / 2];
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int p = 0; p < EE / 2; ++p) acc[a][p] = make_float2(0.f, 0.f);
+    __syncthreads();
     for (int g = 0; g < ng; ++g) {
         if (g + S - 1 < ng) issue(g + S - 1);
         cp_async_commit_s();
@@ -570,15 +595,9 @@ gate_bwd_fused_kernel(const Elt* __restrict__ dxe, const int* __restrict__ prow,
         sdl[q] = e < E ? dlogit[(size_t)(tb0 + r) * E + e] : 0.f;
     }
     const int i0 = tid * 8;
-    // this thread's Wg^T slice, read straight from Wg [d][E] (rows i0..i0+7 are contiguous)
+    // this thread's Wg^T slice, read straight from Wg [d][E] (rows i0..i0+7)
     float2 wg2[EE][4];
-#pragma unroll
-    for (int e = 0; e < EE; ++e)
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-            wg2[e][q] = e < E ? make_float2(__ldg(wg + (size_t)(i0 + 2 * q) * E + e),
-                                            __ldg(wg + (size_t)(i0 + 2 * q + 1) * E + e))
-                              : make_float2(0.f, 0.f);
+    load_wgT<EE>(wg, E, i0, 0, wg2);
     float2 acc[8][EE / 2];
 #pragma unroll
     for (int a = 0; a < 8; ++a)
