@@ -280,7 +280,8 @@ def run_e2e(a, world, ins, ctx, wg, w1, w2, dwg, dw1, dw2, dev, barrier, max_ove
     dxd = [torch.empty(xh.shape, dtype=bf, device=dev) for _ in range(NB)]
     comp = torch.cuda.current_stream()
     s_in, s_out = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
-    ev_in = [torch.cuda.Event() for _ in range(NB)]
+    ev_in = [torch.cuda.Event() for _ in range(NB)]       # x landed (the forward waits on it)
+    ev_in_dy = [torch.cuda.Event() for _ in range(NB)]    # dy landed (only the backward waits)
     ev_fwd = [torch.cuda.Event() for _ in range(NB)]
     ev_bwd = [torch.cuda.Event() for _ in range(NB)]
     ev_out = [torch.cuda.Event() for _ in range(NB)]
@@ -289,8 +290,9 @@ def run_e2e(a, world, ins, ctx, wg, w1, w2, dwg, dw1, dw2, dev, barrier, max_ove
         with torch.cuda.stream(s_in):
             s_in.wait_event(ev_bwd[b])            # buffer b's previous step is done with it
             xd[b].copy_(xh, non_blocking=True)
-            dyd[b].copy_(dyh, non_blocking=True)
             ev_in[b].record(s_in)
+            dyd[b].copy_(dyh, non_blocking=True)
+            ev_in_dy[b].record(s_in)
 
     def run(n):
         for b in range(NB):
@@ -304,6 +306,7 @@ def run_e2e(a, world, ins, ctx, wg, w1, w2, dwg, dw1, dw2, dev, barrier, max_ove
             comp.wait_event(ev_out[b])            # host buffers of step i-NB have been read
             ctx.forward(xd[b], wg, w1, w2, a.k, a.cf, a.chunks, y=yd[b], routing=False)
             ev_fwd[b].record(comp)
+            comp.wait_event(ev_in_dy[b])
             ctx.backward(dyd[b], dx=dxd[b], dwg=dwg, dw1=dw1, dw2=dw2)
             ev_bwd[b].record(comp)
             if i + NB - 1 < n:
