@@ -909,43 +909,60 @@ def run_lancet(a, world, rank, local_rank):
         # transport in push mode -- every exchange of the N > 1 path is executed (to self), so
         # the line carries the metric's second half (exposed vs unoverlapped all-to-all)
         pcfg = dataclasses.replace(cfg, flags=(flags & ~lancet.FLAG_FORCE_EP) | lancet.FLAG_PEER_PUSH)
-        ectx = lancet.Context(pcfg, world=1, rank=0, device=local_rank, transport="peer")
-        ep_flags = pcfg.flags
-        rec = tuner_record(a, ectx, lancet, ep_flags, step_on(ectx), stream, barrier, max_over_ranks, 1,
-                           float(adm * rowb), ns=sorted({1, 2, 4, 8, a.chunks}))
-        out["ep"] = {"transport": "peer push, one-rank group (all exchanges to self)", **rec}
-        ectx.close()
+        try:
+            ectx = lancet.Context(pcfg, world=1, rank=0, device=local_rank, transport="peer")
+            ep_flags = pcfg.flags
+            rec = tuner_record(a, ectx, lancet, ep_flags, step_on(ectx), stream, barrier, max_over_ranks, 1,
+                               float(adm * rowb), ns=sorted({1, 2, 4, 8, a.chunks}))
+            out["ep"] = {"transport": "peer push, one-rank group (all exchanges to self)", **rec}
+            ectx.close()
+        except Exception as ex:  # noqa: BLE001 -- an auxiliary record never costs the headline line
+            out["ep"] = {"error": f"{type(ex).__name__}: {ex}"}
     if world > 1 and not a.no_arms:
         # every transport on the same definitions (push / pull over the peer transport, NCCL)
         arms = {}
         for name in ("push", "pull", "nccl"):
             if name != "nccl" and a.transport_used != "peer":
                 continue
-            if name == ("push" if not a.no_push else "pull") and a.transport_used == "peer":
-                actx, own = ctx, False
-            else:
-                acfg = dataclasses.replace(cfg, flags=flags & ~lancet.FLAG_PEER_PUSH | (lancet.FLAG_PEER_PUSH if name == "push" else 0))
-                actx = lancet.Context(acfg, world=world, rank=rank, device=local_rank,
-                                      pg=dist.group.WORLD, transport="nccl" if name == "nccl" else "peer")
-                own = True
-            afl = flags & ~lancet.FLAG_PEER_PUSH | (lancet.FLAG_PEER_PUSH if name == "push" else 0)
-            arms[name] = measure_arm(a, actx, lancet, afl, step_on(actx), stream, barrier, max_over_ranks, a.chunks)
+            if name == "nccl" and a.same_device:
+                arms[name] = {"skipped": "NCCL refuses several ranks on one device (--same-device)"}
+                continue
+            actx, own = ctx, False
+            try:
+                if not (name == ("push" if not a.no_push else "pull") and a.transport_used == "peer"):
+                    acfg = dataclasses.replace(cfg, flags=flags & ~lancet.FLAG_PEER_PUSH | (lancet.FLAG_PEER_PUSH if name == "push" else 0))
+                    actx = lancet.Context(acfg, world=world, rank=rank, device=local_rank,
+                                          pg=dist.group.WORLD, transport="nccl" if name == "nccl" else "peer")
+                    own = True
+                afl = flags & ~lancet.FLAG_PEER_PUSH | (lancet.FLAG_PEER_PUSH if name == "push" else 0)
+                arms[name] = measure_arm(a, actx, lancet, afl, step_on(actx), stream, barrier, max_over_ranks, a.chunks)
+            except Exception as ex:  # noqa: BLE001 -- an auxiliary record never costs the headline line
+                arms[name] = {"error": f"{type(ex).__name__}: {ex}"}
             if own:
                 barrier()
                 actx.close()
         out["arms"] = arms
         # the chunk-count tuner on the main arm: n = 1, 2, 4, 8 measured, predicted from n = 1, 4
         sched = 1 if (a.transport_used == "peer" and not a.no_push) else 0
-        out["chunk_tuner"] = tuner_record(a, ctx, lancet, flags, step_on(ctx), stream, barrier, max_over_ranks,
-                                          sched, float(adm * rowb))["tuner"]
+        try:
+            out["chunk_tuner"] = tuner_record(a, ctx, lancet, flags, step_on(ctx), stream, barrier, max_over_ranks,
+                                              sched, float(adm * rowb))["tuner"]
+        except Exception as ex:  # noqa: BLE001
+            out["chunk_tuner"] = {"error": f"{type(ex).__name__}: {ex}"}
     if not a.no_block:
-        out["block"] = block_record(a, world, rank, local_rank, stream, barrier, max_over_ranks)
-        if world == 1:
+        try:
+            out["block"] = block_record(a, world, rank, local_rank, stream, barrier, max_over_ranks)
+        except Exception as ex:  # noqa: BLE001
+            out["block"] = {"error": f"{type(ex).__name__}: {ex}"}
+        if world == 1 and "error" not in out["block"]:
             # the per-GPU expert shapes of the 8-GPU run (4 local experts receiving 8192 rows per
             # step) on this GPU: the same block with E = 4 experts in a one-rank group -- with
             # E_l = 32 every chunk splits each expert's ~256 rows into tiny GEMM groups
-            out["block"]["ep8_expert_shapes"] = block_record(a, world, rank, local_rank, stream, barrier,
-                                                             max_over_ranks, experts=4)
+            try:
+                out["block"]["ep8_expert_shapes"] = block_record(a, world, rank, local_rank, stream, barrier,
+                                                                 max_over_ranks, experts=4)
+            except Exception as ex:  # noqa: BLE001
+                out["block"]["ep8_expert_shapes"] = {"error": f"{type(ex).__name__}: {ex}"}
     if rank == 0 and not a.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(a)
     barrier()
