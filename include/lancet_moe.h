@@ -426,6 +426,15 @@ lancet_status lancet_plan_exchange(int32_t G, int32_t E_l, int32_t n, const int3
 /* Bytes of device workspace the context owns. */
 lancet_status lancet_workspace_bytes(const lancet_ctx* ctx, size_t* bytes);
 
+/* NCCL transport (lancet_create with world > 1 or LANCET_FLAG_FORCE_EP): the context's device
+ * buffers come from ncclMemAlloc and are registered with the communicator (ncclCommRegister),
+ * so the grouped send/recv of the exchanges can move rows between registered buffers directly
+ * (NCCL user-buffer registration) instead of staging them through NCCL's own buffers.  *count =
+ * buffers currently registered (0 for the other transports, or where NCCL declined -- the
+ * exchanges then run unregistered).  Environment LANCET_NCCL_REGISTER=0 at creation: plain
+ * cudaMalloc buffers, nothing registered (the A/B). */
+lancet_status lancet_nccl_registered(const lancet_ctx* ctx, int32_t* count);
+
 /* Number of this library's kernel launches enqueued by the last forward / backward. */
 lancet_status lancet_launch_counts(const lancet_ctx* ctx, int32_t* fwd, int32_t* bwd);
 

@@ -13,14 +13,34 @@ namespace lancet {
 struct NcclTransport : Transport {
     ncclComm_t comm = nullptr;
     int* d_scratch = nullptr;
+    std::vector<std::pair<void*, void*>> regs;   // (buffer, registration handle)
 
     ~NcclTransport() override {
-        if (comm) ncclCommDestroy(comm);
+        if (comm) {
+            for (auto& r : regs) ncclCommDeregister(comm, r.second);
+            ncclCommDestroy(comm);
+        }
         if (d_scratch) cudaFree(d_scratch);
     }
     bool is_nccl() const override { return true; }
     void abort() override {
         if (comm) { ncclCommAbort(comm); comm = nullptr; }
+        regs.clear();
+    }
+    int register_buffer(void* p, size_t bytes) override {
+        if (!comm || !p) return 1;
+        void* h = nullptr;
+        if (ncclCommRegister(comm, p, bytes, &h) != ncclSuccess || !h) return 1;
+        regs.push_back({p, h});
+        return 0;
+    }
+    void deregister_buffer(void* p) override {
+        for (size_t i = 0; i < regs.size(); ++i)
+            if (regs[i].first == p) {
+                if (comm) ncclCommDeregister(comm, regs[i].second);
+                regs.erase(regs.begin() + i);
+                return;
+            }
     }
     int exchange(const std::vector<P2P>& sends, const std::vector<P2P>& recvs, cudaStream_t s,
                  std::string& err) override {
@@ -56,6 +76,17 @@ struct NcclTransport : Transport {
         return 0;
     }
 };
+
+void* nccl_mem_alloc(size_t bytes)
+{
+    void* p = nullptr;
+    if (ncclMemAlloc(&p, bytes) != ncclSuccess) return nullptr;
+    return p;
+}
+void nccl_mem_free(void* p)
+{
+    if (p) ncclMemFree(p);
+}
 
 int nccl_unique_id(void* out, std::string& err)
 {

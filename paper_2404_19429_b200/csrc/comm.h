@@ -30,7 +30,18 @@ struct Transport {
     virtual int check_same(unsigned long long v, cudaStream_t s, std::string& err) = 0;
     virtual void abort() {}
     virtual bool is_nccl() const { return false; }
+    // NCCL user-buffer registration (ncclCommRegister) of a buffer the exchanges use: send /
+    // recv over NVLink then move the rows between the registered buffers directly instead of
+    // staging them through NCCL's internal buffers.  Returns 0 if registered, nonzero if the
+    // transport or the buffer does not support it (the exchange still works unregistered).
+    virtual int register_buffer(void* /*p*/, size_t /*bytes*/) { return 1; }
+    virtual void deregister_buffer(void* /*p*/) {}
 };
+
+// ncclMemAlloc / ncclMemFree (cuMem-backed, the allocation NCCL can register for zero-copy
+// point-to-point); nullptr if unavailable
+void* nccl_mem_alloc(size_t bytes);
+void nccl_mem_free(void* p);
 
 // NCCL (one process per GPU).  `id` is the 128-byte ncclUniqueId.
 // max_ctas > 0: the communicator's kernels use at most that many CTAs (ncclConfig_t.maxCTAs)

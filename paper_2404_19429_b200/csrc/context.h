@@ -16,6 +16,7 @@ struct Transport;   // comm.cpp: NCCL or in-process local group
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
+    bool nccl = false;   // ncclMemAlloc (NCCL transport: registrable for zero-copy send/recv)
 };
 
 // Copy-engine peer transport (world > 1 without NCCL): every rank maps the pull sources of its
@@ -130,6 +131,8 @@ struct lancet_ctx {
     int* h_grp = nullptr;
 
     std::vector<lancet::DevBuf> allocs;
+    bool nccl_mem = false;        // NCCL transport: allocate with ncclMemAlloc and register
+    int nccl_registered = 0;      // buffers registered with the communicator
 
     // state of the last forward (pointers only; the caller keeps the tensors alive)
     bool have_fwd = false;

@@ -18,6 +18,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -93,18 +94,31 @@ lancet_status dalloc(lancet_ctx* c, T** p, size_t bytes)
 {
     bytes = std::max<size_t>(bytes, 256);
     void* q = nullptr;
+    if (c->nccl_mem && (q = nccl_mem_alloc(bytes))) {
+        cudaGetLastError();
+        c->allocs.push_back({q, bytes, true});
+        if (c->comm && c->comm->register_buffer(q, bytes) == 0) ++c->nccl_registered;
+        *p = reinterpret_cast<T*>(q);
+        return LANCET_OK;
+    }
     if (cudaMalloc(&q, bytes) != cudaSuccess) {
         cudaGetLastError();
         return fail(c, LANCET_ERR_NOMEM, "cudaMalloc of " + std::to_string(bytes) + " bytes failed");
     }
-    c->allocs.push_back({q, bytes});
+    c->allocs.push_back({q, bytes, false});
     *p = reinterpret_cast<T*>(q);
     return LANCET_OK;
 }
 
+void dfree(const lancet::DevBuf& b)
+{
+    if (b.nccl) nccl_mem_free(b.p);
+    else cudaFree(b.p);
+}
+
 void free_all(lancet_ctx* c)
 {
-    for (auto& b : c->allocs) cudaFree(b.p);
+    for (auto& b : c->allocs) dfree(b);
     c->allocs.clear();
     if (c->h_counts) cudaFreeHost(c->h_counts);
     if (c->h_grp) cudaFreeHost(c->h_grp);
@@ -456,7 +470,15 @@ lancet_status ensure_expert_rows(lancet_ctx* c, int rows)
     for (void* p : olds) {
         if (!p) continue;
         for (size_t i = 0; i < c->allocs.size(); ++i)
-            if (c->allocs[i].p == p) { cudaFree(p); c->allocs.erase(c->allocs.begin() + i); break; }
+            if (c->allocs[i].p == p) {
+                if (c->comm && c->allocs[i].nccl && c->nccl_registered > 0) {
+                    c->comm->deregister_buffer(p);
+                    --c->nccl_registered;
+                }
+                dfree(c->allocs[i]);
+                c->allocs.erase(c->allocs.begin() + i);
+                break;
+            }
     }
     c->xe = c->H = c->Gp = c->out = c->dout = c->dA = c->dXe = nullptr;
     const size_t rf = (size_t)newrows * f * c->elt, rd = (size_t)newrows * d * c->elt;
@@ -1177,12 +1199,19 @@ LANCET_API lancet_status lancet_create(lancet_ctx** out, int32_t world, int32_t 
     lancet_status st = validate_cfg(cfg, world);
     if (st) return st;
     auto* c = new lancet_ctx();
+    // NCCL data plane: buffers from ncclMemAlloc, registered with the communicator below
+    // (LANCET_NCCL_REGISTER=0: plain cudaMalloc, unregistered -- the A/B)
+    const char* reg_env = getenv("LANCET_NCCL_REGISTER");
+    c->nccl_mem = ep && !(reg_env && reg_env[0] == '0');
     st = create_common(c, world, rank, cuda_device, cfg);
     if (!st && ep) {
         std::string err;
         c->comm = make_nccl_transport(world, rank, nccl_id, LANCET_COMM_SMS, err);
         if (!c->comm) st = fail(c, LANCET_ERR_NCCL, err);
         else if (c->comm->check_same(cfg_hash(*cfg), c->s_comm, err)) st = fail(c, LANCET_ERR_ARG, err);
+        else
+            for (const lancet::DevBuf& b : c->allocs)
+                if (b.nccl && c->comm->register_buffer(b.p, b.bytes) == 0) ++c->nccl_registered;
     }
     if (st) {
         g_thread_err = c->err;
@@ -2113,6 +2142,13 @@ LANCET_API lancet_status lancet_workspace_bytes(const lancet_ctx* c, size_t* byt
     size_t b = 0;
     for (const DevBuf& x : c->allocs) b += x.bytes;
     *bytes = b;
+    return LANCET_OK;
+}
+
+LANCET_API lancet_status lancet_nccl_registered(const lancet_ctx* c, int32_t* count)
+{
+    if (!c || !count) return fail(nullptr, LANCET_ERR_ARG, "null argument");
+    *count = c->comm ? c->nccl_registered : 0;
     return LANCET_OK;
 }
 

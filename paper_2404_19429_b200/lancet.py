@@ -46,7 +46,7 @@ EXPORTS = ["lancet_abi_version", "lancet_last_error", "lancet_nccl_unique_id", "
            "lancet_create_peer", "lancet_peer_blob_bytes", "lancet_peer_export", "lancet_peer_import",
            "lancet_moe_backward_dw", "lancet_set_dw_fillers", "lancet_dw_schedule", "lancet_stack_dw_plan",
            "lancet_set_gate_seed", "lancet_set_peer_timeout_ms", "lancet_peer_abort", "lancet_peer_status",
-           "lancet_tune_chunks", "lancet_moe_forward_partitioned"]
+           "lancet_tune_chunks", "lancet_moe_forward_partitioned", "lancet_nccl_registered"]
 
 
 class LancetError(RuntimeError):
@@ -106,6 +106,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "lancet_last_timeline": ([P, ctypes.POINTER(_OpRecord), I32, ctypes.POINTER(I32)], I32),
             "lancet_debug_copy": ([P, I32, P, ctypes.c_size_t], I32),
             "lancet_workspace_bytes": ([P, ctypes.POINTER(ctypes.c_size_t)], I32),
+            "lancet_nccl_registered": ([P, ctypes.POINTER(I32)], I32),
             "lancet_launch_counts": ([P, ctypes.POINTER(I32), ctypes.POINTER(I32)], I32),
             "lancet_plan_exchange": ([I32, I32, I32, P, P, P, P, P, P, P, ctypes.POINTER(I32)], I32),
             "lancet_moe_backward_dw": ([P, I32, P], I32),
@@ -435,6 +436,12 @@ class Context:
         b = ctypes.c_size_t()
         _check(load_library().lancet_workspace_bytes(self._p, ctypes.byref(b)), self._p)
         return b.value
+
+    def nccl_registered(self) -> int:
+        """Buffers registered with the NCCL communicator (lancet_nccl_registered)."""
+        n = ctypes.c_int32()
+        _check(load_library().lancet_nccl_registered(self._p, ctypes.byref(n)), self._p)
+        return n.value
 
     def launch_counts(self):
         f, b = ctypes.c_int32(), ctypes.c_int32()

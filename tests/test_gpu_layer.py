@@ -460,3 +460,29 @@ def test_misaligned_pointers_are_refused():
         ctx.forward(x, wg, w1, w2, k, 1.0, 1)
     assert e.value.status == 1 and "aligned" in str(e.value)
     ctx.close()
+
+
+def test_nccl_registered_buffers_are_bitwise_neutral(monkeypatch):
+    # the NCCL data plane with its buffers from ncclMemAlloc registered with the communicator
+    # (user-buffer registration) against plain cudaMalloc buffers (LANCET_NCCL_REGISTER=0): the
+    # exchanges move the same bytes, so two steps on new inputs agree bit for bit
+    from paper_2404_19429_b200 import FLAG_FORCE_EP, lancet
+    T, d, f, E, k, n = 1500, 256, 512, 8, 2, 3
+    outs, regs = [], []
+    for env in ("1", "0"):
+        monkeypatch.setenv("LANCET_NCCL_REGISTER", env)
+        cfg = lancet.LayerConfig(d_model=d, d_ffn=f, n_experts=E, max_tokens=T, max_k=k, max_chunks=8,
+                                 flags=FLAG_FORCE_EP)
+        ctx = lancet.Context(cfg)
+        try:
+            steps = [run_gpu(inputs(T, d, f, E, k, beta=0.5, seed=500 + s), E, k, 1.0, n, ctx=ctx)
+                     for s in range(2)]
+            regs.append(ctx.nccl_registered())
+        finally:
+            ctx.close()
+        outs.append(steps)
+    assert regs[1] == 0
+    print("registered buffers:", regs[0])
+    for a, b in zip(*outs):
+        for key in ("idx", "slot", "y", "dx", "dwg", "dw1", "dw2"):
+            assert np.array_equal(a[key], b[key]), key
