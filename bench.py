@@ -46,7 +46,11 @@ def parse():
     ap.add_argument("--experts", type=int, default=8)
     ap.add_argument("--k", type=int, default=2)
     ap.add_argument("--cf", type=float, default=1.25)
-    ap.add_argument("--chunks", type=int, default=4)
+    ap.add_argument("--chunks", type=int, default=0,
+                    help="chunk count n of the expert-parallel pipeline; 0 = auto: at N > 1 the "
+                         "fastest of n = 1, 2, 4, 8 in a short probe on this run's ranks (the "
+                         "paper picks n by search, P:L411-L414); at N = 1 the single-GPU path has "
+                         "no exchange to pipeline and runs unchunked")
     ap.add_argument("--beta", type=float, default=0.25)
     ap.add_argument("--seed", type=int, default=2024)
     ap.add_argument("--flags", type=int, default=0, help="extra LANCET_FLAG_* bits")
@@ -79,18 +83,25 @@ def parse():
                     help="N > 1: skip the per-transport arms (push / pull / NCCL on one definition)")
     a = ap.parse_args()
     a.warmup = max(a.warmup, 3)
+    a.chunks_req = a.chunks
+    if a.chunks <= 0:
+        a.chunks = 4           # provisional (shapes, oracle calls: results do not depend on n)
     if a.same_device:
         a.transport = "peer"
     return a
+
+
+def _nlabel(a):
+    return "auto" if getattr(a, "chunks_req", a.chunks) <= 0 else a.chunks
 
 
 def workload(a, world):
     return {
         "workload": f"GPT-MoE layer fwd+bwd: d_model={a.d} ffn={a.f} experts={a.experts} "
                     f"({a.experts // world}/GPU) top-{a.k} cf={a.cf} {a.tokens} tokens/GPU "
-                    f"n_chunks={a.chunks} bf16" + ("" if a.gate == "switch" else f" gate={a.gate}"),
+                    f"n_chunks={_nlabel(a)} bf16" + ("" if a.gate == "switch" else f" gate={a.gate}"),
         "tokens_per_gpu": a.tokens, "d_model": a.d, "d_ffn": a.f, "experts": a.experts,
-        "top_k": a.k, "capacity_factor": a.cf, "n_chunks": a.chunks, "routing_skew_beta": a.beta,
+        "top_k": a.k, "capacity_factor": a.cf, "n_chunks": _nlabel(a), "routing_skew_beta": a.beta,
         "gate": a.gate,
         "parallelism": f"ep{world}" + (f" ({getattr(a, 'transport_used', a.transport)}"
                                        + (" push" if getattr(a, "transport_used", "") == "peer" and not a.no_push else "")
@@ -715,6 +726,29 @@ def run_lancet(a, world, rank, local_rank):
         ctx.close()
         return
 
+    # chunk count: auto at N > 1 = the fastest of n = 1, 2, 4, 8 over a short probe (max over
+    # ranks); the single-GPU path has no exchange and runs unchunked whatever n says
+    ep_path = world > 1 or bool(flags & lancet.FLAG_FORCE_EP) or a.transport == "peer"
+    n_probe = None
+    if a.chunks_req <= 0:
+        if ep_path:
+            n_probe = {}
+            for n in (1, 2, 4, 8):
+                a.chunks = n
+                for _ in range(2):
+                    step()
+                barrier()
+                torch.cuda.synchronize()
+                p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                p0.record(stream)
+                for _ in range(5):
+                    step()
+                p1.record(stream)
+                torch.cuda.synchronize()
+                n_probe[n] = max_over_ranks(p0.elapsed_time(p1) / 5)
+            a.chunks = min(n_probe, key=n_probe.get)
+        else:
+            a.chunks = 1
     clocks = ClockSampler(local_rank).start()
     for _ in range(a.warmup):
         step()
@@ -874,6 +908,13 @@ def run_lancet(a, world, rank, local_rank):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (seeded; synthetic/ recipe, DESIGN.md)",
         "config": workload(a, world),
+        "n_chunks_used": a.chunks if ep_path else 1,
+        "n_chunks_note": ("the fastest of a 5-step probe per n (max over ranks, ms per step): "
+                          + json.dumps({str(k_): round(v_, 4) for k_, v_ in n_probe.items()})
+                          if n_probe else
+                          ("set by --chunks" if ep_path else
+                           "single GPU: no exchange to pipeline, the layer runs unchunked; the "
+                           "'ep' record measures n = 1, 2, 4, 8 over a one-rank group")),
         "host_enqueue_ms_per_step": host_ms,
         "instrumented_ms_per_step": ms_instr,
         "exposed_a2a_ms": exposed_ms, "a2a_ms_on_comm_lane": comm_ms,
