@@ -16,14 +16,12 @@ a = ap.parse_args()
 shapes = []
 for E in (8, 16, 32, 64):
     for T in (4096, 16384, 65536):
-        shapes.append((T, E, 4))
-for n in (1, 2, 8):
-    shapes.append((16384, 8, n))
+        shapes.append((T, E, 0))
 if a.quick:
     shapes = shapes[:3]
 for T, E, n in shapes:
     cmd = [sys.executable, "bench.py", "--steps", "20", "--warmup", "4", "--no-e2e", "--no-cpu-baseline",
-           "--tokens", str(T), "--experts", str(E), "--chunks", str(n)]
+           "--no-ep", "--no-block", "--tokens", str(T), "--experts", str(E), "--chunks", str(n)]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     line = r.stdout.strip().splitlines()[-1] if r.stdout.strip() else json.dumps({"error": r.stderr[-400:]})
     d = json.loads(line)
