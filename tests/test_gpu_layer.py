@@ -486,3 +486,42 @@ def test_nccl_registered_buffers_are_bitwise_neutral(monkeypatch):
     for a, b in zip(*outs):
         for key in ("idx", "slot", "y", "dx", "dwg", "dw1", "dw2"):
             assert np.array_equal(a[key], b[key]), key
+
+
+def test_maximum_experts_and_top_k():
+    # the API's upper limits at once: E = 256 experts (kMaxExperts: tiled gate with 8 experts x 4
+    # tokens per thread, 256-row scan histograms, > 128 GEMM groups in batched launches) and
+    # k = 8 (kMaxK) with a binding capacity, against the oracle
+    T, d, f, E, k, cf, n = 3000, 64, 128, 256, 8, 1.25, 4
+    ins = inputs(T, d, f, E, k, beta=0.5, seed=256)
+    g = run_gpu(ins, E, k, cf, n)
+    o = run_oracle(ins, k, cf, n)
+    assert_routing_exact(g, o)
+    assert np.any(o["rt"].slot < 0), "case must exercise drops"
+    for key in ("y", "dx", "dwg", "dw1", "dw2"):
+        err = normwise(g[key], o[key])
+        assert err <= TOL["bf16"], (key, err)
+
+
+def test_maximum_chunk_count_expert_parallel_path():
+    # n = 64 chunks (kMaxChunks) on the expert-parallel path (one-rank NCCL communicator): 64
+    # per-chunk exchanges and GEMM groups of ~4 rows per expert; rows are independent, so y / dx
+    # / routing are bitwise the single-GPU path's and the gradients meet the oracle
+    from paper_2404_19429_b200 import FLAG_FORCE_EP, lancet
+    T, d, f, E, k, cf, n = 2000, 128, 256, 8, 2, 1.0, 64
+    ins = inputs(T, d, f, E, k, beta=0.5, seed=64)
+    cfg = lancet.LayerConfig(d_model=d, d_ffn=f, n_experts=E, max_tokens=T, max_k=k, max_chunks=64,
+                             flags=FLAG_FORCE_EP)
+    ctx = lancet.Context(cfg)
+    try:
+        ep = run_gpu(ins, E, k, cf, n, ctx=ctx)
+    finally:
+        ctx.close()
+    one = run_gpu(ins, E, k, cf, 1)                 # the single-GPU path is unchunked
+    for key in ("idx", "slot", "y", "dx"):
+        assert np.array_equal(ep[key], one[key]), key
+    o = run_oracle(ins, k, cf, n)
+    assert_routing_exact(ep, o)
+    for key in ("y", "dx", "dwg", "dw1", "dw2"):
+        err = normwise(ep[key], o[key])
+        assert err <= TOL["bf16"], (key, err)
