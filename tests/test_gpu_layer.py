@@ -525,3 +525,35 @@ def test_maximum_chunk_count_expert_parallel_path():
     for key in ("y", "dx", "dwg", "dw1", "dw2"):
         err = normwise(ep[key], o[key])
         assert err <= TOL["bf16"], (key, err)
+
+
+@pytest.mark.parametrize("path", ["single", "force_ep", "push"])
+def test_experts_that_receive_no_rows(path):
+    # degenerate routing: two experts are never selected (their Wg columns are pushed far below
+    # the others), so their GEMM groups are empty on every chunk -- their weight gradients must
+    # be exactly zero, everything else must meet the oracle, on the single-GPU path, the
+    # expert-parallel NCCL path and the push pipeline (one-rank peer group)
+    from paper_2404_19429_b200 import FLAG_FORCE_EP, FLAG_PEER_PUSH, lancet
+    T, d, f, E, k, cf, n = 1300, 128, 256, 8, 2, 1.25, 3
+    ins = inputs(T, d, f, E, k, beta=0.5, seed=13)
+    ins["wg"][:, 3] = -ins["wg"][:, 3].__abs__() - 0.5
+    ins["wg"][:, 6] = -ins["wg"][:, 6].__abs__() - 0.5
+    ins["x"] = np.abs(ins["x"]).astype(ins["x"].dtype)          # x >= 0: those logits stay lowest
+    o = run_oracle(ins, k, cf, n)
+    assert not np.isin(o["rt"].idx, [3, 6]).any(), "construction must leave experts 3 and 6 unused"
+    if path == "single":
+        g = run_gpu(ins, E, k, cf, n)
+    else:
+        fl = FLAG_FORCE_EP if path == "force_ep" else FLAG_PEER_PUSH
+        cfg = lancet.LayerConfig(d_model=d, d_ffn=f, n_experts=E, max_tokens=T, max_k=k, max_chunks=8, flags=fl)
+        ctx = lancet.Context(cfg, transport="nccl" if path == "force_ep" else "peer")
+        try:
+            g = run_gpu(ins, E, k, cf, n, ctx=ctx)
+        finally:
+            ctx.close()
+    assert_routing_exact(g, o)
+    for e in (3, 6):
+        assert not np.any(g["dw1"][e]) and not np.any(g["dw2"][e]), e
+    for key in ("y", "dx", "dwg", "dw1", "dw2"):
+        err = normwise(g[key], o[key])
+        assert err <= TOL["bf16"], (key, err)
