@@ -31,6 +31,8 @@ def _lib():
     (513, 32, 1, 1, 0.0, 1.0, 2),          # one expert
     (1500, 192, 32, 2, 0.5, 1.25, 3),      # warp-streaming gate, 8 threads per token
     (999, 320, 16, 3, 0.5, 1.0, 2),        # warp-streaming gate, 4 threads per token, ragged
+    (10001, 256, 8, 2, 0.5, 1.25, 4),      # two tokens per thread (T >= 9472), ragged last warp
+    (9473, 192, 16, 3, 0.5, 1.0, 3),       # two tokens per thread at E = 16, one token past a block
 ])
 def test_routing_bit_exact(T, d, E, k, beta, cf, n):
     ins = inputs(T, d, 8, E, k, beta=beta, seed=T)
