@@ -333,17 +333,24 @@ def run_e2e(a, world, ins, ctx, wg, w1, w2, dwg, dw1, dw2, dev, barrier, max_ove
     torch.cuda.synchronize()
     barrier()
     ne = max(3, a.steps)
-    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    f0.record(comp)
-    s_in.wait_event(f0)
-    h0 = time.perf_counter()
-    run(ne)
-    host_ms = (time.perf_counter() - h0) * 1000.0 / ne     # host enqueue time per step
-    comp.wait_stream(s_out)
-    f1.record(comp)
-    torch.cuda.synchronize()
-    barrier()
-    ems = max_over_ranks(f0.elapsed_time(f1) / ne)
+
+    def one_pass():
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(comp)
+        s_in.wait_event(f0)
+        h0 = time.perf_counter()
+        run(ne)
+        hms = (time.perf_counter() - h0) * 1000.0 / ne     # host enqueue time per step
+        comp.wait_stream(s_out)
+        f1.record(comp)
+        torch.cuda.synchronize()
+        barrier()
+        return max_over_ranks(f0.elapsed_time(f1) / ne), hms
+
+    # three timed passes of K steps each (PCIe-bound, with more run-to-run spread than the
+    # device-only number): the median is reported, all three are listed
+    passes = [one_pass() for _ in range(3)]
+    ems, host_ms = sorted(passes)[1]
     ok = bool(torch.equal(yh[(ne - 1) % NB], yd[(ne - 1) % NB].cpu()))
     nb = xh.numel() * xh.element_size()
     # the copies alone (no compute): the PCIe ceiling of this end-to-end loop
@@ -380,6 +387,8 @@ def run_e2e(a, world, ins, ctx, wg, w1, w2, dwg, dw1, dw2, dev, barrier, max_ove
     return {"value": world * a.tokens / (ems / 1000.0), "unit": "tokens/s",
             "h2d_bytes_per_step": 2 * nb, "d2h_bytes_per_step": 2 * nb, "ms_per_step": ems,
             "host_enqueue_ms_per_step": host_ms,
+            "passes_ms_per_step": [round(p_[0], 4) for p_ in passes], "reported": "median of the passes",
+            "host_affinity": getattr(a, "cpu_affinity", None),
             "readback_checked": ok,
             "copies_alone_ms": {"h2d": h_ms, "d2h": d_ms, "both_directions": b_ms,
                                 "h2d_gbs": 2 * nb / (h_ms * 1e6), "d2h_gbs": 2 * nb / (d_ms * 1e6)},
@@ -652,6 +661,20 @@ def make_context(a, lancet, cfg, world, rank, local_rank, dev):
     return lancet.Context(cfg, world=world, rank=rank, device=local_rank, pg=pg, transport="nccl")
 
 
+def gpu_local_cpus(local_rank):
+    """The CPUs NVML reports as closest to this GPU (its NUMA node), or None."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(local_rank)
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (os.cpu_count() + 63) // 64)
+        cpus = {64 * i + b for i, w in enumerate(words) for b in range(64) if (w >> b) & 1}
+        cpus &= os.sched_getaffinity(0)
+        return cpus or None
+    except Exception:  # noqa: BLE001
+        return None
+
+
 def run_lancet(a, world, rank, local_rank):
     import torch
     import torch.distributed as dist
@@ -661,6 +684,17 @@ def run_lancet(a, world, rank, local_rank):
         build.build()
     if world > 1:
         dist.barrier()
+    # host threads (and with them the pinned buffers of the end-to-end loop, first-touch) on
+    # the GPU's own NUMA node: on a multi-socket host, DMA to a far socket's memory crosses the
+    # socket link (the pool's boxes are single-node VMs, where this is a no-op; their two-way
+    # copy time still varies between runs, 1.36-1.83 ms per step, hence the median of passes)
+    a.cpu_affinity = None
+    a.cpu_affinity_all = os.sched_getaffinity(0)
+    if not os.environ.get("LANCET_BENCH_NO_AFFINITY"):
+        cpus = gpu_local_cpus(local_rank)
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+            a.cpu_affinity = f"{len(cpus)} CPUs local to GPU {local_rank} (NVML)"
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     E_l = a.experts // world
@@ -1005,6 +1039,7 @@ def run_lancet(a, world, rank, local_rank):
             except Exception as ex:  # noqa: BLE001
                 out["block"]["ep8_expert_shapes"] = {"error": f"{type(ex).__name__}: {ex}"}
     if rank == 0 and not a.no_cpu_baseline:
+        os.sched_setaffinity(0, a.cpu_affinity_all)    # the oracle gets every host core again
         out["cpu_baseline"] = cpu_baseline(a)
     barrier()
     if rank == 0:
