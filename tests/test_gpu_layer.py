@@ -131,6 +131,19 @@ def test_full_size_gpt_moe_layer():
     assert np.all(g["y"][dropped] == 0)
 
 
+def test_full_size_fp32_mode():
+    # the fp32 mode (north_star: <= 1e-5 against the oracle) at the configs[1] per-GPU shape:
+    # fp32 x / W1 / W2 through the SIMT GEMMs, the fp32 gate and every fp32 kernel variant
+    T, d, f, E, k, cf, n = 16384, 1024, 4096, 8, 2, 1.25, 4
+    ins = inputs(T, d, f, E, k, beta=0.25, dtype="fp32", seed=2025)
+    g = run_gpu(ins, E, k, cf, n, dtype="fp32")
+    o = run_oracle(ins, k, cf, n)
+    assert_routing_exact(g, o)
+    for key in ("y", "dx", "dwg", "dw1", "dw2"):
+        err = normwise(g[key], o[key])
+        assert err <= TOL["fp32"], (key, err)
+
+
 @pytest.mark.parametrize("k", [1, 2, 4])
 def test_switch_gate_ties_break_to_the_lower_expert(k):
     # duplicated Wg columns give bitwise-equal logits (R1: the same fp32 chain): top-k must order
