@@ -11,7 +11,8 @@
 // sum l = sum exp2(s - m) online; pass 2 recomputes S_j, writes P_j = exp2(s - m) / l (bf16)
 // into shared memory in the UMMA K-major layout and accumulates O += P_j V_j in TMEM with no
 // correction step.  The extra Q K^T costs 1/3 more MMA work, which the tensor core has to spare
-// here (the kernel is bound by the exponentials on the SFU: 2 x 128 x 128 per key tile).
+// here.  (ncu, configs[3] chunk launches: XU (exp2) pipe 39 % busy, FMA 10 %, issue 29 % -- the
+// kernel is latency-bound on the S -> softmax -> P hand-offs, not SFU-bound.)
 //
 // Roles (384 threads): warp 0 TMA producer | warp 1 MMA issuer (one thread) | warp 2 TMEM
 // allocator | warp 3 idle | warps 4-11 softmax + epilogue: thread = query row (TMEM lane
